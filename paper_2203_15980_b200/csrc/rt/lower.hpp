@@ -1,0 +1,23 @@
+#pragma once
+#include <cstdint>
+#include <vector>
+
+#include "delta/delta.h"
+#include "deltasim/deltasim.hpp"
+
+namespace delta_rt {
+
+struct Program {
+  deltasim::RunResult plan;
+  std::vector<delta_action> actions;
+  std::vector<std::uint64_t> inputs;  // arena offsets of COMPUTE/RECOMPUTE inputs
+  std::uint64_t arena_bytes = 0;
+  std::uint64_t pool_peak = 0;
+  std::uint64_t host_bytes = 0;
+  std::uint32_t n_events = 0;
+};
+
+Program lower_plan(const deltasim::Trace& trace, const deltasim::EngineConfig& cfg,
+                   std::uint64_t align);
+
+}  // namespace delta_rt
