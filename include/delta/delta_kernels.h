@@ -1,0 +1,97 @@
+/* delta-b200 C ABI — the B200 execution side of the DELTA runtime.
+ *
+ * The reference simulates these subsystems (include/deltasim/device.hpp:17-74
+ * MemoryPool / Stream / Clock; OpNode::compute_cost_us at trace.hpp:17 as the
+ * "recompute" of a tensor; policy.cpp:58-64 as the "swap").  Here they are
+ * real:
+ *   recompute engine : sm_100a kernels that (re)produce every activation
+ *                      (tcgen05 implicit-GEMM conv; HBM-bound BN/ReLU/add/pool),
+ *   swap engine      : pinned host slab + D2H/H2D copy-engine streams + events,
+ *   cost model       : device-timed op latencies and a host-link probe.
+ * All tensors are device pointers (NHWC bf16 activations unless stated);
+ * `stream` is a cudaStream_t passed as void*.  Every call is asynchronous on
+ * `stream`; errors are reported as delta_status (delta.h), never thrown.
+ */
+#ifndef DELTA_DELTA_KERNELS_H_
+#define DELTA_DELTA_KERNELS_H_
+
+#include <stdint.h>
+
+#include "delta/delta.h"
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- recompute engine: convolution (ConvForward, ref src/trace.cpp:403) ----
+ * Weights are [K][R][S][C] bf16 (C == 4: [K][ceil(R*S*4/64)*64], taps packed
+ * 4 channels each).  The handle caches the TMA descriptor of the weights. */
+typedef struct delta_conv delta_conv;
+delta_status delta_conv_create(int32_t N, int32_t H, int32_t W, int32_t C, int32_t K,
+                               int32_t R, int32_t S, int32_t stride, int32_t pad,
+                               const void* weight, delta_conv** out);
+delta_status delta_conv_forward(const delta_conv* c, const void* x, void* y, void* stream);
+delta_status delta_conv_geometry(const delta_conv* c, int32_t* P, int32_t* Q, int32_t* kdim,
+                                 int32_t* tile_n);
+void delta_conv_destroy(delta_conv* c);
+
+/* ---- recompute engine: BatchNorm (BNForward, ref src/trace.cpp:405) ---- */
+int64_t delta_bn_workspace_floats(int64_t M, int32_t C);
+/* training-mode statistics; run_mean/run_var may be NULL (recompute never
+ * touches them) */
+delta_status delta_bn_stats(const void* x, int64_t M, int32_t C, float* ws, float* mean,
+                            float* invstd, float eps, float* run_mean, float* run_var,
+                            float momentum, void* stream);
+/* mode 0 relu(bn(x)), 1 relu(bn(x)+res), 2 relu(bn(x)+bn2(res)) */
+delta_status delta_bn_apply(int32_t mode, const void* x, const void* res, void* y, int64_t M,
+                            int32_t C, const float* mean, const float* invstd,
+                            const float* gamma, const float* beta, const float* mean2,
+                            const float* invstd2, const float* gamma2, const float* beta2,
+                            void* stream);
+delta_status delta_bn_backward(const void* up, int32_t pool_hw, const void* mask, const void* x,
+                               void* dx, int64_t M, int32_t C, const float* mean,
+                               const float* invstd, const float* gamma, float* dgamma,
+                               float* dbeta, float* ws, void* stream);
+delta_status delta_add_grad(const void* a, const void* up, int32_t pool_hw, const void* mask,
+                            void* out, int64_t M, int32_t C, void* stream);
+
+/* ---- pooling / head ---- */
+delta_status delta_maxpool3x3s2_fwd(const void* x, void* y, int32_t N, int32_t H, int32_t W,
+                                    int32_t C, void* stream);
+delta_status delta_maxpool3x3s2_bwd(const void* dy, const void* x, void* dx, int32_t N,
+                                    int32_t H, int32_t W, int32_t C, void* stream);
+delta_status delta_avgpool_fwd(const void* x, void* y, int32_t N, int32_t HW, int32_t C,
+                               void* stream);
+delta_status delta_softmax_xent(const float* logits, const int64_t* labels, float* loss,
+                                float* dlogits, float* row_ws, int32_t N, int32_t K,
+                                void* stream);
+
+/* ---- swap engine (Offload/Reload, ref src/engine.cpp:312-331, 396-419,
+ *      533-585): pinned host slab + dedicated copy-engine streams ---- */
+typedef struct delta_swap delta_swap;
+/* Allocates `host_bytes` of pinned host memory and creates two
+ * non-blocking copy streams (D2H, H2D). */
+delta_status delta_swap_create(uint64_t host_bytes, delta_swap** out);
+void* delta_swap_host_ptr(const delta_swap* s);
+void* delta_swap_stream(const delta_swap* s, int32_t which); /* 1 D2H, 2 H2D */
+delta_status delta_swap_offload(delta_swap* s, const void* dev, uint64_t host_off,
+                                uint64_t bytes, void* stream);
+delta_status delta_swap_reload(delta_swap* s, void* dev, uint64_t host_off, uint64_t bytes,
+                               void* stream);
+void delta_swap_destroy(delta_swap* s);
+
+/* ---- cost model: host-link probe (GB/s) with pinned memory ---- */
+delta_status delta_probe_link(uint64_t bytes, int32_t iters, double* h2d_gbs, double* d2h_gbs,
+                              double* duplex_gbs);
+
+/* ---- events for program replay ---- */
+typedef struct delta_events delta_events;
+delta_status delta_events_create(uint32_t n, delta_events** out);
+delta_status delta_event_record(delta_events* e, uint32_t i, void* stream);
+delta_status delta_event_wait(delta_events* e, uint32_t i, void* stream);
+void delta_events_destroy(delta_events* e);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* DELTA_DELTA_KERNELS_H_ */

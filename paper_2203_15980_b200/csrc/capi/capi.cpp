@@ -107,6 +107,10 @@ void fill(delta_result* out) {
 
 }  // namespace
 
+namespace delta_rt {
+void set_error(const std::string& msg) { g_err = msg; }
+}  // namespace delta_rt
+
 extern "C" {
 
 const char* delta_last_error(void) { return g_err.c_str(); }

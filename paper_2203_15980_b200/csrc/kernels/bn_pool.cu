@@ -1,0 +1,576 @@
+// HBM-bound kernels of the recompute engine and the backward pass:
+// BatchNorm statistics / apply (fused ReLU, fused residual add, fused second
+// BN on the shortcut), BN backward, gradient adds, max/avg pooling and the
+// softmax cross-entropy head.
+//
+// Layout: NHWC bf16 viewed as [M = N*H*W rows][C channels], C a power of two
+// (64..2048).  Each thread moves 8 channels (16 B) per access.  Every
+// reduction is deterministic: per-chunk partials in a fixed grid position,
+// merged in a fixed order (no atomics), so the forward statistics — and hence
+// every recomputed activation — are reproducible bit for bit.
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "kernels/kernels.hpp"
+
+namespace delta_k {
+
+using bf16 = __nv_bfloat16;
+
+namespace {
+
+constexpr int CHUNK = 512;  // rows per reduction partial
+constexpr int SLICE = 64;   // channels per reduction block
+
+__device__ __forceinline__ uint4 ld_stream(const void* p) {
+  uint4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(p));
+  return r;
+}
+__device__ __forceinline__ void unpack8(uint4 u, float (&f)[8]) {
+  const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&u);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    float2 t = __bfloat1622float2(h[i]);
+    f[2 * i] = t.x;
+    f[2 * i + 1] = t.y;
+  }
+}
+__device__ __forceinline__ uint4 pack8(const float (&f)[8]) {
+  uint4 u;
+  __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&u);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) h[i] = __floats2bfloat162_rn(f[2 * i], f[2 * i + 1]);
+  return u;
+}
+
+int grid_for(int64_t work_items, int threads) {
+  int64_t blocks = (work_items + threads - 1) / threads;
+  int64_t cap = 148 * 16;
+  return int(blocks < cap ? (blocks < 1 ? 1 : blocks) : cap);
+}
+
+// Chan et al. parallel merge of (n, mean, M2).
+__device__ __forceinline__ void merge(float& n, float& mu, float& m2, float nb, float mub,
+                                      float m2b) {
+  if (nb == 0.f) return;
+  float nn = n + nb;
+  float d = mub - mu;
+  mu += d * (nb / nn);
+  m2 += m2b + d * d * (n * nb / nn);
+  n = nn;
+}
+
+// ---------------------------------------------------------------- BN stats
+__global__ void __launch_bounds__(256) k_bn_stats_partial(const bf16* __restrict__ x, int64_t M,
+                                                          int C, float2* __restrict__ ws) {
+  const int tx = threadIdx.x & 7, ty = threadIdx.x >> 3;
+  const int c0 = blockIdx.x * SLICE + tx * 8;
+  const int64_t r0 = int64_t(blockIdx.y) * CHUNK;
+  const int64_t r1 = min(M, r0 + CHUNK);
+  float s[8] = {0}, q[8] = {0};
+#pragma unroll 4
+  for (int64_t r = r0 + ty; r < r1; r += 32) {
+    float f[8];
+    unpack8(ld_stream(x + r * C + c0), f);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      s[i] += f[i];
+      q[i] = fmaf(f[i], f[i], q[i]);
+    }
+  }
+  __shared__ float ss[32][SLICE + 1], sq[32][SLICE + 1];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    ss[ty][tx * 8 + i] = s[i];
+    sq[ty][tx * 8 + i] = q[i];
+  }
+  __syncthreads();
+  if (threadIdx.x < SLICE) {
+    float S = 0.f, Q = 0.f;
+    for (int j = 0; j < 32; ++j) {
+      S += ss[j][threadIdx.x];
+      Q += sq[j][threadIdx.x];
+    }
+    const float n = float(r1 - r0);
+    const float mu = S / n;
+    ws[int64_t(blockIdx.y) * C + blockIdx.x * SLICE + threadIdx.x] =
+        make_float2(mu, fmaxf(Q - S * mu, 0.f));
+  }
+}
+
+__global__ void __launch_bounds__(256) k_bn_stats_final(const float2* __restrict__ ws, int chunks,
+                                                        int64_t M, int C, float* mean,
+                                                        float* invstd, float eps, float* rm,
+                                                        float* rv, float mom) {
+  const int cl = threadIdx.x >> 3, lane = threadIdx.x & 7;
+  const int c = blockIdx.x * 32 + cl;
+  float n = 0.f, mu = 0.f, m2 = 0.f;
+  if (c < C) {
+    for (int k = lane; k < chunks; k += 8) {
+      const float nb = float(k == chunks - 1 ? M - int64_t(k) * CHUNK : CHUNK);
+      const float2 p = ws[int64_t(k) * C + c];
+      merge(n, mu, m2, nb, p.x, p.y);
+    }
+  }
+  __shared__ float sn[256], smu[256], sm2[256];
+  sn[threadIdx.x] = n;
+  smu[threadIdx.x] = mu;
+  sm2[threadIdx.x] = m2;
+  __syncthreads();
+  if (lane == 0 && c < C) {
+    for (int j = 1; j < 8; ++j)
+      merge(n, mu, m2, sn[threadIdx.x + j], smu[threadIdx.x + j], sm2[threadIdx.x + j]);
+    const float var = m2 / float(M);
+    mean[c] = mu;
+    invstd[c] = rsqrtf(var + eps);
+    if (rm) {
+      rm[c] = (1.f - mom) * rm[c] + mom * mu;
+      rv[c] = (1.f - mom) * rv[c] + mom * (M > 1 ? m2 / float(M - 1) : var);
+    }
+  }
+}
+
+// ---------------------------------------------------------------- BN apply
+template <int MODE>
+__global__ void __launch_bounds__(256)
+    k_bn_apply(const bf16* __restrict__ x, const bf16* __restrict__ res, bf16* __restrict__ y,
+               int64_t vecs, int cmask, int C, const float* mean, const float* invstd,
+               const float* gamma, const float* beta, const float* mean2, const float* invstd2,
+               const float* gamma2, const float* beta2) {
+  extern __shared__ float sp[];  // scale, shift [, scale2, shift2]
+  for (int c = threadIdx.x; c < C; c += blockDim.x) {
+    const float sc = invstd[c] * gamma[c];
+    sp[c] = sc;
+    sp[C + c] = beta[c] - mean[c] * sc;
+    if (MODE == 2) {
+      const float sc2 = invstd2[c] * gamma2[c];
+      sp[2 * C + c] = sc2;
+      sp[3 * C + c] = beta2[c] - mean2[c] * sc2;
+    }
+  }
+  __syncthreads();
+  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < vecs; i += stride) {
+    const int c0 = int(i * 8) & cmask;
+    float f[8];
+    unpack8(ld_stream(x + i * 8), f);
+    float r[8];
+    if (MODE >= 1) unpack8(ld_stream(res + i * 8), r);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      float v = fmaf(f[j], sp[c0 + j], sp[C + c0 + j]);
+      if (MODE == 1) v += r[j];
+      if (MODE == 2) v += fmaf(r[j], sp[2 * C + c0 + j], sp[3 * C + c0 + j]);
+      f[j] = fmaxf(v, 0.f);
+    }
+    reinterpret_cast<uint4*>(y)[i] = pack8(f);
+  }
+}
+
+// ------------------------------------------------------------- BN backward
+__device__ __forceinline__ void load_up(const bf16* up, int pool_hw, float inv_hw, int64_t row,
+                                        int c0, int C, float (&g)[8]) {
+  if (pool_hw) {
+    unpack8(*reinterpret_cast<const uint4*>(up + (row / pool_hw) * C + c0), g);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) g[j] *= inv_hw;
+  } else {
+    unpack8(ld_stream(up + row * C + c0), g);
+  }
+}
+
+__global__ void __launch_bounds__(256)
+    k_bn_bwd_partial(const bf16* __restrict__ up, int pool_hw, const bf16* __restrict__ mask,
+                     const bf16* __restrict__ x, int64_t M, int C, const float* mean,
+                     const float* invstd, float2* __restrict__ ws) {
+  const int tx = threadIdx.x & 7, ty = threadIdx.x >> 3;
+  const int c0 = blockIdx.x * SLICE + tx * 8;
+  const int64_t r0 = int64_t(blockIdx.y) * CHUNK;
+  const int64_t r1 = min(M, r0 + CHUNK);
+  const float inv_hw = pool_hw ? 1.f / float(pool_hw) : 1.f;
+  float mu[8], is[8];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    mu[j] = mean[c0 + j];
+    is[j] = invstd[c0 + j];
+  }
+  float sg[8] = {0}, sgx[8] = {0};
+#pragma unroll 2
+  for (int64_t r = r0 + ty; r < r1; r += 32) {
+    float g[8], m[8], xv[8];
+    load_up(up, pool_hw, inv_hw, r, c0, C, g);
+    unpack8(ld_stream(mask + r * C + c0), m);
+    unpack8(ld_stream(x + r * C + c0), xv);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const float gj = m[j] > 0.f ? g[j] : 0.f;
+      sg[j] += gj;
+      sgx[j] = fmaf(gj, (xv[j] - mu[j]) * is[j], sgx[j]);
+    }
+  }
+  __shared__ float a[32][SLICE + 1], b[32][SLICE + 1];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    a[ty][tx * 8 + j] = sg[j];
+    b[ty][tx * 8 + j] = sgx[j];
+  }
+  __syncthreads();
+  if (threadIdx.x < SLICE) {
+    float A = 0.f, B = 0.f;
+    for (int j = 0; j < 32; ++j) {
+      A += a[j][threadIdx.x];
+      B += b[j][threadIdx.x];
+    }
+    ws[int64_t(blockIdx.y) * C + blockIdx.x * SLICE + threadIdx.x] = make_float2(A, B);
+  }
+}
+
+__global__ void __launch_bounds__(256) k_bn_bwd_final(const float2* __restrict__ ws, int chunks,
+                                                      int C, float* dgamma, float* dbeta) {
+  const int cl = threadIdx.x >> 3, lane = threadIdx.x & 7;
+  const int c = blockIdx.x * 32 + cl;
+  float A = 0.f, B = 0.f;
+  if (c < C)
+    for (int k = lane; k < chunks; k += 8) {
+      const float2 p = ws[int64_t(k) * C + c];
+      A += p.x;
+      B += p.y;
+    }
+  __shared__ float sa[256], sb[256];
+  sa[threadIdx.x] = A;
+  sb[threadIdx.x] = B;
+  __syncthreads();
+  if (lane == 0 && c < C) {
+    for (int j = 1; j < 8; ++j) {
+      A += sa[threadIdx.x + j];
+      B += sb[threadIdx.x + j];
+    }
+    dbeta[c] = A;
+    dgamma[c] = B;
+  }
+}
+
+__global__ void __launch_bounds__(256)
+    k_bn_bwd_apply(const bf16* __restrict__ up, int pool_hw, const bf16* __restrict__ mask,
+                   const bf16* __restrict__ x, bf16* __restrict__ dx, int64_t vecs, int cmask,
+                   int logC, int C, int64_t M, const float* mean, const float* invstd, const float* gamma,
+                   const float* dgamma, const float* dbeta) {
+  extern __shared__ float sp[];  // a, b, d, mean, invstd
+  const float invM = 1.f / float(M);
+  for (int c = threadIdx.x; c < C; c += blockDim.x) {
+    sp[c] = gamma[c] * invstd[c];
+    sp[C + c] = dbeta[c] * invM;
+    sp[2 * C + c] = dgamma[c] * invM;
+    sp[3 * C + c] = mean[c];
+    sp[4 * C + c] = invstd[c];
+  }
+  __syncthreads();
+  const float inv_hw = pool_hw ? 1.f / float(pool_hw) : 1.f;
+  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < vecs; i += stride) {
+    const int c0 = int(i * 8) & cmask;
+    const int64_t row = (i * 8) >> logC;
+    float g[8], m[8], xv[8];
+    load_up(up, pool_hw, inv_hw, row, c0, C, g);
+    unpack8(ld_stream(mask + i * 8), m);
+    unpack8(ld_stream(x + i * 8), xv);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const int c = c0 + j;
+      const float gj = m[j] > 0.f ? g[j] : 0.f;
+      const float xh = (xv[j] - sp[3 * C + c]) * sp[4 * C + c];
+      g[j] = sp[c] * (gj - sp[C + c] - xh * sp[2 * C + c]);
+    }
+    reinterpret_cast<uint4*>(dx)[i] = pack8(g);
+  }
+}
+
+__global__ void __launch_bounds__(256)
+    k_add_grad(const bf16* __restrict__ a, const bf16* __restrict__ up, int pool_hw,
+               const bf16* __restrict__ mask, bf16* __restrict__ out, int64_t vecs, int cmask,
+               int logC, int C) {
+  const float inv_hw = pool_hw ? 1.f / float(pool_hw) : 1.f;
+  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < vecs; i += stride) {
+    const int c0 = int(i * 8) & cmask;
+    const int64_t row = (i * 8) >> logC;
+    float fa[8], g[8];
+    unpack8(ld_stream(a + i * 8), fa);
+    if (mask) {
+      float m[8];
+      load_up(up, pool_hw, inv_hw, row, c0, C, g);
+      unpack8(ld_stream(mask + i * 8), m);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) fa[j] += m[j] > 0.f ? g[j] : 0.f;
+    } else {
+      unpack8(ld_stream(up + i * 8), g);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) fa[j] += g[j];
+    }
+    reinterpret_cast<uint4*>(out)[i] = pack8(fa);
+  }
+}
+
+// ----------------------------------------------------------------- pooling
+__global__ void __launch_bounds__(256) k_maxpool_fwd(const bf16* __restrict__ x,
+                                                     bf16* __restrict__ y, int N, int H, int W,
+                                                     int C, int P, int Q) {
+  const int cg = C / 8;
+  const int64_t total = int64_t(N) * P * Q * cg;
+  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < total; i += stride) {
+    const int c0 = int(i % cg) * 8;
+    int64_t t = i / cg;
+    const int q = int(t % Q);
+    t /= Q;
+    const int p = int(t % P);
+    const int n = int(t / P);
+    float best[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) best[j] = -INFINITY;
+    for (int dh = 0; dh < 3; ++dh) {
+      const int h = 2 * p - 1 + dh;
+      if (h < 0 || h >= H) continue;
+      for (int dw = 0; dw < 3; ++dw) {
+        const int w = 2 * q - 1 + dw;
+        if (w < 0 || w >= W) continue;
+        float f[8];
+        unpack8(*reinterpret_cast<const uint4*>(x + ((int64_t(n) * H + h) * W + w) * C + c0), f);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) best[j] = f[j] > best[j] ? f[j] : best[j];
+      }
+    }
+    reinterpret_cast<uint4*>(y)[i] = pack8(best);
+  }
+}
+
+// Gather form: each input pixel collects the gradient of every (<= 4) output
+// window whose first-in-scan-order argmax it is.  No atomics.
+__global__ void __launch_bounds__(256)
+    k_maxpool_bwd(const bf16* __restrict__ dy, const bf16* __restrict__ x, bf16* __restrict__ dx,
+                  int N, int H, int W, int C, int P, int Q) {
+  const int cg = C / 8;
+  const int64_t total = int64_t(N) * H * W * cg;
+  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < total; i += stride) {
+    const int c0 = int(i % cg) * 8;
+    int64_t t = i / cg;
+    const int w = int(t % W);
+    t /= W;
+    const int h = int(t % H);
+    const int n = int(t / H);
+    float acc[8] = {0};
+    const int p_lo = h / 2, p_hi = min(P - 1, (h + 1) / 2);
+    const int q_lo = w / 2, q_hi = min(Q - 1, (w + 1) / 2);
+    for (int p = p_lo; p <= p_hi; ++p)
+      for (int q = q_lo; q <= q_hi; ++q) {
+        float best[8];
+        int arg[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          best[j] = -INFINITY;
+          arg[j] = -1;
+        }
+        for (int dh = 0; dh < 3; ++dh) {
+          const int hh = 2 * p - 1 + dh;
+          if (hh < 0 || hh >= H) continue;
+          for (int dw = 0; dw < 3; ++dw) {
+            const int ww = 2 * q - 1 + dw;
+            if (ww < 0 || ww >= W) continue;
+            float f[8];
+            unpack8(*reinterpret_cast<const uint4*>(x + ((int64_t(n) * H + hh) * W + ww) * C + c0),
+                    f);
+#pragma unroll
+            for (int j = 0; j < 8; ++j)
+              if (f[j] > best[j]) {
+                best[j] = f[j];
+                arg[j] = hh * W + ww;
+              }
+          }
+        }
+        float g[8];
+        unpack8(*reinterpret_cast<const uint4*>(dy + ((int64_t(n) * P + p) * Q + q) * C + c0), g);
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+          if (arg[j] == h * W + w) acc[j] += g[j];
+      }
+    reinterpret_cast<uint4*>(dx)[i] = pack8(acc);
+  }
+}
+
+__global__ void __launch_bounds__(256) k_avgpool_fwd(const bf16* __restrict__ x,
+                                                     bf16* __restrict__ y, int N, int HW, int C) {
+  const int cg = C / 8;
+  const int64_t total = int64_t(N) * cg;
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < total;
+       i += int64_t(gridDim.x) * blockDim.x) {
+    const int c0 = int(i % cg) * 8;
+    const int n = int(i / cg);
+    float s[8] = {0};
+    for (int k = 0; k < HW; ++k) {
+      float f[8];
+      unpack8(*reinterpret_cast<const uint4*>(x + (int64_t(n) * HW + k) * C + c0), f);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) s[j] += f[j];
+    }
+    const float inv = 1.f / float(HW);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) s[j] *= inv;
+    reinterpret_cast<uint4*>(y)[i] = pack8(s);
+  }
+}
+
+// ------------------------------------------------------- softmax x-entropy
+__global__ void __launch_bounds__(256) k_softmax_xent(const float* __restrict__ logits,
+                                                      const int64_t* __restrict__ labels,
+                                                      float* __restrict__ dlogits,
+                                                      float* __restrict__ row_loss, int N, int K) {
+  const int n = blockIdx.x;
+  const float* l = logits + int64_t(n) * K;
+  __shared__ float red[256];
+  float mx = -INFINITY;
+  for (int k = threadIdx.x; k < K; k += blockDim.x) mx = fmaxf(mx, l[k]);
+  red[threadIdx.x] = mx;
+  __syncthreads();
+  for (int s = 128; s > 0; s >>= 1) {
+    if (threadIdx.x < s) red[threadIdx.x] = fmaxf(red[threadIdx.x], red[threadIdx.x + s]);
+    __syncthreads();
+  }
+  mx = red[0];
+  __syncthreads();
+  float sum = 0.f;
+  for (int k = threadIdx.x; k < K; k += blockDim.x) sum += __expf(l[k] - mx);
+  red[threadIdx.x] = sum;
+  __syncthreads();
+  for (int s = 128; s > 0; s >>= 1) {
+    if (threadIdx.x < s) red[threadIdx.x] += red[threadIdx.x + s];
+    __syncthreads();
+  }
+  sum = red[0];
+  const int lab = int(labels[n]);
+  const float invN = 1.f / float(N);
+  for (int k = threadIdx.x; k < K; k += blockDim.x) {
+    const float p = __expf(l[k] - mx) / sum;
+    dlogits[int64_t(n) * K + k] = (p - (k == lab ? 1.f : 0.f)) * invN;
+  }
+  if (threadIdx.x == 0) row_loss[n] = logf(sum) + mx - l[lab];
+}
+
+__global__ void k_mean_rows(const float* row_loss, int N, float* loss) {
+  if (threadIdx.x == 0 && blockIdx.x == 0) {
+    float s = 0.f;
+    for (int i = 0; i < N; ++i) s += row_loss[i];
+    *loss = s / float(N);
+  }
+}
+
+}  // namespace
+
+int64_t bn_workspace_floats(int64_t M, int C) { return 2 * ((M + CHUNK - 1) / CHUNK) * C; }
+
+cudaError_t bn_stats(const void* x, int64_t M, int C, float* ws, float* mean, float* invstd,
+                     float eps, float* rm, float* rv, float mom, cudaStream_t st) {
+  if (C % SLICE) return cudaErrorInvalidValue;
+  const int chunks = int((M + CHUNK - 1) / CHUNK);
+  k_bn_stats_partial<<<dim3(C / SLICE, chunks), 256, 0, st>>>(static_cast<const bf16*>(x), M, C,
+                                                              reinterpret_cast<float2*>(ws));
+  k_bn_stats_final<<<(C + 31) / 32, 256, 0, st>>>(reinterpret_cast<const float2*>(ws), chunks, M,
+                                                  C, mean, invstd, eps, rm, rv, mom);
+  return cudaGetLastError();
+}
+
+cudaError_t bn_apply(int mode, const void* x, const void* res, void* y, int64_t M, int C,
+                     const float* mean, const float* invstd, const float* gamma, const float* beta,
+                     const float* mean2, const float* invstd2, const float* gamma2,
+                     const float* beta2, cudaStream_t st) {
+  if (C & (C - 1)) return cudaErrorInvalidValue;
+  const int64_t vecs = M * C / 8;
+  const int grid = grid_for(vecs, 256);
+  const size_t smem = size_t(mode == 2 ? 4 : 2) * C * sizeof(float);
+  auto X = static_cast<const bf16*>(x);
+  auto R = static_cast<const bf16*>(res);
+  auto Y = static_cast<bf16*>(y);
+  switch (mode) {
+    case 0:
+      k_bn_apply<0><<<grid, 256, smem, st>>>(X, R, Y, vecs, C - 1, C, mean, invstd, gamma, beta,
+                                             nullptr, nullptr, nullptr, nullptr);
+      break;
+    case 1:
+      k_bn_apply<1><<<grid, 256, smem, st>>>(X, R, Y, vecs, C - 1, C, mean, invstd, gamma, beta,
+                                             nullptr, nullptr, nullptr, nullptr);
+      break;
+    default:
+      k_bn_apply<2><<<grid, 256, smem, st>>>(X, R, Y, vecs, C - 1, C, mean, invstd, gamma, beta,
+                                             mean2, invstd2, gamma2, beta2);
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t bn_backward(const void* up, int pool_hw, const void* mask, const void* x, void* dx,
+                        int64_t M, int C, const float* mean, const float* invstd,
+                        const float* gamma, float* dgamma, float* dbeta, float* ws,
+                        cudaStream_t st) {
+  if (C % SLICE || (C & (C - 1))) return cudaErrorInvalidValue;
+  const int chunks = int((M + CHUNK - 1) / CHUNK);
+  auto U = static_cast<const bf16*>(up);
+  auto Mk = static_cast<const bf16*>(mask);
+  auto X = static_cast<const bf16*>(x);
+  k_bn_bwd_partial<<<dim3(C / SLICE, chunks), 256, 0, st>>>(U, pool_hw, Mk, X, M, C, mean,
+                                                            invstd, reinterpret_cast<float2*>(ws));
+  k_bn_bwd_final<<<(C + 31) / 32, 256, 0, st>>>(reinterpret_cast<const float2*>(ws), chunks, C,
+                                                dgamma, dbeta);
+  const int64_t vecs = M * C / 8;
+  k_bn_bwd_apply<<<grid_for(vecs, 256), 256, 5 * C * sizeof(float), st>>>(
+      U, pool_hw, Mk, X, static_cast<bf16*>(dx), vecs, C - 1, __builtin_ctz(C), C, M, mean, invstd, gamma, dgamma,
+      dbeta);
+  return cudaGetLastError();
+}
+
+cudaError_t add_grad(const void* a, const void* up, int pool_hw, const void* mask, void* out,
+                     int64_t M, int C, cudaStream_t st) {
+  if (C & (C - 1)) return cudaErrorInvalidValue;
+  const int64_t vecs = M * C / 8;
+  k_add_grad<<<grid_for(vecs, 256), 256, 0, st>>>(
+      static_cast<const bf16*>(a), static_cast<const bf16*>(up), pool_hw,
+      static_cast<const bf16*>(mask), static_cast<bf16*>(out), vecs, C - 1, __builtin_ctz(C), C);
+  return cudaGetLastError();
+}
+
+cudaError_t maxpool3x3s2_fwd(const void* x, void* y, int N, int H, int W, int C, cudaStream_t st) {
+  const int P = (H + 2 - 3) / 2 + 1, Q = (W + 2 - 3) / 2 + 1;
+  const int64_t total = int64_t(N) * P * Q * (C / 8);
+  k_maxpool_fwd<<<grid_for(total, 256), 256, 0, st>>>(static_cast<const bf16*>(x),
+                                                      static_cast<bf16*>(y), N, H, W, C, P, Q);
+  return cudaGetLastError();
+}
+
+cudaError_t maxpool3x3s2_bwd(const void* dy, const void* x, void* dx, int N, int H, int W, int C,
+                             cudaStream_t st) {
+  const int P = (H + 2 - 3) / 2 + 1, Q = (W + 2 - 3) / 2 + 1;
+  const int64_t total = int64_t(N) * H * W * (C / 8);
+  k_maxpool_bwd<<<grid_for(total, 256), 256, 0, st>>>(static_cast<const bf16*>(dy),
+                                                      static_cast<const bf16*>(x),
+                                                      static_cast<bf16*>(dx), N, H, W, C, P, Q);
+  return cudaGetLastError();
+}
+
+cudaError_t avgpool_fwd(const void* x, void* y, int N, int HW, int C, cudaStream_t st) {
+  const int64_t total = int64_t(N) * (C / 8);
+  k_avgpool_fwd<<<grid_for(total, 128), 128, 0, st>>>(static_cast<const bf16*>(x),
+                                                      static_cast<bf16*>(y), N, HW, C);
+  return cudaGetLastError();
+}
+
+cudaError_t softmax_xent(const float* logits, const int64_t* labels, float* loss, float* dlogits,
+                         float* row_loss_ws, int N, int K, cudaStream_t st) {
+  k_softmax_xent<<<N, 256, 0, st>>>(logits, labels, dlogits, row_loss_ws, N, K);
+  k_mean_rows<<<1, 32, 0, st>>>(row_loss_ws, N, loss);
+  return cudaGetLastError();
+}
+
+}  // namespace delta_k

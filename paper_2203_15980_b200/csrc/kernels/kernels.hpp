@@ -1,0 +1,53 @@
+// Internal launch interface of the sm_100a kernels (wrapped by capi_kernels.cpp).
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+namespace delta_k {
+
+// ---- implicit-GEMM convolution (conv_fwd.cu) ----
+struct ConvPlan {
+  int N, H, W, C, K, R, S, stride, pad;
+  int P, Q, kdim, bn;
+  alignas(64) unsigned char wmap[128];  // CUtensorMap over the [K][kdim] weight matrix
+};
+// 0 ok, 1 unsupported shape, 2 no driver entry point, 3 tensor-map encode failed
+int conv_plan_init(ConvPlan* cp, const void* w);
+cudaError_t conv_forward(const ConvPlan& cp, const void* x, void* y, cudaStream_t st);
+
+// ---- batch norm / elementwise / pooling (bn_pool.cu) ----
+int64_t bn_workspace_floats(int64_t M, int C);
+cudaError_t bn_stats(const void* x, int64_t M, int C, float* ws, float* mean, float* invstd,
+                     float eps, float* run_mean, float* run_var, float momentum, cudaStream_t st);
+
+// mode 0: y = relu(bn(x)); 1: y = relu(bn(x) + res); 2: y = relu(bn(x) + bn2(res))
+cudaError_t bn_apply(int mode, const void* x, const void* res, void* y, int64_t M, int C,
+                     const float* mean, const float* invstd, const float* gamma, const float* beta,
+                     const float* mean2, const float* invstd2, const float* gamma2,
+                     const float* beta2, cudaStream_t st);
+
+// BN(+ReLU) backward.  g = up * (mask > 0), where `up` is a full [M,C] bf16
+// gradient (pool_hw == 0) or a pooled [N,C] bf16 gradient broadcast over
+// pool_hw pixels and scaled by 1/pool_hw.  Writes dx (bf16) and the
+// parameter gradients dgamma, dbeta (fp32).
+cudaError_t bn_backward(const void* up, int pool_hw, const void* mask, const void* x, void* dx,
+                        int64_t M, int C, const float* mean, const float* invstd,
+                        const float* gamma, float* dgamma, float* dbeta, float* ws,
+                        cudaStream_t st);
+
+// out = a + b (bf16)            when mask == nullptr
+// out = a + up * (mask > 0)     otherwise (up full or pooled as above)
+cudaError_t add_grad(const void* a, const void* up, int pool_hw, const void* mask, void* out,
+                     int64_t M, int C, cudaStream_t st);
+
+cudaError_t maxpool3x3s2_fwd(const void* x, void* y, int N, int H, int W, int C, cudaStream_t st);
+cudaError_t maxpool3x3s2_bwd(const void* dy, const void* x, void* dx, int N, int H, int W, int C,
+                             cudaStream_t st);
+cudaError_t avgpool_fwd(const void* x, void* y, int N, int HW, int C, cudaStream_t st);
+
+// loss = mean_i -log softmax(logits_i)[label_i]; dlogits = (softmax - onehot) / N
+cudaError_t softmax_xent(const float* logits, const int64_t* labels, float* loss, float* dlogits,
+                         float* row_loss_ws, int N, int K, cudaStream_t st);
+
+}  // namespace delta_k

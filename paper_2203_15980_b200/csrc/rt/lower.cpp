@@ -67,7 +67,7 @@ Program lower_plan(const Trace& trace, const EngineConfig& cfg,
       std::uint64_t b = (op.bytes + align - 1) & ~(align - 1);
       live[op.node] = allocs.size();
       alloc_of_op[k] = allocs.size();
-      allocs.push_back({op.node, b, k});
+      allocs.push_back(Alloc{op.node, b, k, kNever, 0, {}});
     } else {
       auto it = live.find(op.node);
       if (it == live.end()) throw InternalError("lower: free of non-live node " + std::to_string(op.node));

@@ -1,0 +1,42 @@
+"""Micro-benchmark of the sm_100a conv kernel on the ResNet-50 bs256 shapes
+(CUDA events on the launching stream, inputs > L2), beside cuDNN."""
+import json, sys, os
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch
+import torch.nn.functional as F
+from paper_2203_15980_b200 import kernels as K
+
+def timeit(fn, iters=20):
+    for _ in range(3): fn()
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize(); s.record()
+    for _ in range(iters): fn()
+    e.record(); torch.cuda.synchronize()
+    return s.elapsed_time(e) / iters
+
+N = int(sys.argv[1]) if len(sys.argv) > 1 else 256
+shapes = [  # H, C, K, R, stride, pad
+    (56, 64, 64, 1, 1, 0), (56, 64, 64, 3, 1, 1), (56, 64, 256, 1, 1, 0), (56, 256, 64, 1, 1, 0),
+    (56, 256, 128, 1, 1, 0), (56, 128, 128, 3, 2, 1), (28, 128, 512, 1, 1, 0), (56, 256, 512, 1, 2, 0),
+    (28, 512, 128, 1, 1, 0), (28, 128, 128, 3, 1, 1), (14, 256, 256, 3, 1, 1), (14, 256, 1024, 1, 1, 0),
+    (14, 1024, 256, 1, 1, 0), (7, 512, 512, 3, 1, 1), (7, 512, 2048, 1, 1, 0), (7, 2048, 512, 1, 1, 0),
+]
+st = torch.cuda.current_stream().cuda_stream
+out = []
+for (H, C, Ko, R, s, p) in shapes:
+    x = torch.randn(N, H, H, C, device="cuda").to(torch.bfloat16)
+    w = (torch.randn(Ko, R, R, C, device="cuda") * 0.05).to(torch.bfloat16)
+    conv = K.Conv(N, H, H, C, Ko, R, R, s, p, w.data_ptr())
+    y = torch.empty(N, conv.P, conv.Q, Ko, device="cuda", dtype=torch.bfloat16)
+    ms = timeit(lambda: conv(x.data_ptr(), y.data_ptr(), st))
+    xc = x.permute(0, 3, 1, 2)  # channels_last view
+    wc = w.permute(0, 3, 1, 2)
+    ms_cudnn = timeit(lambda: F.conv2d(xc, wc, stride=s, padding=p))
+    flops = 2.0 * N * conv.P * conv.Q * Ko * C * R * R
+    byts = x.numel() * 2 + y.numel() * 2
+    out.append(dict(shape=[H, C, Ko, R, s], ms=round(ms, 4), tflops=round(flops / ms / 1e9, 1),
+                    gbs=round(byts / ms / 1e6, 1), cudnn_ms=round(ms_cudnn, 4),
+                    cudnn_tflops=round(flops / ms_cudnn / 1e9, 1)))
+    print(json.dumps(out[-1]), flush=True)
+h2d, d2h, dup = K.probe_link()
+print(json.dumps(dict(link_h2d_gbs=h2d, link_d2h_gbs=d2h, link_duplex_gbs=dup)))

@@ -1,0 +1,213 @@
+"""GPU parity of the sm_100a kernels against a plain PyTorch fp32 reference of
+the same op (tolerances stated per test), plus bitwise determinism (the
+recompute engine's requirement: re-running a kernel on the same inputs
+reproduces the retained tensor bit for bit)."""
+import pytest
+import torch
+import torch.nn.functional as F
+
+pytestmark = pytest.mark.gpu
+
+from paper_2203_15980_b200 import kernels as K  # noqa: E402
+
+
+def _stream():
+    return torch.cuda.current_stream().cuda_stream
+
+
+def ref_conv(x_nhwc, w_krsc, stride, pad):
+    y = F.conv2d(x_nhwc.permute(0, 3, 1, 2).float(), w_krsc.permute(0, 3, 1, 2).float(),
+                 stride=stride, padding=pad)
+    return y.permute(0, 2, 3, 1)
+
+
+CONV_CASES = [
+    # N, H, W, C, K, R, stride, pad
+    (2, 56, 56, 64, 256, 1, 1, 0),
+    (2, 56, 56, 64, 64, 3, 1, 1),
+    (2, 56, 56, 128, 128, 3, 2, 1),
+    (2, 56, 56, 256, 512, 1, 2, 0),
+    (1, 7, 7, 512, 2048, 1, 1, 0),
+    (3, 7, 7, 512, 512, 3, 1, 1),
+    (256, 1, 1, 2048, 1000, 1, 1, 0),
+]
+
+
+@pytest.mark.parametrize("case", CONV_CASES)
+def test_conv_fwd_matches_fp32_reference(case):
+    N, H, W, Cin, Kout, R, st, pad = case
+    g = torch.Generator(device="cuda").manual_seed(0)
+    x = torch.randn(N, H, W, Cin, device="cuda", generator=g).to(torch.bfloat16)
+    w = (torch.randn(Kout, R, R, Cin, device="cuda", generator=g) / (R * R * Cin) ** 0.5).to(torch.bfloat16)
+    conv = K.Conv(N, H, W, Cin, Kout, R, R, st, pad, w.data_ptr())
+    y = torch.empty(N, conv.P, conv.Q, Kout, device="cuda", dtype=torch.bfloat16)
+    conv(x.data_ptr(), y.data_ptr(), _stream())
+    torch.cuda.synchronize()
+    ref = ref_conv(x, w, st, pad)
+    err = (y.float() - ref).abs()
+    # bf16 output rounding (2^-8 relative) + fp32 accumulation-order noise
+    tol = 1e-2 * ref.abs() + 2e-2 * ref.pow(2).mean().sqrt()
+    assert bool((err <= tol).all()), f"max err {err.max().item()} rms {ref.pow(2).mean().sqrt().item()}"
+    # bitwise-identical recompute
+    y2 = torch.empty_like(y)
+    conv(x.data_ptr(), y2.data_ptr(), _stream())
+    torch.cuda.synchronize()
+    assert torch.equal(y, y2)
+
+
+def test_conv_stem_packed_c4():
+    N, H, W, Kout = 2, 224, 224, 64
+    g = torch.Generator(device="cuda").manual_seed(1)
+    x = torch.zeros(N, H, W, 4, device="cuda", dtype=torch.bfloat16)
+    x[..., :3] = torch.randn(N, H, W, 3, device="cuda", generator=g).to(torch.bfloat16)
+    w = (torch.randn(Kout, 7, 7, 3, device="cuda", generator=g) / 12).to(torch.bfloat16)
+    kdim = (7 * 7 * 4 + 63) // 64 * 64
+    wp = torch.zeros(Kout, kdim, device="cuda", dtype=torch.bfloat16)
+    w4 = torch.zeros(Kout, 7, 7, 4, device="cuda", dtype=torch.bfloat16)
+    w4[..., :3] = w
+    wp[:, :7 * 7 * 4] = w4.reshape(Kout, -1)
+    conv = K.Conv(N, H, W, 4, Kout, 7, 7, 2, 3, wp.data_ptr())
+    y = torch.empty(N, conv.P, conv.Q, Kout, device="cuda", dtype=torch.bfloat16)
+    conv(x.data_ptr(), y.data_ptr(), _stream())
+    torch.cuda.synchronize()
+    ref = ref_conv(x[..., :3].contiguous(), w, 2, 3)
+    err = (y.float() - ref).abs()
+    tol = 1e-2 * ref.abs() + 2e-2 * ref.pow(2).mean().sqrt()
+    assert bool((err <= tol).all()), f"max err {err.max().item()}"
+
+
+def _bn_params(C, g):
+    gamma = (1 + 0.1 * torch.randn(C, device="cuda", generator=g)).float()
+    beta = (0.1 * torch.randn(C, device="cuda", generator=g)).float()
+    return gamma, beta
+
+
+@pytest.mark.parametrize("M,C", [(2 * 56 * 56, 64), (2 * 28 * 28, 512), (3 * 7 * 7, 2048), (513, 256)])
+def test_bn_stats_apply_relu(M, C):
+    g = torch.Generator(device="cuda").manual_seed(2)
+    x = (torch.randn(M, C, device="cuda", generator=g) * 2 + 0.5).to(torch.bfloat16)
+    gamma, beta = _bn_params(C, g)
+    ws = torch.empty(K.bn_workspace_floats(M, C), device="cuda")
+    mean = torch.empty(C, device="cuda"); invstd = torch.empty(C, device="cuda")
+    rm = torch.zeros(C, device="cuda"); rv = torch.ones(C, device="cuda")
+    K.bn_stats(x.data_ptr(), M, C, ws.data_ptr(), mean.data_ptr(), invstd.data_ptr(), 1e-5,
+               rm.data_ptr(), rv.data_ptr(), 0.1, _stream())
+    xf = x.float()
+    torch.cuda.synchronize()
+    assert torch.allclose(mean, xf.mean(0), rtol=1e-4, atol=1e-4)
+    assert torch.allclose(invstd, torch.rsqrt(xf.var(0, unbiased=False) + 1e-5), rtol=1e-4)
+    assert torch.allclose(rm, 0.1 * xf.mean(0), rtol=1e-4, atol=1e-5)
+    y = torch.empty_like(x)
+    K.bn_apply(0, x.data_ptr(), None, y.data_ptr(), M, C, mean.data_ptr(), invstd.data_ptr(),
+               gamma.data_ptr(), beta.data_ptr(), stream=_stream())
+    torch.cuda.synchronize()
+    ref = torch.relu((xf - mean) * invstd * gamma + beta)
+    assert (y.float() - ref).abs().max().item() <= 1e-2 * ref.abs().max().item() + 1e-3
+    y2 = torch.empty_like(x)  # recompute with the saved statistics: bit-identical
+    K.bn_apply(0, x.data_ptr(), None, y2.data_ptr(), M, C, mean.data_ptr(), invstd.data_ptr(),
+               gamma.data_ptr(), beta.data_ptr(), stream=_stream())
+    torch.cuda.synchronize()
+    assert torch.equal(y, y2)
+
+
+def test_bn_add_relu_variants():
+    M, C = 2 * 14 * 14, 1024
+    g = torch.Generator(device="cuda").manual_seed(3)
+    x = torch.randn(M, C, device="cuda", generator=g).to(torch.bfloat16)
+    r = torch.randn(M, C, device="cuda", generator=g).to(torch.bfloat16)
+    ga, be = _bn_params(C, g)
+    ga2, be2 = _bn_params(C, g)
+    mu = torch.randn(C, device="cuda", generator=g) * 0.1
+    inv = torch.rand(C, device="cuda", generator=g) + 0.5
+    mu2 = torch.randn(C, device="cuda", generator=g) * 0.1
+    inv2 = torch.rand(C, device="cuda", generator=g) + 0.5
+    y = torch.empty_like(x)
+    K.bn_apply(1, x.data_ptr(), r.data_ptr(), y.data_ptr(), M, C, mu.data_ptr(), inv.data_ptr(),
+               ga.data_ptr(), be.data_ptr(), stream=_stream())
+    torch.cuda.synchronize()
+    ref = torch.relu((x.float() - mu) * inv * ga + be + r.float())
+    assert (y.float() - ref).abs().max().item() < 3e-2
+    K.bn_apply(2, x.data_ptr(), r.data_ptr(), y.data_ptr(), M, C, mu.data_ptr(), inv.data_ptr(),
+               ga.data_ptr(), be.data_ptr(), mu2.data_ptr(), inv2.data_ptr(), ga2.data_ptr(),
+               be2.data_ptr(), stream=_stream())
+    torch.cuda.synchronize()
+    ref = torch.relu((x.float() - mu) * inv * ga + be + (r.float() - mu2) * inv2 * ga2 + be2)
+    assert (y.float() - ref).abs().max().item() < 5e-2
+
+
+@pytest.mark.parametrize("pool_hw", [0, 49])
+def test_bn_backward_matches_autograd(pool_hw):
+    N, HW, C = 4, 49, 256
+    M = N * HW
+    g = torch.Generator(device="cuda").manual_seed(4)
+    x = torch.randn(M, C, device="cuda", generator=g).to(torch.bfloat16)
+    gamma, beta = _bn_params(C, g)
+    xf = x.float().requires_grad_(True)
+    gm = gamma.clone().requires_grad_(True)
+    bt = beta.clone().requires_grad_(True)
+    mean = xf.detach().mean(0)
+    invstd = torch.rsqrt(xf.detach().var(0, unbiased=False) + 1e-5)
+    y = torch.relu(F.batch_norm(xf, None, None, gm, bt, training=True, eps=1e-5))
+    yb = y.detach().to(torch.bfloat16)  # the stored (mask) tensor
+    if pool_hw:
+        up = torch.randn(N, C, device="cuda", generator=g).to(torch.bfloat16)
+        gfull = up.float().repeat_interleave(HW, 0) / HW
+    else:
+        up = torch.randn(M, C, device="cuda", generator=g).to(torch.bfloat16)
+        gfull = up.float()
+    gfull = gfull * (yb.float() > 0)
+    # reference through the mask of the stored bf16 output
+    yy = F.batch_norm(xf, None, None, gm, bt, training=True, eps=1e-5)
+    yy.backward(gfull)
+    dx = torch.empty_like(x)
+    dg = torch.empty(C, device="cuda"); db = torch.empty(C, device="cuda")
+    ws = torch.empty(K.bn_workspace_floats(M, C), device="cuda")
+    K.bn_backward(up.data_ptr(), pool_hw, yb.data_ptr(), x.data_ptr(), dx.data_ptr(), M, C,
+                  mean.data_ptr(), invstd.data_ptr(), gamma.data_ptr(), dg.data_ptr(),
+                  db.data_ptr(), ws.data_ptr(), _stream())
+    torch.cuda.synchronize()
+    assert torch.allclose(db, bt.grad, rtol=1e-3, atol=1e-3)
+    assert torch.allclose(dg, gm.grad, rtol=1e-3, atol=1e-3)
+    scale = xf.grad.abs().max().item()
+    assert (dx.float() - xf.grad).abs().max().item() <= 1.5e-2 * scale
+
+
+def test_maxpool_fwd_bwd_match_torch():
+    N, H, W, C = 2, 112, 112, 64
+    g = torch.Generator(device="cuda").manual_seed(5)
+    x = torch.relu(torch.randn(N, H, W, C, device="cuda", generator=g)).to(torch.bfloat16)
+    xf = x.float().permute(0, 3, 1, 2).contiguous().requires_grad_(True)
+    yr = F.max_pool2d(xf, 3, 2, 1)
+    y = torch.empty(N, 56, 56, C, device="cuda", dtype=torch.bfloat16)
+    K.maxpool_fwd(x.data_ptr(), y.data_ptr(), N, H, W, C, _stream())
+    torch.cuda.synchronize()
+    assert torch.equal(y.float(), yr.detach().permute(0, 2, 3, 1))
+    dy = torch.randn(N, 56, 56, C, device="cuda", generator=g).to(torch.bfloat16)
+    yr.backward(dy.float().permute(0, 3, 1, 2))
+    dx = torch.empty_like(x)
+    K.maxpool_bwd(dy.data_ptr(), x.data_ptr(), dx.data_ptr(), N, H, W, C, _stream())
+    torch.cuda.synchronize()
+    ref = xf.grad.permute(0, 2, 3, 1)
+    assert (dx.float() - ref).abs().max().item() <= 2e-2 * ref.abs().max().item()
+
+
+def test_avgpool_and_softmax_xent():
+    N, HW, C = 8, 49, 2048
+    g = torch.Generator(device="cuda").manual_seed(6)
+    x = torch.randn(N, HW, C, device="cuda", generator=g).to(torch.bfloat16)
+    y = torch.empty(N, C, device="cuda", dtype=torch.bfloat16)
+    K.avgpool_fwd(x.data_ptr(), y.data_ptr(), N, HW, C, _stream())
+    torch.cuda.synchronize()
+    assert (y.float() - x.float().mean(1)).abs().max().item() < 1e-2
+    logits = torch.randn(N, 1000, device="cuda", generator=g) * 3
+    labels = torch.randint(0, 1000, (N,), device="cuda", generator=g)
+    loss = torch.empty(1, device="cuda"); dl = torch.empty_like(logits)
+    ws = torch.empty(N, device="cuda")
+    K.softmax_xent(logits.data_ptr(), labels.data_ptr(), loss.data_ptr(), dl.data_ptr(),
+                   ws.data_ptr(), N, 1000, _stream())
+    lf = logits.clone().requires_grad_(True)
+    ref = F.cross_entropy(lf, labels)
+    ref.backward()
+    torch.cuda.synchronize()
+    assert abs(loss.item() - ref.item()) < 1e-4 * max(1.0, ref.item())
+    assert torch.allclose(dl, lf.grad, atol=1e-6, rtol=1e-4)
