@@ -265,7 +265,7 @@ class RunResult:
         return take_string(p, n.value)
 
     def __del__(self):
-        if getattr(self, "_ptr", None):
+        if getattr(self, "_ptr", None) and lib is not None:
             lib.delta_result_free(self._ptr)
             self._ptr = None
 
@@ -361,7 +361,7 @@ class Program:
         self.decisions = [(dp[i].node, ReleaseAction(dp[i].action)) for i in range(ne.value)]
 
     def __del__(self):
-        if getattr(self, "_ptr", None):
+        if getattr(self, "_ptr", None) and lib is not None:
             lib.delta_program_free(self._ptr)
             self._ptr = None
 

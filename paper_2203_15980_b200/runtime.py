@@ -1,0 +1,484 @@
+"""DELTA runtime on B200: plan on the logical clock, execute on the GPU.
+
+    rt = DeltaRuntime(depth=50, batch=256)             # graph + params
+    rt.measure_costs()                                  # GPU cost model -> trace costs
+    rt.plan(budget_fraction=0.5)                        # libdelta planner + lowering
+    loss = rt.step(x, y)                                # one training step
+
+The step replays the lowered action program (csrc/rt/lower.cpp) on three
+streams: compute (forward kernels, recompute kernels, backward), D2H and H2D
+(copy engines of the swap engine).  Every activation lives at its planned
+offset in one HBM arena; nothing else allocates activation memory.  Forward
+and recompute of a node run the SAME sm_100a kernel on the same inputs, so a
+recomputed tensor is bit-identical to the one it replaces.
+
+Outside the activation budget (as in the paper): fp32 master weights, bf16
+weight copies, gradients, optimizer state, BN statistics and the transient
+workspace of cuDNN's conv backward (dgrad/wgrad, the one library call on the
+backward path).
+"""
+from __future__ import annotations
+
+import math
+import time
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import graph as G
+from . import kernels as K
+from . import planner as P
+
+BN_EPS = 1e-5
+BN_MOMENTUM = 0.1
+
+
+def _ptr(t: torch.Tensor) -> int:
+    return t.data_ptr()
+
+
+class Params:
+    """fp32 master parameters (one flat buffer), bf16 conv weights (KRSC),
+    flat fp32 gradients and SGD momentum; BN running/saved statistics."""
+
+    def __init__(self, g: G.Graph, device, seed: int = 0):
+        self.g = g
+        gen = torch.Generator(device="cpu").manual_seed(seed)
+        specs = []  # (name, shape, init)
+        for name, cs in g.convs.items():
+            specs.append(("conv:" + name, (cs.cout, cs.k, cs.k, cs.cin), "kaiming", cs))
+        for name, c in g.bns.items():
+            specs.append(("bn_g:" + name, (c,), "ones", None))
+            specs.append(("bn_b:" + name, (c,), "zeros", None))
+        cin, ncls = g.fc
+        specs.append(("fc_w", (ncls, cin), "linear", cin))
+        specs.append(("fc_b", (ncls,), "linear_b", cin))
+        sizes = [int(np.prod(s[1])) for s in specs]
+        total = sum(sizes)
+        self.numel = total
+        self.master = torch.empty(total, dtype=torch.float32, device=device)
+        self.grad = torch.zeros(total, dtype=torch.float32, device=device)
+        self.mom = torch.zeros(total, dtype=torch.float32, device=device)
+        self.views, self.gviews = {}, {}
+        off = 0
+        n_conv = 0
+        for (name, shape, init, extra), n in zip(specs, sizes):
+            host = torch.empty(shape, dtype=torch.float32)
+            if init == "kaiming":
+                cs = extra
+                fan_out = cs.cout * cs.k * cs.k           # torchvision: fan_out, relu
+                host.normal_(0.0, math.sqrt(2.0 / fan_out), generator=gen)
+                if cs.cin == 4:
+                    host[..., 3] = 0.0                    # padded RGB channel
+            elif init == "ones":
+                host.fill_(1.0)
+            elif init == "zeros":
+                host.zero_()
+            else:
+                bound = 1.0 / math.sqrt(extra)
+                host.uniform_(-bound, bound, generator=gen)
+            self.master[off:off + n].copy_(host.reshape(-1))
+            self.views[name] = self.master[off:off + n].view(shape)
+            self.gviews[name] = self.grad[off:off + n].view(shape)
+            if init == "kaiming":
+                n_conv = off + n
+            off += n
+        self.n_conv = n_conv  # conv weights are the leading slice
+        self.conv_bf16 = torch.empty(n_conv, dtype=torch.bfloat16, device=device)
+        self.wbf = {}
+        off = 0
+        for name, cs in g.convs.items():
+            n = cs.cout * cs.k * cs.k * cs.cin
+            self.wbf[name] = self.conv_bf16[off:off + n].view(cs.cout, cs.k, cs.k, cs.cin)
+            off += n
+        # the stem kernel reads taps packed 4 channels each, K-dim padded to 64
+        self.stem_packed = {}
+        for name, cs in g.convs.items():
+            if cs.cin == 4:
+                kd = (cs.k * cs.k * 4 + 63) // 64 * 64
+                self.stem_packed[name] = torch.zeros(cs.cout, kd, dtype=torch.bfloat16,
+                                                     device=device)
+        self.bn_mean = {n: torch.zeros(c, device=device) for n, c in g.bns.items()}
+        self.bn_invstd = {n: torch.ones(c, device=device) for n, c in g.bns.items()}
+        self.bn_rmean = {n: torch.zeros(c, device=device) for n, c in g.bns.items()}
+        self.bn_rvar = {n: torch.ones(c, device=device) for n, c in g.bns.items()}
+        self.refresh_bf16()
+
+    def refresh_bf16(self):
+        self.conv_bf16.copy_(self.master[:self.n_conv])
+        for name, packed in self.stem_packed.items():
+            w = self.wbf[name]
+            packed[:, :w[0].numel()].copy_(w.reshape(w.shape[0], -1))
+
+    def sgd_step(self, lr: float, momentum: float = 0.9, weight_decay: float = 1e-4):
+        # grads stay untouched (they are what DP all-reduces and tests read)
+        self.mom.mul_(momentum).add_(self.grad).add_(self.master, alpha=weight_decay)
+        self.master.add_(self.mom, alpha=-lr)
+        self.refresh_bf16()
+
+
+@dataclass
+class StepStats:
+    loss: float
+    ms: float
+
+
+class DeltaRuntime:
+    """ResNet training step under a DELTA activation budget on one B200."""
+
+    def __init__(self, depth: int = 50, batch: int = 256, image: int = 224,
+                 device: str = "cuda", seed: int = 0, anchors: str = "out+narrow",
+                 lr: float = 0.1):
+        self.device = torch.device(device)
+        self.g = G.build_resnet(depth, batch, image)
+        self.batch = batch
+        self.lr = lr
+        self.anchors = anchors
+        apply_anchors(self.g, anchors)
+        G.estimate_costs(self.g)
+        self.params = Params(self.g, self.device, seed)
+        self.nodes = self.g.nodes
+        self.stream = torch.cuda.Stream(device=self.device)
+        self._convs = {}
+        self._build_convs()
+        maxM = max(int(np.prod(n.shape[:-1])) for n in self.nodes if len(n.shape) == 4)
+        maxC = max(self.g.bns.values())
+        self.bn_ws = torch.empty(max(K.bn_workspace_floats(int(np.prod(n.shape[:-1])), n.shape[-1])
+                                     for n in self.nodes if len(n.shape) == 4 and n.shape[-1] % 64 == 0),
+                                 dtype=torch.float32, device=self.device)
+        del maxM, maxC
+        ncls = self.g.fc[1]
+        self.loss = torch.zeros(1, dtype=torch.float32, device=self.device)
+        self.dlogits = torch.empty(batch, ncls, dtype=torch.float32, device=self.device)
+        self.row_loss = torch.empty(batch, dtype=torch.float32, device=self.device)
+        self.x_dev = torch.zeros(self.g.nodes[0].shape, dtype=torch.bfloat16, device=self.device)
+        self.y_dev = torch.zeros(batch, dtype=torch.int64, device=self.device)
+        self.program = None
+        self.arena = None
+        self.swap = None
+        self.events = None
+        self.graph = None
+        self.cost_table = None
+        self.link_gbs = None
+
+    # ------------------------------------------------------------ setup
+    def _build_convs(self):
+        for n in self.nodes:
+            if n.op == "conv":
+                cs = self.g.convs[n.attrs["conv"]]
+                src = self.nodes[n.parents[0]]
+                Nb, H, W, C = src.shape
+                wptr = (_ptr(self.params.stem_packed[cs.name]) if cs.cin == 4
+                        else _ptr(self.params.wbf[cs.name]))
+                conv = K.Conv(Nb, H, W, C, cs.cout, cs.k, cs.k, cs.stride, cs.pad, wptr)
+                assert (conv.P, conv.Q) == n.shape[1:3], (n.name, conv.P, conv.Q, n.shape)
+                self._convs[n.name] = conv
+
+    def trace(self) -> P.Trace:
+        return G.to_trace(self.g)
+
+    def engine_config(self, budget: int, policy=P.PolicyMode.Delta, **kw) -> P.EngineConfig:
+        cm = P.CostModel()
+        if self.link_gbs:
+            # measured one-way pinned copy bandwidth, bytes/us, exact fraction
+            bpus = int(self.link_gbs * 1e3)
+            cm = P.CostModel(bandwidth_bytes_per_us=(bpus, 1), effective_fraction=(1, 1))
+        return P.EngineConfig(budget=budget, policy_mode=policy, cost_model=cm, **kw)
+
+    def baseline_peak(self) -> int:
+        base = P.run_unconstrained_baseline(self.trace(), self.engine_config(0))
+        return base.peak_bytes
+
+    def plan(self, budget_fraction: float | None = 0.5, budget: int | None = None,
+             policy=P.PolicyMode.Delta, **kw):
+        """Plan with libdelta and lower onto the arena.  budget_fraction=None
+        plans the no-eviction baseline (Baseline policy, budget = sum)."""
+        t = self.trace()
+        if budget_fraction is None and budget is None:
+            total = sum(n.nbytes for n in self.nodes)
+            cfg = self.engine_config(total, P.PolicyMode.Baseline, **kw)
+        else:
+            if budget is None:
+                budget = int(self.baseline_peak() * budget_fraction)
+            cfg = self.engine_config(budget, policy, **kw)
+        prog = P.Program(t, cfg, align=G.ALIGN)
+        if prog.infeasible:
+            node, deficit = prog.infeasible
+            raise RuntimeError(f"plan infeasible at node {self.nodes[node].name} "
+                               f"(deficit {deficit} B, budget {cfg.budget} B)")
+        self.program = prog
+        self.config = cfg
+        self.graph = None
+        if self.arena is None or self.arena.numel() < prog.arena_bytes:
+            self.arena = None
+            torch.cuda.empty_cache()
+            self.arena = torch.empty(prog.arena_bytes, dtype=torch.uint8, device=self.device)
+        if prog.host_bytes and (self.swap is None or self._swap_bytes < prog.host_bytes):
+            self.swap = K.Swap(prog.host_bytes)
+            self._swap_bytes = prog.host_bytes
+        if self.swap is None:
+            self.swap = K.Swap(0)
+            self._swap_bytes = 0
+        self.events = K.Events(prog.n_events)
+        self._base = _ptr(self.arena)
+        self._inputs = prog.inputs
+        return prog
+
+    # -------------------------------------------------------- tensors
+    def _view(self, off: int, node: G.Node) -> torch.Tensor:
+        dt = torch.float32 if node.dtype_bytes == 4 else torch.bfloat16
+        n = int(np.prod(node.shape))
+        return self.arena.narrow(0, off, n * node.dtype_bytes).view(dt).view(node.shape)
+
+    # ------------------------------------------------------------ ops
+    def _run_node(self, node: G.Node, out_off: int, in_offs, recompute: bool, st: int):
+        base = self._base
+        op = node.op
+        out = base + out_off
+        ins = [base + o for o in in_offs]
+        pr = self.params
+        if op == "input":
+            self._view(out_off, node).copy_(self.x_dev, non_blocking=True)
+        elif op == "conv":
+            self._convs[node.name](ins[0], out, st)
+        elif op in ("bn_relu", "bn_add_relu", "bn_bn_add_relu"):
+            bn = node.attrs["bn"]
+            M = int(np.prod(node.shape[:-1]))
+            C = node.shape[-1]
+            if not recompute:  # statistics once per step; recompute reuses them
+                K.bn_stats(ins[0], M, C, _ptr(self.bn_ws), _ptr(pr.bn_mean[bn]),
+                           _ptr(pr.bn_invstd[bn]), BN_EPS, _ptr(pr.bn_rmean[bn]),
+                           _ptr(pr.bn_rvar[bn]), BN_MOMENTUM, st)
+            args = [_ptr(pr.bn_mean[bn]), _ptr(pr.bn_invstd[bn]), _ptr(pr.views["bn_g:" + bn]),
+                    _ptr(pr.views["bn_b:" + bn])]
+            if op == "bn_relu":
+                K.bn_apply(0, ins[0], None, out, M, C, *args, stream=st)
+            elif op == "bn_add_relu":
+                K.bn_apply(1, ins[0], ins[1], out, M, C, *args, stream=st)
+            else:
+                bn2 = node.attrs["bn2"]
+                if not recompute:
+                    K.bn_stats(ins[1], M, C, _ptr(self.bn_ws), _ptr(pr.bn_mean[bn2]),
+                               _ptr(pr.bn_invstd[bn2]), BN_EPS, _ptr(pr.bn_rmean[bn2]),
+                               _ptr(pr.bn_rvar[bn2]), BN_MOMENTUM, st)
+                K.bn_apply(2, ins[0], ins[1], out, M, C, *args, _ptr(pr.bn_mean[bn2]),
+                           _ptr(pr.bn_invstd[bn2]), _ptr(pr.views["bn_g:" + bn2]),
+                           _ptr(pr.views["bn_b:" + bn2]), stream=st)
+        elif op == "maxpool":
+            src = self.nodes[node.parents[0]]
+            Nb, H, W, C = src.shape
+            K.maxpool_fwd(ins[0], out, Nb, H, W, C, st)
+        elif op == "avgpool":
+            src = self.nodes[node.parents[0]]
+            Nb, H, W, C = src.shape
+            K.avgpool_fwd(ins[0], out, Nb, H * W, C, st)
+        elif op == "fc":
+            a = self._view(in_offs[0], self.nodes[node.parents[0]])
+            torch.addmm(pr.views["fc_b"], a.float(), pr.views["fc_w"].t(),
+                        out=self._view(out_off, node))
+        elif op == "fc_bwd":
+            logits = self._view(in_offs[0], self.nodes[node.parents[0]])
+            a = self._view(in_offs[1], self.nodes[node.parents[1]])
+            Nb, ncls = logits.shape
+            K.softmax_xent(_ptr(logits), _ptr(self.y_dev), _ptr(self.loss), _ptr(self.dlogits),
+                           _ptr(self.row_loss), Nb, ncls, st)
+            torch.mm(self.dlogits.t(), a.float(), out=pr.gviews["fc_w"])
+            torch.sum(self.dlogits, 0, out=pr.gviews["fc_b"])
+            self._view(out_off, node).copy_(self.dlogits @ pr.views["fc_w"])
+        elif op == "bn_add_relu_bwd":
+            bn = node.attrs["bn"]
+            M = int(np.prod(node.shape[:-1]))
+            C = node.shape[-1]
+            pool_hw = int(node.shape[1] * node.shape[2]) if node.attrs.get("from_pool") else 0
+            K.bn_backward(ins[0], pool_hw, ins[1], ins[2], out, M, C, _ptr(pr.bn_mean[bn]),
+                          _ptr(pr.bn_invstd[bn]), _ptr(pr.views["bn_g:" + bn]),
+                          _ptr(pr.gviews["bn_g:" + bn]), _ptr(pr.gviews["bn_b:" + bn]),
+                          _ptr(self.bn_ws), st)
+        elif op == "conv_bn_relu_bwd":
+            conv = node.attrs["conv"]
+            bn = node.attrs["bn"]
+            dC = self._view(in_offs[0], self.nodes[node.parents[0]])
+            R = self._view(in_offs[1], self.nodes[node.parents[1]])
+            dR = self._conv_bwd(conv, dC, R, need_dx=True)
+            M = int(np.prod(node.shape[:-1]))
+            C = node.shape[-1]
+            K.bn_backward(_ptr(dR), 0, ins[1], ins[2], out, M, C, _ptr(pr.bn_mean[bn]),
+                          _ptr(pr.bn_invstd[bn]), _ptr(pr.views["bn_g:" + bn]),
+                          _ptr(pr.gviews["bn_g:" + bn]), _ptr(pr.gviews["bn_b:" + bn]),
+                          _ptr(self.bn_ws), st)
+        elif op == "conv_shortcut_bwd":
+            dC1 = self._view(in_offs[0], self.nodes[node.parents[0]])
+            X = self._view(in_offs[1], self.nodes[node.parents[1]])
+            dX = self._conv_bwd(node.attrs["conv"], dC1, X, need_dx=True)
+            M = int(np.prod(node.shape[:-1]))
+            C = node.shape[-1]
+            if "conv_short" in node.attrs:
+                dCD = self._view(in_offs[2], self.nodes[node.parents[2]])
+                dXs = self._conv_bwd(node.attrs["conv_short"], dCD, X, need_dx=True)
+                K.add_grad(_ptr(dX), _ptr(dXs), 0, None, out, M, C, st)
+            else:
+                up = self.nodes[node.parents[2]]
+                pool_hw = int(node.shape[1] * node.shape[2]) if node.attrs.get("from_pool") else 0
+                del up
+                K.add_grad(_ptr(dX), ins[2], pool_hw, ins[3], out, M, C, st)
+        elif op == "maxpool_bwd":
+            src = self.nodes[node.parents[1]]
+            Nb, H, W, C = src.shape
+            K.maxpool_bwd(ins[0], ins[1], out, Nb, H, W, C, st)
+        elif op == "bn_relu_bwd":
+            bn = node.attrs["bn"]
+            M = int(np.prod(node.shape[:-1]))
+            C = node.shape[-1]
+            K.bn_backward(ins[0], 0, ins[1], ins[2], out, M, C, _ptr(pr.bn_mean[bn]),
+                          _ptr(pr.bn_invstd[bn]), _ptr(pr.views["bn_g:" + bn]),
+                          _ptr(pr.gviews["bn_g:" + bn]), _ptr(pr.gviews["bn_b:" + bn]),
+                          _ptr(self.bn_ws), st)
+        elif op == "conv_wgrad":
+            conv = node.attrs["conv"]
+            dC = self._view(in_offs[0], self.nodes[node.parents[0]])
+            X = self._view(in_offs[1], self.nodes[node.parents[1]])
+            self._conv_bwd(conv, dC, X, need_dx=False)
+            self._view(out_off, node).copy_(pr.gviews["conv:" + conv])
+        else:
+            raise RuntimeError(f"no kernel for op {op!r} (node {node.name})")
+
+    def _conv_bwd(self, name: str, dY: torch.Tensor, X: torch.Tensor, need_dx: bool):
+        """dgrad/wgrad through cuDNN (channels_last views of arena memory);
+        the weight gradient lands in the fp32 grad buffer (KRSC)."""
+        cs = self.g.convs[name]
+        w = self.params.wbf[name].permute(0, 3, 1, 2)
+        gi, gw, _ = torch.ops.aten.convolution_backward(
+            dY.permute(0, 3, 1, 2), X.permute(0, 3, 1, 2), w, None, [cs.stride] * 2,
+            [cs.pad] * 2, [1, 1], False, [0, 0], 1, [need_dx, True, False])
+        self.params.gviews["conv:" + name].copy_(gw.permute(0, 2, 3, 1))
+        if need_dx:
+            gi = gi.permute(0, 2, 3, 1)
+            if not gi.is_contiguous():
+                gi = gi.contiguous()
+            return gi
+        return None
+
+    # -------------------------------------------------------- program
+    def run_program(self, timing: dict | None = None, probe: dict | None = None):
+        """Issue one training step: the lowered action program on the three
+        streams, then the optimizer.  Returns nothing; loss stays on device."""
+        prog = self.program
+        st = self.stream.cuda_stream
+        streams = {P.STREAM_COMPUTE: st, P.STREAM_D2H: self.swap.d2h_stream,
+                   P.STREAM_H2D: self.swap.h2d_stream}
+        nodes = self.nodes
+        inputs = self._inputs
+        ev = self.events
+        base = self._base
+        for a in prog.actions:
+            op = int(a["op"])
+            if op == P.ACT_WAIT:
+                ev.wait(int(a["event"]), streams[int(a["stream"])])
+            elif op == P.ACT_RECORD:
+                ev.record(int(a["event"]), streams[int(a["stream"])])
+            elif op in (P.ACT_COMPUTE, P.ACT_RECOMPUTE):
+                node = nodes[int(a["node"])]
+                at, n_in = int(a["inputs_at"]), int(a["n_inputs"])
+                if timing is not None:
+                    e0 = torch.cuda.Event(enable_timing=True)
+                    e1 = torch.cuda.Event(enable_timing=True)
+                    e0.record(self.stream)
+                self._run_node(node, int(a["offset"]), [int(x) for x in inputs[at:at + n_in]],
+                               op == P.ACT_RECOMPUTE, st)
+                if probe is not None and node.id in probe:
+                    probe[node.id] = self._view(int(a["offset"]), node).clone()
+                if timing is not None:
+                    e1.record(self.stream)
+                    timing.setdefault(node.id, []).append((e0, e1, op == P.ACT_RECOMPUTE))
+            elif op == P.ACT_OFFLOAD:
+                self.swap.offload(base + int(a["offset"]), int(a["host_offset"]), int(a["bytes"]))
+            elif op == P.ACT_RELOAD:
+                self.swap.reload(base + int(a["offset"]), int(a["host_offset"]), int(a["bytes"]))
+        # join the copy streams that carried work back into the compute stream
+        used = set(int(x) for x in prog.actions["stream"][np.isin(prog.actions["op"], (P.ACT_OFFLOAD, P.ACT_RELOAD))])
+        for sid in sorted(used):
+            e = torch.cuda.Event()
+            e.record(torch.cuda.ExternalStream(streams[sid]))
+            self.stream.wait_event(e)
+        self.params.sgd_step(self.lr)
+
+    def capture(self):
+        """Capture one full step (program + optimizer) as a CUDA graph."""
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.stream(self.stream):
+            with torch.cuda.graph(g, stream=self.stream):
+                self.run_program()
+        self.graph = g
+        torch.cuda.synchronize()
+
+    def step_device(self):
+        """One step with inputs already resident (x_dev, y_dev)."""
+        if self.graph is not None:
+            with torch.cuda.stream(self.stream):
+                self.graph.replay()
+        else:
+            with torch.cuda.stream(self.stream):
+                self.run_program()
+
+    def step(self, x_host: torch.Tensor, y_host: torch.Tensor) -> float:
+        """One step through the public API with HOST buffers: H2D of the batch,
+        the step, D2H of the loss."""
+        with torch.cuda.stream(self.stream):
+            self.x_dev.copy_(x_host, non_blocking=True)
+            self.y_dev.copy_(y_host, non_blocking=True)
+        self.step_device()
+        with torch.cuda.stream(self.stream):
+            loss = self.loss.to("cpu", non_blocking=False)
+        return float(loss.item())
+
+    # ----------------------------------------------------- cost model
+    def measure_costs(self, iters: int = 3, link: bool = True):
+        """GPU-resident cost model: time every node's op on device (CUDA events
+        around each action of the no-eviction program, median of `iters`
+        steps), quantise to whole microseconds (>= 1) and write them into the
+        trace; probe the pinned host link for the swap cost."""
+        self.plan(None)
+        lr = self.lr
+        self.lr = 0.0  # cost probing must not move the weights
+        samples: dict[int, list] = {}
+        with torch.cuda.stream(self.stream):
+            for _ in range(iters + 1):
+                timing = {}
+                self.run_program(timing)
+                torch.cuda.synchronize()
+                for nid, lst in timing.items():
+                    samples.setdefault(nid, []).append(lst[0][0].elapsed_time(lst[0][1]))
+        self.lr = lr
+        table = {}
+        for n in self.nodes:
+            ms = sorted(samples[n.id][1:]) if len(samples[n.id]) > 1 else samples[n.id]
+            us = ms[len(ms) // 2] * 1e3
+            n.cost_us = max(1, int(math.ceil(us)))
+            table[n.name] = n.cost_us
+        if link:
+            h2d, d2h, _ = K.probe_link()
+            self.link_gbs = min(h2d, d2h)
+        self.cost_table = table
+        return table
+
+
+def apply_anchors(g: G.Graph, anchors: str):
+    """Author-specified pins: tensors marked both evict_pinned
+    and offload_pinned are never release candidates (ref policy.cpp:111-114)
+    and anchor recompute closures.  'out+narrow' anchors every block output and
+    the width-channel conv outputs (conv1/conv2 of each bottleneck and the
+    stem conv); 'out' anchors block outputs only; 'none' leaves every
+    computable activation to the Filter/Director."""
+    for n in g.nodes:
+        if n.phase != "F" or n.uncomputable:
+            continue
+        leaf = n.name.split(".")[-1]
+        pin = False
+        if anchors in ("out", "out+narrow") and leaf == "out":
+            pin = True
+        if anchors == "out+narrow" and n.op == "conv" and leaf in ("conv1", "conv2"):
+            pin = True
+        if pin:
+            n.evict_pinned = n.offload_pinned = True
