@@ -41,6 +41,14 @@ for _n, (_r, _a) in _SIGS.items():
     _f.restype = _r
     _f.argtypes = _a
 
+# Number of OUR kernel launches issued through this module (the bench reports
+# launches per step from the delta across one captured step).
+LAUNCHES = [0]
+
+
+def _count(n: int):
+    LAUNCHES[0] += n
+
 
 class Conv:
     """tcgen05 implicit-GEMM convolution with a cached weight TMA descriptor."""
@@ -56,6 +64,7 @@ class Conv:
 
     def __call__(self, x_ptr: int, y_ptr: int, stream: int):
         check(lib.delta_conv_forward(self._h, x_ptr, y_ptr, stream))
+        _count(1)
 
     def __del__(self):
         if getattr(self, "_h", None) and lib is not None:
@@ -69,37 +78,45 @@ def bn_workspace_floats(M: int, C_: int) -> int:
 
 def bn_stats(x, M, C_, ws, mean, invstd, eps, run_mean, run_var, momentum, stream):
     check(lib.delta_bn_stats(x, M, C_, ws, mean, invstd, eps, run_mean, run_var, momentum, stream))
+    _count(2)
 
 
 def bn_apply(mode, x, res, y, M, C_, mean, invstd, gamma, beta, mean2=None, invstd2=None,
              gamma2=None, beta2=None, stream=None):
     check(lib.delta_bn_apply(mode, x, res, y, M, C_, mean, invstd, gamma, beta, mean2, invstd2,
                              gamma2, beta2, stream))
+    _count(1)
 
 
 def bn_backward(up, pool_hw, mask, x, dx, M, C_, mean, invstd, gamma, dgamma, dbeta, ws, stream):
     check(lib.delta_bn_backward(up, pool_hw, mask, x, dx, M, C_, mean, invstd, gamma, dgamma,
                                 dbeta, ws, stream))
+    _count(3)
 
 
 def add_grad(a, up, pool_hw, mask, out, M, C_, stream):
     check(lib.delta_add_grad(a, up, pool_hw, mask, out, M, C_, stream))
+    _count(1)
 
 
 def maxpool_fwd(x, y, N, H, W, C_, stream):
     check(lib.delta_maxpool3x3s2_fwd(x, y, N, H, W, C_, stream))
+    _count(1)
 
 
 def maxpool_bwd(dy, x, dx, N, H, W, C_, stream):
     check(lib.delta_maxpool3x3s2_bwd(dy, x, dx, N, H, W, C_, stream))
+    _count(1)
 
 
 def avgpool_fwd(x, y, N, HW, C_, stream):
     check(lib.delta_avgpool_fwd(x, y, N, HW, C_, stream))
+    _count(1)
 
 
 def softmax_xent(logits, labels, loss, dlogits, row_ws, N, K, stream):
     check(lib.delta_softmax_xent(logits, labels, loss, dlogits, row_ws, N, K, stream))
+    _count(2)
 
 
 class Swap:

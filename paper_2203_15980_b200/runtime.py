@@ -161,6 +161,7 @@ class DeltaRuntime:
         self.graph = None
         self.cost_table = None
         self.link_gbs = None
+        self.dp = None  # torch.distributed group when running data parallel
 
     # ------------------------------------------------------------ setup
     def _build_convs(self):
@@ -371,8 +372,13 @@ class DeltaRuntime:
         inputs = self._inputs
         ev = self.events
         base = self._base
+        n_timed = 0
         for a in prog.actions:
             op = int(a["op"])
+            if timing is not None and op in (P.ACT_COMPUTE, P.ACT_RECOMPUTE) and n_timed % 24 == 0:
+                # keep the GPU busy while the host queues the next actions, so
+                # the event pairs time device execution, not launch latency
+                torch.cuda._sleep(int(3e7))
             if op == P.ACT_WAIT:
                 ev.wait(int(a["event"]), streams[int(a["stream"])])
             elif op == P.ACT_RECORD:
@@ -391,6 +397,7 @@ class DeltaRuntime:
                 if timing is not None:
                     e1.record(self.stream)
                     timing.setdefault(node.id, []).append((e0, e1, op == P.ACT_RECOMPUTE))
+                    n_timed += 1
             elif op == P.ACT_OFFLOAD:
                 self.swap.offload(base + int(a["offset"]), int(a["host_offset"]), int(a["bytes"]))
             elif op == P.ACT_RELOAD:
@@ -401,6 +408,11 @@ class DeltaRuntime:
             e = torch.cuda.Event()
             e.record(torch.cuda.ExternalStream(streams[sid]))
             self.stream.wait_event(e)
+        if self.dp is not None:
+            # data parallel: one DELTA instance per GPU, gradients averaged
+            # with NCCL over NVLink (one flat bucket, on the compute stream)
+            torch.distributed.all_reduce(self.params.grad, op=torch.distributed.ReduceOp.AVG,
+                                         group=self.dp)
         self.params.sgd_step(self.lr)
 
     def capture(self):
