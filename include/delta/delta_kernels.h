@@ -58,8 +58,10 @@ delta_status delta_add_grad(const void* a, const void* up, int32_t pool_hw, cons
 /* ---- pooling / head ---- */
 delta_status delta_maxpool3x3s2_fwd(const void* x, void* y, int32_t N, int32_t H, int32_t W,
                                     int32_t C, void* stream);
+/* `ws`: delta_maxpool_workspace_bytes() of scratch (argmax bytes) */
+int64_t delta_maxpool_workspace_bytes(int32_t N, int32_t H, int32_t W, int32_t C);
 delta_status delta_maxpool3x3s2_bwd(const void* dy, const void* x, void* dx, int32_t N,
-                                    int32_t H, int32_t W, int32_t C, void* stream);
+                                    int32_t H, int32_t W, int32_t C, void* ws, void* stream);
 delta_status delta_avgpool_fwd(const void* x, void* y, int32_t N, int32_t HW, int32_t C,
                                void* stream);
 delta_status delta_softmax_xent(const float* logits, const int64_t* labels, float* loss,

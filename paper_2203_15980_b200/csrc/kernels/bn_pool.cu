@@ -21,8 +21,19 @@ using bf16 = __nv_bfloat16;
 
 namespace {
 
-constexpr int CHUNK = 512;  // rows per reduction partial
 constexpr int SLICE = 64;   // channels per reduction block
+
+// Rows per reduction partial: enough partials to fill ~4 waves of 148 SMs,
+// few enough that the fixed-order merge stays short.  A multiple of 32.
+int64_t chunk_rows(int64_t M, int C) {
+  const int64_t slices = C / SLICE;
+  const int64_t target_ctas = 148 * 4;
+  int64_t chunks = target_ctas / (slices > 0 ? slices : 1);
+  if (chunks < 1) chunks = 1;
+  int64_t rows = (M + chunks - 1) / chunks;
+  rows = (rows + 31) / 32 * 32;
+  return rows < 256 ? 256 : rows;
+}
 
 __device__ __forceinline__ uint4 ld_stream(const void* p) {
   uint4 r;
@@ -67,11 +78,12 @@ __device__ __forceinline__ void merge(float& n, float& mu, float& m2, float nb, 
 
 // ---------------------------------------------------------------- BN stats
 __global__ void __launch_bounds__(256) k_bn_stats_partial(const bf16* __restrict__ x, int64_t M,
-                                                          int C, float2* __restrict__ ws) {
+                                                          int C, int64_t chunk,
+                                                          float2* __restrict__ ws) {
   const int tx = threadIdx.x & 7, ty = threadIdx.x >> 3;
   const int c0 = blockIdx.x * SLICE + tx * 8;
-  const int64_t r0 = int64_t(blockIdx.y) * CHUNK;
-  const int64_t r1 = min(M, r0 + CHUNK);
+  const int64_t r0 = int64_t(blockIdx.y) * chunk;
+  const int64_t r1 = min(M, r0 + chunk);
   float s[8] = {0}, q[8] = {0};
 #pragma unroll 4
   for (int64_t r = r0 + ty; r < r1; r += 32) {
@@ -104,7 +116,7 @@ __global__ void __launch_bounds__(256) k_bn_stats_partial(const bf16* __restrict
 }
 
 __global__ void __launch_bounds__(256) k_bn_stats_final(const float2* __restrict__ ws, int chunks,
-                                                        int64_t M, int C, float* mean,
+                                                        int64_t chunk, int64_t M, int C, float* mean,
                                                         float* invstd, float eps, float* rm,
                                                         float* rv, float mom) {
   const int cl = threadIdx.x >> 3, lane = threadIdx.x & 7;
@@ -112,7 +124,7 @@ __global__ void __launch_bounds__(256) k_bn_stats_final(const float2* __restrict
   float n = 0.f, mu = 0.f, m2 = 0.f;
   if (c < C) {
     for (int k = lane; k < chunks; k += 8) {
-      const float nb = float(k == chunks - 1 ? M - int64_t(k) * CHUNK : CHUNK);
+      const float nb = float(k == chunks - 1 ? M - int64_t(k) * chunk : chunk);
       const float2 p = ws[int64_t(k) * C + c];
       merge(n, mu, m2, nb, p.x, p.y);
     }
@@ -136,36 +148,41 @@ __global__ void __launch_bounds__(256) k_bn_stats_final(const float2* __restrict
 }
 
 // ---------------------------------------------------------------- BN apply
+// blockDim (256) is a multiple of C/8 for every C <= 2048, so with a grid
+// stride that is a multiple of the block, each thread always touches the SAME
+// 8 channels: their scale/shift live in registers, not shared memory.
 template <int MODE>
 __global__ void __launch_bounds__(256)
     k_bn_apply(const bf16* __restrict__ x, const bf16* __restrict__ res, bf16* __restrict__ y,
-               int64_t vecs, int cmask, int C, const float* mean, const float* invstd,
-               const float* gamma, const float* beta, const float* mean2, const float* invstd2,
-               const float* gamma2, const float* beta2) {
-  extern __shared__ float sp[];  // scale, shift [, scale2, shift2]
-  for (int c = threadIdx.x; c < C; c += blockDim.x) {
-    const float sc = invstd[c] * gamma[c];
-    sp[c] = sc;
-    sp[C + c] = beta[c] - mean[c] * sc;
+               int64_t vecs, int cmask, const float* __restrict__ mean,
+               const float* __restrict__ invstd, const float* __restrict__ gamma,
+               const float* __restrict__ beta, const float* __restrict__ mean2,
+               const float* __restrict__ invstd2, const float* __restrict__ gamma2,
+               const float* __restrict__ beta2) {
+  const int64_t first = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int c0 = int(first * 8) & cmask;
+  float sc[8], sh[8], sc2[8], sh2[8];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    sc[j] = invstd[c0 + j] * gamma[c0 + j];
+    sh[j] = beta[c0 + j] - mean[c0 + j] * sc[j];
     if (MODE == 2) {
-      const float sc2 = invstd2[c] * gamma2[c];
-      sp[2 * C + c] = sc2;
-      sp[3 * C + c] = beta2[c] - mean2[c] * sc2;
+      sc2[j] = invstd2[c0 + j] * gamma2[c0 + j];
+      sh2[j] = beta2[c0 + j] - mean2[c0 + j] * sc2[j];
     }
   }
-  __syncthreads();
   const int64_t stride = int64_t(gridDim.x) * blockDim.x;
-  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < vecs; i += stride) {
-    const int c0 = int(i * 8) & cmask;
+#pragma unroll 2
+  for (int64_t i = first; i < vecs; i += stride) {
     float f[8];
     unpack8(ld_stream(x + i * 8), f);
     float r[8];
     if (MODE >= 1) unpack8(ld_stream(res + i * 8), r);
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
-      float v = fmaf(f[j], sp[c0 + j], sp[C + c0 + j]);
+      float v = fmaf(f[j], sc[j], sh[j]);
       if (MODE == 1) v += r[j];
-      if (MODE == 2) v += fmaf(r[j], sp[2 * C + c0 + j], sp[3 * C + c0 + j]);
+      if (MODE == 2) v += fmaf(r[j], sc2[j], sh2[j]);
       f[j] = fmaxf(v, 0.f);
     }
     reinterpret_cast<uint4*>(y)[i] = pack8(f);
@@ -186,12 +203,12 @@ __device__ __forceinline__ void load_up(const bf16* up, int pool_hw, float inv_h
 
 __global__ void __launch_bounds__(256)
     k_bn_bwd_partial(const bf16* __restrict__ up, int pool_hw, const bf16* __restrict__ mask,
-                     const bf16* __restrict__ x, int64_t M, int C, const float* mean,
-                     const float* invstd, float2* __restrict__ ws) {
+                     const bf16* __restrict__ x, int64_t M, int C, int64_t chunk,
+                     const float* mean, const float* invstd, float2* __restrict__ ws) {
   const int tx = threadIdx.x & 7, ty = threadIdx.x >> 3;
   const int c0 = blockIdx.x * SLICE + tx * 8;
-  const int64_t r0 = int64_t(blockIdx.y) * CHUNK;
-  const int64_t r1 = min(M, r0 + CHUNK);
+  const int64_t r0 = int64_t(blockIdx.y) * chunk;
+  const int64_t r1 = min(M, r0 + chunk);
   const float inv_hw = pool_hw ? 1.f / float(pool_hw) : 1.f;
   float mu[8], is[8];
 #pragma unroll
@@ -258,22 +275,26 @@ __global__ void __launch_bounds__(256) k_bn_bwd_final(const float2* __restrict__
 __global__ void __launch_bounds__(256)
     k_bn_bwd_apply(const bf16* __restrict__ up, int pool_hw, const bf16* __restrict__ mask,
                    const bf16* __restrict__ x, bf16* __restrict__ dx, int64_t vecs, int cmask,
-                   int logC, int C, int64_t M, const float* mean, const float* invstd, const float* gamma,
-                   const float* dgamma, const float* dbeta) {
-  extern __shared__ float sp[];  // a, b, d, mean, invstd
+                   int logC, int64_t M, const float* __restrict__ mean,
+                   const float* __restrict__ invstd, const float* __restrict__ gamma,
+                   const float* __restrict__ dgamma, const float* __restrict__ dbeta) {
+  const int64_t first = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int c0 = int(first * 8) & cmask;
+  const int C = cmask + 1;
   const float invM = 1.f / float(M);
-  for (int c = threadIdx.x; c < C; c += blockDim.x) {
-    sp[c] = gamma[c] * invstd[c];
-    sp[C + c] = dbeta[c] * invM;
-    sp[2 * C + c] = dgamma[c] * invM;
-    sp[3 * C + c] = mean[c];
-    sp[4 * C + c] = invstd[c];
+  float ka[8], kb[8], kd[8], mu[8], is[8];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    is[j] = invstd[c0 + j];
+    mu[j] = mean[c0 + j];
+    ka[j] = gamma[c0 + j] * is[j];
+    kb[j] = dbeta[c0 + j] * invM;
+    kd[j] = dgamma[c0 + j] * invM;
   }
-  __syncthreads();
   const float inv_hw = pool_hw ? 1.f / float(pool_hw) : 1.f;
   const int64_t stride = int64_t(gridDim.x) * blockDim.x;
-  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < vecs; i += stride) {
-    const int c0 = int(i * 8) & cmask;
+#pragma unroll 2
+  for (int64_t i = first; i < vecs; i += stride) {
     const int64_t row = (i * 8) >> logC;
     float g[8], m[8], xv[8];
     load_up(up, pool_hw, inv_hw, row, c0, C, g);
@@ -281,10 +302,9 @@ __global__ void __launch_bounds__(256)
     unpack8(ld_stream(x + i * 8), xv);
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
-      const int c = c0 + j;
       const float gj = m[j] > 0.f ? g[j] : 0.f;
-      const float xh = (xv[j] - sp[3 * C + c]) * sp[4 * C + c];
-      g[j] = sp[c] * (gj - sp[C + c] - xh * sp[2 * C + c]);
+      const float xh = (xv[j] - mu[j]) * is[j];
+      g[j] = ka[j] * (gj - kb[j] - xh * kd[j]);
     }
     reinterpret_cast<uint4*>(dx)[i] = pack8(g);
   }
@@ -349,11 +369,53 @@ __global__ void __launch_bounds__(256) k_maxpool_fwd(const bf16* __restrict__ x,
   }
 }
 
-// Gather form: each input pixel collects the gradient of every (<= 4) output
-// window whose first-in-scan-order argmax it is.  No atomics.
+// Backward in two deterministic passes (no atomics):
+//   1. per output window, the first-in-scan-order argmax (0..8) of each
+//      channel -> one byte per output element (transient workspace);
+//   2. per input pixel, sum the gradient of the <= 4 windows whose argmax it is.
 __global__ void __launch_bounds__(256)
-    k_maxpool_bwd(const bf16* __restrict__ dy, const bf16* __restrict__ x, bf16* __restrict__ dx,
-                  int N, int H, int W, int C, int P, int Q) {
+    k_maxpool_argmax(const bf16* __restrict__ x, uint8_t* __restrict__ idx, int N, int H, int W,
+                     int C, int P, int Q) {
+  const int cg = C / 8;
+  const int64_t total = int64_t(N) * P * Q * cg;
+  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < total; i += stride) {
+    const int c0 = int(i % cg) * 8;
+    int64_t t = i / cg;
+    const int q = int(t % Q);
+    t /= Q;
+    const int p = int(t % P);
+    const int n = int(t / P);
+    float best[8];
+    uint32_t arg[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      best[j] = -INFINITY;
+      arg[j] = 0;
+    }
+#pragma unroll
+    for (int k = 0; k < 9; ++k) {
+      const int h = 2 * p - 1 + k / 3, w = 2 * q - 1 + k % 3;
+      if (h < 0 || h >= H || w < 0 || w >= W) continue;
+      float f[8];
+      unpack8(*reinterpret_cast<const uint4*>(x + ((int64_t(n) * H + h) * W + w) * C + c0), f);
+#pragma unroll
+      for (int j = 0; j < 8; ++j)
+        if (f[j] > best[j]) {
+          best[j] = f[j];
+          arg[j] = k;
+        }
+    }
+    uint2 packed;
+    packed.x = arg[0] | (arg[1] << 8) | (arg[2] << 16) | (arg[3] << 24);
+    packed.y = arg[4] | (arg[5] << 8) | (arg[6] << 16) | (arg[7] << 24);
+    reinterpret_cast<uint2*>(idx)[i] = packed;
+  }
+}
+
+__global__ void __launch_bounds__(256)
+    k_maxpool_bwd_gather(const bf16* __restrict__ dy, const uint8_t* __restrict__ idx,
+                         bf16* __restrict__ dx, int N, int H, int W, int C, int P, int Q) {
   const int cg = C / 8;
   const int64_t total = int64_t(N) * H * W * cg;
   const int64_t stride = int64_t(gridDim.x) * blockDim.x;
@@ -369,35 +431,16 @@ __global__ void __launch_bounds__(256)
     const int q_lo = w / 2, q_hi = min(Q - 1, (w + 1) / 2);
     for (int p = p_lo; p <= p_hi; ++p)
       for (int q = q_lo; q <= q_hi; ++q) {
-        float best[8];
-        int arg[8];
+        const uint32_t k = uint32_t((h - (2 * p - 1)) * 3 + (w - (2 * q - 1)));
+        const int64_t o = ((int64_t(n) * P + p) * Q + q) * C + c0;
+        const uint2 a = *reinterpret_cast<const uint2*>(idx + o);
+        float g[8];
+        unpack8(*reinterpret_cast<const uint4*>(dy + o), g);
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
-          best[j] = -INFINITY;
-          arg[j] = -1;
+          const uint32_t aj = ((j < 4 ? a.x : a.y) >> (8 * (j & 3))) & 0xFF;
+          if (aj == k) acc[j] += g[j];
         }
-        for (int dh = 0; dh < 3; ++dh) {
-          const int hh = 2 * p - 1 + dh;
-          if (hh < 0 || hh >= H) continue;
-          for (int dw = 0; dw < 3; ++dw) {
-            const int ww = 2 * q - 1 + dw;
-            if (ww < 0 || ww >= W) continue;
-            float f[8];
-            unpack8(*reinterpret_cast<const uint4*>(x + ((int64_t(n) * H + hh) * W + ww) * C + c0),
-                    f);
-#pragma unroll
-            for (int j = 0; j < 8; ++j)
-              if (f[j] > best[j]) {
-                best[j] = f[j];
-                arg[j] = hh * W + ww;
-              }
-          }
-        }
-        float g[8];
-        unpack8(*reinterpret_cast<const uint4*>(dy + ((int64_t(n) * P + p) * Q + q) * C + c0), g);
-#pragma unroll
-        for (int j = 0; j < 8; ++j)
-          if (arg[j] == h * W + w) acc[j] += g[j];
       }
     reinterpret_cast<uint4*>(dx)[i] = pack8(acc);
   }
@@ -471,16 +514,20 @@ __global__ void k_mean_rows(const float* row_loss, int N, float* loss) {
 
 }  // namespace
 
-int64_t bn_workspace_floats(int64_t M, int C) { return 2 * ((M + CHUNK - 1) / CHUNK) * C; }
+int64_t bn_workspace_floats(int64_t M, int C) {
+  const int64_t chunk = chunk_rows(M, C);
+  return 2 * ((M + chunk - 1) / chunk) * C;
+}
 
 cudaError_t bn_stats(const void* x, int64_t M, int C, float* ws, float* mean, float* invstd,
                      float eps, float* rm, float* rv, float mom, cudaStream_t st) {
   if (C % SLICE) return cudaErrorInvalidValue;
-  const int chunks = int((M + CHUNK - 1) / CHUNK);
+  const int64_t chunk = chunk_rows(M, C);
+  const int chunks = int((M + chunk - 1) / chunk);
   k_bn_stats_partial<<<dim3(C / SLICE, chunks), 256, 0, st>>>(static_cast<const bf16*>(x), M, C,
-                                                              reinterpret_cast<float2*>(ws));
-  k_bn_stats_final<<<(C + 31) / 32, 256, 0, st>>>(reinterpret_cast<const float2*>(ws), chunks, M,
-                                                  C, mean, invstd, eps, rm, rv, mom);
+                                                              chunk, reinterpret_cast<float2*>(ws));
+  k_bn_stats_final<<<(C + 31) / 32, 256, 0, st>>>(reinterpret_cast<const float2*>(ws), chunks,
+                                                  chunk, M, C, mean, invstd, eps, rm, rv, mom);
   return cudaGetLastError();
 }
 
@@ -488,25 +535,24 @@ cudaError_t bn_apply(int mode, const void* x, const void* res, void* y, int64_t 
                      const float* mean, const float* invstd, const float* gamma, const float* beta,
                      const float* mean2, const float* invstd2, const float* gamma2,
                      const float* beta2, cudaStream_t st) {
-  if (C & (C - 1)) return cudaErrorInvalidValue;
+  if ((C & (C - 1)) || C < 8 || C > 2048) return cudaErrorInvalidValue;
   const int64_t vecs = M * C / 8;
   const int grid = grid_for(vecs, 256);
-  const size_t smem = size_t(mode == 2 ? 4 : 2) * C * sizeof(float);
   auto X = static_cast<const bf16*>(x);
   auto R = static_cast<const bf16*>(res);
   auto Y = static_cast<bf16*>(y);
   switch (mode) {
     case 0:
-      k_bn_apply<0><<<grid, 256, smem, st>>>(X, R, Y, vecs, C - 1, C, mean, invstd, gamma, beta,
-                                             nullptr, nullptr, nullptr, nullptr);
+      k_bn_apply<0><<<grid, 256, 0, st>>>(X, R, Y, vecs, C - 1, mean, invstd, gamma, beta,
+                                          nullptr, nullptr, nullptr, nullptr);
       break;
     case 1:
-      k_bn_apply<1><<<grid, 256, smem, st>>>(X, R, Y, vecs, C - 1, C, mean, invstd, gamma, beta,
-                                             nullptr, nullptr, nullptr, nullptr);
+      k_bn_apply<1><<<grid, 256, 0, st>>>(X, R, Y, vecs, C - 1, mean, invstd, gamma, beta,
+                                          nullptr, nullptr, nullptr, nullptr);
       break;
     default:
-      k_bn_apply<2><<<grid, 256, smem, st>>>(X, R, Y, vecs, C - 1, C, mean, invstd, gamma, beta,
-                                             mean2, invstd2, gamma2, beta2);
+      k_bn_apply<2><<<grid, 256, 0, st>>>(X, R, Y, vecs, C - 1, mean, invstd, gamma, beta, mean2,
+                                          invstd2, gamma2, beta2);
   }
   return cudaGetLastError();
 }
@@ -515,19 +561,20 @@ cudaError_t bn_backward(const void* up, int pool_hw, const void* mask, const voi
                         int64_t M, int C, const float* mean, const float* invstd,
                         const float* gamma, float* dgamma, float* dbeta, float* ws,
                         cudaStream_t st) {
-  if (C % SLICE || (C & (C - 1))) return cudaErrorInvalidValue;
-  const int chunks = int((M + CHUNK - 1) / CHUNK);
+  if (C % SLICE || (C & (C - 1)) || C > 2048) return cudaErrorInvalidValue;
+  const int64_t chunk = chunk_rows(M, C);
+  const int chunks = int((M + chunk - 1) / chunk);
   auto U = static_cast<const bf16*>(up);
   auto Mk = static_cast<const bf16*>(mask);
   auto X = static_cast<const bf16*>(x);
-  k_bn_bwd_partial<<<dim3(C / SLICE, chunks), 256, 0, st>>>(U, pool_hw, Mk, X, M, C, mean,
+  k_bn_bwd_partial<<<dim3(C / SLICE, chunks), 256, 0, st>>>(U, pool_hw, Mk, X, M, C, chunk, mean,
                                                             invstd, reinterpret_cast<float2*>(ws));
   k_bn_bwd_final<<<(C + 31) / 32, 256, 0, st>>>(reinterpret_cast<const float2*>(ws), chunks, C,
                                                 dgamma, dbeta);
   const int64_t vecs = M * C / 8;
-  k_bn_bwd_apply<<<grid_for(vecs, 256), 256, 5 * C * sizeof(float), st>>>(
-      U, pool_hw, Mk, X, static_cast<bf16*>(dx), vecs, C - 1, __builtin_ctz(C), C, M, mean, invstd, gamma, dgamma,
-      dbeta);
+  k_bn_bwd_apply<<<grid_for(vecs, 256), 256, 0, st>>>(
+      U, pool_hw, Mk, X, static_cast<bf16*>(dx), vecs, C - 1, __builtin_ctz(C), M, mean, invstd,
+      gamma, dgamma, dbeta);
   return cudaGetLastError();
 }
 
@@ -549,13 +596,22 @@ cudaError_t maxpool3x3s2_fwd(const void* x, void* y, int N, int H, int W, int C,
   return cudaGetLastError();
 }
 
-cudaError_t maxpool3x3s2_bwd(const void* dy, const void* x, void* dx, int N, int H, int W, int C,
-                             cudaStream_t st) {
+int64_t maxpool_workspace_bytes(int N, int H, int W, int C) {
   const int P = (H + 2 - 3) / 2 + 1, Q = (W + 2 - 3) / 2 + 1;
+  return int64_t(N) * P * Q * C;
+}
+
+cudaError_t maxpool3x3s2_bwd(const void* dy, const void* x, void* dx, int N, int H, int W, int C,
+                             void* ws, cudaStream_t st) {
+  const int P = (H + 2 - 3) / 2 + 1, Q = (W + 2 - 3) / 2 + 1;
+  if (C % 8) return cudaErrorInvalidValue;
+  const int64_t outs = int64_t(N) * P * Q * (C / 8);
+  k_maxpool_argmax<<<grid_for(outs, 256), 256, 0, st>>>(static_cast<const bf16*>(x),
+                                                        static_cast<uint8_t*>(ws), N, H, W, C, P, Q);
   const int64_t total = int64_t(N) * H * W * (C / 8);
-  k_maxpool_bwd<<<grid_for(total, 256), 256, 0, st>>>(static_cast<const bf16*>(dy),
-                                                      static_cast<const bf16*>(x),
-                                                      static_cast<bf16*>(dx), N, H, W, C, P, Q);
+  k_maxpool_bwd_gather<<<grid_for(total, 256), 256, 0, st>>>(
+      static_cast<const bf16*>(dy), static_cast<const uint8_t*>(ws), static_cast<bf16*>(dx), N, H,
+      W, C, P, Q);
   return cudaGetLastError();
 }
 

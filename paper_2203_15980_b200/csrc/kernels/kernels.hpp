@@ -42,8 +42,9 @@ cudaError_t add_grad(const void* a, const void* up, int pool_hw, const void* mas
                      int64_t M, int C, cudaStream_t st);
 
 cudaError_t maxpool3x3s2_fwd(const void* x, void* y, int N, int H, int W, int C, cudaStream_t st);
+int64_t maxpool_workspace_bytes(int N, int H, int W, int C);
 cudaError_t maxpool3x3s2_bwd(const void* dy, const void* x, void* dx, int N, int H, int W, int C,
-                             cudaStream_t st);
+                             void* ws, cudaStream_t st);
 cudaError_t avgpool_fwd(const void* x, void* y, int N, int HW, int C, cudaStream_t st);
 
 // loss = mean_i -log softmax(logits_i)[label_i]; dlogits = (softmax - onehot) / N

@@ -115,9 +115,14 @@ delta_status delta_maxpool3x3s2_fwd(const void* x, void* y, int32_t N, int32_t H
   return cuda_status(delta_k::maxpool3x3s2_fwd(x, y, N, H, W, C, S(stream)), "maxpool_fwd");
 }
 
+int64_t delta_maxpool_workspace_bytes(int32_t N, int32_t H, int32_t W, int32_t C) {
+  return delta_k::maxpool_workspace_bytes(N, H, W, C);
+}
+
 delta_status delta_maxpool3x3s2_bwd(const void* dy, const void* x, void* dx, int32_t N, int32_t H,
-                                    int32_t W, int32_t C, void* stream) {
-  return cuda_status(delta_k::maxpool3x3s2_bwd(dy, x, dx, N, H, W, C, S(stream)), "maxpool_bwd");
+                                    int32_t W, int32_t C, void* ws, void* stream) {
+  return cuda_status(delta_k::maxpool3x3s2_bwd(dy, x, dx, N, H, W, C, ws, S(stream)),
+                     "maxpool_bwd");
 }
 
 delta_status delta_avgpool_fwd(const void* x, void* y, int32_t N, int32_t HW, int32_t C,

@@ -21,7 +21,8 @@ _SIGS = {
     "delta_bn_backward": (i32, [vp, i32, vp, vp, vp, i64, i32, vp, vp, vp, vp, vp, vp, vp]),
     "delta_add_grad": (i32, [vp, vp, i32, vp, vp, i64, i32, vp]),
     "delta_maxpool3x3s2_fwd": (i32, [vp, vp, i32, i32, i32, i32, vp]),
-    "delta_maxpool3x3s2_bwd": (i32, [vp, vp, vp, i32, i32, i32, i32, vp]),
+    "delta_maxpool_workspace_bytes": (i64, [i32, i32, i32, i32]),
+    "delta_maxpool3x3s2_bwd": (i32, [vp, vp, vp, i32, i32, i32, i32, vp, vp]),
     "delta_avgpool_fwd": (i32, [vp, vp, i32, i32, i32, vp]),
     "delta_softmax_xent": (i32, [vp, vp, vp, vp, vp, i32, i32, vp]),
     "delta_swap_create": (i32, [u64, P(vp)]),
@@ -104,9 +105,13 @@ def maxpool_fwd(x, y, N, H, W, C_, stream):
     _count(1)
 
 
-def maxpool_bwd(dy, x, dx, N, H, W, C_, stream):
-    check(lib.delta_maxpool3x3s2_bwd(dy, x, dx, N, H, W, C_, stream))
-    _count(1)
+def maxpool_workspace_bytes(N, H, W, C_) -> int:
+    return lib.delta_maxpool_workspace_bytes(N, H, W, C_)
+
+
+def maxpool_bwd(dy, x, dx, N, H, W, C_, ws, stream):
+    check(lib.delta_maxpool3x3s2_bwd(dy, x, dx, N, H, W, C_, ws, stream))
+    _count(2)
 
 
 def avgpool_fwd(x, y, N, HW, C_, stream):

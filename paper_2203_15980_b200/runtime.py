@@ -148,6 +148,9 @@ class DeltaRuntime:
                                      for n in self.nodes if len(n.shape) == 4 and n.shape[-1] % 64 == 0),
                                  dtype=torch.float32, device=self.device)
         del maxM, maxC
+        mp = next(n for n in self.nodes if n.op == "maxpool")
+        self.mp_ws = torch.empty(K.maxpool_workspace_bytes(*self.nodes[mp.parents[0]].shape),
+                                 dtype=torch.uint8, device=self.device)
         ncls = self.g.fc[1]
         self.loss = torch.zeros(1, dtype=torch.float32, device=self.device)
         self.dlogits = torch.empty(batch, ncls, dtype=torch.float32, device=self.device)
@@ -326,7 +329,7 @@ class DeltaRuntime:
         elif op == "maxpool_bwd":
             src = self.nodes[node.parents[1]]
             Nb, H, W, C = src.shape
-            K.maxpool_bwd(ins[0], ins[1], out, Nb, H, W, C, st)
+            K.maxpool_bwd(ins[0], ins[1], out, Nb, H, W, C, _ptr(self.mp_ws), st)
         elif op == "bn_relu_bwd":
             bn = node.attrs["bn"]
             M = int(np.prod(node.shape[:-1]))
@@ -411,8 +414,7 @@ class DeltaRuntime:
         if self.dp is not None:
             # data parallel: one DELTA instance per GPU, gradients averaged
             # with NCCL over NVLink (one flat bucket, on the compute stream)
-            torch.distributed.all_reduce(self.params.grad, op=torch.distributed.ReduceOp.AVG,
-                                         group=self.dp)
+            allreduce_mean(self.params.grad, self.dp)
         self.params.sgd_step(self.lr)
 
     def capture(self):
@@ -494,3 +496,28 @@ def apply_anchors(g: G.Graph, anchors: str):
             pin = True
         if pin:
             n.evict_pinned = n.offload_pinned = True
+
+
+# ------------------------------------------------------ data parallelism
+def allreduce_mean(t: torch.Tensor, group) -> None:
+    """Average `t` across the group in place (NCCL: one AVG all-reduce)."""
+    import torch.distributed as dist
+    if dist.get_backend(group) == "nccl":
+        dist.all_reduce(t, op=dist.ReduceOp.AVG, group=group)
+    else:
+        dist.all_reduce(t, op=dist.ReduceOp.SUM, group=group)
+        t.div_(dist.get_world_size(group))
+
+
+def agree_cost_table(g: G.Graph, link_gbs: float | None, group, device="cpu"):
+    """Make every rank plan from the same cost table: per-node
+    costs are max-reduced and the host-link bandwidth min-reduced, so the
+    DELTA plans — a pure function of (trace, config) — are identical."""
+    import torch.distributed as dist
+    v = torch.tensor([float(n.cost_us) for n in g.nodes] + [-(link_gbs or 0.0)],
+                     dtype=torch.float64, device=device)
+    dist.all_reduce(v, op=dist.ReduceOp.MAX, group=group)
+    for n, c in zip(g.nodes, v[:-1].tolist()):
+        n.cost_us = int(c)
+    link = -float(v[-1].item())
+    return link if link > 0 else None

@@ -40,3 +40,23 @@ for (H, C, Ko, R, s, p) in shapes:
     print(json.dumps(out[-1]), flush=True)
 h2d, d2h, dup = K.probe_link()
 print(json.dumps(dict(link_h2d_gbs=h2d, link_d2h_gbs=d2h, link_duplex_gbs=dup)))
+
+# ---- HBM-bound kernels at layer-1 sizes (bs 256, 56x56) ----
+M, C = N * 56 * 56, 256
+x = torch.randn(M, C, device="cuda").to(torch.bfloat16)
+r = torch.randn(M, C, device="cuda").to(torch.bfloat16)
+y = torch.empty_like(x)
+mean = torch.zeros(C, device="cuda"); inv = torch.ones(C, device="cuda")
+gam = torch.ones(C, device="cuda"); bet = torch.zeros(C, device="cuda")
+ws = torch.empty(K.bn_workspace_floats(M, C), device="cuda")
+dg = torch.empty(C, device="cuda"); db = torch.empty(C, device="cuda")
+nb = M * C * 2
+res = {}
+res["bn_stats"] = (timeit(lambda: K.bn_stats(x.data_ptr(), M, C, ws.data_ptr(), mean.data_ptr(), inv.data_ptr(), 1e-5, 0, 0, 0.1, st)), 1 * nb)
+res["bn_apply_relu"] = (timeit(lambda: K.bn_apply(0, x.data_ptr(), None, y.data_ptr(), M, C, mean.data_ptr(), inv.data_ptr(), gam.data_ptr(), bet.data_ptr(), stream=st)), 2 * nb)
+res["bn_add_relu"] = (timeit(lambda: K.bn_apply(1, x.data_ptr(), r.data_ptr(), y.data_ptr(), M, C, mean.data_ptr(), inv.data_ptr(), gam.data_ptr(), bet.data_ptr(), stream=st)), 3 * nb)
+res["bn_backward"] = (timeit(lambda: K.bn_backward(r.data_ptr(), 0, x.data_ptr(), x.data_ptr(), y.data_ptr(), M, C, mean.data_ptr(), inv.data_ptr(), gam.data_ptr(), dg.data_ptr(), db.data_ptr(), ws.data_ptr(), st)), 7 * nb)
+res["add_grad_mask"] = (timeit(lambda: K.add_grad(x.data_ptr(), r.data_ptr(), 0, x.data_ptr(), y.data_ptr(), M, C, st)), 4 * nb)
+res["torch_copy"] = (timeit(lambda: y.copy_(x)), 2 * nb)
+for k, (ms, b) in res.items():
+    print(json.dumps(dict(kernel=k, ms=round(ms, 4), gbs=round(b / ms / 1e6, 1))))

@@ -30,6 +30,12 @@ CONV_CASES = [
     (1, 7, 7, 512, 2048, 1, 1, 0),
     (3, 7, 7, 512, 512, 3, 1, 1),
     (256, 1, 1, 2048, 1000, 1, 1, 0),
+    # persistent loop: more tiles than SMs, several N tiles, both A paths
+    (8, 56, 56, 64, 64, 3, 1, 1),
+    (8, 56, 56, 256, 64, 1, 1, 0),
+    (16, 28, 28, 128, 512, 1, 1, 0),
+    (16, 28, 28, 256, 512, 1, 2, 0),
+    (9, 14, 14, 256, 256, 3, 1, 1),
 ]
 
 
@@ -185,7 +191,8 @@ def test_maxpool_fwd_bwd_match_torch():
     dy = torch.randn(N, 56, 56, C, device="cuda", generator=g).to(torch.bfloat16)
     yr.backward(dy.float().permute(0, 3, 1, 2))
     dx = torch.empty_like(x)
-    K.maxpool_bwd(dy.data_ptr(), x.data_ptr(), dx.data_ptr(), N, H, W, C, _stream())
+    ws = torch.empty(K.maxpool_workspace_bytes(N, H, W, C), dtype=torch.uint8, device="cuda")
+    K.maxpool_bwd(dy.data_ptr(), x.data_ptr(), dx.data_ptr(), N, H, W, C, ws.data_ptr(), _stream())
     torch.cuda.synchronize()
     ref = xf.grad.permute(0, 2, 3, 1)
     assert (dx.float() - ref).abs().max().item() <= 2e-2 * ref.abs().max().item()
