@@ -30,7 +30,10 @@ typedef struct delta_conv delta_conv;
 delta_status delta_conv_create(int32_t N, int32_t H, int32_t W, int32_t C, int32_t K,
                                int32_t R, int32_t S, int32_t stride, int32_t pad,
                                const void* weight, delta_conv** out);
-delta_status delta_conv_forward(const delta_conv* c, const void* x, void* y, void* stream);
+/* `stats` (nullable): [ceil(N*P*Q/128)][K] float2 (mean, M2) per 128-row tile
+ * of the bf16 outputs — BatchNorm statistics partials fused in the epilogue. */
+delta_status delta_conv_forward(const delta_conv* c, const void* x, void* y, float* stats,
+                                void* stream);
 delta_status delta_conv_geometry(const delta_conv* c, int32_t* P, int32_t* Q, int32_t* kdim,
                                  int32_t* tile_n);
 void delta_conv_destroy(delta_conv* c);
@@ -42,6 +45,11 @@ int64_t delta_bn_workspace_floats(int64_t M, int32_t C);
 delta_status delta_bn_stats(const void* x, int64_t M, int32_t C, float* ws, float* mean,
                             float* invstd, float eps, float* run_mean, float* run_var,
                             float momentum, void* stream);
+/* statistics from the conv epilogue's per-tile partials (rows_per_part = 128) */
+delta_status delta_bn_stats_from_partials(const float* partials, int64_t M, int32_t C,
+                                          int32_t rows_per_part, float* mean, float* invstd,
+                                          float eps, float* run_mean, float* run_var,
+                                          float momentum, void* stream);
 /* mode 0 relu(bn(x)), 1 relu(bn(x)+res), 2 relu(bn(x)+bn2(res)) */
 delta_status delta_bn_apply(int32_t mode, const void* x, const void* res, void* y, int64_t M,
                             int32_t C, const float* mean, const float* invstd,
@@ -52,8 +60,10 @@ delta_status delta_bn_backward(const void* up, int32_t pool_hw, const void* mask
                                void* dx, int64_t M, int32_t C, const float* mean,
                                const float* invstd, const float* gamma, float* dgamma,
                                float* dbeta, float* ws, void* stream);
-delta_status delta_add_grad(const void* a, const void* up, int32_t pool_hw, const void* mask,
-                            void* out, int64_t M, int32_t C, void* stream);
+/* out = (a + up*[up_mask>0]) * [out_mask>0]; null masks are not applied;
+ * pool_hw > 0: `up` is [N,C] broadcast over pool_hw pixels / pool_hw */
+delta_status delta_add_grad(const void* a, const void* up, int32_t pool_hw, const void* up_mask,
+                            const void* out_mask, void* out, int64_t M, int32_t C, void* stream);
 
 /* ---- pooling / head ---- */
 delta_status delta_maxpool3x3s2_fwd(const void* x, void* y, int32_t N, int32_t H, int32_t W,

@@ -115,28 +115,37 @@ __global__ void __launch_bounds__(256) k_bn_stats_partial(const bf16* __restrict
   }
 }
 
-__global__ void __launch_bounds__(256) k_bn_stats_final(const float2* __restrict__ ws, int chunks,
-                                                        int64_t chunk, int64_t M, int C, float* mean,
-                                                        float* invstd, float eps, float* rm,
-                                                        float* rv, float mom) {
-  const int cl = threadIdx.x >> 3, lane = threadIdx.x & 7;
-  const int c = blockIdx.x * 32 + cl;
-  float n = 0.f, mu = 0.f, m2 = 0.f;
-  if (c < C) {
-    for (int k = lane; k < chunks; k += 8) {
-      const float nb = float(k == chunks - 1 ? M - int64_t(k) * chunk : chunk);
-      const float2 p = ws[int64_t(k) * C + c];
-      merge(n, mu, m2, nb, p.x, p.y);
-    }
+// Merge per-chunk (mean, M2) partials of `rows_per` rows (last chunk shorter)
+// into the channel statistics.  Warp per channel, two passes without
+// dependent divisions: (1) total sum -> mean; (2) M2 = sum_i M2_i +
+// n_i (mean_i - mean)^2.  Lane-strided accumulation then a fixed xor
+// butterfly: deterministic.
+__device__ __forceinline__ float warp_sum(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+__global__ void __launch_bounds__(256)
+    k_bn_stats_merge(const float2* __restrict__ ws, int parts, int64_t rows_per, int64_t M, int C,
+                     float* mean, float* invstd, float eps, float* rm, float* rv, float mom) {
+  const int c = blockIdx.x * 8 + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (c >= C) return;
+  const float n_last = float(M - int64_t(parts - 1) * rows_per);
+  const float n_full = float(rows_per);
+  float s = 0.f;
+  for (int k = lane; k < parts; k += 32)
+    s = fmaf(k == parts - 1 ? n_last : n_full, ws[int64_t(k) * C + c].x, s);
+  const float mu = warp_sum(s) / float(M);
+  float m2 = 0.f;
+  for (int k = lane; k < parts; k += 32) {
+    const float2 p = ws[int64_t(k) * C + c];
+    const float d = p.x - mu;
+    m2 += fmaf(k == parts - 1 ? n_last : n_full, d * d, p.y);
   }
-  __shared__ float sn[256], smu[256], sm2[256];
-  sn[threadIdx.x] = n;
-  smu[threadIdx.x] = mu;
-  sm2[threadIdx.x] = m2;
-  __syncthreads();
-  if (lane == 0 && c < C) {
-    for (int j = 1; j < 8; ++j)
-      merge(n, mu, m2, sn[threadIdx.x + j], smu[threadIdx.x + j], sm2[threadIdx.x + j]);
+  m2 = warp_sum(m2);
+  if (lane == 0) {
     const float var = m2 / float(M);
     mean[c] = mu;
     invstd[c] = rsqrtf(var + eps);
@@ -221,7 +230,12 @@ __global__ void __launch_bounds__(256)
   for (int64_t r = r0 + ty; r < r1; r += 32) {
     float g[8], m[8], xv[8];
     load_up(up, pool_hw, inv_hw, r, c0, C, g);
-    unpack8(ld_stream(mask + r * C + c0), m);
+    if (mask) {
+      unpack8(ld_stream(mask + r * C + c0), m);
+    } else {
+#pragma unroll
+      for (int j = 0; j < 8; ++j) m[j] = 1.f;
+    }
     unpack8(ld_stream(x + r * C + c0), xv);
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
@@ -298,7 +312,12 @@ __global__ void __launch_bounds__(256)
     const int64_t row = (i * 8) >> logC;
     float g[8], m[8], xv[8];
     load_up(up, pool_hw, inv_hw, row, c0, C, g);
-    unpack8(ld_stream(mask + i * 8), m);
+    if (mask) {
+      unpack8(ld_stream(mask + i * 8), m);
+    } else {
+#pragma unroll
+      for (int j = 0; j < 8; ++j) m[j] = 1.f;
+    }
     unpack8(ld_stream(x + i * 8), xv);
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
@@ -310,10 +329,11 @@ __global__ void __launch_bounds__(256)
   }
 }
 
+// out = (a + g) [* (out_mask > 0)], g = up [* (up_mask > 0)], up full or pooled
 __global__ void __launch_bounds__(256)
     k_add_grad(const bf16* __restrict__ a, const bf16* __restrict__ up, int pool_hw,
-               const bf16* __restrict__ mask, bf16* __restrict__ out, int64_t vecs, int cmask,
-               int logC, int C) {
+               const bf16* __restrict__ up_mask, const bf16* __restrict__ out_mask,
+               bf16* __restrict__ out, int64_t vecs, int cmask, int logC, int C) {
   const float inv_hw = pool_hw ? 1.f / float(pool_hw) : 1.f;
   const int64_t stride = int64_t(gridDim.x) * blockDim.x;
   for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < vecs; i += stride) {
@@ -321,16 +341,20 @@ __global__ void __launch_bounds__(256)
     const int64_t row = (i * 8) >> logC;
     float fa[8], g[8];
     unpack8(ld_stream(a + i * 8), fa);
-    if (mask) {
+    load_up(up, pool_hw, inv_hw, row, c0, C, g);
+    if (up_mask) {
       float m[8];
-      load_up(up, pool_hw, inv_hw, row, c0, C, g);
-      unpack8(ld_stream(mask + i * 8), m);
+      unpack8(ld_stream(up_mask + i * 8), m);
 #pragma unroll
-      for (int j = 0; j < 8; ++j) fa[j] += m[j] > 0.f ? g[j] : 0.f;
-    } else {
-      unpack8(ld_stream(up + i * 8), g);
+      for (int j = 0; j < 8; ++j) g[j] = m[j] > 0.f ? g[j] : 0.f;
+    }
 #pragma unroll
-      for (int j = 0; j < 8; ++j) fa[j] += g[j];
+    for (int j = 0; j < 8; ++j) fa[j] += g[j];
+    if (out_mask) {
+      float m[8];
+      unpack8(ld_stream(out_mask + i * 8), m);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) fa[j] = m[j] > 0.f ? fa[j] : 0.f;
     }
     reinterpret_cast<uint4*>(out)[i] = pack8(fa);
   }
@@ -526,8 +550,18 @@ cudaError_t bn_stats(const void* x, int64_t M, int C, float* ws, float* mean, fl
   const int chunks = int((M + chunk - 1) / chunk);
   k_bn_stats_partial<<<dim3(C / SLICE, chunks), 256, 0, st>>>(static_cast<const bf16*>(x), M, C,
                                                               chunk, reinterpret_cast<float2*>(ws));
-  k_bn_stats_final<<<(C + 31) / 32, 256, 0, st>>>(reinterpret_cast<const float2*>(ws), chunks,
-                                                  chunk, M, C, mean, invstd, eps, rm, rv, mom);
+  k_bn_stats_merge<<<(C + 7) / 8, 256, 0, st>>>(reinterpret_cast<const float2*>(ws), chunks,
+                                                chunk, M, C, mean, invstd, eps, rm, rv, mom);
+  return cudaGetLastError();
+}
+
+cudaError_t bn_stats_from_partials(const float* partials, int64_t M, int C, int rows_per_part,
+                                   float* mean, float* invstd, float eps, float* rm, float* rv,
+                                   float mom, cudaStream_t st) {
+  const int parts = int((M + rows_per_part - 1) / rows_per_part);
+  k_bn_stats_merge<<<(C + 7) / 8, 256, 0, st>>>(reinterpret_cast<const float2*>(partials), parts,
+                                                rows_per_part, M, C, mean, invstd, eps, rm, rv,
+                                                mom);
   return cudaGetLastError();
 }
 
@@ -578,13 +612,14 @@ cudaError_t bn_backward(const void* up, int pool_hw, const void* mask, const voi
   return cudaGetLastError();
 }
 
-cudaError_t add_grad(const void* a, const void* up, int pool_hw, const void* mask, void* out,
-                     int64_t M, int C, cudaStream_t st) {
+cudaError_t add_grad(const void* a, const void* up, int pool_hw, const void* up_mask,
+                     const void* out_mask, void* out, int64_t M, int C, cudaStream_t st) {
   if (C & (C - 1)) return cudaErrorInvalidValue;
   const int64_t vecs = M * C / 8;
   k_add_grad<<<grid_for(vecs, 256), 256, 0, st>>>(
       static_cast<const bf16*>(a), static_cast<const bf16*>(up), pool_hw,
-      static_cast<const bf16*>(mask), static_cast<bf16*>(out), vecs, C - 1, __builtin_ctz(C), C);
+      static_cast<const bf16*>(up_mask), static_cast<const bf16*>(out_mask),
+      static_cast<bf16*>(out), vecs, C - 1, __builtin_ctz(C), C);
   return cudaGetLastError();
 }
 

@@ -54,6 +54,7 @@ struct ConvArgs {
   int taps;     // R*S
   int n_tiles;  // ceil(K / BN)
   int tiles;    // m_tiles * n_tiles
+  float2* stats;  // optional: per (m_tile, channel) (mean, M2) of the bf16 outputs
 };
 
 __device__ __forceinline__ uint8_t* align1024(uint8_t* p) {
@@ -76,7 +77,10 @@ __global__ void __launch_bounds__(kThreads, 1)
   const uint32_t sB = sA + STAGES * A_STAGE;
   // epilogue staging: 4 warps x 2 buffers x (32 rows x 64 B), 64B-swizzled
   const uint32_t sOut = sA + STAGES * (A_STAGE + B_STAGE);
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * (A_STAGE + B_STAGE) + 16384);
+  // BN-statistics scratch: per quarter-warp column (sum, sumsq), [4][BN] float2
+  float2* red = reinterpret_cast<float2*>(smem + STAGES * (A_STAGE + B_STAGE) + 16384);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * (A_STAGE + B_STAGE) + 16384 +
+                                               4 * BN * sizeof(float2));
   uint64_t* empty = full + STAGES;
   uint64_t* tfull = empty + STAGES;  // [2]
   uint64_t* tempty = tfull + 2;      // [2]
@@ -276,6 +280,42 @@ __global__ void __launch_bounds__(kThreads, 1)
           tma_store_2d(&ymap, buf, col, m0 + quarter * 32);
           bulk_commit();
         }
+        if (a.stats != nullptr) {
+          // column `lane` of this 32x32 block, from the staged bf16 values
+          // (exactly what BN will read back); rows past M are zeros.
+          const uint32_t cbyte = (uint32_t(lane) & 7u) * 2u;
+          const uint32_t c16 = uint32_t(lane) >> 3;
+          float sum = 0.f, sq = 0.f;
+#pragma unroll 8
+          for (int rr = 0; rr < 32; ++rr) {
+            uint16_t h;
+            asm volatile("ld.shared.u16 %0, [%1];"
+                         : "=h"(h)
+                         : "r"(buf + rr * 64 + ((c16 ^ ((rr >> 1) & 3)) << 4) + cbyte));
+            const float f = __bfloat162float(__ushort_as_bfloat16(h));
+            sum += f;
+            sq = fmaf(f, f, sq);
+          }
+          red[quarter * BN + j * 32 + lane] = make_float2(sum, sq);
+        }
+      }
+      if (a.stats != nullptr) {
+        // combine the four row quarters -> one (mean, M2) per channel per tile
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+        const int et = (warp - 4) * 32 + lane;
+        const int n_rows = min(BM, a.M - m0);
+        for (int c = et; c < BN; c += 128) {
+          float S = 0.f, Q = 0.f;
+#pragma unroll
+          for (int qq = 0; qq < 4; ++qq) {
+            S += red[qq * BN + c].x;
+            Q += red[qq * BN + c].y;
+          }
+          const float mu = S / float(n_rows);
+          if (n0 + c < a.K)
+            a.stats[size_t(m0 / BM) * a.K + n0 + c] = make_float2(mu, fmaxf(Q - S * mu, 0.f));
+        }
+        asm volatile("bar.sync 1, 128;" ::: "memory");
       }
       tc_fence_before();
       __syncwarp();
@@ -318,8 +358,8 @@ __global__ void __launch_bounds__(kThreads, 1)
 
 template <int BN, int STAGES>
 constexpr size_t conv_smem_bytes() {
-  return size_t(STAGES) * (BM * 128 + BN * 128) + 16384 /*epilogue staging*/ + 1024 /*align*/ +
-         256 /*barriers*/;
+  return size_t(STAGES) * (BM * 128 + BN * 128) + 16384 /*epilogue staging*/ +
+         4 * BN * 8 /*stats scratch*/ + 1024 /*align*/ + 256 /*barriers*/;
 }
 
 PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
@@ -417,7 +457,7 @@ int num_sms() {
 }
 
 template <int BN, int STAGES, int MODE>
-cudaError_t launch(const ConvPlan& cp, const void* x, void* y, cudaStream_t st) {
+cudaError_t launch(const ConvPlan& cp, const void* x, void* y, float* stats, cudaStream_t st) {
   auto kern = k_conv_fwd<BN, STAGES, MODE>;
   constexpr size_t smem = conv_smem_bytes<BN, STAGES>();
   static bool attr = false;
@@ -436,6 +476,7 @@ cudaError_t launch(const ConvPlan& cp, const void* x, void* y, cudaStream_t st) 
   a.taps = cp.R * cp.S;
   a.n_tiles = (cp.K + BN - 1) / BN;
   a.tiles = ((a.M + BM - 1) / BM) * a.n_tiles;
+  a.stats = reinterpret_cast<float2*>(stats);
   alignas(64) CUtensorMap amap;
   alignas(64) CUtensorMap ymap;
   if (MODE == MODE_TMA) {
@@ -468,26 +509,27 @@ int conv_plan_init(ConvPlan* cp, const void* w) {
              : 3;
 }
 
-cudaError_t conv_forward(const ConvPlan& cp, const void* x, void* y, cudaStream_t st) {
+cudaError_t conv_forward(const ConvPlan& cp, const void* x, void* y, float* stats,
+                         cudaStream_t st) {
   const bool stem = cp.C == 4;
   const bool tma_a = !stem && cp.R == 1 && cp.S == 1 && cp.stride == 1 && cp.pad == 0;
   const bool use_gather = gather_forced();
   switch (cp.bn) {
     case 64:
-      return stem ? launch<64, 8, MODE_STEM>(cp, x, y, st)
-             : tma_a ? launch<64, 8, MODE_TMA>(cp, x, y, st)
-             : use_gather ? launch<64, 8, MODE_GATHER>(cp, x, y, st)
-                          : launch<64, 8, MODE_IM2COL>(cp, x, y, st);
+      return stem ? launch<64, 8, MODE_STEM>(cp, x, y, stats, st)
+             : tma_a ? launch<64, 8, MODE_TMA>(cp, x, y, stats, st)
+             : use_gather ? launch<64, 8, MODE_GATHER>(cp, x, y, stats, st)
+                          : launch<64, 8, MODE_IM2COL>(cp, x, y, stats, st);
     case 128:
-      return stem ? launch<128, 6, MODE_STEM>(cp, x, y, st)
-             : tma_a ? launch<128, 6, MODE_TMA>(cp, x, y, st)
-             : use_gather ? launch<128, 6, MODE_GATHER>(cp, x, y, st)
-                          : launch<128, 6, MODE_IM2COL>(cp, x, y, st);
+      return stem ? launch<128, 6, MODE_STEM>(cp, x, y, stats, st)
+             : tma_a ? launch<128, 6, MODE_TMA>(cp, x, y, stats, st)
+             : use_gather ? launch<128, 6, MODE_GATHER>(cp, x, y, stats, st)
+                          : launch<128, 6, MODE_IM2COL>(cp, x, y, stats, st);
     default:
-      return stem ? launch<256, 4, MODE_STEM>(cp, x, y, st)
-             : tma_a ? launch<256, 4, MODE_TMA>(cp, x, y, st)
-             : use_gather ? launch<256, 4, MODE_GATHER>(cp, x, y, st)
-                          : launch<256, 4, MODE_IM2COL>(cp, x, y, st);
+      return stem ? launch<256, 4, MODE_STEM>(cp, x, y, stats, st)
+             : tma_a ? launch<256, 4, MODE_TMA>(cp, x, y, stats, st)
+             : use_gather ? launch<256, 4, MODE_GATHER>(cp, x, y, stats, st)
+                          : launch<256, 4, MODE_IM2COL>(cp, x, y, stats, st);
   }
 }
 

@@ -14,12 +14,20 @@ struct ConvPlan {
 };
 // 0 ok, 1 unsupported shape, 2 no driver entry point, 3 tensor-map encode failed
 int conv_plan_init(ConvPlan* cp, const void* w);
-cudaError_t conv_forward(const ConvPlan& cp, const void* x, void* y, cudaStream_t st);
+// stats (optional, nullptr = off): [ceil(M/128)][K] float2 (mean, M2) of the
+// bf16 outputs of each 128-row tile — the BN statistics partials.
+cudaError_t conv_forward(const ConvPlan& cp, const void* x, void* y, float* stats,
+                         cudaStream_t st);
 
 // ---- batch norm / elementwise / pooling (bn_pool.cu) ----
 int64_t bn_workspace_floats(int64_t M, int C);
 cudaError_t bn_stats(const void* x, int64_t M, int C, float* ws, float* mean, float* invstd,
                      float eps, float* run_mean, float* run_var, float momentum, cudaStream_t st);
+// Finish BN statistics from per-tile (mean, M2) partials of `rows_per_part`
+// rows each (the conv epilogue's), merged in a fixed order.
+cudaError_t bn_stats_from_partials(const float* partials, int64_t M, int C, int rows_per_part,
+                                   float* mean, float* invstd, float eps, float* run_mean,
+                                   float* run_var, float momentum, cudaStream_t st);
 
 // mode 0: y = relu(bn(x)); 1: y = relu(bn(x) + res); 2: y = relu(bn(x) + bn2(res))
 cudaError_t bn_apply(int mode, const void* x, const void* res, void* y, int64_t M, int C,
@@ -27,7 +35,7 @@ cudaError_t bn_apply(int mode, const void* x, const void* res, void* y, int64_t 
                      const float* mean2, const float* invstd2, const float* gamma2,
                      const float* beta2, cudaStream_t st);
 
-// BN(+ReLU) backward.  g = up * (mask > 0), where `up` is a full [M,C] bf16
+// BN(+ReLU) backward.  g = up * (mask > 0) (mask may be null: g = up), where `up` is a full [M,C] bf16
 // gradient (pool_hw == 0) or a pooled [N,C] bf16 gradient broadcast over
 // pool_hw pixels and scaled by 1/pool_hw.  Writes dx (bf16) and the
 // parameter gradients dgamma, dbeta (fp32).
@@ -36,10 +44,10 @@ cudaError_t bn_backward(const void* up, int pool_hw, const void* mask, const voi
                         const float* gamma, float* dgamma, float* dbeta, float* ws,
                         cudaStream_t st);
 
-// out = a + b (bf16)            when mask == nullptr
-// out = a + up * (mask > 0)     otherwise (up full or pooled as above)
-cudaError_t add_grad(const void* a, const void* up, int pool_hw, const void* mask, void* out,
-                     int64_t M, int C, cudaStream_t st);
+// out = (a + g) * [out_mask > 0], g = up * [up_mask > 0] (up full or pooled as
+// above; a null mask means no masking)
+cudaError_t add_grad(const void* a, const void* up, int pool_hw, const void* up_mask,
+                     const void* out_mask, void* out, int64_t M, int C, cudaStream_t st);
 
 cudaError_t maxpool3x3s2_fwd(const void* x, void* y, int N, int H, int W, int C, cudaStream_t st);
 int64_t maxpool_workspace_bytes(int N, int H, int W, int C);

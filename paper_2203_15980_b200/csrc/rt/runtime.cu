@@ -63,8 +63,9 @@ delta_status delta_conv_create(int32_t N, int32_t H, int32_t W, int32_t C, int32
   return DELTA_OK;
 }
 
-delta_status delta_conv_forward(const delta_conv* c, const void* x, void* y, void* stream) {
-  return cuda_status(delta_k::conv_forward(c->plan, x, y, S(stream)), "conv_forward");
+delta_status delta_conv_forward(const delta_conv* c, const void* x, void* y, float* stats,
+                                void* stream) {
+  return cuda_status(delta_k::conv_forward(c->plan, x, y, stats, S(stream)), "conv_forward");
 }
 
 delta_status delta_conv_geometry(const delta_conv* c, int32_t* P, int32_t* Q, int32_t* kdim,
@@ -87,6 +88,15 @@ delta_status delta_bn_stats(const void* x, int64_t M, int32_t C, float* ws, floa
                      "bn_stats");
 }
 
+delta_status delta_bn_stats_from_partials(const float* partials, int64_t M, int32_t C,
+                                          int32_t rows_per_part, float* mean, float* invstd,
+                                          float eps, float* rm, float* rv, float mom,
+                                          void* stream) {
+  return cuda_status(delta_k::bn_stats_from_partials(partials, M, C, rows_per_part, mean, invstd,
+                                                     eps, rm, rv, mom, S(stream)),
+                     "bn_stats_from_partials");
+}
+
 delta_status delta_bn_apply(int32_t mode, const void* x, const void* res, void* y, int64_t M,
                             int32_t C, const float* mean, const float* invstd, const float* gamma,
                             const float* beta, const float* mean2, const float* invstd2,
@@ -105,9 +115,10 @@ delta_status delta_bn_backward(const void* up, int32_t pool_hw, const void* mask
                      "bn_backward");
 }
 
-delta_status delta_add_grad(const void* a, const void* up, int32_t pool_hw, const void* mask,
-                            void* out, int64_t M, int32_t C, void* stream) {
-  return cuda_status(delta_k::add_grad(a, up, pool_hw, mask, out, M, C, S(stream)), "add_grad");
+delta_status delta_add_grad(const void* a, const void* up, int32_t pool_hw, const void* up_mask,
+                            const void* out_mask, void* out, int64_t M, int32_t C, void* stream) {
+  return cuda_status(delta_k::add_grad(a, up, pool_hw, up_mask, out_mask, out, M, C, S(stream)),
+                     "add_grad");
 }
 
 delta_status delta_maxpool3x3s2_fwd(const void* x, void* y, int32_t N, int32_t H, int32_t W,

@@ -154,33 +154,47 @@ def build_resnet(depth: int = 50, batch: int = 256, image: int = 224,
     # head: softmax-xent + fc backward -> dPooled
     d_pool = g.add("fc.bwd", "fc_bwd", pooled.shape, [logits.id, pooled.id], phase="B")
     d_pool.flops = 4.0 * N * cur.shape[-1] * num_classes
-    upstream = d_pool          # gradient w.r.t. the current block output
+    # Gradient nodes carry the gradient w.r.t. a block's PRE-activation (the
+    # ReLU mask of the block output is applied once, by the node that writes
+    # it), so BN3/downsample backward read no mask.  The exception is the
+    # pooled head gradient of the last block, masked where it is consumed.
+    upstream = d_pool
     upstream_is_pool = True
+    first = blocks[0][0]
     for (pre, X, C1, R1, C2, R2, C3, CD, O) in reversed(blocks):
-        extra = dict(from_pool=upstream_is_pool)
-        d_c3 = g.add(pre + ".bn3.bwd", "bn_add_relu_bwd", C3.shape,
-                     [upstream.id, O.id, C3.id], phase="B", attrs=dict(bn=pre + ".bn3", **extra))
-        d_c3.hbm_bytes = 4 * C3.nbytes
+        bn_parents = (lambda t: [upstream.id, O.id, t.id]) if upstream_is_pool else \
+            (lambda t: [upstream.id, t.id])
+        extra = dict(from_pool=upstream_is_pool, masked=upstream_is_pool)
+        d_c3 = g.add(pre + ".bn3.bwd", "bn_add_relu_bwd", C3.shape, bn_parents(C3), phase="B",
+                     attrs=dict(bn=pre + ".bn3", **extra))
+        d_c3.hbm_bytes = (6 if upstream_is_pool else 5) * C3.nbytes
         d_cd = None
         if CD is not None:
-            d_cd = g.add(pre + ".downsample.1.bwd", "bn_add_relu_bwd", CD.shape,
-                         [upstream.id, O.id, CD.id], phase="B",
-                         attrs=dict(bn=pre + ".downsample.1", **extra))
-            d_cd.hbm_bytes = 4 * CD.nbytes
+            d_cd = g.add(pre + ".downsample.1.bwd", "bn_add_relu_bwd", CD.shape, bn_parents(CD),
+                         phase="B", attrs=dict(bn=pre + ".downsample.1", **extra))
+            d_cd.hbm_bytes = (6 if upstream_is_pool else 5) * CD.nbytes
         d_c2 = g.add(pre + ".conv3.bwd", "conv_bn_relu_bwd", C2.shape,
                      [d_c3.id, R2.id, C2.id], phase="B",
                      attrs=dict(conv=pre + ".conv3", bn=pre + ".bn2"))
-        d_c2.flops = 2 * C3.flops if hasattr(C3, "flops") else 0
+        d_c2.flops = 2 * C3.flops
         d_c1 = g.add(pre + ".conv2.bwd", "conv_bn_relu_bwd", C1.shape,
                      [d_c2.id, R1.id, C1.id], phase="B",
                      attrs=dict(conv=pre + ".conv2", bn=pre + ".bn1"))
         d_c1.flops = 2 * C2.flops
+        # output: gradient of the previous block's pre-activation, i.e. masked
+        # by X > 0 (X is that block's ReLU output); the first block's input is
+        # the maxpool output, whose gradient is left unmasked.
+        mask_out = pre != first
         if CD is not None:
             parents = [d_c1.id, X.id, d_cd.id]
-            attrs = dict(conv=pre + ".conv1", conv_short=pre + ".downsample.0")
-        else:
+            attrs = dict(conv=pre + ".conv1", conv_short=pre + ".downsample.0",
+                         mask_out=mask_out)
+        elif upstream_is_pool:
             parents = [d_c1.id, X.id, upstream.id, O.id]
-            attrs = dict(conv=pre + ".conv1", from_pool=upstream_is_pool)
+            attrs = dict(conv=pre + ".conv1", from_pool=True, mask_out=mask_out)
+        else:
+            parents = [d_c1.id, X.id, upstream.id]
+            attrs = dict(conv=pre + ".conv1", from_pool=False, mask_out=mask_out)
         d_x = g.add(pre + ".conv1.bwd", "conv_shortcut_bwd", X.shape, parents, phase="B",
                     attrs=attrs)
         d_x.flops = 2 * C1.flops + (2 * CD.flops if CD is not None else 0)

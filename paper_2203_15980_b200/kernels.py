@@ -12,14 +12,15 @@ vp, i32, i64, u32, u64, f32 = C.c_void_p, C.c_int32, C.c_int64, C.c_uint32, C.c_
 P = C.POINTER
 _SIGS = {
     "delta_conv_create": (i32, [i32] * 9 + [vp, P(vp)]),
-    "delta_conv_forward": (i32, [vp, vp, vp, vp]),
+    "delta_conv_forward": (i32, [vp, vp, vp, vp, vp]),
+    "delta_bn_stats_from_partials": (i32, [vp, i64, i32, i32, vp, vp, f32, vp, vp, f32, vp]),
     "delta_conv_geometry": (i32, [vp, P(i32), P(i32), P(i32), P(i32)]),
     "delta_conv_destroy": (None, [vp]),
     "delta_bn_workspace_floats": (i64, [i64, i32]),
     "delta_bn_stats": (i32, [vp, i64, i32, vp, vp, vp, f32, vp, vp, f32, vp]),
     "delta_bn_apply": (i32, [i32, vp, vp, vp, i64, i32] + [vp] * 8 + [vp]),
     "delta_bn_backward": (i32, [vp, i32, vp, vp, vp, i64, i32, vp, vp, vp, vp, vp, vp, vp]),
-    "delta_add_grad": (i32, [vp, vp, i32, vp, vp, i64, i32, vp]),
+    "delta_add_grad": (i32, [vp, vp, i32, vp, vp, vp, i64, i32, vp]),
     "delta_maxpool3x3s2_fwd": (i32, [vp, vp, i32, i32, i32, i32, vp]),
     "delta_maxpool_workspace_bytes": (i64, [i32, i32, i32, i32]),
     "delta_maxpool3x3s2_bwd": (i32, [vp, vp, vp, i32, i32, i32, i32, vp, vp]),
@@ -63,8 +64,9 @@ class Conv:
         self.P, self.Q, self.kdim, self.tile_n = p.value, q.value, kd.value, tn.value
         self.shape = (N, H, W, Cin, K, R, S, stride, pad)
 
-    def __call__(self, x_ptr: int, y_ptr: int, stream: int):
-        check(lib.delta_conv_forward(self._h, x_ptr, y_ptr, stream))
+    def __call__(self, x_ptr: int, y_ptr: int, stream: int, stats_ptr: int | None = None):
+        """stats_ptr: optional [ceil(M/128)][K] float2 BN-statistics partials."""
+        check(lib.delta_conv_forward(self._h, x_ptr, y_ptr, stats_ptr, stream))
         _count(1)
 
     def __del__(self):
@@ -82,6 +84,13 @@ def bn_stats(x, M, C_, ws, mean, invstd, eps, run_mean, run_var, momentum, strea
     _count(2)
 
 
+def bn_stats_from_partials(partials, M, C_, mean, invstd, eps, run_mean, run_var, momentum,
+                           stream, rows_per_part=128):
+    check(lib.delta_bn_stats_from_partials(partials, M, C_, rows_per_part, mean, invstd, eps,
+                                           run_mean, run_var, momentum, stream))
+    _count(1)
+
+
 def bn_apply(mode, x, res, y, M, C_, mean, invstd, gamma, beta, mean2=None, invstd2=None,
              gamma2=None, beta2=None, stream=None):
     check(lib.delta_bn_apply(mode, x, res, y, M, C_, mean, invstd, gamma, beta, mean2, invstd2,
@@ -95,8 +104,9 @@ def bn_backward(up, pool_hw, mask, x, dx, M, C_, mean, invstd, gamma, dgamma, db
     _count(3)
 
 
-def add_grad(a, up, pool_hw, mask, out, M, C_, stream):
-    check(lib.delta_add_grad(a, up, pool_hw, mask, out, M, C_, stream))
+def add_grad(a, up, pool_hw, up_mask, out_mask, out, M, C_, stream):
+    """out = (a + up*[up_mask>0]) * [out_mask>0] (None masks skipped)."""
+    check(lib.delta_add_grad(a, up, pool_hw, up_mask, out_mask, out, M, C_, stream))
     _count(1)
 
 

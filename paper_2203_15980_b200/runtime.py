@@ -148,6 +148,13 @@ class DeltaRuntime:
                                      for n in self.nodes if len(n.shape) == 4 and n.shape[-1] % 64 == 0),
                                  dtype=torch.float32, device=self.device)
         del maxM, maxC
+        # BN statistics partials written by the conv epilogue (one 128-row
+        # tile per partial); downsample convs use their own scratch because
+        # their BN is applied together with the block's bn3.
+        n_part = max((int(np.prod(n.shape[:-1])) + 127) // 128 * n.shape[-1]
+                     for n in self.nodes if n.op == "conv")
+        self.stats_main = torch.empty(2 * n_part, dtype=torch.float32, device=self.device)
+        self.stats_ds = torch.empty(2 * n_part, dtype=torch.float32, device=self.device)
         mp = next(n for n in self.nodes if n.op == "maxpool")
         self.mp_ws = torch.empty(K.maxpool_workspace_bytes(*self.nodes[mp.parents[0]].shape),
                                  dtype=torch.uint8, device=self.device)
@@ -168,6 +175,9 @@ class DeltaRuntime:
 
     # ------------------------------------------------------------ setup
     def _build_convs(self):
+        # epilogue BN statistics cost ~11*BN cycles per tile against ~2*kblocks*BN
+        # of MMA: fused only where the main loop hides them (K-dim >= 384)
+        self._fuse_stats = {}
         for n in self.nodes:
             if n.op == "conv":
                 cs = self.g.convs[n.attrs["conv"]]
@@ -178,6 +188,7 @@ class DeltaRuntime:
                 conv = K.Conv(Nb, H, W, C, cs.cout, cs.k, cs.k, cs.stride, cs.pad, wptr)
                 assert (conv.P, conv.Q) == n.shape[1:3], (n.name, conv.P, conv.Q, n.shape)
                 self._convs[n.name] = conv
+                self._fuse_stats[n.name] = conv.kdim >= 384
 
     def trace(self) -> P.Trace:
         return G.to_trace(self.g)
@@ -245,15 +256,18 @@ class DeltaRuntime:
         if op == "input":
             self._view(out_off, node).copy_(self.x_dev, non_blocking=True)
         elif op == "conv":
-            self._convs[node.name](ins[0], out, st)
+            # the first production also emits BN statistics partials from the
+            # epilogue; a recompute must not (the scratch may be in use)
+            scratch = None
+            if not recompute and self._fuse_stats[node.name]:
+                scratch = _ptr(self.stats_ds if "downsample" in node.name else self.stats_main)
+            self._convs[node.name](ins[0], out, st, scratch)
         elif op in ("bn_relu", "bn_add_relu", "bn_bn_add_relu"):
             bn = node.attrs["bn"]
             M = int(np.prod(node.shape[:-1]))
             C = node.shape[-1]
             if not recompute:  # statistics once per step; recompute reuses them
-                K.bn_stats(ins[0], M, C, _ptr(self.bn_ws), _ptr(pr.bn_mean[bn]),
-                           _ptr(pr.bn_invstd[bn]), BN_EPS, _ptr(pr.bn_rmean[bn]),
-                           _ptr(pr.bn_rvar[bn]), BN_MOMENTUM, st)
+                self._bn_stats(node.parents[0], ins[0], bn, self.stats_main, M, C, st)
             args = [_ptr(pr.bn_mean[bn]), _ptr(pr.bn_invstd[bn]), _ptr(pr.views["bn_g:" + bn]),
                     _ptr(pr.views["bn_b:" + bn])]
             if op == "bn_relu":
@@ -263,9 +277,7 @@ class DeltaRuntime:
             else:
                 bn2 = node.attrs["bn2"]
                 if not recompute:
-                    K.bn_stats(ins[1], M, C, _ptr(self.bn_ws), _ptr(pr.bn_mean[bn2]),
-                               _ptr(pr.bn_invstd[bn2]), BN_EPS, _ptr(pr.bn_rmean[bn2]),
-                               _ptr(pr.bn_rvar[bn2]), BN_MOMENTUM, st)
+                    self._bn_stats(node.parents[1], ins[1], bn2, self.stats_ds, M, C, st)
                 K.bn_apply(2, ins[0], ins[1], out, M, C, *args, _ptr(pr.bn_mean[bn2]),
                            _ptr(pr.bn_invstd[bn2]), _ptr(pr.views["bn_g:" + bn2]),
                            _ptr(pr.views["bn_b:" + bn2]), stream=st)
@@ -291,11 +303,14 @@ class DeltaRuntime:
             torch.sum(self.dlogits, 0, out=pr.gviews["fc_b"])
             self._view(out_off, node).copy_(self.dlogits @ pr.views["fc_w"])
         elif op == "bn_add_relu_bwd":
+            # parents: [upstream, (O if masked,) X]; upstream already masked
+            # unless it is the pooled head gradient
             bn = node.attrs["bn"]
             M = int(np.prod(node.shape[:-1]))
             C = node.shape[-1]
             pool_hw = int(node.shape[1] * node.shape[2]) if node.attrs.get("from_pool") else 0
-            K.bn_backward(ins[0], pool_hw, ins[1], ins[2], out, M, C, _ptr(pr.bn_mean[bn]),
+            mask = ins[1] if node.attrs.get("masked") else None
+            K.bn_backward(ins[0], pool_hw, mask, ins[-1], out, M, C, _ptr(pr.bn_mean[bn]),
                           _ptr(pr.bn_invstd[bn]), _ptr(pr.views["bn_g:" + bn]),
                           _ptr(pr.gviews["bn_g:" + bn]), _ptr(pr.gviews["bn_b:" + bn]),
                           _ptr(self.bn_ws), st)
@@ -317,15 +332,16 @@ class DeltaRuntime:
             dX = self._conv_bwd(node.attrs["conv"], dC1, X, need_dx=True)
             M = int(np.prod(node.shape[:-1]))
             C = node.shape[-1]
+            out_mask = ins[1] if node.attrs.get("mask_out") else None
             if "conv_short" in node.attrs:
                 dCD = self._view(in_offs[2], self.nodes[node.parents[2]])
                 dXs = self._conv_bwd(node.attrs["conv_short"], dCD, X, need_dx=True)
-                K.add_grad(_ptr(dX), _ptr(dXs), 0, None, out, M, C, st)
+                K.add_grad(_ptr(dX), _ptr(dXs), 0, None, out_mask, out, M, C, st)
+            elif node.attrs.get("from_pool"):
+                pool_hw = int(node.shape[1] * node.shape[2])
+                K.add_grad(_ptr(dX), ins[2], pool_hw, ins[3], out_mask, out, M, C, st)
             else:
-                up = self.nodes[node.parents[2]]
-                pool_hw = int(node.shape[1] * node.shape[2]) if node.attrs.get("from_pool") else 0
-                del up
-                K.add_grad(_ptr(dX), ins[2], pool_hw, ins[3], out, M, C, st)
+                K.add_grad(_ptr(dX), ins[2], 0, None, out_mask, out, M, C, st)
         elif op == "maxpool_bwd":
             src = self.nodes[node.parents[1]]
             Nb, H, W, C = src.shape
@@ -346,6 +362,19 @@ class DeltaRuntime:
             self._view(out_off, node).copy_(pr.gviews["conv:" + conv])
         else:
             raise RuntimeError(f"no kernel for op {op!r} (node {node.name})")
+
+    def _bn_stats(self, conv_node_id: int, x_ptr: int, bn: str, scratch, M: int, C: int, st):
+        """Training-mode BN statistics of a conv output: from the partials the
+        conv epilogue wrote when the conv is long enough to hide that work,
+        else one streaming pass over the tensor."""
+        pr = self.params
+        conv = self.nodes[conv_node_id]
+        args = (_ptr(pr.bn_mean[bn]), _ptr(pr.bn_invstd[bn]), BN_EPS, _ptr(pr.bn_rmean[bn]),
+                _ptr(pr.bn_rvar[bn]), BN_MOMENTUM)
+        if self._fuse_stats.get(conv.name):
+            K.bn_stats_from_partials(_ptr(scratch), M, C, *args, st)
+        else:
+            K.bn_stats(x_ptr, M, C, _ptr(self.bn_ws), *args, st)
 
     def _conv_bwd(self, name: str, dY: torch.Tensor, X: torch.Tensor, need_dx: bool):
         """dgrad/wgrad through cuDNN (channels_last views of arena memory);

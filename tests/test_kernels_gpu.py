@@ -54,11 +54,19 @@ def test_conv_fwd_matches_fp32_reference(case):
     # bf16 output rounding (2^-8 relative) + fp32 accumulation-order noise
     tol = 1e-2 * ref.abs() + 2e-2 * ref.pow(2).mean().sqrt()
     assert bool((err <= tol).all()), f"max err {err.max().item()} rms {ref.pow(2).mean().sqrt().item()}"
-    # bitwise-identical recompute
+    # bitwise-identical recompute, and BN statistics fused in the epilogue
     y2 = torch.empty_like(y)
-    conv(x.data_ptr(), y2.data_ptr(), _stream())
+    M = N * conv.P * conv.Q
+    parts = torch.empty((M + 127) // 128 * Kout * 2, device="cuda")
+    conv(x.data_ptr(), y2.data_ptr(), _stream(), parts.data_ptr())
+    mean = torch.empty(Kout, device="cuda"); inv = torch.empty(Kout, device="cuda")
+    K.bn_stats_from_partials(parts.data_ptr(), M, Kout, mean.data_ptr(), inv.data_ptr(), 1e-5,
+                             None, None, 0.1, _stream())
     torch.cuda.synchronize()
     assert torch.equal(y, y2)
+    yf = y.float().reshape(M, Kout)
+    assert torch.allclose(mean, yf.mean(0), rtol=1e-4, atol=1e-4)
+    assert torch.allclose(inv, torch.rsqrt(yf.var(0, unbiased=False) + 1e-5), rtol=2e-4, atol=1e-4)
 
 
 def test_conv_stem_packed_c4():

@@ -159,10 +159,11 @@ def test_every_op_matches_fp32_autograd_on_its_inputs(rts):
             expect(n.name, T(n.id), L.grad @ Pw["fc_w"])
             expect("grad fc_w", pr.gviews["fc_w"], L.grad.t() @ ins[1])
         elif n.op in ("bn_add_relu_bwd", "bn_relu_bwd"):
-            up, mask, xin = ins
+            up, xin = ins[0], ins[-1]
             if n.attrs.get("from_pool"):
                 up = up[:, :, None, None].expand_as(xin) / (xin.shape[2] * xin.shape[3])
-            gq = up * (mask > 0)
+            masked = n.op == "bn_relu_bwd" or n.attrs.get("masked")
+            gq = up * (ins[1] > 0) if masked else up
             xr = xin.clone().requires_grad_(True)
             gam = Pw["bn_g:" + n.attrs["bn"]].clone().requires_grad_(True)
             bet = Pw["bn_b:" + n.attrs["bn"]].clone().requires_grad_(True)
@@ -187,11 +188,14 @@ def test_every_op_matches_fp32_autograd_on_its_inputs(rts):
                 wd = W(n.attrs["conv_short"])
                 conv(n.attrs["conv_short"], Xr, wd).backward(ins[2])
                 ref = Xr.grad
-            else:
+            elif n.attrs.get("from_pool"):
                 up, O = ins[2], ins[3]
-                if n.attrs.get("from_pool"):
-                    up = up[:, :, None, None].expand_as(O) / (O.shape[2] * O.shape[3])
+                up = up[:, :, None, None].expand_as(O) / (O.shape[2] * O.shape[3])
                 ref = Xr.grad + up * (O > 0)
+            else:
+                ref = Xr.grad + ins[2]
+            if n.attrs.get("mask_out"):
+                ref = ref * (ins[1] > 0)
             expect(n.name, T(n.id), ref)
             expect("grad conv:" + n.attrs["conv"], pr.gviews["conv:" + n.attrs["conv"]].permute(0, 3, 1, 2), w.grad)
         elif n.op == "maxpool_bwd":
