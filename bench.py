@@ -200,6 +200,7 @@ def main():
         return float(t.item())
 
     B = args.batch
+    free_hbm = torch.cuda.mem_get_info()[0]
     rt = DeltaRuntime(args.depth, B, seed=0, anchors=args.anchors)
     rt.dp = dp
 
@@ -325,6 +326,22 @@ def main():
                    "sample": f"unavailable: {e}"}
         ours_plan_ns = P.plan_time_ns(trace, rt.config, 200)
 
+    # ---- max batch vs no-eviction in this GPU's HBM (planner-decided; the
+    # ---- end-to-end verification is scripts/max_batch_verify.py) ----
+    from paper_2203_15980_b200 import maxbatch as MB
+    per_sample = {n.name: n.cost_us / B for n in rt.nodes}
+    cap = free_hbm - 8 * 2**30  # persistent state + cuDNN workspace + slack
+    bpus = int((rt.link_gbs or 50.0) * 1e3)
+    mb_base = MB.search(args.depth, cap, per_sample, bpus, delta=False)
+    mb_delta = {a: MB.search(args.depth, cap, per_sample, bpus, delta=True, anchors=a)
+                for a in ("out+narrow", "out")}
+    max_batch = {"no_eviction": mb_base.batch if mb_base else None,
+                 "delta": {a: (f.batch if f else None) for a, f in mb_delta.items()},
+                 "capacity_gb": round(cap / 1e9, 1)}
+    best = max((f.batch for f in mb_delta.values() if f), default=None)
+    if best and mb_base:
+        max_batch["ratio"] = round(best / mb_base.batch, 3)
+
     value = world * B / (delta_ms * 1e-3)
     if rank == 0:
         line = {
@@ -364,6 +381,7 @@ def main():
                          "launches_timed": conv_n,
                          "share_of_step": round(conv_ms / all_ms, 4) if all_ms else None,
                          "op_ms": {k: round(v, 3) for k, v in sorted(kinds.items(), key=lambda kv: -kv[1])}},
+            "max_batch": max_batch,
             "cpu_baseline": cpu,
             "gpu_launches": (launches * args.steps) if launches is not None else None,
             "clocks": clk,
