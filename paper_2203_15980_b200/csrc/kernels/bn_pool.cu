@@ -27,7 +27,7 @@ constexpr int SLICE = 64;   // channels per reduction block
 // few enough that the fixed-order merge stays short.  A multiple of 32.
 int64_t chunk_rows(int64_t M, int C) {
   const int64_t slices = C / SLICE;
-  const int64_t target_ctas = 148 * 4;
+  const int64_t target_ctas = 148 * 8;
   int64_t chunks = target_ctas / (slices > 0 ? slices : 1);
   if (chunks < 1) chunks = 1;
   int64_t rows = (M + chunks - 1) / chunks;
@@ -77,7 +77,7 @@ __device__ __forceinline__ void merge(float& n, float& mu, float& m2, float nb, 
 }
 
 // ---------------------------------------------------------------- BN stats
-__global__ void __launch_bounds__(256) k_bn_stats_partial(const bf16* __restrict__ x, int64_t M,
+__global__ void __launch_bounds__(256, 4) k_bn_stats_partial(const bf16* __restrict__ x, int64_t M,
                                                           int C, int64_t chunk,
                                                           float2* __restrict__ ws) {
   const int tx = threadIdx.x & 7, ty = threadIdx.x >> 3;
@@ -85,7 +85,7 @@ __global__ void __launch_bounds__(256) k_bn_stats_partial(const bf16* __restrict
   const int64_t r0 = int64_t(blockIdx.y) * chunk;
   const int64_t r1 = min(M, r0 + chunk);
   float s[8] = {0}, q[8] = {0};
-#pragma unroll 4
+#pragma unroll 2
   for (int64_t r = r0 + ty; r < r1; r += 32) {
     float f[8];
     unpack8(ld_stream(x + r * C + c0), f);
@@ -210,7 +210,10 @@ __device__ __forceinline__ void load_up(const bf16* up, int pool_hw, float inv_h
   }
 }
 
-__global__ void __launch_bounds__(256)
+// Per chunk: sum g and sum g*x (x-hat folded in at the end: sum g*xhat =
+// invstd*(sum g*x - mean*sum g)), so no per-channel parameters stay live in
+// the loop and occupancy is not register-limited.
+__global__ void __launch_bounds__(256, 4)
     k_bn_bwd_partial(const bf16* __restrict__ up, int pool_hw, const bf16* __restrict__ mask,
                      const bf16* __restrict__ x, int64_t M, int C, int64_t chunk,
                      const float* mean, const float* invstd, float2* __restrict__ ws) {
@@ -219,29 +222,22 @@ __global__ void __launch_bounds__(256)
   const int64_t r0 = int64_t(blockIdx.y) * chunk;
   const int64_t r1 = min(M, r0 + chunk);
   const float inv_hw = pool_hw ? 1.f / float(pool_hw) : 1.f;
-  float mu[8], is[8];
-#pragma unroll
-  for (int j = 0; j < 8; ++j) {
-    mu[j] = mean[c0 + j];
-    is[j] = invstd[c0 + j];
-  }
   float sg[8] = {0}, sgx[8] = {0};
 #pragma unroll 2
   for (int64_t r = r0 + ty; r < r1; r += 32) {
-    float g[8], m[8], xv[8];
+    float g[8], xv[8];
     load_up(up, pool_hw, inv_hw, r, c0, C, g);
     if (mask) {
+      float m[8];
       unpack8(ld_stream(mask + r * C + c0), m);
-    } else {
 #pragma unroll
-      for (int j = 0; j < 8; ++j) m[j] = 1.f;
+      for (int j = 0; j < 8; ++j) g[j] = m[j] > 0.f ? g[j] : 0.f;
     }
     unpack8(ld_stream(x + r * C + c0), xv);
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
-      const float gj = m[j] > 0.f ? g[j] : 0.f;
-      sg[j] += gj;
-      sgx[j] = fmaf(gj, (xv[j] - mu[j]) * is[j], sgx[j]);
+      sg[j] += g[j];
+      sgx[j] = fmaf(g[j], xv[j], sgx[j]);
     }
   }
   __shared__ float a[32][SLICE + 1], b[32][SLICE + 1];
@@ -257,36 +253,35 @@ __global__ void __launch_bounds__(256)
       A += a[j][threadIdx.x];
       B += b[j][threadIdx.x];
     }
-    ws[int64_t(blockIdx.y) * C + blockIdx.x * SLICE + threadIdx.x] = make_float2(A, B);
+    const int c = blockIdx.x * SLICE + threadIdx.x;
+    // sum g*xhat over the chunk = invstd * (sum g*x - mean * sum g)
+    ws[int64_t(blockIdx.y) * C + c] = make_float2(A, invstd[c] * (B - mean[c] * A));
   }
 }
 
+// warp per channel, lane-strided sums then a fixed xor butterfly
 __global__ void __launch_bounds__(256) k_bn_bwd_final(const float2* __restrict__ ws, int chunks,
                                                       int C, float* dgamma, float* dbeta) {
-  const int cl = threadIdx.x >> 3, lane = threadIdx.x & 7;
-  const int c = blockIdx.x * 32 + cl;
+  const int c = blockIdx.x * 8 + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (c >= C) return;
   float A = 0.f, B = 0.f;
-  if (c < C)
-    for (int k = lane; k < chunks; k += 8) {
-      const float2 p = ws[int64_t(k) * C + c];
-      A += p.x;
-      B += p.y;
-    }
-  __shared__ float sa[256], sb[256];
-  sa[threadIdx.x] = A;
-  sb[threadIdx.x] = B;
-  __syncthreads();
-  if (lane == 0 && c < C) {
-    for (int j = 1; j < 8; ++j) {
-      A += sa[threadIdx.x + j];
-      B += sb[threadIdx.x + j];
-    }
+  for (int k = lane; k < chunks; k += 32) {
+    const float2 p = ws[int64_t(k) * C + c];
+    A += p.x;
+    B += p.y;
+  }
+  A = warp_sum(A);
+  B = warp_sum(B);
+  if (lane == 0) {
     dbeta[c] = A;
     dgamma[c] = B;
   }
 }
 
-__global__ void __launch_bounds__(256)
+// dx = gamma*invstd*(g - dbeta/M - xhat*dgamma/M), xhat = (x-mean)*invstd,
+// folded per channel into dx = k1*g + k2*x + k3 (3 live coefficients).
+__global__ void __launch_bounds__(256, 4)
     k_bn_bwd_apply(const bf16* __restrict__ up, int pool_hw, const bf16* __restrict__ mask,
                    const bf16* __restrict__ x, bf16* __restrict__ dx, int64_t vecs, int cmask,
                    int logC, int64_t M, const float* __restrict__ mean,
@@ -296,35 +291,32 @@ __global__ void __launch_bounds__(256)
   const int c0 = int(first * 8) & cmask;
   const int C = cmask + 1;
   const float invM = 1.f / float(M);
-  float ka[8], kb[8], kd[8], mu[8], is[8];
+  float k1[8], k2[8], k3[8];
 #pragma unroll
   for (int j = 0; j < 8; ++j) {
-    is[j] = invstd[c0 + j];
-    mu[j] = mean[c0 + j];
-    ka[j] = gamma[c0 + j] * is[j];
-    kb[j] = dbeta[c0 + j] * invM;
-    kd[j] = dgamma[c0 + j] * invM;
+    const float is = invstd[c0 + j];
+    const float a = gamma[c0 + j] * is;
+    const float kd = dgamma[c0 + j] * invM * is;  // coefficient of (x - mean)
+    k1[j] = a;
+    k2[j] = -a * kd;
+    k3[j] = a * (kd * mean[c0 + j] - dbeta[c0 + j] * invM);
   }
   const float inv_hw = pool_hw ? 1.f / float(pool_hw) : 1.f;
   const int64_t stride = int64_t(gridDim.x) * blockDim.x;
 #pragma unroll 2
   for (int64_t i = first; i < vecs; i += stride) {
     const int64_t row = (i * 8) >> logC;
-    float g[8], m[8], xv[8];
+    float g[8], xv[8];
     load_up(up, pool_hw, inv_hw, row, c0, C, g);
     if (mask) {
+      float m[8];
       unpack8(ld_stream(mask + i * 8), m);
-    } else {
 #pragma unroll
-      for (int j = 0; j < 8; ++j) m[j] = 1.f;
+      for (int j = 0; j < 8; ++j) g[j] = m[j] > 0.f ? g[j] : 0.f;
     }
     unpack8(ld_stream(x + i * 8), xv);
 #pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      const float gj = m[j] > 0.f ? g[j] : 0.f;
-      const float xh = (xv[j] - mu[j]) * is[j];
-      g[j] = ka[j] * (gj - kb[j] - xh * kd[j]);
-    }
+    for (int j = 0; j < 8; ++j) g[j] = fmaf(k1[j], g[j], fmaf(k2[j], xv[j], k3[j]));
     reinterpret_cast<uint4*>(dx)[i] = pack8(g);
   }
 }
@@ -603,8 +595,8 @@ cudaError_t bn_backward(const void* up, int pool_hw, const void* mask, const voi
   auto X = static_cast<const bf16*>(x);
   k_bn_bwd_partial<<<dim3(C / SLICE, chunks), 256, 0, st>>>(U, pool_hw, Mk, X, M, C, chunk, mean,
                                                             invstd, reinterpret_cast<float2*>(ws));
-  k_bn_bwd_final<<<(C + 31) / 32, 256, 0, st>>>(reinterpret_cast<const float2*>(ws), chunks, C,
-                                                dgamma, dbeta);
+  k_bn_bwd_final<<<(C + 7) / 8, 256, 0, st>>>(reinterpret_cast<const float2*>(ws), chunks, C,
+                                              dgamma, dbeta);
   const int64_t vecs = M * C / 8;
   k_bn_bwd_apply<<<grid_for(vecs, 256), 256, 0, st>>>(
       U, pool_hw, Mk, X, static_cast<bf16*>(dx), vecs, C - 1, __builtin_ctz(C), M, mean, invstd,

@@ -56,7 +56,13 @@ res["bn_stats"] = (timeit(lambda: K.bn_stats(x.data_ptr(), M, C, ws.data_ptr(), 
 res["bn_apply_relu"] = (timeit(lambda: K.bn_apply(0, x.data_ptr(), None, y.data_ptr(), M, C, mean.data_ptr(), inv.data_ptr(), gam.data_ptr(), bet.data_ptr(), stream=st)), 2 * nb)
 res["bn_add_relu"] = (timeit(lambda: K.bn_apply(1, x.data_ptr(), r.data_ptr(), y.data_ptr(), M, C, mean.data_ptr(), inv.data_ptr(), gam.data_ptr(), bet.data_ptr(), stream=st)), 3 * nb)
 res["bn_backward"] = (timeit(lambda: K.bn_backward(r.data_ptr(), 0, x.data_ptr(), x.data_ptr(), y.data_ptr(), M, C, mean.data_ptr(), inv.data_ptr(), gam.data_ptr(), dg.data_ptr(), db.data_ptr(), ws.data_ptr(), st)), 7 * nb)
-res["add_grad_mask"] = (timeit(lambda: K.add_grad(x.data_ptr(), r.data_ptr(), 0, x.data_ptr(), y.data_ptr(), M, C, st)), 4 * nb)
+res["bn_backward_nomask"] = (timeit(lambda: K.bn_backward(r.data_ptr(), 0, None, x.data_ptr(), y.data_ptr(), M, C, mean.data_ptr(), inv.data_ptr(), gam.data_ptr(), dg.data_ptr(), db.data_ptr(), ws.data_ptr(), st)), 5 * nb)
+res["add_grad_mask"] = (timeit(lambda: K.add_grad(x.data_ptr(), r.data_ptr(), 0, x.data_ptr(), None, y.data_ptr(), M, C, st)), 4 * nb)
+for (MM, CC) in [(N * 14 * 14, 1024), (N * 7 * 7, 2048), (N * 56 * 56, 64)]:
+    xx = torch.randn(MM, CC, device="cuda").to(torch.bfloat16); rr = torch.randn(MM, CC, device="cuda").to(torch.bfloat16)
+    yy = torch.empty_like(xx); m2 = torch.zeros(CC, device="cuda"); i2 = torch.ones(CC, device="cuda"); g2 = torch.ones(CC, device="cuda")
+    d1 = torch.empty(CC, device="cuda"); d2 = torch.empty(CC, device="cuda"); w2 = torch.empty(K.bn_workspace_floats(MM, CC), device="cuda")
+    res[f"bn_backward_{MM}x{CC}"] = (timeit(lambda: K.bn_backward(rr.data_ptr(), 0, xx.data_ptr(), xx.data_ptr(), yy.data_ptr(), MM, CC, m2.data_ptr(), i2.data_ptr(), g2.data_ptr(), d1.data_ptr(), d2.data_ptr(), w2.data_ptr(), st)), 7 * MM * CC * 2)
 res["torch_copy"] = (timeit(lambda: y.copy_(x)), 2 * nb)
 for k, (ms, b) in res.items():
     print(json.dumps(dict(kernel=k, ms=round(ms, 4), gbs=round(b / ms / 1e6, 1))))
