@@ -217,8 +217,9 @@ def main():
         x[..., :3] = torch.randn(B, 224, 224, 3, generator=gen).to(torch.bfloat16)
         y = torch.randint(0, 1000, (B,), generator=gen).pin_memory()
         xs.append((x, y))
-    rt.x_dev.copy_(xs[0][0])
-    rt.y_dev.copy_(xs[0][1])
+    for slot in range(2):
+        rt.x_slots[slot].copy_(xs[0][0])
+        rt.y_slots[slot].copy_(xs[0][1])
 
     def timed_device_steps(n_warm, n_steps):
         for _ in range(n_warm):
@@ -267,15 +268,14 @@ def main():
     delta_ms = timed_device_steps(args.warmup, args.steps)
     clk = clocks.stop()
 
-    # ---- end to end through the public API: host batch -> step -> loss ----
-    for i in range(args.warmup):
-        rt.step(*xs[i % 2])
+    # ---- end to end through the public API: host batches -> steps -> losses
+    # ---- (DeltaRuntime.train: H2D of every batch overlapped with the
+    # ---- previous step on a copy-engine stream, D2H of every loss) ----
+    rt.train([xs[i % 2] for i in range(args.warmup)])
     torch.cuda.synchronize()
     barrier()
     t0 = time.perf_counter()
-    losses = []
-    for i in range(args.steps):
-        losses.append(rt.step(*xs[i % 2]))
+    losses = rt.train([xs[i % 2] for i in range(args.steps)])
     torch.cuda.synchronize()
     e2e_s = max_over_ranks((time.perf_counter() - t0) / args.steps)
     h2d_bytes = xs[0][0].numel() * 2 + xs[0][1].numel() * 8

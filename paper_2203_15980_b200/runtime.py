@@ -162,8 +162,14 @@ class DeltaRuntime:
         self.loss = torch.zeros(1, dtype=torch.float32, device=self.device)
         self.dlogits = torch.empty(batch, ncls, dtype=torch.float32, device=self.device)
         self.row_loss = torch.empty(batch, dtype=torch.float32, device=self.device)
-        self.x_dev = torch.zeros(self.g.nodes[0].shape, dtype=torch.bfloat16, device=self.device)
-        self.y_dev = torch.zeros(batch, dtype=torch.int64, device=self.device)
+        self.x_slots = [torch.zeros(self.g.nodes[0].shape, dtype=torch.bfloat16,
+                                    device=self.device) for _ in range(2)]
+        self.y_slots = [torch.zeros(batch, dtype=torch.int64, device=self.device)
+                        for _ in range(2)]
+        self._use_slot(0)
+        self.graphs = None
+        self._h2d = None
+        self._loss_host = None
         self.program = None
         self.arena = None
         self.swap = None
@@ -225,6 +231,7 @@ class DeltaRuntime:
         self.program = prog
         self.config = cfg
         self.graph = None
+        self.graphs = None
         if self.arena is None or self.arena.numel() < prog.arena_bytes:
             self.arena = None
             torch.cuda.empty_cache()
@@ -447,27 +454,39 @@ class DeltaRuntime:
         self.params.sgd_step(self.lr)
 
     def capture(self):
-        """Capture one full step (program + optimizer) as a CUDA graph."""
+        """Capture one full step (program + optimizer) as a CUDA graph per
+        input staging slot (two slots let `train` overlap the next batch's
+        host->device copy with the current step)."""
         torch.cuda.synchronize()
-        g = torch.cuda.CUDAGraph()
-        with torch.cuda.stream(self.stream):
-            with torch.cuda.graph(g, stream=self.stream):
-                self.run_program()
-        self.graph = g
+        graphs = []
+        for slot in range(2):
+            self._use_slot(slot)
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.stream(self.stream):
+                with torch.cuda.graph(g, stream=self.stream):
+                    self.run_program()
+            graphs.append(g)
+        self._use_slot(0)
+        self.graphs = graphs
+        self.graph = graphs[0]
         torch.cuda.synchronize()
 
+    def _use_slot(self, slot: int):
+        self._slot = slot
+        self.x_dev = self.x_slots[slot]
+        self.y_dev = self.y_slots[slot]
+
     def step_device(self):
-        """One step with inputs already resident (x_dev, y_dev)."""
-        if self.graph is not None:
-            with torch.cuda.stream(self.stream):
-                self.graph.replay()
-        else:
-            with torch.cuda.stream(self.stream):
+        """One step with inputs already resident in the current slot."""
+        with torch.cuda.stream(self.stream):
+            if self.graph is not None:
+                self.graphs[self._slot].replay()
+            else:
                 self.run_program()
 
     def step(self, x_host: torch.Tensor, y_host: torch.Tensor) -> float:
-        """One step through the public API with HOST buffers: H2D of the batch,
-        the step, D2H of the loss."""
+        """One synchronous step through the public API with HOST buffers:
+        H2D of the batch, the step, D2H of the loss."""
         with torch.cuda.stream(self.stream):
             self.x_dev.copy_(x_host, non_blocking=True)
             self.y_dev.copy_(y_host, non_blocking=True)
@@ -475,6 +494,47 @@ class DeltaRuntime:
         with torch.cuda.stream(self.stream):
             loss = self.loss.to("cpu", non_blocking=False)
         return float(loss.item())
+
+    def train(self, batches) -> list:
+        """Train on a sequence of (x, y) pinned host batches.  Each step's
+        inputs are copied host->device on a copy-engine stream into the
+        staging slot the step after next is not using, overlapped with the
+        current step; each step's loss is copied device->host right after it.
+        Returns the per-step losses."""
+        n = len(batches)
+        if n == 0:
+            return []
+        if self._h2d is None:
+            self._h2d = torch.cuda.Stream(device=self.device)
+            self._loss_host = None
+        if self._loss_host is None or self._loss_host.numel() < n:
+            self._loss_host = torch.empty(max(n, 64), dtype=torch.float32).pin_memory()
+        ev_in = [torch.cuda.Event(), torch.cuda.Event()]
+        ev_done = [torch.cuda.Event(), torch.cuda.Event()]
+
+        def h2d(i):
+            slot = i % 2
+            with torch.cuda.stream(self._h2d):
+                if i >= 2:
+                    self._h2d.wait_event(ev_done[slot])  # step i-2 read this slot
+                self.x_slots[slot].copy_(batches[i][0], non_blocking=True)
+                self.y_slots[slot].copy_(batches[i][1], non_blocking=True)
+                ev_in[slot].record(self._h2d)
+
+        h2d(0)
+        for i in range(n):
+            slot = i % 2
+            if i + 1 < n:
+                h2d(i + 1)
+            self.stream.wait_event(ev_in[slot])
+            self._use_slot(slot)
+            self.step_device()
+            ev_done[slot].record(self.stream)
+            with torch.cuda.stream(self.stream):
+                self._loss_host[i].copy_(self.loss[0], non_blocking=True)
+        self.stream.synchronize()
+        self._use_slot(0)
+        return self._loss_host[:n].tolist()
 
     # ----------------------------------------------------- cost model
     def measure_costs(self, iters: int = 3, link: bool = True):

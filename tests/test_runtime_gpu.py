@@ -246,4 +246,12 @@ def test_graph_capture_replay_equals_eager(rts):
     l_graph = delta.step(x, y)
     assert l_graph == l_eager
     assert torch.equal(delta.params.grad, g_eager)
+    # pipelined train(): alternating staging slots, same results per step
+    x2, y2 = make_batch(3)
+    xp, yp = x.pin_memory(), y.pin_memory()
+    x2p, y2p = x2.pin_memory(), y2.pin_memory()
+    losses = delta.train([(xp, yp), (x2p, y2p), (xp, yp)])
+    assert losses[0] == l_eager and losses[2] == l_eager
+    assert losses[1] == delta.step(x2, y2)
     delta.graph = None
+    delta.graphs = None
