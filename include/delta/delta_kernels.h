@@ -24,8 +24,11 @@ extern "C" {
 #endif
 
 /* ---- recompute engine: convolution (ConvForward, ref src/trace.cpp:403) ----
- * Weights are [K][R][S][C] bf16 (C == 4: [K][ceil(R*S*4/64)*64], taps packed
- * 4 channels each).  The handle caches the TMA descriptor of the weights. */
+ * Weights are [K][R][S][C] bf16.  C == 4 is the 7x7/2 pad-3 stem over an
+ * even-width image, computed as a 7x4 conv over pixel pairs: weights
+ * [K][256] bf16, column (r*4 + j)*8 + e*4 + c holds W[k][r][2j+e-1][c]
+ * (zero for 2j+e-1 < 0 and for columns >= 224).  The handle caches the TMA
+ * descriptor of the weights. */
 typedef struct delta_conv delta_conv;
 delta_status delta_conv_create(int32_t N, int32_t H, int32_t W, int32_t C, int32_t K,
                                int32_t R, int32_t S, int32_t stride, int32_t pad,
@@ -34,6 +37,36 @@ delta_status delta_conv_create(int32_t N, int32_t H, int32_t W, int32_t C, int32
  * of the bf16 outputs — BatchNorm statistics partials fused in the epilogue. */
 delta_status delta_conv_forward(const delta_conv* c, const void* x, void* y, float* stats,
                                 void* stream);
+/* Fused epilogues.  The backward pass runs input-gradient (dgrad) convolutions
+ * of stride-1 layers through the same kernel: x = dY [N][P][Q][K], weights
+ * transposed (1x1: [C][K]) or flipped and transposed (RxS: [C][R][S][K] with
+ * W'[c][r][s][k] = W[k][R-1-r][S-1-s][c]).
+ *   DELTA_EPI_ADD_MASK: y = bf16((acc + add') * [out_mask > 0]); add' = add
+ *       ([M][K]), or with pool_hw > 0 the pooled add ([N][K]) / pool_hw *
+ *       [add_mask > 0] (add_mask is read only with a pooled add).
+ *       Null pointers are skipped.  (The residual-branch gradient sum.)
+ *   DELTA_EPI_BN_BWD: y = g = bf16(acc) * [relu(bn(xc)) > 0] with the saved
+ *       statistics (the forward's exact arithmetic), and `stats` receives the
+ *       per-tile (sum g, sum g*xc) partials for delta_bn_backward_from_partials.
+ * Output channels must be a multiple of 32 for the fused modes. */
+enum { DELTA_EPI_STORE = 0, DELTA_EPI_ADD_MASK = 1, DELTA_EPI_BN_BWD = 2 };
+typedef struct delta_conv_epilogue {
+  int32_t mode;
+  int32_t pool_hw;
+  const void* add;
+  const void* add_mask;
+  const void* out_mask;
+  const void* xc;
+  const float* mean;
+  const float* invstd;
+  const float* gamma;
+  const float* beta;
+} delta_conv_epilogue;
+delta_status delta_conv_forward_ex(const delta_conv* c, const void* x, void* y, float* stats,
+                                   const delta_conv_epilogue* epi, void* stream);
+/* Override the output-channel tile (64, 128 or 256, dividing K).  The fused
+ * epilogues (DELTA_EPI_ADD_MASK / DELTA_EPI_BN_BWD) require tile_n <= 128. */
+delta_status delta_conv_set_tile_n(delta_conv* c, int32_t tile_n);
 delta_status delta_conv_geometry(const delta_conv* c, int32_t* P, int32_t* Q, int32_t* kdim,
                                  int32_t* tile_n);
 void delta_conv_destroy(delta_conv* c);
@@ -45,7 +78,10 @@ int64_t delta_bn_workspace_floats(int64_t M, int32_t C);
 delta_status delta_bn_stats(const void* x, int64_t M, int32_t C, float* ws, float* mean,
                             float* invstd, float eps, float* run_mean, float* run_var,
                             float momentum, void* stream);
-/* statistics from the conv epilogue's per-tile partials (rows_per_part = 128) */
+/* statistics from the conv epilogue's per-tile partials (rows_per_part = 128);
+ * the partials buffer holds delta_stats_partials_floats(M, C, rows_per_part)
+ * floats: the epilogue's partials followed by the merge's grouping scratch. */
+int64_t delta_stats_partials_floats(int64_t M, int32_t C, int32_t rows_per_part);
 delta_status delta_bn_stats_from_partials(const float* partials, int64_t M, int32_t C,
                                           int32_t rows_per_part, float* mean, float* invstd,
                                           float eps, float* run_mean, float* run_var,
@@ -60,6 +96,13 @@ delta_status delta_bn_backward(const void* up, int32_t pool_hw, const void* mask
                                void* dx, int64_t M, int32_t C, const float* mean,
                                const float* invstd, const float* gamma, float* dgamma,
                                float* dbeta, float* ws, void* stream);
+/* BN(+ReLU) backward after a DELTA_EPI_BN_BWD conv: `partials` are that
+ * conv's per-128-row-tile (sum g, sum g*x) (sized by delta_stats_partials_floats,
+ * the tail is scratch), g its masked output.  Writes dgamma, dbeta, dx. */
+delta_status delta_bn_backward_from_partials(const float* partials, const void* g, const void* x,
+                                             void* dx, int64_t M, int32_t C, const float* mean,
+                                             const float* invstd, const float* gamma,
+                                             float* dgamma, float* dbeta, void* stream);
 /* out = (a + up*[up_mask>0]) * [out_mask>0]; null masks are not applied;
  * pool_hw > 0: `up` is [N,C] broadcast over pool_hw pixels / pool_hw */
 delta_status delta_add_grad(const void* a, const void* up, int32_t pool_hw, const void* up_mask,

@@ -156,6 +156,35 @@ __global__ void __launch_bounds__(256)
   }
 }
 
+// First level of a two-level merge when there are many partials: thread per
+// (channel, group of GROUP consecutive partials) -> one (mean, M2) partial of
+// the group's rows, two passes (sum -> mean, then M2) in a fixed order.
+constexpr int GROUP = 32;
+__global__ void __launch_bounds__(256)
+    k_bn_stats_group(const float2* __restrict__ ws, int parts, int64_t rows_per, int64_t M, int C,
+                     float2* __restrict__ out) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= C) return;
+  const int k0 = blockIdx.y * GROUP;
+  const int k1 = min(parts, k0 + GROUP);
+  const float n_last = float(M - int64_t(parts - 1) * rows_per);
+  const float n_full = float(rows_per);
+  float s = 0.f, n = 0.f;
+  for (int k = k0; k < k1; ++k) {
+    const float nk = k == parts - 1 ? n_last : n_full;
+    s = fmaf(nk, ws[int64_t(k) * C + c].x, s);
+    n += nk;
+  }
+  const float mu = s / n;
+  float m2 = 0.f;
+  for (int k = k0; k < k1; ++k) {
+    const float2 p = ws[int64_t(k) * C + c];
+    const float d = p.x - mu;
+    m2 += fmaf(k == parts - 1 ? n_last : n_full, d * d, p.y);
+  }
+  out[int64_t(blockIdx.y) * C + c] = make_float2(mu, m2);
+}
+
 // ---------------------------------------------------------------- BN apply
 // blockDim (256) is a multiple of C/8 for every C <= 2048, so with a grid
 // stride that is a multiple of the block, each thread always touches the SAME
@@ -276,6 +305,45 @@ __global__ void __launch_bounds__(256) k_bn_bwd_final(const float2* __restrict__
   if (lane == 0) {
     dbeta[c] = A;
     dgamma[c] = B;
+  }
+}
+
+// Parameter gradients from the conv epilogue's raw per-tile (sum g, sum g*x)
+// partials: pass 1 (when there are many) sums groups of GROUP partials into
+// the scratch after them; pass 2 = warp per channel, fixed order; then
+// dbeta = sum g, dgamma = invstd * (sum g*x - mean * sum g).
+__global__ void __launch_bounds__(256)
+    k_bn_bwd_group(const float2* __restrict__ ws, int parts, int C, float2* __restrict__ out) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= C) return;
+  const int k0 = blockIdx.y * GROUP;
+  const int k1 = min(parts, k0 + GROUP);
+  float A = 0.f, B = 0.f;
+  for (int k = k0; k < k1; ++k) {
+    const float2 p = ws[int64_t(k) * C + c];
+    A += p.x;
+    B += p.y;
+  }
+  out[int64_t(blockIdx.y) * C + c] = make_float2(A, B);
+}
+
+__global__ void __launch_bounds__(256)
+    k_bn_bwd_final_raw(const float2* __restrict__ ws, int parts, int C, const float* mean,
+                       const float* invstd, float* dgamma, float* dbeta) {
+  const int c = blockIdx.x * 8 + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (c >= C) return;
+  float A = 0.f, B = 0.f;
+  for (int k = lane; k < parts; k += 32) {
+    const float2 p = ws[int64_t(k) * C + c];
+    A += p.x;
+    B += p.y;
+  }
+  A = warp_sum(A);
+  B = warp_sum(B);
+  if (lane == 0) {
+    dbeta[c] = A;
+    dgamma[c] = invstd[c] * (B - mean[c] * A);
   }
 }
 
@@ -532,8 +600,31 @@ __global__ void k_mean_rows(const float* row_loss, int N, float* loss) {
 
 int64_t bn_workspace_floats(int64_t M, int C) {
   const int64_t chunk = chunk_rows(M, C);
-  return 2 * ((M + chunk - 1) / chunk) * C;
+  const int64_t chunks = (M + chunk - 1) / chunk;
+  return 2 * (chunks + (chunks + GROUP - 1) / GROUP) * C;
 }
+
+namespace {
+// Merge `parts` (mean, M2) partials of `rows_per` rows (the last shorter) at
+// ws[0 .. parts*C) into the channel statistics.  Above 2*GROUP partials a
+// grouping pass first writes ceil(parts/GROUP) partials after them (the
+// caller's buffer holds both), so each merge warp walks at most a few dozen.
+void merge_partials(const float2* ws, int parts, int64_t rows_per, int64_t M, int C, float* mean,
+                    float* invstd, float eps, float* rm, float* rv, float mom, cudaStream_t st) {
+  if (parts > 2 * GROUP) {
+    const int groups = (parts + GROUP - 1) / GROUP;
+    float2* out = const_cast<float2*>(ws) + int64_t(parts) * C;
+    const int bx = C < 256 ? C : 256;
+    k_bn_stats_group<<<dim3((C + bx - 1) / bx, groups), bx, 0, st>>>(ws, parts, rows_per, M, C,
+                                                                     out);
+    ws = out;
+    parts = groups;
+    rows_per *= GROUP;
+  }
+  k_bn_stats_merge<<<(C + 7) / 8, 256, 0, st>>>(ws, parts, rows_per, M, C, mean, invstd, eps, rm,
+                                                rv, mom);
+}
+}  // namespace
 
 cudaError_t bn_stats(const void* x, int64_t M, int C, float* ws, float* mean, float* invstd,
                      float eps, float* rm, float* rv, float mom, cudaStream_t st) {
@@ -542,18 +633,22 @@ cudaError_t bn_stats(const void* x, int64_t M, int C, float* ws, float* mean, fl
   const int chunks = int((M + chunk - 1) / chunk);
   k_bn_stats_partial<<<dim3(C / SLICE, chunks), 256, 0, st>>>(static_cast<const bf16*>(x), M, C,
                                                               chunk, reinterpret_cast<float2*>(ws));
-  k_bn_stats_merge<<<(C + 7) / 8, 256, 0, st>>>(reinterpret_cast<const float2*>(ws), chunks,
-                                                chunk, M, C, mean, invstd, eps, rm, rv, mom);
+  merge_partials(reinterpret_cast<const float2*>(ws), chunks, chunk, M, C, mean, invstd, eps, rm,
+                 rv, mom, st);
   return cudaGetLastError();
+}
+
+int64_t stats_partials_floats(int64_t M, int C, int rows_per_part) {
+  const int64_t parts = (M + rows_per_part - 1) / rows_per_part;
+  return 2 * (parts + (parts + GROUP - 1) / GROUP) * C;
 }
 
 cudaError_t bn_stats_from_partials(const float* partials, int64_t M, int C, int rows_per_part,
                                    float* mean, float* invstd, float eps, float* rm, float* rv,
                                    float mom, cudaStream_t st) {
   const int parts = int((M + rows_per_part - 1) / rows_per_part);
-  k_bn_stats_merge<<<(C + 7) / 8, 256, 0, st>>>(reinterpret_cast<const float2*>(partials), parts,
-                                                rows_per_part, M, C, mean, invstd, eps, rm, rv,
-                                                mom);
+  merge_partials(reinterpret_cast<const float2*>(partials), parts, rows_per_part, M, C, mean,
+                 invstd, eps, rm, rv, mom, st);
   return cudaGetLastError();
 }
 
@@ -601,6 +696,29 @@ cudaError_t bn_backward(const void* up, int pool_hw, const void* mask, const voi
   k_bn_bwd_apply<<<grid_for(vecs, 256), 256, 0, st>>>(
       U, pool_hw, Mk, X, static_cast<bf16*>(dx), vecs, C - 1, __builtin_ctz(C), M, mean, invstd,
       gamma, dgamma, dbeta);
+  return cudaGetLastError();
+}
+
+cudaError_t bn_backward_from_partials(const float* partials, int rows_per_part, const void* g,
+                                      const void* x, void* dx, int64_t M, int C,
+                                      const float* mean, const float* invstd, const float* gamma,
+                                      float* dgamma, float* dbeta, cudaStream_t st) {
+  if (C % SLICE || (C & (C - 1)) || C > 2048) return cudaErrorInvalidValue;
+  auto ws = reinterpret_cast<const float2*>(partials);
+  int parts = int((M + rows_per_part - 1) / rows_per_part);
+  if (parts > 2 * GROUP) {
+    const int groups = (parts + GROUP - 1) / GROUP;
+    float2* out = const_cast<float2*>(ws) + int64_t(parts) * C;
+    const int bx = C < 256 ? C : 256;
+    k_bn_bwd_group<<<dim3((C + bx - 1) / bx, groups), bx, 0, st>>>(ws, parts, C, out);
+    ws = out;
+    parts = groups;
+  }
+  k_bn_bwd_final_raw<<<(C + 7) / 8, 256, 0, st>>>(ws, parts, C, mean, invstd, dgamma, dbeta);
+  const int64_t vecs = M * C / 8;
+  k_bn_bwd_apply<<<grid_for(vecs, 256), 256, 0, st>>>(
+      static_cast<const bf16*>(g), 0, nullptr, static_cast<const bf16*>(x), static_cast<bf16*>(dx),
+      vecs, C - 1, __builtin_ctz(C), M, mean, invstd, gamma, dgamma, dbeta);
   return cudaGetLastError();
 }
 

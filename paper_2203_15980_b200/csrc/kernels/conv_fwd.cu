@@ -11,10 +11,12 @@
 // Tile 128 x BN x 64, fp32 accumulators in TMEM.
 //
 // Persistent, warp-specialised (one CTA per SM, static round-robin tiles):
-//   warps 0-3 : producers.  MODE_GATHER / MODE_STEM: im2col gather of A with
-//               cp.async (zero-fill implements the padding); MODE_TMA (1x1,
-//               stride 1): A is a plain [M, C] matrix loaded by TMA.  Thread 0
-//               issues the TMA of the weight tile B.
+//   warps 0-3 : producers.  MODE_IM2COL (3x3, strided 1x1): A by the TMA
+//               im2col unit (out-of-image taps zero-filled = the padding);
+//               MODE_STEM: TMA im2col over pixel pairs (see below); MODE_TMA
+//               (1x1, stride 1): A is a plain [M, C] matrix loaded by TMA;
+//               MODE_GATHER (opt-in, DELTA_CONV_GATHER=1): cp.async im2col.
+//               The weight tile B is always one TMA load.
 //   warps 4-7 : epilogue — TMEM -> registers -> bf16 -> HBM, one TMEM lane
 //               quarter each.
 //   warp 8    : TMEM allocation + single-thread tcgen05.mma issue.
@@ -43,6 +45,9 @@ constexpr int BM = 128;
 constexpr int BK = 64;
 constexpr int kThreads = 288;
 constexpr int MODE_GATHER = 0, MODE_STEM = 1, MODE_TMA = 2, MODE_IM2COL = 3;
+// fused-epilogue operand ring: 24 KB per epilogue warp, slots of one 2 KB
+// block per operand (12 slots with one operand, 6 with two)
+constexpr uint32_t EPI_RING_WARP = 24576;
 
 
 struct ConvArgs {
@@ -54,14 +59,82 @@ struct ConvArgs {
   int taps;     // R*S
   int n_tiles;  // ceil(K / BN)
   int tiles;    // m_tiles * n_tiles
-  float2* stats;  // optional: per (m_tile, channel) (mean, M2) of the bf16 outputs
+  float2* stats;  // optional per (m_tile, channel) partials: EPI_STORE (mean, M2) of the
+                  // bf16 outputs; EPI_BN_BWD (sum g, sum g*xc) of the gradients
+  ConvEpilogue e;
 };
+
+// ---- epilogue helpers (one thread = one output row, 32 columns per chunk) ----
+__device__ __forceinline__ uint4 ldg16(const void* p) {
+  return __ldg(reinterpret_cast<const uint4*>(p));
+}
+__device__ __forceinline__ void unpack8f(uint4 u, float* f) {
+  const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&u);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const float2 t = __bfloat1622float2(h[i]);
+    f[2 * i] = t.x;
+    f[2 * i + 1] = t.y;
+  }
+}
+__device__ __forceinline__ float bf16_round(float v) {
+  return __bfloat162float(__float2bfloat16_rn(v));
+}
+// Reduce-scatter of a 32x32 (lanes x registers) block: afterwards lane l
+// holds in v[0] the sum over all lanes of v[l].  Fixed butterfly order, so
+// the result is deterministic.
+__device__ __forceinline__ void transpose_sum32(float (&v)[32], int lane) {
+#pragma unroll
+  for (int o = 16; o >= 1; o >>= 1) {
+    const bool up = (lane & o) != 0;
+#pragma unroll
+    for (int i = 0; i < o; ++i) {
+      const float send = up ? v[i] : v[i + o];
+      const float keep = up ? v[i + o] : v[i];
+      v[i] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+    }
+  }
+}
+
+// Row `lane` (16 B chunk u) of a 32x32 bf16 block staged in smem with the 64B
+// swizzle (the layout of the TMA boxes the epilogue loads and stores).
+__device__ __forceinline__ uint4 ld_row16(uint32_t buf, int lane, int u) {
+  uint4 r;
+  asm volatile("ld.shared.v4.b32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "r"(buf + lane * 64 + ((u ^ ((lane >> 1) & 3)) << 4)));
+  return r;
+}
+
+// Compile-time epilogue variants (the runtime ConvEpilogue.mode picks one at
+// launch): straight-line code, operand presence known, packed bf16x2 math.
+constexpr int EV_STORE = 0;    // y = bf16(acc)                       [+ BN-stats partials]
+constexpr int EV_ADD = 1;      // y = bf16(acc) + add
+constexpr int EV_ADD_OM = 2;   // y = (bf16(acc) + add) & [out_mask > 0]
+constexpr int EV_POOL = 3;     // y = bf16(acc + pooled/hw * [add_mask > 0]) & [out_mask > 0]
+constexpr int EV_BN_BWD = 4;   // y = g = bf16(acc) & [relu(bn(xc)) > 0]; partials (sum g, sum g*xc)
+__host__ __device__ constexpr int ev_operands(int ev) {
+  return ev == EV_ADD || ev == EV_BN_BWD ? 1 : (ev == EV_ADD_OM || ev == EV_POOL ? 2 : 0);
+}
+
+// bf16x2 lanes positive (> +0) -> 0xFFFF, else 0 (bf16 bit patterns read as
+// int16: positive values are exactly the positive int16s)
+__device__ __forceinline__ uint32_t pos_mask2(uint32_t w) { return __vcmpgts2(w, 0u); }
+__device__ __forceinline__ uint32_t add_bf16x2(uint32_t a, uint32_t b) {
+  __nv_bfloat162 r = __hadd2(*reinterpret_cast<__nv_bfloat162*>(&a),
+                             *reinterpret_cast<__nv_bfloat162*>(&b));
+  return *reinterpret_cast<uint32_t*>(&r);
+}
 
 __device__ __forceinline__ uint8_t* align1024(uint8_t* p) {
   return reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(p) + 1023) & ~uintptr_t(1023));
 }
 
-template <int BN, int STAGES, int MODE>
+// EV != EV_STORE: the epilogue reads one or two [M][K] operand blocks (t0,
+// t1) per 32x32 chunk, cp.async-loaded (slots - 1) chunks ahead into a
+// per-warp ring (a chunk's math is far shorter than an HBM round trip; 64 B-row
+// TMA boxes were issue-bound).
+template <int BN, int STAGES, int MODE, int EV>
 __global__ void __launch_bounds__(kThreads, 1)
     k_conv_fwd(const __grid_constant__ CUtensorMap wmap, const __grid_constant__ CUtensorMap amap,
                const __grid_constant__ CUtensorMap ymap, const ConvArgs a) {
@@ -77,10 +150,14 @@ __global__ void __launch_bounds__(kThreads, 1)
   const uint32_t sB = sA + STAGES * A_STAGE;
   // epilogue staging: 4 warps x 2 buffers x (32 rows x 64 B), 64B-swizzled
   const uint32_t sOut = sA + STAGES * (A_STAGE + B_STAGE);
+  // fused-epilogue operand ring: 4 warps x EPI_RING_WARP
+  constexpr bool FUSED = EV != EV_STORE;
+  constexpr uint32_t IN_BYTES = FUSED ? 4 * EPI_RING_WARP : 0;
+  const uint32_t sIn = sOut + 16384;
   // BN-statistics scratch: per quarter-warp column (sum, sumsq), [4][BN] float2
-  float2* red = reinterpret_cast<float2*>(smem + STAGES * (A_STAGE + B_STAGE) + 16384);
+  float2* red = reinterpret_cast<float2*>(smem + STAGES * (A_STAGE + B_STAGE) + 16384 + IN_BYTES);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * (A_STAGE + B_STAGE) + 16384 +
-                                               4 * BN * sizeof(float2));
+                                               IN_BYTES + 4 * BN * sizeof(float2));
   uint64_t* empty = full + STAGES;
   uint64_t* tfull = empty + STAGES;  // [2]
   uint64_t* tempty = tfull + 2;      // [2]
@@ -91,7 +168,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
-      mbar_init(&full[s], (MODE == MODE_TMA || MODE == MODE_IM2COL) ? 1 : 4 + 1);
+      mbar_init(&full[s], MODE == MODE_GATHER ? 4 + 1 : 1);
       mbar_init(&empty[s], 1);
     }
     for (int i = 0; i < 2; ++i) {
@@ -100,7 +177,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     fence_mbar_init();
     tma_prefetch_desc(&wmap);
-    if (MODE == MODE_TMA || MODE == MODE_IM2COL) tma_prefetch_desc(&amap);
+    if (MODE != MODE_GATHER) tma_prefetch_desc(&amap);
     tma_prefetch_desc(&ymap);
   }
   if (warp == 8) tmem_alloc(tslot, TMEM_COLS);
@@ -140,6 +217,30 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
           }
         }
+      } else if constexpr (MODE == MODE_STEM) {
+        // 7x7/2 stem over C=4 viewed as pixel PAIRS (16 B = 8 channels): a
+        // 7x4 stride-(2,1) conv, one 128-pixel x 16 B im2col box per tap,
+        // 8 taps per k-block written as K-adjacent no-swizzle core-matrix
+        // columns 2 KB apart (taps >= 28 repeat tap 27 against zero weights)
+        if (tid == 0) {
+          const int q = m0 % a.Q;
+          const int t = m0 / a.Q;
+          const int n = t / a.P;
+          const int wb = q - 2;
+          const int hb = (t - n * a.P) * 2 - 3;
+          for (int kb = 0; kb < a.kblocks; ++kb, ++it) {
+            const uint32_t s = it % STAGES;
+            if (it >= STAGES) mbar_wait(&empty[s], ((it / STAGES) - 1) & 1);
+            mbar_arrive_expect_tx(&full[s], A_STAGE + B_STAGE);
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+              const int tap = min(kb * 8 + u, 27);
+              tma_load_im2col_4d(sA + s * A_STAGE + u * 2048, &amap, &full[s], 0, wb, hb, n,
+                                 uint16_t(tap & 3), uint16_t(tap >> 2));
+            }
+            tma_load_2d(sB + s * B_STAGE, &wmap, &full[s], kb * BK, n0);
+          }
+        }
       } else if constexpr (MODE == MODE_TMA) {
         if (tid == 0) {
           for (int kb = 0; kb < a.kblocks; ++kb, ++it) {
@@ -151,10 +252,10 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
         }
       } else {
-        constexpr int ROWS = MODE == MODE_GATHER ? 8 : 16;
-        constexpr int RSTEP = MODE == MODE_GATHER ? 16 : 8;
-        const int part = MODE == MODE_GATHER ? (tid & 7) : (tid & 15);
-        const int row0 = MODE == MODE_GATHER ? (tid >> 3) : (tid >> 4);
+        constexpr int ROWS = 8;
+        constexpr int RSTEP = 16;
+        const int part = tid & 7;
+        const int row0 = tid >> 3;
         // Per tile, once: each row's input base pointer (top-left tap, may
         // point into the padding) and a validity mask: bits [0,R) say which
         // filter rows land inside the image, bits [8,8+S) which columns.
@@ -181,10 +282,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         // swizzled smem destination of (row, part): the XOR term is constant
         // per thread because every row this thread owns has the same row & 7
-        const uint32_t dst_thread = MODE == MODE_GATHER
-                                        ? uint32_t(row0 * 128 + ((part ^ (row0 & 7)) << 4))
-                                        : uint32_t(row0 * 128 + (((part >> 1) ^ (row0 & 7)) << 4) +
-                                                   (part & 1) * 8);
+        const uint32_t dst_thread = uint32_t(row0 * 128 + ((part ^ (row0 & 7)) << 4));
         const int cpt = a.C >> 6;  // 64-channel slices per tap (gather mode)
         int tap = 0, c0 = 0;        // gather-mode k-block -> (tap, channel slice)
         for (int kb = 0; kb < a.kblocks; ++kb, ++it) {
@@ -195,7 +293,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             tma_load_2d(sB + s * B_STAGE, &wmap, &full[s], kb * BK, n0);
           }
           const uint32_t dstA = sA + s * A_STAGE + dst_thread;
-          if constexpr (MODE == MODE_GATHER) {
+          {
             const int r = tap / a.S, sx = tap - r * a.S;
             const long long off = (long long)(r * a.W + sx) * a.C + c0 + part * 8;
             const uint32_t need = (1u << r) | (1u << (8 + sx));
@@ -208,16 +306,6 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (c0 == a.C) {
               c0 = 0;
               ++tap;
-            }
-          } else {
-            const int t = kb * 16 + part;
-            const int r = t / a.S, sx = t - r * a.S;
-            const uint32_t need = t < a.taps ? (1u << r) | (1u << (8 + sx)) : 0xFFFFFFFFu;
-            const long long off = (long long)(r * a.W + sx) * 4;
-#pragma unroll
-            for (int i = 0; i < ROWS; ++i) {
-              const bool ok = (vm[i] & need) == need;
-              cp_async_8(dstA + i * (RSTEP * 128), ok ? rowp[i] + off : a.x, ok);
             }
           }
           (void)cpt;
@@ -234,7 +322,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
       }
     }
-    if constexpr (MODE == MODE_GATHER || MODE == MODE_STEM) {
+    if constexpr (MODE == MODE_GATHER) {
       // drain: signal the last LAG stages
       cp_async_wait<0>();
       fence_proxy_async_smem();
@@ -247,6 +335,39 @@ __global__ void __launch_bounds__(kThreads, 1)
   } else if (warp < 8) {
     // ============================ epilogue =============================
     const int quarter = warp & 3;  // TMEM lanes [32*quarter, 32*quarter+32)
+    // fused operands: t0 = add / add_mask (pooled) / xc, t1 = out_mask
+    constexpr int NOPS = ev_operands(EV);
+    constexpr uint32_t SLOT = NOPS * 2048u;
+    constexpr uint32_t NSLOTS = NOPS ? EPI_RING_WARP / SLOT : 1;  // 12 or 6
+    const uint32_t ring = sIn + quarter * EPI_RING_WARP;
+    constexpr int CH = BN / 32;  // chunks per tile
+    const bf16* src0 = static_cast<const bf16*>(
+        EV == EV_BN_BWD ? a.e.xc : (EV == EV_POOL ? a.e.add_mask : a.e.add));
+    const bf16* src1 = static_cast<const bf16*>(a.e.out_mask);
+    // stage this warp's chunk number e (tile = first + (e / CH) * grid, j = e % CH)
+    // with cp.async: 4 x 16 B per lane per operand, 8 full rows per instruction,
+    // rows past M zero-filled; one commit group per chunk (possibly empty)
+    auto prefetch = [&](uint32_t e) {
+      const int tile_ = blockIdx.x + int(e / CH) * gridDim.x;
+      if (tile_ < a.tiles) {
+        const uint32_t sb = ring + (e % NSLOTS) * SLOT;
+        const int pm = (tile_ / a.n_tiles) * BM + quarter * 32;
+        const int pc = (tile_ % a.n_tiles) * BN + int(e % CH) * 32;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const int r = i * 8 + (lane >> 2), u = lane & 3;
+          const bool ok = pm + r < a.M;
+          const int64_t go = int64_t(ok ? pm + r : 0) * a.K + pc + u * 8;
+          const uint32_t so = r * 64 + ((u ^ ((r >> 1) & 3)) << 4);
+          cp_async_16(sb + so, src0 + go, ok);
+          if (NOPS == 2) cp_async_16(sb + 2048 + so, src1 + go, ok);
+        }
+      }
+      cp_async_commit();
+    };
+    if constexpr (FUSED)
+      for (uint32_t e = 0; e + 1 < NSLOTS; ++e) prefetch(e);
+    uint32_t ec = 0;  // chunks consumed by this warp
     uint32_t lt = 0;
     for (int tile = blockIdx.x; tile < a.tiles; tile += gridDim.x, ++lt) {
       const int m0 = (tile / a.n_tiles) * BM;
@@ -256,24 +377,93 @@ __global__ void __launch_bounds__(kThreads, 1)
       tc_fence_after();
       const uint32_t stage_base = sOut + quarter * 4096;
 #pragma unroll 1
-      for (int j = 0; j < BN / 32; ++j) {
+      for (int j = 0; j < BN / 32; ++j, ++ec) {
+        // the slot refilled here was consumed (and __syncwarp'ed) last chunk
+        if constexpr (FUSED) prefetch(ec + NSLOTS - 1);
         float v[32];
         tmem_ld_32x32b_x32(tmem + (uint32_t(quarter * 32) << 16) + acc * ACC_COLS + j * 32, v);
         const int col = n0 + j * 32;
+        const uint32_t sb = ring + (ec % NSLOTS) * SLOT;
+        if constexpr (FUSED) {
+          cp_async_wait<NSLOTS - 1>();  // this chunk's group is the oldest committed
+          __syncwarp();
+        }
+        if constexpr (EV == EV_POOL) {
+          // pooled head gradient (read through L1) masked by add_mask, added in fp32
+          const int64_t m = int64_t(m0) + quarter * 32 + lane;
+          const bf16* pool = static_cast<const bf16*>(a.e.add);
+          const float inv = 1.f / float(a.e.pool_hw);
+          const int64_t prow = (m < a.M ? m : 0) / a.e.pool_hw;
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            float g[8], mk[8];
+            unpack8f(ldg16(pool + prow * a.K + col + u * 8), g);
+            unpack8f(ld_row16(sb, lane, u), mk);
+#pragma unroll
+            for (int i = 0; i < 8; ++i) v[u * 8 + i] += mk[i] > 0.f ? g[i] * inv : 0.f;
+          }
+        }
+        // pack to bf16 (packed epilogue ops on top), stage for the TMA store
+        uint4 pk[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          pk[u].x = pack_bf16x2(v[u * 8 + 0], v[u * 8 + 1]);
+          pk[u].y = pack_bf16x2(v[u * 8 + 2], v[u * 8 + 3]);
+          pk[u].z = pack_bf16x2(v[u * 8 + 4], v[u * 8 + 5]);
+          pk[u].w = pack_bf16x2(v[u * 8 + 6], v[u * 8 + 7]);
+        }
+        if constexpr (EV == EV_ADD || EV == EV_ADD_OM) {
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const uint4 ad = ld_row16(sb, lane, u);
+            pk[u].x = add_bf16x2(pk[u].x, ad.x);
+            pk[u].y = add_bf16x2(pk[u].y, ad.y);
+            pk[u].z = add_bf16x2(pk[u].z, ad.z);
+            pk[u].w = add_bf16x2(pk[u].w, ad.w);
+          }
+        }
+        if constexpr (EV == EV_ADD_OM || EV == EV_POOL) {
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const uint4 om = ld_row16(sb + 2048, lane, u);
+            pk[u].x &= pos_mask2(om.x);
+            pk[u].y &= pos_mask2(om.y);
+            pk[u].z &= pos_mask2(om.z);
+            pk[u].w &= pos_mask2(om.w);
+          }
+        }
+        if constexpr (EV == EV_BN_BWD) {
+          // ReLU mask of the forward output relu(bn(xc)) = bf16(max(xc*sc+sh, 0)):
+          // positive iff xc*sc+sh > 2^-134 (the bf16 rounding threshold), with
+          // k_bn_apply<0>'s exact scale/shift arithmetic
+          const float my_sc = __ldg(a.e.invstd + col + lane) * __ldg(a.e.gamma + col + lane);
+          const float my_sh = fmaf(-__ldg(a.e.mean + col + lane), my_sc, __ldg(a.e.beta + col + lane));
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            float x[8];
+            unpack8f(ld_row16(sb, lane, u), x);
+            uint32_t bits = 0;
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+              const float sc = __shfl_sync(0xffffffffu, my_sc, u * 8 + i);
+              const float sh = __shfl_sync(0xffffffffu, my_sh, u * 8 + i);
+              bits |= (fmaf(x[i], sc, sh) > 0x1p-134f ? 0xFFFFu : 0u) << (16 * (i & 1));
+              if (i & 1) {
+                (&pk[u].x)[i >> 1] &= bits;
+                bits = 0;
+              }
+            }
+          }
+        }
+        if constexpr (FUSED) __syncwarp();  // every lane has read the slot before it is refilled
         const uint32_t buf = stage_base + (j & 1) * 2048;
         // the TMA store that last read this buffer (two chunks ago) is done
         if (lane == 0) bulk_wait_read<1>();
         __syncwarp();
         // row `lane` = 64 B = 4 chunks of 16 B; 64B swizzle: chunk ^= (row>>1)&3
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          uint4 pk;
-          pk.x = pack_bf16x2(v[u * 8 + 0], v[u * 8 + 1]);
-          pk.y = pack_bf16x2(v[u * 8 + 2], v[u * 8 + 3]);
-          pk.z = pack_bf16x2(v[u * 8 + 4], v[u * 8 + 5]);
-          pk.w = pack_bf16x2(v[u * 8 + 6], v[u * 8 + 7]);
-          st_shared_v4(buf + lane * 64 + ((u ^ ((lane >> 1) & 3)) << 4), pk);
-        }
+        for (int u = 0; u < 4; ++u)
+          st_shared_v4(buf + lane * 64 + ((u ^ ((lane >> 1) & 3)) << 4), pk[u]);
         fence_proxy_async_smem();
         __syncwarp();
         if (lane == 0 && col < a.K) {
@@ -282,25 +472,32 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         if (a.stats != nullptr) {
           // column `lane` of this 32x32 block, from the staged bf16 values
-          // (exactly what BN will read back); rows past M are zeros.
+          // (exactly what is stored); rows past M are zeros.
           const uint32_t cbyte = (uint32_t(lane) & 7u) * 2u;
           const uint32_t c16 = uint32_t(lane) >> 3;
           float sum = 0.f, sq = 0.f;
 #pragma unroll 8
           for (int rr = 0; rr < 32; ++rr) {
+            const uint32_t off = rr * 64 + ((c16 ^ ((rr >> 1) & 3)) << 4) + cbyte;
             uint16_t h;
-            asm volatile("ld.shared.u16 %0, [%1];"
-                         : "=h"(h)
-                         : "r"(buf + rr * 64 + ((c16 ^ ((rr >> 1) & 3)) << 4) + cbyte));
+            asm volatile("ld.shared.u16 %0, [%1];" : "=h"(h) : "r"(buf + off));
             const float f = __bfloat162float(__ushort_as_bfloat16(h));
             sum += f;
-            sq = fmaf(f, f, sq);
+            if constexpr (EV == EV_BN_BWD) {
+              // (sum g, sum g*xc): xc from the operand ring (same layout)
+              uint16_t hx;
+              asm volatile("ld.shared.u16 %0, [%1];" : "=h"(hx) : "r"(sb + off));
+              sq = fmaf(f, __bfloat162float(__ushort_as_bfloat16(hx)), sq);
+            } else {
+              sq = fmaf(f, f, sq);
+            }
           }
           red[quarter * BN + j * 32 + lane] = make_float2(sum, sq);
         }
+        if constexpr (EV == EV_BN_BWD) __syncwarp();  // ring slot read by the stats pass
       }
       if (a.stats != nullptr) {
-        // combine the four row quarters -> one (mean, M2) per channel per tile
+        // combine the four row quarters -> one partial per channel per tile
         asm volatile("bar.sync 1, 128;" ::: "memory");
         const int et = (warp - 4) * 32 + lane;
         const int n_rows = min(BM, a.M - m0);
@@ -311,9 +508,16 @@ __global__ void __launch_bounds__(kThreads, 1)
             S += red[qq * BN + c].x;
             Q += red[qq * BN + c].y;
           }
-          const float mu = S / float(n_rows);
-          if (n0 + c < a.K)
-            a.stats[size_t(m0 / BM) * a.K + n0 + c] = make_float2(mu, fmaxf(Q - S * mu, 0.f));
+          if (n0 + c < a.K) {
+            float2 out;
+            if (EV == EV_BN_BWD) {
+              out = make_float2(S, Q);
+            } else {
+              const float mu = S / float(n_rows);
+              out = make_float2(mu, fmaxf(Q - S * mu, 0.f));
+            }
+            a.stats[size_t(m0 / BM) * a.K + n0 + c] = out;
+          }
         }
         asm volatile("bar.sync 1, 128;" ::: "memory");
       }
@@ -338,7 +542,9 @@ __global__ void __launch_bounds__(kThreads, 1)
           tc_fence_after();
 #pragma unroll
           for (int k = 0; k < BK / 16; ++k) {
-            const uint64_t ad = umma_desc_sw128(sA + s * A_STAGE + k * 32);
+            const uint64_t ad = MODE == MODE_STEM
+                                    ? umma_desc_noswz(sA + s * A_STAGE + k * 4096, 2048, 128)
+                                    : umma_desc_sw128(sA + s * A_STAGE + k * 32);
             const uint64_t bd = umma_desc_sw128(sB + s * B_STAGE + k * 32);
             umma_bf16(d, ad, bd, idesc, (kb | k) != 0 ? 1u : 0u);
           }
@@ -356,10 +562,11 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == 8) tmem_dealloc(tmem, TMEM_COLS);
 }
 
-template <int BN, int STAGES>
+template <int BN, int STAGES, bool FUSED>
 constexpr size_t conv_smem_bytes() {
   return size_t(STAGES) * (BM * 128 + BN * 128) + 16384 /*epilogue staging*/ +
-         4 * BN * 8 /*stats scratch*/ + 1024 /*align*/ + 256 /*barriers*/;
+         (FUSED ? 4 * EPI_RING_WARP : 0) /*epilogue operand ring*/ + 4 * BN * 8 /*stats scratch*/ +
+         1024 /*align*/ + 256 /*barriers*/;
 }
 
 PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
@@ -420,6 +627,23 @@ bool encode_im2col(CUtensorMap* m, const void* x, const ConvPlan& cp) {
             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+// Stem im2col map over the C=4 input viewed as [N][H][W/2][8] (pixel pairs,
+// 16 B): traversal stride (w 1, h 2), box corners give exactly P x Q output
+// positions (w from -2, h from -3), one 16 B channel box per pixel, no swizzle.
+bool encode_stem_im2col(CUtensorMap* m, const void* x, const ConvPlan& cp) {
+  auto fn = encode_im2col_fn();
+  if (!fn) return false;
+  const int W2 = cp.W / 2;
+  cuuint64_t dims[4] = {8, cuuint64_t(W2), cuuint64_t(cp.H), cuuint64_t(cp.N)};
+  cuuint64_t strides[3] = {16, cuuint64_t(W2) * 16, cuuint64_t(cp.H) * W2 * 16};
+  int lower[2] = {-2, -3};
+  int upper[2] = {cp.Q - W2 - 2, 2 * cp.P - cp.H - 3};
+  cuuint32_t estr[4] = {1, 1, 2, 1};
+  return fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(x), dims, strides, lower,
+            upper, 8, BM, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+            CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 // Output map: [M rows][K cols] bf16, 32x32 box, 64-byte swizzle (epilogue
 // staging layout), out-of-range rows/cols clipped by the TMA unit.
 bool encode_out(CUtensorMap* m, void* y, uint64_t cols, uint64_t rows) {
@@ -456,10 +680,12 @@ int num_sms() {
   return n;
 }
 
-template <int BN, int STAGES, int MODE>
-cudaError_t launch(const ConvPlan& cp, const void* x, void* y, float* stats, cudaStream_t st) {
-  auto kern = k_conv_fwd<BN, STAGES, MODE>;
-  constexpr size_t smem = conv_smem_bytes<BN, STAGES>();
+template <int BN, int STAGES, int MODE, int EV>
+cudaError_t launch(const ConvPlan& cp, const void* x, void* y, float* stats,
+                   const ConvEpilogue& epi, cudaStream_t st) {
+  auto kern = k_conv_fwd<BN, STAGES, MODE, EV>;
+  constexpr size_t smem = conv_smem_bytes<BN, STAGES, EV != EV_STORE>();
+  static_assert(smem <= 227 * 1024, "shared memory");
   static bool attr = false;
   if (!attr) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
@@ -477,12 +703,15 @@ cudaError_t launch(const ConvPlan& cp, const void* x, void* y, float* stats, cud
   a.n_tiles = (cp.K + BN - 1) / BN;
   a.tiles = ((a.M + BM - 1) / BM) * a.n_tiles;
   a.stats = reinterpret_cast<float2*>(stats);
+  a.e = epi;
   alignas(64) CUtensorMap amap;
   alignas(64) CUtensorMap ymap;
   if (MODE == MODE_TMA) {
     if (!encode_2d(&amap, x, uint64_t(cp.C), uint64_t(a.M), BM)) return cudaErrorInvalidValue;
   } else if (MODE == MODE_IM2COL) {
     if (!encode_im2col(&amap, x, cp)) return cudaErrorInvalidValue;
+  } else if (MODE == MODE_STEM) {
+    if (!encode_stem_im2col(&amap, x, cp)) return cudaErrorInvalidValue;
   } else {
     amap = *reinterpret_cast<const CUtensorMap*>(cp.wmap);  // unused
   }
@@ -498,9 +727,12 @@ cudaError_t launch(const ConvPlan& cp, const void* x, void* y, float* stats, cud
 int conv_plan_init(ConvPlan* cp, const void* w) {
   if (cp->C % 64 != 0 && cp->C != 4) return 1;
   if (cp->K % 8 != 0) return 1;
+  // the C=4 stem path is the 7x7/2 pad-3 ResNet stem over an even width
+  if (cp->C == 4 && (cp->R != 7 || cp->S != 7 || cp->stride != 2 || cp->pad != 3 || (cp->W & 1)))
+    return 1;
   cp->P = (cp->H + 2 * cp->pad - cp->R) / cp->stride + 1;
   cp->Q = (cp->W + 2 * cp->pad - cp->S) / cp->stride + 1;
-  cp->kdim = cp->C == 4 ? ((cp->R * cp->S * 4 + 63) / 64) * 64 : cp->R * cp->S * cp->C;
+  cp->kdim = cp->C == 4 ? 256 : cp->R * cp->S * cp->C;
   cp->bn = cp->K <= 64 ? 64 : (cp->K <= 128 ? 128 : 256);
   if (!encode_fn()) return 2;
   return encode_2d(reinterpret_cast<CUtensorMap*>(cp->wmap), w, uint64_t(cp->kdim),
@@ -509,27 +741,73 @@ int conv_plan_init(ConvPlan* cp, const void* w) {
              : 3;
 }
 
+int conv_plan_set_tile_n(ConvPlan* cp, int bn, const void* w) {
+  if (bn != 64 && bn != 128 && bn != 256) return 1;
+  if (cp->C == 4 || cp->K % bn != 0) return 1;
+  cp->bn = bn;
+  return encode_2d(reinterpret_cast<CUtensorMap*>(cp->wmap), w, uint64_t(cp->kdim),
+                   uint64_t(cp->K), uint32_t(cp->bn))
+             ? 0
+             : 3;
+}
+
 cudaError_t conv_forward(const ConvPlan& cp, const void* x, void* y, float* stats,
-                         cudaStream_t st) {
+                         cudaStream_t st, const ConvEpilogue* epi) {
+  ConvEpilogue e{};
+  if (epi != nullptr) e = *epi;
+  if (e.mode != EPI_STORE && (cp.K % 32 != 0 || cp.C == 4)) return cudaErrorInvalidValue;
+  if (e.mode == EPI_BN_BWD && (!e.xc || !e.mean || !e.invstd || !e.gamma || !e.beta))
+    return cudaErrorInvalidValue;
   const bool stem = cp.C == 4;
   const bool tma_a = !stem && cp.R == 1 && cp.S == 1 && cp.stride == 1 && cp.pad == 0;
   const bool use_gather = gather_forced();
+  if (e.mode != EPI_STORE) {
+    // fused epilogues (backward dgrad): fewer stages pay for the operand ring;
+    // N tiles are capped at 128 (delta_conv_set_tile_n)
+    int ev;
+    if (e.mode == EPI_BN_BWD) {
+      ev = EV_BN_BWD;
+    } else if (e.pool_hw) {
+      if (!e.add || !e.add_mask || !e.out_mask) return cudaErrorInvalidValue;
+      ev = EV_POOL;
+    } else {
+      if (!e.add) return cudaErrorInvalidValue;
+      ev = e.out_mask ? EV_ADD_OM : EV_ADD;
+    }
+    if (cp.bn != 64 && cp.bn != 128) return cudaErrorInvalidValue;
+#define DELTA_FUSED(EVV)                                                                    \
+  case EVV:                                                                                 \
+    if (cp.bn == 64)                                                                        \
+      return tma_a ? launch<64, 4, MODE_TMA, EVV>(cp, x, y, stats, e, st)                    \
+                   : launch<64, 4, MODE_IM2COL, EVV>(cp, x, y, stats, e, st);                \
+    return tma_a ? launch<128, 3, MODE_TMA, EVV>(cp, x, y, stats, e, st)                     \
+                 : launch<128, 3, MODE_IM2COL, EVV>(cp, x, y, stats, e, st);
+    switch (ev) {
+      DELTA_FUSED(EV_ADD)
+      DELTA_FUSED(EV_ADD_OM)
+      DELTA_FUSED(EV_POOL)
+      DELTA_FUSED(EV_BN_BWD)
+      default:
+        return cudaErrorInvalidValue;
+    }
+#undef DELTA_FUSED
+  }
   switch (cp.bn) {
     case 64:
-      return stem ? launch<64, 8, MODE_STEM>(cp, x, y, stats, st)
-             : tma_a ? launch<64, 8, MODE_TMA>(cp, x, y, stats, st)
-             : use_gather ? launch<64, 8, MODE_GATHER>(cp, x, y, stats, st)
-                          : launch<64, 8, MODE_IM2COL>(cp, x, y, stats, st);
+      return stem ? launch<64, 8, MODE_STEM, EV_STORE>(cp, x, y, stats, e, st)
+             : tma_a ? launch<64, 8, MODE_TMA, EV_STORE>(cp, x, y, stats, e, st)
+             : use_gather ? launch<64, 8, MODE_GATHER, EV_STORE>(cp, x, y, stats, e, st)
+                          : launch<64, 8, MODE_IM2COL, EV_STORE>(cp, x, y, stats, e, st);
     case 128:
-      return stem ? launch<128, 6, MODE_STEM>(cp, x, y, stats, st)
-             : tma_a ? launch<128, 6, MODE_TMA>(cp, x, y, stats, st)
-             : use_gather ? launch<128, 6, MODE_GATHER>(cp, x, y, stats, st)
-                          : launch<128, 6, MODE_IM2COL>(cp, x, y, stats, st);
+      return stem ? launch<128, 6, MODE_STEM, EV_STORE>(cp, x, y, stats, e, st)
+             : tma_a ? launch<128, 6, MODE_TMA, EV_STORE>(cp, x, y, stats, e, st)
+             : use_gather ? launch<128, 6, MODE_GATHER, EV_STORE>(cp, x, y, stats, e, st)
+                          : launch<128, 6, MODE_IM2COL, EV_STORE>(cp, x, y, stats, e, st);
     default:
-      return stem ? launch<256, 4, MODE_STEM>(cp, x, y, stats, st)
-             : tma_a ? launch<256, 4, MODE_TMA>(cp, x, y, stats, st)
-             : use_gather ? launch<256, 4, MODE_GATHER>(cp, x, y, stats, st)
-                          : launch<256, 4, MODE_IM2COL>(cp, x, y, stats, st);
+      return stem ? launch<256, 4, MODE_STEM, EV_STORE>(cp, x, y, stats, e, st)
+             : tma_a ? launch<256, 4, MODE_TMA, EV_STORE>(cp, x, y, stats, e, st)
+             : use_gather ? launch<256, 4, MODE_GATHER, EV_STORE>(cp, x, y, stats, e, st)
+                          : launch<256, 4, MODE_IM2COL, EV_STORE>(cp, x, y, stats, e, st);
   }
 }
 

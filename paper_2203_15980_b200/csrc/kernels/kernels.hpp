@@ -12,19 +12,44 @@ struct ConvPlan {
   int P, Q, kdim, bn;
   alignas(64) unsigned char wmap[128];  // CUtensorMap over the [K][kdim] weight matrix
 };
+// Fused epilogues (the backward pass runs input-gradient convolutions through
+// the same kernel with transposed/flipped weights):
+//   EPI_STORE    y = bf16(acc)                                  [+ BN-stats partials]
+//   EPI_ADD_MASK y = bf16((acc + add') * [out_mask > 0]),  add' = add or pooled
+//                add / pool_hw, times [add_mask > 0]             (gradient adds)
+//   EPI_BN_BWD   y = g = bf16(acc) * [relu(bn(xc)) > 0], partials (sum g,
+//                sum g*xc) per 128-row tile                     (BN+ReLU backward)
+constexpr int EPI_STORE = 0, EPI_ADD_MASK = 1, EPI_BN_BWD = 2;
+struct ConvEpilogue {
+  int mode;
+  int pool_hw;
+  const void* add;
+  const void* add_mask;
+  const void* out_mask;
+  const void* xc;
+  const float* mean;
+  const float* invstd;
+  const float* gamma;
+  const float* beta;
+};
 // 0 ok, 1 unsupported shape, 2 no driver entry point, 3 tensor-map encode failed
 int conv_plan_init(ConvPlan* cp, const void* w);
+// choose the N tile (64/128/256, dividing K; fused epilogues need <= 128)
+int conv_plan_set_tile_n(ConvPlan* cp, int bn, const void* w);
 // stats (optional, nullptr = off): [ceil(M/128)][K] float2 (mean, M2) of the
 // bf16 outputs of each 128-row tile — the BN statistics partials.
 cudaError_t conv_forward(const ConvPlan& cp, const void* x, void* y, float* stats,
-                         cudaStream_t st);
+                         cudaStream_t st, const ConvEpilogue* epi = nullptr);
 
 // ---- batch norm / elementwise / pooling (bn_pool.cu) ----
 int64_t bn_workspace_floats(int64_t M, int C);
 cudaError_t bn_stats(const void* x, int64_t M, int C, float* ws, float* mean, float* invstd,
                      float eps, float* run_mean, float* run_var, float momentum, cudaStream_t st);
 // Finish BN statistics from per-tile (mean, M2) partials of `rows_per_part`
-// rows each (the conv epilogue's), merged in a fixed order.
+// rows each (the conv epilogue's), merged in a fixed order.  `partials` holds
+// stats_partials_floats(M, C, rows_per_part) floats (the partials, then the
+// grouping pass's scratch).
+int64_t stats_partials_floats(int64_t M, int C, int rows_per_part);
 cudaError_t bn_stats_from_partials(const float* partials, int64_t M, int C, int rows_per_part,
                                    float* mean, float* invstd, float eps, float* run_mean,
                                    float* run_var, float momentum, cudaStream_t st);
@@ -43,6 +68,15 @@ cudaError_t bn_backward(const void* up, int pool_hw, const void* mask, const voi
                         int64_t M, int C, const float* mean, const float* invstd,
                         const float* gamma, float* dgamma, float* dbeta, float* ws,
                         cudaStream_t st);
+
+// BN(+ReLU) backward whose reductions were fused into the producing conv's
+// EPI_BN_BWD epilogue: `partials` = per-tile (sum g, sum g*x) of g (already
+// masked), sized stats_partials_floats(M, C, rows_per_part).  Writes dgamma,
+// dbeta and dx = BN-backward(g, x).
+cudaError_t bn_backward_from_partials(const float* partials, int rows_per_part, const void* g,
+                                      const void* x, void* dx, int64_t M, int C,
+                                      const float* mean, const float* invstd, const float* gamma,
+                                      float* dgamma, float* dbeta, cudaStream_t st);
 
 // out = (a + g) * [out_mask > 0], g = up * [up_mask > 0] (up full or pooled as
 // above; a null mask means no masking)

@@ -150,6 +150,19 @@ __device__ __forceinline__ uint64_t umma_desc_sw128(uint32_t smem_addr) {
   return d;
 }
 
+// K-major operand, no swizzle: 8-row x 16 B core matrices stored as 128 B
+// blocks; `lbo` = byte distance between core matrices adjacent in K, `sbo` =
+// between 8-row groups adjacent in M/N.
+__device__ __forceinline__ uint64_t umma_desc_noswz(uint32_t smem_addr, uint32_t lbo,
+                                                    uint32_t sbo) {
+  uint64_t d = 0;
+  d |= static_cast<uint64_t>((smem_addr & 0x3FFFF) >> 4);
+  d |= static_cast<uint64_t>((lbo >> 4) & 0x3FFF) << 16;
+  d |= static_cast<uint64_t>((sbo >> 4) & 0x3FFF) << 32;
+  d |= static_cast<uint64_t>(1) << 46;  // version; layout bits 61-63 = 0 (none)
+  return d;
+}
+
 // kind::f16 instruction descriptor: BF16 x BF16 -> F32, both K-major.
 __host__ __device__ constexpr uint32_t umma_idesc_bf16(int M, int N) {
   return (1u << 4)            // D format F32

@@ -30,6 +30,7 @@ inline cudaStream_t S(void* p) { return static_cast<cudaStream_t>(p); }
 
 struct delta_conv {
   delta_k::ConvPlan plan;
+  const void* weight = nullptr;
 };
 
 struct delta_swap {
@@ -51,6 +52,7 @@ delta_status delta_conv_create(int32_t N, int32_t H, int32_t W, int32_t C, int32
   std::memset(&c->plan, 0, sizeof(c->plan));
   c->plan.N = N; c->plan.H = H; c->plan.W = W; c->plan.C = C; c->plan.K = K;
   c->plan.R = R; c->plan.S = S_; c->plan.stride = stride; c->plan.pad = pad;
+  c->weight = weight;
   int rc = delta_k::conv_plan_init(&c->plan, weight);
   if (rc != 0) {
     delete c;
@@ -66,6 +68,35 @@ delta_status delta_conv_create(int32_t N, int32_t H, int32_t W, int32_t C, int32
 delta_status delta_conv_forward(const delta_conv* c, const void* x, void* y, float* stats,
                                 void* stream) {
   return cuda_status(delta_k::conv_forward(c->plan, x, y, stats, S(stream)), "conv_forward");
+}
+
+static_assert(sizeof(delta_conv_epilogue) == sizeof(delta_k::ConvEpilogue),
+              "C-ABI epilogue struct mirrors the kernel's");
+
+delta_status delta_conv_forward_ex(const delta_conv* c, const void* x, void* y, float* stats,
+                                   const delta_conv_epilogue* epi, void* stream) {
+  delta_k::ConvEpilogue e{};
+  if (epi) {
+    e.mode = epi->mode;
+    e.pool_hw = epi->pool_hw;
+    e.add = epi->add;
+    e.add_mask = epi->add_mask;
+    e.out_mask = epi->out_mask;
+    e.xc = epi->xc;
+    e.mean = epi->mean;
+    e.invstd = epi->invstd;
+    e.gamma = epi->gamma;
+    e.beta = epi->beta;
+  }
+  return cuda_status(delta_k::conv_forward(c->plan, x, y, stats, S(stream), &e), "conv_forward_ex");
+}
+
+delta_status delta_conv_set_tile_n(delta_conv* c, int32_t tile_n) {
+  const int rc = delta_k::conv_plan_set_tile_n(&c->plan, tile_n, c->weight);
+  if (rc == 0) return DELTA_OK;
+  delta_rt::set_error(rc == 1 ? "conv: tile_n must be 64/128/256 and divide K"
+                              : "conv: tensor map encode failed");
+  return rc == 1 ? DELTA_E_UNSUPPORTED : DELTA_E_CUDA;
 }
 
 delta_status delta_conv_geometry(const delta_conv* c, int32_t* P, int32_t* Q, int32_t* kdim,
@@ -86,6 +117,10 @@ delta_status delta_bn_stats(const void* x, int64_t M, int32_t C, float* ws, floa
                             void* stream) {
   return cuda_status(delta_k::bn_stats(x, M, C, ws, mean, invstd, eps, rm, rv, mom, S(stream)),
                      "bn_stats");
+}
+
+int64_t delta_stats_partials_floats(int64_t M, int32_t C, int32_t rows_per_part) {
+  return delta_k::stats_partials_floats(M, C, rows_per_part);
 }
 
 delta_status delta_bn_stats_from_partials(const float* partials, int64_t M, int32_t C,
@@ -113,6 +148,15 @@ delta_status delta_bn_backward(const void* up, int32_t pool_hw, const void* mask
   return cuda_status(delta_k::bn_backward(up, pool_hw, mask, x, dx, M, C, mean, invstd, gamma,
                                           dgamma, dbeta, ws, S(stream)),
                      "bn_backward");
+}
+
+delta_status delta_bn_backward_from_partials(const float* partials, const void* g, const void* x,
+                                             void* dx, int64_t M, int32_t C, const float* mean,
+                                             const float* invstd, const float* gamma,
+                                             float* dgamma, float* dbeta, void* stream) {
+  return cuda_status(delta_k::bn_backward_from_partials(partials, 128, g, x, dx, M, C, mean, invstd,
+                                                        gamma, dgamma, dbeta, S(stream)),
+                     "bn_backward_from_partials");
 }
 
 delta_status delta_add_grad(const void* a, const void* up, int32_t pool_hw, const void* up_mask,

@@ -13,7 +13,11 @@ P = C.POINTER
 _SIGS = {
     "delta_conv_create": (i32, [i32] * 9 + [vp, P(vp)]),
     "delta_conv_forward": (i32, [vp, vp, vp, vp, vp]),
+    "delta_stats_partials_floats": (i64, [i64, i32, i32]),
     "delta_bn_stats_from_partials": (i32, [vp, i64, i32, i32, vp, vp, f32, vp, vp, f32, vp]),
+    "delta_conv_forward_ex": (i32, [vp, vp, vp, vp, vp, vp]),
+    "delta_conv_set_tile_n": (i32, [vp, i32]),
+    "delta_bn_backward_from_partials": (i32, [vp, vp, vp, vp, i64, i32, vp, vp, vp, vp, vp, vp]),
     "delta_conv_geometry": (i32, [vp, P(i32), P(i32), P(i32), P(i32)]),
     "delta_conv_destroy": (None, [vp]),
     "delta_bn_workspace_floats": (i64, [i64, i32]),
@@ -52,6 +56,15 @@ def _count(n: int):
     LAUNCHES[0] += n
 
 
+EPI_STORE, EPI_ADD_MASK, EPI_BN_BWD = 0, 1, 2
+
+
+class ConvEpilogue(C.Structure):
+    """delta_conv_epilogue (include/delta/delta_kernels.h)."""
+    _fields_ = [("mode", i32), ("pool_hw", i32), ("add", vp), ("add_mask", vp), ("out_mask", vp),
+                ("xc", vp), ("mean", vp), ("invstd", vp), ("gamma", vp), ("beta", vp)]
+
+
 class Conv:
     """tcgen05 implicit-GEMM convolution with a cached weight TMA descriptor."""
 
@@ -69,26 +82,82 @@ class Conv:
         check(lib.delta_conv_forward(self._h, x_ptr, y_ptr, stats_ptr, stream))
         _count(1)
 
+    def set_tile_n(self, tile_n: int):
+        check(lib.delta_conv_set_tile_n(self._h, tile_n))
+        self.tile_n = tile_n
+
+    def add_mask(self, x_ptr, y_ptr, stream, add=None, pool_hw=0, add_mask=None, out_mask=None):
+        """y = (conv(x) + add') * [out_mask > 0]; add' = add, or the pooled add
+        / pool_hw * [add_mask > 0] (add_mask is only read with a pooled add)."""
+        e = ConvEpilogue(EPI_ADD_MASK, pool_hw, add, add_mask, out_mask, None, None, None, None,
+                         None)
+        check(lib.delta_conv_forward_ex(self._h, x_ptr, y_ptr, None, C.byref(e), stream))
+        _count(1)
+
+    def bn_bwd(self, x_ptr, g_ptr, partials_ptr, xc, mean, invstd, gamma, beta, stream):
+        """g = bf16(conv(x)) * [relu(bn(xc)) > 0] and per-tile (sum g, sum g*xc)."""
+        e = ConvEpilogue(EPI_BN_BWD, 0, None, None, None, xc, mean, invstd, gamma, beta)
+        check(lib.delta_conv_forward_ex(self._h, x_ptr, g_ptr, partials_ptr, C.byref(e), stream))
+        _count(1)
+
     def __del__(self):
         if getattr(self, "_h", None) and lib is not None:
             lib.delta_conv_destroy(self._h)
             self._h = None
 
 
+STEM_KDIM = 256
+
+
+def pack_stem_weights(w_krsc, out=None):
+    """[K,7,7,4] stem weights -> the pixel-pair layout the C=4 conv path reads
+    ([K,256]; column (r*4+j)*8 + e*4 + c = W[k,r,2j+e-1,c], zero elsewhere;
+    include/delta/delta_kernels.h).  `w_krsc` and `out` are torch tensors on
+    the same device; returns `out`."""
+    import torch
+    K_ = w_krsc.shape[0]
+    if out is None:
+        out = torch.zeros(K_, STEM_KDIM, dtype=torch.bfloat16, device=w_krsc.device)
+    w8 = torch.zeros(K_, 7, 8, 4, dtype=out.dtype, device=w_krsc.device)
+    w8[:, :, 1:] = w_krsc                      # s' = s + 1; s' = 0 is the zero tap
+    out[:, :224].copy_(w8.reshape(K_, 224))    # [K,7,4(j),2(e),4(c)] row-major
+    out[:, 224:].zero_()
+    return out
+
+
 def bn_workspace_floats(M: int, C_: int) -> int:
     return lib.delta_bn_workspace_floats(M, C_)
 
 
+def _merge_launches(parts: int) -> int:
+    """Launches of a fixed-order partials merge (bn_pool.cu merge_partials /
+    bn_backward_from_partials): a grouping pass above 2*32 partials."""
+    return 2 if parts > 64 else 1
+
+
+def _chunks(M: int, C_: int) -> int:
+    """Number of reduction chunks of the streaming BN kernels (bn_pool.cu chunk_rows)."""
+    slices = max(1, C_ // 64)
+    chunks = max(1, (148 * 8) // slices)
+    rows = (M + chunks - 1) // chunks
+    rows = max(256, (rows + 31) // 32 * 32)
+    return (M + rows - 1) // rows
+
+
 def bn_stats(x, M, C_, ws, mean, invstd, eps, run_mean, run_var, momentum, stream):
     check(lib.delta_bn_stats(x, M, C_, ws, mean, invstd, eps, run_mean, run_var, momentum, stream))
-    _count(2)
+    _count(1 + _merge_launches(_chunks(M, C_)))
+
+
+def stats_partials_floats(M: int, C_: int, rows_per_part: int = 128) -> int:
+    return lib.delta_stats_partials_floats(M, C_, rows_per_part)
 
 
 def bn_stats_from_partials(partials, M, C_, mean, invstd, eps, run_mean, run_var, momentum,
                            stream, rows_per_part=128):
     check(lib.delta_bn_stats_from_partials(partials, M, C_, rows_per_part, mean, invstd, eps,
                                            run_mean, run_var, momentum, stream))
-    _count(1)
+    _count(_merge_launches((M + rows_per_part - 1) // rows_per_part))
 
 
 def bn_apply(mode, x, res, y, M, C_, mean, invstd, gamma, beta, mean2=None, invstd2=None,
@@ -102,6 +171,13 @@ def bn_backward(up, pool_hw, mask, x, dx, M, C_, mean, invstd, gamma, dgamma, db
     check(lib.delta_bn_backward(up, pool_hw, mask, x, dx, M, C_, mean, invstd, gamma, dgamma,
                                 dbeta, ws, stream))
     _count(3)
+
+
+def bn_backward_from_partials(partials, g, x, dx, M, C_, mean, invstd, gamma, dgamma, dbeta,
+                              stream):
+    check(lib.delta_bn_backward_from_partials(partials, g, x, dx, M, C_, mean, invstd, gamma,
+                                              dgamma, dbeta, stream))
+    _count(1 + _merge_launches((M + 127) // 128))
 
 
 def add_grad(a, up, pool_hw, up_mask, out_mask, out, M, C_, stream):

@@ -31,8 +31,8 @@ def resident_workspace_bytes(g: G.Graph, batch: int) -> int:
     buffers), maxpool argmax scratch, head gradients."""
     x = g.nodes[0].nbytes
     convs = [n for n in g.nodes if n.op == "conv"]
-    parts = 2 * max(((n.shape[0] * n.shape[1] * n.shape[2] + 127) // 128) * n.shape[3] * 8
-                    for n in convs)
+    parts = 2 * max((((n.shape[0] * n.shape[1] * n.shape[2] + 127) // 128) * 33 // 32 + 1)
+                    * n.shape[3] * 8 for n in convs)
     mp = next(n for n in g.nodes if n.op == "maxpool")
     return x + parts + mp.nbytes // 2 + batch * 1000 * 8
 

@@ -92,13 +92,19 @@ class Params:
             n = cs.cout * cs.k * cs.k * cs.cin
             self.wbf[name] = self.conv_bf16[off:off + n].view(cs.cout, cs.k, cs.k, cs.cin)
             off += n
-        # the stem kernel reads taps packed 4 channels each, K-dim padded to 64
+        # the stem kernel reads its weights in the pixel-pair layout
         self.stem_packed = {}
         for name, cs in g.convs.items():
             if cs.cin == 4:
-                kd = (cs.k * cs.k * 4 + 63) // 64 * 64
-                self.stem_packed[name] = torch.zeros(cs.cout, kd, dtype=torch.bfloat16,
+                self.stem_packed[name] = torch.zeros(cs.cout, K.STEM_KDIM, dtype=torch.bfloat16,
                                                      device=device)
+        # input-gradient (dgrad) weights of the stride-1 convs, run through our
+        # conv kernel: [C][R][S][K], W'[c][r][s][k] = W[k][R-1-r][S-1-s][c]
+        self.wd = {}
+        for name, cs in g.convs.items():
+            if own_dgrad(cs):
+                self.wd[name] = torch.empty(cs.cin, cs.k, cs.k, cs.cout, dtype=torch.bfloat16,
+                                            device=device)
         self.bn_mean = {n: torch.zeros(c, device=device) for n, c in g.bns.items()}
         self.bn_invstd = {n: torch.ones(c, device=device) for n, c in g.bns.items()}
         self.bn_rmean = {n: torch.zeros(c, device=device) for n, c in g.bns.items()}
@@ -108,14 +114,24 @@ class Params:
     def refresh_bf16(self):
         self.conv_bf16.copy_(self.master[:self.n_conv])
         for name, packed in self.stem_packed.items():
-            w = self.wbf[name]
-            packed[:, :w[0].numel()].copy_(w.reshape(w.shape[0], -1))
+            K.pack_stem_weights(self.wbf[name], packed)
+        for name, wd in self.wd.items():
+            wd.copy_(self.wbf[name].flip(1, 2).permute(3, 1, 2, 0))
 
     def sgd_step(self, lr: float, momentum: float = 0.9, weight_decay: float = 1e-4):
         # grads stay untouched (they are what DP all-reduces and tests read)
         self.mom.mul_(momentum).add_(self.grad).add_(self.master, alpha=weight_decay)
         self.master.add_(self.mom, alpha=-lr)
         self.refresh_bf16()
+
+
+def own_dgrad(cs: G.ConvSpec) -> bool:
+    """Input gradients of the stride-1 1x1 convs run through our tcgen05 conv
+    kernel (transposed weights, fused backward epilogues: residual add + ReLU
+    mask, BN-backward reductions).  3x3 and strided dgrads stay with cuDNN for
+    now (our 3x3 kernel is slower than cuDNN's at the narrow layer-1/2 widths,
+    scripts/kbench_dgrad.py); the stem has no input gradient."""
+    return cs.stride == 1 and cs.k == 1 and cs.cin != 4
 
 
 @dataclass
@@ -151,10 +167,18 @@ class DeltaRuntime:
         # BN statistics partials written by the conv epilogue (one 128-row
         # tile per partial); downsample convs use their own scratch because
         # their BN is applied together with the block's bn3.
-        n_part = max((int(np.prod(n.shape[:-1])) + 127) // 128 * n.shape[-1]
-                     for n in self.nodes if n.op == "conv")
-        self.stats_main = torch.empty(2 * n_part, dtype=torch.float32, device=self.device)
-        self.stats_ds = torch.empty(2 * n_part, dtype=torch.float32, device=self.device)
+        n_part = max(K.stats_partials_floats(int(np.prod(n.shape[:-1])), n.shape[-1])
+                     for n in self.nodes if n.op in ("conv", "conv_bn_relu_bwd"))
+        self.stats_main = torch.empty(n_part, dtype=torch.float32, device=self.device)
+        self.stats_ds = torch.empty(n_part, dtype=torch.float32, device=self.device)
+        # backward scratch outside the budget: the masked gradient g of a fused
+        # conv->BN backward, and the input gradient of a stride-1 shortcut conv
+        self.g_ws = torch.empty(max(n.nbytes for n in self.nodes if n.op == "conv_bn_relu_bwd"),
+                                dtype=torch.uint8, device=self.device)
+        short = [self.nodes[n.parents[1]].nbytes for n in self.nodes
+                 if n.op == "conv_shortcut_bwd" and "conv_short" in n.attrs
+                 and own_dgrad(self.g.convs[n.attrs["conv_short"]])]
+        self.short_ws = torch.empty(max(short + [256]), dtype=torch.uint8, device=self.device)
         mp = next(n for n in self.nodes if n.op == "maxpool")
         self.mp_ws = torch.empty(K.maxpool_workspace_bytes(*self.nodes[mp.parents[0]].shape),
                                  dtype=torch.uint8, device=self.device)
@@ -184,6 +208,7 @@ class DeltaRuntime:
         # epilogue BN statistics cost ~11*BN cycles per tile against ~2*kblocks*BN
         # of MMA: fused only where the main loop hides them (K-dim >= 384)
         self._fuse_stats = {}
+        self._dconvs = {}
         for n in self.nodes:
             if n.op == "conv":
                 cs = self.g.convs[n.attrs["conv"]]
@@ -195,6 +220,13 @@ class DeltaRuntime:
                 assert (conv.P, conv.Q) == n.shape[1:3], (n.name, conv.P, conv.Q, n.shape)
                 self._convs[n.name] = conv
                 self._fuse_stats[n.name] = conv.kdim >= 384
+                if own_dgrad(cs):
+                    _, P_, Q_, _ = n.shape
+                    dconv = K.Conv(Nb, P_, Q_, cs.cout, cs.cin, cs.k, cs.k, 1, cs.k // 2,
+                                   _ptr(self.params.wd[cs.name]))
+                    if dconv.tile_n > 128:
+                        dconv.set_tile_n(128)  # fused backward epilogues
+                    self._dconvs[cs.name] = dconv
 
     def trace(self) -> P.Trace:
         return G.to_trace(self.g)
@@ -322,33 +354,61 @@ class DeltaRuntime:
                           _ptr(pr.gviews["bn_g:" + bn]), _ptr(pr.gviews["bn_b:" + bn]),
                           _ptr(self.bn_ws), st)
         elif op == "conv_bn_relu_bwd":
+            # parents [dC, R = relu(bn(X)), X]
             conv = node.attrs["conv"]
             bn = node.attrs["bn"]
             dC = self._view(in_offs[0], self.nodes[node.parents[0]])
             R = self._view(in_offs[1], self.nodes[node.parents[1]])
-            dR = self._conv_bwd(conv, dC, R, need_dx=True)
             M = int(np.prod(node.shape[:-1]))
             C = node.shape[-1]
-            K.bn_backward(_ptr(dR), 0, ins[1], ins[2], out, M, C, _ptr(pr.bn_mean[bn]),
-                          _ptr(pr.bn_invstd[bn]), _ptr(pr.views["bn_g:" + bn]),
-                          _ptr(pr.gviews["bn_g:" + bn]), _ptr(pr.gviews["bn_b:" + bn]),
-                          _ptr(self.bn_ws), st)
+            bnp = (_ptr(pr.bn_mean[bn]), _ptr(pr.bn_invstd[bn]))
+            if conv in self._dconvs:
+                # dgrad on the tensor cores; the epilogue applies the ReLU mask
+                # (recomputed from X) and reduces sum g, sum g*X per tile
+                g_ptr = _ptr(self.g_ws)
+                self._dconvs[conv].bn_bwd(ins[0], g_ptr, _ptr(self.stats_main), ins[2], *bnp,
+                                          _ptr(pr.views["bn_g:" + bn]), _ptr(pr.views["bn_b:" + bn]),
+                                          st)
+                K.bn_backward_from_partials(_ptr(self.stats_main), g_ptr, ins[2], out, M, C, *bnp,
+                                            _ptr(pr.views["bn_g:" + bn]),
+                                            _ptr(pr.gviews["bn_g:" + bn]),
+                                            _ptr(pr.gviews["bn_b:" + bn]), st)
+                self._conv_bwd(conv, dC, R, need_dx=False)
+            else:
+                dR = self._conv_bwd(conv, dC, R, need_dx=True)
+                K.bn_backward(_ptr(dR), 0, ins[1], ins[2], out, M, C, *bnp,
+                              _ptr(pr.views["bn_g:" + bn]), _ptr(pr.gviews["bn_g:" + bn]),
+                              _ptr(pr.gviews["bn_b:" + bn]), _ptr(self.bn_ws), st)
         elif op == "conv_shortcut_bwd":
+            # out = (dgrad(conv1, dC1) + shortcut gradient) * [X > 0]; the sum
+            # and the mask are the dgrad kernel's epilogue
+            conv = node.attrs["conv"]
             dC1 = self._view(in_offs[0], self.nodes[node.parents[0]])
             X = self._view(in_offs[1], self.nodes[node.parents[1]])
-            dX = self._conv_bwd(node.attrs["conv"], dC1, X, need_dx=True)
-            M = int(np.prod(node.shape[:-1]))
-            C = node.shape[-1]
             out_mask = ins[1] if node.attrs.get("mask_out") else None
+            add, pool_hw, add_mask = None, 0, None
             if "conv_short" in node.attrs:
+                short = node.attrs["conv_short"]
                 dCD = self._view(in_offs[2], self.nodes[node.parents[2]])
-                dXs = self._conv_bwd(node.attrs["conv_short"], dCD, X, need_dx=True)
-                K.add_grad(_ptr(dX), _ptr(dXs), 0, None, out_mask, out, M, C, st)
+                if short in self._dconvs:
+                    add = _ptr(self.short_ws)
+                    self._dconvs[short](ins[2], add, st)
+                    self._conv_bwd(short, dCD, X, need_dx=False)
+                else:
+                    dXs = self._conv_bwd(short, dCD, X, need_dx=True)
+                    add = _ptr(dXs)
             elif node.attrs.get("from_pool"):
-                pool_hw = int(node.shape[1] * node.shape[2])
-                K.add_grad(_ptr(dX), ins[2], pool_hw, ins[3], out_mask, out, M, C, st)
+                add, pool_hw, add_mask = ins[2], int(node.shape[1] * node.shape[2]), ins[3]
             else:
-                K.add_grad(_ptr(dX), ins[2], 0, None, out_mask, out, M, C, st)
+                add = ins[2]
+            if conv in self._dconvs:
+                self._dconvs[conv].add_mask(ins[0], out, st, add=add, pool_hw=pool_hw,
+                                            add_mask=add_mask, out_mask=out_mask)
+                self._conv_bwd(conv, dC1, X, need_dx=False)
+            else:
+                dX = self._conv_bwd(conv, dC1, X, need_dx=True)
+                M = int(np.prod(node.shape[:-1]))
+                K.add_grad(_ptr(dX), add, pool_hw, add_mask, out_mask, out, M, node.shape[-1], st)
         elif op == "maxpool_bwd":
             src = self.nodes[node.parents[1]]
             Nb, H, W, C = src.shape

@@ -23,6 +23,23 @@ shapes = [  # H, C, K, R, stride, pad
 ]
 st = torch.cuda.current_stream().cuda_stream
 out = []
+# stem 7x7/2 over C=4 (pixel-pair TMA im2col path)
+x = torch.randn(N, 224, 224, 4, device="cuda").to(torch.bfloat16)
+w4 = (torch.randn(64, 7, 7, 4, device="cuda") * 0.05).to(torch.bfloat16)
+wp = K.pack_stem_weights(w4)
+conv = K.Conv(N, 224, 224, 4, 64, 7, 7, 2, 3, wp.data_ptr())
+y = torch.empty(N, 112, 112, 64, device="cuda", dtype=torch.bfloat16)
+ms = timeit(lambda: conv(x.data_ptr(), y.data_ptr(), st))
+ms_cudnn = timeit(lambda: F.conv2d(x.permute(0, 3, 1, 2), w4.permute(0, 3, 1, 2), stride=2, padding=3))
+flops = 2.0 * N * 112 * 112 * 64 * 7 * 7 * 3
+print(json.dumps(dict(shape="stem7x7s2", ms=round(ms, 4), tflops_rgb=round(flops / ms / 1e9, 1),
+                      gbs=round((x.numel() + y.numel()) * 2 / ms / 1e6, 1), cudnn_ms=round(ms_cudnn, 4))), flush=True)
+# BN statistics from the epilogue partials of a 56x56x64 conv (6272 partials)
+M = N * 56 * 56
+parts = torch.randn(K.stats_partials_floats(M, 64), device="cuda").abs()
+mean = torch.empty(64, device="cuda"); inv = torch.empty(64, device="cuda")
+ms = timeit(lambda: K.bn_stats_from_partials(parts.data_ptr(), M, 64, mean.data_ptr(), inv.data_ptr(), 1e-5, None, None, 0.1, st))
+print(json.dumps(dict(kernel="bn_stats_from_partials_56x56x64", us=round(ms * 1e3, 2))), flush=True)
 for (H, C, Ko, R, s, p) in shapes:
     x = torch.randn(N, H, H, C, device="cuda").to(torch.bfloat16)
     w = (torch.randn(Ko, R, R, C, device="cuda") * 0.05).to(torch.bfloat16)

@@ -57,7 +57,7 @@ def test_conv_fwd_matches_fp32_reference(case):
     # bitwise-identical recompute, and BN statistics fused in the epilogue
     y2 = torch.empty_like(y)
     M = N * conv.P * conv.Q
-    parts = torch.empty((M + 127) // 128 * Kout * 2, device="cuda")
+    parts = torch.empty(K.stats_partials_floats(M, Kout), device="cuda")
     conv(x.data_ptr(), y2.data_ptr(), _stream(), parts.data_ptr())
     mean = torch.empty(Kout, device="cuda"); inv = torch.empty(Kout, device="cuda")
     K.bn_stats_from_partials(parts.data_ptr(), M, Kout, mean.data_ptr(), inv.data_ptr(), 1e-5,
@@ -69,17 +69,16 @@ def test_conv_fwd_matches_fp32_reference(case):
     assert torch.allclose(inv, torch.rsqrt(yf.var(0, unbiased=False) + 1e-5), rtol=2e-4, atol=1e-4)
 
 
-def test_conv_stem_packed_c4():
-    N, H, W, Kout = 2, 224, 224, 64
+@pytest.mark.parametrize("N,H,W", [(2, 224, 224), (3, 30, 46), (1, 17, 8)])
+def test_conv_stem_packed_c4(N, H, W):
+    Kout = 64
     g = torch.Generator(device="cuda").manual_seed(1)
     x = torch.zeros(N, H, W, 4, device="cuda", dtype=torch.bfloat16)
     x[..., :3] = torch.randn(N, H, W, 3, device="cuda", generator=g).to(torch.bfloat16)
     w = (torch.randn(Kout, 7, 7, 3, device="cuda", generator=g) / 12).to(torch.bfloat16)
-    kdim = (7 * 7 * 4 + 63) // 64 * 64
-    wp = torch.zeros(Kout, kdim, device="cuda", dtype=torch.bfloat16)
     w4 = torch.zeros(Kout, 7, 7, 4, device="cuda", dtype=torch.bfloat16)
     w4[..., :3] = w
-    wp[:, :7 * 7 * 4] = w4.reshape(Kout, -1)
+    wp = K.pack_stem_weights(w4)
     conv = K.Conv(N, H, W, 4, Kout, 7, 7, 2, 3, wp.data_ptr())
     y = torch.empty(N, conv.P, conv.Q, Kout, device="cuda", dtype=torch.bfloat16)
     conv(x.data_ptr(), y.data_ptr(), _stream())
@@ -88,6 +87,10 @@ def test_conv_stem_packed_c4():
     err = (y.float() - ref).abs()
     tol = 1e-2 * ref.abs() + 2e-2 * ref.pow(2).mean().sqrt()
     assert bool((err <= tol).all()), f"max err {err.max().item()}"
+    y2 = torch.empty_like(y)
+    conv(x.data_ptr(), y2.data_ptr(), _stream())
+    torch.cuda.synchronize()
+    assert torch.equal(y, y2)
 
 
 def _bn_params(C, g):
@@ -226,3 +229,102 @@ def test_avgpool_and_softmax_xent():
     torch.cuda.synchronize()
     assert abs(loss.item() - ref.item()) < 1e-4 * max(1.0, ref.item())
     assert torch.allclose(dl, lf.grad, atol=1e-6, rtol=1e-4)
+
+
+# ------------------------------------------------ dgrad through the conv kernel
+DGRAD_CASES = [
+    # N, H, W, C (forward input channels = dgrad outputs), K (forward outputs), R
+    (2, 56, 56, 64, 256, 1),
+    (2, 56, 56, 256, 64, 1),
+    (2, 56, 56, 64, 64, 3),
+    (4, 14, 14, 256, 256, 3),
+    (16, 28, 28, 512, 128, 1),
+    (3, 7, 7, 2048, 512, 1),
+]
+
+
+def _dgrad_setup(case, seed):
+    N, H, W, Cin, Kout, R = case
+    g = torch.Generator(device="cuda").manual_seed(seed)
+    w = (torch.randn(Kout, R, R, Cin, device="cuda", generator=g) / (R * R * Kout) ** 0.5).to(torch.bfloat16)
+    dy = torch.randn(N, H, W, Kout, device="cuda", generator=g).to(torch.bfloat16)
+    wd = w.flip(1, 2).permute(3, 1, 2, 0).contiguous()        # [C][R][S][K]
+    conv = K.Conv(N, H, W, Kout, Cin, R, R, 1, R // 2, wd.data_ptr())
+    conv.keep = wd  # the handle caches a descriptor of wd's memory: keep it alive
+    if conv.tile_n > 128:
+        conv.set_tile_n(128)
+    ref = torch.nn.grad.conv2d_input((N, Cin, H, W), w.permute(0, 3, 1, 2).float(),
+                                     dy.permute(0, 3, 1, 2).float(), padding=R // 2)
+    return g, w, dy, conv, ref.permute(0, 2, 3, 1).contiguous()
+
+
+def _close(y, ref, what):
+    err = (y.float() - ref).abs()
+    tol = 1e-2 * ref.abs() + 2e-2 * ref.pow(2).mean().sqrt() + 1e-6
+    assert bool((err <= tol).all()), f"{what}: max err {err.max().item()}"
+
+
+@pytest.mark.parametrize("case", DGRAD_CASES)
+def test_dgrad_and_add_mask_epilogue(case):
+    g, w, dy, conv, ref = _dgrad_setup(case, 7)
+    N, H, W, Cin = ref.shape
+    y = torch.empty(N, H, W, Cin, device="cuda", dtype=torch.bfloat16)
+    conv(dy.data_ptr(), y.data_ptr(), _stream())
+    torch.cuda.synchronize()
+    _close(y, ref, "dgrad")
+    add = torch.randn(N, H, W, Cin, device="cuda", generator=g).to(torch.bfloat16)
+    am = torch.randn(N, H, W, Cin, device="cuda", generator=g).to(torch.bfloat16)
+    om = torch.randn(N, H, W, Cin, device="cuda", generator=g).to(torch.bfloat16)
+    y2 = torch.empty_like(y)
+    conv.add_mask(dy.data_ptr(), y2.data_ptr(), _stream(), add=add.data_ptr(),
+                  out_mask=om.data_ptr())
+    torch.cuda.synchronize()
+    ref2 = (ref + add.float()) * (om.float() > 0)
+    _close(y2, ref2, "add+mask")
+    # pooled upstream gradient broadcast over H*W pixels, scaled by 1/(H*W),
+    # masked by add_mask (the last block's output)
+    pooled = torch.randn(N, Cin, device="cuda", generator=g).to(torch.bfloat16)
+    conv.add_mask(dy.data_ptr(), y2.data_ptr(), _stream(), add=pooled.data_ptr(), pool_hw=H * W,
+                  add_mask=am.data_ptr(), out_mask=om.data_ptr())
+    torch.cuda.synchronize()
+    up = (pooled.float() / (H * W))[:, None, None, :] * (am.float() > 0)
+    _close(y2, (ref + up) * (om.float() > 0), "pooled add")
+
+
+@pytest.mark.parametrize("case", DGRAD_CASES[:4])
+def test_dgrad_bn_backward_epilogue(case):
+    """g = dgrad * [relu(bn(xc)) > 0] bit-exact against the plain dgrad masked
+    by OUR forward BN-ReLU output; partials -> dgamma/dbeta/dx vs autograd."""
+    g, w, dy, conv, ref = _dgrad_setup(case, 8)
+    N, H, W, C = ref.shape
+    M = N * H * W
+    xc = (torch.randn(M, C, device="cuda", generator=g) * 1.5 + 0.2).to(torch.bfloat16)
+    gamma, beta = _bn_params(C, g)
+    xf = xc.float()
+    mean = xf.mean(0)
+    invstd = torch.rsqrt(xf.var(0, unbiased=False) + 1e-5)
+    relu_out = torch.empty_like(xc)
+    K.bn_apply(0, xc.data_ptr(), None, relu_out.data_ptr(), M, C, mean.data_ptr(),
+               invstd.data_ptr(), gamma.data_ptr(), beta.data_ptr(), stream=_stream())
+    plain = torch.empty(N, H, W, C, device="cuda", dtype=torch.bfloat16)
+    conv(dy.data_ptr(), plain.data_ptr(), _stream())
+    gbuf = torch.empty_like(plain)
+    parts = torch.empty(K.stats_partials_floats(M, C), device="cuda")
+    conv.bn_bwd(dy.data_ptr(), gbuf.data_ptr(), parts.data_ptr(), xc.data_ptr(), mean.data_ptr(),
+                invstd.data_ptr(), gamma.data_ptr(), beta.data_ptr(), _stream())
+    torch.cuda.synchronize()
+    gexp = torch.where(relu_out.view(N, H, W, C) > 0, plain, torch.zeros_like(plain))
+    assert torch.equal(gbuf, gexp)
+    dx = torch.empty_like(xc)
+    dg = torch.empty(C, device="cuda"); db = torch.empty(C, device="cuda")
+    K.bn_backward_from_partials(parts.data_ptr(), gbuf.data_ptr(), xc.data_ptr(), dx.data_ptr(),
+                                M, C, mean.data_ptr(), invstd.data_ptr(), gamma.data_ptr(),
+                                dg.data_ptr(), db.data_ptr(), _stream())
+    torch.cuda.synchronize()
+    xr = xf.clone().requires_grad_(True)
+    gm = gamma.clone().requires_grad_(True)
+    bt = beta.clone().requires_grad_(True)
+    F.batch_norm(xr, None, None, gm, bt, training=True, eps=1e-5).backward(gbuf.float().view(M, C))
+    assert torch.allclose(db, bt.grad, rtol=1e-3, atol=1e-2)
+    assert torch.allclose(dg, gm.grad, rtol=1e-3, atol=1e-2)
+    assert (dx.float() - xr.grad).abs().max().item() <= 1.5e-2 * xr.grad.abs().max().item()
