@@ -30,6 +30,7 @@ import time
 HERE = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, HERE)
 
+PCIE5_X16_GBS = 64.0  # nominal per direction (32 GT/s x 16 lanes, 128b/130b)
 METRIC = "ResNet-50 imgs/sec at 50% activation budget; peak act GB; max batch vs baseline"
 TRACE_FIXTURE = os.path.join(HERE, "tests", "golden", "resnet50_bs256_trace.json")
 
@@ -290,9 +291,18 @@ def main():
             rt.run_program(timing=timing)
         torch.cuda.synchronize()
     rt.graph = saved_graph
+    hbm_peak, tc_peak, tc_sus, peak_kind = measured_peaks()
     conv_ms, conv_flops, conv_n, all_ms = 0.0, 0.0, 0, 0.0
     kinds = {}
+    rc = {"launches": 0, "ms": 0.0, "roofline_ms": 0.0, "flops": 0.0, "bytes": 0.0, "by_op": {}}
+    swap_ms, swap_bytes, swap_n = 0.0, 0, 0
     for nid, lst in timing.items():
+        if nid == "swap":
+            for (a, b, op, nb) in lst:
+                swap_ms += a.elapsed_time(b)
+                swap_bytes += nb
+                swap_n += 1
+            continue
         node = rt.nodes[nid]
         for (a, b, rec) in lst:
             ms = a.elapsed_time(b)
@@ -302,7 +312,19 @@ def main():
                 conv_ms += ms
                 conv_flops += node.flops
                 conv_n += 1
-    hbm_peak, tc_peak, tc_sus, peak_kind = measured_peaks()
+            if rec:
+                # recompute engine: each re-launch against its own roofline
+                # (tensor-core FLOPs or HBM bytes, whichever bounds it)
+                t_roof = max(node.flops / (tc_peak * 1e9), node.hbm_bytes / (hbm_peak * 1e6))
+                rc["launches"] += 1
+                rc["ms"] += ms
+                bo = rc["by_op"].setdefault(node.op, [0, 0.0, 0.0])
+                bo[0] += 1
+                bo[1] += ms
+                bo[2] += t_roof
+                rc["roofline_ms"] += t_roof
+                rc["flops"] += node.flops
+                rc["bytes"] += node.hbm_bytes
     achieved = conv_flops / (conv_ms * 1e-3) / 1e12 if conv_ms else 0.0
 
     # ---- CPU baseline: the reference simulator planning this exact trace ----
@@ -341,6 +363,15 @@ def main():
     best = max((f.batch for f in mb_delta.values() if f), default=None)
     if best and mb_base:
         max_batch["ratio"] = round(best / mb_base.batch, 3)
+    # config 3: ResNet-101 (its extra layer3 blocks take layer3.1's per-sample costs)
+    ps101 = MB.per_sample_costs(101, per_sample)
+    b101 = MB.search(101, cap, ps101, bpus, delta=False)
+    d101 = MB.search(101, cap, ps101, bpus, delta=True, anchors="out")
+    max_batch["resnet101"] = {"no_eviction": b101.batch if b101 else None,
+                              "delta": d101.batch if d101 else None,
+                              "ratio": round(d101.batch / b101.batch, 3) if b101 and d101 else None}
+    max_batch["note"] = ("planner-decided (arena + batch-proportional workspace <= capacity); "
+                         "real steps at these sizes: scripts/max_batch_verify.py")
 
     value = world * B / (delta_ms * 1e-3)
     if rank == 0:
@@ -381,6 +412,25 @@ def main():
                          "launches_timed": conv_n,
                          "share_of_step": round(conv_ms / all_ms, 4) if all_ms else None,
                          "op_ms": {k: round(v, 3) for k, v in sorted(kinds.items(), key=lambda kv: -kv[1])}},
+            "recompute": {"launches": rc["launches"], "ms_per_step": round(rc["ms"], 3),
+                          "share_of_step": round(rc["ms"] / all_ms, 4) if all_ms else None,
+                          "roofline_ms": round(rc["roofline_ms"], 3),
+                          "frac_of_roofline": round(rc["roofline_ms"] / rc["ms"], 4) if rc["ms"] else None,
+                          "hbm_gb": round(rc["bytes"] / 1e9, 3),
+                          "by_op": {k: {"n": v[0], "ms": round(v[1], 3),
+                                        "frac_of_roofline": round(v[2] / v[1], 3) if v[1] else None}
+                                    for k, v in rc["by_op"].items()},
+                          "note": "eager step, CUDA events per recompute launch; roofline = "
+                                  "max(FLOPs/TC peak, algorithmic bytes/HBM peak) per launch"},
+            "swap": {"copies": swap_n, "bytes_per_step": swap_bytes,
+                     "ms_per_step": round(swap_ms, 3),
+                     "achieved_gbs": round(swap_bytes / (swap_ms * 1e6), 2) if swap_ms else None,
+                     "link_probe_gbs": round(rt.link_gbs, 2) if rt.link_gbs else None,
+                     "peak_gbs": PCIE5_X16_GBS,
+                     "frac_of_link_peak": round(swap_bytes / (swap_ms * 1e6) / PCIE5_X16_GBS, 4)
+                     if swap_ms else None,
+                     "note": "copy-engine D2H/H2D on their own streams (events on those streams); "
+                             "peak = PCIe Gen5 x16 nominal per direction"},
             "max_batch": max_batch,
             "cpu_baseline": cpu,
             "gpu_launches": (launches * args.steps) if launches is not None else None,

@@ -137,6 +137,10 @@ delta_status delta_report_json(const delta_result* run, const delta_result* base
                                char** out, uint64_t* len);
 /* timeline_to_chrome_trace (src/metrics.cpp:255) */
 delta_status delta_chrome_trace(const delta_result* r, char** out, uint64_t* len);
+/* timeline_to_chrome_trace of a caller-built event array (e.g. the executed
+ * GPU timeline: the plan's events re-stamped with measured device times) */
+delta_status delta_chrome_trace_events(const delta_event* ev, uint64_t n, char** out,
+                                       uint64_t* len);
 void delta_result_free(delta_result* r);
 
 /* CPU planner timing: mean ns per run_iteration over `iters` calls. */

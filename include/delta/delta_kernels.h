@@ -43,7 +43,9 @@ delta_status delta_conv_forward(const delta_conv* c, const void* x, void* y, flo
  * W'[c][r][s][k] = W[k][R-1-r][S-1-s][c]).
  *   DELTA_EPI_ADD_MASK: y = bf16((acc + add') * [out_mask > 0]); add' = add
  *       ([M][K]), or with pool_hw > 0 the pooled add ([N][K]) / pool_hw *
- *       [add_mask > 0] (add_mask is read only with a pooled add).
+ *       [add_mask > 0] (add_mask is read only with a pooled add).  With
+ *       add_stride2 = 1 the full add is the input gradient of a stride-2 1x1
+ *       conv: given as [N][P/2][Q/2][K] at the even rows/columns, zero elsewhere.
  *       Null pointers are skipped.  (The residual-branch gradient sum.)
  *   DELTA_EPI_BN_BWD: y = g = bf16(acc) * [relu(bn(xc)) > 0] with the saved
  *       statistics (the forward's exact arithmetic), and `stats` receives the
@@ -53,6 +55,8 @@ enum { DELTA_EPI_STORE = 0, DELTA_EPI_ADD_MASK = 1, DELTA_EPI_BN_BWD = 2 };
 typedef struct delta_conv_epilogue {
   int32_t mode;
   int32_t pool_hw;
+  int32_t add_stride2;
+  int32_t reserved;
   const void* add;
   const void* add_mask;
   const void* out_mask;

@@ -97,6 +97,7 @@ def _load():
         "delta_result_decisions": (P(DeltaDecision), [vp, P(u64)]),
         "delta_report_json": (i32, [vp, vp, P(vp), P(u64)]),
         "delta_chrome_trace": (i32, [vp, P(vp), P(u64)]),
+        "delta_chrome_trace_events": (i32, [vp, u64, P(vp), P(u64)]),
         "delta_result_free": (None, [vp]),
         "delta_plan_time_ns": (i32, [vp, P(DeltaConfig), u32, P(C.c_double)]),
         "delta_transfer_time_us": (i32, [u64, P(DeltaConfig), P(u64)]),

@@ -293,6 +293,30 @@ delta_status delta_chrome_trace(const delta_result* r, char** out, uint64_t* len
   return guard([&] { *out = dup_str(timeline_to_chrome_trace(r->r.timeline), len); });
 }
 
+delta_status delta_chrome_trace_events(const delta_event* ev, uint64_t n, char** out,
+                                       uint64_t* len) {
+  return guard([&] {
+    Timeline t;
+    t.events.reserve(n);
+    for (uint64_t i = 0; i < n; ++i) {
+      TimelineEvent e;
+      e.ts = ev[i].ts;
+      e.node = ev[i].node;
+      e.duration = ev[i].duration;
+      e.bytes = ev[i].bytes;
+      e.burst = ev[i].burst;
+      if (ev[i].stream > 1 || ev[i].kind > static_cast<uint8_t>(EventKind::Free) || ev[i].phase > 1)
+        throw ArgumentError("chrome_trace_events: bad event " + std::to_string(i));
+      e.stream = static_cast<StreamKind>(ev[i].stream);
+      e.kind = static_cast<EventKind>(ev[i].kind);
+      e.phase = static_cast<Phase>(ev[i].phase);
+      e.prefetch = ev[i].prefetch != 0;
+      t.events.push_back(e);
+    }
+    *out = dup_str(timeline_to_chrome_trace(t), len);
+  });
+}
+
 void delta_result_free(delta_result* r) { delete r; }
 
 delta_status delta_plan_time_ns(const delta_trace* t, const delta_config* c,

@@ -21,18 +21,21 @@ using bf16 = __nv_bfloat16;
 
 namespace {
 
-constexpr int SLICE = 64;   // channels per reduction block
+constexpr int SLICE = 64;   // channel granularity (C is a power of two, 64..2048)
+// Streaming loops issue UNROLL vectors' loads of every input before any math
+// (memory-level parallelism: 2-3 input streams need ~100+ KB in flight per SM
+// to reach HBM speed; a load-use loop kept only ~60 KB and ran at ~4.4 TB/s).
+constexpr int UNROLL = 4;
 
-// Rows per reduction partial: enough partials to fill ~4 waves of 148 SMs,
-// few enough that the fixed-order merge stays short.  A multiple of 32.
+// Rows per reduction partial.  A reduction block covers ALL C channels of its
+// rows (C/8 threads per row, 2048/C rows per step: every warp reads whole
+// contiguous rows), so there are M / rows partials: ~8 per SM, merged in a
+// fixed order by the two-level merge.  A multiple of 16.
 int64_t chunk_rows(int64_t M, int C) {
-  const int64_t slices = C / SLICE;
   const int64_t target_ctas = 148 * 8;
-  int64_t chunks = target_ctas / (slices > 0 ? slices : 1);
-  if (chunks < 1) chunks = 1;
-  int64_t rows = (M + chunks - 1) / chunks;
-  rows = (rows + 31) / 32 * 32;
-  return rows < 256 ? 256 : rows;
+  int64_t rows = (M + target_ctas - 1) / target_ctas;
+  rows = (rows + 15) / 16 * 16;
+  return rows < 16 ? 16 : rows;
 }
 
 __device__ __forceinline__ uint4 ld_stream(const void* p) {
@@ -77,41 +80,51 @@ __device__ __forceinline__ void merge(float& n, float& mu, float& m2, float nb, 
 }
 
 // ---------------------------------------------------------------- BN stats
+// Per-chunk (mean, M2) of every channel.  Thread layout: tx = channel group
+// (8 channels, 16 B), ty = row phase; rows r0+ty, r0+ty+RPI, ... (RPI =
+// 256 / (C/8)).  Row-phase partials are combined in smem (fixed order).
 __global__ void __launch_bounds__(256, 4) k_bn_stats_partial(const bf16* __restrict__ x, int64_t M,
                                                           int C, int64_t chunk,
                                                           float2* __restrict__ ws) {
-  const int tx = threadIdx.x & 7, ty = threadIdx.x >> 3;
-  const int c0 = blockIdx.x * SLICE + tx * 8;
-  const int64_t r0 = int64_t(blockIdx.y) * chunk;
+  const int tpr = C >> 3, rpi = 256 / tpr;
+  const int tx = threadIdx.x % tpr, ty = threadIdx.x / tpr;
+  const int c0 = tx * 8;
+  const int64_t r0 = int64_t(blockIdx.x) * chunk;
   const int64_t r1 = min(M, r0 + chunk);
   float s[8] = {0}, q[8] = {0};
-#pragma unroll 2
-  for (int64_t r = r0 + ty; r < r1; r += 32) {
-    float f[8];
-    unpack8(ld_stream(x + r * C + c0), f);
+  for (int64_t rb = r0 + ty; rb < r1; rb += 2 * UNROLL * rpi) {
+    uint4 xv[2 * UNROLL];
 #pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      s[i] += f[i];
-      q[i] = fmaf(f[i], f[i], q[i]);
+    for (int u = 0; u < 2 * UNROLL; ++u)
+      if (rb + u * rpi < r1) xv[u] = ld_stream(x + (rb + u * rpi) * C + c0);
+#pragma unroll
+    for (int u = 0; u < 2 * UNROLL; ++u) {
+      if (rb + u * rpi >= r1) break;
+      float f[8];
+      unpack8(xv[u], f);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        s[i] += f[i];
+        q[i] = fmaf(f[i], f[i], q[i]);
+      }
     }
   }
-  __shared__ float ss[32][SLICE + 1], sq[32][SLICE + 1];
+  __shared__ float ss[2048], sq[2048];  // [rpi][C]
 #pragma unroll
   for (int i = 0; i < 8; ++i) {
-    ss[ty][tx * 8 + i] = s[i];
-    sq[ty][tx * 8 + i] = q[i];
+    ss[ty * C + c0 + i] = s[i];
+    sq[ty * C + c0 + i] = q[i];
   }
   __syncthreads();
-  if (threadIdx.x < SLICE) {
+  for (int c = threadIdx.x; c < C; c += 256) {
     float S = 0.f, Q = 0.f;
-    for (int j = 0; j < 32; ++j) {
-      S += ss[j][threadIdx.x];
-      Q += sq[j][threadIdx.x];
+    for (int j = 0; j < rpi; ++j) {
+      S += ss[j * C + c];
+      Q += sq[j * C + c];
     }
     const float n = float(r1 - r0);
     const float mu = S / n;
-    ws[int64_t(blockIdx.y) * C + blockIdx.x * SLICE + threadIdx.x] =
-        make_float2(mu, fmaxf(Q - S * mu, 0.f));
+    ws[int64_t(blockIdx.x) * C + c] = make_float2(mu, fmaxf(Q - S * mu, 0.f));
   }
 }
 
@@ -189,6 +202,7 @@ __global__ void __launch_bounds__(256)
 // blockDim (256) is a multiple of C/8 for every C <= 2048, so with a grid
 // stride that is a multiple of the block, each thread always touches the SAME
 // 8 channels: their scale/shift live in registers, not shared memory.
+
 template <int MODE>
 __global__ void __launch_bounds__(256)
     k_bn_apply(const bf16* __restrict__ x, const bf16* __restrict__ res, bf16* __restrict__ y,
@@ -202,89 +216,122 @@ __global__ void __launch_bounds__(256)
   float sc[8], sh[8], sc2[8], sh2[8];
 #pragma unroll
   for (int j = 0; j < 8; ++j) {
+    // explicit FMAs: the dgrad BN-backward epilogue (conv_fwd.cu) recomputes
+    // this ReLU mask with the identical arithmetic
     sc[j] = invstd[c0 + j] * gamma[c0 + j];
-    sh[j] = beta[c0 + j] - mean[c0 + j] * sc[j];
+    sh[j] = fmaf(-mean[c0 + j], sc[j], beta[c0 + j]);
     if (MODE == 2) {
       sc2[j] = invstd2[c0 + j] * gamma2[c0 + j];
-      sh2[j] = beta2[c0 + j] - mean2[c0 + j] * sc2[j];
+      sh2[j] = fmaf(-mean2[c0 + j], sc2[j], beta2[c0 + j]);
     }
   }
   const int64_t stride = int64_t(gridDim.x) * blockDim.x;
-#pragma unroll 2
-  for (int64_t i = first; i < vecs; i += stride) {
-    float f[8];
-    unpack8(ld_stream(x + i * 8), f);
-    float r[8];
-    if (MODE >= 1) unpack8(ld_stream(res + i * 8), r);
+  for (int64_t i0 = first; i0 < vecs; i0 += UNROLL * stride) {
+    uint4 xv[UNROLL], rv[UNROLL];
 #pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      float v = fmaf(f[j], sc[j], sh[j]);
-      if (MODE == 1) v += r[j];
-      if (MODE == 2) v += fmaf(r[j], sc2[j], sh2[j]);
-      f[j] = fmaxf(v, 0.f);
+    for (int u = 0; u < UNROLL; ++u) {
+      const int64_t i = i0 + u * stride;
+      if (i < vecs) {
+        xv[u] = ld_stream(x + i * 8);
+        if (MODE >= 1) rv[u] = ld_stream(res + i * 8);
+      }
     }
-    reinterpret_cast<uint4*>(y)[i] = pack8(f);
+#pragma unroll
+    for (int u = 0; u < UNROLL; ++u) {
+      const int64_t i = i0 + u * stride;
+      if (i >= vecs) break;
+      float f[8], r[8];
+      unpack8(xv[u], f);
+      if (MODE >= 1) unpack8(rv[u], r);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        float v = fmaf(f[j], sc[j], sh[j]);
+        if (MODE == 1) v += r[j];
+        if (MODE == 2) v += fmaf(r[j], sc2[j], sh2[j]);
+        f[j] = fmaxf(v, 0.f);
+      }
+      reinterpret_cast<uint4*>(y)[i] = pack8(f);
+    }
   }
 }
 
 // ------------------------------------------------------------- BN backward
-__device__ __forceinline__ void load_up(const bf16* up, int pool_hw, float inv_hw, int64_t row,
-                                        int c0, int C, float (&g)[8]) {
-  if (pool_hw) {
-    unpack8(*reinterpret_cast<const uint4*>(up + (row / pool_hw) * C + c0), g);
+// upstream gradient of row `row`, channels c0..c0+7: full [M,C] (streamed) or
+// pooled [N,C] / pool_hw (POOLED; read through L1, rows of one image share it)
+template <bool POOLED>
+__device__ __forceinline__ uint4 load_up(const bf16* up, int pool_hw, int64_t row, int c0, int C) {
+  if (POOLED) return *reinterpret_cast<const uint4*>(up + (row / pool_hw) * C + c0);
+  return ld_stream(up + row * C + c0);
+}
+template <bool POOLED>
+__device__ __forceinline__ void unpack_up(uint4 u, float inv_hw, float (&g)[8]) {
+  unpack8(u, g);
+  if (POOLED) {
 #pragma unroll
     for (int j = 0; j < 8; ++j) g[j] *= inv_hw;
-  } else {
-    unpack8(ld_stream(up + row * C + c0), g);
   }
 }
 
 // Per chunk: sum g and sum g*x (x-hat folded in at the end: sum g*xhat =
 // invstd*(sum g*x - mean*sum g)), so no per-channel parameters stay live in
 // the loop and occupancy is not register-limited.
-__global__ void __launch_bounds__(256, 4)
+template <bool MASKED, bool POOLED>
+__global__ void __launch_bounds__(256)
     k_bn_bwd_partial(const bf16* __restrict__ up, int pool_hw, const bf16* __restrict__ mask,
                      const bf16* __restrict__ x, int64_t M, int C, int64_t chunk,
                      const float* mean, const float* invstd, float2* __restrict__ ws) {
-  const int tx = threadIdx.x & 7, ty = threadIdx.x >> 3;
-  const int c0 = blockIdx.x * SLICE + tx * 8;
-  const int64_t r0 = int64_t(blockIdx.y) * chunk;
+  const int tpr = C >> 3, rpi = 256 / tpr;
+  const int tx = threadIdx.x % tpr, ty = threadIdx.x / tpr;
+  const int c0 = tx * 8;
+  const int64_t r0 = int64_t(blockIdx.x) * chunk;
   const int64_t r1 = min(M, r0 + chunk);
-  const float inv_hw = pool_hw ? 1.f / float(pool_hw) : 1.f;
+  const float inv_hw = POOLED ? 1.f / float(pool_hw) : 1.f;
   float sg[8] = {0}, sgx[8] = {0};
-#pragma unroll 2
-  for (int64_t r = r0 + ty; r < r1; r += 32) {
-    float g[8], xv[8];
-    load_up(up, pool_hw, inv_hw, r, c0, C, g);
-    if (mask) {
-      float m[8];
-      unpack8(ld_stream(mask + r * C + c0), m);
+  for (int64_t rb = r0 + ty; rb < r1; rb += UNROLL * rpi) {
+    uint4 uv[UNROLL], mv[UNROLL], xv[UNROLL];
 #pragma unroll
-      for (int j = 0; j < 8; ++j) g[j] = m[j] > 0.f ? g[j] : 0.f;
+    for (int u = 0; u < UNROLL; ++u) {
+      const int64_t r = rb + u * rpi;
+      if (r < r1) {
+        uv[u] = load_up<POOLED>(up, pool_hw, r, c0, C);
+        if (MASKED) mv[u] = ld_stream(mask + r * C + c0);
+        xv[u] = ld_stream(x + r * C + c0);
+      }
     }
-    unpack8(ld_stream(x + r * C + c0), xv);
 #pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      sg[j] += g[j];
-      sgx[j] = fmaf(g[j], xv[j], sgx[j]);
+    for (int u = 0; u < UNROLL; ++u) {
+      if (rb + u * rpi >= r1) break;
+      float g[8], xf[8];
+      unpack_up<POOLED>(uv[u], inv_hw, g);
+      if (MASKED) {
+        float m[8];
+        unpack8(mv[u], m);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) g[j] = m[j] > 0.f ? g[j] : 0.f;
+      }
+      unpack8(xv[u], xf);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        sg[j] += g[j];
+        sgx[j] = fmaf(g[j], xf[j], sgx[j]);
+      }
     }
   }
-  __shared__ float a[32][SLICE + 1], b[32][SLICE + 1];
+  __shared__ float a[2048], b[2048];  // [rpi][C]
 #pragma unroll
   for (int j = 0; j < 8; ++j) {
-    a[ty][tx * 8 + j] = sg[j];
-    b[ty][tx * 8 + j] = sgx[j];
+    a[ty * C + c0 + j] = sg[j];
+    b[ty * C + c0 + j] = sgx[j];
   }
   __syncthreads();
-  if (threadIdx.x < SLICE) {
+  for (int c = threadIdx.x; c < C; c += 256) {
     float A = 0.f, B = 0.f;
-    for (int j = 0; j < 32; ++j) {
-      A += a[j][threadIdx.x];
-      B += b[j][threadIdx.x];
+    for (int j = 0; j < rpi; ++j) {
+      A += a[j * C + c];
+      B += b[j * C + c];
     }
-    const int c = blockIdx.x * SLICE + threadIdx.x;
     // sum g*xhat over the chunk = invstd * (sum g*x - mean * sum g)
-    ws[int64_t(blockIdx.y) * C + c] = make_float2(A, invstd[c] * (B - mean[c] * A));
+    ws[int64_t(blockIdx.x) * C + c] = make_float2(A, invstd[c] * (B - mean[c] * A));
   }
 }
 
@@ -349,7 +396,8 @@ __global__ void __launch_bounds__(256)
 
 // dx = gamma*invstd*(g - dbeta/M - xhat*dgamma/M), xhat = (x-mean)*invstd,
 // folded per channel into dx = k1*g + k2*x + k3 (3 live coefficients).
-__global__ void __launch_bounds__(256, 4)
+template <bool MASKED, bool POOLED>
+__global__ void __launch_bounds__(256)
     k_bn_bwd_apply(const bf16* __restrict__ up, int pool_hw, const bf16* __restrict__ mask,
                    const bf16* __restrict__ x, bf16* __restrict__ dx, int64_t vecs, int cmask,
                    int logC, int64_t M, const float* __restrict__ mean,
@@ -369,39 +417,54 @@ __global__ void __launch_bounds__(256, 4)
     k2[j] = -a * kd;
     k3[j] = a * (kd * mean[c0 + j] - dbeta[c0 + j] * invM);
   }
-  const float inv_hw = pool_hw ? 1.f / float(pool_hw) : 1.f;
+  const float inv_hw = POOLED ? 1.f / float(pool_hw) : 1.f;
   const int64_t stride = int64_t(gridDim.x) * blockDim.x;
-#pragma unroll 2
-  for (int64_t i = first; i < vecs; i += stride) {
-    const int64_t row = (i * 8) >> logC;
-    float g[8], xv[8];
-    load_up(up, pool_hw, inv_hw, row, c0, C, g);
-    if (mask) {
-      float m[8];
-      unpack8(ld_stream(mask + i * 8), m);
+  for (int64_t i0 = first; i0 < vecs; i0 += UNROLL * stride) {
+    uint4 uv[UNROLL], mv[UNROLL], xv[UNROLL];
 #pragma unroll
-      for (int j = 0; j < 8; ++j) g[j] = m[j] > 0.f ? g[j] : 0.f;
+    for (int u = 0; u < UNROLL; ++u) {
+      const int64_t i = i0 + u * stride;
+      if (i < vecs) {
+        uv[u] = POOLED ? load_up<true>(up, pool_hw, (i * 8) >> logC, c0, C)
+                       : ld_stream(up + i * 8);
+        if (MASKED) mv[u] = ld_stream(mask + i * 8);
+        xv[u] = ld_stream(x + i * 8);
+      }
     }
-    unpack8(ld_stream(x + i * 8), xv);
 #pragma unroll
-    for (int j = 0; j < 8; ++j) g[j] = fmaf(k1[j], g[j], fmaf(k2[j], xv[j], k3[j]));
-    reinterpret_cast<uint4*>(dx)[i] = pack8(g);
+    for (int u = 0; u < UNROLL; ++u) {
+      const int64_t i = i0 + u * stride;
+      if (i >= vecs) break;
+      float g[8], xf[8];
+      unpack_up<POOLED>(uv[u], inv_hw, g);
+      if (MASKED) {
+        float m[8];
+        unpack8(mv[u], m);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) g[j] = m[j] > 0.f ? g[j] : 0.f;
+      }
+      unpack8(xv[u], xf);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) g[j] = fmaf(k1[j], g[j], fmaf(k2[j], xf[j], k3[j]));
+      reinterpret_cast<uint4*>(dx)[i] = pack8(g);
+    }
   }
 }
 
 // out = (a + g) [* (out_mask > 0)], g = up [* (up_mask > 0)], up full or pooled
+template <bool POOLED>
 __global__ void __launch_bounds__(256)
     k_add_grad(const bf16* __restrict__ a, const bf16* __restrict__ up, int pool_hw,
                const bf16* __restrict__ up_mask, const bf16* __restrict__ out_mask,
                bf16* __restrict__ out, int64_t vecs, int cmask, int logC, int C) {
-  const float inv_hw = pool_hw ? 1.f / float(pool_hw) : 1.f;
+  const float inv_hw = POOLED ? 1.f / float(pool_hw) : 1.f;
   const int64_t stride = int64_t(gridDim.x) * blockDim.x;
   for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < vecs; i += stride) {
     const int c0 = int(i * 8) & cmask;
     const int64_t row = (i * 8) >> logC;
     float fa[8], g[8];
     unpack8(ld_stream(a + i * 8), fa);
-    load_up(up, pool_hw, inv_hw, row, c0, C, g);
+    unpack_up<POOLED>(load_up<POOLED>(up, pool_hw, row, c0, C), inv_hw, g);
     if (up_mask) {
       float m[8];
       unpack8(ld_stream(up_mask + i * 8), m);
@@ -628,10 +691,10 @@ void merge_partials(const float2* ws, int parts, int64_t rows_per, int64_t M, in
 
 cudaError_t bn_stats(const void* x, int64_t M, int C, float* ws, float* mean, float* invstd,
                      float eps, float* rm, float* rv, float mom, cudaStream_t st) {
-  if (C % SLICE) return cudaErrorInvalidValue;
+  if (C % SLICE || (C & (C - 1)) || C > 2048) return cudaErrorInvalidValue;
   const int64_t chunk = chunk_rows(M, C);
   const int chunks = int((M + chunk - 1) / chunk);
-  k_bn_stats_partial<<<dim3(C / SLICE, chunks), 256, 0, st>>>(static_cast<const bf16*>(x), M, C,
+  k_bn_stats_partial<<<chunks, 256, 0, st>>>(static_cast<const bf16*>(x), M, C,
                                                               chunk, reinterpret_cast<float2*>(ws));
   merge_partials(reinterpret_cast<const float2*>(ws), chunks, chunk, M, C, mean, invstd, eps, rm,
                  rv, mom, st);
@@ -688,14 +751,18 @@ cudaError_t bn_backward(const void* up, int pool_hw, const void* mask, const voi
   auto U = static_cast<const bf16*>(up);
   auto Mk = static_cast<const bf16*>(mask);
   auto X = static_cast<const bf16*>(x);
-  k_bn_bwd_partial<<<dim3(C / SLICE, chunks), 256, 0, st>>>(U, pool_hw, Mk, X, M, C, chunk, mean,
-                                                            invstd, reinterpret_cast<float2*>(ws));
+  const auto part = Mk ? (pool_hw ? k_bn_bwd_partial<true, true> : k_bn_bwd_partial<true, false>)
+                      : (pool_hw ? k_bn_bwd_partial<false, true> : k_bn_bwd_partial<false, false>);
+  part<<<chunks, 256, 0, st>>>(U, pool_hw, Mk, X, M, C, chunk, mean, invstd,
+                               reinterpret_cast<float2*>(ws));
   k_bn_bwd_final<<<(C + 7) / 8, 256, 0, st>>>(reinterpret_cast<const float2*>(ws), chunks, C,
                                               dgamma, dbeta);
   const int64_t vecs = M * C / 8;
-  k_bn_bwd_apply<<<grid_for(vecs, 256), 256, 0, st>>>(
-      U, pool_hw, Mk, X, static_cast<bf16*>(dx), vecs, C - 1, __builtin_ctz(C), M, mean, invstd,
-      gamma, dgamma, dbeta);
+  const auto app = Mk ? (pool_hw ? k_bn_bwd_apply<true, true> : k_bn_bwd_apply<true, false>)
+                     : (pool_hw ? k_bn_bwd_apply<false, true> : k_bn_bwd_apply<false, false>);
+  app<<<grid_for(vecs, 256), 256, 0, st>>>(U, pool_hw, Mk, X, static_cast<bf16*>(dx), vecs, C - 1,
+                                           __builtin_ctz(C), M, mean, invstd, gamma, dgamma,
+                                           dbeta);
   return cudaGetLastError();
 }
 
@@ -716,7 +783,7 @@ cudaError_t bn_backward_from_partials(const float* partials, int rows_per_part, 
   }
   k_bn_bwd_final_raw<<<(C + 7) / 8, 256, 0, st>>>(ws, parts, C, mean, invstd, dgamma, dbeta);
   const int64_t vecs = M * C / 8;
-  k_bn_bwd_apply<<<grid_for(vecs, 256), 256, 0, st>>>(
+  k_bn_bwd_apply<false, false><<<grid_for(vecs, 256), 256, 0, st>>>(
       static_cast<const bf16*>(g), 0, nullptr, static_cast<const bf16*>(x), static_cast<bf16*>(dx),
       vecs, C - 1, __builtin_ctz(C), M, mean, invstd, gamma, dgamma, dbeta);
   return cudaGetLastError();
@@ -726,7 +793,7 @@ cudaError_t add_grad(const void* a, const void* up, int pool_hw, const void* up_
                      const void* out_mask, void* out, int64_t M, int C, cudaStream_t st) {
   if (C & (C - 1)) return cudaErrorInvalidValue;
   const int64_t vecs = M * C / 8;
-  k_add_grad<<<grid_for(vecs, 256), 256, 0, st>>>(
+  (pool_hw ? k_add_grad<true> : k_add_grad<false>)<<<grid_for(vecs, 256), 256, 0, st>>>(
       static_cast<const bf16*>(a), static_cast<const bf16*>(up), pool_hw,
       static_cast<const bf16*>(up_mask), static_cast<const bf16*>(out_mask),
       static_cast<bf16*>(out), vecs, C - 1, __builtin_ctz(C), C);

@@ -353,13 +353,38 @@ __global__ void __launch_bounds__(kThreads, 1)
         const uint32_t sb = ring + (e % NSLOTS) * SLOT;
         const int pm = (tile_ / a.n_tiles) * BM + quarter * 32;
         const int pc = (tile_ % a.n_tiles) * BN + int(e % CH) * 32;
+        // stride-2 add: (n, p, q) of the block's first row, once per chunk
+        int q0 = 0, p0 = 0, n0_ = 0;
+        if ((EV == EV_ADD || EV == EV_ADD_OM) && a.e.add_stride2) {
+          q0 = pm % a.Q;
+          const int t = pm / a.Q;
+          p0 = t % a.P;
+          n0_ = t / a.P;
+        }
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
           const int r = i * 8 + (lane >> 2), u = lane & 3;
-          const bool ok = pm + r < a.M;
-          const int64_t go = int64_t(ok ? pm + r : 0) * a.K + pc + u * 8;
+          const int m = pm + r;
+          const bool ok = m < a.M;
+          const int64_t go = int64_t(ok ? m : 0) * a.K + pc + u * 8;
           const uint32_t so = r * 64 + ((u ^ ((r >> 1) & 3)) << 4);
-          cp_async_16(sb + so, src0 + go, ok);
+          if ((EV == EV_ADD || EV == EV_ADD_OM) && a.e.add_stride2) {
+            // the add is the input gradient of a stride-2 1x1 conv, given at
+            // its [N][P/2][Q/2] sampling points: zero at odd rows/columns
+            int q = q0 + r, pp = p0, n = n0_;
+            while (q >= a.Q) {  // a 32-row block wraps an image row at most 32/Q times
+              q -= a.Q;
+              if (++pp == a.P) {
+                pp = 0;
+                ++n;
+              }
+            }
+            const bool on = ok && !((pp | q) & 1);
+            const int64_t srow = (int64_t(n) * (a.P >> 1) + (pp >> 1)) * (a.Q >> 1) + (q >> 1);
+            cp_async_16(sb + so, src0 + (on ? srow : 0) * a.K + pc + u * 8, on);
+          } else {
+            cp_async_16(sb + so, src0 + go, ok);
+          }
           if (NOPS == 2) cp_async_16(sb + 2048 + so, src1 + go, ok);
         }
       }
@@ -775,6 +800,8 @@ cudaError_t conv_forward(const ConvPlan& cp, const void* x, void* y, float* stat
       ev = e.out_mask ? EV_ADD_OM : EV_ADD;
     }
     if (cp.bn != 64 && cp.bn != 128) return cudaErrorInvalidValue;
+    if (e.add_stride2 && (ev == EV_POOL || ev == EV_BN_BWD || (cp.P & 1) || (cp.Q & 1)))
+      return cudaErrorInvalidValue;
 #define DELTA_FUSED(EVV)                                                                    \
   case EVV:                                                                                 \
     if (cp.bn == 64)                                                                        \

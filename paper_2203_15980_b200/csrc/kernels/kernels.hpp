@@ -23,6 +23,9 @@ constexpr int EPI_STORE = 0, EPI_ADD_MASK = 1, EPI_BN_BWD = 2;
 struct ConvEpilogue {
   int mode;
   int pool_hw;
+  int add_stride2;  // EPI_ADD_MASK: `add` is given at the even rows/columns only,
+                    // as a [N][P/2][Q/2][K] tensor (zero elsewhere)
+  int pad_;
   const void* add;
   const void* add_mask;
   const void* out_mask;

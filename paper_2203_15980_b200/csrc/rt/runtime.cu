@@ -79,6 +79,7 @@ delta_status delta_conv_forward_ex(const delta_conv* c, const void* x, void* y, 
   if (epi) {
     e.mode = epi->mode;
     e.pool_hw = epi->pool_hw;
+    e.add_stride2 = epi->add_stride2;
     e.add = epi->add;
     e.add_mask = epi->add_mask;
     e.out_mask = epi->out_mask;

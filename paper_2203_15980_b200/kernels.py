@@ -61,7 +61,8 @@ EPI_STORE, EPI_ADD_MASK, EPI_BN_BWD = 0, 1, 2
 
 class ConvEpilogue(C.Structure):
     """delta_conv_epilogue (include/delta/delta_kernels.h)."""
-    _fields_ = [("mode", i32), ("pool_hw", i32), ("add", vp), ("add_mask", vp), ("out_mask", vp),
+    _fields_ = [("mode", i32), ("pool_hw", i32), ("add_stride2", i32), ("reserved", i32),
+                ("add", vp), ("add_mask", vp), ("out_mask", vp),
                 ("xc", vp), ("mean", vp), ("invstd", vp), ("gamma", vp), ("beta", vp)]
 
 
@@ -86,17 +87,19 @@ class Conv:
         check(lib.delta_conv_set_tile_n(self._h, tile_n))
         self.tile_n = tile_n
 
-    def add_mask(self, x_ptr, y_ptr, stream, add=None, pool_hw=0, add_mask=None, out_mask=None):
+    def add_mask(self, x_ptr, y_ptr, stream, add=None, pool_hw=0, add_mask=None, out_mask=None,
+                 add_stride2=False):
         """y = (conv(x) + add') * [out_mask > 0]; add' = add, or the pooled add
-        / pool_hw * [add_mask > 0] (add_mask is only read with a pooled add)."""
-        e = ConvEpilogue(EPI_ADD_MASK, pool_hw, add, add_mask, out_mask, None, None, None, None,
-                         None)
+        / pool_hw * [add_mask > 0] (add_mask is only read with a pooled add),
+        or (add_stride2) an [N,P/2,Q/2,K] add placed at the even rows/columns."""
+        e = ConvEpilogue(EPI_ADD_MASK, pool_hw, int(add_stride2), 0, add, add_mask, out_mask,
+                         None, None, None, None, None)
         check(lib.delta_conv_forward_ex(self._h, x_ptr, y_ptr, None, C.byref(e), stream))
         _count(1)
 
     def bn_bwd(self, x_ptr, g_ptr, partials_ptr, xc, mean, invstd, gamma, beta, stream):
         """g = bf16(conv(x)) * [relu(bn(xc)) > 0] and per-tile (sum g, sum g*xc)."""
-        e = ConvEpilogue(EPI_BN_BWD, 0, None, None, None, xc, mean, invstd, gamma, beta)
+        e = ConvEpilogue(EPI_BN_BWD, 0, 0, 0, None, None, None, xc, mean, invstd, gamma, beta)
         check(lib.delta_conv_forward_ex(self._h, x_ptr, g_ptr, partials_ptr, C.byref(e), stream))
         _count(1)
 
@@ -137,10 +140,8 @@ def _merge_launches(parts: int) -> int:
 
 def _chunks(M: int, C_: int) -> int:
     """Number of reduction chunks of the streaming BN kernels (bn_pool.cu chunk_rows)."""
-    slices = max(1, C_ // 64)
-    chunks = max(1, (148 * 8) // slices)
-    rows = (M + chunks - 1) // chunks
-    rows = max(256, (rows + 31) // 32 * 32)
+    rows = (M + 148 * 8 - 1) // (148 * 8)
+    rows = max(16, (rows + 15) // 16 * 16)
     return (M + rows - 1) // rows
 
 

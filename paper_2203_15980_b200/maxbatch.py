@@ -27,21 +27,16 @@ class Fit:
 
 def resident_workspace_bytes(g: G.Graph, batch: int) -> int:
     """Batch-proportional buffers DeltaRuntime allocates up front, outside the
-    activation budget: input staging, BN-statistics partials (2 scratch
-    buffers), maxpool argmax scratch, head gradients."""
-    x = g.nodes[0].nbytes
-    convs = [n for n in g.nodes if n.op == "conv"]
-    parts = 2 * max((((n.shape[0] * n.shape[1] * n.shape[2] + 127) // 128) * 33 // 32 + 1)
-                    * n.shape[3] * 8 for n in convs)
-    mp = next(n for n in g.nodes if n.op == "maxpool")
-    return x + parts + mp.nbytes // 2 + batch * 1000 * 8
+    activation budget (runtime.workspace_plan)."""
+    from .runtime import workspace_plan
+    ws = workspace_plan(g)
+    return sum(v for k, v in ws.items() if k != "transient")
 
 
 def transient_workspace_bytes(g: G.Graph, batch: int) -> int:
-    """cuDNN dgrad outputs alive at once during a backward node (conv1 +
-    downsample input gradients of a block)."""
-    convs = [n for n in g.nodes if n.op == "conv"]
-    return 2 * max(g.nodes[n.parents[0]].nbytes for n in convs)
+    """cuDNN input-gradient outputs alive at once inside one backward node."""
+    from .runtime import workspace_plan
+    return workspace_plan(g)["transient"]
 
 
 def workspace_bytes(g: G.Graph, batch: int) -> int:
@@ -74,6 +69,21 @@ def fits(depth, batch, capacity, anchors, costs_per_sample, link_bpus, delta: bo
     if prog.infeasible or prog.arena_bytes > room:
         return None
     return Fit(batch, prog.arena_bytes, ws, anchors, prog.plan_counts)
+
+
+def per_sample_costs(depth: int, per50: dict) -> dict:
+    """Per-sample node costs for ResNet-`depth` from ResNet-50's (same node
+    names); blocks ResNet-50 lacks (layer3.6+) take layer3.1's costs."""
+    if depth == 50:
+        return dict(per50)
+    g = G.build_resnet(depth, 1)
+    out = {}
+    for n in g.nodes:
+        key = n.name
+        if key not in per50 and key.startswith("layer3."):
+            key = "layer3.1." + key.split(".", 2)[2]
+        out[n.name] = per50.get(key, min(per50.values()))
+    return out
 
 
 def search(depth, capacity, costs_per_sample, link_bpus, delta: bool, anchors="out+narrow",

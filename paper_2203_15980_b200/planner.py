@@ -270,6 +270,15 @@ class RunResult:
             self._ptr = None
 
 
+def chrome_trace_events(events: np.ndarray) -> str:
+    """timeline_to_chrome_trace of an EVENT_DTYPE array (ref src/metrics.cpp:255)."""
+    ev = np.ascontiguousarray(events, dtype=EVENT_DTYPE)
+    p, n = C.c_void_p(), C.c_uint64()
+    check(lib.delta_chrome_trace_events(ev.ctypes.data_as(C.c_void_p), len(ev), C.byref(p),
+                                        C.byref(n)))
+    return take_string(p, n.value)
+
+
 def _plan(fn, trace: Trace, cfg: EngineConfig) -> RunResult:
     h = _CTrace(trace)
     try:
@@ -371,4 +380,5 @@ __all__ = [
     "PrefetchGuard", "EventKind", "StreamKind", "OpNode", "AccessEvent", "Trace",
     "CostModel", "EngineConfig", "RunResult", "run_iteration", "run_unconstrained_baseline",
     "report_json", "plan_time_ns", "transfer_time_us", "Program", "DeltaError",
+    "chrome_trace_events",
 ]

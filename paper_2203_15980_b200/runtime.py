@@ -125,13 +125,45 @@ class Params:
         self.refresh_bf16()
 
 
+def workspace_plan(g: G.Graph) -> dict:
+    """Bytes of every batch-proportional buffer DeltaRuntime allocates outside
+    the activation budget (the max-batch search plans with the same numbers).
+    'transient' = the largest cuDNN output alive inside one backward node
+    (the 3x3 input gradients)."""
+    nodes = g.nodes
+    M = lambda n: int(np.prod(n.shape[:-1]))
+    batch = nodes[0].shape[0]
+    ws = {}
+    ws["bn_ws"] = 4 * max(K.bn_workspace_floats(M(n), n.shape[-1]) for n in nodes
+                          if len(n.shape) == 4 and n.shape[-1] % 64 == 0)
+    parts = 4 * max(K.stats_partials_floats(M(n), n.shape[-1]) for n in nodes
+                    if n.op in ("conv", "conv_bn_relu_bwd"))
+    ws["stats_main"] = ws["stats_ds"] = parts
+    short = [nodes[n.parents[2]].nbytes * g.convs[n.attrs["conv_short"]].cin
+             // g.convs[n.attrs["conv_short"]].cout for n in nodes
+             if n.op == "conv_shortcut_bwd" and "conv_short" in n.attrs
+             and g.convs[n.attrs["conv_short"]].stride != 1]
+    ws["short_ws"] = max(short + [256])
+    mp = next(n for n in nodes if n.op == "maxpool")
+    ws["mp_ws"] = K.maxpool_workspace_bytes(*nodes[mp.parents[0]].shape)
+    ws["head"] = 4 + batch * g.fc[1] * 4 + batch * 4
+    ws["input_slots"] = 2 * (nodes[0].nbytes + batch * 8)
+    trans = [0]
+    for n in nodes:
+        if n.op == "conv_bn_relu_bwd" and not own_dgrad(g.convs[n.attrs["conv"]]):
+            trans.append(nodes[n.parents[1]].nbytes)          # cuDNN dgrad output
+    ws["transient"] = max(trans)
+    return ws
+
+
 def own_dgrad(cs: G.ConvSpec) -> bool:
-    """Input gradients of the stride-1 1x1 convs run through our tcgen05 conv
-    kernel (transposed weights, fused backward epilogues: residual add + ReLU
-    mask, BN-backward reductions).  3x3 and strided dgrads stay with cuDNN for
-    now (our 3x3 kernel is slower than cuDNN's at the narrow layer-1/2 widths,
-    scripts/kbench_dgrad.py); the stem has no input gradient."""
-    return cs.stride == 1 and cs.k == 1 and cs.cin != 4
+    """Input gradients of the 1x1 convs run through our tcgen05 conv kernel
+    (transposed weights; fused backward epilogues: residual add + ReLU mask,
+    BN-backward reductions; a stride-2 1x1's gradient is computed on its
+    sampling grid and scattered by the consumer's epilogue).  3x3 dgrads stay
+    with cuDNN for now (our 3x3 kernel is slower than cuDNN's at the narrow
+    layer-1/2 widths, scripts/kbench_dgrad.py); the stem has no input gradient."""
+    return cs.k == 1 and cs.cin != 4
 
 
 @dataclass
@@ -158,30 +190,19 @@ class DeltaRuntime:
         self.stream = torch.cuda.Stream(device=self.device)
         self._convs = {}
         self._build_convs()
-        maxM = max(int(np.prod(n.shape[:-1])) for n in self.nodes if len(n.shape) == 4)
-        maxC = max(self.g.bns.values())
-        self.bn_ws = torch.empty(max(K.bn_workspace_floats(int(np.prod(n.shape[:-1])), n.shape[-1])
-                                     for n in self.nodes if len(n.shape) == 4 and n.shape[-1] % 64 == 0),
-                                 dtype=torch.float32, device=self.device)
-        del maxM, maxC
+        ws = workspace_plan(self.g)
+        f32 = lambda key: torch.empty(ws[key] // 4, dtype=torch.float32, device=self.device)
+        u8 = lambda key: torch.empty(ws[key], dtype=torch.uint8, device=self.device)
+        self.bn_ws = f32("bn_ws")
         # BN statistics partials written by the conv epilogue (one 128-row
         # tile per partial); downsample convs use their own scratch because
         # their BN is applied together with the block's bn3.
-        n_part = max(K.stats_partials_floats(int(np.prod(n.shape[:-1])), n.shape[-1])
-                     for n in self.nodes if n.op in ("conv", "conv_bn_relu_bwd"))
-        self.stats_main = torch.empty(n_part, dtype=torch.float32, device=self.device)
-        self.stats_ds = torch.empty(n_part, dtype=torch.float32, device=self.device)
-        # backward scratch outside the budget: the masked gradient g of a fused
-        # conv->BN backward, and the input gradient of a stride-1 shortcut conv
-        self.g_ws = torch.empty(max(n.nbytes for n in self.nodes if n.op == "conv_bn_relu_bwd"),
-                                dtype=torch.uint8, device=self.device)
-        short = [self.nodes[n.parents[1]].nbytes for n in self.nodes
-                 if n.op == "conv_shortcut_bwd" and "conv_short" in n.attrs
-                 and own_dgrad(self.g.convs[n.attrs["conv_short"]])]
-        self.short_ws = torch.empty(max(short + [256]), dtype=torch.uint8, device=self.device)
-        mp = next(n for n in self.nodes if n.op == "maxpool")
-        self.mp_ws = torch.empty(K.maxpool_workspace_bytes(*self.nodes[mp.parents[0]].shape),
-                                 dtype=torch.uint8, device=self.device)
+        self.stats_main = f32("stats_main")
+        self.stats_ds = f32("stats_ds")
+        # backward scratch outside the budget: the input gradient of a stride-2
+        # shortcut conv at its sampling grid
+        self.short_ws = u8("short_ws")
+        self.mp_ws = u8("mp_ws")
         ncls = self.g.fc[1]
         self.loss = torch.zeros(1, dtype=torch.float32, device=self.device)
         self.dlogits = torch.empty(batch, ncls, dtype=torch.float32, device=self.device)
@@ -221,6 +242,8 @@ class DeltaRuntime:
                 self._convs[n.name] = conv
                 self._fuse_stats[n.name] = conv.kdim >= 384
                 if own_dgrad(cs):
+                    # on the conv's output grid (a stride-2 1x1's gradient lives at
+                    # its sampling points; the consumer scatters it)
                     _, P_, Q_, _ = n.shape
                     dconv = K.Conv(Nb, P_, Q_, cs.cout, cs.cin, cs.k, cs.k, 1, cs.k // 2,
                                    _ptr(self.params.wd[cs.name]))
@@ -365,7 +388,7 @@ class DeltaRuntime:
             if conv in self._dconvs:
                 # dgrad on the tensor cores; the epilogue applies the ReLU mask
                 # (recomputed from X) and reduces sum g, sum g*X per tile
-                g_ptr = _ptr(self.g_ws)
+                g_ptr = out  # g is written in place of its BN-backward output
                 self._dconvs[conv].bn_bwd(ins[0], g_ptr, _ptr(self.stats_main), ins[2], *bnp,
                                           _ptr(pr.views["bn_g:" + bn]), _ptr(pr.views["bn_b:" + bn]),
                                           st)
@@ -386,12 +409,15 @@ class DeltaRuntime:
             dC1 = self._view(in_offs[0], self.nodes[node.parents[0]])
             X = self._view(in_offs[1], self.nodes[node.parents[1]])
             out_mask = ins[1] if node.attrs.get("mask_out") else None
-            add, pool_hw, add_mask = None, 0, None
+            add, pool_hw, add_mask, stride2 = None, 0, None, False
             if "conv_short" in node.attrs:
                 short = node.attrs["conv_short"]
                 dCD = self._view(in_offs[2], self.nodes[node.parents[2]])
                 if short in self._dconvs:
-                    add = _ptr(self.short_ws)
+                    if self.g.convs[short].stride == 1:
+                        add = out   # summed in place by conv1's dgrad epilogue
+                    else:
+                        add, stride2 = _ptr(self.short_ws), True  # at its sampling grid
                     self._dconvs[short](ins[2], add, st)
                     self._conv_bwd(short, dCD, X, need_dx=False)
                 else:
@@ -403,7 +429,8 @@ class DeltaRuntime:
                 add = ins[2]
             if conv in self._dconvs:
                 self._dconvs[conv].add_mask(ins[0], out, st, add=add, pool_hw=pool_hw,
-                                            add_mask=add_mask, out_mask=out_mask)
+                                            add_mask=add_mask, out_mask=out_mask,
+                                            add_stride2=stride2)
                 self._conv_bwd(conv, dC1, X, need_dx=False)
             else:
                 dX = self._conv_bwd(conv, dC1, X, need_dx=True)
@@ -460,9 +487,13 @@ class DeltaRuntime:
         return None
 
     # -------------------------------------------------------- program
-    def run_program(self, timing: dict | None = None, probe: dict | None = None):
+    def run_program(self, timing: dict | None = None, probe: dict | None = None,
+                    stamps: list | None = None):
         """Issue one training step: the lowered action program on the three
-        streams, then the optimizer.  Returns nothing; loss stays on device."""
+        streams, then the optimizer.  Returns nothing; loss stays on device.
+        `timing`: per-node (and "swap") CUDA event pairs; `stamps`: receives
+        (action index, start event, end event) of every compute/recompute/
+        offload/reload action (events on the action's own stream)."""
         prog = self.program
         st = self.stream.cuda_stream
         streams = {P.STREAM_COMPUTE: st, P.STREAM_D2H: self.swap.d2h_stream,
@@ -472,7 +503,7 @@ class DeltaRuntime:
         ev = self.events
         base = self._base
         n_timed = 0
-        for a in prog.actions:
+        for ai, a in enumerate(prog.actions):
             op = int(a["op"])
             if timing is not None and op in (P.ACT_COMPUTE, P.ACT_RECOMPUTE) and n_timed % 24 == 0:
                 # keep the GPU busy while the host queues the next actions, so
@@ -485,6 +516,10 @@ class DeltaRuntime:
             elif op in (P.ACT_COMPUTE, P.ACT_RECOMPUTE):
                 node = nodes[int(a["node"])]
                 at, n_in = int(a["inputs_at"]), int(a["n_inputs"])
+                if timing is None and stamps is not None:
+                    e0 = torch.cuda.Event(enable_timing=True)
+                    e1 = torch.cuda.Event(enable_timing=True)
+                    e0.record(self.stream)
                 if timing is not None:
                     e0 = torch.cuda.Event(enable_timing=True)
                     e1 = torch.cuda.Event(enable_timing=True)
@@ -493,14 +528,32 @@ class DeltaRuntime:
                                op == P.ACT_RECOMPUTE, st)
                 if probe is not None and node.id in probe:
                     probe[node.id] = self._view(int(a["offset"]), node).clone()
-                if timing is not None:
+                if timing is not None or stamps is not None:
                     e1.record(self.stream)
+                if timing is not None:
                     timing.setdefault(node.id, []).append((e0, e1, op == P.ACT_RECOMPUTE))
                     n_timed += 1
-            elif op == P.ACT_OFFLOAD:
-                self.swap.offload(base + int(a["offset"]), int(a["host_offset"]), int(a["bytes"]))
-            elif op == P.ACT_RELOAD:
-                self.swap.reload(base + int(a["offset"]), int(a["host_offset"]), int(a["bytes"]))
+                if stamps is not None:
+                    stamps.append((ai, e0, e1))
+            elif op in (P.ACT_OFFLOAD, P.ACT_RELOAD):
+                sid = streams[int(a["stream"])]
+                if timing is not None or stamps is not None:
+                    xs = torch.cuda.ExternalStream(sid)
+                    c0 = torch.cuda.Event(enable_timing=True)
+                    c1 = torch.cuda.Event(enable_timing=True)
+                    c0.record(xs)
+                if op == P.ACT_OFFLOAD:
+                    self.swap.offload(base + int(a["offset"]), int(a["host_offset"]),
+                                      int(a["bytes"]), sid)
+                else:
+                    self.swap.reload(base + int(a["offset"]), int(a["host_offset"]),
+                                     int(a["bytes"]), sid)
+                if timing is not None or stamps is not None:
+                    c1.record(xs)
+                if timing is not None:
+                    timing.setdefault("swap", []).append((c0, c1, op, int(a["bytes"])))
+                if stamps is not None:
+                    stamps.append((ai, c0, c1))
         # join the copy streams that carried work back into the compute stream
         used = set(int(x) for x in prog.actions["stream"][np.isin(prog.actions["op"], (P.ACT_OFFLOAD, P.ACT_RELOAD))])
         for sid in sorted(used):
@@ -596,6 +649,42 @@ class DeltaRuntime:
         self._use_slot(0)
         return self._loss_host[:n].tolist()
 
+    def executed_timeline(self) -> np.ndarray:
+        """One eager step with every device action time-stamped; returns the
+        plan's timeline (ref Timeline, engine.hpp:44-70) re-stamped with the
+        MEASURED device times (µs from the step start): Compute/Recompute/
+        Offload/Reload take their kernel's or copy's start and duration;
+        zero-duration markers (Use, Free, Evict, Stall) take the end of the
+        latest compute-stream action before them.  Feed it to the
+        reference's oracle::replay_check (oracle/ref.replay_check) for an
+        independent safety certificate of what the GPU actually did."""
+        prog = self.program
+        stamps = []
+        start = torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        with torch.cuda.stream(self.stream):
+            start.record(self.stream)
+            self.run_program(stamps=stamps)
+        torch.cuda.synchronize()
+        plan = P.run_iteration(self.trace(), self.config).events
+        ev = plan.copy()
+        t_of = {}
+        for ai, e0, e1 in stamps:
+            pe = int(prog.actions[ai]["plan_event"])
+            t0 = start.elapsed_time(e0) * 1e3
+            t1 = start.elapsed_time(e1) * 1e3
+            t_of[pe] = (int(round(t0)), max(0, int(round(t1)) - int(round(t0))))
+        now = 0
+        for i in range(len(ev)):
+            if i in t_of:
+                ev[i]["ts"], ev[i]["duration"] = t_of[i]
+                if ev[i]["stream"] == P.StreamKind.Compute:
+                    now = max(now, int(ev[i]["ts"] + ev[i]["duration"]))
+            else:
+                ev[i]["ts"] = now
+                ev[i]["duration"] = 0
+        return ev
+
     # ----------------------------------------------------- cost model
     def measure_costs(self, iters: int = 3, link: bool = True):
         """GPU-resident cost model: time every node's op on device (CUDA events
@@ -612,7 +701,8 @@ class DeltaRuntime:
                 self.run_program(timing)
                 torch.cuda.synchronize()
                 for nid, lst in timing.items():
-                    samples.setdefault(nid, []).append(lst[0][0].elapsed_time(lst[0][1]))
+                    if nid != "swap":
+                        samples.setdefault(nid, []).append(lst[0][0].elapsed_time(lst[0][1]))
         self.lr = lr
         table = {}
         for n in self.nodes:

@@ -50,3 +50,20 @@ for (H, C, Ko, R) in shapes:
                           bn_bwd_us=round(t_bn * 1e3, 1), cudnn_us=round(t_cudnn * 1e3, 1),
                           plain_tflops=round(flops / t_plain / 1e9, 1),
                           min_hbm_us=round((M * C + M * Ko) * 2 / 6.5e6, 1))), flush=True)
+
+# stride-2 shortcut: conv1 dgrad + the downsample's gradient at its sampling grid
+for (H, C, Ko) in [(56, 256, 128), (28, 512, 256), (14, 1024, 512)]:
+    M = N * H * H
+    w = (torch.randn(Ko, 1, 1, C, device="cuda") * 0.05).to(torch.bfloat16)
+    wd = w.permute(3, 1, 2, 0).contiguous()
+    dy = torch.randn(N, H, H, Ko, device="cuda").to(torch.bfloat16)
+    conv = K.Conv(N, H, H, Ko, C, 1, 1, 1, 0, wd.data_ptr())
+    if conv.tile_n > 128:
+        conv.set_tile_n(128)
+    y = torch.empty(N, H, H, C, device="cuda", dtype=torch.bfloat16)
+    sub = torch.randn(N, H // 2, H // 2, C, device="cuda").to(torch.bfloat16)
+    m = torch.randn(N, H, H, C, device="cuda").to(torch.bfloat16)
+    full = torch.randn(N, H, H, C, device="cuda").to(torch.bfloat16)
+    t_s2 = timeit(lambda: conv.add_mask(dy.data_ptr(), y.data_ptr(), st, add=sub.data_ptr(), out_mask=m.data_ptr(), add_stride2=True))
+    t_full = timeit(lambda: conv.add_mask(dy.data_ptr(), y.data_ptr(), st, add=full.data_ptr(), out_mask=m.data_ptr()))
+    print(json.dumps(dict(shape=[H, C, Ko], add_stride2_us=round(t_s2 * 1e3, 1), add_full_us=round(t_full * 1e3, 1))), flush=True)

@@ -22,16 +22,7 @@ per = {n["name"]: n["compute_cost_us"] / 256 for n in tr["nodes"]}
 
 
 def per_sample(depth):
-    if depth == 50:
-        return per
-    g = G.build_resnet(depth, 1)
-    out = {}
-    for n in g.nodes:
-        key = n.name
-        if key not in per and key.startswith("layer3."):
-            key = "layer3.1." + key.split(".", 2)[2]
-        out[n.name] = per.get(key, 1.0 / 256)
-    return out
+    return MB.per_sample_costs(depth, per)
 
 
 def run(depth, batch, anchors, delta, steps=2):
