@@ -484,36 +484,35 @@ __global__ void __launch_bounds__(256)
 }
 
 // ----------------------------------------------------------------- pooling
+// Grids: blockIdx.x = one image row (n, row), blockIdx.y x 256 threads span
+// (column, 8-channel group) of that row; C/8 is a power of two, so the only
+// divisions left are one 32-bit div/mod per thread.
 __global__ void __launch_bounds__(256) k_maxpool_fwd(const bf16* __restrict__ x,
                                                      bf16* __restrict__ y, int N, int H, int W,
-                                                     int C, int P, int Q) {
-  const int cg = C / 8;
-  const int64_t total = int64_t(N) * P * Q * cg;
-  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
-  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < total; i += stride) {
-    const int c0 = int(i % cg) * 8;
-    int64_t t = i / cg;
-    const int q = int(t % Q);
-    t /= Q;
-    const int p = int(t % P);
-    const int n = int(t / P);
-    float best[8];
+                                                     int C, int P, int Q, int lcg) {
+  const int cg = 1 << lcg;
+  const int item = blockIdx.y * 256 + threadIdx.x;
+  if (item >= Q * cg) return;
+  const int q = item >> lcg, c0 = (item & (cg - 1)) * 8;
+  const int n = blockIdx.x / P, p = blockIdx.x - n * P;
+  float best[8];
 #pragma unroll
-    for (int j = 0; j < 8; ++j) best[j] = -INFINITY;
-    for (int dh = 0; dh < 3; ++dh) {
-      const int h = 2 * p - 1 + dh;
-      if (h < 0 || h >= H) continue;
-      for (int dw = 0; dw < 3; ++dw) {
-        const int w = 2 * q - 1 + dw;
-        if (w < 0 || w >= W) continue;
-        float f[8];
-        unpack8(*reinterpret_cast<const uint4*>(x + ((int64_t(n) * H + h) * W + w) * C + c0), f);
+  for (int j = 0; j < 8; ++j) best[j] = -INFINITY;
 #pragma unroll
-        for (int j = 0; j < 8; ++j) best[j] = f[j] > best[j] ? f[j] : best[j];
-      }
+  for (int dh = 0; dh < 3; ++dh) {
+    const int h = 2 * p - 1 + dh;
+    if (h < 0 || h >= H) continue;
+#pragma unroll
+    for (int dw = 0; dw < 3; ++dw) {
+      const int w = 2 * q - 1 + dw;
+      if (w < 0 || w >= W) continue;
+      float f[8];
+      unpack8(*reinterpret_cast<const uint4*>(x + ((int64_t(n) * H + h) * W + w) * C + c0), f);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) best[j] = f[j] > best[j] ? f[j] : best[j];
     }
-    reinterpret_cast<uint4*>(y)[i] = pack8(best);
   }
+  reinterpret_cast<uint4*>(y)[(int64_t(blockIdx.x) * Q + q) * cg + (c0 >> 3)] = pack8(best);
 }
 
 // Backward in two deterministic passes (no atomics):
@@ -522,74 +521,86 @@ __global__ void __launch_bounds__(256) k_maxpool_fwd(const bf16* __restrict__ x,
 //   2. per input pixel, sum the gradient of the <= 4 windows whose argmax it is.
 __global__ void __launch_bounds__(256)
     k_maxpool_argmax(const bf16* __restrict__ x, uint8_t* __restrict__ idx, int N, int H, int W,
-                     int C, int P, int Q) {
-  const int cg = C / 8;
-  const int64_t total = int64_t(N) * P * Q * cg;
-  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
-  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < total; i += stride) {
-    const int c0 = int(i % cg) * 8;
-    int64_t t = i / cg;
-    const int q = int(t % Q);
-    t /= Q;
-    const int p = int(t % P);
-    const int n = int(t / P);
-    float best[8];
-    uint32_t arg[8];
+                     int C, int P, int Q, int lcg) {
+  const int cg = 1 << lcg;
+  const int item = blockIdx.y * 256 + threadIdx.x;
+  if (item >= Q * cg) return;
+  const int q = item >> lcg, c0 = (item & (cg - 1)) * 8;
+  const int n = blockIdx.x / P, p = blockIdx.x - n * P;
+  float best[8];
+  uint32_t arg[8];
 #pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      best[j] = -INFINITY;
-      arg[j] = 0;
-    }
-#pragma unroll
-    for (int k = 0; k < 9; ++k) {
-      const int h = 2 * p - 1 + k / 3, w = 2 * q - 1 + k % 3;
-      if (h < 0 || h >= H || w < 0 || w >= W) continue;
-      float f[8];
-      unpack8(*reinterpret_cast<const uint4*>(x + ((int64_t(n) * H + h) * W + w) * C + c0), f);
-#pragma unroll
-      for (int j = 0; j < 8; ++j)
-        if (f[j] > best[j]) {
-          best[j] = f[j];
-          arg[j] = k;
-        }
-    }
-    uint2 packed;
-    packed.x = arg[0] | (arg[1] << 8) | (arg[2] << 16) | (arg[3] << 24);
-    packed.y = arg[4] | (arg[5] << 8) | (arg[6] << 16) | (arg[7] << 24);
-    reinterpret_cast<uint2*>(idx)[i] = packed;
+  for (int j = 0; j < 8; ++j) {
+    best[j] = -INFINITY;
+    arg[j] = 0;
   }
+#pragma unroll
+  for (int k = 0; k < 9; ++k) {
+    const int h = 2 * p - 1 + k / 3, w = 2 * q - 1 + k % 3;
+    if (h < 0 || h >= H || w < 0 || w >= W) continue;
+    float f[8];
+    unpack8(*reinterpret_cast<const uint4*>(x + ((int64_t(n) * H + h) * W + w) * C + c0), f);
+#pragma unroll
+    for (int j = 0; j < 8; ++j)
+      if (f[j] > best[j]) {
+        best[j] = f[j];
+        arg[j] = k;
+      }
+  }
+  uint2 packed;
+  packed.x = arg[0] | (arg[1] << 8) | (arg[2] << 16) | (arg[3] << 24);
+  packed.y = arg[4] | (arg[5] << 8) | (arg[6] << 16) | (arg[7] << 24);
+  reinterpret_cast<uint2*>(idx)[(int64_t(blockIdx.x) * Q + q) * cg + (c0 >> 3)] = packed;
 }
 
+// Thread per (output window (p, q), 8 channels): writes the 2x2 input block
+// rows {2p, 2p+1} x cols {2q, 2q+1} (H = 2P, W = 2Q: a partition of the
+// input).  Even rows/cols lie in one window, odd ones in two: the block sums
+// windows (p..p+1, q..q+1), in a fixed order, where their argmax lands.
 __global__ void __launch_bounds__(256)
     k_maxpool_bwd_gather(const bf16* __restrict__ dy, const uint8_t* __restrict__ idx,
-                         bf16* __restrict__ dx, int N, int H, int W, int C, int P, int Q) {
-  const int cg = C / 8;
-  const int64_t total = int64_t(N) * H * W * cg;
-  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
-  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < total; i += stride) {
-    const int c0 = int(i % cg) * 8;
-    int64_t t = i / cg;
-    const int w = int(t % W);
-    t /= W;
-    const int h = int(t % H);
-    const int n = int(t / H);
-    float acc[8] = {0};
-    const int p_lo = h / 2, p_hi = min(P - 1, (h + 1) / 2);
-    const int q_lo = w / 2, q_hi = min(Q - 1, (w + 1) / 2);
-    for (int p = p_lo; p <= p_hi; ++p)
-      for (int q = q_lo; q <= q_hi; ++q) {
-        const uint32_t k = uint32_t((h - (2 * p - 1)) * 3 + (w - (2 * q - 1)));
-        const int64_t o = ((int64_t(n) * P + p) * Q + q) * C + c0;
-        const uint2 a = *reinterpret_cast<const uint2*>(idx + o);
-        float g[8];
-        unpack8(*reinterpret_cast<const uint4*>(dy + o), g);
+                         bf16* __restrict__ dx, int N, int H, int W, int C, int P, int Q,
+                         int lcg) {
+  const int cg = 1 << lcg;
+  const int item = blockIdx.y * 256 + threadIdx.x;
+  if (item >= Q * cg) return;
+  const int q = item >> lcg, c0 = (item & (cg - 1)) * 8;
+  const int n = blockIdx.x / P, p = blockIdx.x - n * P;
+  float acc[4][8];
+#pragma unroll
+  for (int b = 0; b < 4; ++b)
+#pragma unroll
+    for (int j = 0; j < 8; ++j) acc[b][j] = 0.f;
+#pragma unroll
+  for (int dp = 0; dp < 2; ++dp)
+#pragma unroll
+    for (int dq = 0; dq < 2; ++dq) {
+      const int pp = p + dp, qq = q + dq;
+      if (pp >= P || qq >= Q) continue;
+      const int64_t o = ((int64_t(n) * P + pp) * Q + qq) * C + c0;
+      const uint2 a = *reinterpret_cast<const uint2*>(idx + o);
+      float g[8];
+      unpack8(*reinterpret_cast<const uint4*>(dy + o), g);
+#pragma unroll
+      for (int b = 0; b < 4; ++b) {
+        // input pixel (2p + (b>>1), 2q + (b&1)) inside window (pp, qq) at tap k
+        const int h = 2 * p + (b >> 1), w = 2 * q + (b & 1);
+        const int kh = h - (2 * pp - 1), kw = w - (2 * qq - 1);
+        if (kh < 0 || kh > 2 || kw < 0 || kw > 2) continue;
+        const uint32_t k = uint32_t(kh * 3 + kw);
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
           const uint32_t aj = ((j < 4 ? a.x : a.y) >> (8 * (j & 3))) & 0xFF;
-          if (aj == k) acc[j] += g[j];
+          if (aj == k) acc[b][j] += g[j];
         }
       }
-    reinterpret_cast<uint4*>(dx)[i] = pack8(acc);
+    }
+#pragma unroll
+  for (int b = 0; b < 4; ++b) {
+    const int h = 2 * p + (b >> 1), w = 2 * q + (b & 1);
+    if (h < H && w < W)
+      reinterpret_cast<uint4*>(dx)[((int64_t(n) * H + h) * W + w) * cg + (c0 >> 3)] =
+          pack8(acc[b]);
   }
 }
 
@@ -802,9 +813,10 @@ cudaError_t add_grad(const void* a, const void* up, int pool_hw, const void* up_
 
 cudaError_t maxpool3x3s2_fwd(const void* x, void* y, int N, int H, int W, int C, cudaStream_t st) {
   const int P = (H + 2 - 3) / 2 + 1, Q = (W + 2 - 3) / 2 + 1;
-  const int64_t total = int64_t(N) * P * Q * (C / 8);
-  k_maxpool_fwd<<<grid_for(total, 256), 256, 0, st>>>(static_cast<const bf16*>(x),
-                                                      static_cast<bf16*>(y), N, H, W, C, P, Q);
+  if (C % 8 || ((C / 8) & (C / 8 - 1))) return cudaErrorInvalidValue;
+  const int lcg = __builtin_ctz(C / 8);
+  k_maxpool_fwd<<<dim3(unsigned(N) * P, (Q * (C / 8) + 255) / 256), 256, 0, st>>>(
+      static_cast<const bf16*>(x), static_cast<bf16*>(y), N, H, W, C, P, Q, lcg);
   return cudaGetLastError();
 }
 
@@ -816,14 +828,14 @@ int64_t maxpool_workspace_bytes(int N, int H, int W, int C) {
 cudaError_t maxpool3x3s2_bwd(const void* dy, const void* x, void* dx, int N, int H, int W, int C,
                              void* ws, cudaStream_t st) {
   const int P = (H + 2 - 3) / 2 + 1, Q = (W + 2 - 3) / 2 + 1;
-  if (C % 8) return cudaErrorInvalidValue;
-  const int64_t outs = int64_t(N) * P * Q * (C / 8);
-  k_maxpool_argmax<<<grid_for(outs, 256), 256, 0, st>>>(static_cast<const bf16*>(x),
-                                                        static_cast<uint8_t*>(ws), N, H, W, C, P, Q);
-  const int64_t total = int64_t(N) * H * W * (C / 8);
-  k_maxpool_bwd_gather<<<grid_for(total, 256), 256, 0, st>>>(
+  if (C % 8 || ((C / 8) & (C / 8 - 1))) return cudaErrorInvalidValue;
+  const int lcg = __builtin_ctz(C / 8);
+  k_maxpool_argmax<<<dim3(unsigned(N) * P, (Q * (C / 8) + 255) / 256), 256, 0, st>>>(
+      static_cast<const bf16*>(x), static_cast<uint8_t*>(ws), N, H, W, C, P, Q, lcg);
+  if (H != 2 * P || W != 2 * Q) return cudaErrorInvalidValue;  // even input sizes
+  k_maxpool_bwd_gather<<<dim3(unsigned(N) * P, (Q * (C / 8) + 255) / 256), 256, 0, st>>>(
       static_cast<const bf16*>(dy), static_cast<const uint8_t*>(ws), static_cast<bf16*>(dx), N, H,
-      W, C, P, Q);
+      W, C, P, Q, lcg);
   return cudaGetLastError();
 }
 

@@ -31,6 +31,10 @@ from . import kernels as K
 from . import planner as P
 
 BN_EPS = 1e-5
+# BN statistics are reduced in the conv epilogue when the conv's reduction
+# length is at least this (the epilogue work hides under the main loop);
+# shorter convs get a separate streaming statistics pass.
+FUSE_STATS_MIN_KDIM = int(__import__("os").environ.get("DELTA_FUSE_STATS_MIN_KDIM", "384"))
 BN_MOMENTUM = 0.1
 
 
@@ -240,7 +244,7 @@ class DeltaRuntime:
                 conv = K.Conv(Nb, H, W, C, cs.cout, cs.k, cs.k, cs.stride, cs.pad, wptr)
                 assert (conv.P, conv.Q) == n.shape[1:3], (n.name, conv.P, conv.Q, n.shape)
                 self._convs[n.name] = conv
-                self._fuse_stats[n.name] = conv.kdim >= 384
+                self._fuse_stats[n.name] = conv.kdim >= FUSE_STATS_MIN_KDIM
                 if own_dgrad(cs):
                     # on the conv's output grid (a stride-2 1x1's gradient lives at
                     # its sampling points; the consumer scatters it)

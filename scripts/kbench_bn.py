@@ -39,3 +39,22 @@ for (H, C) in [(56, 256), (56, 64), (28, 512), (14, 1024), (7, 2048)]:
                     key = base + ("_mask" if name == "bwd_mask" and "bwd" in base else "")
                     out[f"{name}:{base}"] = dict(us=round(us, 1), gbs=round(byts.get(key, 0) / us / 1e3, 1))
     print(json.dumps(out), flush=True)
+
+# max pool 3x3/2 on the stem output (N, 112, 112, 64)
+x = torch.relu(torch.randn(N, 112, 112, 64, device="cuda")).to(torch.bfloat16)
+y = torch.empty(N, 56, 56, 64, device="cuda", dtype=torch.bfloat16)
+dy = torch.randn(N, 56, 56, 64, device="cuda").to(torch.bfloat16)
+dx = torch.empty_like(x)
+ws = torch.empty(K.maxpool_workspace_bytes(N, 112, 112, 64), dtype=torch.uint8, device="cuda")
+def t(fn, iters=10):
+    for _ in range(3): fn()
+    s_, e_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize(); s_.record()
+    for _ in range(iters): fn()
+    e_.record(); torch.cuda.synchronize()
+    return s_.elapsed_time(e_) / iters * 1e3
+tf = t(lambda: K.maxpool_fwd(x.data_ptr(), y.data_ptr(), N, 112, 112, 64, st))
+tb = t(lambda: K.maxpool_bwd(dy.data_ptr(), x.data_ptr(), dx.data_ptr(), N, 112, 112, 64, ws.data_ptr(), st))
+print(json.dumps(dict(maxpool_fwd_us=round(tf, 1), fwd_gbs=round((x.numel() + y.numel()) * 2 / tf / 1e3),
+                      maxpool_bwd_us=round(tb, 1),
+                      bwd_gbs=round((x.numel() * 2 + dy.numel() * 2 * 2 + ws.numel() * 2 + dx.numel() * 2) / tb / 1e3))))
