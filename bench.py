@@ -242,12 +242,9 @@ def main():
         rt.step_device()  # eager warm step (cuDNN autotune, allocator)
         torch.cuda.synchronize()
         if not args.no_graph:
-            l0 = K.LAUNCHES[0]
             rt.capture()
-            launches = K.LAUNCHES[0] - l0
-        else:
-            launches = None
-        return prog, launches
+        # our kernel launches per step, counted from the bound recipes
+        return prog, rt.executor.launches_per_step
 
     # ---- no-eviction upper bound (same kernels, Baseline policy) ----
     base_prog, _ = prepare(None)
@@ -298,14 +295,13 @@ def main():
     swap_ms, swap_bytes, swap_n = 0.0, 0, 0
     for nid, lst in timing.items():
         if nid == "swap":
-            for (a, b, op, nb) in lst:
-                swap_ms += a.elapsed_time(b)
+            for (ms, op, nb) in lst:
+                swap_ms += ms
                 swap_bytes += nb
                 swap_n += 1
             continue
         node = rt.nodes[nid]
-        for (a, b, rec) in lst:
-            ms = a.elapsed_time(b)
+        for (ms, rec) in lst:
             all_ms += ms
             kinds[node.op] = kinds.get(node.op, 0.0) + ms
             if node.op == "conv":
@@ -433,7 +429,7 @@ def main():
                              "peak = PCIe Gen5 x16 nominal per direction"},
             "max_batch": max_batch,
             "cpu_baseline": cpu,
-            "gpu_launches": (launches * args.steps) if launches is not None else None,
+            "gpu_launches": launches * args.steps,
             "clocks": clk,
         }
         print(json.dumps(line), flush=True)

@@ -111,6 +111,12 @@ namespace delta_rt {
 void set_error(const std::string& msg) { g_err = msg; }
 }  // namespace delta_rt
 
+// for translation units that also see the C type `delta_rt` (rt/executor.cu)
+void delta_set_error(const std::string& msg) { delta_rt::set_error(msg); }
+
+namespace delta_rt {
+}  // namespace delta_rt
+
 extern "C" {
 
 const char* delta_last_error(void) { return g_err.c_str(); }

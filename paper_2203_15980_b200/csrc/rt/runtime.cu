@@ -9,6 +9,7 @@
 
 #include "delta/delta_kernels.h"
 #include "kernels/kernels.hpp"
+#include "rt/handles.hpp"
 
 namespace delta_rt {
 void set_error(const std::string& msg);  // capi.cpp
@@ -27,11 +28,6 @@ delta_status cuda_status(cudaError_t e, const char* what) {
 inline cudaStream_t S(void* p) { return static_cast<cudaStream_t>(p); }
 
 }  // namespace
-
-struct delta_conv {
-  delta_k::ConvPlan plan;
-  const void* weight = nullptr;
-};
 
 struct delta_swap {
   void* host = nullptr;

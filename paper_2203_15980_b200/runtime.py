@@ -26,6 +26,7 @@ from dataclasses import dataclass
 import numpy as np
 import torch
 
+from . import executor as X
 from . import graph as G
 from . import kernels as K
 from . import planner as P
@@ -221,8 +222,10 @@ class DeltaRuntime:
         self._loss_host = None
         self.program = None
         self.arena = None
-        self.swap = None
-        self.events = None
+        self.executor = None
+        self._bound_slot = None
+        self._keep = []
+        self._cur_parents = ()
         self.graph = None
         self.cost_table = None
         self.link_gbs = None
@@ -292,18 +295,15 @@ class DeltaRuntime:
         self.graph = None
         self.graphs = None
         if self.arena is None or self.arena.numel() < prog.arena_bytes:
+            self.executor = None
             self.arena = None
             torch.cuda.empty_cache()
             self.arena = torch.empty(prog.arena_bytes, dtype=torch.uint8, device=self.device)
-        if prog.host_bytes and (self.swap is None or self._swap_bytes < prog.host_bytes):
-            self.swap = K.Swap(prog.host_bytes)
-            self._swap_bytes = prog.host_bytes
-        if self.swap is None:
-            self.swap = K.Swap(0)
-            self._swap_bytes = 0
-        self.events = K.Events(prog.n_events)
+        if self.executor is None or self.executor.host_bytes < prog.host_bytes:
+            host = max(prog.host_bytes, self.executor.host_bytes if self.executor else 0)
+            self.executor = X.Executor(_ptr(self.arena), self.arena.numel(), host)
         self._base = _ptr(self.arena)
-        self._inputs = prog.inputs
+        self._bound_slot = None
         return prog
 
     # -------------------------------------------------------- tensors
@@ -313,166 +313,222 @@ class DeltaRuntime:
         return self.arena.narrow(0, off, n * node.dtype_bytes).view(dt).view(node.shape)
 
     # ------------------------------------------------------------ ops
-    def _run_node(self, node: G.Node, out_off: int, in_offs, recompute: bool, st: int):
-        base = self._base
-        op = node.op
-        out = base + out_off
-        ins = [base + o for o in in_offs]
+    # ------------------------------------------------------------ recipes
+    def _recipe(self, node: G.Node, host) -> tuple:
+        """The kernel ops that (re)produce `node` on the executor: symbolic
+        arena operands (OUT, IN(i)), parameter / workspace pointers, HOST ops
+        (registered through `host`) for the library calls.  Returns (ops,
+        (launches of our kernels on first production, on recompute))."""
         pr = self.params
+        op = node.op
+        ops = []
+        nl = [0, 0]
+
+        def add(k, first=1, rec=1):
+            ops.append(k)
+            if not (k.flags & X.RECOMPUTE_ONLY):
+                nl[0] += first
+            if not (k.flags & X.FIRST_ONLY):
+                nl[1] += rec
+
+        M = int(np.prod(node.shape[:-1])) if len(node.shape) == 4 else 0
+        C = node.shape[-1]
+        bnp = lambda bn: (_ptr(pr.bn_mean[bn]), _ptr(pr.bn_invstd[bn]))
+        gb = lambda bn: (_ptr(pr.views["bn_g:" + bn]), _ptr(pr.views["bn_b:" + bn]))
+        dgb = lambda bn: (_ptr(pr.gviews["bn_g:" + bn]), _ptr(pr.gviews["bn_b:" + bn]))
+
+        def stats(conv_node_id, src_ref, bn, scratch):
+            """training-mode BN statistics (first production only: a recompute
+            reuses them): from the conv epilogue's partials when that conv is
+            long enough to hide the work, else one streaming pass."""
+            conv = self.nodes[conv_node_id]
+            tail = (_ptr(pr.bn_mean[bn]), _ptr(pr.bn_invstd[bn]), _ptr(pr.bn_rmean[bn]),
+                    _ptr(pr.bn_rvar[bn]))
+            if self._fuse_stats.get(conv.name):
+                add(X.kop(X.K_BN_STATS_PARTS, (_ptr(scratch), None) + tail, (M, C, 128),
+                          (BN_EPS, BN_MOMENTUM), flags=X.FIRST_ONLY),
+                    K._merge_launches((M + 127) // 128), 0)
+            else:
+                add(X.kop(X.K_BN_STATS, (src_ref, _ptr(self.bn_ws)) + tail, (M, C),
+                          (BN_EPS, BN_MOMENTUM), flags=X.FIRST_ONLY),
+                    1 + K._merge_launches(K._chunks(M, C)), 0)
+
         if op == "input":
-            self._view(out_off, node).copy_(self.x_dev, non_blocking=True)
+            add(X.kop(X.K_COPY, (X.OUT(), _ptr(self.x_dev)), (self.x_dev.numel() * 2,)))
         elif op == "conv":
             # the first production also emits BN statistics partials from the
             # epilogue; a recompute must not (the scratch may be in use)
-            scratch = None
-            if not recompute and self._fuse_stats[node.name]:
-                scratch = _ptr(self.stats_ds if "downsample" in node.name else self.stats_main)
-            self._convs[node.name](ins[0], out, st, scratch)
+            conv = self._convs[node.name]._h
+            if self._fuse_stats[node.name]:
+                scratch = self.stats_ds if "downsample" in node.name else self.stats_main
+                add(X.kop(X.K_CONV, (X.IN(0), X.OUT(), _ptr(scratch)), conv=conv,
+                          flags=X.FIRST_ONLY))
+                add(X.kop(X.K_CONV, (X.IN(0), X.OUT(), None), conv=conv, flags=X.RECOMPUTE_ONLY))
+            else:
+                add(X.kop(X.K_CONV, (X.IN(0), X.OUT(), None), conv=conv))
         elif op in ("bn_relu", "bn_add_relu", "bn_bn_add_relu"):
             bn = node.attrs["bn"]
-            M = int(np.prod(node.shape[:-1]))
-            C = node.shape[-1]
-            if not recompute:  # statistics once per step; recompute reuses them
-                self._bn_stats(node.parents[0], ins[0], bn, self.stats_main, M, C, st)
-            args = [_ptr(pr.bn_mean[bn]), _ptr(pr.bn_invstd[bn]), _ptr(pr.views["bn_g:" + bn]),
-                    _ptr(pr.views["bn_b:" + bn])]
-            if op == "bn_relu":
-                K.bn_apply(0, ins[0], None, out, M, C, *args, stream=st)
-            elif op == "bn_add_relu":
-                K.bn_apply(1, ins[0], ins[1], out, M, C, *args, stream=st)
-            else:
+            stats(node.parents[0], X.IN(0), bn, self.stats_main)
+            mode = {"bn_relu": 0, "bn_add_relu": 1, "bn_bn_add_relu": 2}[op]
+            p2 = (None,) * 4
+            if mode == 2:
                 bn2 = node.attrs["bn2"]
-                if not recompute:
-                    self._bn_stats(node.parents[1], ins[1], bn2, self.stats_ds, M, C, st)
-                K.bn_apply(2, ins[0], ins[1], out, M, C, *args, _ptr(pr.bn_mean[bn2]),
-                           _ptr(pr.bn_invstd[bn2]), _ptr(pr.views["bn_g:" + bn2]),
-                           _ptr(pr.views["bn_b:" + bn2]), stream=st)
+                stats(node.parents[1], X.IN(1), bn2, self.stats_ds)
+                p2 = bnp(bn2) + gb(bn2)
+            add(X.kop(X.K_BN_APPLY, (X.IN(0), X.IN(1) if mode else None, X.OUT()) + bnp(bn)
+                      + gb(bn) + p2, (mode, M, C)))
         elif op == "maxpool":
-            src = self.nodes[node.parents[0]]
-            Nb, H, W, C = src.shape
-            K.maxpool_fwd(ins[0], out, Nb, H, W, C, st)
+            Nb, H, W, Cs = self.nodes[node.parents[0]].shape
+            add(X.kop(X.K_MAXPOOL_FWD, (X.IN(0), X.OUT()), (Nb, H, W, Cs)))
         elif op == "avgpool":
-            src = self.nodes[node.parents[0]]
-            Nb, H, W, C = src.shape
-            K.avgpool_fwd(ins[0], out, Nb, H * W, C, st)
+            Nb, H, W, Cs = self.nodes[node.parents[0]].shape
+            add(X.kop(X.K_AVGPOOL, (X.IN(0), X.OUT()), (Nb, H * W, Cs)))
         elif op == "fc":
-            a = self._view(in_offs[0], self.nodes[node.parents[0]])
-            torch.addmm(pr.views["fc_b"], a.float(), pr.views["fc_w"].t(),
-                        out=self._view(out_off, node))
+            src = self.nodes[node.parents[0]]
+
+            def fc(out, ins, rec, stream, node=node, src=src):
+                a_ = self._view(ins[0] - self._base, src)
+                torch.addmm(pr.views["fc_b"], a_.float(), pr.views["fc_w"].t(),
+                            out=self._view(out - self._base, node))
+            add(X.kop(X.K_HOST, (), (host(fc),)), 0, 0)
         elif op == "fc_bwd":
-            logits = self._view(in_offs[0], self.nodes[node.parents[0]])
-            a = self._view(in_offs[1], self.nodes[node.parents[1]])
-            Nb, ncls = logits.shape
-            K.softmax_xent(_ptr(logits), _ptr(self.y_dev), _ptr(self.loss), _ptr(self.dlogits),
-                           _ptr(self.row_loss), Nb, ncls, st)
-            torch.mm(self.dlogits.t(), a.float(), out=pr.gviews["fc_w"])
-            torch.sum(self.dlogits, 0, out=pr.gviews["fc_b"])
-            self._view(out_off, node).copy_(self.dlogits @ pr.views["fc_w"])
+            logits_n, src = self.nodes[node.parents[0]], self.nodes[node.parents[1]]
+            Nb, ncls = logits_n.shape
+            add(X.kop(X.K_SOFTMAX_XENT, (X.IN(0), _ptr(self.y_dev), _ptr(self.loss),
+                                         _ptr(self.dlogits), _ptr(self.row_loss)), (Nb, ncls)), 2, 2)
+
+            def fc_bwd(out, ins, rec, stream, node=node, src=src):
+                a_ = self._view(ins[1] - self._base, src)
+                torch.mm(self.dlogits.t(), a_.float(), out=pr.gviews["fc_w"])
+                torch.sum(self.dlogits, 0, out=pr.gviews["fc_b"])
+                self._view(out - self._base, node).copy_(self.dlogits @ pr.views["fc_w"])
+            add(X.kop(X.K_HOST, (), (host(fc_bwd),)), 0, 0)
         elif op == "bn_add_relu_bwd":
             # parents: [upstream, (O if masked,) X]; upstream already masked
             # unless it is the pooled head gradient
             bn = node.attrs["bn"]
-            M = int(np.prod(node.shape[:-1]))
-            C = node.shape[-1]
             pool_hw = int(node.shape[1] * node.shape[2]) if node.attrs.get("from_pool") else 0
-            mask = ins[1] if node.attrs.get("masked") else None
-            K.bn_backward(ins[0], pool_hw, mask, ins[-1], out, M, C, _ptr(pr.bn_mean[bn]),
-                          _ptr(pr.bn_invstd[bn]), _ptr(pr.views["bn_g:" + bn]),
-                          _ptr(pr.gviews["bn_g:" + bn]), _ptr(pr.gviews["bn_b:" + bn]),
-                          _ptr(self.bn_ws), st)
+            mask = X.IN(1) if node.attrs.get("masked") else None
+            add(X.kop(X.K_BN_BWD, (X.IN(0), mask, X.IN(len(node.parents) - 1), X.OUT()) + bnp(bn)
+                      + (gb(bn)[0],) + dgb(bn) + (_ptr(self.bn_ws),), (pool_hw, M, C)), 3, 3)
         elif op == "conv_bn_relu_bwd":
             # parents [dC, R = relu(bn(X)), X]
-            conv = node.attrs["conv"]
-            bn = node.attrs["bn"]
-            dC = self._view(in_offs[0], self.nodes[node.parents[0]])
-            R = self._view(in_offs[1], self.nodes[node.parents[1]])
-            M = int(np.prod(node.shape[:-1]))
-            C = node.shape[-1]
-            bnp = (_ptr(pr.bn_mean[bn]), _ptr(pr.bn_invstd[bn]))
+            conv, bn = node.attrs["conv"], node.attrs["bn"]
             if conv in self._dconvs:
-                # dgrad on the tensor cores; the epilogue applies the ReLU mask
-                # (recomputed from X) and reduces sum g, sum g*X per tile
-                g_ptr = out  # g is written in place of its BN-backward output
-                self._dconvs[conv].bn_bwd(ins[0], g_ptr, _ptr(self.stats_main), ins[2], *bnp,
-                                          _ptr(pr.views["bn_g:" + bn]), _ptr(pr.views["bn_b:" + bn]),
-                                          st)
-                K.bn_backward_from_partials(_ptr(self.stats_main), g_ptr, ins[2], out, M, C, *bnp,
-                                            _ptr(pr.views["bn_g:" + bn]),
-                                            _ptr(pr.gviews["bn_g:" + bn]),
-                                            _ptr(pr.gviews["bn_b:" + bn]), st)
-                self._conv_bwd(conv, dC, R, need_dx=False)
+                wg = host(self._wgrad_op(conv, node.parents[0], node.parents[1]))
+                # dgrad on the tensor cores; its epilogue applies the ReLU mask
+                # (recomputed from X) and reduces sum g, sum g*X per tile; g is
+                # written in place of its BN-backward output
+                add(X.kop(X.K_CONV_EX, (X.IN(0), X.OUT(), _ptr(self.stats_main), None, None, None,
+                                        X.IN(2)) + bnp(bn) + gb(bn),
+                          (K.EPI_BN_BWD, 0, 0), conv=self._dconvs[conv]._h))
+                add(X.kop(X.K_BN_BWD_PARTS, (_ptr(self.stats_main), X.OUT(), X.IN(2), X.OUT())
+                          + bnp(bn) + (gb(bn)[0],) + dgb(bn), (0, M, C)),
+                    1 + K._merge_launches((M + 127) // 128), 0)
+                add(X.kop(X.K_HOST, (), (wg,)), 0, 0)
             else:
-                dR = self._conv_bwd(conv, dC, R, need_dx=True)
-                K.bn_backward(_ptr(dR), 0, ins[1], ins[2], out, M, C, *bnp,
-                              _ptr(pr.views["bn_g:" + bn]), _ptr(pr.gviews["bn_g:" + bn]),
-                              _ptr(pr.gviews["bn_b:" + bn]), _ptr(self.bn_ws), st)
+                # cuDNN dgrad + wgrad in one call; the input gradient -> SCRATCH(0)
+                dg = host(self._dgrad_op(conv, node.parents[0], node.parents[1]))
+                add(X.kop(X.K_HOST, (), (dg,)), 0, 0)
+                add(X.kop(X.K_BN_BWD, (X.SCRATCH(0), X.IN(1), X.IN(2), X.OUT()) + bnp(bn)
+                          + (gb(bn)[0],) + dgb(bn) + (_ptr(self.bn_ws),), (0, M, C)), 3, 3)
         elif op == "conv_shortcut_bwd":
             # out = (dgrad(conv1, dC1) + shortcut gradient) * [X > 0]; the sum
             # and the mask are the dgrad kernel's epilogue
             conv = node.attrs["conv"]
-            dC1 = self._view(in_offs[0], self.nodes[node.parents[0]])
-            X = self._view(in_offs[1], self.nodes[node.parents[1]])
-            out_mask = ins[1] if node.attrs.get("mask_out") else None
-            add, pool_hw, add_mask, stride2 = None, 0, None, False
+            out_mask = X.IN(1) if node.attrs.get("mask_out") else None
+            add_, pool_hw, add_mask, stride2 = None, 0, None, 0
+            n_host = 0
             if "conv_short" in node.attrs:
                 short = node.attrs["conv_short"]
-                dCD = self._view(in_offs[2], self.nodes[node.parents[2]])
                 if short in self._dconvs:
                     if self.g.convs[short].stride == 1:
-                        add = out   # summed in place by conv1's dgrad epilogue
+                        dst = X.OUT()   # summed in place by conv1's dgrad epilogue
                     else:
-                        add, stride2 = _ptr(self.short_ws), True  # at its sampling grid
-                    self._dconvs[short](ins[2], add, st)
-                    self._conv_bwd(short, dCD, X, need_dx=False)
-                else:
-                    dXs = self._conv_bwd(short, dCD, X, need_dx=True)
-                    add = _ptr(dXs)
+                        dst, stride2 = _ptr(self.short_ws), 1  # at its sampling grid
+                    add(X.kop(X.K_CONV, (X.IN(2), dst, None), conv=self._dconvs[short]._h))
+                    add_ = dst
+                    add(X.kop(X.K_HOST, (), (host(self._wgrad_op(short, node.parents[2],
+                                                                  node.parents[1])),)), 0, 0)
+                    n_host += 1
+                else:  # cuDNN dgrad + wgrad in one call
+                    add(X.kop(X.K_HOST, (), (host(self._dgrad_op(short, node.parents[2],
+                                                                  node.parents[1])),)), 0, 0)
+                    add_ = X.SCRATCH(n_host)
+                    n_host += 1
             elif node.attrs.get("from_pool"):
-                add, pool_hw, add_mask = ins[2], int(node.shape[1] * node.shape[2]), ins[3]
+                add_, pool_hw, add_mask = X.IN(2), int(node.shape[1] * node.shape[2]), X.IN(3)
             else:
-                add = ins[2]
-            if conv in self._dconvs:
-                self._dconvs[conv].add_mask(ins[0], out, st, add=add, pool_hw=pool_hw,
-                                            add_mask=add_mask, out_mask=out_mask,
-                                            add_stride2=stride2)
-                self._conv_bwd(conv, dC1, X, need_dx=False)
-            else:
-                dX = self._conv_bwd(conv, dC1, X, need_dx=True)
-                M = int(np.prod(node.shape[:-1]))
-                K.add_grad(_ptr(dX), add, pool_hw, add_mask, out_mask, out, M, node.shape[-1], st)
+                add_ = X.IN(2)
+            if conv not in self._dconvs:
+                raise RuntimeError(f"{node.name}: the shortcut's conv1 must be a 1x1 (own dgrad)")
+            add(X.kop(X.K_CONV_EX, (X.IN(0), X.OUT(), None, add_, add_mask, out_mask),
+                      (K.EPI_ADD_MASK, pool_hw, stride2), conv=self._dconvs[conv]._h))
+            add(X.kop(X.K_HOST, (), (host(self._wgrad_op(conv, node.parents[0],
+                                                          node.parents[1])),)), 0, 0)
         elif op == "maxpool_bwd":
-            src = self.nodes[node.parents[1]]
-            Nb, H, W, C = src.shape
-            K.maxpool_bwd(ins[0], ins[1], out, Nb, H, W, C, _ptr(self.mp_ws), st)
+            Nb, H, W, Cs = self.nodes[node.parents[1]].shape
+            add(X.kop(X.K_MAXPOOL_BWD, (X.IN(0), X.IN(1), X.OUT(), _ptr(self.mp_ws)),
+                      (Nb, H, W, Cs)), 2, 2)
         elif op == "bn_relu_bwd":
             bn = node.attrs["bn"]
-            M = int(np.prod(node.shape[:-1]))
-            C = node.shape[-1]
-            K.bn_backward(ins[0], 0, ins[1], ins[2], out, M, C, _ptr(pr.bn_mean[bn]),
-                          _ptr(pr.bn_invstd[bn]), _ptr(pr.views["bn_g:" + bn]),
-                          _ptr(pr.gviews["bn_g:" + bn]), _ptr(pr.gviews["bn_b:" + bn]),
-                          _ptr(self.bn_ws), st)
+            add(X.kop(X.K_BN_BWD, (X.IN(0), X.IN(1), X.IN(2), X.OUT()) + bnp(bn) + (gb(bn)[0],)
+                      + dgb(bn) + (_ptr(self.bn_ws),), (0, M, C)), 3, 3)
         elif op == "conv_wgrad":
             conv = node.attrs["conv"]
-            dC = self._view(in_offs[0], self.nodes[node.parents[0]])
-            X = self._view(in_offs[1], self.nodes[node.parents[1]])
-            self._conv_bwd(conv, dC, X, need_dx=False)
-            self._view(out_off, node).copy_(pr.gviews["conv:" + conv])
+            wg = self._wgrad_op(conv, node.parents[0], node.parents[1])
+
+            def wgrad_out(out, ins, rec, stream, node=node, conv=conv, wg=wg):
+                wg(out, ins, rec, stream)
+                self._view(out - self._base, node).copy_(pr.gviews["conv:" + conv])
+            add(X.kop(X.K_HOST, (), (host(wgrad_out),)), 0, 0)
         else:
             raise RuntimeError(f"no kernel for op {op!r} (node {node.name})")
+        return ops, tuple(nl)
 
-    def _bn_stats(self, conv_node_id: int, x_ptr: int, bn: str, scratch, M: int, C: int, st):
-        """Training-mode BN statistics of a conv output: from the partials the
-        conv epilogue wrote when the conv is long enough to hide that work,
-        else one streaming pass over the tensor."""
-        pr = self.params
-        conv = self.nodes[conv_node_id]
-        args = (_ptr(pr.bn_mean[bn]), _ptr(pr.bn_invstd[bn]), BN_EPS, _ptr(pr.bn_rmean[bn]),
-                _ptr(pr.bn_rvar[bn]), BN_MOMENTUM)
-        if self._fuse_stats.get(conv.name):
-            K.bn_stats_from_partials(_ptr(scratch), M, C, *args, st)
-        else:
-            K.bn_stats(x_ptr, M, C, _ptr(self.bn_ws), *args, st)
+    def _arena_view(self, ptr: int, node_id: int) -> torch.Tensor:
+        return self._view(ptr - self._base, self.nodes[node_id])
+
+    def _wgrad_op(self, conv: str, dy_node: int, x_node: int):
+        """HOST op: cuDNN weight gradient (fp32 KRSC into the flat grad buffer).
+        Input slots are located by node id among the consumer's parents (set
+        by _bind's host-op wrapper)."""
+        def op(out, ins, rec, stream):
+            node = self._cur_parents
+            dY = self._arena_view(ins[node.index(dy_node)], dy_node)
+            Xv = self._arena_view(ins[node.index(x_node)], x_node)
+            self._conv_bwd(conv, dY, Xv, need_dx=False)
+        return op
+
+    def _dgrad_op(self, conv: str, dy_node: int, x_node: int):
+        """HOST op: cuDNN input AND weight gradient (one call); returns the
+        input gradient's device pointer (the recipe's SCRATCH operand), kept
+        alive until the next step."""
+        def op(out, ins, rec, stream):
+            node = self._cur_parents
+            dY = self._arena_view(ins[node.index(dy_node)], dy_node)
+            Xv = self._arena_view(ins[node.index(x_node)], x_node)
+            gi = self._conv_bwd(conv, dY, Xv, need_dx=True)
+            self._keep.append(gi)
+            return _ptr(gi)
+        return op
+
+    def _bind(self):
+        """(Re)build the recipe table for the current input slot and bind it,
+        with the current program, to the executor."""
+        recipes, host_ops, launches = {}, [], {}
+        for node in self.nodes:
+            def host(fn, parents=tuple(node.parents)):
+                def call(out, ins, rec, stream, fn=fn, parents=parents):
+                    self._cur_parents = parents
+                    return fn(out, ins, rec, stream)
+                host_ops.append(call)
+                return len(host_ops) - 1
+            ops, nl = self._recipe(node, host)
+            recipes[node.id] = ops
+            launches[node.id] = nl
+        self.executor.bind(self.program, recipes, host_ops, launches)
+        self._bound_slot = self._slot
 
     def _conv_bwd(self, name: str, dY: torch.Tensor, X: torch.Tensor, need_dx: bool):
         """dgrad/wgrad through cuDNN (channels_last views of arena memory);
@@ -493,82 +549,46 @@ class DeltaRuntime:
     # -------------------------------------------------------- program
     def run_program(self, timing: dict | None = None, probe: dict | None = None,
                     stamps: list | None = None):
-        """Issue one training step: the lowered action program on the three
-        streams, then the optimizer.  Returns nothing; loss stays on device.
-        `timing`: per-node (and "swap") CUDA event pairs; `stamps`: receives
-        (action index, start event, end event) of every compute/recompute/
-        offload/reload action (events on the action's own stream)."""
-        prog = self.program
+        """Issue one training step: the lowered action program through the
+        C++ executor (csrc/rt/executor.cu) on the compute stream and the two
+        copy engines, then the optimizer.  The loss stays on device.
+        `timing`: node id -> [(ms, recomputed)], plus "swap" -> [(ms, op,
+        bytes)]; `probe`: node id -> a clone of its output after its (last)
+        production; `stamps`: receives (action index, start_ms, end_ms) of
+        every compute/recompute/offload/reload action."""
         st = self.stream.cuda_stream
-        streams = {P.STREAM_COMPUTE: st, P.STREAM_D2H: self.swap.d2h_stream,
-                   P.STREAM_H2D: self.swap.h2d_stream}
-        nodes = self.nodes
-        inputs = self._inputs
-        ev = self.events
-        base = self._base
-        n_timed = 0
-        for ai, a in enumerate(prog.actions):
-            op = int(a["op"])
-            if timing is not None and op in (P.ACT_COMPUTE, P.ACT_RECOMPUTE) and n_timed % 24 == 0:
-                # keep the GPU busy while the host queues the next actions, so
-                # the event pairs time device execution, not launch latency
-                torch.cuda._sleep(int(3e7))
-            if op == P.ACT_WAIT:
-                ev.wait(int(a["event"]), streams[int(a["stream"])])
-            elif op == P.ACT_RECORD:
-                ev.record(int(a["event"]), streams[int(a["stream"])])
-            elif op in (P.ACT_COMPUTE, P.ACT_RECOMPUTE):
-                node = nodes[int(a["node"])]
-                at, n_in = int(a["inputs_at"]), int(a["n_inputs"])
-                if timing is None and stamps is not None:
-                    e0 = torch.cuda.Event(enable_timing=True)
-                    e1 = torch.cuda.Event(enable_timing=True)
-                    e0.record(self.stream)
-                if timing is not None:
-                    e0 = torch.cuda.Event(enable_timing=True)
-                    e1 = torch.cuda.Event(enable_timing=True)
-                    e0.record(self.stream)
-                self._run_node(node, int(a["offset"]), [int(x) for x in inputs[at:at + n_in]],
-                               op == P.ACT_RECOMPUTE, st)
-                if probe is not None and node.id in probe:
-                    probe[node.id] = self._view(int(a["offset"]), node).clone()
-                if timing is not None or stamps is not None:
-                    e1.record(self.stream)
-                if timing is not None:
-                    timing.setdefault(node.id, []).append((e0, e1, op == P.ACT_RECOMPUTE))
-                    n_timed += 1
-                if stamps is not None:
-                    stamps.append((ai, e0, e1))
-            elif op in (P.ACT_OFFLOAD, P.ACT_RELOAD):
-                sid = streams[int(a["stream"])]
-                if timing is not None or stamps is not None:
-                    xs = torch.cuda.ExternalStream(sid)
-                    c0 = torch.cuda.Event(enable_timing=True)
-                    c1 = torch.cuda.Event(enable_timing=True)
-                    c0.record(xs)
-                if op == P.ACT_OFFLOAD:
-                    self.swap.offload(base + int(a["offset"]), int(a["host_offset"]),
-                                      int(a["bytes"]), sid)
-                else:
-                    self.swap.reload(base + int(a["offset"]), int(a["host_offset"]),
-                                     int(a["bytes"]), sid)
-                if timing is not None or stamps is not None:
-                    c1.record(xs)
-                if timing is not None:
-                    timing.setdefault("swap", []).append((c0, c1, op, int(a["bytes"])))
-                if stamps is not None:
-                    stamps.append((ai, c0, c1))
-        # join the copy streams that carried work back into the compute stream
-        used = set(int(x) for x in prog.actions["stream"][np.isin(prog.actions["op"], (P.ACT_OFFLOAD, P.ACT_RELOAD))])
-        for sid in sorted(used):
-            e = torch.cuda.Event()
-            e.record(torch.cuda.ExternalStream(streams[sid]))
-            self.stream.wait_event(e)
+        if self._bound_slot != self._slot:
+            self._bind()
+        self._keep = []
+        after = None
+        if probe is not None:
+            def after(ai, node, out):
+                if node in probe:
+                    probe[node] = self._arena_view(out, node).clone()
+        if timing is not None or stamps is not None:
+            t0, t1 = self.executor.step_timed(st, after)
+            acts = self.program.actions
+            for ai, a in enumerate(acts):
+                op = int(a["op"])
+                if op in (P.ACT_COMPUTE, P.ACT_RECOMPUTE, P.ACT_OFFLOAD, P.ACT_RELOAD):
+                    if stamps is not None:
+                        stamps.append((ai, float(t0[ai]), float(t1[ai])))
+                    if timing is not None:
+                        ms = float(t1[ai] - t0[ai])
+                        if op in (P.ACT_COMPUTE, P.ACT_RECOMPUTE):
+                            timing.setdefault(int(a["node"]), []).append(
+                                (ms, op == P.ACT_RECOMPUTE))
+                        else:
+                            timing.setdefault("swap", []).append((ms, op, int(a["bytes"])))
+        else:
+            self.executor.step(st, after)
+        K._count(self.executor.launches_per_step)
         if self.dp is not None:
             # data parallel: one DELTA instance per GPU, gradients averaged
             # with NCCL over NVLink (one flat bucket, on the compute stream)
             allreduce_mean(self.params.grad, self.dp)
         self.params.sgd_step(self.lr)
+
 
     def capture(self):
         """Capture one full step (program + optimizer) as a CUDA graph per
@@ -578,6 +598,7 @@ class DeltaRuntime:
         graphs = []
         for slot in range(2):
             self._use_slot(slot)
+            self._bind()  # the recipe table reads this slot's input buffers
             g = torch.cuda.CUDAGraph()
             with torch.cuda.stream(self.stream):
                 with torch.cuda.graph(g, stream=self.stream):
@@ -662,22 +683,17 @@ class DeltaRuntime:
         latest compute-stream action before them.  Feed it to the
         reference's oracle::replay_check (oracle/ref.replay_check) for an
         independent safety certificate of what the GPU actually did."""
-        prog = self.program
         stamps = []
-        start = torch.cuda.Event(enable_timing=True)
-        torch.cuda.synchronize()
         with torch.cuda.stream(self.stream):
-            start.record(self.stream)
             self.run_program(stamps=stamps)
         torch.cuda.synchronize()
         plan = P.run_iteration(self.trace(), self.config).events
         ev = plan.copy()
         t_of = {}
-        for ai, e0, e1 in stamps:
-            pe = int(prog.actions[ai]["plan_event"])
-            t0 = start.elapsed_time(e0) * 1e3
-            t1 = start.elapsed_time(e1) * 1e3
-            t_of[pe] = (int(round(t0)), max(0, int(round(t1)) - int(round(t0))))
+        for ai, ms0, ms1 in stamps:
+            pe = int(self.program.actions[ai]["plan_event"])
+            t0, t1 = int(round(ms0 * 1e3)), int(round(ms1 * 1e3))
+            t_of[pe] = (t0, max(0, t1 - t0))
         now = 0
         for i in range(len(ev)):
             if i in t_of:
@@ -698,21 +714,14 @@ class DeltaRuntime:
         self.plan(None)
         lr = self.lr
         self.lr = 0.0  # cost probing must not move the weights
-        samples: dict[int, list] = {}
+        if self._bound_slot != self._slot:
+            self._bind()
         with torch.cuda.stream(self.stream):
-            for _ in range(iters + 1):
-                timing = {}
-                self.run_program(timing)
-                torch.cuda.synchronize()
-                for nid, lst in timing.items():
-                    if nid != "swap":
-                        samples.setdefault(nid, []).append(lst[0][0].elapsed_time(lst[0][1]))
+            costs = self.executor.measure_costs(self.stream.cuda_stream, iters, len(self.nodes))
         self.lr = lr
         table = {}
         for n in self.nodes:
-            ms = sorted(samples[n.id][1:]) if len(samples[n.id]) > 1 else samples[n.id]
-            us = ms[len(ms) // 2] * 1e3
-            n.cost_us = max(1, int(math.ceil(us)))
+            n.cost_us = max(1, int(costs[n.id]))
             table[n.name] = n.cost_us
         if link:
             h2d, d2h, _ = K.probe_link()
