@@ -171,29 +171,38 @@ __global__ void __launch_bounds__(256)
 
 // First level of a two-level merge when there are many partials: thread per
 // (channel, group of GROUP consecutive partials) -> one (mean, M2) partial of
-// the group's rows, two passes (sum -> mean, then M2) in a fixed order.
-constexpr int GROUP = 32;
+// the group's rows.  The group's partials are loaded up front (one memory
+// round trip, not GROUP dependent ones), then two passes over registers
+// (sum -> mean, then M2) in a fixed order.
+constexpr int GROUP = 16;
 __global__ void __launch_bounds__(256)
     k_bn_stats_group(const float2* __restrict__ ws, int parts, int64_t rows_per, int64_t M, int C,
                      float2* __restrict__ out) {
   const int c = blockIdx.x * blockDim.x + threadIdx.x;
   if (c >= C) return;
   const int k0 = blockIdx.y * GROUP;
-  const int k1 = min(parts, k0 + GROUP);
   const float n_last = float(M - int64_t(parts - 1) * rows_per);
   const float n_full = float(rows_per);
+  float2 p[GROUP];
+  float nk[GROUP];
+#pragma unroll
+  for (int j = 0; j < GROUP; ++j) {
+    const int k = k0 + j;
+    p[j] = k < parts ? ws[int64_t(k) * C + c] : make_float2(0.f, 0.f);
+    nk[j] = k < parts ? (k == parts - 1 ? n_last : n_full) : 0.f;
+  }
   float s = 0.f, n = 0.f;
-  for (int k = k0; k < k1; ++k) {
-    const float nk = k == parts - 1 ? n_last : n_full;
-    s = fmaf(nk, ws[int64_t(k) * C + c].x, s);
-    n += nk;
+#pragma unroll
+  for (int j = 0; j < GROUP; ++j) {
+    s = fmaf(nk[j], p[j].x, s);
+    n += nk[j];
   }
   const float mu = s / n;
   float m2 = 0.f;
-  for (int k = k0; k < k1; ++k) {
-    const float2 p = ws[int64_t(k) * C + c];
-    const float d = p.x - mu;
-    m2 += fmaf(k == parts - 1 ? n_last : n_full, d * d, p.y);
+#pragma unroll
+  for (int j = 0; j < GROUP; ++j) {
+    const float d = p[j].x - mu;
+    m2 += fmaf(nk[j], d * d, p[j].y);
   }
   out[int64_t(blockIdx.y) * C + c] = make_float2(mu, m2);
 }
@@ -364,12 +373,15 @@ __global__ void __launch_bounds__(256)
   const int c = blockIdx.x * blockDim.x + threadIdx.x;
   if (c >= C) return;
   const int k0 = blockIdx.y * GROUP;
-  const int k1 = min(parts, k0 + GROUP);
+  float2 p[GROUP];
+#pragma unroll
+  for (int j = 0; j < GROUP; ++j)
+    p[j] = k0 + j < parts ? ws[int64_t(k0 + j) * C + c] : make_float2(0.f, 0.f);
   float A = 0.f, B = 0.f;
-  for (int k = k0; k < k1; ++k) {
-    const float2 p = ws[int64_t(k) * C + c];
-    A += p.x;
-    B += p.y;
+#pragma unroll
+  for (int j = 0; j < GROUP; ++j) {
+    A += p[j].x;
+    B += p[j].y;
   }
   out[int64_t(blockIdx.y) * C + c] = make_float2(A, B);
 }
@@ -766,8 +778,17 @@ cudaError_t bn_backward(const void* up, int pool_hw, const void* mask, const voi
                       : (pool_hw ? k_bn_bwd_partial<false, true> : k_bn_bwd_partial<false, false>);
   part<<<chunks, 256, 0, st>>>(U, pool_hw, Mk, X, M, C, chunk, mean, invstd,
                                reinterpret_cast<float2*>(ws));
-  k_bn_bwd_final<<<(C + 7) / 8, 256, 0, st>>>(reinterpret_cast<const float2*>(ws), chunks, C,
-                                              dgamma, dbeta);
+  const float2* w2 = reinterpret_cast<const float2*>(ws);
+  int parts = chunks;
+  if (parts > 2 * GROUP) {  // two-level fixed-order sum (scratch after the partials)
+    const int groups = (parts + GROUP - 1) / GROUP;
+    float2* out = reinterpret_cast<float2*>(ws) + int64_t(parts) * C;
+    const int bx = C < 256 ? C : 256;
+    k_bn_bwd_group<<<dim3((C + bx - 1) / bx, groups), bx, 0, st>>>(w2, parts, C, out);
+    w2 = out;
+    parts = groups;
+  }
+  k_bn_bwd_final<<<(C + 7) / 8, 256, 0, st>>>(w2, parts, C, dgamma, dbeta);
   const int64_t vecs = M * C / 8;
   const auto app = Mk ? (pool_hw ? k_bn_bwd_apply<true, true> : k_bn_bwd_apply<true, false>)
                      : (pool_hw ? k_bn_bwd_apply<false, true> : k_bn_bwd_apply<false, false>);

@@ -134,8 +134,8 @@ def bn_workspace_floats(M: int, C_: int) -> int:
 
 def _merge_launches(parts: int) -> int:
     """Launches of a fixed-order partials merge (bn_pool.cu merge_partials /
-    bn_backward_from_partials): a grouping pass above 2*32 partials."""
-    return 2 if parts > 64 else 1
+    bn_backward*): a grouping pass above 2*GROUP = 32 partials."""
+    return 2 if parts > 32 else 1
 
 
 def _chunks(M: int, C_: int) -> int:
@@ -171,7 +171,7 @@ def bn_apply(mode, x, res, y, M, C_, mean, invstd, gamma, beta, mean2=None, invs
 def bn_backward(up, pool_hw, mask, x, dx, M, C_, mean, invstd, gamma, dgamma, dbeta, ws, stream):
     check(lib.delta_bn_backward(up, pool_hw, mask, x, dx, M, C_, mean, invstd, gamma, dgamma,
                                 dbeta, ws, stream))
-    _count(3)
+    _count(2 + _merge_launches(_chunks(M, C_)))
 
 
 def bn_backward_from_partials(partials, g, x, dx, M, C_, mean, invstd, gamma, dgamma, dbeta,

@@ -333,6 +333,7 @@ class DeltaRuntime:
 
         M = int(np.prod(node.shape[:-1])) if len(node.shape) == 4 else 0
         C = node.shape[-1]
+        bwd_n = 2 + K._merge_launches(K._chunks(M, C)) if M else 0  # streaming BN backward
         bnp = lambda bn: (_ptr(pr.bn_mean[bn]), _ptr(pr.bn_invstd[bn]))
         gb = lambda bn: (_ptr(pr.views["bn_g:" + bn]), _ptr(pr.views["bn_b:" + bn]))
         dgb = lambda bn: (_ptr(pr.gviews["bn_g:" + bn]), _ptr(pr.gviews["bn_b:" + bn]))
@@ -410,7 +411,7 @@ class DeltaRuntime:
             pool_hw = int(node.shape[1] * node.shape[2]) if node.attrs.get("from_pool") else 0
             mask = X.IN(1) if node.attrs.get("masked") else None
             add(X.kop(X.K_BN_BWD, (X.IN(0), mask, X.IN(len(node.parents) - 1), X.OUT()) + bnp(bn)
-                      + (gb(bn)[0],) + dgb(bn) + (_ptr(self.bn_ws),), (pool_hw, M, C)), 3, 3)
+                      + (gb(bn)[0],) + dgb(bn) + (_ptr(self.bn_ws),), (pool_hw, M, C)), bwd_n, bwd_n)
         elif op == "conv_bn_relu_bwd":
             # parents [dC, R = relu(bn(X)), X]
             conv, bn = node.attrs["conv"], node.attrs["bn"]
@@ -431,7 +432,7 @@ class DeltaRuntime:
                 dg = host(self._dgrad_op(conv, node.parents[0], node.parents[1]))
                 add(X.kop(X.K_HOST, (), (dg,)), 0, 0)
                 add(X.kop(X.K_BN_BWD, (X.SCRATCH(0), X.IN(1), X.IN(2), X.OUT()) + bnp(bn)
-                          + (gb(bn)[0],) + dgb(bn) + (_ptr(self.bn_ws),), (0, M, C)), 3, 3)
+                          + (gb(bn)[0],) + dgb(bn) + (_ptr(self.bn_ws),), (0, M, C)), bwd_n, bwd_n)
         elif op == "conv_shortcut_bwd":
             # out = (dgrad(conv1, dC1) + shortcut gradient) * [X > 0]; the sum
             # and the mask are the dgrad kernel's epilogue
@@ -473,7 +474,7 @@ class DeltaRuntime:
         elif op == "bn_relu_bwd":
             bn = node.attrs["bn"]
             add(X.kop(X.K_BN_BWD, (X.IN(0), X.IN(1), X.IN(2), X.OUT()) + bnp(bn) + (gb(bn)[0],)
-                      + dgb(bn) + (_ptr(self.bn_ws),), (0, M, C)), 3, 3)
+                      + dgb(bn) + (_ptr(self.bn_ws),), (0, M, C)), bwd_n, bwd_n)
         elif op == "conv_wgrad":
             conv = node.attrs["conv"]
             wg = self._wgrad_op(conv, node.parents[0], node.parents[1])
@@ -502,14 +503,17 @@ class DeltaRuntime:
 
     def _dgrad_op(self, conv: str, dy_node: int, x_node: int):
         """HOST op: cuDNN input AND weight gradient (one call); returns the
-        input gradient's device pointer (the recipe's SCRATCH operand), kept
-        alive until the next step."""
+        input gradient's device pointer (the recipe's SCRATCH operand)."""
         def op(out, ins, rec, stream):
             node = self._cur_parents
             dY = self._arena_view(ins[node.index(dy_node)], dy_node)
             Xv = self._arena_view(ins[node.index(x_node)], x_node)
             gi = self._conv_bwd(conv, dY, Xv, need_dx=True)
-            self._keep.append(gi)
+            # the caching allocator is stream-ordered: once dropped, this block
+            # is only reused by allocations enqueued after the recipe's consumer
+            # of it; holding the latest one just keeps the pointer valid until
+            # the executor has enqueued that consumer
+            self._keep = [gi]
             return _ptr(gi)
         return op
 

@@ -50,6 +50,8 @@ def run(depth, batch, anchors, delta, steps=2):
                peak_alloc_gb=round(torch.cuda.max_memory_allocated() / 1e9, 2),
                img_s=round(batch / dt, 1), loss=losses[-1])
     del rt, prog
+    import gc
+    gc.collect()  # the executor's host callbacks close a reference cycle
     torch.cuda.empty_cache()
     return res
 
@@ -62,6 +64,9 @@ for depth in (50, 101):
     free = torch.cuda.mem_get_info()[0] - MARGIN - 2 * 2**30  # params/optimizer (~0.4 GB) + slack
     b = MB.search(depth, free, per_sample(depth), int(LINK * 1e3), delta=False)
     d = MB.search(depth, free, per_sample(depth), int(LINK * 1e3), delta=True, anchors="out")
+    if b is None or d is None:
+        print(json.dumps(dict(depth=depth, error="no feasible batch", free_gb=free / 1e9)))
+        continue
     entry = dict(depth=depth, planned_no_eviction=b.batch, planned_delta=d.batch,
                  ratio=round(d.batch / b.batch, 3))
     try:

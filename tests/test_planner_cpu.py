@@ -199,10 +199,11 @@ def test_live_reference_fuzz():
 # ------------------------------------------------------------- C ABI surface
 def test_c_abi_exports_every_declared_symbol():
     names = set()
-    for h in ("delta.h", "delta_kernels.h"):
+    for h in ("delta.h", "delta_kernels.h", "delta_rt.h"):
         text = open(os.path.join(ROOT, "include", "delta", h)).read()
         names |= set(re.findall(r"^[\w ]*?[\w\*]+\s+\**(delta_[a-z0-9_]+)\s*\(", text, re.M))
-    assert len(names) > 50
+    assert len(names) > 60
+    assert {"delta_rt_create", "delta_rt_bind", "delta_rt_step", "delta_rt_measure_costs"} <= names
     missing = [n for n in sorted(names) if not hasattr(lib, n)]
     assert not missing, missing
     out = subprocess.run(["nm", "-D", "--defined-only", LIB_PATH], capture_output=True, text=True)
