@@ -75,6 +75,19 @@ delta_status delta_conv_geometry(const delta_conv* c, int32_t* P, int32_t* Q, in
                                  int32_t* tile_n);
 void delta_conv_destroy(delta_conv* c);
 
+/* ---- backward: convolution weight gradient ----
+ * dW[k][r][s][c] = sum over output pixels of dY[n,p,q,k] * X[n, p*st-pad+r,
+ * q*st-pad+s, c]; fp32 KRSC output (overwritten), deterministic split-K over
+ * pixels (tcgen05, MN-major operands).  C == 4 is the 7x7/2 stem (input
+ * channel 3 is the zero pad).  `ws` must hold delta_wgrad_workspace_bytes. */
+typedef struct delta_wgrad delta_wgrad;
+delta_status delta_wgrad_create(int32_t N, int32_t H, int32_t W, int32_t C, int32_t K, int32_t R,
+                                int32_t S, int32_t stride, int32_t pad, delta_wgrad** out);
+uint64_t delta_wgrad_workspace_bytes(const delta_wgrad* w);
+delta_status delta_wgrad_run(const delta_wgrad* w, const void* dy, const void* x, float* dw, void* ws,
+                         void* stream);
+void delta_wgrad_destroy(delta_wgrad* w);
+
 /* ---- recompute engine: BatchNorm (BNForward, ref src/trace.cpp:405) ---- */
 int64_t delta_bn_workspace_floats(int64_t M, int32_t C);
 /* training-mode statistics; run_mean/run_var may be NULL (recompute never

@@ -64,6 +64,7 @@ typedef struct delta_ref {
  *  AVGPOOL         r0 x, r1 y, i0 N, i1 HW, i2 C
  *  SOFTMAX_XENT    r0 logits, r1 labels, r2 loss, r3 dlogits, r4 row_ws, i0 N, i1 K
  *  HOST            i0 host op id (passed to the host callback)
+ *  WGRAD           conv = a delta_wgrad*, r0 dy, r1 x, r2 dw (fp32 KRSC), r3 ws
  */
 enum {
   DELTA_K_COPY = 1,
@@ -79,7 +80,8 @@ enum {
   DELTA_K_MAXPOOL_BWD = 11,
   DELTA_K_AVGPOOL = 12,
   DELTA_K_SOFTMAX_XENT = 13,
-  DELTA_K_HOST = 14
+  DELTA_K_HOST = 14,
+  DELTA_K_WGRAD = 15
 };
 enum {
   DELTA_KOP_FIRST_ONLY = 1,     /* skipped when the node is recomputed        */

@@ -44,6 +44,18 @@ int conv_plan_set_tile_n(ConvPlan* cp, int bn, const void* w);
 cudaError_t conv_forward(const ConvPlan& cp, const void* x, void* y, float* stats,
                          cudaStream_t st, const ConvEpilogue* epi = nullptr);
 
+// ---- weight gradient (wgrad.cu) ----
+struct WgradPlan {
+  int N, H, W, C, K, R, S, stride, pad;  // the forward conv (C == 4: the pair-view stem)
+  int P, Q, mode, bn, taps, tiles, splits, kb_per_split;
+};
+// 0 ok, 1 unsupported shape
+int wgrad_plan_init(WgradPlan* wp);
+size_t wgrad_workspace_bytes(const WgradPlan& wp);
+// dw: fp32 [K][R][S][C] (overwritten); ws: wgrad_workspace_bytes of scratch
+cudaError_t wgrad(const WgradPlan& wp, const void* dy, const void* x, float* dw, float* ws,
+                  cudaStream_t st);
+
 // ---- batch norm / elementwise / pooling (bn_pool.cu) ----
 int64_t bn_workspace_floats(int64_t M, int C);
 cudaError_t bn_stats(const void* x, int64_t M, int C, float* ws, float* mean, float* invstd,

@@ -1,0 +1,437 @@
+// Convolution weight gradient for sm_100a (tcgen05 + TMEM + TMA), replacing
+// the library wgrad on the backward path.
+//
+// GEMM view (NHWC activations, KRSC weights), reduction over output pixels:
+//   dW[k, (r,s,c)] = sum_m dY[m, k] * X[n, p*st-pad+r, q*st-pad+s, c],  m = (n,p,q)
+// Both operands are MN-major in shared memory: a TMA box of 64 pixels x 64
+// channels lands as 64 rows of 128 B (channels contiguous) — dY rows give the
+// A tile (M' = 128 output channels = two boxes), X rows (plain 2D for a 1x1
+// stride-1 conv, TMA im2col per tap otherwise, pixel-pair im2col for the C=4
+// stem) give the B tile (N' = BN input channels of one tap).  The MMA reads
+// them through MN-major descriptors (tcgen05 instruction-descriptor transpose
+// bits), so no data is transposed anywhere.
+//
+// The reduction (N*P*Q pixels: up to 800k) is split over CTAs: work item =
+// (split, output tile) with a contiguous pixel range; each writes its fp32
+// partial tile to a workspace and a second kernel sums the splits in a fixed
+// order straight into the fp32 KRSC gradient (deterministic, no atomics).
+//
+// Persistent, warp-specialised: warp 0 = TMA producer, warp 1 = TMEM owner +
+// single-thread MMA issuer, warps 2-5 = epilogue (TMEM lane quarter = warp%4),
+// two TMEM accumulators so the epilogue of one item overlaps the next.
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdlib>
+
+#include "kernels/kernels.hpp"
+#include "kernels/sm100_common.cuh"
+#include "kernels/tma_host.hpp"
+
+namespace delta_k {
+
+using namespace dsm100;
+
+namespace {
+
+constexpr int WG_THREADS = 192;
+constexpr int KPIX = 64;  // pixels per k-block
+constexpr int WG_PLAIN = 0, WG_IM2COL = 1, WG_STEM = 2;
+
+struct WgArgs {
+  int K, C, taps, S, P, Q, stride, pad;
+  int M;             // pixels N*P*Q
+  int kblocks;       // ceil(M / KPIX)
+  int tiles_m;       // ceil(K / 128)
+  int ntot;          // N' = taps * C (flattened (tap, channel) columns)
+  int tiles;         // tiles_m * ceil(ntot / BN) (stem: tiles_m)
+  int splits, kb_per_split;
+  int items;         // splits * tiles
+  float* ws;         // [items][128][BN] fp32 partials
+};
+
+__device__ __forceinline__ uint8_t* align1024(uint8_t* p) {
+  return reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(p) + 1023) & ~uintptr_t(1023));
+}
+
+// MN-major operand descriptor, 128-byte swizzle: rows of 128 B along MN (64
+// bf16), 8-row (K) groups 1 KB apart (SBO), MN atoms `lbo` bytes apart.
+__device__ __forceinline__ uint64_t desc_mn_sw128(uint32_t addr, uint32_t lbo) {
+  uint64_t d = 0;
+  d |= uint64_t((addr & 0x3FFFF) >> 4);
+  d |= uint64_t((lbo >> 4) & 0x3FFF) << 16;
+  d |= uint64_t(1024 >> 4) << 32;
+  d |= uint64_t(1) << 46;
+  d |= uint64_t(2) << 61;  // SWIZZLE_128B
+  return d;
+}
+// MN-major, no swizzle: core matrix = 8 K-rows x 16 B (8 MN elements); K
+// groups `lbo` bytes apart, MN groups `sbo` bytes apart.
+__device__ __forceinline__ uint64_t desc_mn_interleave(uint32_t addr, uint32_t lbo, uint32_t sbo) {
+  uint64_t d = 0;
+  d |= uint64_t((addr & 0x3FFFF) >> 4);
+  d |= uint64_t((lbo >> 4) & 0x3FFF) << 16;
+  d |= uint64_t((sbo >> 4) & 0x3FFF) << 32;
+  d |= uint64_t(1) << 46;
+  return d;
+}
+
+template <int BN, int MODE>
+__global__ void __launch_bounds__(WG_THREADS, 1)
+    k_wgrad(const __grid_constant__ CUtensorMap amap, const __grid_constant__ CUtensorMap bmap,
+            const WgArgs a) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = align1024(smem_raw);
+  constexpr int STAGES = BN >= 256 ? 4 : 6;
+  constexpr uint32_t A_STAGE = 2 * KPIX * 128;                           // 2 boxes of 64 ch
+  constexpr uint32_t B_STAGE = MODE == WG_STEM ? 32 * KPIX * 16 : (BN / 64) * KPIX * 128;
+  const uint32_t sA = smem_u32(smem);
+  const uint32_t sB = sA + STAGES * A_STAGE;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * (A_STAGE + B_STAGE));
+  uint64_t* empty = full + STAGES;
+  uint64_t* tfull = empty + STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&tfull[i], 1);
+      mbar_init(&tempty[i], 4);
+    }
+    fence_mbar_init();
+    tma_prefetch_desc(&amap);
+    tma_prefetch_desc(&bmap);
+  }
+  if (warp == 1) tmem_alloc(tslot, 2 * BN);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tslot;
+
+  // work item -> (split, tile); tile -> (m block, first flattened column n0);
+  // a tile's BN columns may span several taps when C < BN
+  auto decode = [&](int item, int& m0, int& n0, int& kb0, int& kb1) {
+    const int split = item / a.tiles, tile = item % a.tiles;
+    m0 = (tile % a.tiles_m) * 128;
+    n0 = (tile / a.tiles_m) * BN;
+    kb0 = split * a.kb_per_split;
+    kb1 = min(a.kblocks, kb0 + a.kb_per_split);
+  };
+
+  if (warp == 0) {
+    // ================================ producer ================================
+    if (lane == 0) {
+      uint32_t it = 0;
+      for (int item = blockIdx.x; item < a.items; item += gridDim.x) {
+        int m0, n0, kb0, kb1;
+        decode(item, m0, n0, kb0, kb1);
+        // B boxes of this tile: 64 flattened columns each, inside [0, ntot)
+        const int nbox = MODE == WG_STEM ? 28 : min(BN / 64, (a.ntot - n0) / 64);
+        const uint32_t b_bytes = MODE == WG_STEM ? 28 * KPIX * 16 : nbox * KPIX * 128;
+        // per item: each B box's (channel, tap column, tap row) — the single
+        // producer thread must not spend its k-loop on divisions
+        int bc[BN / 64], bs[BN / 64], br[BN / 64];
+#pragma unroll
+        for (int b = 0; b < BN / 64; ++b) {
+          const int col = n0 + 64 * b, tap = col / a.C;
+          bc[b] = col - tap * a.C;
+          bs[b] = tap % a.S;
+          br[b] = tap / a.S;
+        }
+        // output pixel of the k-block -> (n, p, q), advanced incrementally
+        int q = 0, p = 0, n = 0;
+        if (MODE != WG_PLAIN) {
+          const int pix0 = kb0 * KPIX;
+          q = pix0 % a.Q;
+          const int t = pix0 / a.Q;
+          n = t / a.P;
+          p = t - n * a.P;
+        }
+        for (int kb = kb0; kb < kb1; ++kb, ++it) {
+          const uint32_t s = it % STAGES;
+          if (it >= STAGES) mbar_wait(&empty[s], ((it / STAGES) - 1) & 1);
+          const int pix = kb * KPIX;
+          // the second 64-channel half of the A tile only where K has it (rows
+          // of D past K are never read back)
+          const bool a2 = m0 + 64 < a.K;
+          mbar_arrive_expect_tx(&full[s], (a2 ? A_STAGE : A_STAGE / 2) + b_bytes);
+          tma_load_2d(sA + s * A_STAGE, &amap, &full[s], m0, pix);
+          if (a2) tma_load_2d(sA + s * A_STAGE + KPIX * 128, &amap, &full[s], m0 + 64, pix);
+          if constexpr (MODE == WG_PLAIN) {
+#pragma unroll
+            for (int b = 0; b < BN / 64; ++b)
+              if (b < nbox)
+                tma_load_2d(sB + s * B_STAGE + b * KPIX * 128, &bmap, &full[s], n0 + 64 * b, pix);
+          } else if constexpr (MODE == WG_IM2COL) {
+            const int wb = q * a.stride - a.pad, hb = p * a.stride - a.pad;
+#pragma unroll
+            for (int b = 0; b < BN / 64; ++b)
+              if (b < nbox)
+                tma_load_im2col_4d(sB + s * B_STAGE + b * KPIX * 128, &bmap, &full[s], bc[b],
+                                   wb, hb, n, uint16_t(bs[b]), uint16_t(br[b]));
+          } else {
+            // stem over pixel pairs: 28 taps (7 rows x 4 pairs) x 8 channels
+            const int wb = q - 2, hb = p * 2 - 3;
+            for (int u = 0; u < 28; ++u)
+              tma_load_im2col_4d(sB + s * B_STAGE + u * KPIX * 16, &bmap, &full[s], 0, wb, hb, n,
+                                 uint16_t(u & 3), uint16_t(u >> 2));
+          }
+          if (MODE != WG_PLAIN) {
+            q += KPIX;
+            while (q >= a.Q) {
+              q -= a.Q;
+              if (++p == a.P) {
+                p = 0;
+                ++n;
+              }
+            }
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ============================== MMA issuer ===============================
+    if (lane == 0) {
+      constexpr uint32_t idesc = umma_idesc_bf16(128, BN) | (1u << 15) | (1u << 16);
+      uint32_t it = 0, lt = 0;
+      for (int item = blockIdx.x; item < a.items; item += gridDim.x, ++lt) {
+        int m0, n0, kb0, kb1;
+        decode(item, m0, n0, kb0, kb1);
+        const uint32_t acc = lt & 1;
+        if (lt >= 2) mbar_wait(&tempty[acc], ((lt >> 1) - 1) & 1);
+        tc_fence_after();
+        const uint32_t d = tmem + acc * BN;
+        for (int kb = kb0; kb < kb1; ++kb, ++it) {
+          const uint32_t s = it % STAGES;
+          mbar_wait(&full[s], (it / STAGES) & 1);
+          tc_fence_after();
+#pragma unroll
+          for (int k = 0; k < KPIX / 16; ++k) {
+            const uint64_t ad = desc_mn_sw128(sA + s * A_STAGE + k * 2048, KPIX * 128);
+            const uint64_t bd =
+                MODE == WG_STEM
+                    ? desc_mn_interleave(sB + s * B_STAGE + k * 256, 128, KPIX * 16)
+                    : desc_mn_sw128(sB + s * B_STAGE + k * 2048, KPIX * 128);
+            umma_bf16(d, ad, bd, idesc, (kb != kb0 || k) ? 1u : 0u);
+          }
+          umma_commit(&empty[s]);
+        }
+        umma_commit(&tfull[acc]);
+      }
+    }
+    __syncwarp();
+  } else {
+    // =============================== epilogue ================================
+    const int quarter = warp & 3;
+    uint32_t lt = 0;
+    for (int item = blockIdx.x; item < a.items; item += gridDim.x, ++lt) {
+      const uint32_t acc = lt & 1;
+      mbar_wait(&tfull[acc], (lt >> 1) & 1);
+      tc_fence_after();
+      float* out = a.ws + (size_t(item) * 128 + quarter * 32 + lane) * BN;
+#pragma unroll 1
+      for (int j = 0; j < BN / 32; ++j) {
+        float v[32];
+        tmem_ld_32x32b_x32(tmem + (uint32_t(quarter * 32) << 16) + acc * BN + j * 32, v);
+        float4* o = reinterpret_cast<float4*>(out + j * 32);
+#pragma unroll
+        for (int u = 0; u < 8; ++u) o[u] = make_float4(v[4 * u], v[4 * u + 1], v[4 * u + 2], v[4 * u + 3]);
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty[acc]);
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 1) tmem_dealloc(tmem, 2 * BN);
+}
+
+// dW[k][n] (KRSC, n = tap*C + c, fp32) = sum over splits of the partial tiles,
+// in split order.  Thread per output element; consecutive threads = consecutive n.
+template <int BN>
+__global__ void __launch_bounds__(256)
+    k_wgrad_reduce(const float* __restrict__ ws, float* __restrict__ dw, int K, int ntot,
+                   int tiles_m, int tiles, int splits) {
+  const int64_t total = int64_t(K) * ntot;
+  for (int64_t e = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; e < total;
+       e += int64_t(gridDim.x) * blockDim.x) {
+    const int n = int(e % ntot);
+    const int k = int(e / ntot);
+    const int tile = (n / BN) * tiles_m + k / 128;
+    const size_t off = (size_t(tile) * 128 + (k % 128)) * BN + (n % BN);
+    float s = 0.f;
+    for (int sp = 0; sp < splits; ++sp) s += ws[size_t(sp) * tiles * 128 * BN + off];
+    dw[e] = s;
+  }
+}
+
+// stem: partial columns n = (r*4 + j)*8 + e*4 + ch -> dW[k][r][2j+e-1][ch]
+__global__ void __launch_bounds__(256)
+    k_wgrad_reduce_stem(const float* __restrict__ ws, float* __restrict__ dw, int K, int splits,
+                        int tiles) {
+  const int total = K * 7 * 7 * 4;
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < total; e += gridDim.x * blockDim.x) {
+    const int ch = e & 3;
+    const int s = (e >> 2) % 7;
+    const int r = (e / 28) % 7;
+    const int k = e / 196;
+    const int sp1 = s + 1, j = sp1 >> 1, ee = sp1 & 1;
+    const int n = (r * 4 + j) * 8 + ee * 4 + ch;
+    const size_t off = (size_t(k / 128) * 128 + (k % 128)) * 256 + n;
+    float acc = 0.f;
+    for (int sp = 0; sp < splits; ++sp) acc += ws[size_t(sp) * tiles * 128 * 256 + off];
+    dw[e] = acc;
+  }
+}
+
+template <int BN, int MODE>
+constexpr size_t wg_smem_bytes() {
+  constexpr int STAGES = BN >= 256 ? 4 : 6;
+  constexpr size_t A = 2 * KPIX * 128;
+  constexpr size_t B = MODE == WG_STEM ? 32 * KPIX * 16 : (BN / 64) * KPIX * 128;
+  return STAGES * (A + B) + 1024 + 256;
+}
+
+int num_sms_wg() {
+  static int n = 0;
+  if (!n) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (n <= 0) n = 148;
+  }
+  return n;
+}
+
+template <int BN, int MODE>
+cudaError_t wg_launch(const WgradPlan& wp, const void* dy, const void* x, float* dw, float* ws,
+                      cudaStream_t st) {
+  auto kern = k_wgrad<BN, MODE>;
+  constexpr size_t smem = wg_smem_bytes<BN, MODE>();
+  static_assert(smem <= 227 * 1024, "shared memory");
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  WgArgs a{};
+  a.K = wp.K; a.C = wp.C; a.taps = wp.taps; a.S = wp.S; a.P = wp.P; a.Q = wp.Q;
+  a.stride = wp.stride; a.pad = wp.pad;
+  a.M = wp.N * wp.P * wp.Q;
+  a.kblocks = (a.M + KPIX - 1) / KPIX;
+  a.tiles_m = (wp.K + 127) / 128;
+  a.ntot = wp.taps * wp.C;
+  a.tiles = wp.tiles;
+  a.splits = wp.splits;
+  a.kb_per_split = wp.kb_per_split;
+  a.items = wp.splits * wp.tiles;
+  a.ws = ws;
+  alignas(64) CUtensorMap amap, bmap;
+  if (!tma_2d_bf16(&amap, dy, uint64_t(wp.K), uint64_t(a.M), uint64_t(wp.K), 64, KPIX,
+                   CU_TENSOR_MAP_SWIZZLE_128B))
+    return cudaErrorInvalidValue;
+  bool ok;
+  if (MODE == WG_PLAIN) {
+    ok = tma_2d_bf16(&bmap, x, uint64_t(wp.C), uint64_t(a.M), uint64_t(wp.C), 64, KPIX,
+                     CU_TENSOR_MAP_SWIZZLE_128B);
+  } else if (MODE == WG_IM2COL) {
+    ok = tma_im2col_bf16(&bmap, x, wp.C, wp.W, wp.H, wp.N, -wp.pad, -wp.pad,
+                         wp.pad - (wp.S - 1), wp.pad - (wp.R - 1), wp.stride, wp.stride, 64, KPIX,
+                         CU_TENSOR_MAP_SWIZZLE_128B);
+  } else {  // stem: [N][H][W/2][8] pixel pairs, stride (w 1, h 2)
+    const int W2 = wp.W / 2;
+    ok = tma_im2col_bf16(&bmap, x, 8, W2, wp.H, wp.N, -2, -3, wp.Q - W2 - 2, 2 * wp.P - wp.H - 3,
+                         1, 2, 8, KPIX, CU_TENSOR_MAP_SWIZZLE_NONE);
+  }
+  if (!ok) return cudaErrorInvalidValue;
+  const int grid = std::min(a.items, num_sms_wg());
+  kern<<<grid, WG_THREADS, smem, st>>>(amap, bmap, a);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  if (MODE == WG_STEM) {
+    k_wgrad_reduce_stem<<<(wp.K * 196 + 255) / 256, 256, 0, st>>>(ws, dw, wp.K, wp.splits,
+                                                                  wp.tiles);
+  } else {
+    const int64_t total = int64_t(wp.K) * a.ntot;
+    const int64_t blocks = std::min<int64_t>((total + 255) / 256, 148 * 16);
+    k_wgrad_reduce<BN><<<int(blocks), 256, 0, st>>>(ws, dw, wp.K, a.ntot, a.tiles_m, wp.tiles,
+                                                   wp.splits);
+  }
+  return cudaGetLastError();
+}
+
+}  // namespace
+
+int wgrad_plan_init(WgradPlan* wp) {
+  WgradPlan& p = *wp;
+  const bool stem = p.C == 4;
+  if (stem) {
+    if (p.R != 7 || p.S != 7 || p.stride != 2 || p.pad != 3 || (p.W & 1)) return 1;
+  } else if (p.C % 64 != 0) {
+    return 1;
+  }
+  if (p.K % 64 != 0) return 1;
+  p.P = (p.H + 2 * p.pad - p.R) / p.stride + 1;
+  p.Q = (p.W + 2 * p.pad - p.S) / p.stride + 1;
+  p.mode = stem ? WG_STEM : (p.R == 1 && p.S == 1 && p.stride == 1 && p.pad == 0 ? WG_PLAIN : WG_IM2COL);
+  p.taps = stem ? 1 : p.R * p.S;
+  const int ntot = p.taps * p.C;  // flattened (tap, channel) columns
+  p.bn = stem ? 256 : (ntot >= 256 ? 256 : (ntot >= 128 ? 128 : 64));
+  const int tiles_m = (p.K + 127) / 128;
+  p.tiles = stem ? tiles_m : tiles_m * ((ntot + p.bn - 1) / p.bn);
+  const int M = p.N * p.P * p.Q;
+  const int kblocks = (M + KPIX - 1) / KPIX;
+  // at least two waves of work items over the 148 SMs, each at least 8
+  // k-blocks long (measured: more, shorter items beat fewer, longer ones)
+  static const int waves = [] {
+    const char* e = std::getenv("DELTA_WGRAD_WAVES");
+    return e ? std::max(1, std::atoi(e)) : 2;
+  }();
+  int splits = std::max(1, (waves * 148 + p.tiles - 1) / p.tiles);
+  splits = std::min(splits, std::max(1, kblocks / 8));
+  // the fp32 partials (written, then read by the reduce) must stay well below
+  // the main loop's own time, or many-tile shapes (K x taps*C large, few
+  // pixels: layer 4 1x1) spend it on partials; never below one full wave
+  const double t_mma = 2.0 * M * double(p.K) * ntot / 1.2e15;
+  const double t_op = 2.0 * M * (double(p.K) + double(p.C) * (stem ? 2 : 1)) / 6e12;
+  const double t_split = 8.0 * p.tiles * 128 * p.bn / 6e12;
+  const int cap = std::max((148 + p.tiles - 1) / p.tiles,
+                           int(0.4 * std::max(t_mma, t_op) / t_split));
+  splits = std::max(1, std::min(splits, cap));
+  p.kb_per_split = (kblocks + splits - 1) / splits;
+  p.splits = (kblocks + p.kb_per_split - 1) / p.kb_per_split;
+  return 0;
+}
+
+size_t wgrad_workspace_bytes(const WgradPlan& wp) {
+  return size_t(wp.splits) * wp.tiles * 128 * wp.bn * sizeof(float);
+}
+
+cudaError_t wgrad(const WgradPlan& wp, const void* dy, const void* x, float* dw, float* ws,
+                  cudaStream_t st) {
+  if (wp.mode == WG_STEM) return wg_launch<256, WG_STEM>(wp, dy, x, dw, ws, st);
+  switch (wp.bn) {
+    case 64:
+      return wp.mode == WG_PLAIN ? wg_launch<64, WG_PLAIN>(wp, dy, x, dw, ws, st)
+                                 : wg_launch<64, WG_IM2COL>(wp, dy, x, dw, ws, st);
+    case 128:
+      return wp.mode == WG_PLAIN ? wg_launch<128, WG_PLAIN>(wp, dy, x, dw, ws, st)
+                                 : wg_launch<128, WG_IM2COL>(wp, dy, x, dw, ws, st);
+    default:
+      return wp.mode == WG_PLAIN ? wg_launch<256, WG_PLAIN>(wp, dy, x, dw, ws, st)
+                                 : wg_launch<256, WG_IM2COL>(wp, dy, x, dw, ws, st);
+  }
+}
+
+}  // namespace delta_k

@@ -165,6 +165,13 @@ delta_status run_kop(delta_rt* rt, const delta_kop& k, Frame& fr, uint64_t node,
                                 rp<float>(fr, r[2]), rp<float>(fr, r[3]), rp<float>(fr, r[4]),
                                 int(i[0]), int(i[1]), st);
       break;
+    case DELTA_K_WGRAD: {
+      auto* w = reinterpret_cast<const delta_wgrad*>(k.conv);
+      if (!w) return fail(DELTA_E_ARGUMENT, "recipe: WGRAD without a wgrad handle");
+      e = delta_k::wgrad(w->plan, ref(fr, r[0]), ref(fr, r[1]), rp<float>(fr, r[2]),
+                         rp<float>(fr, r[3]), st);
+      break;
+    }
     case DELTA_K_HOST: {
       if (!rt->host_fn) return fail(DELTA_E_ARGUMENT, "recipe: HOST op without a host callback");
       std::vector<uint64_t> ins(fr.n_in);

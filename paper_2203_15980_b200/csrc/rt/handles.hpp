@@ -10,5 +10,9 @@ struct delta_conv {
   const void* weight = nullptr;
 };
 
+struct delta_wgrad {
+  delta_k::WgradPlan plan;
+};
+
 // thread-local last error of the C ABI (capi.cpp; also delta_rt::set_error)
 void delta_set_error(const std::string& msg);

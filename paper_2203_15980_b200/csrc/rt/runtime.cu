@@ -88,6 +88,33 @@ delta_status delta_conv_forward_ex(const delta_conv* c, const void* x, void* y, 
   return cuda_status(delta_k::conv_forward(c->plan, x, y, stats, S(stream), &e), "conv_forward_ex");
 }
 
+delta_status delta_wgrad_create(int32_t N, int32_t H, int32_t W, int32_t C, int32_t K, int32_t R,
+                                int32_t S_, int32_t stride, int32_t pad, delta_wgrad** out) {
+  auto* w = new delta_wgrad;
+  std::memset(&w->plan, 0, sizeof(w->plan));
+  w->plan.N = N; w->plan.H = H; w->plan.W = W; w->plan.C = C; w->plan.K = K;
+  w->plan.R = R; w->plan.S = S_; w->plan.stride = stride; w->plan.pad = pad;
+  if (delta_k::wgrad_plan_init(&w->plan) != 0) {
+    delete w;
+    delta_rt::set_error("wgrad: unsupported shape (need C%64==0 or the C==4 stem, K%64==0)");
+    return DELTA_E_UNSUPPORTED;
+  }
+  *out = w;
+  return DELTA_OK;
+}
+
+uint64_t delta_wgrad_workspace_bytes(const delta_wgrad* w) {
+  return delta_k::wgrad_workspace_bytes(w->plan);
+}
+
+delta_status delta_wgrad_run(const delta_wgrad* w, const void* dy, const void* x, float* dw, void* ws,
+                         void* stream) {
+  return cuda_status(delta_k::wgrad(w->plan, dy, x, dw, static_cast<float*>(ws), S(stream)),
+                     "wgrad");
+}
+
+void delta_wgrad_destroy(delta_wgrad* w) { delete w; }
+
 delta_status delta_conv_set_tile_n(delta_conv* c, int32_t tile_n) {
   const int rc = delta_k::conv_plan_set_tile_n(&c->plan, tile_n, c->weight);
   if (rc == 0) return DELTA_OK;

@@ -17,6 +17,10 @@ _SIGS = {
     "delta_bn_stats_from_partials": (i32, [vp, i64, i32, i32, vp, vp, f32, vp, vp, f32, vp]),
     "delta_conv_forward_ex": (i32, [vp, vp, vp, vp, vp, vp]),
     "delta_conv_set_tile_n": (i32, [vp, i32]),
+    "delta_wgrad_create": (i32, [i32] * 9 + [P(vp)]),
+    "delta_wgrad_workspace_bytes": (u64, [vp]),
+    "delta_wgrad_run": (i32, [vp, vp, vp, vp, vp, vp]),
+    "delta_wgrad_destroy": (None, [vp]),
     "delta_bn_backward_from_partials": (i32, [vp, vp, vp, vp, i64, i32, vp, vp, vp, vp, vp, vp]),
     "delta_conv_geometry": (i32, [vp, P(i32), P(i32), P(i32), P(i32)]),
     "delta_conv_destroy": (None, [vp]),
@@ -106,6 +110,24 @@ class Conv:
     def __del__(self):
         if getattr(self, "_h", None) and lib is not None:
             lib.delta_conv_destroy(self._h)
+            self._h = None
+
+
+class Wgrad:
+    """tcgen05 convolution weight gradient (fp32 KRSC, deterministic split-K)."""
+
+    def __init__(self, N, H, W, Cin, K, R, S, stride, pad):
+        self._h = vp()
+        check(lib.delta_wgrad_create(N, H, W, Cin, K, R, S, stride, pad, C.byref(self._h)))
+        self.workspace_bytes = int(lib.delta_wgrad_workspace_bytes(self._h))
+
+    def __call__(self, dy_ptr: int, x_ptr: int, dw_ptr: int, ws_ptr: int, stream: int):
+        check(lib.delta_wgrad_run(self._h, dy_ptr, x_ptr, dw_ptr, ws_ptr, stream))
+        _count(2)
+
+    def __del__(self):
+        if getattr(self, "_h", None) and lib is not None:
+            lib.delta_wgrad_destroy(self._h)
             self._h = None
 
 

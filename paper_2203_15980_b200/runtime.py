@@ -151,6 +151,14 @@ def workspace_plan(g: G.Graph) -> dict:
     ws["short_ws"] = max(short + [256])
     mp = next(n for n in nodes if n.op == "maxpool")
     ws["mp_ws"] = K.maxpool_workspace_bytes(*nodes[mp.parents[0]].shape)
+    wg = 0
+    for n in nodes:
+        if n.op == "conv":
+            cs = g.convs[n.attrs["conv"]]
+            Nb, H, W, Cin = nodes[n.parents[0]].shape
+            wg = max(wg, K.Wgrad(Nb, H, W, Cin, cs.cout, cs.k, cs.k, cs.stride,
+                                 cs.pad).workspace_bytes)
+    ws["wgrad_ws"] = wg
     ws["head"] = 4 + batch * g.fc[1] * 4 + batch * 4
     ws["input_slots"] = 2 * (nodes[0].nbytes + batch * 8)
     trans = [0]
@@ -208,6 +216,7 @@ class DeltaRuntime:
         # shortcut conv at its sampling grid
         self.short_ws = u8("short_ws")
         self.mp_ws = u8("mp_ws")
+        self.wg_ws = u8("wgrad_ws")
         ncls = self.g.fc[1]
         self.loss = torch.zeros(1, dtype=torch.float32, device=self.device)
         self.dlogits = torch.empty(batch, ncls, dtype=torch.float32, device=self.device)
@@ -237,6 +246,7 @@ class DeltaRuntime:
         # of MMA: fused only where the main loop hides them (K-dim >= 384)
         self._fuse_stats = {}
         self._dconvs = {}
+        self._wgrads = {}
         for n in self.nodes:
             if n.op == "conv":
                 cs = self.g.convs[n.attrs["conv"]]
@@ -248,6 +258,8 @@ class DeltaRuntime:
                 assert (conv.P, conv.Q) == n.shape[1:3], (n.name, conv.P, conv.Q, n.shape)
                 self._convs[n.name] = conv
                 self._fuse_stats[n.name] = conv.kdim >= FUSE_STATS_MIN_KDIM
+                self._wgrads[cs.name] = K.Wgrad(Nb, H, W, C, cs.cout, cs.k, cs.k, cs.stride,
+                                                cs.pad)
                 if own_dgrad(cs):
                     # on the conv's output grid (a stride-2 1x1's gradient lives at
                     # its sampling points; the consumer scatters it)
@@ -354,6 +366,11 @@ class DeltaRuntime:
                           (BN_EPS, BN_MOMENTUM), flags=X.FIRST_ONLY),
                     1 + K._merge_launches(K._chunks(M, C)), 0)
 
+        def wgrad(conv, dy_in, x_in):
+            """our tcgen05 weight gradient straight into the fp32 KRSC grad buffer"""
+            return X.kop(X.K_WGRAD, (X.IN(dy_in), X.IN(x_in), _ptr(pr.gviews["conv:" + conv]),
+                                     _ptr(self.wg_ws)), conv=self._wgrads[conv]._h)
+
         if op == "input":
             add(X.kop(X.K_COPY, (X.OUT(), _ptr(self.x_dev)), (self.x_dev.numel() * 2,)))
         elif op == "conv":
@@ -416,7 +433,6 @@ class DeltaRuntime:
             # parents [dC, R = relu(bn(X)), X]
             conv, bn = node.attrs["conv"], node.attrs["bn"]
             if conv in self._dconvs:
-                wg = host(self._wgrad_op(conv, node.parents[0], node.parents[1]))
                 # dgrad on the tensor cores; its epilogue applies the ReLU mask
                 # (recomputed from X) and reduces sum g, sum g*X per tile; g is
                 # written in place of its BN-backward output
@@ -426,13 +442,13 @@ class DeltaRuntime:
                 add(X.kop(X.K_BN_BWD_PARTS, (_ptr(self.stats_main), X.OUT(), X.IN(2), X.OUT())
                           + bnp(bn) + (gb(bn)[0],) + dgb(bn), (0, M, C)),
                     1 + K._merge_launches((M + 127) // 128), 0)
-                add(X.kop(X.K_HOST, (), (wg,)), 0, 0)
             else:
-                # cuDNN dgrad + wgrad in one call; the input gradient -> SCRATCH(0)
+                # cuDNN input gradient (3x3) -> SCRATCH(0)
                 dg = host(self._dgrad_op(conv, node.parents[0], node.parents[1]))
                 add(X.kop(X.K_HOST, (), (dg,)), 0, 0)
                 add(X.kop(X.K_BN_BWD, (X.SCRATCH(0), X.IN(1), X.IN(2), X.OUT()) + bnp(bn)
                           + (gb(bn)[0],) + dgb(bn) + (_ptr(self.bn_ws),), (0, M, C)), bwd_n, bwd_n)
+            add(wgrad(conv, 0, 1), 2, 2)
         elif op == "conv_shortcut_bwd":
             # out = (dgrad(conv1, dC1) + shortcut gradient) * [X > 0]; the sum
             # and the mask are the dgrad kernel's epilogue
@@ -449,14 +465,12 @@ class DeltaRuntime:
                         dst, stride2 = _ptr(self.short_ws), 1  # at its sampling grid
                     add(X.kop(X.K_CONV, (X.IN(2), dst, None), conv=self._dconvs[short]._h))
                     add_ = dst
-                    add(X.kop(X.K_HOST, (), (host(self._wgrad_op(short, node.parents[2],
-                                                                  node.parents[1])),)), 0, 0)
-                    n_host += 1
-                else:  # cuDNN dgrad + wgrad in one call
+                else:  # cuDNN input gradient
                     add(X.kop(X.K_HOST, (), (host(self._dgrad_op(short, node.parents[2],
                                                                   node.parents[1])),)), 0, 0)
                     add_ = X.SCRATCH(n_host)
                     n_host += 1
+                add(wgrad(short, 2, 1), 2, 2)
             elif node.attrs.get("from_pool"):
                 add_, pool_hw, add_mask = X.IN(2), int(node.shape[1] * node.shape[2]), X.IN(3)
             else:
@@ -465,8 +479,7 @@ class DeltaRuntime:
                 raise RuntimeError(f"{node.name}: the shortcut's conv1 must be a 1x1 (own dgrad)")
             add(X.kop(X.K_CONV_EX, (X.IN(0), X.OUT(), None, add_, add_mask, out_mask),
                       (K.EPI_ADD_MASK, pool_hw, stride2), conv=self._dconvs[conv]._h))
-            add(X.kop(X.K_HOST, (), (host(self._wgrad_op(conv, node.parents[0],
-                                                          node.parents[1])),)), 0, 0)
+            add(wgrad(conv, 0, 1), 2, 2)
         elif op == "maxpool_bwd":
             Nb, H, W, Cs = self.nodes[node.parents[1]].shape
             add(X.kop(X.K_MAXPOOL_BWD, (X.IN(0), X.IN(1), X.OUT(), _ptr(self.mp_ws)),
@@ -476,13 +489,12 @@ class DeltaRuntime:
             add(X.kop(X.K_BN_BWD, (X.IN(0), X.IN(1), X.IN(2), X.OUT()) + bnp(bn) + (gb(bn)[0],)
                       + dgb(bn) + (_ptr(self.bn_ws),), (0, M, C)), bwd_n, bwd_n)
         elif op == "conv_wgrad":
+            # the node's output IS the weight gradient (fp32): written in place,
+            # then copied into the flat gradient buffer
             conv = node.attrs["conv"]
-            wg = self._wgrad_op(conv, node.parents[0], node.parents[1])
-
-            def wgrad_out(out, ins, rec, stream, node=node, conv=conv, wg=wg):
-                wg(out, ins, rec, stream)
-                self._view(out - self._base, node).copy_(pr.gviews["conv:" + conv])
-            add(X.kop(X.K_HOST, (), (host(wgrad_out),)), 0, 0)
+            add(X.kop(X.K_WGRAD, (X.IN(0), X.IN(1), X.OUT(), _ptr(self.wg_ws)),
+                      conv=self._wgrads[conv]._h), 2, 2)
+            add(X.kop(X.K_COPY, (_ptr(pr.gviews["conv:" + conv]), X.OUT()), (node.nbytes,)))
         else:
             raise RuntimeError(f"no kernel for op {op!r} (node {node.name})")
         return ops, tuple(nl)
@@ -490,20 +502,10 @@ class DeltaRuntime:
     def _arena_view(self, ptr: int, node_id: int) -> torch.Tensor:
         return self._view(ptr - self._base, self.nodes[node_id])
 
-    def _wgrad_op(self, conv: str, dy_node: int, x_node: int):
-        """HOST op: cuDNN weight gradient (fp32 KRSC into the flat grad buffer).
-        Input slots are located by node id among the consumer's parents (set
-        by _bind's host-op wrapper)."""
-        def op(out, ins, rec, stream):
-            node = self._cur_parents
-            dY = self._arena_view(ins[node.index(dy_node)], dy_node)
-            Xv = self._arena_view(ins[node.index(x_node)], x_node)
-            self._conv_bwd(conv, dY, Xv, need_dx=False)
-        return op
-
     def _dgrad_op(self, conv: str, dy_node: int, x_node: int):
-        """HOST op: cuDNN input AND weight gradient (one call); returns the
-        input gradient's device pointer (the recipe's SCRATCH operand)."""
+        """HOST op: cuDNN input gradient (3x3 convs); returns its device
+        pointer (the recipe's SCRATCH operand).  Input slots are located by
+        node id among the consumer's parents (set by _bind's host-op wrapper)."""
         def op(out, ins, rec, stream):
             node = self._cur_parents
             dY = self._arena_view(ins[node.index(dy_node)], dy_node)
@@ -534,21 +536,18 @@ class DeltaRuntime:
         self.executor.bind(self.program, recipes, host_ops, launches)
         self._bound_slot = self._slot
 
-    def _conv_bwd(self, name: str, dY: torch.Tensor, X: torch.Tensor, need_dx: bool):
-        """dgrad/wgrad through cuDNN (channels_last views of arena memory);
-        the weight gradient lands in the fp32 grad buffer (KRSC)."""
+    def _conv_bwd(self, name: str, dY: torch.Tensor, X: torch.Tensor, need_dx: bool = True):
+        """cuDNN input gradient (channels_last views of arena memory) — the 3x3
+        convs whose dgrad our kernel does not cover yet."""
         cs = self.g.convs[name]
         w = self.params.wbf[name].permute(0, 3, 1, 2)
-        gi, gw, _ = torch.ops.aten.convolution_backward(
+        gi, _, _ = torch.ops.aten.convolution_backward(
             dY.permute(0, 3, 1, 2), X.permute(0, 3, 1, 2), w, None, [cs.stride] * 2,
-            [cs.pad] * 2, [1, 1], False, [0, 0], 1, [need_dx, True, False])
-        self.params.gviews["conv:" + name].copy_(gw.permute(0, 2, 3, 1))
-        if need_dx:
-            gi = gi.permute(0, 2, 3, 1)
-            if not gi.is_contiguous():
-                gi = gi.contiguous()
-            return gi
-        return None
+            [cs.pad] * 2, [1, 1], False, [0, 0], 1, [True, False, False])
+        gi = gi.permute(0, 2, 3, 1)
+        if not gi.is_contiguous():
+            gi = gi.contiguous()
+        return gi
 
     # -------------------------------------------------------- program
     def run_program(self, timing: dict | None = None, probe: dict | None = None,

@@ -343,3 +343,63 @@ def test_swap_engine_round_trip():
     assert torch.equal(src, dst)
     h2d, d2h, duplex = K.probe_link(64 << 20, 4)
     assert 5.0 < h2d < 200.0 and 5.0 < d2h < 200.0 and duplex > 0
+
+
+# ------------------------------------------------------------ weight gradient
+WGRAD_CASES = [
+    # N, H, W, C, K, R, stride, pad
+    (2, 56, 56, 64, 256, 1, 1, 0),
+    (2, 56, 56, 256, 64, 1, 1, 0),
+    (2, 56, 56, 64, 64, 3, 1, 1),
+    (4, 28, 28, 128, 128, 3, 1, 1),
+    (2, 56, 56, 128, 128, 3, 2, 1),
+    (2, 56, 56, 256, 512, 1, 2, 0),
+    (3, 14, 14, 1024, 256, 1, 1, 0),
+    (5, 7, 7, 512, 512, 3, 1, 1),
+]
+
+
+def _wgrad_ref(x, dy, K, R, stride, pad):
+    xc = x.permute(0, 3, 1, 2).float()
+    g = torch.nn.grad.conv2d_weight(xc, (K, x.shape[-1], R, R), dy.permute(0, 3, 1, 2).float(),
+                                    stride=stride, padding=pad)
+    return g.permute(0, 2, 3, 1).contiguous()  # KRSC
+
+
+@pytest.mark.parametrize("case", WGRAD_CASES)
+def test_wgrad_matches_fp32_reference(case):
+    N, H, W, Cin, Kout, R, st, pad = case
+    g = torch.Generator(device="cuda").manual_seed(9)
+    x = torch.randn(N, H, W, Cin, device="cuda", generator=g).to(torch.bfloat16)
+    P_, Q_ = (H + 2 * pad - R) // st + 1, (W + 2 * pad - R) // st + 1
+    dy = torch.randn(N, P_, Q_, Kout, device="cuda", generator=g).to(torch.bfloat16)
+    wg = K.Wgrad(N, H, W, Cin, Kout, R, R, st, pad)
+    ws = torch.empty(wg.workspace_bytes, dtype=torch.uint8, device="cuda")
+    dw = torch.full((Kout, R, R, Cin), float("nan"), device="cuda")
+    wg(dy.data_ptr(), x.data_ptr(), dw.data_ptr(), ws.data_ptr(), _stream())
+    torch.cuda.synchronize()
+    ref = _wgrad_ref(x, dy, Kout, R, st, pad)
+    err = (dw - ref).abs()
+    tol = 1e-3 * ref.abs() + 1e-3 * ref.pow(2).mean().sqrt()
+    assert bool((err <= tol).all()), f"max err {err.max().item()} rms {ref.pow(2).mean().sqrt().item()}"
+    dw2 = torch.empty_like(dw)  # deterministic: same bits again
+    wg(dy.data_ptr(), x.data_ptr(), dw2.data_ptr(), ws.data_ptr(), _stream())
+    torch.cuda.synchronize()
+    assert torch.equal(dw, dw2)
+
+
+def test_wgrad_stem_pairs():
+    N, H, W = 2, 224, 224
+    g = torch.Generator(device="cuda").manual_seed(10)
+    x = torch.zeros(N, H, W, 4, device="cuda", dtype=torch.bfloat16)
+    x[..., :3] = torch.randn(N, H, W, 3, device="cuda", generator=g).to(torch.bfloat16)
+    dy = torch.randn(N, 112, 112, 64, device="cuda", generator=g).to(torch.bfloat16)
+    wg = K.Wgrad(N, H, W, 4, 64, 7, 7, 2, 3)
+    ws = torch.empty(wg.workspace_bytes, dtype=torch.uint8, device="cuda")
+    dw = torch.full((64, 7, 7, 4), float("nan"), device="cuda")
+    wg(dy.data_ptr(), x.data_ptr(), dw.data_ptr(), ws.data_ptr(), _stream())
+    torch.cuda.synchronize()
+    ref = _wgrad_ref(x, dy, 64, 7, 2, 3)
+    err = (dw - ref).abs()
+    tol = 1e-3 * ref.abs() + 1e-3 * ref.pow(2).mean().sqrt()
+    assert bool((err <= tol).all()), f"max err {err.max().item()}"
