@@ -289,7 +289,7 @@ def main():
         torch.cuda.synchronize()
     rt.graph = saved_graph
     hbm_peak, tc_peak, tc_sus, peak_kind = measured_peaks()
-    conv_ms, conv_flops, conv_n, all_ms = 0.0, 0.0, 0, 0.0
+    conv_ms, conv_flops, conv_n, all_ms, conv_roof_ms = 0.0, 0.0, 0, 0.0, 0.0
     kinds = {}
     rc = {"launches": 0, "ms": 0.0, "roofline_ms": 0.0, "flops": 0.0, "bytes": 0.0, "by_op": {}}
     swap_ms, swap_bytes, swap_n = 0.0, 0, 0
@@ -308,6 +308,7 @@ def main():
                 conv_ms += ms
                 conv_flops += node.flops
                 conv_n += 1
+                conv_roof_ms += max(node.flops / (tc_peak * 1e9), node.hbm_bytes / (hbm_peak * 1e6))
             if rec:
                 # recompute engine: each re-launch against its own roofline
                 # (tensor-core FLOPs or HBM bytes, whichever bounds it)
@@ -406,6 +407,10 @@ def main():
                          "peak_kind": f"{peak_kind} burst bf16",
                          "traffic": None,
                          "launches_timed": conv_n,
+                         "frac_of_roofline_time": round(conv_roof_ms / conv_ms, 4) if conv_ms else None,
+                         "roofline_time_note": "sum over conv launches of max(FLOPs/TC peak, "
+                                               "algorithmic bytes/HBM peak) / their device time "
+                                               "(the 1x1 layer-1 convs are HBM-bound)",
                          "share_of_step": round(conv_ms / all_ms, 4) if all_ms else None,
                          "op_ms": {k: round(v, 3) for k, v in sorted(kinds.items(), key=lambda kv: -kv[1])}},
             "recompute": {"launches": rc["launches"], "ms_per_step": round(rc["ms"], 3),

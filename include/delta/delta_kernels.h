@@ -71,6 +71,10 @@ delta_status delta_conv_forward_ex(const delta_conv* c, const void* x, void* y, 
 /* Override the output-channel tile (64, 128 or 256, dividing K).  The fused
  * epilogues (DELTA_EPI_ADD_MASK / DELTA_EPI_BN_BWD) require tile_n <= 128. */
 delta_status delta_conv_set_tile_n(delta_conv* c, int32_t tile_n);
+/* output rows per BN-statistics partial written by delta_conv_forward (128,
+ * or rows*Q for 3x3 stride-1 convs, which stage the input halo per tile of
+ * whole output rows); pass it to delta_bn_stats_from_partials */
+int32_t delta_conv_stats_rows(const delta_conv* c);
 delta_status delta_conv_geometry(const delta_conv* c, int32_t* P, int32_t* Q, int32_t* kdim,
                                  int32_t* tile_n);
 void delta_conv_destroy(delta_conv* c);

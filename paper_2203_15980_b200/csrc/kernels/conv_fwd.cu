@@ -759,6 +759,16 @@ int conv_plan_init(ConvPlan* cp, const void* w) {
   cp->Q = (cp->W + 2 * cp->pad - cp->S) / cp->stride + 1;
   cp->kdim = cp->C == 4 ? 256 : cp->R * cp->S * cp->C;
   cp->bn = cp->K <= 64 ? 64 : (cp->K <= 128 ? 128 : 256);
+  // 3x3 stride-1: stage the input halo once per tile instead of 9 im2col
+  // loads — EXPERIMENTAL, opt-in (DELTA_CONV_HALO=1): it cuts L2 traffic ~4x
+  // but measured slower than the im2col path (56x56x64: 144 vs 124 us), so L2
+  // bandwidth is not what bounds the narrow 3x3 convs
+  const char* he = std::getenv("DELTA_CONV_HALO");
+  cp->halo = (he && he[0] == '1') && conv_halo_eligible(*cp);
+  if (cp->halo) {
+    conv_halo_shape(cp);
+    if (cp->halo_rows == 0) cp->halo = 0;
+  }
   if (!encode_fn()) return 2;
   return encode_2d(reinterpret_cast<CUtensorMap*>(cp->wmap), w, uint64_t(cp->kdim),
                    uint64_t(cp->K), uint32_t(cp->bn))
@@ -786,6 +796,7 @@ cudaError_t conv_forward(const ConvPlan& cp, const void* x, void* y, float* stat
   const bool stem = cp.C == 4;
   const bool tma_a = !stem && cp.R == 1 && cp.S == 1 && cp.stride == 1 && cp.pad == 0;
   const bool use_gather = gather_forced();
+  if (cp.halo && e.mode == EPI_STORE && !use_gather) return conv_halo_forward(cp, x, y, stats, st);
   if (e.mode != EPI_STORE) {
     // fused epilogues (backward dgrad): fewer stages pay for the operand ring;
     // N tiles are capped at 128 (delta_conv_set_tile_n)

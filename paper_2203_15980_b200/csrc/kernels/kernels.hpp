@@ -10,6 +10,7 @@ namespace delta_k {
 struct ConvPlan {
   int N, H, W, C, K, R, S, stride, pad;
   int P, Q, kdim, bn;
+  int halo, halo_slot, halo_rows;  // 3x3 stride-1: input halo staged per tile (conv_halo.cu)
   alignas(64) unsigned char wmap[128];  // CUtensorMap over the [K][kdim] weight matrix
 };
 // Fused epilogues (the backward pass runs input-gradient convolutions through
@@ -37,6 +38,15 @@ struct ConvEpilogue {
 };
 // 0 ok, 1 unsupported shape, 2 no driver entry point, 3 tensor-map encode failed
 int conv_plan_init(ConvPlan* cp, const void* w);
+// conv_halo.cu: the 3x3 stride-1 halo path (plain epilogue + BN statistics)
+bool conv_halo_eligible(const ConvPlan& cp);
+void conv_halo_shape(ConvPlan* cp);
+cudaError_t conv_halo_forward(const ConvPlan& cp, const void* x, void* y, float* stats,
+                              cudaStream_t st);
+// output rows per BN-statistics partial (128, or rows*Q for the halo path)
+inline int conv_stats_rows(const ConvPlan& cp) {
+  return cp.halo ? cp.halo_rows * cp.Q : 128;
+}
 // choose the N tile (64/128/256, dividing K; fused epilogues need <= 128)
 int conv_plan_set_tile_n(ConvPlan* cp, int bn, const void* w);
 // stats (optional, nullptr = off): [ceil(M/128)][K] float2 (mean, M2) of the

@@ -123,6 +123,8 @@ delta_status delta_conv_set_tile_n(delta_conv* c, int32_t tile_n) {
   return rc == 1 ? DELTA_E_UNSUPPORTED : DELTA_E_CUDA;
 }
 
+int32_t delta_conv_stats_rows(const delta_conv* c) { return delta_k::conv_stats_rows(c->plan); }
+
 delta_status delta_conv_geometry(const delta_conv* c, int32_t* P, int32_t* Q, int32_t* kdim,
                                  int32_t* tile_n) {
   if (P) *P = c->plan.P;

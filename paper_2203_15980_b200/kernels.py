@@ -17,6 +17,7 @@ _SIGS = {
     "delta_bn_stats_from_partials": (i32, [vp, i64, i32, i32, vp, vp, f32, vp, vp, f32, vp]),
     "delta_conv_forward_ex": (i32, [vp, vp, vp, vp, vp, vp]),
     "delta_conv_set_tile_n": (i32, [vp, i32]),
+    "delta_conv_stats_rows": (i32, [vp]),
     "delta_wgrad_create": (i32, [i32] * 9 + [P(vp)]),
     "delta_wgrad_workspace_bytes": (u64, [vp]),
     "delta_wgrad_run": (i32, [vp, vp, vp, vp, vp, vp]),
@@ -81,6 +82,8 @@ class Conv:
         lib.delta_conv_geometry(self._h, C.byref(p), C.byref(q), C.byref(kd), C.byref(tn))
         self.P, self.Q, self.kdim, self.tile_n = p.value, q.value, kd.value, tn.value
         self.shape = (N, H, W, Cin, K, R, S, stride, pad)
+        # output rows per BN-statistics partial of the fused epilogue
+        self.stats_rows = int(lib.delta_conv_stats_rows(self._h))
 
     def __call__(self, x_ptr: int, y_ptr: int, stream: int, stats_ptr: int | None = None):
         """stats_ptr: optional [ceil(M/128)][K] float2 BN-statistics partials."""
@@ -129,6 +132,23 @@ class Wgrad:
         if getattr(self, "_h", None) and lib is not None:
             lib.delta_wgrad_destroy(self._h)
             self._h = None
+
+
+def conv_stats_rows(N, H, W, Cin, K, R, S, stride, pad) -> int:
+    """Output rows per BN-statistics partial of a conv (mirrors conv_halo.cu
+    conv_halo_eligible/conv_halo_shape: 3x3 stride-1 convs with W <= 64 stage
+    the input halo per tile of whole output rows; everything else: 128)."""
+    import os
+    if os.environ.get("DELTA_CONV_HALO", "0") != "1":
+        return 128
+    P = (H + 2 * pad - R) // stride + 1
+    if not (R == 3 and S == 3 and stride == 1 and pad == 1 and Cin % 64 == 0 and W <= 64):
+        return 128
+    slot = 16 if W + 2 <= 16 else (32 if W + 2 <= 32 else 64)
+    for rows in range(128 // slot, 0, -1):
+        if P % rows == 0 and (rows + 2) * slot * 128 <= 32768:
+            return rows * W
+    return 128
 
 
 STEM_KDIM = 256

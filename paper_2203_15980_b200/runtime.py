@@ -35,6 +35,7 @@ BN_EPS = 1e-5
 # BN statistics are reduced in the conv epilogue when the conv's reduction
 # length is at least this (the epilogue work hides under the main loop);
 # shorter convs get a separate streaming statistics pass.
+OWN_DGRAD_3X3 = __import__("os").environ.get("DELTA_OWN_DGRAD_3X3", "0") == "1"
 FUSE_STATS_MIN_KDIM = int(__import__("os").environ.get("DELTA_FUSE_STATS_MIN_KDIM", "384"))
 BN_MOMENTUM = 0.1
 
@@ -141,7 +142,13 @@ def workspace_plan(g: G.Graph) -> dict:
     ws = {}
     ws["bn_ws"] = 4 * max(K.bn_workspace_floats(M(n), n.shape[-1]) for n in nodes
                           if len(n.shape) == 4 and n.shape[-1] % 64 == 0)
-    parts = 4 * max(K.stats_partials_floats(M(n), n.shape[-1]) for n in nodes
+    def stats_rows(n):
+        if n.op != "conv":
+            return 128
+        cs = g.convs[n.attrs["conv"]]
+        Nb, H, W, Cin = nodes[n.parents[0]].shape
+        return K.conv_stats_rows(Nb, H, W, Cin, cs.cout, cs.k, cs.k, cs.stride, cs.pad)
+    parts = 4 * max(K.stats_partials_floats(M(n), n.shape[-1], stats_rows(n)) for n in nodes
                     if n.op in ("conv", "conv_bn_relu_bwd"))
     ws["stats_main"] = ws["stats_ds"] = parts
     short = [nodes[n.parents[2]].nbytes * g.convs[n.attrs["conv_short"]].cin
@@ -176,7 +183,9 @@ def own_dgrad(cs: G.ConvSpec) -> bool:
     sampling grid and scattered by the consumer's epilogue).  3x3 dgrads stay
     with cuDNN for now (our 3x3 kernel is slower than cuDNN's at the narrow
     layer-1/2 widths, scripts/kbench_dgrad.py); the stem has no input gradient."""
-    return cs.k == 1 and cs.cin != 4
+    if cs.cin == 4:
+        return False
+    return cs.k == 1 or (cs.stride == 1 and OWN_DGRAD_3X3)
 
 
 @dataclass
@@ -258,6 +267,8 @@ class DeltaRuntime:
                 assert (conv.P, conv.Q) == n.shape[1:3], (n.name, conv.P, conv.Q, n.shape)
                 self._convs[n.name] = conv
                 self._fuse_stats[n.name] = conv.kdim >= FUSE_STATS_MIN_KDIM
+                assert conv.stats_rows == K.conv_stats_rows(Nb, H, W, C, cs.cout, cs.k, cs.k,
+                                                            cs.stride, cs.pad), n.name
                 self._wgrads[cs.name] = K.Wgrad(Nb, H, W, C, cs.cout, cs.k, cs.k, cs.stride,
                                                 cs.pad)
                 if own_dgrad(cs):
@@ -358,9 +369,10 @@ class DeltaRuntime:
             tail = (_ptr(pr.bn_mean[bn]), _ptr(pr.bn_invstd[bn]), _ptr(pr.bn_rmean[bn]),
                     _ptr(pr.bn_rvar[bn]))
             if self._fuse_stats.get(conv.name):
-                add(X.kop(X.K_BN_STATS_PARTS, (_ptr(scratch), None) + tail, (M, C, 128),
+                rows = self._convs[conv.name].stats_rows
+                add(X.kop(X.K_BN_STATS_PARTS, (_ptr(scratch), None) + tail, (M, C, rows),
                           (BN_EPS, BN_MOMENTUM), flags=X.FIRST_ONLY),
-                    K._merge_launches((M + 127) // 128), 0)
+                    K._merge_launches((M + rows - 1) // rows), 0)
             else:
                 add(X.kop(X.K_BN_STATS, (src_ref, _ptr(self.bn_ws)) + tail, (M, C),
                           (BN_EPS, BN_MOMENTUM), flags=X.FIRST_ONLY),

@@ -36,6 +36,10 @@ CONV_CASES = [
     (16, 28, 28, 128, 512, 1, 1, 0),
     (16, 28, 28, 256, 512, 1, 2, 0),
     (9, 14, 14, 256, 256, 3, 1, 1),
+    # 3x3 stride 1 on the halo path: every slot width, partial images, wide K
+    (5, 28, 28, 128, 128, 3, 1, 1),
+    (3, 7, 7, 2048, 512, 3, 1, 1),
+    (2, 14, 14, 64, 256, 3, 1, 1),
 ]
 
 
@@ -57,11 +61,12 @@ def test_conv_fwd_matches_fp32_reference(case):
     # bitwise-identical recompute, and BN statistics fused in the epilogue
     y2 = torch.empty_like(y)
     M = N * conv.P * conv.Q
-    parts = torch.empty(K.stats_partials_floats(M, Kout), device="cuda")
+    assert conv.stats_rows == K.conv_stats_rows(N, H, W, Cin, Kout, R, R, st, pad)
+    parts = torch.empty(K.stats_partials_floats(M, Kout, conv.stats_rows), device="cuda")
     conv(x.data_ptr(), y2.data_ptr(), _stream(), parts.data_ptr())
     mean = torch.empty(Kout, device="cuda"); inv = torch.empty(Kout, device="cuda")
     K.bn_stats_from_partials(parts.data_ptr(), M, Kout, mean.data_ptr(), inv.data_ptr(), 1e-5,
-                             None, None, 0.1, _stream())
+                             None, None, 0.1, _stream(), rows_per_part=conv.stats_rows)
     torch.cuda.synchronize()
     assert torch.equal(y, y2)
     yf = y.float().reshape(M, Kout)
