@@ -242,7 +242,15 @@ def main():
         rt.step_device()  # eager warm step (cuDNN autotune, allocator)
         torch.cuda.synchronize()
         if not args.no_graph:
-            rt.capture()
+            try:
+                rt.capture()
+            except Exception as e:  # noqa: BLE001 - e.g. a collective not capturable here
+                if dp is None:
+                    raise
+                print(json.dumps({"warning": f"CUDA graph capture with NCCL failed ({e}); "
+                                             "running eager steps"}), file=sys.stderr)
+                rt.graph = rt.graphs = None
+                torch.cuda.synchronize()
         # our kernel launches per step, counted from the bound recipes
         return prog, rt.executor.launches_per_step
 

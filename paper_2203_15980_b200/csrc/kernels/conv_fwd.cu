@@ -759,12 +759,12 @@ int conv_plan_init(ConvPlan* cp, const void* w) {
   cp->Q = (cp->W + 2 * cp->pad - cp->S) / cp->stride + 1;
   cp->kdim = cp->C == 4 ? 256 : cp->R * cp->S * cp->C;
   cp->bn = cp->K <= 64 ? 64 : (cp->K <= 128 ? 128 : 256);
-  // 3x3 stride-1: stage the input halo once per tile instead of 9 im2col
-  // loads — EXPERIMENTAL, opt-in (DELTA_CONV_HALO=1): it cuts L2 traffic ~4x
-  // but measured slower than the im2col path (56x56x64: 144 vs 124 us), so L2
-  // bandwidth is not what bounds the narrow 3x3 convs
+  // 3x3 stride-1, 64 -> 64 channels: stage the input halo once per tile with
+  // the 9 weight tiles resident (conv_halo.cu; 124 -> 88 us at 56x56, bs 256).
+  // DELTA_CONV_HALO=0 disables it, =1 also routes the other 3x3 stride-1
+  // shapes there (experimental).
   const char* he = std::getenv("DELTA_CONV_HALO");
-  cp->halo = (he && he[0] == '1') && conv_halo_eligible(*cp);
+  cp->halo = he ? (he[0] == '1' && conv_halo_eligible(*cp)) : conv_halo_default(*cp);
   if (cp->halo) {
     conv_halo_shape(cp);
     if (cp->halo_rows == 0) cp->halo = 0;

@@ -40,6 +40,7 @@ struct ConvEpilogue {
 int conv_plan_init(ConvPlan* cp, const void* w);
 // conv_halo.cu: the 3x3 stride-1 halo path (plain epilogue + BN statistics)
 bool conv_halo_eligible(const ConvPlan& cp);
+bool conv_halo_default(const ConvPlan& cp);  // the shapes it is dispatched for by default
 void conv_halo_shape(ConvPlan* cp);
 cudaError_t conv_halo_forward(const ConvPlan& cp, const void* x, void* y, float* stats,
                               cudaStream_t st);

@@ -136,13 +136,14 @@ class Wgrad:
 
 def conv_stats_rows(N, H, W, Cin, K, R, S, stride, pad) -> int:
     """Output rows per BN-statistics partial of a conv (mirrors conv_halo.cu
-    conv_halo_eligible/conv_halo_shape: 3x3 stride-1 convs with W <= 64 stage
-    the input halo per tile of whole output rows; everything else: 128)."""
+    conv_halo_default/conv_halo_shape: the 3x3 stride-1 64->64 convs stage the
+    input halo per tile of whole output rows; everything else: 128)."""
     import os
-    if os.environ.get("DELTA_CONV_HALO", "0") != "1":
-        return 128
+    env = os.environ.get("DELTA_CONV_HALO")
     P = (H + 2 * pad - R) // stride + 1
     if not (R == 3 and S == 3 and stride == 1 and pad == 1 and Cin % 64 == 0 and W <= 64):
+        return 128
+    if env == "0" or (env is None and not (Cin == 64 and K == 64)):
         return 128
     slot = 16 if W + 2 <= 16 else (32 if W + 2 <= 32 else 64)
     for rows in range(128 // slot, 0, -1):
