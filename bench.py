@@ -297,6 +297,18 @@ def main():
         torch.cuda.synchronize()
     rt.graph = saved_graph
     hbm_peak, tc_peak, tc_sus, peak_kind = measured_peaks()
+    # DRAM bytes per forward conv launch from the committed ncu capture
+    # (scripts/gpu_traffic.sh + scripts/conv_traffic.py), vs its algorithmic bytes
+    conv_traffic = {}
+    try:
+        with open(os.path.join(HERE, "profiles", "r01_conv_traffic.json")) as f:
+            t = json.load(f)
+        conv_traffic = {"dram_bytes_per_launch": t["dram_bytes_per_launch"],
+                        "note": f"ncu dram read+write per forward conv launch = "
+                                f"{t['traffic_over_algorithmic']}x its algorithmic bytes "
+                                f"({t['launches']} launches, profiles/r01_conv_traffic.json)"}
+    except Exception:  # noqa: BLE001
+        conv_traffic = {}
     conv_ms, conv_flops, conv_n, all_ms, conv_roof_ms = 0.0, 0.0, 0, 0.0, 0.0
     kinds = {}
     rc = {"launches": 0, "ms": 0.0, "roofline_ms": 0.0, "flops": 0.0, "bytes": 0.0, "by_op": {}}
@@ -413,7 +425,8 @@ def main():
                          "peak": tc_peak, "unit": "TFLOP/s",
                          "frac": round(achieved / tc_peak, 4) if tc_peak else None,
                          "peak_kind": f"{peak_kind} burst bf16",
-                         "traffic": None,
+                         "traffic": conv_traffic.get("dram_bytes_per_launch"),
+                         "traffic_note": conv_traffic.get("note"),
                          "launches_timed": conv_n,
                          "frac_of_roofline_time": round(conv_roof_ms / conv_ms, 4) if conv_ms else None,
                          "roofline_time_note": "sum over conv launches of max(FLOPs/TC peak, "

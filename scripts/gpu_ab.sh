@@ -1,5 +1,4 @@
-# A/B: 3x3 stride-1 input gradients on our kernel (fused BN backward) vs cuDNN
-for v in 0 1; do
-DELTA_OWN_DGRAD_3X3=$v timeout 600 python bench.py --steps 10 2>&1 | tail -1 | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('own3x3=$v', d['value'], d['no_eviction']['images_per_s'], d['roofline']['op_ms'])"
+# A/B: DELTA anchor sets at the 50% budget
+for a in out+narrow out; do
+timeout 600 python bench.py --steps 10 --anchors $a 2>&1 | tail -1 | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('anchors=$a', d.get('value'), d.get('no_eviction',{}).get('images_per_s'), d.get('plan',{}).get('counts'), d.get('recompute',{}).get('ms_per_step'))" 2>&1 | tail -1
 done
-DELTA_OWN_DGRAD_3X3=1 timeout 600 python -m pytest tests/test_runtime_gpu.py -q -x 2>&1 | tail -2
