@@ -12,6 +12,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <unordered_map>
@@ -35,6 +36,12 @@ struct delta_rt {
   std::unordered_map<uint64_t, std::pair<uint32_t, uint32_t>> recipe;  // node -> (first, count)
   bool copy_used[3] = {false, false, false};
   cudaEvent_t join[3] = {nullptr, nullptr, nullptr};
+  // side compute stream: ops flagged DELTA_KOP_SIDE run there, concurrently
+  // with the rest of their node, and are joined back before the node ends
+  cudaStream_t side = nullptr;
+  cudaEvent_t fork = nullptr, side_done = nullptr;
+  bool side_enabled = false;  // DELTA_SIDE_STREAM=1 (measured neutral: both chains are
+                              // bandwidth-bound full-grid kernels)
   delta_host_fn host_fn = nullptr;
   delta_action_fn after_fn = nullptr;
   void* ctx = nullptr;
@@ -207,12 +214,26 @@ delta_status run_node(delta_rt* rt, const delta_action& a, cudaStream_t st) {
   fr.n_in = a.n_inputs;
   const bool recompute = a.op == DELTA_ACT_RECOMPUTE;
   int n_host = 0;
+  bool forked = false;
   for (uint32_t j = 0; j < it->second.second; ++j) {
     const delta_kop& k = rt->kops[it->second.first + j];
     if (recompute && (k.flags & DELTA_KOP_FIRST_ONLY)) continue;
     if (!recompute && (k.flags & DELTA_KOP_RECOMPUTE_ONLY)) continue;
-    delta_status s = run_kop(rt, k, fr, a.node, recompute, st, n_host);
+    cudaStream_t ks = st;
+    if ((k.flags & DELTA_KOP_SIDE) && rt->side_enabled) {
+      if (!forked) {  // the side stream starts after everything before this node
+        RT_CUDA(cudaEventRecord(rt->fork, st));
+        RT_CUDA(cudaStreamWaitEvent(rt->side, rt->fork, 0));
+        forked = true;
+      }
+      ks = rt->side;
+    }
+    delta_status s = run_kop(rt, k, fr, a.node, recompute, ks, n_host);
     if (s) return s;
+  }
+  if (forked) {  // join: the node (and its arena reads) ends when both are done
+    RT_CUDA(cudaEventRecord(rt->side_done, rt->side));
+    RT_CUDA(cudaStreamWaitEvent(st, rt->side_done, 0));
   }
   return DELTA_OK;
 }
@@ -290,6 +311,10 @@ delta_status delta_rt_create(void* arena, uint64_t arena_bytes, uint64_t host_by
   if (e == cudaSuccess) e = cudaStreamCreateWithPriority(&rt->h2d, cudaStreamNonBlocking, hi);
   for (int s = 1; s < 3 && e == cudaSuccess; ++s)
     e = cudaEventCreateWithFlags(&rt->join[s], cudaEventDisableTiming);
+  if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&rt->side, cudaStreamNonBlocking);
+  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&rt->fork, cudaEventDisableTiming);
+  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&rt->side_done, cudaEventDisableTiming);
+  if (const char* v = std::getenv("DELTA_SIDE_STREAM")) rt->side_enabled = v[0] == '1';
   if (e != cudaSuccess) {
     delta_rt_destroy(rt);
     return cuda_fail(e, "delta_rt_create");
@@ -429,6 +454,9 @@ void delta_rt_destroy(delta_rt* rt) {
     if (ev) cudaEventDestroy(ev);
   for (int s = 1; s < 3; ++s)
     if (rt->join[s]) cudaEventDestroy(rt->join[s]);
+  if (rt->side) cudaStreamDestroy(rt->side);
+  if (rt->fork) cudaEventDestroy(rt->fork);
+  if (rt->side_done) cudaEventDestroy(rt->side_done);
   if (rt->d2h) cudaStreamDestroy(rt->d2h);
   if (rt->h2d) cudaStreamDestroy(rt->h2d);
   if (rt->host) cudaFreeHost(rt->host);

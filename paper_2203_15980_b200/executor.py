@@ -21,7 +21,7 @@ vp, i32, i64, u32, u64, f32 = C.c_void_p, C.c_int32, C.c_int64, C.c_uint32, C.c_
 REF_PTR, REF_OUT, REF_IN, REF_SCRATCH = 0, 1, 2, 3
 (K_COPY, K_CONV, K_CONV_EX, K_BN_STATS, K_BN_STATS_PARTS, K_BN_APPLY, K_BN_BWD, K_BN_BWD_PARTS,
  K_ADD_GRAD, K_MAXPOOL_FWD, K_MAXPOOL_BWD, K_AVGPOOL, K_SOFTMAX_XENT, K_HOST, K_WGRAD) = range(1, 16)
-FIRST_ONLY, RECOMPUTE_ONLY = 1, 2
+FIRST_ONLY, RECOMPUTE_ONLY, SIDE = 1, 2, 4
 
 
 

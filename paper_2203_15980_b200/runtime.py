@@ -225,7 +225,7 @@ class DeltaRuntime:
         # shortcut conv at its sampling grid
         self.short_ws = u8("short_ws")
         self.mp_ws = u8("mp_ws")
-        self.wg_ws = u8("wgrad_ws")
+        self.wg_ws = u8("wgrad_ws")  # weight-gradient partials (side stream: serial use)
         ncls = self.g.fc[1]
         self.loss = torch.zeros(1, dtype=torch.float32, device=self.device)
         self.dlogits = torch.empty(batch, ncls, dtype=torch.float32, device=self.device)
@@ -378,10 +378,13 @@ class DeltaRuntime:
                           (BN_EPS, BN_MOMENTUM), flags=X.FIRST_ONLY),
                     1 + K._merge_launches(K._chunks(M, C)), 0)
 
-        def wgrad(conv, dy_in, x_in):
-            """our tcgen05 weight gradient straight into the fp32 KRSC grad buffer"""
+        def wgrad(conv, dy_in, x_in, side=True):
+            """our tcgen05 weight gradient straight into the fp32 KRSC grad buffer,
+            on the side stream (it only reads the node's inputs: it overlaps the
+            input-gradient chain and is joined at the node's end)"""
             return X.kop(X.K_WGRAD, (X.IN(dy_in), X.IN(x_in), _ptr(pr.gviews["conv:" + conv]),
-                                     _ptr(self.wg_ws)), conv=self._wgrads[conv]._h)
+                                     _ptr(self.wg_ws)),
+                         conv=self._wgrads[conv]._h, flags=X.SIDE if side else 0)
 
         if op == "input":
             add(X.kop(X.K_COPY, (X.OUT(), _ptr(self.x_dev)), (self.x_dev.numel() * 2,)))
