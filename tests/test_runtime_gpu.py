@@ -297,7 +297,7 @@ def test_executed_gpu_timeline_passes_reference_replay_check(rts):
     assert violations == [], violations[:5]
 
 
-@pytest.mark.parametrize("frac,policy", [(0.44, P.PolicyMode.Delta), (0.7, P.PolicyMode.Delta),
+@pytest.mark.parametrize("frac,policy", [(0.55, P.PolicyMode.Delta), (0.7, P.PolicyMode.Delta),
                                          (0.5, P.PolicyMode.OffloadOnly),
                                          (0.5, P.PolicyMode.RecomputeOnly)])
 def test_budgets_and_policies_bit_identical_and_certified(rts, frac, policy):
