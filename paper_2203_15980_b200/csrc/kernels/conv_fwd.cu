@@ -44,10 +44,20 @@ namespace {
 constexpr int BM = 128;
 constexpr int BK = 64;
 constexpr int kThreads = 288;
-constexpr int MODE_GATHER = 0, MODE_STEM = 1, MODE_TMA = 2, MODE_IM2COL = 3;
+constexpr int MODE_GATHER = 0, MODE_STEM = 1, MODE_TMA = 2, MODE_IM2COL = 3, MODE_STEMG = 4,
+              MODE_STEMRAW = 5;
+// one output row per tile (rows >= Q of the 128-row tile are junk)
+constexpr bool row_tiled(int mode) { return mode == MODE_STEMRAW; }
+// MODE_STEMRAW: smem bytes per staged input row.  The row's pixel pairs land
+// at +RAW_DATA (128 B aligned for the TMA), pairs -2, -1 and W/2, W/2+1 are
+// zeros written once; the junk tile rows q < 128 read up to pair q+3.
+constexpr uint32_t RAW_ROW = 2304, RAW_DATA = 128;
+// A operand written by the producer threads (cp.async) rather than the TMA unit
+constexpr bool gathers(int mode) { return mode == MODE_GATHER || mode == MODE_STEMG; }
 // fused-epilogue operand ring: 24 KB per epilogue warp, slots of one 2 KB
 // block per operand (12 slots with one operand, 6 with two)
 constexpr uint32_t EPI_RING_WARP = 24576;
+
 
 
 struct ConvArgs {
@@ -161,24 +171,37 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* empty = full + STAGES;
   uint64_t* tfull = empty + STAGES;  // [2]
   uint64_t* tempty = tfull + 2;      // [2]
-  uint32_t* tslot = reinterpret_cast<uint32_t*>(tempty + 2);
+  uint64_t* bfull = tempty + 2;      // MODE_STEMRAW: resident weights landed
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(bfull + 1);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
-      mbar_init(&full[s], MODE == MODE_GATHER ? 4 + 1 : 1);
+      mbar_init(&full[s], gathers(MODE) ? 4 + 1 : 1);
       mbar_init(&empty[s], 1);
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&tfull[i], 1);
       mbar_init(&tempty[i], 4);
     }
+    mbar_init(bfull, 1);
     fence_mbar_init();
     tma_prefetch_desc(&wmap);
-    if (MODE != MODE_GATHER) tma_prefetch_desc(&amap);
+    if (!gathers(MODE)) tma_prefetch_desc(&amap);
     tma_prefetch_desc(&ymap);
+  }
+  if constexpr (MODE == MODE_STEMRAW) {
+    // the padding pairs around every staged input row: zero once (the TMA
+    // only ever writes the W/2 data pairs between them)
+    const uint32_t data_end = RAW_DATA + uint32_t(a.W >> 1) * 16;
+    for (int i = threadIdx.x; i < STAGES * 7 * 4; i += blockDim.x) {
+      const int row = i >> 2, part = i & 3;
+      const uint32_t off = (part < 2 ? RAW_DATA - 32 : data_end) + (part & 1) * 16;
+      st_shared_v4(sA + (row / 7) * A_STAGE + (row % 7) * RAW_ROW + off, make_uint4(0, 0, 0, 0));
+    }
+    fence_proxy_async_smem();
   }
   if (warp == 8) tmem_alloc(tslot, TMEM_COLS);
   tc_fence_before();
@@ -217,6 +240,31 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
           }
         }
+      } else if constexpr (MODE == MODE_STEMRAW) {
+        // Stem, one output row (n, p) per tile, no im2col at all: the 7 input
+        // rows 2p-3+r are staged as they are (pixel pairs, 2 zero pairs of
+        // padding each side from the TMA's out-of-bounds fill), and the MMA
+        // reads A straight from them: row q, K-chunk j of filter row r is
+        // pair q-2+j, i.e. a K-major no-swizzle operand with 16 B between
+        // K-adjacent core matrices and 128 B between M-adjacent ones
+        // (overlapping core matrices — each staged pair feeds 4 output
+        // columns).  The 32 KB of weights stay resident (loaded once).
+        const int n = tile / a.P;
+        const int p = tile - n * a.P;
+        if (tid == 0) {
+          if (tile == int(blockIdx.x)) {
+            mbar_arrive_expect_tx(bfull, 4 * B_STAGE);
+            for (int kb = 0; kb < 4; ++kb) tma_load_2d(sB + kb * B_STAGE, &wmap, bfull, kb * BK, 0);
+          }
+          const uint32_t s = it % STAGES;
+          if (it >= STAGES) mbar_wait(&empty[s], ((it / STAGES) - 1) & 1);
+          mbar_arrive_expect_tx(&full[s], 7u * uint32_t(a.W >> 1) * 16u);
+#pragma unroll
+          for (int r = 0; r < 7; ++r)
+            tma_load_4d(sA + s * A_STAGE + r * RAW_ROW + RAW_DATA, &amap, &full[s], 0, 0,
+                        2 * p - 3 + r, n);
+        }
+        ++it;
       } else if constexpr (MODE == MODE_STEM) {
         // 7x7/2 stem over C=4 viewed as pixel PAIRS (16 B = 8 channels): a
         // 7x4 stride-(2,1) conv, one 128-pixel x 16 B im2col box per tap,
@@ -262,22 +310,44 @@ __global__ void __launch_bounds__(kThreads, 1)
         // Per k-block the only address math left is one scalar tap offset.
         const bf16* rowp[ROWS];
         uint32_t vm[ROWS];
+        {
+          // decode (n, p, q) of this thread's first row once, then step by
+          // RSTEP rows (a division-free walk: RSTEP < Q for every ResNet conv
+          // but the loop handles any Q)
+          const int mfirst = m0 + row0;
+          int q = mfirst % a.Q;
+          const int t = mfirst / a.Q;
+          int n = t / a.P;
+          int p = t - n * a.P;
+          const bool stem = MODE == MODE_STEMG;
+          const int R = stem ? 7 : a.R, S = stem ? 4 : a.S;
+          const int Wv = stem ? (a.W >> 1) : a.W;          // pixels (pairs for the stem)
+          const long long pix = stem ? 8ll : (long long)a.C;  // elements per (pair) pixel
+          const int st = stem ? 2 : a.stride, sp = stem ? 3 : a.pad;
 #pragma unroll
-        for (int i = 0; i < ROWS; ++i) {
-          const int m = m0 + row0 + RSTEP * i;
-          vm[i] = 0;
-          rowp[i] = a.x;
-          if (m < a.M) {
-            const int q = m % a.Q;
-            const int t = m / a.Q;
-            const int n = t / a.P;
-            const int hb = (t - n * a.P) * a.stride - a.pad;
-            const int wb = q * a.stride - a.pad;
-            rowp[i] = a.x + (((long long)n * a.H + hb) * a.W + wb) * (long long)a.C;
-            uint32_t rm = 0, cm = 0;
-            for (int r = 0; r < a.R; ++r) rm |= uint32_t((unsigned)(hb + r) < (unsigned)a.H) << r;
-            for (int c = 0; c < a.S; ++c) cm |= uint32_t((unsigned)(wb + c) < (unsigned)a.W) << c;
-            vm[i] = rm | (cm << 8);
+          for (int i = 0; i < ROWS; ++i) {
+            const int m = mfirst + RSTEP * i;
+            vm[i] = 0;
+            rowp[i] = a.x;
+            if (m < a.M) {
+              const int hb = p * st - sp;
+              const int wb = stem ? q - 2 : q * st - sp;
+              rowp[i] = a.x + (((long long)n * a.H + hb) * Wv + wb) * pix;
+              // valid filter rows r: 0 <= hb + r < H; columns c: 0 <= wb + c < Wv
+              const int rlo = min(max(-hb, 0), R), rhi = min(max(a.H - hb, 0), R);
+              const int clo = min(max(-wb, 0), S), chi = min(max(Wv - wb, 0), S);
+              const uint32_t rm = ((1u << rhi) - 1u) & ~((1u << rlo) - 1u);
+              const uint32_t cm = ((1u << chi) - 1u) & ~((1u << clo) - 1u);
+              vm[i] = rm | (cm << 8);
+            }
+            q += RSTEP;
+            while (q >= a.Q) {
+              q -= a.Q;
+              if (++p == a.P) {
+                p = 0;
+                ++n;
+              }
+            }
           }
         }
         // swizzled smem destination of (row, part): the XOR term is constant
@@ -293,7 +363,20 @@ __global__ void __launch_bounds__(kThreads, 1)
             tma_load_2d(sB + s * B_STAGE, &wmap, &full[s], kb * BK, n0);
           }
           const uint32_t dstA = sA + s * A_STAGE + dst_thread;
-          {
+          if constexpr (MODE == MODE_STEMG) {
+            // this thread's 16 B column of the k-block is pair-tap kb*8+part
+            // (taps >= 28 meet zero weights: zero-filled)
+            const int tp = kb * 8 + part;
+            const int r = tp >> 2, j = tp & 3;
+            const long long off = (long long)(r * (a.W >> 1) + j) * 8;
+            const uint32_t need = (1u << r) | (1u << (8 + j));
+#pragma unroll
+            for (int i = 0; i < ROWS; ++i) {
+              const bool ok = tp < 28 && (vm[i] & need) == need;
+              // L1-allocating: neighbouring rows' windows overlap
+              cp_async_16_ca(dstA + i * (RSTEP * 128), ok ? rowp[i] + off : a.x, ok);
+            }
+          } else {
             const int r = tap / a.S, sx = tap - r * a.S;
             const long long off = (long long)(r * a.W + sx) * a.C + c0 + part * 8;
             const uint32_t need = (1u << r) | (1u << (8 + sx));
@@ -322,7 +405,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
       }
     }
-    if constexpr (MODE == MODE_GATHER) {
+    if constexpr (gathers(MODE)) {
       // drain: signal the last LAG stages
       cp_async_wait<0>();
       fence_proxy_async_smem();
@@ -395,7 +478,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint32_t ec = 0;  // chunks consumed by this warp
     uint32_t lt = 0;
     for (int tile = blockIdx.x; tile < a.tiles; tile += gridDim.x, ++lt) {
-      const int m0 = (tile / a.n_tiles) * BM;
+      // row-tiled stem: tile = one output row of Q pixels (rows >= Q are junk)
+      const int m0 = (tile / a.n_tiles) * (row_tiled(MODE) ? a.Q : BM);
       const int n0 = (tile % a.n_tiles) * BN;
       const uint32_t acc = lt & 1;
       mbar_wait(&tfull[acc], (lt >> 1) & 1);
@@ -426,6 +510,13 @@ __global__ void __launch_bounds__(kThreads, 1)
             unpack8f(ld_row16(sb, lane, u), mk);
 #pragma unroll
             for (int i = 0; i < 8; ++i) v[u * 8 + i] += mk[i] > 0.f ? g[i] * inv : 0.f;
+          }
+        }
+        if constexpr (row_tiled(MODE)) {
+          // junk rows past the output row: zero (they feed the BN statistics)
+          if (quarter * 32 + lane >= a.Q) {
+#pragma unroll
+            for (int i = 0; i < 32; ++i) v[i] = 0.f;
           }
         }
         // pack to bf16 (packed epilogue ops on top), stage for the TMA store
@@ -492,7 +583,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         fence_proxy_async_smem();
         __syncwarp();
         if (lane == 0 && col < a.K) {
-          tma_store_2d(&ymap, buf, col, m0 + quarter * 32);
+          if constexpr (row_tiled(MODE))
+            tma_store_3d(&ymap, buf, col, quarter * 32, tile / a.n_tiles);  // clipped at Q
+          else
+            tma_store_2d(&ymap, buf, col, m0 + quarter * 32);
           bulk_commit();
         }
         if (a.stats != nullptr) {
@@ -525,7 +619,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         // combine the four row quarters -> one partial per channel per tile
         asm volatile("bar.sync 1, 128;" ::: "memory");
         const int et = (warp - 4) * 32 + lane;
-        const int n_rows = min(BM, a.M - m0);
+        const int n_rows = row_tiled(MODE) ? a.Q : min(BM, a.M - m0);
         for (int c = et; c < BN; c += 128) {
           float S = 0.f, Q = 0.f;
 #pragma unroll
@@ -541,7 +635,7 @@ __global__ void __launch_bounds__(kThreads, 1)
               const float mu = S / float(n_rows);
               out = make_float2(mu, fmaxf(Q - S * mu, 0.f));
             }
-            a.stats[size_t(m0 / BM) * a.K + n0 + c] = out;
+            a.stats[size_t(tile / a.n_tiles) * a.K + n0 + c] = out;
           }
         }
         asm volatile("bar.sync 1, 128;" ::: "memory");
@@ -560,7 +654,24 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (lt >= 2) mbar_wait(&tempty[acc], ((lt >> 1) - 1) & 1);
         tc_fence_after();
         const uint32_t d = tmem + acc * ACC_COLS;
-        for (int kb = 0; kb < a.kblocks; ++kb, ++it) {
+        if constexpr (MODE == MODE_STEMRAW) {
+          if (lt == 0) mbar_wait(bfull, 0);
+          const uint32_t s = it % STAGES;
+          mbar_wait(&full[s], (it / STAGES) & 1);
+          tc_fence_after();
+#pragma unroll
+          for (int r = 0; r < 7; ++r)
+#pragma unroll
+            for (int k = 0; k < 2; ++k) {
+              const uint64_t ad = umma_desc_noswz(
+                  sA + s * A_STAGE + r * RAW_ROW + RAW_DATA - 32 + k * 32, 16, 128);
+              const uint64_t bd = umma_desc_sw128(sB + (r >> 1) * B_STAGE + (r & 1) * 64 + k * 32);
+              umma_bf16(d, ad, bd, idesc, (r | k) != 0 ? 1u : 0u);
+            }
+          umma_commit(&empty[s]);
+          ++it;
+        }
+        for (int kb = 0; kb < (MODE == MODE_STEMRAW ? 0 : a.kblocks); ++kb, ++it) {
           const uint32_t s = it % STAGES;
           mbar_wait(&full[s], (it / STAGES) & 1);
           fence_proxy_async_smem();
@@ -683,6 +794,39 @@ bool encode_out(CUtensorMap* m, void* y, uint64_t cols, uint64_t rows) {
             CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+// MODE_STEMRAW input rows: [N][H][W/2 pairs] viewed as runs of c = 8 x 2^k
+// elements (the longest run of <= 8 pixel pairs that divides W/2): one box =
+// one whole input row; rows outside the image are zero-filled; no swizzle.
+bool encode_stem_raw(CUtensorMap* m, const void* x, const ConvPlan& cp) {
+  auto fn = encode_fn();
+  if (!fn) return false;
+  const uint64_t W2 = uint64_t(cp.W / 2);
+  uint64_t c = 8;
+  while (c < 64 && (W2 * 8) % (2 * c) == 0) c *= 2;
+  const uint64_t runs = W2 * 8 / c;
+  if (runs > 256) return false;
+  cuuint64_t dims[4] = {c, runs, cuuint64_t(cp.H), cuuint64_t(cp.N)};
+  cuuint64_t strides[3] = {c * 2, W2 * 16, uint64_t(cp.H) * W2 * 16};
+  cuuint32_t box[4] = {cuuint32_t(c), cuuint32_t(runs), 1, 1};
+  cuuint32_t estr[4] = {1, 1, 1, 1};
+  return fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(x), dims, strides, box,
+            estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+// Output of the row-tiled stem: [N*P rows][Q][K], 32x32 boxes clipped at Q.
+bool encode_out_rows(CUtensorMap* m, void* y, const ConvPlan& cp) {
+  auto fn = encode_fn();
+  if (!fn) return false;
+  cuuint64_t dims[3] = {cuuint64_t(cp.K), cuuint64_t(cp.Q), cuuint64_t(cp.N) * cp.P};
+  cuuint64_t strides[2] = {cuuint64_t(cp.K) * 2, cuuint64_t(cp.Q) * cp.K * 2};
+  cuuint32_t box[3] = {32, 32, 1};
+  cuuint32_t estr[3] = {1, 1, 1};
+  return fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, y, dims, strides, box, estr,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B,
+            CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 // DELTA_CONV_GATHER=1 selects the cp.async im2col gather instead of the TMA
 // im2col unit (kept as the reference path for the A operand).
 bool gather_forced() {
@@ -690,6 +834,18 @@ bool gather_forced() {
   if (v < 0) {
     const char* e = std::getenv("DELTA_CONV_GATHER");
     v = (e && e[0] == '1') ? 1 : 0;
+  }
+  return v == 1;
+}
+
+// Stems whose output rows do not fit a tile (or DELTA_STEM_MODE=tma|gather):
+// 128-pixel tiles with the A operand from the TMA im2col unit (one 128 x 16 B
+// box per pair-tap) or gathered by the producer threads (cp.async, 16 B pairs).
+bool stem_tma() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = std::getenv("DELTA_STEM_MODE");
+    v = (e && e[0] == 't') ? 1 : 0;
   }
   return v == 1;
 }
@@ -726,7 +882,7 @@ cudaError_t launch(const ConvPlan& cp, const void* x, void* y, float* stats,
   a.kblocks = cp.kdim / BK;
   a.taps = cp.R * cp.S;
   a.n_tiles = (cp.K + BN - 1) / BN;
-  a.tiles = ((a.M + BM - 1) / BM) * a.n_tiles;
+  a.tiles = (row_tiled(MODE) ? cp.N * cp.P : (a.M + BM - 1) / BM) * a.n_tiles;
   a.stats = reinterpret_cast<float2*>(stats);
   a.e = epi;
   alignas(64) CUtensorMap amap;
@@ -737,10 +893,14 @@ cudaError_t launch(const ConvPlan& cp, const void* x, void* y, float* stats,
     if (!encode_im2col(&amap, x, cp)) return cudaErrorInvalidValue;
   } else if (MODE == MODE_STEM) {
     if (!encode_stem_im2col(&amap, x, cp)) return cudaErrorInvalidValue;
+  } else if (MODE == MODE_STEMRAW) {
+    if (!encode_stem_raw(&amap, x, cp)) return cudaErrorInvalidValue;
   } else {
     amap = *reinterpret_cast<const CUtensorMap*>(cp.wmap);  // unused
   }
-  if (!encode_out(&ymap, y, uint64_t(cp.K), uint64_t(a.M))) return cudaErrorInvalidValue;
+  if (row_tiled(MODE) ? !encode_out_rows(&ymap, y, cp)
+                           : !encode_out(&ymap, y, uint64_t(cp.K), uint64_t(a.M)))
+    return cudaErrorInvalidValue;
   const int grid = a.tiles < num_sms() ? a.tiles : num_sms();
   kern<<<grid, kThreads, smem, st>>>(*reinterpret_cast<const CUtensorMap*>(cp.wmap), amap, ymap,
                                      a);
@@ -763,8 +923,15 @@ int conv_plan_init(ConvPlan* cp, const void* w) {
   // the 9 weight tiles resident (conv_halo.cu; 124 -> 88 us at 56x56, bs 256).
   // DELTA_CONV_HALO=0 disables it, =1 also routes the other 3x3 stride-1
   // shapes there (experimental).
+  // the stem runs row-tiled over raw input rows (MODE_STEMRAW) when an output
+  // row fits a tile; DELTA_STEM_MODE=tma / gather select the 128-pixel-tile
+  // im2col paths (also the fallback for wider images)
+  const char* sm = std::getenv("DELTA_STEM_MODE");
+  cp->stem_rows = cp->C == 4 && cp->K <= 64 && cp->Q >= 4 && cp->Q <= 124 && !(sm && sm[0]);
   const char* he = std::getenv("DELTA_CONV_HALO");
-  cp->halo = he ? (he[0] == '1' && conv_halo_eligible(*cp)) : conv_halo_default(*cp);
+  cp->halo = gather_forced() ? 0
+             : he             ? (he[0] == '1' && conv_halo_eligible(*cp))
+                              : conv_halo_default(*cp);
   if (cp->halo) {
     conv_halo_shape(cp);
     if (cp->halo_rows == 0) cp->halo = 0;
@@ -832,6 +999,8 @@ cudaError_t conv_forward(const ConvPlan& cp, const void* x, void* y, float* stat
   }
   switch (cp.bn) {
     case 64:
+      if (stem && cp.stem_rows) return launch<64, 8, MODE_STEMRAW, EV_STORE>(cp, x, y, stats, e, st);
+      if (stem && !stem_tma()) return launch<64, 8, MODE_STEMG, EV_STORE>(cp, x, y, stats, e, st);
       return stem ? launch<64, 8, MODE_STEM, EV_STORE>(cp, x, y, stats, e, st)
              : tma_a ? launch<64, 8, MODE_TMA, EV_STORE>(cp, x, y, stats, e, st)
              : use_gather ? launch<64, 8, MODE_GATHER, EV_STORE>(cp, x, y, stats, e, st)

@@ -11,6 +11,7 @@ struct ConvPlan {
   int N, H, W, C, K, R, S, stride, pad;
   int P, Q, kdim, bn;
   int halo, halo_slot, halo_rows;  // 3x3 stride-1: input halo staged per tile (conv_halo.cu)
+  int stem_rows;                   // C=4 stem: one output row per tile (conv_fwd.cu MODE_STEMROW)
   alignas(64) unsigned char wmap[128];  // CUtensorMap over the [K][kdim] weight matrix
 };
 // Fused epilogues (the backward pass runs input-gradient convolutions through
@@ -44,9 +45,10 @@ bool conv_halo_default(const ConvPlan& cp);  // the shapes it is dispatched for 
 void conv_halo_shape(ConvPlan* cp);
 cudaError_t conv_halo_forward(const ConvPlan& cp, const void* x, void* y, float* stats,
                               cudaStream_t st);
-// output rows per BN-statistics partial (128, or rows*Q for the halo path)
+// output rows per BN-statistics partial (128, rows*Q for the halo path, Q
+// for the row-tiled stem)
 inline int conv_stats_rows(const ConvPlan& cp) {
-  return cp.halo ? cp.halo_rows * cp.Q : 128;
+  return cp.halo ? cp.halo_rows * cp.Q : (cp.stem_rows ? cp.Q : 128);
 }
 // choose the N tile (64/128/256, dividing K; fused epilogues need <= 128)
 int conv_plan_set_tile_n(ConvPlan* cp, int bn, const void* w);

@@ -135,15 +135,21 @@ class Wgrad:
 
 
 def conv_stats_rows(N, H, W, Cin, K, R, S, stride, pad) -> int:
-    """Output rows per BN-statistics partial of a conv (mirrors conv_halo.cu
-    conv_halo_default/conv_halo_shape: the 3x3 stride-1 64->64 convs stage the
-    input halo per tile of whole output rows; everything else: 128)."""
+    """Output rows per BN-statistics partial of a conv (mirrors kernels.hpp
+    conv_stats_rows: the 3x3 stride-1 64->64 convs stage the input halo per
+    tile of whole output rows (conv_halo.cu), the stem is tiled by output row,
+    everything else: 128)."""
     import os
     env = os.environ.get("DELTA_CONV_HALO")
     P = (H + 2 * pad - R) // stride + 1
+    if Cin == 4:  # the row-tiled stem (conv_fwd.cu MODE_STEMROW): one partial per output row
+        Q = (W + 2 * pad - S) // stride + 1
+        if K <= 64 and 4 <= Q <= 124 and not os.environ.get("DELTA_STEM_MODE"):
+            return Q
+        return 128
     if not (R == 3 and S == 3 and stride == 1 and pad == 1 and Cin % 64 == 0 and W <= 64):
         return 128
-    if env == "0" or (env is None and not (Cin == 64 and K == 64)):
+    if env == "0" or os.environ.get("DELTA_CONV_GATHER") == "1" or (env is None and not (Cin == 64 and K == 64)):
         return 128
     slot = 16 if W + 2 <= 16 else (32 if W + 2 <= 32 else 64)
     for rows in range(128 // slot, 0, -1):
