@@ -13,13 +13,17 @@
 // Persistent, warp-specialised (one CTA per SM, static round-robin tiles):
 //   warps 0-3 : producers.  MODE_IM2COL (3x3, strided 1x1): A by the TMA
 //               im2col unit (out-of-image taps zero-filled = the padding);
-//               MODE_STEM: TMA im2col over pixel pairs (see below); MODE_TMA
-//               (1x1, stride 1): A is a plain [M, C] matrix loaded by TMA;
-//               MODE_GATHER (opt-in, DELTA_CONV_GATHER=1): cp.async im2col.
-//               The weight tile B is always one TMA load.
-//   warps 4-7 : epilogue — TMEM -> registers -> bf16 -> HBM, one TMEM lane
-//               quarter each.
-//   warp 8    : TMEM allocation + single-thread tcgen05.mma issue.
+//               MODE_STEMRAW (the C=4 stem): raw input rows, one output row
+//               per tile, A addressed straight into them (see below);
+//               MODE_TMA (1x1, stride 1): A is a plain [M, C] matrix loaded
+//               by TMA; MODE_GATHER (opt-in, DELTA_CONV_GATHER=1) and
+//               MODE_STEMG: cp.async im2col; MODE_STEM: TMA im2col over pixel
+//               pairs (wide stems).  The weight tile B is one TMA load.
+//   warps 4-11: epilogue — TMEM -> registers -> bf16 -> HBM; two warps per
+//               TMEM lane quarter, alternating 32-column chunks (8 epilogue
+//               warps: the per-chunk work — fused operands, ReLU masks, BN
+//               partials — was the pacing stage with 4).
+//   warp 12   : TMEM allocation + single-thread tcgen05.mma issue.
 // Two TMEM accumulators: the epilogue of tile i drains one while the MMAs of
 // tile i+1 fill the other.  smem stages ring with full/empty mbarriers;
 // tcgen05.commit releases a stage the moment the tensor core has consumed it.
@@ -43,7 +47,14 @@ namespace {
 
 constexpr int BM = 128;
 constexpr int BK = 64;
-constexpr int kThreads = 288;
+// warps 0-3 producers, 4 .. 4+EPI_W-1 epilogue (EPI_W/4 warps per TMEM lane
+// quarter, splitting a tile's 32-column chunks), then the MMA warp
+#ifndef DELTA_CONV_EPI_WARPS
+#define DELTA_CONV_EPI_WARPS 8
+#endif
+constexpr int EPI_W = DELTA_CONV_EPI_WARPS;
+constexpr int MMA_WARP = 4 + EPI_W;
+constexpr int kThreads = (MMA_WARP + 1) * 32;
 constexpr int MODE_GATHER = 0, MODE_STEM = 1, MODE_TMA = 2, MODE_IM2COL = 3, MODE_STEMG = 4,
               MODE_STEMRAW = 5;
 // one output row per tile (rows >= Q of the 128-row tile are junk)
@@ -56,7 +67,16 @@ constexpr uint32_t RAW_ROW = 2304, RAW_DATA = 128;
 constexpr bool gathers(int mode) { return mode == MODE_GATHER || mode == MODE_STEMG; }
 // fused-epilogue operand ring: 24 KB per epilogue warp, slots of one 2 KB
 // block per operand (12 slots with one operand, 6 with two)
-constexpr uint32_t EPI_RING_WARP = 24576;
+// Fused-epilogue operand ring (all epilogue warps): whatever shared memory the
+// operand stages, the output staging and the statistics scratch leave, in
+// whole 2 KB blocks per warp — the ring depth is what keeps the epilogue's
+// operand reads in flight.
+constexpr uint32_t SMEM_MAX = 232448;
+template <int BN, int STAGES>
+constexpr uint32_t epi_ring_bytes() {
+  return (SMEM_MAX - 1024 - 256 - 4 * BN * 8 - 16384 - STAGES * (128 * 128 + BN * 128)) /
+         (EPI_W * 2048) * (EPI_W * 2048);
+}
 
 
 
@@ -160,9 +180,10 @@ __global__ void __launch_bounds__(kThreads, 1)
   const uint32_t sB = sA + STAGES * A_STAGE;
   // epilogue staging: 4 warps x 2 buffers x (32 rows x 64 B), 64B-swizzled
   const uint32_t sOut = sA + STAGES * (A_STAGE + B_STAGE);
-  // fused-epilogue operand ring: 4 warps x EPI_RING_WARP
+  // fused-epilogue operand ring: EPI_W warps x EPI_RING_WARP
   constexpr bool FUSED = EV != EV_STORE;
-  constexpr uint32_t IN_BYTES = FUSED ? 4 * EPI_RING_WARP : 0;
+  constexpr uint32_t EPI_RING_WARP = epi_ring_bytes<BN, STAGES>() / EPI_W;
+  constexpr uint32_t IN_BYTES = FUSED ? EPI_W * EPI_RING_WARP : 0;
   const uint32_t sIn = sOut + 16384;
   // BN-statistics scratch: per quarter-warp column (sum, sumsq), [4][BN] float2
   float2* red = reinterpret_cast<float2*>(smem + STAGES * (A_STAGE + B_STAGE) + 16384 + IN_BYTES);
@@ -184,7 +205,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&tfull[i], 1);
-      mbar_init(&tempty[i], 4);
+      mbar_init(&tempty[i], EPI_W);
     }
     mbar_init(bfull, 1);
     fence_mbar_init();
@@ -203,7 +224,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     fence_proxy_async_smem();
   }
-  if (warp == 8) tmem_alloc(tslot, TMEM_COLS);
+  if (warp == MMA_WARP) tmem_alloc(tslot, TMEM_COLS);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -415,27 +436,35 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (uint32_t j = first; j < it; ++j) mbar_arrive(&full[j % STAGES]);
       }
     }
-  } else if (warp < 8) {
+  } else if (warp < MMA_WARP) {
     // ============================ epilogue =============================
     const int quarter = warp & 3;  // TMEM lanes [32*quarter, 32*quarter+32)
+    // HALVES warps share a lane quarter: warp `half` takes chunks half,
+    // half + HALVES, ... of every tile (CHW of them)
+    constexpr int HALVES = EPI_W / 4;
+    const int half = (warp - 4) >> 2;
     // fused operands: t0 = add / add_mask (pooled) / xc, t1 = out_mask
     constexpr int NOPS = ev_operands(EV);
     constexpr uint32_t SLOT = NOPS * 2048u;
-    constexpr uint32_t NSLOTS = NOPS ? EPI_RING_WARP / SLOT : 1;  // 12 or 6
-    const uint32_t ring = sIn + quarter * EPI_RING_WARP;
-    constexpr int CH = BN / 32;  // chunks per tile
+    constexpr uint32_t NSLOTS = NOPS ? EPI_RING_WARP / SLOT : 1;
+    static_assert(!NOPS || NSLOTS >= 2, "operand ring");
+    const uint32_t ring = sIn + (warp - 4) * EPI_RING_WARP;
+    constexpr int CH = BN / 32;         // chunks per tile
+    constexpr int CHW = CH / HALVES;    // chunks per tile of this warp
+    static_assert(CHW >= 1 && CH % HALVES == 0, "epilogue split");
     const bf16* src0 = static_cast<const bf16*>(
         EV == EV_BN_BWD ? a.e.xc : (EV == EV_POOL ? a.e.add_mask : a.e.add));
     const bf16* src1 = static_cast<const bf16*>(a.e.out_mask);
-    // stage this warp's chunk number e (tile = first + (e / CH) * grid, j = e % CH)
+    // stage this warp's chunk number e (tile = first + (e / CHW) * grid,
+    // chunk j = half + (e % CHW) * HALVES)
     // with cp.async: 4 x 16 B per lane per operand, 8 full rows per instruction,
     // rows past M zero-filled; one commit group per chunk (possibly empty)
     auto prefetch = [&](uint32_t e) {
-      const int tile_ = blockIdx.x + int(e / CH) * gridDim.x;
+      const int tile_ = blockIdx.x + int(e / CHW) * gridDim.x;
       if (tile_ < a.tiles) {
         const uint32_t sb = ring + (e % NSLOTS) * SLOT;
         const int pm = (tile_ / a.n_tiles) * BM + quarter * 32;
-        const int pc = (tile_ % a.n_tiles) * BN + int(e % CH) * 32;
+        const int pc = (tile_ % a.n_tiles) * BN + (half + int(e % CHW) * HALVES) * 32;
         // stride-2 add: (n, p, q) of the block's first row, once per chunk
         int q0 = 0, p0 = 0, n0_ = 0;
         if ((EV == EV_ADD || EV == EV_ADD_OM) && a.e.add_stride2) {
@@ -484,9 +513,11 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint32_t acc = lt & 1;
       mbar_wait(&tfull[acc], (lt >> 1) & 1);
       tc_fence_after();
-      const uint32_t stage_base = sOut + quarter * 4096;
+      // TMA-store staging: 16 KB over the epilogue warps, NBUF 2 KB buffers each
+      constexpr int NBUF = 16384 / EPI_W / 2048;
+      const uint32_t stage_base = sOut + (warp - 4) * (NBUF * 2048);
 #pragma unroll 1
-      for (int j = 0; j < BN / 32; ++j, ++ec) {
+      for (int j = half; j < CH; j += HALVES, ++ec) {
         // the slot refilled here was consumed (and __syncwarp'ed) last chunk
         if constexpr (FUSED) prefetch(ec + NSLOTS - 1);
         float v[32];
@@ -572,9 +603,9 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
         }
         if constexpr (FUSED) __syncwarp();  // every lane has read the slot before it is refilled
-        const uint32_t buf = stage_base + (j & 1) * 2048;
-        // the TMA store that last read this buffer (two chunks ago) is done
-        if (lane == 0) bulk_wait_read<1>();
+        const uint32_t buf = stage_base + (ec % NBUF) * 2048;
+        // the TMA store that last read this buffer (NBUF chunks ago) is done
+        if (lane == 0) bulk_wait_read<NBUF - 1>();
         __syncwarp();
         // row `lane` = 64 B = 4 chunks of 16 B; 64B swizzle: chunk ^= (row>>1)&3
 #pragma unroll
@@ -617,10 +648,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       if (a.stats != nullptr) {
         // combine the four row quarters -> one partial per channel per tile
-        asm volatile("bar.sync 1, 128;" ::: "memory");
+        asm volatile("bar.sync 1, %0;" ::"n"(EPI_W * 32) : "memory");
         const int et = (warp - 4) * 32 + lane;
         const int n_rows = row_tiled(MODE) ? a.Q : min(BM, a.M - m0);
-        for (int c = et; c < BN; c += 128) {
+        for (int c = et; c < BN; c += EPI_W * 32) {
           float S = 0.f, Q = 0.f;
 #pragma unroll
           for (int qq = 0; qq < 4; ++qq) {
@@ -638,7 +669,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             a.stats[size_t(tile / a.n_tiles) * a.K + n0 + c] = out;
           }
         }
-        asm volatile("bar.sync 1, 128;" ::: "memory");
+        asm volatile("bar.sync 1, %0;" ::"n"(EPI_W * 32) : "memory");
       }
       tc_fence_before();
       __syncwarp();
@@ -691,17 +722,17 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     __syncwarp();
   }
-  if (warp >= 4 && warp < 8 && lane == 0) bulk_wait<0>();  // output visible before exit
+  if (warp >= 4 && warp < MMA_WARP && lane == 0) bulk_wait<0>();  // output visible before exit
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  if (warp == 8) tmem_dealloc(tmem, TMEM_COLS);
+  if (warp == MMA_WARP) tmem_dealloc(tmem, TMEM_COLS);
 }
 
 template <int BN, int STAGES, bool FUSED>
 constexpr size_t conv_smem_bytes() {
   return size_t(STAGES) * (BM * 128 + BN * 128) + 16384 /*epilogue staging*/ +
-         (FUSED ? 4 * EPI_RING_WARP : 0) /*epilogue operand ring*/ + 4 * BN * 8 /*stats scratch*/ +
+         (FUSED ? epi_ring_bytes<BN, STAGES>() : 0) /*epilogue operand ring*/ + 4 * BN * 8 /*stats scratch*/ +
          1024 /*align*/ + 256 /*barriers*/;
 }
 
