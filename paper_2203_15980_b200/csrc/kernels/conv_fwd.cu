@@ -37,6 +37,7 @@
 
 #include "kernels/kernels.hpp"
 #include "kernels/sm100_common.cuh"
+#include "kernels/tma_host.hpp"
 
 namespace delta_k {
 
@@ -677,50 +678,58 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   } else {
     // ============================ MMA issuer ===========================
-    if (lane == 0) {
-      constexpr uint32_t idesc = umma_idesc_bf16(BM, BN);
-      uint32_t it = 0, lt = 0;
-      for (int tile = blockIdx.x; tile < a.tiles; tile += gridDim.x, ++lt) {
-        const uint32_t acc = lt & 1;
-        if (lt >= 2) mbar_wait(&tempty[acc], ((lt >> 1) - 1) & 1);
+    // The whole warp walks the loop (barrier waits, warp-uniform descriptors
+    // built by 64-bit adds), one elected lane issues each k-block's MMAs:
+    // issuing from lane 0 alone cost a dozen dependent uniform-datapath
+    // instructions per MMA, the pacing stage for the N <= 128 tiles.
+    constexpr uint32_t idesc = umma_idesc_bf16(BM, BN);
+    uint32_t it = 0, lt = 0;
+    for (int tile = blockIdx.x; tile < a.tiles; tile += gridDim.x, ++lt) {
+      const uint32_t acc = lt & 1;
+      if (lt >= 2) mbar_wait(&tempty[acc], ((lt >> 1) - 1) & 1);
+      tc_fence_after();
+      const uint32_t d = tmem + acc * ACC_COLS;
+      if constexpr (MODE == MODE_STEMRAW) {
+        if (lt == 0) mbar_wait(bfull, 0);
+        const uint32_t s = it % STAGES;
+        mbar_wait(&full[s], (it / STAGES) & 1);
         tc_fence_after();
-        const uint32_t d = tmem + acc * ACC_COLS;
-        if constexpr (MODE == MODE_STEMRAW) {
-          if (lt == 0) mbar_wait(bfull, 0);
-          const uint32_t s = it % STAGES;
-          mbar_wait(&full[s], (it / STAGES) & 1);
-          tc_fence_after();
+        // A: K step k of filter row r = 16 B x (2k) into the staged row
+        const uint64_t ad0 = umma_desc_noswz(sA + s * A_STAGE + RAW_DATA - 32, 16, 128);
+        const uint64_t bd0 = umma_desc_sw128(sB);
+        if (elect_one()) {
 #pragma unroll
           for (int r = 0; r < 7; ++r)
 #pragma unroll
-            for (int k = 0; k < 2; ++k) {
-              const uint64_t ad = umma_desc_noswz(
-                  sA + s * A_STAGE + r * RAW_ROW + RAW_DATA - 32 + k * 32, 16, 128);
-              const uint64_t bd = umma_desc_sw128(sB + (r >> 1) * B_STAGE + (r & 1) * 64 + k * 32);
-              umma_bf16(d, ad, bd, idesc, (r | k) != 0 ? 1u : 0u);
-            }
-          umma_commit(&empty[s]);
-          ++it;
-        }
-        for (int kb = 0; kb < (MODE == MODE_STEMRAW ? 0 : a.kblocks); ++kb, ++it) {
-          const uint32_t s = it % STAGES;
-          mbar_wait(&full[s], (it / STAGES) & 1);
-          fence_proxy_async_smem();
-          tc_fence_after();
-#pragma unroll
-          for (int k = 0; k < BK / 16; ++k) {
-            const uint64_t ad = MODE == MODE_STEM
-                                    ? umma_desc_noswz(sA + s * A_STAGE + k * 4096, 2048, 128)
-                                    : umma_desc_sw128(sA + s * A_STAGE + k * 32);
-            const uint64_t bd = umma_desc_sw128(sB + s * B_STAGE + k * 32);
-            umma_bf16(d, ad, bd, idesc, (kb | k) != 0 ? 1u : 0u);
-          }
+            for (int k = 0; k < 2; ++k)
+              umma_bf16(d, ad0 + uint64_t(r * (RAW_ROW >> 4) + k * 2),
+                        bd0 + uint64_t((r >> 1) * (B_STAGE >> 4) + (r & 1) * 4 + k * 2), idesc,
+                        (r | k) != 0 ? 1u : 0u);
           umma_commit(&empty[s]);
         }
-        umma_commit(&tfull[acc]);
+        __syncwarp();
+        ++it;
       }
+      for (int kb = 0; kb < (MODE == MODE_STEMRAW ? 0 : a.kblocks); ++kb, ++it) {
+        const uint32_t s = it % STAGES;
+        mbar_wait(&full[s], (it / STAGES) & 1);
+        fence_proxy_async_smem();
+        tc_fence_after();
+        const uint64_t ad0 = MODE == MODE_STEM ? umma_desc_noswz(sA + s * A_STAGE, 2048, 128)
+                                               : umma_desc_sw128(sA + s * A_STAGE);
+        const uint64_t bd0 = umma_desc_sw128(sB + s * B_STAGE);
+        if (elect_one()) {
+#pragma unroll
+          for (int k = 0; k < BK / 16; ++k)
+            umma_bf16(d, ad0 + uint64_t(MODE == MODE_STEM ? k * 256 : k * 2), bd0 + uint64_t(k * 2),
+                      idesc, (kb | k) != 0 ? 1u : 0u);
+          umma_commit(&empty[s]);
+        }
+        __syncwarp();
+      }
+      if (elect_one()) umma_commit(&tfull[acc]);
+      __syncwarp();
     }
-    __syncwarp();
   }
   if (warp >= 4 && warp < MMA_WARP && lane == 0) bulk_wait<0>();  // output visible before exit
   tc_fence_before();
@@ -825,26 +834,6 @@ bool encode_out(CUtensorMap* m, void* y, uint64_t cols, uint64_t rows) {
             CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-// MODE_STEMRAW input rows: [N][H][W/2 pairs] viewed as runs of c = 8 x 2^k
-// elements (the longest run of <= 8 pixel pairs that divides W/2): one box =
-// one whole input row; rows outside the image are zero-filled; no swizzle.
-bool encode_stem_raw(CUtensorMap* m, const void* x, const ConvPlan& cp) {
-  auto fn = encode_fn();
-  if (!fn) return false;
-  const uint64_t W2 = uint64_t(cp.W / 2);
-  uint64_t c = 8;
-  while (c < 64 && (W2 * 8) % (2 * c) == 0) c *= 2;
-  const uint64_t runs = W2 * 8 / c;
-  if (runs > 256) return false;
-  cuuint64_t dims[4] = {c, runs, cuuint64_t(cp.H), cuuint64_t(cp.N)};
-  cuuint64_t strides[3] = {c * 2, W2 * 16, uint64_t(cp.H) * W2 * 16};
-  cuuint32_t box[4] = {cuuint32_t(c), cuuint32_t(runs), 1, 1};
-  cuuint32_t estr[4] = {1, 1, 1, 1};
-  return fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(x), dims, strides, box,
-            estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
-}
-
 // Output of the row-tiled stem: [N*P rows][Q][K], 32x32 boxes clipped at Q.
 bool encode_out_rows(CUtensorMap* m, void* y, const ConvPlan& cp) {
   auto fn = encode_fn();
@@ -925,7 +914,7 @@ cudaError_t launch(const ConvPlan& cp, const void* x, void* y, float* stats,
   } else if (MODE == MODE_STEM) {
     if (!encode_stem_im2col(&amap, x, cp)) return cudaErrorInvalidValue;
   } else if (MODE == MODE_STEMRAW) {
-    if (!encode_stem_raw(&amap, x, cp)) return cudaErrorInvalidValue;
+    if (!stem_raw_rows_map(&amap, x, cp.N, cp.H, cp.W)) return cudaErrorInvalidValue;
   } else {
     amap = *reinterpret_cast<const CUtensorMap*>(cp.wmap);  // unused
   }

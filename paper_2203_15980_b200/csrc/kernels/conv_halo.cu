@@ -228,47 +228,51 @@ __global__ void __launch_bounds__(HT, 1)
     }
   } else {
     // ============================== MMA issuer ===============================
-    if (lane == 0) {
-      constexpr uint32_t idesc = umma_idesc_bf16(BM, BN);
-      uint32_t ia = 0, ib = 0, lt = 0;
-      if constexpr (RES) mbar_wait(bres, 0);
-      for (int tile = blockIdx.x; tile < a.tiles; tile += gridDim.x, ++lt) {
-        const uint32_t acc = lt & 1;
-        if (lt >= 2) mbar_wait(&tempty[acc], ((lt >> 1) - 1) & 1);
+    // whole warp walks the loop (uniform 64-bit descriptor adds), one elected
+    // lane issues: single-lane issue cost ~12 dependent instructions per MMA
+    constexpr uint32_t idesc = umma_idesc_bf16(BM, BN);
+    uint32_t ia = 0, ib = 0, lt = 0;
+    if constexpr (RES) mbar_wait(bres, 0);
+    for (int tile = blockIdx.x; tile < a.tiles; tile += gridDim.x, ++lt) {
+      const uint32_t acc = lt & 1;
+      if (lt >= 2) mbar_wait(&tempty[acc], ((lt >> 1) - 1) & 1);
+      tc_fence_after();
+      const uint32_t d = tmem + acc * BN;
+      for (int kc = 0; kc < a.kc; ++kc, ++ia) {
+        const uint32_t s = ia % A_STAGES;
+        mbar_wait(&afull[s], (ia / A_STAGES) & 1);
         tc_fence_after();
-        const uint32_t d = tmem + acc * BN;
-        for (int kc = 0; kc < a.kc; ++kc, ++ia) {
-          const uint32_t s = ia % A_STAGES;
-          mbar_wait(&afull[s], (ia / A_STAGES) & 1);
-          tc_fence_after();
-          const uint32_t abase = sA + s * A_MAX;
-          for (int tap = 0; tap < 9; ++tap) {
-            uint32_t bst;
-            if constexpr (RES) {
-              bst = sB + tap * B_STAGE;
-            } else {
-              const uint32_t sb = ib % B_STAGES;
-              mbar_wait(&bfull[sb], (ib / B_STAGES) & 1);
-              tc_fence_after();
-              bst = sB + sb * B_STAGE;
-            }
-            const int r = tap / 3, sx = tap - r * 3;
-            const uint32_t win = abase + uint32_t(r * a.slot + sx) * 128;
+        const uint64_t ad0 = desc_sw128_at(sA + s * A_MAX);
+        for (int tap = 0; tap < 9; ++tap) {
+          uint32_t bst;
+          if constexpr (RES) {
+            bst = sB + tap * B_STAGE;
+          } else {
+            const uint32_t sb = ib % B_STAGES;
+            mbar_wait(&bfull[sb], (ib / B_STAGES) & 1);
+            tc_fence_after();
+            bst = sB + sb * B_STAGE;
+          }
+          const int r = tap / 3, sx = tap - r * 3;
+          // window of this tap: (r * slot + sx) rows of 128 B into the halo
+          const uint64_t aw = ad0 + uint64_t((r * a.slot + sx) * 8);
+          const uint64_t bw = umma_desc_sw128(bst);
+          if (elect_one()) {
 #pragma unroll
             for (int k = 0; k < 4; ++k)
-              umma_bf16(d, desc_sw128_at(win + k * 32), umma_desc_sw128(bst + k * 32), idesc,
+              umma_bf16(d, aw + uint64_t(k * 2), bw + uint64_t(k * 2), idesc,
                         (kc | tap | k) != 0 ? 1u : 0u);
-            if constexpr (!RES) {
-              umma_commit(&bempty[ib % B_STAGES]);
-              ++ib;
-            }
+            if constexpr (!RES) umma_commit(&bempty[ib % B_STAGES]);
           }
-          umma_commit(&aempty[s]);
+          __syncwarp();
+          if constexpr (!RES) ++ib;
         }
-        umma_commit(&tfull[acc]);
+        if (elect_one()) umma_commit(&aempty[s]);
+        __syncwarp();
       }
+      if (elect_one()) umma_commit(&tfull[acc]);
+      __syncwarp();
     }
-    __syncwarp();
   }
   if (warp >= 4 && warp < 8 && lane == 0) bulk_wait<0>();
   tc_fence_before();

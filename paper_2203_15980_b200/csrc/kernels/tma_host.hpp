@@ -68,4 +68,25 @@ inline bool tma_im2col_bf16(CUtensorMap* m, const void* x, int C, int W, int H, 
             CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+// The C=4 stem input [N][H][W/2 pixel pairs][8] as whole input rows: runs of
+// c = 8 x 2^k elements (the longest run of <= 8 pairs dividing W/2), one box =
+// one row (W/2*8/c runs), rows outside the image zero-filled, no swizzle.
+// Used by the raw-row stem forward and weight-gradient kernels.
+inline bool stem_raw_rows_map(CUtensorMap* m, const void* x, int N, int H, int W) {
+  auto fn = tma_tiled_fn();
+  if (!fn) return false;
+  const uint64_t W2 = uint64_t(W / 2);
+  uint64_t c = 8;
+  while (c < 64 && (W2 * 8) % (2 * c) == 0) c *= 2;
+  const uint64_t runs = W2 * 8 / c;
+  if (runs > 256) return false;
+  cuuint64_t dims[4] = {c, runs, cuuint64_t(H), cuuint64_t(N)};
+  cuuint64_t strides[3] = {c * 2, W2 * 16, uint64_t(H) * W2 * 16};
+  cuuint32_t box[4] = {cuuint32_t(c), cuuint32_t(runs), 1, 1};
+  cuuint32_t estr[4] = {1, 1, 1, 1};
+  return fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(x), dims, strides, box,
+            estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 }  // namespace delta_k

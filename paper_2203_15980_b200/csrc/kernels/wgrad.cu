@@ -38,12 +38,17 @@ namespace {
 
 constexpr int WG_THREADS = 192;
 constexpr int KPIX = 64;  // pixels per k-block
-constexpr int WG_PLAIN = 0, WG_IM2COL = 1, WG_STEM = 2;
+constexpr int WG_PLAIN = 0, WG_IM2COL = 1, WG_STEM = 2, WG_STEMRAW = 3;
+// WG_STEMRAW: a k-block is one output row (n, p) of the stem; its 7 input
+// rows are staged raw (pixel pairs, zero pads around them, conv_fwd.cu
+// MODE_STEMRAW) and the B operand is addressed straight into them
+constexpr uint32_t RAW_ROW = 2304, RAW_DATA = 128;
 
 struct WgArgs {
   int K, C, taps, S, P, Q, stride, pad;
   int M;             // pixels N*P*Q
-  int kblocks;       // ceil(M / KPIX)
+  int kblocks;       // ceil(M / KPIX) (WG_STEMRAW: N*P output rows)
+  int W2;            // WG_STEMRAW: pixel pairs per input row
   int tiles_m;       // ceil(K / 128)
   int ntot;          // N' = taps * C (flattened (tap, channel) columns)
   int tiles;         // tiles_m * ceil(ntot / BN) (stem: tiles_m)
@@ -84,9 +89,11 @@ __global__ void __launch_bounds__(WG_THREADS, 1)
             const WgArgs a) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = align1024(smem_raw);
-  constexpr int STAGES = BN >= 256 ? 4 : 6;
+  constexpr int STAGES = MODE == WG_STEMRAW ? 6 : (BN >= 256 ? 4 : 6);
   constexpr uint32_t A_STAGE = 2 * KPIX * 128;                           // 2 boxes of 64 ch
-  constexpr uint32_t B_STAGE = MODE == WG_STEM ? 32 * KPIX * 16 : (BN / 64) * KPIX * 128;
+  constexpr uint32_t B_STAGE = MODE == WG_STEMRAW ? 7 * RAW_ROW
+                               : MODE == WG_STEM  ? 32 * KPIX * 16
+                                                  : (BN / 64) * KPIX * 128;
   const uint32_t sA = smem_u32(smem);
   const uint32_t sB = sA + STAGES * A_STAGE;
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * (A_STAGE + B_STAGE));
@@ -109,6 +116,16 @@ __global__ void __launch_bounds__(WG_THREADS, 1)
     fence_mbar_init();
     tma_prefetch_desc(&amap);
     tma_prefetch_desc(&bmap);
+  }
+  if constexpr (MODE == WG_STEMRAW) {
+    // zero pads (2 pairs) either side of every staged input row, once
+    const uint32_t data_end = RAW_DATA + uint32_t(a.W2) * 16;
+    for (int i = threadIdx.x; i < STAGES * 7 * 4; i += blockDim.x) {
+      const int row = i >> 2, part = i & 3;
+      const uint32_t off = (part < 2 ? RAW_DATA - 32 : data_end) + (part & 1) * 16;
+      st_shared_v4(sB + (row / 7) * B_STAGE + (row % 7) * RAW_ROW + off, make_uint4(0, 0, 0, 0));
+    }
+    fence_proxy_async_smem();
   }
   if (warp == 1) tmem_alloc(tslot, 2 * BN);
   tc_fence_before();
@@ -145,6 +162,26 @@ __global__ void __launch_bounds__(WG_THREADS, 1)
           bc[b] = col - tap * a.C;
           bs[b] = tap % a.S;
           br[b] = tap / a.S;
+        }
+        if constexpr (MODE == WG_STEMRAW) {
+          // k-block = output row kb: dY rows [kb*Q, kb*Q+Q) and input rows 2p-3+r
+          const uint32_t tx = uint32_t(a.Q) * 128u + 7u * uint32_t(a.W2) * 16u;
+          int n = kb0 / a.P, p = kb0 - (kb0 / a.P) * a.P;
+          for (int kb = kb0; kb < kb1; ++kb, ++it) {
+            const uint32_t s = it % STAGES;
+            if (it >= STAGES) mbar_wait(&empty[s], ((it / STAGES) - 1) & 1);
+            mbar_arrive_expect_tx(&full[s], tx);
+            tma_load_2d(sA + s * A_STAGE, &amap, &full[s], 0, kb * a.Q);
+#pragma unroll
+            for (int r = 0; r < 7; ++r)
+              tma_load_4d(sB + s * B_STAGE + r * RAW_ROW + RAW_DATA, &bmap, &full[s], 0, 0,
+                          2 * p - 3 + r, n);
+            if (++p == a.P) {
+              p = 0;
+              ++n;
+            }
+          }
+          continue;
         }
         // output pixel of the k-block -> (n, p, q), advanced incrementally
         int q = 0, p = 0, n = 0;
@@ -199,7 +236,45 @@ __global__ void __launch_bounds__(WG_THREADS, 1)
     }
   } else if (warp == 1) {
     // ============================== MMA issuer ===============================
-    if (lane == 0) {
+    if constexpr (MODE == WG_STEMRAW) {
+      // the whole warp walks the loop (uniform descriptors: one 64-bit add per
+      // MMA), one elected lane issues.  Per 16-pixel step, one M=64 (the 64
+      // output channels) x N=32 MMA per filter row r into columns [32r, 32r+32):
+      // B = the staged row, MN-major no-swizzle, pixel q's window at +16q (K
+      // groups of 8 pixels 128 B apart, the 4 pair columns of a window 16 B
+      // apart).  M=64 accumulator rows 16h..16h+15 sit in TMEM lanes 32h..+15.
+      constexpr uint32_t idesc32 = umma_idesc_bf16(64, 32) | (1u << 15) | (1u << 16);
+      uint32_t it = 0, lt = 0;
+      for (int item = blockIdx.x; item < a.items; item += gridDim.x, ++lt) {
+        int m0, n0, kb0, kb1;
+        decode(item, m0, n0, kb0, kb1);
+        const uint32_t acc = lt & 1;
+        if (lt >= 2) mbar_wait(&tempty[acc], ((lt >> 1) - 1) & 1);
+        tc_fence_after();
+        const uint32_t d = tmem + acc * BN;
+        for (int kb = kb0; kb < kb1; ++kb, ++it) {
+          const uint32_t s = it % STAGES;
+          mbar_wait(&full[s], (it / STAGES) & 1);
+          tc_fence_after();
+          const uint64_t ad0 = desc_mn_sw128(sA + s * A_STAGE, 0);
+          const uint64_t bd0 = desc_mn_interleave(sB + s * B_STAGE + RAW_DATA - 32, 128, 16);
+          for (int k = 0; k < a.Q / 16; ++k) {
+            if (elect_one()) {
+#pragma unroll
+              for (int r = 0; r < 7; ++r)
+                umma_bf16(d + r * 32, ad0 + uint64_t(k) * 128,
+                          bd0 + uint64_t(r * (RAW_ROW >> 4) + k * 16), idesc32,
+                          (kb != kb0 || k) ? 1u : 0u);
+            }
+            __syncwarp();
+          }
+          if (elect_one()) umma_commit(&empty[s]);
+          __syncwarp();
+        }
+        if (elect_one()) umma_commit(&tfull[acc]);
+        __syncwarp();
+      }
+    } else {
       constexpr uint32_t idesc = umma_idesc_bf16(128, BN) | (1u << 15) | (1u << 16);
       uint32_t it = 0, lt = 0;
       for (int item = blockIdx.x; item < a.items; item += gridDim.x, ++lt) {
@@ -213,21 +288,23 @@ __global__ void __launch_bounds__(WG_THREADS, 1)
           const uint32_t s = it % STAGES;
           mbar_wait(&full[s], (it / STAGES) & 1);
           tc_fence_after();
+          // 16-pixel K steps: 2 KB into the MN-major SW128 tiles (256 B of pairs for the stem)
+          const uint64_t ad0 = desc_mn_sw128(sA + s * A_STAGE, KPIX * 128);
+          const uint64_t bd0 = MODE == WG_STEM ? desc_mn_interleave(sB + s * B_STAGE, 128, KPIX * 16)
+                                               : desc_mn_sw128(sB + s * B_STAGE, KPIX * 128);
+          if (elect_one()) {
 #pragma unroll
-          for (int k = 0; k < KPIX / 16; ++k) {
-            const uint64_t ad = desc_mn_sw128(sA + s * A_STAGE + k * 2048, KPIX * 128);
-            const uint64_t bd =
-                MODE == WG_STEM
-                    ? desc_mn_interleave(sB + s * B_STAGE + k * 256, 128, KPIX * 16)
-                    : desc_mn_sw128(sB + s * B_STAGE + k * 2048, KPIX * 128);
-            umma_bf16(d, ad, bd, idesc, (kb != kb0 || k) ? 1u : 0u);
+            for (int k = 0; k < KPIX / 16; ++k)
+              umma_bf16(d, ad0 + uint64_t(k * 128), bd0 + uint64_t(MODE == WG_STEM ? k * 16 : k * 128),
+                        idesc, (kb != kb0 || k) ? 1u : 0u);
+            umma_commit(&empty[s]);
           }
-          umma_commit(&empty[s]);
+          __syncwarp();
         }
-        umma_commit(&tfull[acc]);
+        if (elect_one()) umma_commit(&tfull[acc]);
+        __syncwarp();
       }
     }
-    __syncwarp();
   } else {
     // =============================== epilogue ================================
     const int quarter = warp & 3;
@@ -236,14 +313,20 @@ __global__ void __launch_bounds__(WG_THREADS, 1)
       const uint32_t acc = lt & 1;
       mbar_wait(&tfull[acc], (lt >> 1) & 1);
       tc_fence_after();
-      float* out = a.ws + (size_t(item) * 128 + quarter * 32 + lane) * BN;
+      // WG_STEMRAW (M=64 MMAs): this quarter's lanes 0-15 hold rows 16q..16q+15
+      const int row = MODE == WG_STEMRAW ? quarter * 16 + lane : quarter * 32 + lane;
+      const bool live = MODE != WG_STEMRAW || lane < 16;
+      float* out = a.ws + (size_t(item) * 128 + row) * BN;
 #pragma unroll 1
       for (int j = 0; j < BN / 32; ++j) {
         float v[32];
         tmem_ld_32x32b_x32(tmem + (uint32_t(quarter * 32) << 16) + acc * BN + j * 32, v);
         float4* o = reinterpret_cast<float4*>(out + j * 32);
+        if (live) {
 #pragma unroll
-        for (int u = 0; u < 8; ++u) o[u] = make_float4(v[4 * u], v[4 * u + 1], v[4 * u + 2], v[4 * u + 3]);
+          for (int u = 0; u < 8; ++u)
+            o[u] = make_float4(v[4 * u], v[4 * u + 1], v[4 * u + 2], v[4 * u + 3]);
+        }
       }
       tc_fence_before();
       __syncwarp();
@@ -296,9 +379,11 @@ __global__ void __launch_bounds__(256)
 
 template <int BN, int MODE>
 constexpr size_t wg_smem_bytes() {
-  constexpr int STAGES = BN >= 256 ? 4 : 6;
+  constexpr int STAGES = MODE == WG_STEMRAW ? 6 : (BN >= 256 ? 4 : 6);
   constexpr size_t A = 2 * KPIX * 128;
-  constexpr size_t B = MODE == WG_STEM ? 32 * KPIX * 16 : (BN / 64) * KPIX * 128;
+  constexpr size_t B = MODE == WG_STEMRAW ? 7 * RAW_ROW
+                       : MODE == WG_STEM  ? 32 * KPIX * 16
+                                          : (BN / 64) * KPIX * 128;
   return STAGES * (A + B) + 1024 + 256;
 }
 
@@ -329,7 +414,8 @@ cudaError_t wg_launch(const WgradPlan& wp, const void* dy, const void* x, float*
   a.K = wp.K; a.C = wp.C; a.taps = wp.taps; a.S = wp.S; a.P = wp.P; a.Q = wp.Q;
   a.stride = wp.stride; a.pad = wp.pad;
   a.M = wp.N * wp.P * wp.Q;
-  a.kblocks = (a.M + KPIX - 1) / KPIX;
+  a.kblocks = MODE == WG_STEMRAW ? wp.N * wp.P : (a.M + KPIX - 1) / KPIX;
+  a.W2 = wp.W / 2;
   a.tiles_m = (wp.K + 127) / 128;
   a.ntot = wp.taps * wp.C;
   a.tiles = wp.tiles;
@@ -338,8 +424,8 @@ cudaError_t wg_launch(const WgradPlan& wp, const void* dy, const void* x, float*
   a.items = wp.splits * wp.tiles;
   a.ws = ws;
   alignas(64) CUtensorMap amap, bmap;
-  if (!tma_2d_bf16(&amap, dy, uint64_t(wp.K), uint64_t(a.M), uint64_t(wp.K), 64, KPIX,
-                   CU_TENSOR_MAP_SWIZZLE_128B))
+  if (!tma_2d_bf16(&amap, dy, uint64_t(wp.K), uint64_t(a.M), uint64_t(wp.K), 64,
+                   MODE == WG_STEMRAW ? uint32_t(wp.Q) : uint32_t(KPIX), CU_TENSOR_MAP_SWIZZLE_128B))
     return cudaErrorInvalidValue;
   bool ok;
   if (MODE == WG_PLAIN) {
@@ -349,6 +435,8 @@ cudaError_t wg_launch(const WgradPlan& wp, const void* dy, const void* x, float*
     ok = tma_im2col_bf16(&bmap, x, wp.C, wp.W, wp.H, wp.N, -wp.pad, -wp.pad,
                          wp.pad - (wp.S - 1), wp.pad - (wp.R - 1), wp.stride, wp.stride, 64, KPIX,
                          CU_TENSOR_MAP_SWIZZLE_128B);
+  } else if (MODE == WG_STEMRAW) {
+    ok = stem_raw_rows_map(&bmap, x, wp.N, wp.H, wp.W);
   } else {  // stem: [N][H][W/2][8] pixel pairs, stride (w 1, h 2)
     const int W2 = wp.W / 2;
     ok = tma_im2col_bf16(&bmap, x, 8, W2, wp.H, wp.N, -2, -3, wp.Q - W2 - 2, 2 * wp.P - wp.H - 3,
@@ -359,7 +447,7 @@ cudaError_t wg_launch(const WgradPlan& wp, const void* dy, const void* x, float*
   kern<<<grid, WG_THREADS, smem, st>>>(amap, bmap, a);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
-  if (MODE == WG_STEM) {
+  if (MODE == WG_STEM || MODE == WG_STEMRAW) {
     k_wgrad_reduce_stem<<<(wp.K * 196 + 255) / 256, 256, 0, st>>>(ws, dw, wp.K, wp.splits,
                                                                   wp.tiles);
   } else {
@@ -384,14 +472,16 @@ int wgrad_plan_init(WgradPlan* wp) {
   if (p.K % 64 != 0) return 1;
   p.P = (p.H + 2 * p.pad - p.R) / p.stride + 1;
   p.Q = (p.W + 2 * p.pad - p.S) / p.stride + 1;
-  p.mode = stem ? WG_STEM : (p.R == 1 && p.S == 1 && p.stride == 1 && p.pad == 0 ? WG_PLAIN : WG_IM2COL);
+  const char* sm = std::getenv("DELTA_STEM_MODE");
+  p.mode = stem ? (p.Q % 16 == 0 && p.Q <= 124 && p.K <= 64 && !(sm && sm[0]) ? WG_STEMRAW : WG_STEM)
+                : (p.R == 1 && p.S == 1 && p.stride == 1 && p.pad == 0 ? WG_PLAIN : WG_IM2COL);
   p.taps = stem ? 1 : p.R * p.S;
   const int ntot = p.taps * p.C;  // flattened (tap, channel) columns
   p.bn = stem ? 256 : (ntot >= 256 ? 256 : (ntot >= 128 ? 128 : 64));
   const int tiles_m = (p.K + 127) / 128;
   p.tiles = stem ? tiles_m : tiles_m * ((ntot + p.bn - 1) / p.bn);
   const int M = p.N * p.P * p.Q;
-  const int kblocks = (M + KPIX - 1) / KPIX;
+  const int kblocks = p.mode == WG_STEMRAW ? p.N * p.P : (M + KPIX - 1) / KPIX;
   // at least two waves of work items over the 148 SMs, each at least 8
   // k-blocks long (measured: more, shorter items beat fewer, longer ones)
   static const int waves = [] {
@@ -399,7 +489,7 @@ int wgrad_plan_init(WgradPlan* wp) {
     return e ? std::max(1, std::atoi(e)) : 2;
   }();
   int splits = std::max(1, (waves * 148 + p.tiles - 1) / p.tiles);
-  splits = std::min(splits, std::max(1, kblocks / 8));
+  splits = std::min(splits, std::max(1, kblocks / (p.mode == WG_STEMRAW ? 4 : 8)));
   // the fp32 partials (written, then read by the reduce) must stay well below
   // the main loop's own time, or many-tile shapes (K x taps*C large, few
   // pixels: layer 4 1x1) spend it on partials; never below one full wave
@@ -420,6 +510,7 @@ size_t wgrad_workspace_bytes(const WgradPlan& wp) {
 
 cudaError_t wgrad(const WgradPlan& wp, const void* dy, const void* x, float* dw, float* ws,
                   cudaStream_t st) {
+  if (wp.mode == WG_STEMRAW) return wg_launch<256, WG_STEMRAW>(wp, dy, x, dw, ws, st);
   if (wp.mode == WG_STEM) return wg_launch<256, WG_STEM>(wp, dy, x, dw, ws, st);
   switch (wp.bn) {
     case 64:
