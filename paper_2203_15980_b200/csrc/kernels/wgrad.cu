@@ -49,12 +49,12 @@ struct WgArgs {
   int M;             // pixels N*P*Q
   int kblocks;       // ceil(M / KPIX) (WG_STEMRAW: N*P output rows)
   int W2;            // WG_STEMRAW: pixel pairs per input row
-  int tiles_m;       // ceil(K / 128)
+  int tiles_m;       // ceil(K / (128 * MT))
   int ntot;          // N' = taps * C (flattened (tap, channel) columns)
   int tiles;         // tiles_m * ceil(ntot / BN) (stem: tiles_m)
   int splits, kb_per_split;
   int items;         // splits * tiles
-  float* ws;         // [items][128][BN] fp32 partials
+  float* ws;         // [items][128 * MT][BN] fp32 partials
 };
 
 __device__ __forceinline__ uint8_t* align1024(uint8_t* p) {
@@ -83,14 +83,22 @@ __device__ __forceinline__ uint64_t desc_mn_interleave(uint32_t addr, uint32_t l
   return d;
 }
 
-template <int BN, int MODE>
+// MT = 2: a tile is 256 output channels x BN columns — two accumulators (the
+// whole TMEM, so no double buffering) fed by the same B tile, halving the B
+// traffic per flop (the operand stream from L2 paces the large-K shapes)
+template <int MODE, int BN, int MT>
+constexpr int wg_stages() {
+  return MODE == WG_STEMRAW ? 6 : (MT == 2 ? 3 : (BN >= 256 ? 4 : 6));
+}
+
+template <int BN, int MODE, int MT>
 __global__ void __launch_bounds__(WG_THREADS, 1)
     k_wgrad(const __grid_constant__ CUtensorMap amap, const __grid_constant__ CUtensorMap bmap,
             const WgArgs a) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = align1024(smem_raw);
-  constexpr int STAGES = MODE == WG_STEMRAW ? 6 : (BN >= 256 ? 4 : 6);
-  constexpr uint32_t A_STAGE = 2 * KPIX * 128;                           // 2 boxes of 64 ch
+  constexpr int STAGES = wg_stages<MODE, BN, MT>();
+  constexpr uint32_t A_STAGE = MT * 2 * KPIX * 128;                      // 2 boxes of 64 ch per 128
   constexpr uint32_t B_STAGE = MODE == WG_STEMRAW ? 7 * RAW_ROW
                                : MODE == WG_STEM  ? 32 * KPIX * 16
                                                   : (BN / 64) * KPIX * 128;
@@ -127,7 +135,9 @@ __global__ void __launch_bounds__(WG_THREADS, 1)
     }
     fence_proxy_async_smem();
   }
-  if (warp == 1) tmem_alloc(tslot, 2 * BN);
+  constexpr uint32_t TMEM_COLS = 2 * BN;  // MT=1: two accumulators; MT=2: lo/hi halves
+  constexpr uint32_t NACC = MT == 2 ? 1 : 2;  // accumulator buffers
+  if (warp == 1) tmem_alloc(tslot, TMEM_COLS);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -137,7 +147,7 @@ __global__ void __launch_bounds__(WG_THREADS, 1)
   // a tile's BN columns may span several taps when C < BN
   auto decode = [&](int item, int& m0, int& n0, int& kb0, int& kb1) {
     const int split = item / a.tiles, tile = item % a.tiles;
-    m0 = (tile % a.tiles_m) * 128;
+    m0 = (tile % a.tiles_m) * 128 * MT;
     n0 = (tile / a.tiles_m) * BN;
     kb0 = split * a.kb_per_split;
     kb1 = min(a.kblocks, kb0 + a.kb_per_split);
@@ -196,12 +206,14 @@ __global__ void __launch_bounds__(WG_THREADS, 1)
           const uint32_t s = it % STAGES;
           if (it >= STAGES) mbar_wait(&empty[s], ((it / STAGES) - 1) & 1);
           const int pix = kb * KPIX;
-          // the second 64-channel half of the A tile only where K has it (rows
-          // of D past K are never read back)
+          // the 64-channel boxes of the A tile only where K has them (rows of D
+          // past K are never read back); MT=2 implies K % 256 == 0
           const bool a2 = m0 + 64 < a.K;
-          mbar_arrive_expect_tx(&full[s], (a2 ? A_STAGE : A_STAGE / 2) + b_bytes);
-          tma_load_2d(sA + s * A_STAGE, &amap, &full[s], m0, pix);
-          if (a2) tma_load_2d(sA + s * A_STAGE + KPIX * 128, &amap, &full[s], m0 + 64, pix);
+          mbar_arrive_expect_tx(&full[s], (MT == 2 || a2 ? A_STAGE : A_STAGE / 2) + b_bytes);
+#pragma unroll
+          for (int h = 0; h < 2 * MT; ++h)
+            if (MT == 2 || h == 0 || a2)
+              tma_load_2d(sA + s * A_STAGE + h * KPIX * 128, &amap, &full[s], m0 + 64 * h, pix);
           if constexpr (MODE == WG_PLAIN) {
 #pragma unroll
             for (int b = 0; b < BN / 64; ++b)
@@ -280,8 +292,8 @@ __global__ void __launch_bounds__(WG_THREADS, 1)
       for (int item = blockIdx.x; item < a.items; item += gridDim.x, ++lt) {
         int m0, n0, kb0, kb1;
         decode(item, m0, n0, kb0, kb1);
-        const uint32_t acc = lt & 1;
-        if (lt >= 2) mbar_wait(&tempty[acc], ((lt >> 1) - 1) & 1);
+        const uint32_t acc = lt % NACC;
+        if (lt >= NACC) mbar_wait(&tempty[acc], ((lt / NACC) - 1) & 1);
         tc_fence_after();
         const uint32_t d = tmem + acc * BN;
         for (int kb = kb0; kb < kb1; ++kb, ++it) {
@@ -295,8 +307,11 @@ __global__ void __launch_bounds__(WG_THREADS, 1)
           if (elect_one()) {
 #pragma unroll
             for (int k = 0; k < KPIX / 16; ++k)
-              umma_bf16(d, ad0 + uint64_t(k * 128), bd0 + uint64_t(MODE == WG_STEM ? k * 16 : k * 128),
-                        idesc, (kb != kb0 || k) ? 1u : 0u);
+#pragma unroll
+              for (int h = 0; h < MT; ++h)  // MT=2: the hi 128 channels at +16 KB, columns +BN
+                umma_bf16(d + h * BN, ad0 + uint64_t(k * 128 + h * 1024),
+                          bd0 + uint64_t(MODE == WG_STEM ? k * 16 : k * 128), idesc,
+                          (kb != kb0 || k) ? 1u : 0u);
             umma_commit(&empty[s]);
           }
           __syncwarp();
@@ -310,23 +325,25 @@ __global__ void __launch_bounds__(WG_THREADS, 1)
     const int quarter = warp & 3;
     uint32_t lt = 0;
     for (int item = blockIdx.x; item < a.items; item += gridDim.x, ++lt) {
-      const uint32_t acc = lt & 1;
-      mbar_wait(&tfull[acc], (lt >> 1) & 1);
+      const uint32_t acc = lt % NACC;
+      mbar_wait(&tfull[acc], (lt / NACC) & 1);
       tc_fence_after();
       // WG_STEMRAW (M=64 MMAs): this quarter's lanes 0-15 hold rows 16q..16q+15
       const int row = MODE == WG_STEMRAW ? quarter * 16 + lane : quarter * 32 + lane;
       const bool live = MODE != WG_STEMRAW || lane < 16;
-      float* out = a.ws + (size_t(item) * 128 + row) * BN;
+      for (int h = 0; h < MT; ++h) {
+      float* out = a.ws + (size_t(item) * 128 * MT + h * 128 + row) * BN;
 #pragma unroll 1
       for (int j = 0; j < BN / 32; ++j) {
         float v[32];
-        tmem_ld_32x32b_x32(tmem + (uint32_t(quarter * 32) << 16) + acc * BN + j * 32, v);
+        tmem_ld_32x32b_x32(tmem + (uint32_t(quarter * 32) << 16) + (acc + h) * BN + j * 32, v);
         float4* o = reinterpret_cast<float4*>(out + j * 32);
         if (live) {
 #pragma unroll
           for (int u = 0; u < 8; ++u)
             o[u] = make_float4(v[4 * u], v[4 * u + 1], v[4 * u + 2], v[4 * u + 3]);
         }
+      }
       }
       tc_fence_before();
       __syncwarp();
@@ -336,12 +353,12 @@ __global__ void __launch_bounds__(WG_THREADS, 1)
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  if (warp == 1) tmem_dealloc(tmem, 2 * BN);
+  if (warp == 1) tmem_dealloc(tmem, TMEM_COLS);
 }
 
 // dW[k][n] (KRSC, n = tap*C + c, fp32) = sum over splits of the partial tiles,
 // in split order.  Thread per output element; consecutive threads = consecutive n.
-template <int BN>
+template <int BN, int TM>
 __global__ void __launch_bounds__(256)
     k_wgrad_reduce(const float* __restrict__ ws, float* __restrict__ dw, int K, int ntot,
                    int tiles_m, int tiles, int splits) {
@@ -350,10 +367,10 @@ __global__ void __launch_bounds__(256)
        e += int64_t(gridDim.x) * blockDim.x) {
     const int n = int(e % ntot);
     const int k = int(e / ntot);
-    const int tile = (n / BN) * tiles_m + k / 128;
-    const size_t off = (size_t(tile) * 128 + (k % 128)) * BN + (n % BN);
+    const int tile = (n / BN) * tiles_m + k / TM;
+    const size_t off = (size_t(tile) * TM + (k % TM)) * BN + (n % BN);
     float s = 0.f;
-    for (int sp = 0; sp < splits; ++sp) s += ws[size_t(sp) * tiles * 128 * BN + off];
+    for (int sp = 0; sp < splits; ++sp) s += ws[size_t(sp) * tiles * TM * BN + off];
     dw[e] = s;
   }
 }
@@ -377,10 +394,10 @@ __global__ void __launch_bounds__(256)
   }
 }
 
-template <int BN, int MODE>
+template <int BN, int MODE, int MT>
 constexpr size_t wg_smem_bytes() {
-  constexpr int STAGES = MODE == WG_STEMRAW ? 6 : (BN >= 256 ? 4 : 6);
-  constexpr size_t A = 2 * KPIX * 128;
+  constexpr int STAGES = wg_stages<MODE, BN, MT>();
+  constexpr size_t A = MT * 2 * KPIX * 128;
   constexpr size_t B = MODE == WG_STEMRAW ? 7 * RAW_ROW
                        : MODE == WG_STEM  ? 32 * KPIX * 16
                                           : (BN / 64) * KPIX * 128;
@@ -398,11 +415,11 @@ int num_sms_wg() {
   return n;
 }
 
-template <int BN, int MODE>
+template <int BN, int MODE, int MT = 1>
 cudaError_t wg_launch(const WgradPlan& wp, const void* dy, const void* x, float* dw, float* ws,
                       cudaStream_t st) {
-  auto kern = k_wgrad<BN, MODE>;
-  constexpr size_t smem = wg_smem_bytes<BN, MODE>();
+  auto kern = k_wgrad<BN, MODE, MT>;
+  constexpr size_t smem = wg_smem_bytes<BN, MODE, MT>();
   static_assert(smem <= 227 * 1024, "shared memory");
   static bool attr = false;
   if (!attr) {
@@ -416,7 +433,7 @@ cudaError_t wg_launch(const WgradPlan& wp, const void* dy, const void* x, float*
   a.M = wp.N * wp.P * wp.Q;
   a.kblocks = MODE == WG_STEMRAW ? wp.N * wp.P : (a.M + KPIX - 1) / KPIX;
   a.W2 = wp.W / 2;
-  a.tiles_m = (wp.K + 127) / 128;
+  a.tiles_m = (wp.K + 128 * MT - 1) / (128 * MT);
   a.ntot = wp.taps * wp.C;
   a.tiles = wp.tiles;
   a.splits = wp.splits;
@@ -453,8 +470,8 @@ cudaError_t wg_launch(const WgradPlan& wp, const void* dy, const void* x, float*
   } else {
     const int64_t total = int64_t(wp.K) * a.ntot;
     const int64_t blocks = std::min<int64_t>((total + 255) / 256, 148 * 16);
-    k_wgrad_reduce<BN><<<int(blocks), 256, 0, st>>>(ws, dw, wp.K, a.ntot, a.tiles_m, wp.tiles,
-                                                   wp.splits);
+    k_wgrad_reduce<BN, 128 * MT><<<int(blocks), 256, 0, st>>>(ws, dw, wp.K, a.ntot, a.tiles_m,
+                                                             wp.tiles, wp.splits);
   }
   return cudaGetLastError();
 }
@@ -478,34 +495,49 @@ int wgrad_plan_init(WgradPlan* wp) {
   p.taps = stem ? 1 : p.R * p.S;
   const int ntot = p.taps * p.C;  // flattened (tap, channel) columns
   p.bn = stem ? 256 : (ntot >= 256 ? 256 : (ntot >= 128 ? 128 : 64));
-  const int tiles_m = (p.K + 127) / 128;
+  // 256-channel tiles (two accumulators on one B tile) for the 3x3 convs with
+  // K % 256 == 0 (measured: 62.5 -> 57.5 us at 14x14x256, 76 -> 60 us at
+  // 7x7x512); the 1x1 shapes' short items lose more to the undoubled
+  // accumulator drain than they gain (39 -> 48 us at 14x14 256->1024)
+  static const bool mt2_on = [] {
+    const char* e = std::getenv("DELTA_WGRAD_MT2");
+    return !(e && e[0] == '0');
+  }();
+  p.mt = (!stem && mt2_on && p.taps > 1 && p.bn == 256 && p.K % 256 == 0) ? 2 : 1;
+  const int tiles_m = (p.K + 128 * p.mt - 1) / (128 * p.mt);
   p.tiles = stem ? tiles_m : tiles_m * ((ntot + p.bn - 1) / p.bn);
   const int M = p.N * p.P * p.Q;
   const int kblocks = p.mode == WG_STEMRAW ? p.N * p.P : (M + KPIX - 1) / KPIX;
-  // at least two waves of work items over the 148 SMs, each at least 8
-  // k-blocks long (measured: more, shorter items beat fewer, longer ones)
-  static const int waves = [] {
-    const char* e = std::getenv("DELTA_WGRAD_WAVES");
-    return e ? std::max(1, std::atoi(e)) : 2;
-  }();
-  int splits = std::max(1, (waves * 148 + p.tiles - 1) / p.tiles);
-  splits = std::min(splits, std::max(1, kblocks / (p.mode == WG_STEMRAW ? 4 : 8)));
-  // the fp32 partials (written, then read by the reduce) must stay well below
-  // the main loop's own time, or many-tile shapes (K x taps*C large, few
-  // pixels: layer 4 1x1) spend it on partials; never below one full wave
-  const double t_mma = 2.0 * M * double(p.K) * ntot / 1.2e15;
-  const double t_op = 2.0 * M * (double(p.K) + double(p.C) * (stem ? 2 : 1)) / 6e12;
-  const double t_split = 8.0 * p.tiles * 128 * p.bn / 6e12;
-  const int cap = std::max((148 + p.tiles - 1) / p.tiles,
-                           int(0.4 * std::max(t_mma, t_op) / t_split));
-  splits = std::max(1, std::min(splits, cap));
+  // Split count: minimise the modelled makespan — whole waves of work items
+  // over the SMs (a partial last wave costs a full one) times the item
+  // length, plus the fp32 partials written and re-read by the reduce.
+  // (Rounding "two waves" up left 30% of the SMs idle in the last wave.)
+  const int sms = 148;
+  const double t_kb = p.mode == WG_STEMRAW ? 1.3e-6                       // one output row
+                                           : 2.0 * 128 * p.mt * p.bn * KPIX / (1.0e15 / sms);
+  const double t_ramp = 1.5 * t_kb;  // per item: pipeline fill + accumulator drain
+  const double part_bytes = 8.0 * p.tiles * 128 * p.mt * p.bn;  // per split: write + reduce read
+  const int smax = std::max(1, kblocks / (p.mode == WG_STEMRAW ? 4 : 8));
+  int splits = 1;
+  double best = 1e30;
+  for (int sp = 1; sp <= smax; ++sp) {
+    const int kbps = (kblocks + sp - 1) / sp;
+    const int s_eff = (kblocks + kbps - 1) / kbps;
+    if (s_eff != sp) continue;  // same partition as a smaller count
+    const int waves = (s_eff * p.tiles + sms - 1) / sms;
+    const double t = waves * (kbps * t_kb + t_ramp) + s_eff * part_bytes / 6e12;
+    if (t < best * 0.999) {
+      best = t;
+      splits = s_eff;
+    }
+  }
   p.kb_per_split = (kblocks + splits - 1) / splits;
   p.splits = (kblocks + p.kb_per_split - 1) / p.kb_per_split;
   return 0;
 }
 
 size_t wgrad_workspace_bytes(const WgradPlan& wp) {
-  return size_t(wp.splits) * wp.tiles * 128 * wp.bn * sizeof(float);
+  return size_t(wp.splits) * wp.tiles * 128 * wp.mt * wp.bn * sizeof(float);
 }
 
 cudaError_t wgrad(const WgradPlan& wp, const void* dy, const void* x, float* dw, float* ws,
@@ -520,6 +552,9 @@ cudaError_t wgrad(const WgradPlan& wp, const void* dy, const void* x, float* dw,
       return wp.mode == WG_PLAIN ? wg_launch<128, WG_PLAIN>(wp, dy, x, dw, ws, st)
                                  : wg_launch<128, WG_IM2COL>(wp, dy, x, dw, ws, st);
     default:
+      if (wp.mt == 2)
+        return wp.mode == WG_PLAIN ? wg_launch<256, WG_PLAIN, 2>(wp, dy, x, dw, ws, st)
+                                   : wg_launch<256, WG_IM2COL, 2>(wp, dy, x, dw, ws, st);
       return wp.mode == WG_PLAIN ? wg_launch<256, WG_PLAIN>(wp, dy, x, dw, ws, st)
                                  : wg_launch<256, WG_IM2COL>(wp, dy, x, dw, ws, st);
   }

@@ -142,7 +142,7 @@ def conv_stats_rows(N, H, W, Cin, K, R, S, stride, pad) -> int:
     import os
     env = os.environ.get("DELTA_CONV_HALO")
     P = (H + 2 * pad - R) // stride + 1
-    if Cin == 4:  # the row-tiled stem (conv_fwd.cu MODE_STEMROW): one partial per output row
+    if Cin == 4:  # the row-tiled stem (conv_fwd.cu MODE_STEMRAW): one partial per output row
         Q = (W + 2 * pad - S) // stride + 1
         if K <= 64 and 4 <= Q <= 124 and not os.environ.get("DELTA_STEM_MODE"):
             return Q

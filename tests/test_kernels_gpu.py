@@ -361,6 +361,9 @@ WGRAD_CASES = [
     (2, 56, 56, 256, 512, 1, 2, 0),
     (3, 14, 14, 1024, 256, 1, 1, 0),
     (5, 7, 7, 512, 512, 3, 1, 1),
+    # 256-channel tiles (two accumulators per B tile) with several N tiles
+    (2, 14, 14, 256, 1024, 1, 1, 0),
+    (3, 14, 14, 256, 256, 3, 1, 1),
 ]
 
 
