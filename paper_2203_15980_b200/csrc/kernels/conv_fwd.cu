@@ -165,10 +165,16 @@ __device__ __forceinline__ uint8_t* align1024(uint8_t* p) {
 // t1) per 32x32 chunk, cp.async-loaded (slots - 1) chunks ahead into a
 // per-warp ring (a chunk's math is far shorter than an HBM round trip; 64 B-row
 // TMA boxes were issue-bound).
-template <int BN, int STAGES, int MODE, int EV>
+// OPT: the fused epilogue's operands ([M][K] tensors: add, out_mask, xc) are
+// TMA-loaded per tile by producer warp 1 into a double-buffered tile slot
+// (32-column x 128-row boxes, the same 64B-swizzled layout the cp.async ring
+// uses), instead of per-chunk cp.async gathers by the epilogue warps.
+constexpr int OPT_NB = 2;
+template <int BN, int STAGES, int MODE, int EV, bool OPT = false>
 __global__ void __launch_bounds__(kThreads, 1)
     k_conv_fwd(const __grid_constant__ CUtensorMap wmap, const __grid_constant__ CUtensorMap amap,
-               const __grid_constant__ CUtensorMap ymap, const ConvArgs a) {
+               const __grid_constant__ CUtensorMap ymap, const __grid_constant__ CUtensorMap emap0,
+               const __grid_constant__ CUtensorMap emap1, const ConvArgs a) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = align1024(smem_raw);
   // producer signalling lag: a thread keeps LAG+1 stages of gathers in flight
@@ -184,7 +190,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   // fused-epilogue operand ring: EPI_W warps x EPI_RING_WARP
   constexpr bool FUSED = EV != EV_STORE;
   constexpr uint32_t EPI_RING_WARP = epi_ring_bytes<BN, STAGES>() / EPI_W;
-  constexpr uint32_t IN_BYTES = FUSED ? EPI_W * EPI_RING_WARP : 0;
+  constexpr int NOPS_ = ev_operands(EV);
+  constexpr uint32_t OPT_TILE = uint32_t(NOPS_) * BN * 256;  // per tile: NOPS x [128][BN] bf16
+  constexpr uint32_t IN_BYTES = !FUSED ? 0 : (OPT ? OPT_NB * OPT_TILE : EPI_W * EPI_RING_WARP);
   const uint32_t sIn = sOut + 16384;
   // BN-statistics scratch: per quarter-warp column (sum, sumsq), [4][BN] float2
   float2* red = reinterpret_cast<float2*>(smem + STAGES * (A_STAGE + B_STAGE) + 16384 + IN_BYTES);
@@ -194,7 +202,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* tfull = empty + STAGES;  // [2]
   uint64_t* tempty = tfull + 2;      // [2]
   uint64_t* bfull = tempty + 2;      // MODE_STEMRAW: resident weights landed
-  uint32_t* tslot = reinterpret_cast<uint32_t*>(bfull + 1);
+  uint64_t* ofull = bfull + 1;       // OPT: epilogue operand tile landed [OPT_NB]
+  uint64_t* oempty = ofull + OPT_NB; // OPT: ... and consumed [OPT_NB]
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(oempty + OPT_NB);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -209,7 +219,15 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&tempty[i], EPI_W);
     }
     mbar_init(bfull, 1);
+    for (int i = 0; i < OPT_NB; ++i) {
+      mbar_init(&ofull[i], 1);
+      mbar_init(&oempty[i], EPI_W);
+    }
     fence_mbar_init();
+    if (OPT) {
+      tma_prefetch_desc(&emap0);
+      if (NOPS_ == 2) tma_prefetch_desc(&emap1);
+    }
     tma_prefetch_desc(&wmap);
     if (!gathers(MODE)) tma_prefetch_desc(&amap);
     tma_prefetch_desc(&ymap);
@@ -234,6 +252,30 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp < 4) {
     // ============================ producers ============================
     const int tid = threadIdx.x;
+    if constexpr (OPT) {
+      if (warp == 1) {
+        // epilogue operands of every tile of this CTA, two tiles ahead
+        if (lane == 0) {
+          uint32_t lt = 0;
+          for (int tile = blockIdx.x; tile < a.tiles; tile += gridDim.x, ++lt) {
+            const int m0 = (tile / a.n_tiles) * BM;
+            const int n0 = (tile % a.n_tiles) * BN;
+            const uint32_t b = lt % OPT_NB;
+            if (lt >= OPT_NB) mbar_wait(&oempty[b], ((lt / OPT_NB) - 1) & 1);
+            mbar_arrive_expect_tx(&ofull[b], OPT_TILE);
+            const uint32_t base = sIn + b * OPT_TILE;
+#pragma unroll
+            for (int j = 0; j < BN / 32; ++j) {
+              tma_load_2d(base + j * 8192, &emap0, &ofull[b], n0 + j * 32, m0);
+              if (NOPS_ == 2)
+                tma_load_2d(base + BN * 256 + j * 8192, &emap1, &ofull[b], n0 + j * 32, m0);
+            }
+          }
+        }
+        goto producers_done;
+      }
+    }
+    {
     uint32_t it = 0;  // global k-iteration counter (stage ring position)
     for (int tile = blockIdx.x; tile < a.tiles; tile += gridDim.x) {
       const int m0 = (tile / a.n_tiles) * BM;
@@ -437,6 +479,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (uint32_t j = first; j < it; ++j) mbar_arrive(&full[j % STAGES]);
       }
     }
+    }
+  producers_done:;
   } else if (warp < MMA_WARP) {
     // ============================ epilogue =============================
     const int quarter = warp & 3;  // TMEM lanes [32*quarter, 32*quarter+32)
@@ -448,7 +492,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     constexpr int NOPS = ev_operands(EV);
     constexpr uint32_t SLOT = NOPS * 2048u;
     constexpr uint32_t NSLOTS = NOPS ? EPI_RING_WARP / SLOT : 1;
-    static_assert(!NOPS || NSLOTS >= 2, "operand ring");
+    static_assert(OPT || !NOPS || NSLOTS >= 2, "operand ring");
+    constexpr uint32_t OP1 = OPT ? BN * 256 : 2048;  // second operand, from the first's slot
     const uint32_t ring = sIn + (warp - 4) * EPI_RING_WARP;
     constexpr int CH = BN / 32;         // chunks per tile
     constexpr int CHW = CH / HALVES;    // chunks per tile of this warp
@@ -498,12 +543,12 @@ __global__ void __launch_bounds__(kThreads, 1)
           } else {
             cp_async_16(sb + so, src0 + go, ok);
           }
-          if (NOPS == 2) cp_async_16(sb + 2048 + so, src1 + go, ok);
+          if (NOPS == 2) cp_async_16(sb + OP1 + so, src1 + go, ok);
         }
       }
       cp_async_commit();
     };
-    if constexpr (FUSED)
+    if constexpr (FUSED && !OPT)
       for (uint32_t e = 0; e + 1 < NSLOTS; ++e) prefetch(e);
     uint32_t ec = 0;  // chunks consumed by this warp
     uint32_t lt = 0;
@@ -514,18 +559,20 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint32_t acc = lt & 1;
       mbar_wait(&tfull[acc], (lt >> 1) & 1);
       tc_fence_after();
+      const uint32_t obuf = sIn + (lt % OPT_NB) * OPT_TILE;
+      if constexpr (FUSED && OPT) mbar_wait(&ofull[lt % OPT_NB], (lt / OPT_NB) & 1);
       // TMA-store staging: 16 KB over the epilogue warps, NBUF 2 KB buffers each
       constexpr int NBUF = 16384 / EPI_W / 2048;
       const uint32_t stage_base = sOut + (warp - 4) * (NBUF * 2048);
 #pragma unroll 1
       for (int j = half; j < CH; j += HALVES, ++ec) {
         // the slot refilled here was consumed (and __syncwarp'ed) last chunk
-        if constexpr (FUSED) prefetch(ec + NSLOTS - 1);
+        if constexpr (FUSED && !OPT) prefetch(ec + NSLOTS - 1);
         float v[32];
         tmem_ld_32x32b_x32(tmem + (uint32_t(quarter * 32) << 16) + acc * ACC_COLS + j * 32, v);
         const int col = n0 + j * 32;
-        const uint32_t sb = ring + (ec % NSLOTS) * SLOT;
-        if constexpr (FUSED) {
+        const uint32_t sb = OPT ? obuf + j * 8192 + quarter * 2048 : ring + (ec % NSLOTS) * SLOT;
+        if constexpr (FUSED && !OPT) {
           cp_async_wait<NSLOTS - 1>();  // this chunk's group is the oldest committed
           __syncwarp();
         }
@@ -573,7 +620,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         if constexpr (EV == EV_ADD_OM || EV == EV_POOL) {
 #pragma unroll
           for (int u = 0; u < 4; ++u) {
-            const uint4 om = ld_row16(sb + 2048, lane, u);
+            const uint4 om = ld_row16(sb + OP1, lane, u);
             pk[u].x &= pos_mask2(om.x);
             pk[u].y &= pos_mask2(om.y);
             pk[u].z &= pos_mask2(om.z);
@@ -674,7 +721,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&tempty[acc]);
+      if (lane == 0) {
+        mbar_arrive(&tempty[acc]);
+        if (FUSED && OPT) mbar_arrive(&oempty[lt % OPT_NB]);  // operand tile read
+      }
     }
   } else {
     // ============================ MMA issuer ===========================
@@ -738,10 +788,13 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == MMA_WARP) tmem_dealloc(tmem, TMEM_COLS);
 }
 
-template <int BN, int STAGES, bool FUSED>
+template <int BN, int STAGES, int EV, bool OPT>
 constexpr size_t conv_smem_bytes() {
+  constexpr bool FUSED = EV != EV_STORE;
   return size_t(STAGES) * (BM * 128 + BN * 128) + 16384 /*epilogue staging*/ +
-         (FUSED ? epi_ring_bytes<BN, STAGES>() : 0) /*epilogue operand ring*/ + 4 * BN * 8 /*stats scratch*/ +
+         (!FUSED ? 0
+          : OPT  ? size_t(OPT_NB) * ev_operands(EV) * BN * 256
+                 : epi_ring_bytes<BN, STAGES>()) /*epilogue operands*/ + 4 * BN * 8 /*stats scratch*/ +
          1024 /*align*/ + 256 /*barriers*/;
 }
 
@@ -847,6 +900,16 @@ bool encode_out_rows(CUtensorMap* m, void* y, const ConvPlan& cp) {
             CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+// DELTA_EPI_TMA=0 keeps the fused epilogue operands on the cp.async ring
+bool operands_tma() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = std::getenv("DELTA_EPI_TMA");
+    v = (e && e[0] == '0') ? 0 : 1;
+  }
+  return v == 1;
+}
+
 // DELTA_CONV_GATHER=1 selects the cp.async im2col gather instead of the TMA
 // im2col unit (kept as the reference path for the A operand).
 bool gather_forced() {
@@ -881,11 +944,11 @@ int num_sms() {
   return n;
 }
 
-template <int BN, int STAGES, int MODE, int EV>
+template <int BN, int STAGES, int MODE, int EV, bool OPT = false>
 cudaError_t launch(const ConvPlan& cp, const void* x, void* y, float* stats,
                    const ConvEpilogue& epi, cudaStream_t st) {
-  auto kern = k_conv_fwd<BN, STAGES, MODE, EV>;
-  constexpr size_t smem = conv_smem_bytes<BN, STAGES, EV != EV_STORE>();
+  auto kern = k_conv_fwd<BN, STAGES, MODE, EV, OPT>;
+  constexpr size_t smem = conv_smem_bytes<BN, STAGES, EV, OPT>();
   static_assert(smem <= 227 * 1024, "shared memory");
   static bool attr = false;
   if (!attr) {
@@ -921,9 +984,21 @@ cudaError_t launch(const ConvPlan& cp, const void* x, void* y, float* stats,
   if (row_tiled(MODE) ? !encode_out_rows(&ymap, y, cp)
                            : !encode_out(&ymap, y, uint64_t(cp.K), uint64_t(a.M)))
     return cudaErrorInvalidValue;
+  // OPT: the fused epilogue's [M][K] operands as 32-column x 128-row boxes
+  alignas(64) CUtensorMap emap0 = ymap, emap1 = ymap;
+  if (OPT) {
+    const void* op0 = EV == EV_BN_BWD ? epi.xc : (EV == EV_POOL ? epi.add_mask : epi.add);
+    if (!tma_2d_bf16(&emap0, op0, uint64_t(cp.K), uint64_t(a.M), uint64_t(cp.K), 32, BM,
+                     CU_TENSOR_MAP_SWIZZLE_64B))
+      return cudaErrorInvalidValue;
+    if (ev_operands(EV) == 2 &&
+        !tma_2d_bf16(&emap1, epi.out_mask, uint64_t(cp.K), uint64_t(a.M), uint64_t(cp.K), 32, BM,
+                     CU_TENSOR_MAP_SWIZZLE_64B))
+      return cudaErrorInvalidValue;
+  }
   const int grid = a.tiles < num_sms() ? a.tiles : num_sms();
   kern<<<grid, kThreads, smem, st>>>(*reinterpret_cast<const CUtensorMap*>(cp.wmap), amap, ymap,
-                                     a);
+                                     emap0, emap1, a);
   return cudaGetLastError();
 }
 
@@ -1000,8 +1075,16 @@ cudaError_t conv_forward(const ConvPlan& cp, const void* x, void* y, float* stat
     if (cp.bn != 64 && cp.bn != 128) return cudaErrorInvalidValue;
     if (e.add_stride2 && (ev == EV_POOL || ev == EV_BN_BWD || (cp.P & 1) || (cp.Q & 1)))
       return cudaErrorInvalidValue;
+    // operands by TMA (per-tile boxes) for the 1x1 input gradients with a
+    // short reduction: two operand stages leave room for two tile buffers
+    // (measured: 281 -> 218 us at 56x56 64->256, floor 205; a 512-deep
+    // reduction loses more to the 2 stages than it gains); the stride-2
+    // shortcut add stays on the cp.async gather
+    const bool opt = tma_a && !e.add_stride2 && cp.kdim <= 256 && operands_tma();
 #define DELTA_FUSED(EVV)                                                                    \
   case EVV:                                                                                 \
+    if (opt && cp.bn == 64) return launch<64, 4, MODE_TMA, EVV, true>(cp, x, y, stats, e, st); \
+    if (opt) return launch<128, 2, MODE_TMA, EVV, true>(cp, x, y, stats, e, st);            \
     if (cp.bn == 64)                                                                        \
       return tma_a ? launch<64, 4, MODE_TMA, EVV>(cp, x, y, stats, e, st)                    \
                    : launch<64, 4, MODE_IM2COL, EVV>(cp, x, y, stats, e, st);                \
