@@ -96,6 +96,21 @@ def test_conv_stem_packed_c4(N, H, W):
     conv(x.data_ptr(), y2.data_ptr(), _stream())
     torch.cuda.synchronize()
     assert torch.equal(y, y2)
+    # BN statistics from the epilogue partials (one partial per output row on
+    # the row-tiled path) match the statistics of the stored bf16 output
+    M = N * conv.P * conv.Q
+    assert conv.stats_rows == K.conv_stats_rows(N, H, W, 4, Kout, 7, 7, 2, 3)
+    parts = torch.empty(K.stats_partials_floats(M, Kout, conv.stats_rows), device="cuda")
+    y3 = torch.empty_like(y)
+    conv(x.data_ptr(), y3.data_ptr(), _stream(), parts.data_ptr())
+    mean = torch.empty(Kout, device="cuda"); inv = torch.empty(Kout, device="cuda")
+    K.bn_stats_from_partials(parts.data_ptr(), M, Kout, mean.data_ptr(), inv.data_ptr(), 1e-5,
+                             None, None, 0.1, _stream(), rows_per_part=conv.stats_rows)
+    torch.cuda.synchronize()
+    assert torch.equal(y, y3)
+    yf = y.float().reshape(M, Kout)
+    assert torch.allclose(mean, yf.mean(0), rtol=1e-4, atol=1e-4)
+    assert torch.allclose(inv, torch.rsqrt(yf.var(0, unbiased=False) + 1e-5), rtol=2e-4, atol=1e-4)
 
 
 def _bn_params(C, g):
