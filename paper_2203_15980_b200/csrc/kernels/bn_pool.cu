@@ -14,6 +14,7 @@
 #include <cstdint>
 
 #include "kernels/kernels.hpp"
+#include "kernels/launch.hpp"
 
 namespace delta_k {
 
@@ -86,6 +87,8 @@ __device__ __forceinline__ void merge(float& n, float& mu, float& m2, float nb, 
 __global__ void __launch_bounds__(256, 4) k_bn_stats_partial(const bf16* __restrict__ x, int64_t M,
                                                           int C, int64_t chunk,
                                                           float2* __restrict__ ws) {
+  pdl_wait();
+  pdl_trigger();
   const int tpr = C >> 3, rpi = 256 / tpr;
   const int tx = threadIdx.x % tpr, ty = threadIdx.x / tpr;
   const int c0 = tx * 8;
@@ -142,6 +145,8 @@ __device__ __forceinline__ float warp_sum(float v) {
 __global__ void __launch_bounds__(256)
     k_bn_stats_merge(const float2* __restrict__ ws, int parts, int64_t rows_per, int64_t M, int C,
                      float* mean, float* invstd, float eps, float* rm, float* rv, float mom) {
+  pdl_wait();
+  pdl_trigger();
   const int c = blockIdx.x * 8 + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   if (c >= C) return;
@@ -178,6 +183,8 @@ constexpr int GROUP = 16;
 __global__ void __launch_bounds__(256)
     k_bn_stats_group(const float2* __restrict__ ws, int parts, int64_t rows_per, int64_t M, int C,
                      float2* __restrict__ out) {
+  pdl_wait();
+  pdl_trigger();
   const int c = blockIdx.x * blockDim.x + threadIdx.x;
   if (c >= C) return;
   const int k0 = blockIdx.y * GROUP;
@@ -220,6 +227,8 @@ __global__ void __launch_bounds__(256)
                const float* __restrict__ beta, const float* __restrict__ mean2,
                const float* __restrict__ invstd2, const float* __restrict__ gamma2,
                const float* __restrict__ beta2) {
+  pdl_wait();
+  pdl_trigger();
   const int64_t first = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   const int c0 = int(first * 8) & cmask;
   float sc[8], sh[8], sc2[8], sh2[8];
@@ -289,6 +298,8 @@ __global__ void __launch_bounds__(256)
     k_bn_bwd_partial(const bf16* __restrict__ up, int pool_hw, const bf16* __restrict__ mask,
                      const bf16* __restrict__ x, int64_t M, int C, int64_t chunk,
                      const float* mean, const float* invstd, float2* __restrict__ ws) {
+  pdl_wait();
+  pdl_trigger();
   const int tpr = C >> 3, rpi = 256 / tpr;
   const int tx = threadIdx.x % tpr, ty = threadIdx.x / tpr;
   const int c0 = tx * 8;
@@ -347,6 +358,8 @@ __global__ void __launch_bounds__(256)
 // warp per channel, lane-strided sums then a fixed xor butterfly
 __global__ void __launch_bounds__(256) k_bn_bwd_final(const float2* __restrict__ ws, int chunks,
                                                       int C, float* dgamma, float* dbeta) {
+  pdl_wait();
+  pdl_trigger();
   const int c = blockIdx.x * 8 + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   if (c >= C) return;
@@ -370,6 +383,8 @@ __global__ void __launch_bounds__(256) k_bn_bwd_final(const float2* __restrict__
 // dbeta = sum g, dgamma = invstd * (sum g*x - mean * sum g).
 __global__ void __launch_bounds__(256)
     k_bn_bwd_group(const float2* __restrict__ ws, int parts, int C, float2* __restrict__ out) {
+  pdl_wait();
+  pdl_trigger();
   const int c = blockIdx.x * blockDim.x + threadIdx.x;
   if (c >= C) return;
   const int k0 = blockIdx.y * GROUP;
@@ -389,6 +404,8 @@ __global__ void __launch_bounds__(256)
 __global__ void __launch_bounds__(256)
     k_bn_bwd_final_raw(const float2* __restrict__ ws, int parts, int C, const float* mean,
                        const float* invstd, float* dgamma, float* dbeta) {
+  pdl_wait();
+  pdl_trigger();
   const int c = blockIdx.x * 8 + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   if (c >= C) return;
@@ -415,6 +432,8 @@ __global__ void __launch_bounds__(256)
                    int logC, int64_t M, const float* __restrict__ mean,
                    const float* __restrict__ invstd, const float* __restrict__ gamma,
                    const float* __restrict__ dgamma, const float* __restrict__ dbeta) {
+  pdl_wait();
+  pdl_trigger();
   const int64_t first = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   const int c0 = int(first * 8) & cmask;
   const int C = cmask + 1;
@@ -469,6 +488,8 @@ __global__ void __launch_bounds__(256)
     k_add_grad(const bf16* __restrict__ a, const bf16* __restrict__ up, int pool_hw,
                const bf16* __restrict__ up_mask, const bf16* __restrict__ out_mask,
                bf16* __restrict__ out, int64_t vecs, int cmask, int logC, int C) {
+  pdl_wait();
+  pdl_trigger();
   const float inv_hw = POOLED ? 1.f / float(pool_hw) : 1.f;
   const int64_t stride = int64_t(gridDim.x) * blockDim.x;
   for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < vecs; i += stride) {
@@ -502,6 +523,8 @@ __global__ void __launch_bounds__(256)
 __global__ void __launch_bounds__(256) k_maxpool_fwd(const bf16* __restrict__ x,
                                                      bf16* __restrict__ y, int N, int H, int W,
                                                      int C, int P, int Q, int lcg) {
+  pdl_wait();
+  pdl_trigger();
   const int cg = 1 << lcg;
   const int item = blockIdx.y * 256 + threadIdx.x;
   if (item >= Q * cg) return;
@@ -534,6 +557,8 @@ __global__ void __launch_bounds__(256) k_maxpool_fwd(const bf16* __restrict__ x,
 __global__ void __launch_bounds__(256)
     k_maxpool_argmax(const bf16* __restrict__ x, uint8_t* __restrict__ idx, int N, int H, int W,
                      int C, int P, int Q, int lcg) {
+  pdl_wait();
+  pdl_trigger();
   const int cg = 1 << lcg;
   const int item = blockIdx.y * 256 + threadIdx.x;
   if (item >= Q * cg) return;
@@ -573,6 +598,8 @@ __global__ void __launch_bounds__(256)
     k_maxpool_bwd_gather(const bf16* __restrict__ dy, const uint8_t* __restrict__ idx,
                          bf16* __restrict__ dx, int N, int H, int W, int C, int P, int Q,
                          int lcg) {
+  pdl_wait();
+  pdl_trigger();
   const int cg = 1 << lcg;
   const int item = blockIdx.y * 256 + threadIdx.x;
   if (item >= Q * cg) return;
@@ -618,6 +645,8 @@ __global__ void __launch_bounds__(256)
 
 __global__ void __launch_bounds__(256) k_avgpool_fwd(const bf16* __restrict__ x,
                                                      bf16* __restrict__ y, int N, int HW, int C) {
+  pdl_wait();
+  pdl_trigger();
   const int cg = C / 8;
   const int64_t total = int64_t(N) * cg;
   for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < total;
@@ -643,6 +672,8 @@ __global__ void __launch_bounds__(256) k_softmax_xent(const float* __restrict__ 
                                                       const int64_t* __restrict__ labels,
                                                       float* __restrict__ dlogits,
                                                       float* __restrict__ row_loss, int N, int K) {
+  pdl_wait();
+  pdl_trigger();
   const int n = blockIdx.x;
   const float* l = logits + int64_t(n) * K;
   __shared__ float red[256];
@@ -675,6 +706,8 @@ __global__ void __launch_bounds__(256) k_softmax_xent(const float* __restrict__ 
 }
 
 __global__ void k_mean_rows(const float* row_loss, int N, float* loss) {
+  pdl_wait();
+  pdl_trigger();
   if (threadIdx.x == 0 && blockIdx.x == 0) {
     float s = 0.f;
     for (int i = 0; i < N; ++i) s += row_loss[i];
@@ -695,20 +728,20 @@ namespace {
 // ws[0 .. parts*C) into the channel statistics.  Above 2*GROUP partials a
 // grouping pass first writes ceil(parts/GROUP) partials after them (the
 // caller's buffer holds both), so each merge warp walks at most a few dozen.
-void merge_partials(const float2* ws, int parts, int64_t rows_per, int64_t M, int C, float* mean,
-                    float* invstd, float eps, float* rm, float* rv, float mom, cudaStream_t st) {
+cudaError_t merge_partials(const float2* ws, int parts, int64_t rows_per, int64_t M, int C,
+                           float* mean, float* invstd, float eps, float* rm, float* rv, float mom,
+                           cudaStream_t st) {
   if (parts > 2 * GROUP) {
     const int groups = (parts + GROUP - 1) / GROUP;
     float2* out = const_cast<float2*>(ws) + int64_t(parts) * C;
     const int bx = C < 256 ? C : 256;
-    k_bn_stats_group<<<dim3((C + bx - 1) / bx, groups), bx, 0, st>>>(ws, parts, rows_per, M, C,
-                                                                     out);
+    if (cudaError_t e_ = launch_k(k_bn_stats_group, dim3(dim3((C + bx - 1) / bx, groups)), dim3(bx), 0, st, ws, parts, rows_per, M, C, out)) return e_;
     ws = out;
     parts = groups;
     rows_per *= GROUP;
   }
-  k_bn_stats_merge<<<(C + 7) / 8, 256, 0, st>>>(ws, parts, rows_per, M, C, mean, invstd, eps, rm,
-                                                rv, mom);
+  return launch_k(k_bn_stats_merge, dim3((C + 7) / 8), dim3(256), 0, st, ws, parts, rows_per, M, C,
+                  mean, invstd, eps, rm, rv, mom);
 }
 }  // namespace
 
@@ -717,11 +750,9 @@ cudaError_t bn_stats(const void* x, int64_t M, int C, float* ws, float* mean, fl
   if (C % SLICE || (C & (C - 1)) || C > 2048) return cudaErrorInvalidValue;
   const int64_t chunk = chunk_rows(M, C);
   const int chunks = int((M + chunk - 1) / chunk);
-  k_bn_stats_partial<<<chunks, 256, 0, st>>>(static_cast<const bf16*>(x), M, C,
-                                                              chunk, reinterpret_cast<float2*>(ws));
-  merge_partials(reinterpret_cast<const float2*>(ws), chunks, chunk, M, C, mean, invstd, eps, rm,
-                 rv, mom, st);
-  return cudaGetLastError();
+  if (cudaError_t e_ = launch_k(k_bn_stats_partial, dim3(chunks), dim3(256), 0, st, static_cast<const bf16*>(x), M, C, chunk, reinterpret_cast<float2*>(ws))) return e_;
+  return merge_partials(reinterpret_cast<const float2*>(ws), chunks, chunk, M, C, mean, invstd, eps,
+                        rm, rv, mom, st);
 }
 
 int64_t stats_partials_floats(int64_t M, int C, int rows_per_part) {
@@ -733,9 +764,8 @@ cudaError_t bn_stats_from_partials(const float* partials, int64_t M, int C, int 
                                    float* mean, float* invstd, float eps, float* rm, float* rv,
                                    float mom, cudaStream_t st) {
   const int parts = int((M + rows_per_part - 1) / rows_per_part);
-  merge_partials(reinterpret_cast<const float2*>(partials), parts, rows_per_part, M, C, mean,
-                 invstd, eps, rm, rv, mom, st);
-  return cudaGetLastError();
+  return merge_partials(reinterpret_cast<const float2*>(partials), parts, rows_per_part, M, C, mean,
+                        invstd, eps, rm, rv, mom, st);
 }
 
 cudaError_t bn_apply(int mode, const void* x, const void* res, void* y, int64_t M, int C,
@@ -750,16 +780,13 @@ cudaError_t bn_apply(int mode, const void* x, const void* res, void* y, int64_t 
   auto Y = static_cast<bf16*>(y);
   switch (mode) {
     case 0:
-      k_bn_apply<0><<<grid, 256, 0, st>>>(X, R, Y, vecs, C - 1, mean, invstd, gamma, beta,
-                                          nullptr, nullptr, nullptr, nullptr);
+      if (cudaError_t e_ = launch_k(k_bn_apply<0>, dim3(grid), dim3(256), 0, st, X, R, Y, vecs, C - 1, mean, invstd, gamma, beta, nullptr, nullptr, nullptr, nullptr)) return e_;
       break;
     case 1:
-      k_bn_apply<1><<<grid, 256, 0, st>>>(X, R, Y, vecs, C - 1, mean, invstd, gamma, beta,
-                                          nullptr, nullptr, nullptr, nullptr);
+      if (cudaError_t e_ = launch_k(k_bn_apply<1>, dim3(grid), dim3(256), 0, st, X, R, Y, vecs, C - 1, mean, invstd, gamma, beta, nullptr, nullptr, nullptr, nullptr)) return e_;
       break;
     default:
-      k_bn_apply<2><<<grid, 256, 0, st>>>(X, R, Y, vecs, C - 1, mean, invstd, gamma, beta, mean2,
-                                          invstd2, gamma2, beta2);
+      if (cudaError_t e_ = launch_k(k_bn_apply<2>, dim3(grid), dim3(256), 0, st, X, R, Y, vecs, C - 1, mean, invstd, gamma, beta, mean2, invstd2, gamma2, beta2)) return e_;
   }
   return cudaGetLastError();
 }
@@ -776,25 +803,22 @@ cudaError_t bn_backward(const void* up, int pool_hw, const void* mask, const voi
   auto X = static_cast<const bf16*>(x);
   const auto part = Mk ? (pool_hw ? k_bn_bwd_partial<true, true> : k_bn_bwd_partial<true, false>)
                       : (pool_hw ? k_bn_bwd_partial<false, true> : k_bn_bwd_partial<false, false>);
-  part<<<chunks, 256, 0, st>>>(U, pool_hw, Mk, X, M, C, chunk, mean, invstd,
-                               reinterpret_cast<float2*>(ws));
+  if (cudaError_t e_ = launch_k(part, dim3(chunks), dim3(256), 0, st, U, pool_hw, Mk, X, M, C, chunk, mean, invstd, reinterpret_cast<float2*>(ws))) return e_;
   const float2* w2 = reinterpret_cast<const float2*>(ws);
   int parts = chunks;
   if (parts > 2 * GROUP) {  // two-level fixed-order sum (scratch after the partials)
     const int groups = (parts + GROUP - 1) / GROUP;
     float2* out = reinterpret_cast<float2*>(ws) + int64_t(parts) * C;
     const int bx = C < 256 ? C : 256;
-    k_bn_bwd_group<<<dim3((C + bx - 1) / bx, groups), bx, 0, st>>>(w2, parts, C, out);
+    if (cudaError_t e_ = launch_k(k_bn_bwd_group, dim3(dim3((C + bx - 1) / bx, groups)), dim3(bx), 0, st, w2, parts, C, out)) return e_;
     w2 = out;
     parts = groups;
   }
-  k_bn_bwd_final<<<(C + 7) / 8, 256, 0, st>>>(w2, parts, C, dgamma, dbeta);
+  if (cudaError_t e_ = launch_k(k_bn_bwd_final, dim3((C + 7) / 8), dim3(256), 0, st, w2, parts, C, dgamma, dbeta)) return e_;
   const int64_t vecs = M * C / 8;
   const auto app = Mk ? (pool_hw ? k_bn_bwd_apply<true, true> : k_bn_bwd_apply<true, false>)
                      : (pool_hw ? k_bn_bwd_apply<false, true> : k_bn_bwd_apply<false, false>);
-  app<<<grid_for(vecs, 256), 256, 0, st>>>(U, pool_hw, Mk, X, static_cast<bf16*>(dx), vecs, C - 1,
-                                           __builtin_ctz(C), M, mean, invstd, gamma, dgamma,
-                                           dbeta);
+  if (cudaError_t e_ = launch_k(app, dim3(grid_for(vecs, 256)), dim3(256), 0, st, U, pool_hw, Mk, X, static_cast<bf16*>(dx), vecs, C - 1, __builtin_ctz(C), M, mean, invstd, gamma, dgamma, dbeta)) return e_;
   return cudaGetLastError();
 }
 
@@ -809,15 +833,13 @@ cudaError_t bn_backward_from_partials(const float* partials, int rows_per_part, 
     const int groups = (parts + GROUP - 1) / GROUP;
     float2* out = const_cast<float2*>(ws) + int64_t(parts) * C;
     const int bx = C < 256 ? C : 256;
-    k_bn_bwd_group<<<dim3((C + bx - 1) / bx, groups), bx, 0, st>>>(ws, parts, C, out);
+    if (cudaError_t e_ = launch_k(k_bn_bwd_group, dim3(dim3((C + bx - 1) / bx, groups)), dim3(bx), 0, st, ws, parts, C, out)) return e_;
     ws = out;
     parts = groups;
   }
-  k_bn_bwd_final_raw<<<(C + 7) / 8, 256, 0, st>>>(ws, parts, C, mean, invstd, dgamma, dbeta);
+  if (cudaError_t e_ = launch_k(k_bn_bwd_final_raw, dim3((C + 7) / 8), dim3(256), 0, st, ws, parts, C, mean, invstd, dgamma, dbeta)) return e_;
   const int64_t vecs = M * C / 8;
-  k_bn_bwd_apply<false, false><<<grid_for(vecs, 256), 256, 0, st>>>(
-      static_cast<const bf16*>(g), 0, nullptr, static_cast<const bf16*>(x), static_cast<bf16*>(dx),
-      vecs, C - 1, __builtin_ctz(C), M, mean, invstd, gamma, dgamma, dbeta);
+  if (cudaError_t e_ = launch_k(k_bn_bwd_apply<false, false>, dim3(grid_for(vecs, 256)), dim3(256), 0, st, static_cast<const bf16*>(g), 0, nullptr, static_cast<const bf16*>(x), static_cast<bf16*>(dx), vecs, C - 1, __builtin_ctz(C), M, mean, invstd, gamma, dgamma, dbeta)) return e_;
   return cudaGetLastError();
 }
 
@@ -825,10 +847,7 @@ cudaError_t add_grad(const void* a, const void* up, int pool_hw, const void* up_
                      const void* out_mask, void* out, int64_t M, int C, cudaStream_t st) {
   if (C & (C - 1)) return cudaErrorInvalidValue;
   const int64_t vecs = M * C / 8;
-  (pool_hw ? k_add_grad<true> : k_add_grad<false>)<<<grid_for(vecs, 256), 256, 0, st>>>(
-      static_cast<const bf16*>(a), static_cast<const bf16*>(up), pool_hw,
-      static_cast<const bf16*>(up_mask), static_cast<const bf16*>(out_mask),
-      static_cast<bf16*>(out), vecs, C - 1, __builtin_ctz(C), C);
+  if (cudaError_t e_ = launch_k((pool_hw ? k_add_grad<true> : k_add_grad<false>), dim3(grid_for(vecs, 256)), dim3(256), 0, st, static_cast<const bf16*>(a), static_cast<const bf16*>(up), pool_hw, static_cast<const bf16*>(up_mask), static_cast<const bf16*>(out_mask), static_cast<bf16*>(out), vecs, C - 1, __builtin_ctz(C), C)) return e_;
   return cudaGetLastError();
 }
 
@@ -836,8 +855,7 @@ cudaError_t maxpool3x3s2_fwd(const void* x, void* y, int N, int H, int W, int C,
   const int P = (H + 2 - 3) / 2 + 1, Q = (W + 2 - 3) / 2 + 1;
   if (C % 8 || ((C / 8) & (C / 8 - 1))) return cudaErrorInvalidValue;
   const int lcg = __builtin_ctz(C / 8);
-  k_maxpool_fwd<<<dim3(unsigned(N) * P, (Q * (C / 8) + 255) / 256), 256, 0, st>>>(
-      static_cast<const bf16*>(x), static_cast<bf16*>(y), N, H, W, C, P, Q, lcg);
+  if (cudaError_t e_ = launch_k(k_maxpool_fwd, dim3(dim3(unsigned(N) * P, (Q * (C / 8) + 255) / 256)), dim3(256), 0, st, static_cast<const bf16*>(x), static_cast<bf16*>(y), N, H, W, C, P, Q, lcg)) return e_;
   return cudaGetLastError();
 }
 
@@ -851,26 +869,22 @@ cudaError_t maxpool3x3s2_bwd(const void* dy, const void* x, void* dx, int N, int
   const int P = (H + 2 - 3) / 2 + 1, Q = (W + 2 - 3) / 2 + 1;
   if (C % 8 || ((C / 8) & (C / 8 - 1))) return cudaErrorInvalidValue;
   const int lcg = __builtin_ctz(C / 8);
-  k_maxpool_argmax<<<dim3(unsigned(N) * P, (Q * (C / 8) + 255) / 256), 256, 0, st>>>(
-      static_cast<const bf16*>(x), static_cast<uint8_t*>(ws), N, H, W, C, P, Q, lcg);
+  if (cudaError_t e_ = launch_k(k_maxpool_argmax, dim3(dim3(unsigned(N) * P, (Q * (C / 8) + 255) / 256)), dim3(256), 0, st, static_cast<const bf16*>(x), static_cast<uint8_t*>(ws), N, H, W, C, P, Q, lcg)) return e_;
   if (H != 2 * P || W != 2 * Q) return cudaErrorInvalidValue;  // even input sizes
-  k_maxpool_bwd_gather<<<dim3(unsigned(N) * P, (Q * (C / 8) + 255) / 256), 256, 0, st>>>(
-      static_cast<const bf16*>(dy), static_cast<const uint8_t*>(ws), static_cast<bf16*>(dx), N, H,
-      W, C, P, Q, lcg);
+  if (cudaError_t e_ = launch_k(k_maxpool_bwd_gather, dim3(dim3(unsigned(N) * P, (Q * (C / 8) + 255) / 256)), dim3(256), 0, st, static_cast<const bf16*>(dy), static_cast<const uint8_t*>(ws), static_cast<bf16*>(dx), N, H, W, C, P, Q, lcg)) return e_;
   return cudaGetLastError();
 }
 
 cudaError_t avgpool_fwd(const void* x, void* y, int N, int HW, int C, cudaStream_t st) {
   const int64_t total = int64_t(N) * (C / 8);
-  k_avgpool_fwd<<<grid_for(total, 128), 128, 0, st>>>(static_cast<const bf16*>(x),
-                                                      static_cast<bf16*>(y), N, HW, C);
+  if (cudaError_t e_ = launch_k(k_avgpool_fwd, dim3(grid_for(total, 128)), dim3(128), 0, st, static_cast<const bf16*>(x), static_cast<bf16*>(y), N, HW, C)) return e_;
   return cudaGetLastError();
 }
 
 cudaError_t softmax_xent(const float* logits, const int64_t* labels, float* loss, float* dlogits,
                          float* row_loss_ws, int N, int K, cudaStream_t st) {
-  k_softmax_xent<<<N, 256, 0, st>>>(logits, labels, dlogits, row_loss_ws, N, K);
-  k_mean_rows<<<1, 32, 0, st>>>(row_loss_ws, N, loss);
+  if (cudaError_t e_ = launch_k(k_softmax_xent, dim3(N), dim3(256), 0, st, logits, labels, dlogits, row_loss_ws, N, K)) return e_;
+  if (cudaError_t e_ = launch_k(k_mean_rows, dim3(1), dim3(32), 0, st, row_loss_ws, N, loss)) return e_;
   return cudaGetLastError();
 }
 

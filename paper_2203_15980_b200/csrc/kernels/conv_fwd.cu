@@ -36,6 +36,7 @@
 #include <mutex>
 
 #include "kernels/kernels.hpp"
+#include "kernels/launch.hpp"
 #include "kernels/sm100_common.cuh"
 #include "kernels/tma_host.hpp"
 
@@ -248,6 +249,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tslot;
+  // prologue done (barriers, TMEM, descriptors): now wait for the predecessor
+  pdl_wait();
+  pdl_trigger();
 
   if (warp < 4) {
     // ============================ producers ============================
@@ -997,8 +1001,7 @@ cudaError_t launch(const ConvPlan& cp, const void* x, void* y, float* stats,
       return cudaErrorInvalidValue;
   }
   const int grid = a.tiles < num_sms() ? a.tiles : num_sms();
-  kern<<<grid, kThreads, smem, st>>>(*reinterpret_cast<const CUtensorMap*>(cp.wmap), amap, ymap,
-                                     emap0, emap1, a);
+  if (cudaError_t e_ = launch_k(kern, dim3(grid), dim3(kThreads), smem, st, *reinterpret_cast<const CUtensorMap*>(cp.wmap), amap, ymap, emap0, emap1, a)) return e_;
   return cudaGetLastError();
 }
 

@@ -24,6 +24,7 @@
 #include <cuda_runtime.h>
 
 #include "kernels/kernels.hpp"
+#include "kernels/launch.hpp"
 #include "kernels/sm100_common.cuh"
 #include "kernels/tma_host.hpp"
 
@@ -115,6 +116,9 @@ __global__ void __launch_bounds__(HT, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tslot;
+  // prologue done (barriers, TMEM, descriptors): now wait for the predecessor
+  pdl_wait();
+  pdl_trigger();
 
   if (warp == 0) {
     // ================================ producer ================================
@@ -338,7 +342,7 @@ cudaError_t halo_launch(const ConvPlan& cp, const void* x, void* y, float* stats
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const int grid = a.tiles < sms ? a.tiles : sms;
-  kern<<<grid, HT, smem, st>>>(*reinterpret_cast<const CUtensorMap*>(cp.wmap), xmap, ymap, a);
+  if (cudaError_t e_ = launch_k(kern, dim3(grid), dim3(HT), smem, st, *reinterpret_cast<const CUtensorMap*>(cp.wmap), xmap, ymap, a)) return e_;
   return cudaGetLastError();
 }
 

@@ -1,0 +1,49 @@
+// Kernel launches, optionally with programmatic dependent launch (PDL): the
+// successor kernel in the stream (or CUDA graph) may be scheduled as soon as
+// this one triggers; every kernel calls pdl_wait() before its first global
+// memory access, so ordering is unchanged.  DELTA_PDL=1 enables it; measured
+// neutral on the graph-replayed ResNet-50 step (11.44k vs 11.48k img/s A/B on
+// one box), so plain stream order is the default.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdlib>
+#include <utility>
+
+namespace delta_k {
+
+// Device side: wait for the predecessor grid (completion + memory flush)
+// before the first global memory access, and let the successor launch at
+// once — its CTAs take SMs as this grid's CTAs retire and run their prologue
+// (barrier init, TMEM alloc, descriptor prefetch) under this grid's tail.
+// Both are no-ops for a launch without the attribute.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
+inline bool pdl_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("DELTA_PDL");
+    return e && e[0] == '1';
+  }();
+  return on;
+}
+
+template <typename... KArgs, typename... Args>
+cudaError_t launch_k(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                     cudaStream_t st, Args&&... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
+}
+
+}  // namespace delta_k

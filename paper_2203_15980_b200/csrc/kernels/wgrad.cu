@@ -27,6 +27,7 @@
 #include <cstdlib>
 
 #include "kernels/kernels.hpp"
+#include "kernels/launch.hpp"
 #include "kernels/sm100_common.cuh"
 #include "kernels/tma_host.hpp"
 
@@ -142,6 +143,9 @@ __global__ void __launch_bounds__(WG_THREADS, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tslot;
+  // prologue done (barriers, TMEM, descriptors): now wait for the predecessor
+  pdl_wait();
+  pdl_trigger();
 
   // work item -> (split, tile); tile -> (m block, first flattened column n0);
   // a tile's BN columns may span several taps when C < BN
@@ -362,6 +366,8 @@ template <int BN, int TM>
 __global__ void __launch_bounds__(256)
     k_wgrad_reduce(const float* __restrict__ ws, float* __restrict__ dw, int K, int ntot,
                    int tiles_m, int tiles, int splits) {
+  pdl_wait();
+  pdl_trigger();
   const int64_t total = int64_t(K) * ntot;
   for (int64_t e = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; e < total;
        e += int64_t(gridDim.x) * blockDim.x) {
@@ -379,6 +385,8 @@ __global__ void __launch_bounds__(256)
 __global__ void __launch_bounds__(256)
     k_wgrad_reduce_stem(const float* __restrict__ ws, float* __restrict__ dw, int K, int splits,
                         int tiles) {
+  pdl_wait();
+  pdl_trigger();
   const int total = K * 7 * 7 * 4;
   for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < total; e += gridDim.x * blockDim.x) {
     const int ch = e & 3;
@@ -461,17 +469,15 @@ cudaError_t wg_launch(const WgradPlan& wp, const void* dy, const void* x, float*
   }
   if (!ok) return cudaErrorInvalidValue;
   const int grid = std::min(a.items, num_sms_wg());
-  kern<<<grid, WG_THREADS, smem, st>>>(amap, bmap, a);
+  if (cudaError_t e_ = launch_k(kern, dim3(grid), dim3(WG_THREADS), smem, st, amap, bmap, a)) return e_;
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   if (MODE == WG_STEM || MODE == WG_STEMRAW) {
-    k_wgrad_reduce_stem<<<(wp.K * 196 + 255) / 256, 256, 0, st>>>(ws, dw, wp.K, wp.splits,
-                                                                  wp.tiles);
+    if (cudaError_t e_ = launch_k(k_wgrad_reduce_stem, dim3((wp.K * 196 + 255) / 256), dim3(256), 0, st, ws, dw, wp.K, wp.splits, wp.tiles)) return e_;
   } else {
     const int64_t total = int64_t(wp.K) * a.ntot;
     const int64_t blocks = std::min<int64_t>((total + 255) / 256, 148 * 16);
-    k_wgrad_reduce<BN, 128 * MT><<<int(blocks), 256, 0, st>>>(ws, dw, wp.K, a.ntot, a.tiles_m,
-                                                             wp.tiles, wp.splits);
+    if (cudaError_t e_ = launch_k(k_wgrad_reduce<BN, 128 * MT>, dim3(int(blocks)), dim3(256), 0, st, ws, dw, wp.K, a.ntot, a.tiles_m, wp.tiles, wp.splits)) return e_;
   }
   return cudaGetLastError();
 }
