@@ -38,8 +38,8 @@ TRACE_FIXTURE = os.path.join(HERE, "tests", "golden", "resnet50_bs256_trace.json
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
-    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--batch", type=int, default=256)
     ap.add_argument("--depth", type=int, default=50)
@@ -313,6 +313,10 @@ def main():
     kinds = {}
     rc = {"launches": 0, "ms": 0.0, "roofline_ms": 0.0, "flops": 0.0, "bytes": 0.0, "by_op": {}}
     swap_ms, swap_bytes, swap_n = 0.0, 0, 0
+    # the whole step against its serial roofline: every action of the plan
+    # (first productions and recomputes) at max(FLOPs/TC peak, algorithmic
+    # HBM bytes/HBM peak) — the time a speed-of-light kernel sequence needs
+    step_roof = {"ms": 0.0, "flops": 0.0, "bytes": 0.0, "tensor_bound_ms": 0.0, "hbm_bound_ms": 0.0}
     for nid, lst in timing.items():
         if nid == "swap":
             for (ms, op, nb) in lst:
@@ -322,6 +326,12 @@ def main():
             continue
         node = rt.nodes[nid]
         for (ms, rec) in lst:
+            t_tc = node.flops / (tc_peak * 1e9)
+            t_mem = (node.hbm_bytes or 2 * node.nbytes) / (hbm_peak * 1e6)
+            step_roof["ms"] += max(t_tc, t_mem)
+            step_roof["flops"] += node.flops
+            step_roof["bytes"] += node.hbm_bytes or 2 * node.nbytes
+            step_roof["tensor_bound_ms" if t_tc >= t_mem else "hbm_bound_ms"] += max(t_tc, t_mem)
             all_ms += ms
             kinds[node.op] = kinds.get(node.op, 0.0) + ms
             if node.op == "conv":
@@ -434,6 +444,15 @@ def main():
                                                "(the 1x1 layer-1 convs are HBM-bound)",
                          "share_of_step": round(conv_ms / all_ms, 4) if all_ms else None,
                          "op_ms": {k: round(v, 3) for k, v in sorted(kinds.items(), key=lambda kv: -kv[1])}},
+            "step_roofline": {"serial_roofline_ms": round(step_roof["ms"], 3),
+                              "frac": round(step_roof["ms"] / delta_ms, 4),
+                              "tflop": round(step_roof["flops"] / 1e12, 3),
+                              "hbm_gb": round(step_roof["bytes"] / 1e9, 2),
+                              "tensor_bound_ms": round(step_roof["tensor_bound_ms"], 3),
+                              "hbm_bound_ms": round(step_roof["hbm_bound_ms"], 3),
+                              "note": "sum over every action of the DELTA step (incl. recomputes) "
+                                      "of max(FLOPs/TC peak, algorithmic HBM bytes/HBM peak), "
+                                      "vs the measured graph step (graph.py byte model)"},
             "recompute": {"launches": rc["launches"], "ms_per_step": round(rc["ms"], 3),
                           "share_of_step": round(rc["ms"] / all_ms, 4) if all_ms else None,
                           "roofline_ms": round(rc["roofline_ms"], 3),

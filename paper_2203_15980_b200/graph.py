@@ -177,10 +177,14 @@ def build_resnet(depth: int = 50, batch: int = 256, image: int = 224,
                      [d_c3.id, R2.id, C2.id], phase="B",
                      attrs=dict(conv=pre + ".conv3", bn=pre + ".bn2"))
         d_c2.flops = 2 * C3.flops
+        # dgrad (read dY, write g) + BN backward (g and BN input twice, write
+        # dX) + weight gradient (read dY and the conv input)
+        d_c2.hbm_bytes = 2 * d_c3.nbytes + 6 * C2.nbytes
         d_c1 = g.add(pre + ".conv2.bwd", "conv_bn_relu_bwd", C1.shape,
                      [d_c2.id, R1.id, C1.id], phase="B",
                      attrs=dict(conv=pre + ".conv2", bn=pre + ".bn1"))
         d_c1.flops = 2 * C2.flops
+        d_c1.hbm_bytes = 2 * d_c2.nbytes + 6 * C1.nbytes
         # output: gradient of the previous block's pre-activation, i.e. masked
         # by X > 0 (X is that block's ReLU output); the first block's input is
         # the maxpool output, whose gradient is left unmasked.
@@ -198,15 +202,23 @@ def build_resnet(depth: int = 50, batch: int = 256, image: int = 224,
         d_x = g.add(pre + ".conv1.bwd", "conv_shortcut_bwd", X.shape, parents, phase="B",
                     attrs=attrs)
         d_x.flops = 2 * C1.flops + (2 * CD.flops if CD is not None else 0)
+        # conv1 dgrad (read dY, write dX) + residual add + ReLU mask reads +
+        # weight gradient (dY, X); the downsample's dgrad and wgrad likewise
+        d_x.hbm_bytes = 2 * d_c1.nbytes + 4 * X.nbytes + \
+            (2 * d_cd.nbytes + 2 * X.nbytes if CD is not None else 0)
         upstream = d_x
         upstream_is_pool = False
     # stem: maxpool backward, bn1-relu backward, conv1 weight gradient
     d_r0 = g.add("maxpool.bwd", "maxpool_bwd", r0.shape, [upstream.id, r0.id], phase="B")
+    d_r0.hbm_bytes = upstream.nbytes + 2 * r0.nbytes  # argmax pass + gather
     d_c0 = g.add("bn1.bwd", "bn_relu_bwd", c0.shape, [d_r0.id, r0.id, c0.id], phase="B",
                  attrs=dict(bn="bn1"))
+    d_c0.hbm_bytes = 7 * c0.nbytes  # masked streaming BN backward: 3 reads, then 3 + 1 write
     # conv1 has no input gradient; its node output is the weight gradient (fp32)
-    g.add("conv1.bwd", "conv_wgrad", (64, 7, 7, stem_cin), [d_c0.id, x.id], phase="B",
-          attrs=dict(conv="conv1"), dtype_bytes=4)
+    wg = g.add("conv1.bwd", "conv_wgrad", (64, 7, 7, stem_cin), [d_c0.id, x.id], phase="B",
+               attrs=dict(conv="conv1"), dtype_bytes=4)
+    wg.flops = c0.flops
+    wg.hbm_bytes = d_c0.nbytes + x.nbytes
     return g
 
 
