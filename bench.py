@@ -316,7 +316,8 @@ def main():
     # the whole step against its serial roofline: every action of the plan
     # (first productions and recomputes) at max(FLOPs/TC peak, algorithmic
     # HBM bytes/HBM peak) — the time a speed-of-light kernel sequence needs
-    step_roof = {"ms": 0.0, "flops": 0.0, "bytes": 0.0, "tensor_bound_ms": 0.0, "hbm_bound_ms": 0.0}
+    step_roof = {"ms": 0.0, "flops": 0.0, "bytes": 0.0, "tensor_bound_ms": 0.0, "hbm_bound_ms": 0.0,
+                 "by_op": {}}
     for nid, lst in timing.items():
         if nid == "swap":
             for (ms, op, nb) in lst:
@@ -332,6 +333,9 @@ def main():
             step_roof["flops"] += node.flops
             step_roof["bytes"] += node.hbm_bytes or 2 * node.nbytes
             step_roof["tensor_bound_ms" if t_tc >= t_mem else "hbm_bound_ms"] += max(t_tc, t_mem)
+            bo = step_roof["by_op"].setdefault(node.op, [0.0, 0.0])
+            bo[0] += ms
+            bo[1] += max(t_tc, t_mem)
             all_ms += ms
             kinds[node.op] = kinds.get(node.op, 0.0) + ms
             if node.op == "conv":
@@ -450,6 +454,9 @@ def main():
                               "hbm_gb": round(step_roof["bytes"] / 1e9, 2),
                               "tensor_bound_ms": round(step_roof["tensor_bound_ms"], 3),
                               "hbm_bound_ms": round(step_roof["hbm_bound_ms"], 3),
+                              "by_op_ms_vs_roofline": {k: [round(v[0], 3), round(v[1], 3)] for k, v in
+                                                       sorted(step_roof["by_op"].items(),
+                                                              key=lambda kv: kv[1][1] - kv[1][0])},
                               "note": "sum over every action of the DELTA step (incl. recomputes) "
                                       "of max(FLOPs/TC peak, algorithmic HBM bytes/HBM peak), "
                                       "vs the measured graph step (graph.py byte model)"},

@@ -142,6 +142,28 @@ delta_status delta_softmax_xent(const float* logits, const int64_t* labels, floa
                                 float* dlogits, float* row_ws, int32_t N, int32_t K,
                                 void* stream);
 
+/* ---- optimizer step and the per-step weight views (optim.cu) ---- */
+/* SGD with momentum and weight decay over flat fp32 buffers (n floats, 16 B
+ * aligned): mom = mom*momentum + g + weight_decay*w; w -= lr*mom; and the
+ * first n_bf elements of w rounded to bf16 into wbf (the conv weights). */
+delta_status delta_sgd_step(float* w, float* mom, const float* g, void* wbf, int64_t n,
+                            int64_t n_bf, float lr, float momentum, float weight_decay,
+                            void* stream);
+/* Derived bf16 weight tensors from bf16 [K][R][S][C] conv weights, one launch
+ * for a device-resident table of views:
+ *   DELTA_VIEW_DGRAD: dst[c][r][s][k] = src[k][R-1-r][S-1-s][c] (input-gradient
+ *                     convs through our kernel)
+ *   DELTA_VIEW_STEM:  dst[k][256] pixel-pair stem layout (C = 4, 7x7): column
+ *                     (r*4+j)*8 + e*4 + c = src[k][r][2j+e-1][c], zero elsewhere */
+enum { DELTA_VIEW_DGRAD = 0, DELTA_VIEW_STEM = 1 };
+typedef struct delta_weight_view {
+  int32_t kind, K, R, S, C, reserved;
+  const void* src;
+  void* dst;
+} delta_weight_view;
+delta_status delta_weight_views(const delta_weight_view* views_dev, int32_t n_views,
+                                void* stream);
+
 /* ---- swap engine (Offload/Reload, ref src/engine.cpp:312-331, 396-419,
  *      533-585): pinned host slab + dedicated copy-engine streams ---- */
 typedef struct delta_swap delta_swap;

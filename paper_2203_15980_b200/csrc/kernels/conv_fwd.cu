@@ -109,24 +109,6 @@ __device__ __forceinline__ void unpack8f(uint4 u, float* f) {
     f[2 * i + 1] = t.y;
   }
 }
-__device__ __forceinline__ float bf16_round(float v) {
-  return __bfloat162float(__float2bfloat16_rn(v));
-}
-// Reduce-scatter of a 32x32 (lanes x registers) block: afterwards lane l
-// holds in v[0] the sum over all lanes of v[l].  Fixed butterfly order, so
-// the result is deterministic.
-__device__ __forceinline__ void transpose_sum32(float (&v)[32], int lane) {
-#pragma unroll
-  for (int o = 16; o >= 1; o >>= 1) {
-    const bool up = (lane & o) != 0;
-#pragma unroll
-    for (int i = 0; i < o; ++i) {
-      const float send = up ? v[i] : v[i + o];
-      const float keep = up ? v[i + o] : v[i];
-      v[i] = keep + __shfl_xor_sync(0xffffffffu, send, o);
-    }
-  }
-}
 
 // Row `lane` (16 B chunk u) of a 32x32 bf16 block staged in smem with the 64B
 // swizzle (the layout of the TMA boxes the epilogue loads and stores).
@@ -256,8 +238,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp < 4) {
     // ============================ producers ============================
     const int tid = threadIdx.x;
-    if constexpr (OPT) {
-      if (warp == 1) {
+    if (OPT && warp == 1) {
+      if constexpr (OPT) {
         // epilogue operands of every tile of this CTA, two tiles ahead
         if (lane == 0) {
           uint32_t lt = 0;
@@ -276,10 +258,8 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
           }
         }
-        goto producers_done;
       }
-    }
-    {
+    } else {
     uint32_t it = 0;  // global k-iteration counter (stage ring position)
     for (int tile = blockIdx.x; tile < a.tiles; tile += gridDim.x) {
       const int m0 = (tile / a.n_tiles) * BM;
@@ -484,7 +464,6 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
     }
-  producers_done:;
   } else if (warp < MMA_WARP) {
     // ============================ epilogue =============================
     const int quarter = warp & 3;  // TMEM lanes [32*quarter, 32*quarter+32)
@@ -904,6 +883,13 @@ bool encode_out_rows(CUtensorMap* m, void* y, const ConvPlan& cp) {
             CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+// operand stages at BN=128 with TMA-loaded epilogue operands: the two tile
+// buffers of a two-operand epilogue leave room for two
+template <int EV>
+constexpr int opt_stages() {
+  return ev_operands(EV) == 1 ? 3 : 2;
+}
+
 // DELTA_EPI_TMA=0 keeps the fused epilogue operands on the cp.async ring
 bool operands_tma() {
   static int v = -1;
@@ -1078,20 +1064,26 @@ cudaError_t conv_forward(const ConvPlan& cp, const void* x, void* y, float* stat
     if (cp.bn != 64 && cp.bn != 128) return cudaErrorInvalidValue;
     if (e.add_stride2 && (ev == EV_POOL || ev == EV_BN_BWD || (cp.P & 1) || (cp.Q & 1)))
       return cudaErrorInvalidValue;
-    // operands by TMA (per-tile boxes) for the 1x1 input gradients with a
-    // short reduction: two operand stages leave room for two tile buffers
-    // (measured: 281 -> 218 us at 56x56 64->256, floor 205; a 512-deep
-    // reduction loses more to the 2 stages than it gains); the stride-2
-    // shortcut add stays on the cp.async gather
-    const bool opt = tma_a && !e.add_stride2 && cp.kdim <= 256 && operands_tma();
-#define DELTA_FUSED(EVV)                                                                    \
-  case EVV:                                                                                 \
-    if (opt && cp.bn == 64) return launch<64, 4, MODE_TMA, EVV, true>(cp, x, y, stats, e, st); \
-    if (opt) return launch<128, 2, MODE_TMA, EVV, true>(cp, x, y, stats, e, st);            \
-    if (cp.bn == 64)                                                                        \
-      return tma_a ? launch<64, 4, MODE_TMA, EVV>(cp, x, y, stats, e, st)                    \
-                   : launch<64, 4, MODE_IM2COL, EVV>(cp, x, y, stats, e, st);                \
-    return tma_a ? launch<128, 3, MODE_TMA, EVV>(cp, x, y, stats, e, st)                     \
+    // Operands by TMA (per-tile boxes into two tile buffers) unless the add is
+    // the stride-2 shortcut gradient (cp.async gather from its sampling grid).
+    // One-operand epilogues (BN backward, plain add) keep the usual stage
+    // count; two-operand ones need two stages at BN=128, which only pays for
+    // a short reduction (measured: 281 -> 218 us at 56x56 64->256, floor 205;
+    // a 512-deep one loses more to the 2 stages than it gains).
+    const bool one_op = ev == EV_BN_BWD || ev == EV_ADD;
+    const bool opt = !e.add_stride2 && operands_tma() && (one_op || cp.bn == 64 || cp.kdim <= 256);
+#define DELTA_FUSED(EVV)                                                                      \
+  case EVV:                                                                                   \
+    if (opt && cp.bn == 64)                                                                   \
+      return tma_a ? launch<64, 4, MODE_TMA, EVV, true>(cp, x, y, stats, e, st)                \
+                   : launch<64, 4, MODE_IM2COL, EVV, true>(cp, x, y, stats, e, st);            \
+    if (opt)                                                                                  \
+      return tma_a ? launch<128, opt_stages<EVV>(), MODE_TMA, EVV, true>(cp, x, y, stats, e, st) \
+                   : launch<128, opt_stages<EVV>(), MODE_IM2COL, EVV, true>(cp, x, y, stats, e, st); \
+    if (cp.bn == 64)                                                                          \
+      return tma_a ? launch<64, 4, MODE_TMA, EVV>(cp, x, y, stats, e, st)                      \
+                   : launch<64, 4, MODE_IM2COL, EVV>(cp, x, y, stats, e, st);                  \
+    return tma_a ? launch<128, 3, MODE_TMA, EVV>(cp, x, y, stats, e, st)                       \
                  : launch<128, 3, MODE_IM2COL, EVV>(cp, x, y, stats, e, st);
     switch (ev) {
       DELTA_FUSED(EV_ADD)

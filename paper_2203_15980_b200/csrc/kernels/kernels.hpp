@@ -4,6 +4,8 @@
 
 #include <cstdint>
 
+#include "delta/delta_kernels.h"
+
 namespace delta_k {
 
 // ---- implicit-GEMM convolution (conv_fwd.cu) ----
@@ -56,6 +58,11 @@ int conv_plan_set_tile_n(ConvPlan* cp, int bn, const void* w);
 // bf16 outputs of each 128-row tile — the BN statistics partials.
 cudaError_t conv_forward(const ConvPlan& cp, const void* x, void* y, float* stats,
                          cudaStream_t st, const ConvEpilogue* epi = nullptr);
+
+// ---- optimizer step + weight views (optim.cu) ----
+cudaError_t sgd_step(float* w, float* mom, const float* g, void* wbf, int64_t n, int64_t n_bf,
+                     float lr, float m, float wd, cudaStream_t st);
+cudaError_t weight_views(const delta_weight_view* views_dev, int n_views, cudaStream_t st);
 
 // ---- weight gradient (wgrad.cu) ----
 struct WgradPlan {

@@ -158,6 +158,19 @@ delta_status delta_bn_stats_from_partials(const float* partials, int64_t M, int3
                      "bn_stats_from_partials");
 }
 
+delta_status delta_sgd_step(float* w, float* mom, const float* g, void* wbf, int64_t n,
+                            int64_t n_bf, float lr, float momentum, float weight_decay,
+                            void* stream) {
+  return cuda_status(
+      delta_k::sgd_step(w, mom, g, wbf, n, n_bf, lr, momentum, weight_decay, S(stream)),
+      "sgd_step");
+}
+
+delta_status delta_weight_views(const delta_weight_view* views_dev, int32_t n_views,
+                                void* stream) {
+  return cuda_status(delta_k::weight_views(views_dev, n_views, S(stream)), "weight_views");
+}
+
 delta_status delta_bn_apply(int32_t mode, const void* x, const void* res, void* y, int64_t M,
                             int32_t C, const float* mean, const float* invstd, const float* gamma,
                             const float* beta, const float* mean2, const float* invstd2,

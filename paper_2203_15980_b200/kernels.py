@@ -35,6 +35,8 @@ _SIGS = {
     "delta_maxpool3x3s2_bwd": (i32, [vp, vp, vp, i32, i32, i32, i32, vp, vp]),
     "delta_avgpool_fwd": (i32, [vp, vp, i32, i32, i32, vp]),
     "delta_softmax_xent": (i32, [vp, vp, vp, vp, vp, i32, i32, vp]),
+    "delta_sgd_step": (i32, [vp, vp, vp, vp, i64, i64, f32, f32, f32, vp]),
+    "delta_weight_views": (i32, [vp, i32, vp]),
     "delta_swap_create": (i32, [u64, P(vp)]),
     "delta_swap_host_ptr": (vp, [vp]),
     "delta_swap_stream": (vp, [vp, i32]),
@@ -215,6 +217,28 @@ def bn_apply(mode, x, res, y, M, C_, mean, invstd, gamma, beta, mean2=None, invs
     check(lib.delta_bn_apply(mode, x, res, y, M, C_, mean, invstd, gamma, beta, mean2, invstd2,
                              gamma2, beta2, stream))
     _count(1)
+
+
+VIEW_DGRAD, VIEW_STEM = 0, 1
+
+
+class WeightView(C.Structure):
+    """delta_weight_view (include/delta/delta_kernels.h)."""
+    _fields_ = [("kind", i32), ("K", i32), ("R", i32), ("S", i32), ("C", i32),
+                ("reserved", i32), ("src", vp), ("dst", vp)]
+
+
+def sgd_step(w, mom, g, wbf, n, n_bf, lr, momentum, weight_decay, stream):
+    """One fused SGD pass over the flat fp32 buffers (+ bf16 copy of the first n_bf)."""
+    check(lib.delta_sgd_step(w, mom, g, wbf, n, n_bf, lr, momentum, weight_decay, stream))
+    _count(1)
+
+
+def weight_views(table_dev, n, stream):
+    """All derived bf16 weight tensors (transposed dgrad / pixel-pair stem) in one launch;
+    `table_dev` = device copy of a WeightView array."""
+    check(lib.delta_weight_views(table_dev, n, stream))
+    _count(1 if n else 0)
 
 
 def bn_backward(up, pool_hw, mask, x, dx, M, C_, mean, invstd, gamma, dgamma, dbeta, ws, stream):

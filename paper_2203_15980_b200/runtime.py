@@ -112,6 +112,19 @@ class Params:
             if own_dgrad(cs):
                 self.wd[name] = torch.empty(cs.cin, cs.k, cs.k, cs.cout, dtype=torch.bfloat16,
                                             device=device)
+        # every derived weight tensor as one table for the weight-view kernel
+        views = []
+        for name, packed in self.stem_packed.items():
+            cs = g.convs[name]
+            views.append(K.WeightView(K.VIEW_STEM, cs.cout, cs.k, cs.k, cs.cin, 0,
+                                      self.wbf[name].data_ptr(), packed.data_ptr()))
+        for name, wd in self.wd.items():
+            cs = g.convs[name]
+            views.append(K.WeightView(K.VIEW_DGRAD, cs.cout, cs.k, cs.k, cs.cin, 0,
+                                      self.wbf[name].data_ptr(), wd.data_ptr()))
+        self.n_views = len(views)
+        arr = (K.WeightView * max(1, len(views)))(*views)
+        self.views_dev = torch.frombuffer(bytearray(arr), dtype=torch.uint8).to(device)
         self.bn_mean = {n: torch.zeros(c, device=device) for n, c in g.bns.items()}
         self.bn_invstd = {n: torch.ones(c, device=device) for n, c in g.bns.items()}
         self.bn_rmean = {n: torch.zeros(c, device=device) for n, c in g.bns.items()}
@@ -119,17 +132,20 @@ class Params:
         self.refresh_bf16()
 
     def refresh_bf16(self):
+        """bf16 conv weights from the fp32 masters, then every derived view."""
         self.conv_bf16.copy_(self.master[:self.n_conv])
-        for name, packed in self.stem_packed.items():
-            K.pack_stem_weights(self.wbf[name], packed)
-        for name, wd in self.wd.items():
-            wd.copy_(self.wbf[name].flip(1, 2).permute(3, 1, 2, 0))
+        K.weight_views(self.views_dev.data_ptr(), self.n_views,
+                       torch.cuda.current_stream().cuda_stream)
 
     def sgd_step(self, lr: float, momentum: float = 0.9, weight_decay: float = 1e-4):
-        # grads stay untouched (they are what DP all-reduces and tests read)
-        self.mom.mul_(momentum).add_(self.grad).add_(self.master, alpha=weight_decay)
-        self.master.add_(self.mom, alpha=-lr)
-        self.refresh_bf16()
+        """SGD with momentum + weight decay, the bf16 conv weights and their
+        derived views: two launches (optim.cu).  Grads stay untouched (they
+        are what DP all-reduces and tests read)."""
+        st = torch.cuda.current_stream().cuda_stream
+        K.sgd_step(self.master.data_ptr(), self.mom.data_ptr(), self.grad.data_ptr(),
+                   self.conv_bf16.data_ptr(), self.numel, self.n_conv, lr, momentum,
+                   weight_decay, st)
+        K.weight_views(self.views_dev.data_ptr(), self.n_views, st)
 
 
 def workspace_plan(g: G.Graph) -> dict:

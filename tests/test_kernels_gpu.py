@@ -426,3 +426,40 @@ def test_wgrad_stem_pairs():
     err = (dw - ref).abs()
     tol = 1e-3 * ref.abs() + 1e-3 * ref.pow(2).mean().sqrt()
     assert bool((err <= tol).all()), f"max err {err.max().item()}"
+
+
+@pytest.mark.gpu
+def test_sgd_step_and_weight_views_match_torch():
+    g = torch.Generator(device="cuda").manual_seed(11)
+    n, n_bf = 10_000_003, 6_000_001          # odd sizes: vector body + scalar tail
+    w = torch.randn(n, device="cuda", generator=g)
+    mom = torch.randn(n, device="cuda", generator=g)
+    grad = torch.randn(n, device="cuda", generator=g)
+    wbf = torch.empty(n_bf, device="cuda", dtype=torch.bfloat16)
+    w_ref, mom_ref = w.clone(), mom.clone()
+    lr, m, wd = 0.1, 0.9, 1e-4
+    K.sgd_step(w.data_ptr(), mom.data_ptr(), grad.data_ptr(), wbf.data_ptr(), n, n_bf, lr, m, wd,
+               _stream())
+    mom_ref.mul_(m).add_(grad).add_(w_ref, alpha=wd)
+    w_ref.add_(mom_ref, alpha=-lr)
+    torch.cuda.synchronize()
+    assert torch.allclose(mom, mom_ref, rtol=1e-6, atol=1e-6)
+    assert torch.allclose(w, w_ref, rtol=1e-6, atol=1e-6)
+    assert torch.equal(wbf, w[:n_bf].to(torch.bfloat16))
+    # weight views: transposed input-gradient weights and the pixel-pair stem
+    conv = (torch.randn(256, 3, 3, 64, device="cuda", generator=g)).to(torch.bfloat16)
+    one = (torch.randn(512, 1, 1, 128, device="cuda", generator=g)).to(torch.bfloat16)
+    stem = (torch.randn(64, 7, 7, 4, device="cuda", generator=g)).to(torch.bfloat16)
+    d3 = torch.empty(64, 3, 3, 256, device="cuda", dtype=torch.bfloat16)
+    d1 = torch.empty(128, 1, 1, 512, device="cuda", dtype=torch.bfloat16)
+    sp = torch.full((64, K.STEM_KDIM), 7.0, device="cuda", dtype=torch.bfloat16)
+    views = [K.WeightView(K.VIEW_DGRAD, 256, 3, 3, 64, 0, conv.data_ptr(), d3.data_ptr()),
+             K.WeightView(K.VIEW_DGRAD, 512, 1, 1, 128, 0, one.data_ptr(), d1.data_ptr()),
+             K.WeightView(K.VIEW_STEM, 64, 7, 7, 4, 0, stem.data_ptr(), sp.data_ptr())]
+    arr = (K.WeightView * 3)(*views)
+    table = torch.frombuffer(bytearray(arr), dtype=torch.uint8).cuda()
+    K.weight_views(table.data_ptr(), 3, _stream())
+    torch.cuda.synchronize()
+    assert torch.equal(d3, conv.flip(1, 2).permute(3, 1, 2, 0))
+    assert torch.equal(d1, one.flip(1, 2).permute(3, 1, 2, 0))
+    assert torch.equal(sp, K.pack_stem_weights(stem))
