@@ -39,6 +39,7 @@ BN_EPS = 1e-5
 OWN_DGRAD_3X3 = __import__("os").environ.get("DELTA_OWN_DGRAD_3X3", "0") == "1"
 FUSE_STATS_MIN_KDIM = int(__import__("os").environ.get("DELTA_FUSE_STATS_MIN_KDIM", "0"))
 BN_MOMENTUM = 0.1
+_TORCH_OPTIM = __import__("os").environ.get("DELTA_TORCH_OPTIM", "0") == "1"
 
 
 def _ptr(t: torch.Tensor) -> int:
@@ -142,6 +143,15 @@ class Params:
         derived views: two launches (optim.cu).  Grads stay untouched (they
         are what DP all-reduces and tests read)."""
         st = torch.cuda.current_stream().cuda_stream
+        if _TORCH_OPTIM:  # the per-tensor torch sequence the fused kernels replaced (A/B)
+            self.mom.mul_(momentum).add_(self.grad).add_(self.master, alpha=weight_decay)
+            self.master.add_(self.mom, alpha=-lr)
+            self.conv_bf16.copy_(self.master[:self.n_conv])
+            for name, packed in self.stem_packed.items():
+                K.pack_stem_weights(self.wbf[name], packed)
+            for name, wd in self.wd.items():
+                wd.copy_(self.wbf[name].flip(1, 2).permute(3, 1, 2, 0))
+            return
         K.sgd_step(self.master.data_ptr(), self.mom.data_ptr(), self.grad.data_ptr(),
                    self.conv_bf16.data_ptr(), self.numel, self.n_conv, lr, momentum,
                    weight_decay, st)
