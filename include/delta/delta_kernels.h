@@ -49,7 +49,7 @@ delta_status delta_conv_forward(const delta_conv* c, const void* x, void* y, flo
  *       Null pointers are skipped.  (The residual-branch gradient sum.)
  *   DELTA_EPI_BN_BWD: y = g = bf16(acc) * [relu(bn(xc)) > 0] with the saved
  *       statistics (the forward's exact arithmetic), and `stats` receives the
- *       per-tile (sum g, sum g*xc) partials for delta_bn_backward_from_partials.
+ *       per-CTA (sum g, sum g*xc) partial rows for delta_bn_backward_from_partials.
  * Output channels must be a multiple of 32 for the fused modes. */
 enum { DELTA_EPI_STORE = 0, DELTA_EPI_ADD_MASK = 1, DELTA_EPI_BN_BWD = 2 };
 typedef struct delta_conv_epilogue {
@@ -71,10 +71,6 @@ delta_status delta_conv_forward_ex(const delta_conv* c, const void* x, void* y, 
 /* Override the output-channel tile (64, 128 or 256, dividing K).  The fused
  * epilogues (DELTA_EPI_ADD_MASK / DELTA_EPI_BN_BWD) require tile_n <= 128. */
 delta_status delta_conv_set_tile_n(delta_conv* c, int32_t tile_n);
-/* output rows per BN-statistics partial written by delta_conv_forward (128,
- * or rows*Q for 3x3 stride-1 convs, which stage the input halo per tile of
- * whole output rows); pass it to delta_bn_stats_from_partials */
-int32_t delta_conv_stats_rows(const delta_conv* c);
 delta_status delta_conv_geometry(const delta_conv* c, int32_t* P, int32_t* Q, int32_t* kdim,
                                  int32_t* tile_n);
 void delta_conv_destroy(delta_conv* c);
@@ -99,14 +95,16 @@ int64_t delta_bn_workspace_floats(int64_t M, int32_t C);
 delta_status delta_bn_stats(const void* x, int64_t M, int32_t C, float* ws, float* mean,
                             float* invstd, float eps, float* run_mean, float* run_var,
                             float momentum, void* stream);
-/* statistics from the conv epilogue's per-tile partials (rows_per_part = 128);
- * the partials buffer holds delta_stats_partials_floats(M, C, rows_per_part)
- * floats: the epilogue's partials followed by the merge's grouping scratch. */
-int64_t delta_stats_partials_floats(int64_t M, int32_t C, int32_t rows_per_part);
-delta_status delta_bn_stats_from_partials(const float* partials, int64_t M, int32_t C,
-                                          int32_t rows_per_part, float* mean, float* invstd,
-                                          float eps, float* run_mean, float* run_var,
-                                          float momentum, void* stream);
+/* BN statistics from a conv's epilogue partials.  A conv launched with a
+ * `stats` buffer writes one partial row per CTA — delta_stats_parts() rows
+ * (one CTA per SM) of float4 (count, mean, M2) per channel, merged tile by
+ * tile in the CTA's fixed tile order — and one launch reduces the rows in a
+ * fixed order.  The buffer holds delta_stats_partials_floats(C) floats. */
+int32_t delta_stats_parts(void);
+int64_t delta_stats_partials_floats(int32_t C);
+delta_status delta_bn_stats_from_partials(const float* partials, int32_t C, float* mean,
+                                          float* invstd, float eps, float* run_mean,
+                                          float* run_var, float momentum, void* stream);
 /* mode 0 relu(bn(x)), 1 relu(bn(x)+res), 2 relu(bn(x)+bn2(res)) */
 delta_status delta_bn_apply(int32_t mode, const void* x, const void* res, void* y, int64_t M,
                             int32_t C, const float* mean, const float* invstd,
@@ -118,8 +116,8 @@ delta_status delta_bn_backward(const void* up, int32_t pool_hw, const void* mask
                                const float* invstd, const float* gamma, float* dgamma,
                                float* dbeta, float* ws, void* stream);
 /* BN(+ReLU) backward after a DELTA_EPI_BN_BWD conv: `partials` are that
- * conv's per-128-row-tile (sum g, sum g*x) (sized by delta_stats_partials_floats,
- * the tail is scratch), g its masked output.  Writes dgamma, dbeta, dx. */
+ * conv's per-CTA (sum g, sum g*x) rows (delta_stats_partials_floats(C)
+ * floats), g its masked output.  Writes dgamma, dbeta, dx. */
 delta_status delta_bn_backward_from_partials(const float* partials, const void* g, const void* x,
                                              void* dx, int64_t M, int32_t C, const float* mean,
                                              const float* invstd, const float* gamma,

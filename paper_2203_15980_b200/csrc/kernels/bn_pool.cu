@@ -174,6 +174,67 @@ __global__ void __launch_bounds__(256)
   }
 }
 
+// Statistics from the conv epilogues' per-CTA rows (stats_cta.cuh): float4
+// (count, mean, M2) per (CTA, channel), at most a few hundred rows — one warp
+// per channel, lane-strided then a fixed butterfly, so the order is fixed.
+__global__ void __launch_bounds__(256)
+    k_bn_stats_merge_cta(const float4* __restrict__ ws, int parts, int C, float* mean,
+                         float* invstd, float eps, float* rm, float* rv, float mom) {
+  pdl_wait();
+  pdl_trigger();
+  const int c = blockIdx.x * 8 + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (c >= C) return;
+  float s = 0.f, n = 0.f;
+  for (int k = lane; k < parts; k += 32) {
+    const float4 p = ws[int64_t(k) * C + c];
+    s = fmaf(p.x, p.y, s);
+    n += p.x;
+  }
+  n = warp_sum(n);
+  const float mu = warp_sum(s) / n;
+  float m2 = 0.f;
+  for (int k = lane; k < parts; k += 32) {
+    const float4 p = ws[int64_t(k) * C + c];
+    const float d = p.y - mu;
+    m2 += fmaf(p.x, d * d, p.z);
+  }
+  m2 = warp_sum(m2);
+  if (lane == 0) {
+    const float var = m2 / n;
+    mean[c] = mu;
+    invstd[c] = rsqrtf(var + eps);
+    if (rm) {
+      rm[c] = (1.f - mom) * rm[c] + mom * mu;
+      rv[c] = (1.f - mom) * rv[c] + mom * (n > 1.f ? m2 / (n - 1.f) : var);
+    }
+  }
+}
+
+// BN backward reductions from the per-CTA rows (sum g, sum g*xc): dbeta,
+// dgamma per channel, fixed order
+__global__ void __launch_bounds__(256)
+    k_bn_bwd_final_cta(const float4* __restrict__ ws, int parts, int C, const float* mean,
+                       const float* invstd, float* dgamma, float* dbeta) {
+  pdl_wait();
+  pdl_trigger();
+  const int c = blockIdx.x * 8 + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (c >= C) return;
+  float A = 0.f, B = 0.f;
+  for (int k = lane; k < parts; k += 32) {
+    const float4 p = ws[int64_t(k) * C + c];
+    A += p.x;
+    B += p.y;
+  }
+  A = warp_sum(A);
+  B = warp_sum(B);
+  if (lane == 0) {
+    dbeta[c] = A;
+    dgamma[c] = invstd[c] * (B - mean[c] * A);
+  }
+}
+
 // First level of a two-level merge when there are many partials: thread per
 // (channel, group of GROUP consecutive partials) -> one (mean, M2) partial of
 // the group's rows.  The group's partials are loaded up front (one memory
@@ -755,17 +816,24 @@ cudaError_t bn_stats(const void* x, int64_t M, int C, float* ws, float* mean, fl
                         rm, rv, mom, st);
 }
 
-int64_t stats_partials_floats(int64_t M, int C, int rows_per_part) {
-  const int64_t parts = (M + rows_per_part - 1) / rows_per_part;
-  return 2 * (parts + (parts + GROUP - 1) / GROUP) * C;
+int stats_parts() {
+  static int n = 0;
+  if (!n) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (n <= 0) n = 148;
+  }
+  return n;
 }
 
-cudaError_t bn_stats_from_partials(const float* partials, int64_t M, int C, int rows_per_part,
-                                   float* mean, float* invstd, float eps, float* rm, float* rv,
-                                   float mom, cudaStream_t st) {
-  const int parts = int((M + rows_per_part - 1) / rows_per_part);
-  return merge_partials(reinterpret_cast<const float2*>(partials), parts, rows_per_part, M, C, mean,
-                        invstd, eps, rm, rv, mom, st);
+int64_t stats_partials_floats(int C) { return int64_t(stats_parts()) * C * 4; }
+
+cudaError_t bn_stats_from_partials(const float* partials, int C, float* mean, float* invstd,
+                                   float eps, float* rm, float* rv, float mom, cudaStream_t st) {
+  return launch_k(k_bn_stats_merge_cta, dim3((C + 7) / 8), dim3(256), 0, st,
+                  reinterpret_cast<const float4*>(partials), stats_parts(), C, mean, invstd, eps,
+                  rm, rv, mom);
 }
 
 cudaError_t bn_apply(int mode, const void* x, const void* res, void* y, int64_t M, int C,
@@ -822,25 +890,20 @@ cudaError_t bn_backward(const void* up, int pool_hw, const void* mask, const voi
   return cudaGetLastError();
 }
 
-cudaError_t bn_backward_from_partials(const float* partials, int rows_per_part, const void* g,
-                                      const void* x, void* dx, int64_t M, int C,
-                                      const float* mean, const float* invstd, const float* gamma,
-                                      float* dgamma, float* dbeta, cudaStream_t st) {
+cudaError_t bn_backward_from_partials(const float* partials, const void* g, const void* x,
+                                      void* dx, int64_t M, int C, const float* mean,
+                                      const float* invstd, const float* gamma, float* dgamma,
+                                      float* dbeta, cudaStream_t st) {
   if (C % SLICE || (C & (C - 1)) || C > 2048) return cudaErrorInvalidValue;
-  auto ws = reinterpret_cast<const float2*>(partials);
-  int parts = int((M + rows_per_part - 1) / rows_per_part);
-  if (parts > 2 * GROUP) {
-    const int groups = (parts + GROUP - 1) / GROUP;
-    float2* out = const_cast<float2*>(ws) + int64_t(parts) * C;
-    const int bx = C < 256 ? C : 256;
-    if (cudaError_t e_ = launch_k(k_bn_bwd_group, dim3(dim3((C + bx - 1) / bx, groups)), dim3(bx), 0, st, ws, parts, C, out)) return e_;
-    ws = out;
-    parts = groups;
-  }
-  if (cudaError_t e_ = launch_k(k_bn_bwd_final_raw, dim3((C + 7) / 8), dim3(256), 0, st, ws, parts, C, mean, invstd, dgamma, dbeta)) return e_;
+  if (cudaError_t e_ = launch_k(k_bn_bwd_final_cta, dim3((C + 7) / 8), dim3(256), 0, st,
+                                reinterpret_cast<const float4*>(partials), stats_parts(), C, mean,
+                                invstd, dgamma, dbeta))
+    return e_;
   const int64_t vecs = M * C / 8;
-  if (cudaError_t e_ = launch_k(k_bn_bwd_apply<false, false>, dim3(grid_for(vecs, 256)), dim3(256), 0, st, static_cast<const bf16*>(g), 0, nullptr, static_cast<const bf16*>(x), static_cast<bf16*>(dx), vecs, C - 1, __builtin_ctz(C), M, mean, invstd, gamma, dgamma, dbeta)) return e_;
-  return cudaGetLastError();
+  return launch_k(k_bn_bwd_apply<false, false>, dim3(grid_for(vecs, 256)), dim3(256), 0, st,
+                  static_cast<const bf16*>(g), 0, nullptr, static_cast<const bf16*>(x),
+                  static_cast<bf16*>(dx), vecs, C - 1, __builtin_ctz(C), M, mean, invstd, gamma,
+                  dgamma, dbeta);
 }
 
 cudaError_t add_grad(const void* a, const void* up, int pool_hw, const void* up_mask,

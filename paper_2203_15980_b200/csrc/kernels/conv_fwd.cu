@@ -38,6 +38,7 @@
 #include "kernels/kernels.hpp"
 #include "kernels/launch.hpp"
 #include "kernels/sm100_common.cuh"
+#include "kernels/stats_cta.cuh"
 #include "kernels/tma_host.hpp"
 
 namespace delta_k {
@@ -91,8 +92,8 @@ struct ConvArgs {
   int taps;     // R*S
   int n_tiles;  // ceil(K / BN)
   int tiles;    // m_tiles * n_tiles
-  float2* stats;  // optional per (m_tile, channel) partials: EPI_STORE (mean, M2) of the
-                  // bf16 outputs; EPI_BN_BWD (sum g, sum g*xc) of the gradients
+  float4* stats;  // optional per-CTA partials [grid][K] (stats_cta.cuh): EPI_STORE (count,
+                  // mean, M2) of the bf16 outputs; EPI_BN_BWD (sum g, sum g*xc)
   ConvEpilogue e;
 };
 
@@ -533,6 +534,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     };
     if constexpr (FUSED && !OPT)
       for (uint32_t e = 0; e + 1 < NSLOTS; ++e) prefetch(e);
+    if (a.stats != nullptr) stats_row_zero(a.stats, a.K, BN, (warp - 4) * 32 + lane, EPI_W * 32);
     uint32_t ec = 0;  // chunks consumed by this warp
     uint32_t lt = 0;
     for (int tile = blockIdx.x; tile < a.tiles; tile += gridDim.x, ++lt) {
@@ -678,7 +680,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         if constexpr (EV == EV_BN_BWD) __syncwarp();  // ring slot read by the stats pass
       }
       if (a.stats != nullptr) {
-        // combine the four row quarters -> one partial per channel per tile
+        // combine the four row quarters -> this tile's column partials, folded
+        // into the CTA's row of the statistics table
         asm volatile("bar.sync 1, %0;" ::"n"(EPI_W * 32) : "memory");
         const int et = (warp - 4) * 32 + lane;
         const int n_rows = row_tiled(MODE) ? a.Q : min(BM, a.M - m0);
@@ -689,16 +692,8 @@ __global__ void __launch_bounds__(kThreads, 1)
             S += red[qq * BN + c].x;
             Q += red[qq * BN + c].y;
           }
-          if (n0 + c < a.K) {
-            float2 out;
-            if (EV == EV_BN_BWD) {
-              out = make_float2(S, Q);
-            } else {
-              const float mu = S / float(n_rows);
-              out = make_float2(mu, fmaxf(Q - S * mu, 0.f));
-            }
-            a.stats[size_t(tile / a.n_tiles) * a.K + n0 + c] = out;
-          }
+          if (n0 + c < a.K)
+            stats_merge_tile<EV == EV_BN_BWD>(a.stats, a.K, n0 + c, float(n_rows), S, Q);
         }
         asm volatile("bar.sync 1, %0;" ::"n"(EPI_W * 32) : "memory");
       }
@@ -956,7 +951,7 @@ cudaError_t launch(const ConvPlan& cp, const void* x, void* y, float* stats,
   a.taps = cp.R * cp.S;
   a.n_tiles = (cp.K + BN - 1) / BN;
   a.tiles = (row_tiled(MODE) ? cp.N * cp.P : (a.M + BM - 1) / BM) * a.n_tiles;
-  a.stats = reinterpret_cast<float2*>(stats);
+  a.stats = reinterpret_cast<float4*>(stats);
   a.e = epi;
   alignas(64) CUtensorMap amap;
   alignas(64) CUtensorMap ymap;
@@ -986,7 +981,8 @@ cudaError_t launch(const ConvPlan& cp, const void* x, void* y, float* stats,
                      CU_TENSOR_MAP_SWIZZLE_64B))
       return cudaErrorInvalidValue;
   }
-  const int grid = a.tiles < num_sms() ? a.tiles : num_sms();
+  // statistics come as one partial row per CTA: always one CTA per SM then
+  const int grid = (stats != nullptr || a.tiles > num_sms()) ? num_sms() : a.tiles;
   if (cudaError_t e_ = launch_k(kern, dim3(grid), dim3(kThreads), smem, st, *reinterpret_cast<const CUtensorMap*>(cp.wmap), amap, ymap, emap0, emap1, a)) return e_;
   return cudaGetLastError();
 }

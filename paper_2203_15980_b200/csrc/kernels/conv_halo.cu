@@ -26,6 +26,7 @@
 #include "kernels/kernels.hpp"
 #include "kernels/launch.hpp"
 #include "kernels/sm100_common.cuh"
+#include "kernels/stats_cta.cuh"
 #include "kernels/tma_host.hpp"
 
 namespace delta_k {
@@ -45,7 +46,7 @@ struct HaloArgs {
   int m_tiles;        // N * tiles_per_img
   int n_tiles, tiles;
   int kc;             // C / 64 channel blocks
-  float2* stats;      // optional: per (m tile, channel) (mean, M2) of the rows*W valid outputs
+  float4* stats;      // optional: per-CTA (count, mean, M2) rows [grid][K] (stats_cta.cuh)
 };
 
 __device__ __forceinline__ uint8_t* align1024(uint8_t* p) {
@@ -154,6 +155,7 @@ __global__ void __launch_bounds__(HT, 1)
     const int quarter = warp & 3;
     const int qpx = a.slot < 32 ? a.slot : 32;  // pixels per store row
     const int qrows = 32 / qpx;                 // image rows per 32-row chunk
+    if (a.stats != nullptr) stats_row_zero(a.stats, a.K, BN, (warp - 4) * 32 + lane, 128);
     uint32_t lt = 0;
     for (int tile = blockIdx.x; tile < a.tiles; tile += gridDim.x, ++lt) {
       const int mt = tile / a.n_tiles, n0 = (tile % a.n_tiles) * BN;
@@ -220,9 +222,7 @@ __global__ void __launch_bounds__(HT, 1)
             S += red[qq * BN + c].x;
             Qs += red[qq * BN + c].y;
           }
-          const float mu = S / n_rows;
-          if (n0 + c < a.K)
-            a.stats[size_t(mt) * a.K + n0 + c] = make_float2(mu, fmaxf(Qs - S * mu, 0.f));
+          if (n0 + c < a.K) stats_merge_tile<false>(a.stats, a.K, n0 + c, n_rows, S, Qs);
         }
         asm volatile("bar.sync 1, 128;" ::: "memory");
       }
@@ -311,7 +311,7 @@ cudaError_t halo_launch(const ConvPlan& cp, const void* x, void* y, float* stats
   a.n_tiles = (cp.K + BN - 1) / BN;
   a.tiles = a.m_tiles * a.n_tiles;
   a.kc = cp.C / 64;
-  a.stats = reinterpret_cast<float2*>(stats);
+  a.stats = reinterpret_cast<float4*>(stats);
   // input: 4-D [N][H][W][C], box {64 ch, slot px, rows+2 rows, 1}, 128B swizzle
   alignas(64) CUtensorMap xmap, ymap;
   {
@@ -341,7 +341,7 @@ cudaError_t halo_launch(const ConvPlan& cp, const void* x, void* y, float* stats
   int dev = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const int grid = a.tiles < sms ? a.tiles : sms;
+  const int grid = (stats != nullptr || a.tiles > sms) ? sms : a.tiles;
   if (cudaError_t e_ = launch_k(kern, dim3(grid), dim3(HT), smem, st, *reinterpret_cast<const CUtensorMap*>(cp.wmap), xmap, ymap, a)) return e_;
   return cudaGetLastError();
 }

@@ -47,11 +47,6 @@ bool conv_halo_default(const ConvPlan& cp);  // the shapes it is dispatched for 
 void conv_halo_shape(ConvPlan* cp);
 cudaError_t conv_halo_forward(const ConvPlan& cp, const void* x, void* y, float* stats,
                               cudaStream_t st);
-// output rows per BN-statistics partial (128, rows*Q for the halo path, Q
-// for the row-tiled stem)
-inline int conv_stats_rows(const ConvPlan& cp) {
-  return cp.halo ? cp.halo_rows * cp.Q : (cp.stem_rows ? cp.Q : 128);
-}
 // choose the N tile (64/128/256, dividing K; fused epilogues need <= 128)
 int conv_plan_set_tile_n(ConvPlan* cp, int bn, const void* w);
 // stats (optional, nullptr = off): [ceil(M/128)][K] float2 (mean, M2) of the
@@ -81,14 +76,15 @@ cudaError_t wgrad(const WgradPlan& wp, const void* dy, const void* x, float* dw,
 int64_t bn_workspace_floats(int64_t M, int C);
 cudaError_t bn_stats(const void* x, int64_t M, int C, float* ws, float* mean, float* invstd,
                      float eps, float* run_mean, float* run_var, float momentum, cudaStream_t st);
-// Finish BN statistics from per-tile (mean, M2) partials of `rows_per_part`
-// rows each (the conv epilogue's), merged in a fixed order.  `partials` holds
-// stats_partials_floats(M, C, rows_per_part) floats (the partials, then the
-// grouping pass's scratch).
-int64_t stats_partials_floats(int64_t M, int C, int rows_per_part);
-cudaError_t bn_stats_from_partials(const float* partials, int64_t M, int C, int rows_per_part,
-                                   float* mean, float* invstd, float eps, float* run_mean,
-                                   float* run_var, float momentum, cudaStream_t st);
+// Finish BN statistics from the conv epilogue's per-CTA partial rows
+// (stats_cta.cuh: stats_parts() rows of float4 (count, mean, M2) per channel),
+// merged in a fixed order by one launch.  `partials` holds
+// stats_partials_floats(C) floats.
+int stats_parts();
+int64_t stats_partials_floats(int C);
+cudaError_t bn_stats_from_partials(const float* partials, int C, float* mean, float* invstd,
+                                   float eps, float* run_mean, float* run_var, float momentum,
+                                   cudaStream_t st);
 
 // mode 0: y = relu(bn(x)); 1: y = relu(bn(x) + res); 2: y = relu(bn(x) + bn2(res))
 cudaError_t bn_apply(int mode, const void* x, const void* res, void* y, int64_t M, int C,
@@ -106,13 +102,13 @@ cudaError_t bn_backward(const void* up, int pool_hw, const void* mask, const voi
                         cudaStream_t st);
 
 // BN(+ReLU) backward whose reductions were fused into the producing conv's
-// EPI_BN_BWD epilogue: `partials` = per-tile (sum g, sum g*x) of g (already
-// masked), sized stats_partials_floats(M, C, rows_per_part).  Writes dgamma,
-// dbeta and dx = BN-backward(g, x).
-cudaError_t bn_backward_from_partials(const float* partials, int rows_per_part, const void* g,
-                                      const void* x, void* dx, int64_t M, int C,
-                                      const float* mean, const float* invstd, const float* gamma,
-                                      float* dgamma, float* dbeta, cudaStream_t st);
+// EPI_BN_BWD epilogue: `partials` = per-CTA rows (sum g, sum g*x) of g (already
+// masked), sized stats_partials_floats(C).  Writes dgamma, dbeta and
+// dx = BN-backward(g, x).
+cudaError_t bn_backward_from_partials(const float* partials, const void* g, const void* x,
+                                      void* dx, int64_t M, int C, const float* mean,
+                                      const float* invstd, const float* gamma, float* dgamma,
+                                      float* dbeta, cudaStream_t st);
 
 // out = (a + g) * [out_mask > 0], g = up * [up_mask > 0] (up full or pooled as
 // above; a null mask means no masking)

@@ -128,7 +128,7 @@ delta_status run_kop(delta_rt* rt, const delta_kop& k, Frame& fr, uint64_t node,
                             k.f[1], st);
       break;
     case DELTA_K_BN_STATS_PARTS:
-      e = delta_k::bn_stats_from_partials(rp<const float>(fr, r[0]), i[0], int(i[1]), int(i[2]),
+      e = delta_k::bn_stats_from_partials(rp<const float>(fr, r[0]), int(i[1]),
                                           rp<float>(fr, r[2]), rp<float>(fr, r[3]), k.f[0],
                                           rp<float>(fr, r[4]), rp<float>(fr, r[5]), k.f[1], st);
       break;
@@ -146,7 +146,7 @@ delta_status run_kop(delta_rt* rt, const delta_kop& k, Frame& fr, uint64_t node,
                                rp<float>(fr, r[7]), rp<float>(fr, r[8]), rp<float>(fr, r[9]), st);
       break;
     case DELTA_K_BN_BWD_PARTS:
-      e = delta_k::bn_backward_from_partials(rp<const float>(fr, r[0]), 128, ref(fr, r[1]),
+      e = delta_k::bn_backward_from_partials(rp<const float>(fr, r[0]), ref(fr, r[1]),
                                              ref(fr, r[2]), ref(fr, r[3]), i[1], int(i[2]),
                                              rp<const float>(fr, r[4]), rp<const float>(fr, r[5]),
                                              rp<const float>(fr, r[6]), rp<float>(fr, r[7]),

@@ -123,7 +123,6 @@ delta_status delta_conv_set_tile_n(delta_conv* c, int32_t tile_n) {
   return rc == 1 ? DELTA_E_UNSUPPORTED : DELTA_E_CUDA;
 }
 
-int32_t delta_conv_stats_rows(const delta_conv* c) { return delta_k::conv_stats_rows(c->plan); }
 
 delta_status delta_conv_geometry(const delta_conv* c, int32_t* P, int32_t* Q, int32_t* kdim,
                                  int32_t* tile_n) {
@@ -145,17 +144,16 @@ delta_status delta_bn_stats(const void* x, int64_t M, int32_t C, float* ws, floa
                      "bn_stats");
 }
 
-int64_t delta_stats_partials_floats(int64_t M, int32_t C, int32_t rows_per_part) {
-  return delta_k::stats_partials_floats(M, C, rows_per_part);
-}
+int32_t delta_stats_parts(void) { return delta_k::stats_parts(); }
 
-delta_status delta_bn_stats_from_partials(const float* partials, int64_t M, int32_t C,
-                                          int32_t rows_per_part, float* mean, float* invstd,
-                                          float eps, float* rm, float* rv, float mom,
-                                          void* stream) {
-  return cuda_status(delta_k::bn_stats_from_partials(partials, M, C, rows_per_part, mean, invstd,
-                                                     eps, rm, rv, mom, S(stream)),
-                     "bn_stats_from_partials");
+int64_t delta_stats_partials_floats(int32_t C) { return delta_k::stats_partials_floats(C); }
+
+delta_status delta_bn_stats_from_partials(const float* partials, int32_t C, float* mean,
+                                          float* invstd, float eps, float* rm, float* rv,
+                                          float mom, void* stream) {
+  return cuda_status(
+      delta_k::bn_stats_from_partials(partials, C, mean, invstd, eps, rm, rv, mom, S(stream)),
+      "bn_stats_from_partials");
 }
 
 delta_status delta_sgd_step(float* w, float* mom, const float* g, void* wbf, int64_t n,
@@ -193,7 +191,7 @@ delta_status delta_bn_backward_from_partials(const float* partials, const void* 
                                              void* dx, int64_t M, int32_t C, const float* mean,
                                              const float* invstd, const float* gamma,
                                              float* dgamma, float* dbeta, void* stream) {
-  return cuda_status(delta_k::bn_backward_from_partials(partials, 128, g, x, dx, M, C, mean, invstd,
+  return cuda_status(delta_k::bn_backward_from_partials(partials, g, x, dx, M, C, mean, invstd,
                                                         gamma, dgamma, dbeta, S(stream)),
                      "bn_backward_from_partials");
 }

@@ -13,11 +13,11 @@ P = C.POINTER
 _SIGS = {
     "delta_conv_create": (i32, [i32] * 9 + [vp, P(vp)]),
     "delta_conv_forward": (i32, [vp, vp, vp, vp, vp]),
-    "delta_stats_partials_floats": (i64, [i64, i32, i32]),
-    "delta_bn_stats_from_partials": (i32, [vp, i64, i32, i32, vp, vp, f32, vp, vp, f32, vp]),
+    "delta_stats_parts": (i32, []),
+    "delta_stats_partials_floats": (i64, [i32]),
+    "delta_bn_stats_from_partials": (i32, [vp, i32, vp, vp, f32, vp, vp, f32, vp]),
     "delta_conv_forward_ex": (i32, [vp, vp, vp, vp, vp, vp]),
     "delta_conv_set_tile_n": (i32, [vp, i32]),
-    "delta_conv_stats_rows": (i32, [vp]),
     "delta_wgrad_create": (i32, [i32] * 9 + [P(vp)]),
     "delta_wgrad_workspace_bytes": (u64, [vp]),
     "delta_wgrad_run": (i32, [vp, vp, vp, vp, vp, vp]),
@@ -84,11 +84,10 @@ class Conv:
         lib.delta_conv_geometry(self._h, C.byref(p), C.byref(q), C.byref(kd), C.byref(tn))
         self.P, self.Q, self.kdim, self.tile_n = p.value, q.value, kd.value, tn.value
         self.shape = (N, H, W, Cin, K, R, S, stride, pad)
-        # output rows per BN-statistics partial of the fused epilogue
-        self.stats_rows = int(lib.delta_conv_stats_rows(self._h))
 
     def __call__(self, x_ptr: int, y_ptr: int, stream: int, stats_ptr: int | None = None):
-        """stats_ptr: optional [ceil(M/128)][K] float2 BN-statistics partials."""
+        """stats_ptr: optional BN-statistics partials, stats_partials_floats(K) floats
+        (one (count, mean, M2) row per CTA)."""
         check(lib.delta_conv_forward(self._h, x_ptr, y_ptr, stats_ptr, stream))
         _count(1)
 
@@ -136,30 +135,6 @@ class Wgrad:
             self._h = None
 
 
-def conv_stats_rows(N, H, W, Cin, K, R, S, stride, pad) -> int:
-    """Output rows per BN-statistics partial of a conv (mirrors kernels.hpp
-    conv_stats_rows: the 3x3 stride-1 64->64 convs stage the input halo per
-    tile of whole output rows (conv_halo.cu), the stem is tiled by output row,
-    everything else: 128)."""
-    import os
-    env = os.environ.get("DELTA_CONV_HALO")
-    P = (H + 2 * pad - R) // stride + 1
-    if Cin == 4:  # the row-tiled stem (conv_fwd.cu MODE_STEMRAW): one partial per output row
-        Q = (W + 2 * pad - S) // stride + 1
-        if K <= 64 and 4 <= Q <= 124 and not os.environ.get("DELTA_STEM_MODE"):
-            return Q
-        return 128
-    if not (R == 3 and S == 3 and stride == 1 and pad == 1 and Cin % 64 == 0 and W <= 64):
-        return 128
-    if env == "0" or os.environ.get("DELTA_CONV_GATHER") == "1" or (env is None and not (Cin == 64 and K == 64)):
-        return 128
-    slot = 16 if W + 2 <= 16 else (32 if W + 2 <= 32 else 64)
-    for rows in range(128 // slot, 0, -1):
-        if P % rows == 0 and (rows + 2) * slot * 128 <= 32768:
-            return rows * W
-    return 128
-
-
 STEM_KDIM = 256
 
 
@@ -201,15 +176,19 @@ def bn_stats(x, M, C_, ws, mean, invstd, eps, run_mean, run_var, momentum, strea
     _count(1 + _merge_launches(_chunks(M, C_)))
 
 
-def stats_partials_floats(M: int, C_: int, rows_per_part: int = 128) -> int:
-    return lib.delta_stats_partials_floats(M, C_, rows_per_part)
+def stats_parts() -> int:
+    """Partial rows a conv epilogue writes (one per CTA = one per SM)."""
+    return int(lib.delta_stats_parts())
 
 
-def bn_stats_from_partials(partials, M, C_, mean, invstd, eps, run_mean, run_var, momentum,
-                           stream, rows_per_part=128):
-    check(lib.delta_bn_stats_from_partials(partials, M, C_, rows_per_part, mean, invstd, eps,
-                                           run_mean, run_var, momentum, stream))
-    _count(_merge_launches((M + rows_per_part - 1) // rows_per_part))
+def stats_partials_floats(C_: int) -> int:
+    return int(lib.delta_stats_partials_floats(C_))
+
+
+def bn_stats_from_partials(partials, C_, mean, invstd, eps, run_mean, run_var, momentum, stream):
+    check(lib.delta_bn_stats_from_partials(partials, C_, mean, invstd, eps, run_mean, run_var,
+                                           momentum, stream))
+    _count(1)
 
 
 def bn_apply(mode, x, res, y, M, C_, mean, invstd, gamma, beta, mean2=None, invstd2=None,
@@ -251,7 +230,7 @@ def bn_backward_from_partials(partials, g, x, dx, M, C_, mean, invstd, gamma, dg
                               stream):
     check(lib.delta_bn_backward_from_partials(partials, g, x, dx, M, C_, mean, invstd, gamma,
                                               dgamma, dbeta, stream))
-    _count(1 + _merge_launches((M + 127) // 128))
+    _count(2)
 
 
 def add_grad(a, up, pool_hw, up_mask, out_mask, out, M, C_, stream):

@@ -169,13 +169,8 @@ def workspace_plan(g: G.Graph) -> dict:
     ws = {}
     ws["bn_ws"] = 4 * max(K.bn_workspace_floats(M(n), n.shape[-1]) for n in nodes
                           if len(n.shape) == 4 and n.shape[-1] % 64 == 0)
-    def stats_rows(n):
-        if n.op != "conv":
-            return 128
-        cs = g.convs[n.attrs["conv"]]
-        Nb, H, W, Cin = nodes[n.parents[0]].shape
-        return K.conv_stats_rows(Nb, H, W, Cin, cs.cout, cs.k, cs.k, cs.stride, cs.pad)
-    parts = 4 * max(K.stats_partials_floats(M(n), n.shape[-1], stats_rows(n)) for n in nodes
+    # BN-statistics partials: one (count, mean, M2) row per CTA of the conv
+    parts = 4 * max(K.stats_partials_floats(n.shape[-1]) for n in nodes
                     if n.op in ("conv", "conv_bn_relu_bwd"))
     ws["stats_main"] = ws["stats_ds"] = parts
     short = [nodes[n.parents[2]].nbytes * g.convs[n.attrs["conv_short"]].cin
@@ -294,8 +289,6 @@ class DeltaRuntime:
                 assert (conv.P, conv.Q) == n.shape[1:3], (n.name, conv.P, conv.Q, n.shape)
                 self._convs[n.name] = conv
                 self._fuse_stats[n.name] = conv.kdim >= FUSE_STATS_MIN_KDIM
-                assert conv.stats_rows == K.conv_stats_rows(Nb, H, W, C, cs.cout, cs.k, cs.k,
-                                                            cs.stride, cs.pad), n.name
                 self._wgrads[cs.name] = K.Wgrad(Nb, H, W, C, cs.cout, cs.k, cs.k, cs.stride,
                                                 cs.pad)
                 if own_dgrad(cs):
@@ -396,10 +389,8 @@ class DeltaRuntime:
             tail = (_ptr(pr.bn_mean[bn]), _ptr(pr.bn_invstd[bn]), _ptr(pr.bn_rmean[bn]),
                     _ptr(pr.bn_rvar[bn]))
             if self._fuse_stats.get(conv.name):
-                rows = self._convs[conv.name].stats_rows
-                add(X.kop(X.K_BN_STATS_PARTS, (_ptr(scratch), None) + tail, (M, C, rows),
-                          (BN_EPS, BN_MOMENTUM), flags=X.FIRST_ONLY),
-                    K._merge_launches((M + rows - 1) // rows), 0)
+                add(X.kop(X.K_BN_STATS_PARTS, (_ptr(scratch), None) + tail, (M, C, 0),
+                          (BN_EPS, BN_MOMENTUM), flags=X.FIRST_ONLY), 1, 0)
             else:
                 add(X.kop(X.K_BN_STATS, (src_ref, _ptr(self.bn_ws)) + tail, (M, C),
                           (BN_EPS, BN_MOMENTUM), flags=X.FIRST_ONLY),
@@ -482,8 +473,7 @@ class DeltaRuntime:
                                         X.IN(2)) + bnp(bn) + gb(bn),
                           (K.EPI_BN_BWD, 0, 0), conv=self._dconvs[conv]._h))
                 add(X.kop(X.K_BN_BWD_PARTS, (_ptr(self.stats_main), X.OUT(), X.IN(2), X.OUT())
-                          + bnp(bn) + (gb(bn)[0],) + dgb(bn), (0, M, C)),
-                    1 + K._merge_launches((M + 127) // 128), 0)
+                          + bnp(bn) + (gb(bn)[0],) + dgb(bn), (0, M, C)), 2, 0)
             else:
                 # cuDNN input gradient (3x3) -> SCRATCH(0)
                 dg = host(self._dgrad_op(conv, node.parents[0], node.parents[1]))

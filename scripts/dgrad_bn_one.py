@@ -17,7 +17,7 @@ y = torch.empty(N, H, H, C, device="cuda", dtype=torch.bfloat16)
 a = torch.randn(N, H, H, C, device="cuda").to(torch.bfloat16)
 mean = torch.zeros(C, device="cuda"); inv = torch.ones(C, device="cuda")
 gam = torch.ones(C, device="cuda"); bet = torch.zeros(C, device="cuda")
-parts = torch.empty(K.stats_partials_floats(M, C), device="cuda")
+parts = torch.empty(K.stats_partials_floats(C), device="cuda")
 st = torch.cuda.current_stream().cuda_stream
 for _ in range(4):
     conv.bn_bwd(dy.data_ptr(), y.data_ptr(), parts.data_ptr(), a.data_ptr(), mean.data_ptr(),

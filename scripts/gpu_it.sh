@@ -1,1 +1,4 @@
-for m in 0 1 0 1; do DELTA_TORCH_OPTIM=$m timeout 900 python bench.py --cpu-sample-s 1 > gpurun_out/bench.log 2>&1; echo -n "TORCH_OPTIM=$m "; tail -1 gpurun_out/bench.log | python -c "import json,sys; d=json.loads(sys.stdin.read()); print(d['value'], d['no_eviction']['images_per_s'], d['e2e']['value'])"; done
+mkdir -p gpurun_out
+timeout 600 python -m pytest tests -x -q -m gpu 2>&1 | tail -3
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" 2>&1 | tail -1 | cut -c1-200
+for i in 1 2; do timeout 900 python bench.py --cpu-sample-s 1 > gpurun_out/bench.log 2>&1; tail -1 gpurun_out/bench.log | python -c "import json,sys; d=json.loads(sys.stdin.read()); print(d['value'], d['no_eviction']['images_per_s'], d['e2e']['value'], d['gpu_launches'])"; done

@@ -38,7 +38,7 @@ for (H, C, Ko, R) in shapes:
     m = torch.randn(N, H, H, C, device="cuda").to(torch.bfloat16)
     mean = torch.zeros(C, device="cuda"); inv = torch.ones(C, device="cuda")
     gam = torch.ones(C, device="cuda"); bet = torch.zeros(C, device="cuda")
-    parts = torch.empty(K.stats_partials_floats(M, C), device="cuda")
+    parts = torch.empty(K.stats_partials_floats(C), device="cuda")
     t_plain = timeit(lambda: conv(dy.data_ptr(), y.data_ptr(), st))
     t_add = timeit(lambda: conv.add_mask(dy.data_ptr(), y.data_ptr(), st, add=a.data_ptr(), out_mask=m.data_ptr()))
     t_bn = timeit(lambda: conv.bn_bwd(dy.data_ptr(), y.data_ptr(), parts.data_ptr(), a.data_ptr(), mean.data_ptr(), inv.data_ptr(), gam.data_ptr(), bet.data_ptr(), st))

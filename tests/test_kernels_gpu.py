@@ -61,12 +61,11 @@ def test_conv_fwd_matches_fp32_reference(case):
     # bitwise-identical recompute, and BN statistics fused in the epilogue
     y2 = torch.empty_like(y)
     M = N * conv.P * conv.Q
-    assert conv.stats_rows == K.conv_stats_rows(N, H, W, Cin, Kout, R, R, st, pad)
-    parts = torch.empty(K.stats_partials_floats(M, Kout, conv.stats_rows), device="cuda")
+    parts = torch.full((K.stats_partials_floats(Kout),), float("nan"), device="cuda")
     conv(x.data_ptr(), y2.data_ptr(), _stream(), parts.data_ptr())
     mean = torch.empty(Kout, device="cuda"); inv = torch.empty(Kout, device="cuda")
-    K.bn_stats_from_partials(parts.data_ptr(), M, Kout, mean.data_ptr(), inv.data_ptr(), 1e-5,
-                             None, None, 0.1, _stream(), rows_per_part=conv.stats_rows)
+    K.bn_stats_from_partials(parts.data_ptr(), Kout, mean.data_ptr(), inv.data_ptr(), 1e-5,
+                             None, None, 0.1, _stream())
     torch.cuda.synchronize()
     assert torch.equal(y, y2)
     yf = y.float().reshape(M, Kout)
@@ -99,13 +98,12 @@ def test_conv_stem_packed_c4(N, H, W):
     # BN statistics from the epilogue partials (one partial per output row on
     # the row-tiled path) match the statistics of the stored bf16 output
     M = N * conv.P * conv.Q
-    assert conv.stats_rows == K.conv_stats_rows(N, H, W, 4, Kout, 7, 7, 2, 3)
-    parts = torch.empty(K.stats_partials_floats(M, Kout, conv.stats_rows), device="cuda")
+    parts = torch.full((K.stats_partials_floats(Kout),), float("nan"), device="cuda")
     y3 = torch.empty_like(y)
     conv(x.data_ptr(), y3.data_ptr(), _stream(), parts.data_ptr())
     mean = torch.empty(Kout, device="cuda"); inv = torch.empty(Kout, device="cuda")
-    K.bn_stats_from_partials(parts.data_ptr(), M, Kout, mean.data_ptr(), inv.data_ptr(), 1e-5,
-                             None, None, 0.1, _stream(), rows_per_part=conv.stats_rows)
+    K.bn_stats_from_partials(parts.data_ptr(), Kout, mean.data_ptr(), inv.data_ptr(), 1e-5,
+                             None, None, 0.1, _stream())
     torch.cuda.synchronize()
     assert torch.equal(y, y3)
     yf = y.float().reshape(M, Kout)
@@ -329,7 +327,7 @@ def test_dgrad_bn_backward_epilogue(case):
     plain = torch.empty(N, H, W, C, device="cuda", dtype=torch.bfloat16)
     conv(dy.data_ptr(), plain.data_ptr(), _stream())
     gbuf = torch.empty_like(plain)
-    parts = torch.empty(K.stats_partials_floats(M, C), device="cuda")
+    parts = torch.full((K.stats_partials_floats(C),), float("nan"), device="cuda")
     conv.bn_bwd(dy.data_ptr(), gbuf.data_ptr(), parts.data_ptr(), xc.data_ptr(), mean.data_ptr(),
                 invstd.data_ptr(), gamma.data_ptr(), beta.data_ptr(), _stream())
     torch.cuda.synchronize()
