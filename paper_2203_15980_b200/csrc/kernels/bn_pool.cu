@@ -12,6 +12,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdlib>
 
 #include "kernels/kernels.hpp"
 #include "kernels/launch.hpp"
@@ -241,6 +242,16 @@ __global__ void __launch_bounds__(256)
 // round trip, not GROUP dependent ones), then two passes over registers
 // (sum -> mean, then M2) in a fixed order.
 constexpr int GROUP = 16;
+// a grouping pass only above this many partials: the streaming passes write
+// ~148*8 chunk partials, which one warp per channel reduces directly (~2 us)
+// faster than a second launch would
+int group_above() {
+  static const int v = [] {
+    const char* e = std::getenv("DELTA_BN_GROUP_ABOVE");
+    return e ? std::atoi(e) : 4096;
+  }();
+  return v;
+}
 __global__ void __launch_bounds__(256)
     k_bn_stats_group(const float2* __restrict__ ws, int parts, int64_t rows_per, int64_t M, int C,
                      float2* __restrict__ out) {
@@ -792,7 +803,7 @@ namespace {
 cudaError_t merge_partials(const float2* ws, int parts, int64_t rows_per, int64_t M, int C,
                            float* mean, float* invstd, float eps, float* rm, float* rv, float mom,
                            cudaStream_t st) {
-  if (parts > 2 * GROUP) {
+  if (parts > group_above()) {
     const int groups = (parts + GROUP - 1) / GROUP;
     float2* out = const_cast<float2*>(ws) + int64_t(parts) * C;
     const int bx = C < 256 ? C : 256;
@@ -874,7 +885,7 @@ cudaError_t bn_backward(const void* up, int pool_hw, const void* mask, const voi
   if (cudaError_t e_ = launch_k(part, dim3(chunks), dim3(256), 0, st, U, pool_hw, Mk, X, M, C, chunk, mean, invstd, reinterpret_cast<float2*>(ws))) return e_;
   const float2* w2 = reinterpret_cast<const float2*>(ws);
   int parts = chunks;
-  if (parts > 2 * GROUP) {  // two-level fixed-order sum (scratch after the partials)
+  if (parts > group_above()) {  // two-level fixed-order sum (scratch after the partials)
     const int groups = (parts + GROUP - 1) / GROUP;
     float2* out = reinterpret_cast<float2*>(ws) + int64_t(parts) * C;
     const int bx = C < 256 ? C : 256;

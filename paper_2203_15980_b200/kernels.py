@@ -160,8 +160,8 @@ def bn_workspace_floats(M: int, C_: int) -> int:
 
 def _merge_launches(parts: int) -> int:
     """Launches of a fixed-order partials merge (bn_pool.cu merge_partials /
-    bn_backward*): a grouping pass above 2*GROUP = 32 partials."""
-    return 2 if parts > 32 else 1
+    bn_backward): a grouping pass above GROUP_ABOVE = 4096 partials."""
+    return 2 if parts > 4096 else 1
 
 
 def _chunks(M: int, C_: int) -> int:
