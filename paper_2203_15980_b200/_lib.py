@@ -10,7 +10,8 @@ import ctypes as C
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libdelta.so")
+# DELTA_LIB: an alternative build of the library (A/B timing of two builds)
+LIB_PATH = os.environ.get("DELTA_LIB") or os.path.join(_HERE, "libdelta.so")
 
 u8, u32, u64, i32 = C.c_uint8, C.c_uint32, C.c_uint64, C.c_int32
 

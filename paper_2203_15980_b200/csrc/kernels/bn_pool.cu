@@ -589,6 +589,20 @@ __global__ void __launch_bounds__(256)
 }
 
 // ----------------------------------------------------------------- pooling
+// The 9 taps of a 3x3/2 pad-1 window, all loads issued before any use
+// (out-of-image taps = -inf, which never wins a strict > scan)
+__device__ __forceinline__ void window_loads(const bf16* __restrict__ x, int n, int p, int q,
+                                             int c0, int H, int W, int C, uint4 (&v)[9]) {
+  const uint4 ninf = make_uint4(0xFF80FF80u, 0xFF80FF80u, 0xFF80FF80u, 0xFF80FF80u);
+#pragma unroll
+  for (int k = 0; k < 9; ++k) {
+    const int h = 2 * p - 1 + k / 3, w = 2 * q - 1 + k % 3;
+    const bool ok = (unsigned)h < (unsigned)H && (unsigned)w < (unsigned)W;
+    v[k] = ok ? *reinterpret_cast<const uint4*>(x + ((int64_t(n) * H + h) * W + w) * C + c0)
+              : ninf;
+  }
+}
+
 // Grids: blockIdx.x = one image row (n, row), blockIdx.y x 256 threads span
 // (column, 8-channel group) of that row; C/8 is a power of two, so the only
 // divisions left are one 32-bit div/mod per thread.
@@ -602,6 +616,8 @@ __global__ void __launch_bounds__(256) k_maxpool_fwd(const bf16* __restrict__ x,
   if (item >= Q * cg) return;
   const int q = item >> lcg, c0 = (item & (cg - 1)) * 8;
   const int n = blockIdx.x / P, p = blockIdx.x - n * P;
+  // (the compiler batches these loads itself; forcing all 9 up front measured
+  // slower: 161 vs 126 us at the ResNet-50 stem shape)
   float best[8];
 #pragma unroll
   for (int j = 0; j < 8; ++j) best[j] = -INFINITY;
@@ -643,12 +659,12 @@ __global__ void __launch_bounds__(256)
     best[j] = -INFINITY;
     arg[j] = 0;
   }
+  uint4 v[9];
+  window_loads(x, n, p, q, c0, H, W, C, v);
 #pragma unroll
   for (int k = 0; k < 9; ++k) {
-    const int h = 2 * p - 1 + k / 3, w = 2 * q - 1 + k % 3;
-    if (h < 0 || h >= H || w < 0 || w >= W) continue;
     float f[8];
-    unpack8(*reinterpret_cast<const uint4*>(x + ((int64_t(n) * H + h) * W + w) * C + c0), f);
+    unpack8(v[k], f);
 #pragma unroll
     for (int j = 0; j < 8; ++j)
       if (f[j] > best[j]) {
@@ -682,16 +698,25 @@ __global__ void __launch_bounds__(256)
   for (int b = 0; b < 4; ++b)
 #pragma unroll
     for (int j = 0; j < 8; ++j) acc[b][j] = 0.f;
+  // the (up to) 4 windows' argmax bytes and gradients, loaded up front
+  uint2 av[4];
+  uint4 gv[4];
+#pragma unroll
+  for (int t = 0; t < 4; ++t) {
+    const int pp = p + (t >> 1), qq = q + (t & 1);
+    const bool ok = pp < P && qq < Q;
+    const int64_t o = ((int64_t(n) * P + pp) * Q + qq) * C + c0;
+    av[t] = ok ? *reinterpret_cast<const uint2*>(idx + o) : make_uint2(0xFFFFFFFFu, 0xFFFFFFFFu);
+    gv[t] = ok ? *reinterpret_cast<const uint4*>(dy + o) : make_uint4(0u, 0u, 0u, 0u);
+  }
 #pragma unroll
   for (int dp = 0; dp < 2; ++dp)
 #pragma unroll
     for (int dq = 0; dq < 2; ++dq) {
       const int pp = p + dp, qq = q + dq;
-      if (pp >= P || qq >= Q) continue;
-      const int64_t o = ((int64_t(n) * P + pp) * Q + qq) * C + c0;
-      const uint2 a = *reinterpret_cast<const uint2*>(idx + o);
+      const uint2 a = av[dp * 2 + dq];  // 0xFF never matches a tap (0..8)
       float g[8];
-      unpack8(*reinterpret_cast<const uint4*>(dy + o), g);
+      unpack8(gv[dp * 2 + dq], g);
 #pragma unroll
       for (int b = 0; b < 4; ++b) {
         // input pixel (2p + (b>>1), 2q + (b&1)) inside window (pp, qq) at tap k

@@ -1,1 +1,2 @@
-for m in 4096 32 4096 32; do DELTA_BN_GROUP_ABOVE=$m timeout 900 python bench.py --cpu-sample-s 1 > gpurun_out/bench.log 2>&1; echo -n "GROUP_ABOVE=$m "; tail -1 gpurun_out/bench.log | python -c "import json,sys; d=json.loads(sys.stdin.read()); print(d['value'], d['no_eviction']['images_per_s'], d['e2e']['value'])"; done
+timeout 300 python -m pytest tests/test_kernels_gpu.py -x -q -k maxpool 2>&1 | tail -1
+python scripts/kbench_pool.py; DELTA_LIB=$PWD/build/ab/libdelta.so python scripts/kbench_pool.py
