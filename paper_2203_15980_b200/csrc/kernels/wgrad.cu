@@ -89,7 +89,7 @@ __device__ __forceinline__ uint64_t desc_mn_interleave(uint32_t addr, uint32_t l
 // traffic per flop (the operand stream from L2 paces the large-K shapes)
 template <int MODE, int BN, int MT>
 constexpr int wg_stages() {
-  return MODE == WG_STEMRAW ? 6 : (MT == 2 ? 3 : (BN >= 256 ? 4 : 6));
+  return MODE == WG_STEMRAW ? 6 : (MT == 2 ? 3 : (BN >= 192 ? 4 : 6));
 }
 
 template <int BN, int MODE, int MT>
@@ -136,7 +136,8 @@ __global__ void __launch_bounds__(WG_THREADS, 1)
     }
     fence_proxy_async_smem();
   }
-  constexpr uint32_t TMEM_COLS = 2 * BN;  // MT=1: two accumulators; MT=2: lo/hi halves
+  // MT=1: two accumulators; MT=2: lo/hi halves (allocation: a power of two)
+  constexpr uint32_t TMEM_COLS = 2 * BN <= 256 ? 2 * BN : 512;
   constexpr uint32_t NACC = MT == 2 ? 1 : 2;  // accumulator buffers
   if (warp == 1) tmem_alloc(tslot, TMEM_COLS);
   tc_fence_before();
@@ -500,7 +501,13 @@ int wgrad_plan_init(WgradPlan* wp) {
                 : (p.R == 1 && p.S == 1 && p.stride == 1 && p.pad == 0 ? WG_PLAIN : WG_IM2COL);
   p.taps = stem ? 1 : p.R * p.S;
   const int ntot = p.taps * p.C;  // flattened (tap, channel) columns
+  // N tile: 256, unless 256-wide tiles would leave much padding and 192 none
+  // (3x3 over 64 channels: 576 = 3 x 192 instead of 3 x 256 with a quarter-
+  // full last tile: 120 -> 108 us; at 1152 = 4.5 x 256 the 256 tiles win)
   p.bn = stem ? 256 : (ntot >= 256 ? 256 : (ntot >= 128 ? 128 : 64));
+  if (!stem && ntot % 192 == 0 && ntot > 256 &&
+      double(ntot) / (double((ntot + 255) / 256) * 256.0) < 0.85)
+    p.bn = 192;
   // 256-channel tiles (two accumulators on one B tile) for the 3x3 convs with
   // K % 256 == 0 (measured: 62.5 -> 57.5 us at 14x14x256, 76 -> 60 us at
   // 7x7x512); the 1x1 shapes' short items lose more to the undoubled
@@ -557,6 +564,9 @@ cudaError_t wgrad(const WgradPlan& wp, const void* dy, const void* x, float* dw,
     case 128:
       return wp.mode == WG_PLAIN ? wg_launch<128, WG_PLAIN>(wp, dy, x, dw, ws, st)
                                  : wg_launch<128, WG_IM2COL>(wp, dy, x, dw, ws, st);
+    case 192:
+      return wp.mode == WG_PLAIN ? wg_launch<192, WG_PLAIN>(wp, dy, x, dw, ws, st)
+                                 : wg_launch<192, WG_IM2COL>(wp, dy, x, dw, ws, st);
     default:
       if (wp.mt == 2)
         return wp.mode == WG_PLAIN ? wg_launch<256, WG_PLAIN, 2>(wp, dy, x, dw, ws, st)
