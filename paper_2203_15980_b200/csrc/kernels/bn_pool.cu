@@ -143,6 +143,34 @@ __device__ __forceinline__ float warp_sum(float v) {
   return v;
 }
 
+// Fixed-order column sums over partial rows for the 8 channels c0..c0+7 of a
+// block: thread t takes channel t&7 of rows t>>3, (t>>3)+32, ... (each warp
+// reads 4 rows x 8 adjacent channels: coalesced), then warp 0 adds the 32
+// stripes in order.  Returns the sums in thread ch < 8 of warp 0.
+template <typename T, typename F>
+__device__ __forceinline__ float2 rows_sum8(const T* __restrict__ ws, int rows, int C, int c0,
+                                            F&& term) {
+  __shared__ float2 part[32][9];
+  const int ch = threadIdx.x & 7, stripe = threadIdx.x >> 3;
+  float2 acc = make_float2(0.f, 0.f);
+  if (c0 + ch < C)
+    for (int k = stripe; k < rows; k += 32) {
+      const float2 v = term(ws[int64_t(k) * C + c0 + ch]);
+      acc.x += v.x;
+      acc.y += v.y;
+    }
+  part[stripe][ch] = acc;
+  __syncthreads();
+  float2 r = make_float2(0.f, 0.f);
+  if (threadIdx.x < 8)
+    for (int k = 0; k < 32; ++k) {
+      r.x += part[k][threadIdx.x].x;
+      r.y += part[k][threadIdx.x].y;
+    }
+  __syncthreads();
+  return r;
+}
+
 __global__ void __launch_bounds__(256)
     k_bn_stats_merge(const float2* __restrict__ ws, int parts, int64_t rows_per, int64_t M, int C,
                      float* mean, float* invstd, float eps, float* rm, float* rv, float mom) {
@@ -183,31 +211,28 @@ __global__ void __launch_bounds__(256)
                          float* invstd, float eps, float* rm, float* rv, float mom) {
   pdl_wait();
   pdl_trigger();
-  const int c = blockIdx.x * 8 + (threadIdx.x >> 5);
-  const int lane = threadIdx.x & 31;
-  if (c >= C) return;
-  float s = 0.f, n = 0.f;
-  for (int k = lane; k < parts; k += 32) {
-    const float4 p = ws[int64_t(k) * C + c];
-    s = fmaf(p.x, p.y, s);
-    n += p.x;
-  }
-  n = warp_sum(n);
-  const float mu = warp_sum(s) / n;
-  float m2 = 0.f;
-  for (int k = lane; k < parts; k += 32) {
-    const float4 p = ws[int64_t(k) * C + c];
-    const float d = p.y - mu;
-    m2 += fmaf(p.x, d * d, p.z);
-  }
-  m2 = warp_sum(m2);
-  if (lane == 0) {
-    const float var = m2 / n;
+  __shared__ float mu_s[8];
+  const int c0 = blockIdx.x * 8;
+  // pass 1: count and sum(count * mean) -> the channel mean
+  const float2 sn = rows_sum8(ws, parts, C, c0,
+                              [](float4 p) { return make_float2(p.x * p.y, p.x); });
+  if (threadIdx.x < 8) mu_s[threadIdx.x] = sn.y > 0.f ? sn.x / sn.y : 0.f;
+  __syncthreads();
+  // pass 2: sum(M2 + count * (mean - mu)^2)
+  const float mu_c = mu_s[threadIdx.x & 7];
+  const float2 m2 = rows_sum8(ws, parts, C, c0, [mu_c](float4 p) {
+    const float d = p.y - mu_c;
+    return make_float2(fmaf(p.x, d * d, p.z), 0.f);
+  });
+  const int c = c0 + threadIdx.x;
+  if (threadIdx.x < 8 && c < C) {
+    const float n = sn.y, mu = mu_s[threadIdx.x];
+    const float var = m2.x / n;
     mean[c] = mu;
     invstd[c] = rsqrtf(var + eps);
     if (rm) {
       rm[c] = (1.f - mom) * rm[c] + mom * mu;
-      rv[c] = (1.f - mom) * rv[c] + mom * (n > 1.f ? m2 / (n - 1.f) : var);
+      rv[c] = (1.f - mom) * rv[c] + mom * (n > 1.f ? m2.x / (n - 1.f) : var);
     }
   }
 }
@@ -219,20 +244,12 @@ __global__ void __launch_bounds__(256)
                        const float* invstd, float* dgamma, float* dbeta) {
   pdl_wait();
   pdl_trigger();
-  const int c = blockIdx.x * 8 + (threadIdx.x >> 5);
-  const int lane = threadIdx.x & 31;
-  if (c >= C) return;
-  float A = 0.f, B = 0.f;
-  for (int k = lane; k < parts; k += 32) {
-    const float4 p = ws[int64_t(k) * C + c];
-    A += p.x;
-    B += p.y;
-  }
-  A = warp_sum(A);
-  B = warp_sum(B);
-  if (lane == 0) {
-    dbeta[c] = A;
-    dgamma[c] = invstd[c] * (B - mean[c] * A);
+  const int c0 = blockIdx.x * 8;
+  const float2 AB = rows_sum8(ws, parts, C, c0, [](float4 p) { return make_float2(p.x, p.y); });
+  const int c = c0 + threadIdx.x;
+  if (threadIdx.x < 8 && c < C) {
+    dbeta[c] = AB.x;
+    dgamma[c] = invstd[c] * (AB.y - mean[c] * AB.x);
   }
 }
 
@@ -432,20 +449,12 @@ __global__ void __launch_bounds__(256) k_bn_bwd_final(const float2* __restrict__
                                                       int C, float* dgamma, float* dbeta) {
   pdl_wait();
   pdl_trigger();
-  const int c = blockIdx.x * 8 + (threadIdx.x >> 5);
-  const int lane = threadIdx.x & 31;
-  if (c >= C) return;
-  float A = 0.f, B = 0.f;
-  for (int k = lane; k < chunks; k += 32) {
-    const float2 p = ws[int64_t(k) * C + c];
-    A += p.x;
-    B += p.y;
-  }
-  A = warp_sum(A);
-  B = warp_sum(B);
-  if (lane == 0) {
-    dbeta[c] = A;
-    dgamma[c] = B;
+  const int c0 = blockIdx.x * 8;
+  const float2 AB = rows_sum8(ws, chunks, C, c0, [](float2 p) { return p; });
+  const int c = c0 + threadIdx.x;
+  if (threadIdx.x < 8 && c < C) {
+    dbeta[c] = AB.x;
+    dgamma[c] = AB.y;
   }
 }
 
