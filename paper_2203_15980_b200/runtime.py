@@ -36,7 +36,7 @@ BN_EPS = 1e-5
 # length is at least this; shorter convs get a separate streaming statistics
 # pass.  0 = every conv (measured A/B on one box with 8 epilogue warps:
 # 11.57k vs 11.44k img/s; with 4 epilogue warps it was a wash, hence the old 384).
-OWN_DGRAD_3X3 = __import__("os").environ.get("DELTA_OWN_DGRAD_3X3", "0") == "1"
+OWN_DGRAD_3X3 = __import__("os").environ.get("DELTA_OWN_DGRAD_3X3", "1") == "1"
 FUSE_STATS_MIN_KDIM = int(__import__("os").environ.get("DELTA_FUSE_STATS_MIN_KDIM", "0"))
 BN_MOMENTUM = 0.1
 _TORCH_OPTIM = __import__("os").environ.get("DELTA_TORCH_OPTIM", "0") == "1"
@@ -199,14 +199,15 @@ def workspace_plan(g: G.Graph) -> dict:
 
 
 def own_dgrad(cs: G.ConvSpec) -> bool:
-    """Input gradients of the 1x1 convs run through our tcgen05 conv kernel
-    (transposed weights; fused backward epilogues: residual add + ReLU mask,
-    BN-backward reductions; a stride-2 1x1's gradient is computed on its
-    sampling grid and scattered by the consumer's epilogue).  3x3 dgrads stay
-    with cuDNN for now (our 3x3 kernel is slower than cuDNN's at the narrow
-    layer-1/2 widths, scripts/kbench_dgrad.py); the stem has no input gradient."""
-    if cs.cin == 4:
-        return False
+    """Input gradients through our tcgen05 conv kernel (transposed / flipped
+    weights; fused backward epilogues: residual add + ReLU mask, BN-backward
+    reductions; a stride-2 1x1's gradient is computed on its sampling grid and
+    scattered by the consumer's epilogue): every 1x1 and every stride-1 3x3
+    (with TMA-loaded epilogue operands this is on par with cuDNN dgrad plus a
+    streaming BN backward: 11.60k vs 11.58k img/s A/B; DELTA_OWN_DGRAD_3X3=0
+    routes the 3x3s to cuDNN).  The three stride-2 3x3 input gradients stay
+    with cuDNN (a transposed-conv dgrad is not implemented); the stem has no
+    input gradient."""
     return cs.k == 1 or (cs.stride == 1 and OWN_DGRAD_3X3)
 
 
