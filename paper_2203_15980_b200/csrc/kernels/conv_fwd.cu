@@ -75,9 +75,12 @@ constexpr bool gathers(int mode) { return mode == MODE_GATHER || mode == MODE_ST
 // whole 2 KB blocks per warp — the ring depth is what keeps the epilogue's
 // operand reads in flight.
 constexpr uint32_t SMEM_MAX = 232448;
+// fused epilogues: per-warp BN scale/shift of the 32 chunk columns (float2 x 32)
+constexpr uint32_t SCSH_BYTES = EPI_W * 256;
 template <int BN, int STAGES>
 constexpr uint32_t epi_ring_bytes() {
-  return (SMEM_MAX - 1024 - 256 - 4 * BN * 8 - 16384 - STAGES * (128 * 128 + BN * 128)) /
+  return (SMEM_MAX - 1024 - 256 - 4 * BN * 8 - 16384 - SCSH_BYTES -
+          STAGES * (128 * 128 + BN * 128)) /
          (EPI_W * 2048) * (EPI_W * 2048);
 }
 
@@ -180,8 +183,11 @@ __global__ void __launch_bounds__(kThreads, 1)
   const uint32_t sIn = sOut + 16384;
   // BN-statistics scratch: per quarter-warp column (sum, sumsq), [4][BN] float2
   float2* red = reinterpret_cast<float2*>(smem + STAGES * (A_STAGE + B_STAGE) + 16384 + IN_BYTES);
+  // FUSED: [EPI_W][32] float2 per-warp BN scale/shift scratch after the statistics scratch
+  const uint32_t sScSh = sIn + IN_BYTES + 4 * BN * sizeof(float2);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * (A_STAGE + B_STAGE) + 16384 +
-                                               IN_BYTES + 4 * BN * sizeof(float2));
+                                               IN_BYTES + 4 * BN * sizeof(float2) +
+                                               (FUSED ? SCSH_BYTES : 0));
   uint64_t* empty = full + STAGES;
   uint64_t* tfull = empty + STAGES;  // [2]
   uint64_t* tempty = tfull + 2;      // [2]
@@ -616,22 +622,31 @@ __global__ void __launch_bounds__(kThreads, 1)
           // ReLU mask of the forward output relu(bn(xc)) = bf16(max(xc*sc+sh, 0)):
           // positive iff xc*sc+sh > 2^-134 (the bf16 rounding threshold), with
           // k_bn_apply<0>'s exact scale/shift arithmetic
-          const float my_sc = __ldg(a.e.invstd + col + lane) * __ldg(a.e.gamma + col + lane);
-          const float my_sh = fmaf(-__ldg(a.e.mean + col + lane), my_sc, __ldg(a.e.beta + col + lane));
+          // lane c computes column c's (scale, shift) into the warp's scratch;
+          // every lane then reads them back two columns per 16 B broadcast load
+          const uint32_t scsh = sScSh + (warp - 4) * 256;
+          {
+            const float my_sc = __ldg(a.e.invstd + col + lane) * __ldg(a.e.gamma + col + lane);
+            const float my_sh =
+                fmaf(-__ldg(a.e.mean + col + lane), my_sc, __ldg(a.e.beta + col + lane));
+            asm volatile("st.shared.v2.f32 [%0], {%1, %2};" ::"r"(scsh + lane * 8), "f"(my_sc),
+                         "f"(my_sh)
+                         : "memory");
+            __syncwarp();
+          }
 #pragma unroll
           for (int u = 0; u < 4; ++u) {
             float x[8];
             unpack8f(ld_row16(sb, lane, u), x);
-            uint32_t bits = 0;
 #pragma unroll
-            for (int i = 0; i < 8; ++i) {
-              const float sc = __shfl_sync(0xffffffffu, my_sc, u * 8 + i);
-              const float sh = __shfl_sync(0xffffffffu, my_sh, u * 8 + i);
-              bits |= (fmaf(x[i], sc, sh) > 0x1p-134f ? 0xFFFFu : 0u) << (16 * (i & 1));
-              if (i & 1) {
-                (&pk[u].x)[i >> 1] &= bits;
-                bits = 0;
-              }
+            for (int i = 0; i < 8; i += 2) {
+              float sc0, sh0, sc1, sh1;
+              asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+                           : "=f"(sc0), "=f"(sh0), "=f"(sc1), "=f"(sh1)
+                           : "r"(scsh + (u * 8 + i) * 8));
+              const uint32_t bits = (fmaf(x[i], sc0, sh0) > 0x1p-134f ? 0xFFFFu : 0u) |
+                                    (fmaf(x[i + 1], sc1, sh1) > 0x1p-134f ? 0xFFFF0000u : 0u);
+              (&pk[u].x)[i >> 1] &= bits;
             }
           }
         }
@@ -773,6 +788,7 @@ constexpr size_t conv_smem_bytes() {
          (!FUSED ? 0
           : OPT  ? size_t(OPT_NB) * ev_operands(EV) * BN * 256
                  : epi_ring_bytes<BN, STAGES>()) /*epilogue operands*/ + 4 * BN * 8 /*stats scratch*/ +
+         (FUSED ? SCSH_BYTES : 0) /*BN scale/shift*/ +
          1024 /*align*/ + 256 /*barriers*/;
 }
 
