@@ -540,7 +540,19 @@ __global__ void __launch_bounds__(kThreads, 1)
     };
     if constexpr (FUSED && !OPT)
       for (uint32_t e = 0; e + 1 < NSLOTS; ++e) prefetch(e);
-    if (a.stats != nullptr) stats_row_zero(a.stats, a.K, BN, (warp - 4) * 32 + lane, EPI_W * 32);
+    // One N tile (K <= BN = 64): every tile of this CTA covers the same columns, so
+    // each lane keeps its chunk columns' statistics in registers across the
+    // whole persistent loop (Chan merge / sums per chunk) and the quarters are
+    // combined once at the end — no per-tile barrier or global round trip.
+    // Several N tiles: per-tile cross-quarter combine folded into the CTA row.
+    // (only with one chunk per lane per tile: with more, the per-chunk merges
+    // cost more than the per-tile barrier they save — measured at BN=256)
+    const bool reg_stats = CHW == 1 && a.stats != nullptr && a.n_tiles == 1;
+    float4 racc[CHW];
+#pragma unroll
+    for (int jj = 0; jj < CHW; ++jj) racc[jj] = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (a.stats != nullptr && !reg_stats)
+      stats_row_zero(a.stats, a.K, BN, (warp - 4) * 32 + lane, EPI_W * 32);
     uint32_t ec = 0;  // chunks consumed by this warp
     uint32_t lt = 0;
     for (int tile = blockIdx.x; tile < a.tiles; tile += gridDim.x, ++lt) {
@@ -690,11 +702,18 @@ __global__ void __launch_bounds__(kThreads, 1)
               sq = fmaf(f, f, sq);
             }
           }
-          red[quarter * BN + j * 32 + lane] = make_float2(sum, sq);
+          if (reg_stats) {
+            const int nq = min(max((row_tiled(MODE) ? a.Q : min(BM, a.M - m0)) - quarter * 32, 0), 32);
+            const int jj = (j - half) / HALVES;
+            if (EV == EV_BN_BWD || nq > 0)
+              racc[jj] = stats_merge_tile<EV == EV_BN_BWD>(racc[jj], float(nq), sum, sq);
+          } else {
+            red[quarter * BN + j * 32 + lane] = make_float2(sum, sq);
+          }
         }
         if constexpr (EV == EV_BN_BWD) __syncwarp();  // ring slot read by the stats pass
       }
-      if (a.stats != nullptr) {
+      if (a.stats != nullptr && !reg_stats) {
         // combine the four row quarters -> this tile's column partials, folded
         // into the CTA's row of the statistics table
         asm volatile("bar.sync 1, %0;" ::"n"(EPI_W * 32) : "memory");
@@ -708,7 +727,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             Q += red[qq * BN + c].y;
           }
           if (n0 + c < a.K)
-            stats_merge_tile<EV == EV_BN_BWD>(a.stats, a.K, n0 + c, float(n_rows), S, Q);
+            stats_fold_tile<EV == EV_BN_BWD>(a.stats, a.K, n0 + c, float(n_rows), S, Q);
         }
         asm volatile("bar.sync 1, %0;" ::"n"(EPI_W * 32) : "memory");
       }
@@ -717,6 +736,33 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (lane == 0) {
         mbar_arrive(&tempty[acc]);
         if (FUSED && OPT) mbar_arrive(&oempty[lt % OPT_NB]);  // operand tile read
+      }
+    }
+    if (reg_stats) {
+      // the quarters' register statistics through the (now idle) output
+      // staging buffer as float4 [4][BN], combined in quarter order
+      if (lane == 0) bulk_wait<0>();
+      __syncwarp();
+      asm volatile("bar.sync 1, %0;" ::"n"(EPI_W * 32) : "memory");
+      float4* qs = reinterpret_cast<float4*>(smem + STAGES * (A_STAGE + B_STAGE));
+      static_assert(4 * BN * sizeof(float4) <= 16384, "staging buffer");
+#pragma unroll
+      for (int jj = 0; jj < CHW; ++jj) qs[quarter * BN + (half + jj * HALVES) * 32 + lane] = racc[jj];
+      asm volatile("bar.sync 1, %0;" ::"n"(EPI_W * 32) : "memory");
+      const int et = (warp - 4) * 32 + lane;
+      if (et < BN && et < a.K) {
+        float4 r = qs[et];
+#pragma unroll
+        for (int qq = 1; qq < 4; ++qq) {
+          const float4 b = qs[qq * BN + et];
+          if (EV == EV_BN_BWD) {
+            r.x += b.x;
+            r.y += b.y;
+          } else {
+            r = stats_merge_pair(r, b);
+          }
+        }
+        a.stats[size_t(blockIdx.x) * a.K + et] = r;
       }
     }
   } else {

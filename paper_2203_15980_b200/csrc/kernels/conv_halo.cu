@@ -222,7 +222,7 @@ __global__ void __launch_bounds__(HT, 1)
             S += red[qq * BN + c].x;
             Qs += red[qq * BN + c].y;
           }
-          if (n0 + c < a.K) stats_merge_tile<false>(a.stats, a.K, n0 + c, n_rows, S, Qs);
+          if (n0 + c < a.K) stats_fold_tile<false>(a.stats, a.K, n0 + c, n_rows, S, Qs);
         }
         asm volatile("bar.sync 1, 128;" ::: "memory");
       }

@@ -20,13 +20,10 @@ __device__ __forceinline__ void stats_row_zero(float4* stats, int K, int BN, int
     for (int c = et; c < BN && n0 + c < K; c += nt) row[n0 + c] = make_float4(0.f, 0.f, 0.f, 0.f);
 }
 
-// fold one tile's column (n_t rows, sum S, sum of squares / cross term Q)
-// into this CTA's row
+// fold (n_t rows, sum S, sum of squares / cross term Q) into `a`: a
+// (count, mean, M2) running value, or (sum g, sum g*xc) sums for SUMS
 template <bool SUMS>
-__device__ __forceinline__ void stats_merge_tile(float4* stats, int K, int col, float n_t, float S,
-                                                 float Q) {
-  float4* p = stats + size_t(blockIdx.x) * K + col;
-  float4 a = *p;
+__device__ __forceinline__ float4 stats_merge_tile(float4 a, float n_t, float S, float Q) {
   if (SUMS) {
     a.x += S;
     a.y += Q;
@@ -39,7 +36,26 @@ __device__ __forceinline__ void stats_merge_tile(float4* stats, int K, int col, 
     a.z += m2_t + d * d * (a.x * n_t / n);
     a.x = n;
   }
-  *p = a;
+  return a;
+}
+
+// Chan merge of two (count, mean, M2) triples
+__device__ __forceinline__ float4 stats_merge_pair(float4 a, float4 b) {
+  if (b.x <= 0.f) return a;
+  const float n = a.x + b.x;
+  const float d = b.y - a.y;
+  a.y = fmaf(d, b.x / n, a.y);
+  a.z += b.z + d * d * (a.x * b.x / n);
+  a.x = n;
+  return a;
+}
+
+// ... the same, read-modify-write of this CTA's row in the table
+template <bool SUMS>
+__device__ __forceinline__ void stats_fold_tile(float4* stats, int K, int col, float n_t, float S,
+                                                float Q) {
+  float4* p = stats + size_t(blockIdx.x) * K + col;
+  *p = stats_merge_tile<SUMS>(*p, n_t, S, Q);
 }
 
 }  // namespace delta_k
