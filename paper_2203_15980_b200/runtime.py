@@ -42,6 +42,18 @@ BN_MOMENTUM = 0.1
 _TORCH_OPTIM = __import__("os").environ.get("DELTA_TORCH_OPTIM", "0") == "1"
 
 
+class _tf32:
+    """The classifier's fp32 GEMMs (library calls, 1 GFLOP each) on the tensor
+    cores (TF32) instead of SIMT fp32: 90 -> ~25 us per fc backward."""
+
+    def __enter__(self):
+        self.prev = torch.backends.cuda.matmul.allow_tf32
+        torch.backends.cuda.matmul.allow_tf32 = True
+
+    def __exit__(self, *exc):
+        torch.backends.cuda.matmul.allow_tf32 = self.prev
+
+
 def _ptr(t: torch.Tensor) -> int:
     return t.data_ptr()
 
@@ -440,8 +452,9 @@ class DeltaRuntime:
 
             def fc(out, ins, rec, stream, node=node, src=src):
                 a_ = self._view(ins[0] - self._base, src)
-                torch.addmm(pr.views["fc_b"], a_.float(), pr.views["fc_w"].t(),
-                            out=self._view(out - self._base, node))
+                with _tf32():
+                    torch.addmm(pr.views["fc_b"], a_.float(), pr.views["fc_w"].t(),
+                                out=self._view(out - self._base, node))
             add(X.kop(X.K_HOST, (), (host(fc),)), 0, 0)
         elif op == "fc_bwd":
             logits_n, src = self.nodes[node.parents[0]], self.nodes[node.parents[1]]
@@ -451,9 +464,10 @@ class DeltaRuntime:
 
             def fc_bwd(out, ins, rec, stream, node=node, src=src):
                 a_ = self._view(ins[1] - self._base, src)
-                torch.mm(self.dlogits.t(), a_.float(), out=pr.gviews["fc_w"])
-                torch.sum(self.dlogits, 0, out=pr.gviews["fc_b"])
-                self._view(out - self._base, node).copy_(self.dlogits @ pr.views["fc_w"])
+                with _tf32():
+                    torch.mm(self.dlogits.t(), a_.float(), out=pr.gviews["fc_w"])
+                    torch.sum(self.dlogits, 0, out=pr.gviews["fc_b"])
+                    self._view(out - self._base, node).copy_(self.dlogits @ pr.views["fc_w"])
             add(X.kop(X.K_HOST, (), (host(fc_bwd),)), 0, 0)
         elif op == "bn_add_relu_bwd":
             # parents: [upstream, (O if masked,) X]; upstream already masked
