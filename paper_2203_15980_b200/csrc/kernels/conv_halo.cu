@@ -155,7 +155,14 @@ __global__ void __launch_bounds__(HT, 1)
     const int quarter = warp & 3;
     const int qpx = a.slot < 32 ? a.slot : 32;  // pixels per store row
     const int qrows = 32 / qpx;                 // image rows per 32-row chunk
-    if (a.stats != nullptr) stats_row_zero(a.stats, a.K, BN, (warp - 4) * 32 + lane, 128);
+    // one N tile: each lane keeps its columns' statistics in registers across
+    // the persistent loop, the quarters are combined once at the end
+    const bool reg_stats = a.stats != nullptr && a.n_tiles == 1;
+    float4 racc[BN / 32];
+#pragma unroll
+    for (int j = 0; j < BN / 32; ++j) racc[j] = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (a.stats != nullptr && !reg_stats)
+      stats_row_zero(a.stats, a.K, BN, (warp - 4) * 32 + lane, 128);
     uint32_t lt = 0;
     for (int tile = blockIdx.x; tile < a.tiles; tile += gridDim.x, ++lt) {
       const int mt = tile / a.n_tiles, n0 = (tile % a.n_tiles) * BN;
@@ -163,6 +170,13 @@ __global__ void __launch_bounds__(HT, 1)
       const int i0 = quarter * 32;  // first tile row of this warp
       const int prow = p0 + i0 / a.slot, pcol = i0 % a.slot;
       const uint32_t acc = lt & 1;
+      // this warp's valid rows (pixel column < Q, inside the tile's rows),
+      // as a bit mask, once per tile
+      uint32_t vmask = 0;
+      if (a.stats != nullptr) {
+        const bool ok = ((i0 + lane) % a.slot) < a.Q && (i0 + lane) < a.rows * a.slot;
+        vmask = __ballot_sync(0xffffffffu, ok);
+      }
       mbar_wait(&tfull[acc], (lt >> 1) & 1);
       tc_fence_after();
       const uint32_t stage_base = sOut + quarter * 4096;
@@ -202,16 +216,20 @@ __global__ void __launch_bounds__(HT, 1)
                          : "=h"(h)
                          : "r"(buf + rr * 64 + ((c16 ^ ((rr >> 1) & 3)) << 4) + cbyte));
             const float f = __bfloat162float(__ushort_as_bfloat16(h));
-            const bool ok = ((i0 + rr) % a.slot) < a.Q && (i0 + rr) < a.rows * a.slot;
-            const float g = ok ? f : 0.f;  // garbage rows may hold anything, even NaN
+            const float g = (vmask >> rr) & 1u ? f : 0.f;  // garbage rows may hold anything
             sum += g;
             sq = fmaf(g, g, sq);
           }
-          red[quarter * BN + j * 32 + lane] = make_float2(sum, sq);
+          if (reg_stats) {
+            const float nq = float(__popc(vmask));
+            if (nq > 0.f) racc[j] = stats_merge_tile<false>(racc[j], nq, sum, sq);
+          } else {
+            red[quarter * BN + j * 32 + lane] = make_float2(sum, sq);
+          }
         }
       }
       (void)qrows;
-      if (a.stats != nullptr) {
+      if (a.stats != nullptr && !reg_stats) {
         asm volatile("bar.sync 1, 128;" ::: "memory");
         const int et = (warp - 4) * 32 + lane;
         const float n_rows = float(a.rows * a.Q);
@@ -229,6 +247,23 @@ __global__ void __launch_bounds__(HT, 1)
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&tempty[acc]);
+    }
+    if (reg_stats) {
+      // quarters combined through the idle output staging buffer, in order
+      if (lane == 0) bulk_wait<0>();
+      __syncwarp();
+      asm volatile("bar.sync 1, 128;" ::: "memory");
+      float4* qs = reinterpret_cast<float4*>(smem + (sOut - smem_u32(smem)));
+      static_assert(4 * BN * sizeof(float4) <= 16384, "staging buffer");
+#pragma unroll
+      for (int j = 0; j < BN / 32; ++j) qs[quarter * BN + j * 32 + lane] = racc[j];
+      asm volatile("bar.sync 1, 128;" ::: "memory");
+      for (int c = (warp - 4) * 32 + lane; c < BN && c < a.K; c += 128) {
+        float4 r = qs[c];
+#pragma unroll
+        for (int qq = 1; qq < 4; ++qq) r = stats_merge_pair(r, qs[qq * BN + c]);
+        a.stats[size_t(blockIdx.x) * a.K + c] = r;
+      }
     }
   } else {
     // ============================== MMA issuer ===============================
