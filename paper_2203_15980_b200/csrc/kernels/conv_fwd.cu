@@ -157,6 +157,7 @@ __device__ __forceinline__ uint8_t* align1024(uint8_t* p) {
 // (32-column x 128-row boxes, the same 64B-swizzled layout the cp.async ring
 // uses), instead of per-chunk cp.async gathers by the epilogue warps.
 constexpr int OPT_NB = 2;
+
 template <int BN, int STAGES, int MODE, int EV, bool OPT = false>
 __global__ void __launch_bounds__(kThreads, 1)
     k_conv_fwd(const __grid_constant__ CUtensorMap wmap, const __grid_constant__ CUtensorMap amap,

@@ -28,12 +28,14 @@ __device__ __forceinline__ float4 stats_merge_tile(float4 a, float n_t, float S,
     a.x += S;
     a.y += Q;
   } else {
-    const float mu_t = S / n_t;
+    // fast reciprocal: deterministic, ~2 ulp, and off the epilogue's critical path
+    const float mu_t = __fdividef(S, n_t);
     const float m2_t = fmaxf(Q - S * mu_t, 0.f);
     const float n = a.x + n_t;
+    const float w = __fdividef(n_t, n);
     const float d = mu_t - a.y;
-    a.y = fmaf(d, n_t / n, a.y);
-    a.z += m2_t + d * d * (a.x * n_t / n);
+    a.y = fmaf(d, w, a.y);
+    a.z += m2_t + d * d * (a.x * w);
     a.x = n;
   }
   return a;
