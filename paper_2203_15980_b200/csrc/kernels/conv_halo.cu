@@ -18,7 +18,7 @@
 // so the statistics partials have a constant row count.
 //
 // Warp roles as in conv_fwd.cu: warp 0 thread 0 = TMA producer (A-halo ring +
-// weight ring), warps 4-7 = epilogue, warp 8 = TMEM owner + MMA issuer.
+// weight ring), warps 4-11 = epilogue, warp 12 = TMEM owner + MMA issuer.
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
@@ -36,7 +36,11 @@ using bf16 = __nv_bfloat16;
 
 namespace {
 
-constexpr int HT = 288;  // threads
+// warps 0 producer, 1-3 idle, 4..4+HE-1 epilogue (two per TMEM lane quarter,
+// alternating 32-column chunks, as in conv_fwd.cu), then the MMA warp
+constexpr int HE = 8;
+constexpr int HMMA = 4 + HE;
+constexpr int HT = (HMMA + 1) * 32;  // threads
 constexpr int BM = 128;
 
 struct HaloArgs {
@@ -104,7 +108,7 @@ __global__ void __launch_bounds__(HT, 1)
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&tfull[i], 1);
-      mbar_init(&tempty[i], 4);
+      mbar_init(&tempty[i], HE);
     }
     mbar_init(bres, 1);
     fence_mbar_init();
@@ -112,7 +116,7 @@ __global__ void __launch_bounds__(HT, 1)
     tma_prefetch_desc(&xmap);
     tma_prefetch_desc(&ymap);
   }
-  if (warp == 8) tmem_alloc(tslot, 2 * BN);
+  if (warp == HMMA) tmem_alloc(tslot, 2 * BN);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -150,9 +154,13 @@ __global__ void __launch_bounds__(HT, 1)
     }
   } else if (warp < 4) {
     // idle
-  } else if (warp < 8) {
+  } else if (warp < HMMA) {
     // ================================ epilogue ================================
     const int quarter = warp & 3;
+    constexpr int HALVES = HE / 4;
+    const int half = (warp - 4) >> 2;
+    constexpr int NBUF = 16384 / HE / 2048;  // 2 KB TMA-store staging buffers per warp
+    uint32_t ec = 0;
     const int qpx = a.slot < 32 ? a.slot : 32;  // pixels per store row
     const int qrows = 32 / qpx;                 // image rows per 32-row chunk
     // one N tile: each lane keeps its columns' statistics in registers across
@@ -162,7 +170,7 @@ __global__ void __launch_bounds__(HT, 1)
 #pragma unroll
     for (int j = 0; j < BN / 32; ++j) racc[j] = make_float4(0.f, 0.f, 0.f, 0.f);
     if (a.stats != nullptr && !reg_stats)
-      stats_row_zero(a.stats, a.K, BN, (warp - 4) * 32 + lane, 128);
+      stats_row_zero(a.stats, a.K, BN, (warp - 4) * 32 + lane, HE * 32);
     uint32_t lt = 0;
     for (int tile = blockIdx.x; tile < a.tiles; tile += gridDim.x, ++lt) {
       const int mt = tile / a.n_tiles, n0 = (tile % a.n_tiles) * BN;
@@ -179,14 +187,14 @@ __global__ void __launch_bounds__(HT, 1)
       }
       mbar_wait(&tfull[acc], (lt >> 1) & 1);
       tc_fence_after();
-      const uint32_t stage_base = sOut + quarter * 4096;
+      const uint32_t stage_base = sOut + (warp - 4) * (NBUF * 2048);
 #pragma unroll 1
-      for (int j = 0; j < BN / 32; ++j) {
+      for (int j = half; j < BN / 32; j += HALVES, ++ec) {
         float v[32];
         tmem_ld_32x32b_x32(tmem + (uint32_t(quarter * 32) << 16) + acc * BN + j * 32, v);
         const int col = n0 + j * 32;
-        const uint32_t buf = stage_base + (j & 1) * 2048;
-        if (lane == 0) bulk_wait_read<1>();
+        const uint32_t buf = stage_base + (ec % NBUF) * 2048;
+        if (lane == 0) bulk_wait_read<NBUF - 1>();
         __syncwarp();
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
@@ -230,10 +238,10 @@ __global__ void __launch_bounds__(HT, 1)
       }
       (void)qrows;
       if (a.stats != nullptr && !reg_stats) {
-        asm volatile("bar.sync 1, 128;" ::: "memory");
+        asm volatile("bar.sync 1, %0;" ::"n"(HE * 32) : "memory");
         const int et = (warp - 4) * 32 + lane;
         const float n_rows = float(a.rows * a.Q);
-        for (int c = et; c < BN; c += 128) {
+        for (int c = et; c < BN; c += HE * 32) {
           float S = 0.f, Qs = 0.f;
 #pragma unroll
           for (int qq = 0; qq < 4; ++qq) {
@@ -242,7 +250,7 @@ __global__ void __launch_bounds__(HT, 1)
           }
           if (n0 + c < a.K) stats_fold_tile<false>(a.stats, a.K, n0 + c, n_rows, S, Qs);
         }
-        asm volatile("bar.sync 1, 128;" ::: "memory");
+        asm volatile("bar.sync 1, %0;" ::"n"(HE * 32) : "memory");
       }
       tc_fence_before();
       __syncwarp();
@@ -252,13 +260,13 @@ __global__ void __launch_bounds__(HT, 1)
       // quarters combined through the idle output staging buffer, in order
       if (lane == 0) bulk_wait<0>();
       __syncwarp();
-      asm volatile("bar.sync 1, 128;" ::: "memory");
+      asm volatile("bar.sync 1, %0;" ::"n"(HE * 32) : "memory");
       float4* qs = reinterpret_cast<float4*>(smem + (sOut - smem_u32(smem)));
       static_assert(4 * BN * sizeof(float4) <= 16384, "staging buffer");
 #pragma unroll
-      for (int j = 0; j < BN / 32; ++j) qs[quarter * BN + j * 32 + lane] = racc[j];
-      asm volatile("bar.sync 1, 128;" ::: "memory");
-      for (int c = (warp - 4) * 32 + lane; c < BN && c < a.K; c += 128) {
+      for (int j = half; j < BN / 32; j += HALVES) qs[quarter * BN + j * 32 + lane] = racc[j];
+      asm volatile("bar.sync 1, %0;" ::"n"(HE * 32) : "memory");
+      for (int c = (warp - 4) * 32 + lane; c < BN && c < a.K; c += HE * 32) {
         float4 r = qs[c];
 #pragma unroll
         for (int qq = 1; qq < 4; ++qq) r = stats_merge_pair(r, qs[qq * BN + c]);
@@ -313,11 +321,11 @@ __global__ void __launch_bounds__(HT, 1)
       __syncwarp();
     }
   }
-  if (warp >= 4 && warp < 8 && lane == 0) bulk_wait<0>();
+  if (warp >= 4 && warp < HMMA && lane == 0) bulk_wait<0>();
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  if (warp == 8) tmem_dealloc(tmem, 2 * BN);
+  if (warp == HMMA) tmem_dealloc(tmem, 2 * BN);
 }
 
 template <int BN, int A_STAGES, int B_STAGES, bool RES>
