@@ -945,7 +945,7 @@ bool encode_out_rows(CUtensorMap* m, void* y, const ConvPlan& cp) {
 // buffers of a two-operand epilogue leave room for two
 template <int EV>
 constexpr int opt_stages() {
-  return ev_operands(EV) == 1 ? 3 : 2;
+  return ev_operands(EV) == 1 ? 4 : 2;
 }
 
 // DELTA_EPI_TMA=0 keeps the fused epilogue operands on the cp.async ring
@@ -1120,6 +1120,9 @@ cudaError_t conv_forward(const ConvPlan& cp, const void* x, void* y, float* stat
       if (!e.add) return cudaErrorInvalidValue;
       ev = e.out_mask ? EV_ADD_OM : EV_ADD;
     }
+    if (cp.bn == 256 && ev == EV_BN_BWD)
+      return tma_a ? launch<256, 3, MODE_TMA, EV_BN_BWD>(cp, x, y, stats, e, st)
+                   : launch<256, 3, MODE_IM2COL, EV_BN_BWD>(cp, x, y, stats, e, st);
     if (cp.bn != 64 && cp.bn != 128) return cudaErrorInvalidValue;
     if (e.add_stride2 && (ev == EV_POOL || ev == EV_BN_BWD || (cp.P & 1) || (cp.Q & 1)))
       return cudaErrorInvalidValue;

@@ -37,6 +37,7 @@ BN_EPS = 1e-5
 # pass.  0 = every conv (measured A/B on one box with 8 epilogue warps:
 # 11.57k vs 11.44k img/s; with 4 epilogue warps it was a wash, hence the old 384).
 OWN_DGRAD_3X3 = __import__("os").environ.get("DELTA_OWN_DGRAD_3X3", "1") == "1"
+DGRAD_BN256 = __import__("os").environ.get("DELTA_DGRAD_BN256", "1") == "1"
 FUSE_STATS_MIN_KDIM = int(__import__("os").environ.get("DELTA_FUSE_STATS_MIN_KDIM", "0"))
 BN_MOMENTUM = 0.1
 _TORCH_OPTIM = __import__("os").environ.get("DELTA_TORCH_OPTIM", "0") == "1"
@@ -291,6 +292,7 @@ class DeltaRuntime:
         self._fuse_stats = {}
         self._dconvs = {}
         self._wgrads = {}
+        bn_bwd_convs = {n.attrs["conv"] for n in self.nodes if n.op == "conv_bn_relu_bwd"}
         for n in self.nodes:
             if n.op == "conv":
                 cs = self.g.convs[n.attrs["conv"]]
@@ -311,7 +313,12 @@ class DeltaRuntime:
                     dconv = K.Conv(Nb, P_, Q_, cs.cout, cs.cin, cs.k, cs.k, 1, cs.k // 2,
                                    _ptr(self.params.wd[cs.name]))
                     if dconv.tile_n > 128:
-                        dconv.set_tile_n(128)  # fused backward epilogues
+                        # fused backward epilogues run at N tiles of 128, except
+                        # the BN-backward one at >= 2 waves of 256-column tiles
+                        # (layer 3: 65 -> 52 us per 3x3, 44 -> 40 per 1x1)
+                        wide = (DGRAD_BN256 and cs.name in bn_bwd_convs
+                                and Nb * P_ * Q_ >= 2 * 148 * 128)
+                        dconv.set_tile_n(256 if wide else 128)
                     self._dconvs[cs.name] = dconv
 
     def trace(self) -> P.Trace:

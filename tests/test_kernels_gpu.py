@@ -261,7 +261,7 @@ DGRAD_CASES = [
 ]
 
 
-def _dgrad_setup(case, seed):
+def _dgrad_setup(case, seed, tile_n=128):
     N, H, W, Cin, Kout, R = case
     g = torch.Generator(device="cuda").manual_seed(seed)
     w = (torch.randn(Kout, R, R, Cin, device="cuda", generator=g) / (R * R * Kout) ** 0.5).to(torch.bfloat16)
@@ -269,8 +269,8 @@ def _dgrad_setup(case, seed):
     wd = w.flip(1, 2).permute(3, 1, 2, 0).contiguous()        # [C][R][S][K]
     conv = K.Conv(N, H, W, Kout, Cin, R, R, 1, R // 2, wd.data_ptr())
     conv.keep = wd  # the handle caches a descriptor of wd's memory: keep it alive
-    if conv.tile_n > 128:
-        conv.set_tile_n(128)
+    if conv.tile_n > tile_n:
+        conv.set_tile_n(tile_n)
     ref = torch.nn.grad.conv2d_input((N, Cin, H, W), w.permute(0, 3, 1, 2).float(),
                                      dy.permute(0, 3, 1, 2).float(), padding=R // 2)
     return g, w, dy, conv, ref.permute(0, 2, 3, 1).contiguous()
@@ -309,11 +309,13 @@ def test_dgrad_and_add_mask_epilogue(case):
     _close(y2, (ref + up) * (om.float() > 0), "pooled add")
 
 
-@pytest.mark.parametrize("case", DGRAD_CASES[:4])
-def test_dgrad_bn_backward_epilogue(case):
+@pytest.mark.parametrize("case,tile_n", [(c, 128) for c in DGRAD_CASES[:4]]
+                         + [(c, 256) for c in DGRAD_CASES if c[3] >= 256])
+def test_dgrad_bn_backward_epilogue(case, tile_n):
     """g = dgrad * [relu(bn(xc)) > 0] bit-exact against the plain dgrad masked
-    by OUR forward BN-ReLU output; partials -> dgamma/dbeta/dx vs autograd."""
-    g, w, dy, conv, ref = _dgrad_setup(case, 8)
+    by OUR forward BN-ReLU output; partials -> dgamma/dbeta/dx vs autograd.
+    tile_n 256: the wide-tile BN-backward variant (cp.async operand ring)."""
+    g, w, dy, conv, ref = _dgrad_setup(case, 8, tile_n)
     N, H, W, C = ref.shape
     M = N * H * W
     xc = (torch.randn(M, C, device="cuda", generator=g) * 1.5 + 0.2).to(torch.bfloat16)
