@@ -153,12 +153,24 @@ __device__ __forceinline__ float2 rows_sum8(const T* __restrict__ ws, int rows, 
   __shared__ float2 part[32][9];
   const int ch = threadIdx.x & 7, stripe = threadIdx.x >> 3;
   float2 acc = make_float2(0.f, 0.f);
-  if (c0 + ch < C)
-    for (int k = stripe; k < rows; k += 32) {
-      const float2 v = term(ws[int64_t(k) * C + c0 + ch]);
-      acc.x += v.x;
-      acc.y += v.y;
+  if (c0 + ch < C) {
+    // RB rows in flight per thread (the loop is load-latency bound), summed
+    // in the same k order as one row at a time
+    constexpr int RB = 8;
+    for (int k0 = stripe; k0 < rows; k0 += 32 * RB) {
+      T v[RB];
+#pragma unroll
+      for (int b = 0; b < RB; ++b)
+        if (k0 + b * 32 < rows) v[b] = ws[int64_t(k0 + b * 32) * C + c0 + ch];
+#pragma unroll
+      for (int b = 0; b < RB; ++b)
+        if (k0 + b * 32 < rows) {
+          const float2 t = term(v[b]);
+          acc.x += t.x;
+          acc.y += t.y;
+        }
     }
+  }
   part[stripe][ch] = acc;
   __syncthreads();
   float2 r = make_float2(0.f, 0.f);
