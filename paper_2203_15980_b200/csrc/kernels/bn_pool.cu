@@ -395,12 +395,11 @@ __device__ __forceinline__ void unpack_up(uint4 u, float inv_hw, float (&g)[8]) 
 // invstd*(sum g*x - mean*sum g)), so no per-channel parameters stay live in
 // the loop and occupancy is not register-limited.
 template <bool MASKED, bool POOLED>
-__global__ void __launch_bounds__(256)
-    k_bn_bwd_partial(const bf16* __restrict__ up, int pool_hw, const bf16* __restrict__ mask,
-                     const bf16* __restrict__ x, int64_t M, int C, int64_t chunk,
-                     const float* mean, const float* invstd, float2* __restrict__ ws) {
-  pdl_wait();
-  pdl_trigger();
+__device__ __forceinline__ void bn_bwd_chunk(const bf16* __restrict__ up, int pool_hw,
+                                             const bf16* __restrict__ mask,
+                                             const bf16* __restrict__ x, int64_t M, int C,
+                                             int64_t chunk, const float* mean,
+                                             const float* invstd, float2* __restrict__ ws) {
   const int tpr = C >> 3, rpi = 256 / tpr;
   const int tx = threadIdx.x % tpr, ty = threadIdx.x / tpr;
   const int c0 = tx * 8;
@@ -453,6 +452,124 @@ __global__ void __launch_bounds__(256)
     }
     // sum g*xhat over the chunk = invstd * (sum g*x - mean * sum g)
     ws[int64_t(blockIdx.x) * C + c] = make_float2(A, invstd[c] * (B - mean[c] * A));
+  }
+}
+
+template <bool MASKED, bool POOLED>
+__global__ void __launch_bounds__(256)
+    k_bn_bwd_partial(const bf16* __restrict__ up, int pool_hw, const bf16* __restrict__ mask,
+                     const bf16* __restrict__ x, int64_t M, int C, int64_t chunk,
+                     const float* mean, const float* invstd, float2* __restrict__ ws) {
+  pdl_wait();
+  pdl_trigger();
+  bn_bwd_chunk<MASKED, POOLED>(up, pool_hw, mask, x, M, C, chunk, mean, invstd, ws);
+}
+
+// Grid-wide barrier for a grid whose CTAs are all co-resident (sized by the
+// occupancy API): generation counter, the last CTA to arrive resets the count
+// and then releases the others; reusable across launches without a memset.
+__device__ unsigned int g_bar_count;
+__device__ unsigned int g_bar_gen;
+__device__ __forceinline__ void grid_barrier() {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned int gen;
+    asm volatile("ld.acquire.gpu.u32 %0, [%1];" : "=r"(gen) : "l"(&g_bar_gen) : "memory");
+    __threadfence();
+    if (atomicAdd(&g_bar_count, 1u) == gridDim.x - 1) {
+      atomicExch(&g_bar_count, 0u);
+      __threadfence();
+      atomicAdd(&g_bar_gen, 1u);
+    } else {
+      unsigned int g;
+      do {
+        asm volatile("ld.acquire.gpu.u32 %0, [%1];" : "=r"(g) : "l"(&g_bar_gen) : "memory");
+      } while (g == gen);
+    }
+    __threadfence();
+  }
+  __syncthreads();
+}
+
+// The whole BN backward in one persistent launch (all CTAs resident):
+//   1. per-CTA (sum g, sum g*xhat) over a contiguous chunk of rows (bn_bwd_chunk)
+//   2. grid barrier; channel c's sums over the CTA rows by one warp, in a fixed
+//      order (lane-strided, xor butterfly) -> dbeta, dgamma
+//   3. grid barrier; dx over the SAME chunk, last rows first, so the tail of
+//      what phase 1 streamed is still in L2.
+// Saves the merge launch and, per CTA, up to an L2's share of the second read.
+template <bool MASKED, bool POOLED>
+__global__ void __launch_bounds__(256)
+    k_bn_bwd_grid(const bf16* __restrict__ up, int pool_hw, const bf16* __restrict__ mask,
+                  const bf16* __restrict__ x, bf16* __restrict__ dx, int64_t M, int C,
+                  int64_t chunk, const float* __restrict__ mean,
+                  const float* __restrict__ invstd, const float* __restrict__ gamma,
+                  float* dgamma, float* dbeta, float2* ws) {
+  pdl_wait();
+  bn_bwd_chunk<MASKED, POOLED>(up, pool_hw, mask, x, M, C, chunk, mean, invstd, ws);
+  grid_barrier();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int c = blockIdx.x * 8 + warp; c < C; c += gridDim.x * 8) {
+    float A = 0.f, B = 0.f;
+    for (int k = lane; k < int(gridDim.x); k += 32) {
+      const float2 p = __ldcg(ws + int64_t(k) * C + c);
+      A += p.x;
+      B += p.y;
+    }
+    A = warp_sum(A);
+    B = warp_sum(B);
+    if (lane == 0) {
+      dbeta[c] = A;
+      dgamma[c] = B;
+    }
+  }
+  grid_barrier();
+  pdl_trigger();
+  const int tpr = C >> 3, rpi = 256 / tpr;
+  const int tx = threadIdx.x % tpr, ty = threadIdx.x / tpr;
+  const int c0 = tx * 8;
+  const float invM = 1.f / float(M);
+  float k1[8], k2[8], k3[8];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    const float is = invstd[c0 + j];
+    const float a = gamma[c0 + j] * is;
+    const float kd = __ldcg(dgamma + c0 + j) * invM * is;
+    k1[j] = a;
+    k2[j] = -a * kd;
+    k3[j] = a * (kd * mean[c0 + j] - __ldcg(dbeta + c0 + j) * invM);
+  }
+  const float inv_hw = POOLED ? 1.f / float(pool_hw) : 1.f;
+  const int64_t r0 = int64_t(blockIdx.x) * chunk;
+  const int64_t r1 = min(M, r0 + chunk);
+  for (int64_t rb = r1 - 1 - ty; rb >= r0; rb -= UNROLL * rpi) {
+    uint4 uv[UNROLL], mv[UNROLL], xv[UNROLL];
+#pragma unroll
+    for (int u = 0; u < UNROLL; ++u) {
+      const int64_t r = rb - u * rpi;
+      if (r >= r0) {
+        uv[u] = load_up<POOLED>(up, pool_hw, r, c0, C);
+        if (MASKED) mv[u] = ld_stream(mask + r * C + c0);
+        xv[u] = ld_stream(x + r * C + c0);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < UNROLL; ++u) {
+      const int64_t r = rb - u * rpi;
+      if (r < r0) break;
+      float g[8], xf[8];
+      unpack_up<POOLED>(uv[u], inv_hw, g);
+      if (MASKED) {
+        float m[8];
+        unpack8(mv[u], m);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) g[j] = m[j] > 0.f ? g[j] : 0.f;
+      }
+      unpack8(xv[u], xf);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) g[j] = fmaf(k1[j], g[j], fmaf(k2[j], xf[j], k3[j]));
+      *reinterpret_cast<uint4*>(dx + r * C + c0) = pack8(g);
+    }
   }
 }
 
@@ -916,16 +1033,50 @@ cudaError_t bn_apply(int mode, const void* x, const void* res, void* y, int64_t 
   return cudaGetLastError();
 }
 
+// DELTA_BN_BWD_GRID=0: the three-launch BN backward (partial, merge, apply)
+bool bn_bwd_one_launch() {
+  static const bool on = [] {
+    const char* e = std::getenv("DELTA_BN_BWD_GRID");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
+// CTAs of `kernel` (block threads, no dynamic smem) resident at once on the
+// current device, capped by the workspace's partial rows (bn_workspace_floats)
+template <typename K>
+int resident_ctas(K kernel, int threads) {
+  int dev = 0, sms = 0, per_sm = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, threads, 0);
+  const int cap = sms * (per_sm > 0 ? per_sm : 1);
+  return cap < 148 * 8 ? cap : 148 * 8;
+}
+
 cudaError_t bn_backward(const void* up, int pool_hw, const void* mask, const void* x, void* dx,
                         int64_t M, int C, const float* mean, const float* invstd,
                         const float* gamma, float* dgamma, float* dbeta, float* ws,
                         cudaStream_t st) {
   if (C % SLICE || (C & (C - 1)) || C > 2048) return cudaErrorInvalidValue;
-  const int64_t chunk = chunk_rows(M, C);
-  const int chunks = int((M + chunk - 1) / chunk);
   auto U = static_cast<const bf16*>(up);
   auto Mk = static_cast<const bf16*>(mask);
   auto X = static_cast<const bf16*>(x);
+  if (bn_bwd_one_launch()) {
+    const auto k = Mk ? (pool_hw ? k_bn_bwd_grid<true, true> : k_bn_bwd_grid<true, false>)
+                      : (pool_hw ? k_bn_bwd_grid<false, true> : k_bn_bwd_grid<false, false>);
+    const int cap = resident_ctas(k, 256);
+    int64_t chunk = (M + cap - 1) / cap;
+    chunk = (chunk + 15) / 16 * 16;
+    const int grid = int((M + chunk - 1) / chunk);
+    if (cudaError_t e_ = launch_k(k, dim3(grid), dim3(256), 0, st, U, pool_hw, Mk, X,
+                                  static_cast<bf16*>(dx), M, C, chunk, mean, invstd, gamma,
+                                  dgamma, dbeta, reinterpret_cast<float2*>(ws)))
+      return e_;
+    return cudaGetLastError();
+  }
+  const int64_t chunk = chunk_rows(M, C);
+  const int chunks = int((M + chunk - 1) / chunk);
   const auto part = Mk ? (pool_hw ? k_bn_bwd_partial<true, true> : k_bn_bwd_partial<true, false>)
                       : (pool_hw ? k_bn_bwd_partial<false, true> : k_bn_bwd_partial<false, false>);
   if (cudaError_t e_ = launch_k(part, dim3(chunks), dim3(256), 0, st, U, pool_hw, Mk, X, M, C, chunk, mean, invstd, reinterpret_cast<float2*>(ws))) return e_;
