@@ -683,26 +683,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         if (a.stats != nullptr) {
           // column `lane` of this 32x32 block, from the staged bf16 values
-          // (exactly what is stored); rows past M are zeros.
-          const uint32_t cbyte = (uint32_t(lane) & 7u) * 2u;
-          const uint32_t c16 = uint32_t(lane) >> 3;
-          float sum = 0.f, sq = 0.f;
-#pragma unroll 8
-          for (int rr = 0; rr < 32; ++rr) {
-            const uint32_t off = rr * 64 + ((c16 ^ ((rr >> 1) & 3)) << 4) + cbyte;
-            uint16_t h;
-            asm volatile("ld.shared.u16 %0, [%1];" : "=h"(h) : "r"(buf + off));
-            const float f = __bfloat162float(__ushort_as_bfloat16(h));
-            sum += f;
-            if constexpr (EV == EV_BN_BWD) {
-              // (sum g, sum g*xc): xc from the operand ring (same layout)
-              uint16_t hx;
-              asm volatile("ld.shared.u16 %0, [%1];" : "=h"(hx) : "r"(sb + off));
-              sq = fmaf(f, __bfloat162float(__ushort_as_bfloat16(hx)), sq);
-            } else {
-              sq = fmaf(f, f, sq);
-            }
-          }
+          // (exactly what is stored); rows past M are zeros.  BN backward:
+          // (sum g, sum g*xc), xc from the operand buffer (same layout)
+          const float2 cs = column_sums32<EV == EV_BN_BWD>(buf, sb, 0xFFFFFFFFu, lane);
+          const float sum = cs.x, sq = cs.y;
           if (reg_stats) {
             const int nq = min(max((row_tiled(MODE) ? a.Q : min(BM, a.M - m0)) - quarter * 32, 0), 32);
             const int jj = (j - half) / HALVES;

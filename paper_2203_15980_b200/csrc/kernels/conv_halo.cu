@@ -213,21 +213,10 @@ __global__ void __launch_bounds__(HT, 1)
           bulk_commit();
         }
         if (a.stats != nullptr) {
-          // column `lane`, over this warp's valid rows (pixel column < Q)
-          const uint32_t cbyte = (uint32_t(lane) & 7u) * 2u;
-          const uint32_t c16 = uint32_t(lane) >> 3;
-          float sum = 0.f, sq = 0.f;
-#pragma unroll 8
-          for (int rr = 0; rr < 32; ++rr) {
-            uint16_t h;
-            asm volatile("ld.shared.u16 %0, [%1];"
-                         : "=h"(h)
-                         : "r"(buf + rr * 64 + ((c16 ^ ((rr >> 1) & 3)) << 4) + cbyte));
-            const float f = __bfloat162float(__ushort_as_bfloat16(h));
-            const float g = (vmask >> rr) & 1u ? f : 0.f;  // garbage rows may hold anything
-            sum += g;
-            sq = fmaf(g, g, sq);
-          }
+          // column `lane`, over this warp's valid rows (pixel column < Q;
+          // garbage rows may hold anything)
+          const float2 cs = column_sums32<false>(buf, buf, vmask, lane);
+          const float sum = cs.x, sq = cs.y;
           if (reg_stats) {
             const float nq = float(__popc(vmask));
             if (nq > 0.f) racc[j] = stats_merge_tile<false>(racc[j], nq, sum, sq);

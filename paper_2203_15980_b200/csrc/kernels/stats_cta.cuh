@@ -60,4 +60,47 @@ __device__ __forceinline__ void stats_fold_tile(float4* stats, int K, int col, f
   *p = stats_merge_tile<SUMS>(*p, n_t, S, Q);
 }
 
+// Column sums of a 32x32 bf16 block staged with the 64B swizzle (row r at
+// byte r*64, its 16 B chunk c at ((c ^ ((r >> 1) & 3)) << 4)) — the epilogue's
+// TMA-store staging layout.  Lane c returns (sum of column c, sum of column c
+// times the same column of `obuf` (CROSS: BN backward's sum g*xc) or of
+// itself (sum of squares)) over the rows set in `rowmask`.  Each lane walks a
+// column PAIR over every other row with packed fp32 math (FADD2/FFMA2), the
+// two row parities are combined by one xor shuffle and the pairs spread back
+// to one column per lane: fixed order, deterministic.
+template <bool CROSS>
+__device__ __forceinline__ float2 column_sums32(uint32_t buf, uint32_t obuf, uint32_t rowmask,
+                                                int lane) {
+  const int pr = lane >> 4;        // row parity
+  const uint32_t cp = lane & 15;   // columns 2cp, 2cp + 1
+  const uint32_t cb = (cp & 3u) * 4u, c16 = cp >> 2;
+  float2 s = make_float2(0.f, 0.f), q = make_float2(0.f, 0.f);
+#pragma unroll 8
+  for (int i = 0; i < 16; ++i) {
+    const int rr = 2 * i + pr;
+    const uint32_t off = rr * 64 + ((c16 ^ ((rr >> 1) & 3)) << 4) + cb;
+    uint32_t w;
+    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(w) : "r"(buf + off));
+    if (!((rowmask >> rr) & 1u)) w = 0u;
+    const float2 f = make_float2(__uint_as_float(w << 16), __uint_as_float(w & 0xFFFF0000u));
+    s = __fadd2_rn(s, f);
+    if (CROSS) {
+      uint32_t wx;
+      asm volatile("ld.shared.u32 %0, [%1];" : "=r"(wx) : "r"(obuf + off));
+      const float2 x = make_float2(__uint_as_float(wx << 16), __uint_as_float(wx & 0xFFFF0000u));
+      q = __ffma2_rn(f, x, q);
+    } else {
+      q = __ffma2_rn(f, f, q);
+    }
+  }
+  s.x += __shfl_xor_sync(0xffffffffu, s.x, 16);
+  s.y += __shfl_xor_sync(0xffffffffu, s.y, 16);
+  q.x += __shfl_xor_sync(0xffffffffu, q.x, 16);
+  q.y += __shfl_xor_sync(0xffffffffu, q.y, 16);
+  const int src = lane >> 1;
+  const float s0 = __shfl_sync(0xffffffffu, s.x, src), s1 = __shfl_sync(0xffffffffu, s.y, src);
+  const float q0 = __shfl_sync(0xffffffffu, q.x, src), q1 = __shfl_sync(0xffffffffu, q.y, src);
+  return (lane & 1) ? make_float2(s1, q1) : make_float2(s0, q0);
+}
+
 }  // namespace delta_k
