@@ -131,8 +131,16 @@ constexpr int EV_ADD = 1;      // y = bf16(acc) + add
 constexpr int EV_ADD_OM = 2;   // y = (bf16(acc) + add) & [out_mask > 0]
 constexpr int EV_POOL = 3;     // y = bf16(acc + pooled/hw * [add_mask > 0]) & [out_mask > 0]
 constexpr int EV_BN_BWD = 4;   // y = g = bf16(acc) & [relu(bn(xc)) > 0]; partials (sum g, sum g*xc)
+constexpr int EV_ADD_OM_ST = 5;  // EV_ADD_OM + partials (sum y, sum y*xc): the next BN's backward sums
 __host__ __device__ constexpr int ev_operands(int ev) {
-  return ev == EV_ADD || ev == EV_BN_BWD ? 1 : (ev == EV_ADD_OM || ev == EV_POOL ? 2 : 0);
+  return ev == EV_ADD || ev == EV_BN_BWD
+             ? 1
+             : (ev == EV_ADD_OM || ev == EV_POOL ? 2 : (ev == EV_ADD_OM_ST ? 3 : 0));
+}
+// epilogues whose statistics are (sum y, sum y*xc) rather than (count, mean, M2)
+__host__ __device__ constexpr bool ev_cross(int ev) { return ev == EV_BN_BWD || ev == EV_ADD_OM_ST; }
+__host__ __device__ constexpr bool ev_adds(int ev) {
+  return ev == EV_ADD || ev == EV_ADD_OM || ev == EV_ADD_OM_ST;
 }
 
 // bf16x2 lanes positive (> +0) -> 0xFFFF, else 0 (bf16 bit patterns read as
@@ -162,7 +170,8 @@ template <int BN, int STAGES, int MODE, int EV, bool OPT = false>
 __global__ void __launch_bounds__(kThreads, 1)
     k_conv_fwd(const __grid_constant__ CUtensorMap wmap, const __grid_constant__ CUtensorMap amap,
                const __grid_constant__ CUtensorMap ymap, const __grid_constant__ CUtensorMap emap0,
-               const __grid_constant__ CUtensorMap emap1, const ConvArgs a) {
+               const __grid_constant__ CUtensorMap emap1, const __grid_constant__ CUtensorMap emap2,
+               const ConvArgs a) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = align1024(smem_raw);
   // producer signalling lag: a thread keeps LAG+1 stages of gathers in flight
@@ -180,6 +189,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   constexpr uint32_t EPI_RING_WARP = epi_ring_bytes<BN, STAGES>() / EPI_W;
   constexpr int NOPS_ = ev_operands(EV);
   constexpr uint32_t OPT_TILE = uint32_t(NOPS_) * BN * 256;  // per tile: NOPS x [128][BN] bf16
+  static_assert(EV != EV_ADD_OM_ST || OPT, "three-operand epilogue: TMA-loaded operands only");
   constexpr uint32_t IN_BYTES = !FUSED ? 0 : (OPT ? OPT_NB * OPT_TILE : EPI_W * EPI_RING_WARP);
   const uint32_t sIn = sOut + 16384;
   // BN-statistics scratch: per quarter-warp column (sum, sumsq), [4][BN] float2
@@ -217,7 +227,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     fence_mbar_init();
     if (OPT) {
       tma_prefetch_desc(&emap0);
-      if (NOPS_ == 2) tma_prefetch_desc(&emap1);
+      if (NOPS_ >= 2) tma_prefetch_desc(&emap1);
+      if (NOPS_ == 3) tma_prefetch_desc(&emap2);
     }
     tma_prefetch_desc(&wmap);
     if (!gathers(MODE)) tma_prefetch_desc(&amap);
@@ -261,8 +272,10 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
             for (int j = 0; j < BN / 32; ++j) {
               tma_load_2d(base + j * 8192, &emap0, &ofull[b], n0 + j * 32, m0);
-              if (NOPS_ == 2)
+              if (NOPS_ >= 2)
                 tma_load_2d(base + BN * 256 + j * 8192, &emap1, &ofull[b], n0 + j * 32, m0);
+              if (NOPS_ == 3)
+                tma_load_2d(base + 2 * BN * 256 + j * 8192, &emap2, &ofull[b], n0 + j * 32, m0);
             }
           }
         }
@@ -504,7 +517,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int pc = (tile_ % a.n_tiles) * BN + (half + int(e % CHW) * HALVES) * 32;
         // stride-2 add: (n, p, q) of the block's first row, once per chunk
         int q0 = 0, p0 = 0, n0_ = 0;
-        if ((EV == EV_ADD || EV == EV_ADD_OM) && a.e.add_stride2) {
+        if (ev_adds(EV) && a.e.add_stride2) {
           q0 = pm % a.Q;
           const int t = pm / a.Q;
           p0 = t % a.P;
@@ -517,7 +530,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           const bool ok = m < a.M;
           const int64_t go = int64_t(ok ? m : 0) * a.K + pc + u * 8;
           const uint32_t so = r * 64 + ((u ^ ((r >> 1) & 3)) << 4);
-          if ((EV == EV_ADD || EV == EV_ADD_OM) && a.e.add_stride2) {
+          if (ev_adds(EV) && a.e.add_stride2) {
             // the add is the input gradient of a stride-2 1x1 conv, given at
             // its [N][P/2][Q/2] sampling points: zero at odd rows/columns
             int q = q0 + r, pp = p0, n = n0_;
@@ -611,7 +624,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           pk[u].z = pack_bf16x2(v[u * 8 + 4], v[u * 8 + 5]);
           pk[u].w = pack_bf16x2(v[u * 8 + 6], v[u * 8 + 7]);
         }
-        if constexpr (EV == EV_ADD || EV == EV_ADD_OM) {
+        if constexpr (ev_adds(EV)) {
 #pragma unroll
           for (int u = 0; u < 4; ++u) {
             const uint4 ad = ld_row16(sb, lane, u);
@@ -621,7 +634,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             pk[u].w = add_bf16x2(pk[u].w, ad.w);
           }
         }
-        if constexpr (EV == EV_ADD_OM || EV == EV_POOL) {
+        if constexpr (EV == EV_ADD_OM || EV == EV_POOL || EV == EV_ADD_OM_ST) {
 #pragma unroll
           for (int u = 0; u < 4; ++u) {
             const uint4 om = ld_row16(sb + OP1, lane, u);
@@ -685,18 +698,19 @@ __global__ void __launch_bounds__(kThreads, 1)
           // column `lane` of this 32x32 block, from the staged bf16 values
           // (exactly what is stored); rows past M are zeros.  BN backward:
           // (sum g, sum g*xc), xc from the operand buffer (same layout)
-          const float2 cs = column_sums32<EV == EV_BN_BWD>(buf, sb, 0xFFFFFFFFu, lane);
+          const float2 cs = column_sums32<ev_cross(EV)>(
+              buf, EV == EV_ADD_OM_ST ? sb + 2 * OP1 : sb, 0xFFFFFFFFu, lane);
           const float sum = cs.x, sq = cs.y;
           if (reg_stats) {
             const int nq = min(max((row_tiled(MODE) ? a.Q : min(BM, a.M - m0)) - quarter * 32, 0), 32);
             const int jj = (j - half) / HALVES;
-            if (EV == EV_BN_BWD || nq > 0)
-              racc[jj] = stats_merge_tile<EV == EV_BN_BWD>(racc[jj], float(nq), sum, sq);
+            if (ev_cross(EV) || nq > 0)
+              racc[jj] = stats_merge_tile<ev_cross(EV)>(racc[jj], float(nq), sum, sq);
           } else {
             red[quarter * BN + j * 32 + lane] = make_float2(sum, sq);
           }
         }
-        if constexpr (EV == EV_BN_BWD) __syncwarp();  // ring slot read by the stats pass
+        if constexpr (ev_cross(EV)) __syncwarp();  // ring slot read by the stats pass
       }
       if (a.stats != nullptr && !reg_stats) {
         // combine the four row quarters -> this tile's column partials, folded
@@ -712,7 +726,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             Q += red[qq * BN + c].y;
           }
           if (n0 + c < a.K)
-            stats_fold_tile<EV == EV_BN_BWD>(a.stats, a.K, n0 + c, float(n_rows), S, Q);
+            stats_fold_tile<ev_cross(EV)>(a.stats, a.K, n0 + c, float(n_rows), S, Q);
         }
         asm volatile("bar.sync 1, %0;" ::"n"(EPI_W * 32) : "memory");
       }
@@ -740,7 +754,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
         for (int qq = 1; qq < 4; ++qq) {
           const float4 b = qs[qq * BN + et];
-          if (EV == EV_BN_BWD) {
+          if (ev_cross(EV)) {
             r.x += b.x;
             r.y += b.y;
           } else {
@@ -1017,20 +1031,24 @@ cudaError_t launch(const ConvPlan& cp, const void* x, void* y, float* stats,
                            : !encode_out(&ymap, y, uint64_t(cp.K), uint64_t(a.M)))
     return cudaErrorInvalidValue;
   // OPT: the fused epilogue's [M][K] operands as 32-column x 128-row boxes
-  alignas(64) CUtensorMap emap0 = ymap, emap1 = ymap;
+  alignas(64) CUtensorMap emap0 = ymap, emap1 = ymap, emap2 = ymap;
   if (OPT) {
     const void* op0 = EV == EV_BN_BWD ? epi.xc : (EV == EV_POOL ? epi.add_mask : epi.add);
     if (!tma_2d_bf16(&emap0, op0, uint64_t(cp.K), uint64_t(a.M), uint64_t(cp.K), 32, BM,
                      CU_TENSOR_MAP_SWIZZLE_64B))
       return cudaErrorInvalidValue;
-    if (ev_operands(EV) == 2 &&
+    if (ev_operands(EV) >= 2 &&
         !tma_2d_bf16(&emap1, epi.out_mask, uint64_t(cp.K), uint64_t(a.M), uint64_t(cp.K), 32, BM,
+                     CU_TENSOR_MAP_SWIZZLE_64B))
+      return cudaErrorInvalidValue;
+    if (ev_operands(EV) == 3 &&
+        !tma_2d_bf16(&emap2, epi.xc, uint64_t(cp.K), uint64_t(a.M), uint64_t(cp.K), 32, BM,
                      CU_TENSOR_MAP_SWIZZLE_64B))
       return cudaErrorInvalidValue;
   }
   // statistics come as one partial row per CTA: always one CTA per SM then
   const int grid = (stats != nullptr || a.tiles > num_sms()) ? num_sms() : a.tiles;
-  if (cudaError_t e_ = launch_k(kern, dim3(grid), dim3(kThreads), smem, st, *reinterpret_cast<const CUtensorMap*>(cp.wmap), amap, ymap, emap0, emap1, a)) return e_;
+  if (cudaError_t e_ = launch_k(kern, dim3(grid), dim3(kThreads), smem, st, *reinterpret_cast<const CUtensorMap*>(cp.wmap), amap, ymap, emap0, emap1, emap2, a)) return e_;
   return cudaGetLastError();
 }
 
@@ -1103,6 +1121,12 @@ cudaError_t conv_forward(const ConvPlan& cp, const void* x, void* y, float* stat
     } else {
       if (!e.add) return cudaErrorInvalidValue;
       ev = e.out_mask ? EV_ADD_OM : EV_ADD;
+      // + the following BN backward's sums (sum y, sum y*xc): three TMA-loaded
+      // operands, 64-column N tiles (the operand tiles of two tiles in flight)
+      if (e.out_mask && e.xc && stats) {
+        if (!tma_a || e.add_stride2 || cp.bn != 64 || !operands_tma()) return cudaErrorInvalidValue;
+        return launch<64, 4, MODE_TMA, EV_ADD_OM_ST, true>(cp, x, y, stats, e, st);
+      }
     }
     if (cp.bn == 256 && ev == EV_BN_BWD)
       return tma_a ? launch<256, 3, MODE_TMA, EV_BN_BWD>(cp, x, y, stats, e, st)

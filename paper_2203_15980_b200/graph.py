@@ -13,9 +13,13 @@ the arena alignment so trace bytes == arena allocation bytes.
 """
 from __future__ import annotations
 
+import os
 from dataclasses import dataclass, field
 
 ALIGN = 256
+# the shortcut dgrad's epilogue also reduces the next BN3 backward's sums
+# (DELTA_FUSE_BN3_SUMS=0: a separate partial pass)
+FUSE_BN3_SUMS = os.environ.get("DELTA_FUSE_BN3_SUMS", "1") == "1"
 
 
 def rnd(b: int) -> int:
@@ -160,14 +164,17 @@ def build_resnet(depth: int = 50, batch: int = 256, image: int = 224,
     # pooled head gradient of the last block, masked where it is consumed.
     upstream = d_pool
     upstream_is_pool = True
+    upstream_sums = False
     first = blocks[0][0]
-    for (pre, X, C1, R1, C2, R2, C3, CD, O) in reversed(blocks):
+    for bi in reversed(range(len(blocks))):
+        (pre, X, C1, R1, C2, R2, C3, CD, O) = blocks[bi]
         bn_parents = (lambda t: [upstream.id, O.id, t.id]) if upstream_is_pool else \
             (lambda t: [upstream.id, t.id])
         extra = dict(from_pool=upstream_is_pool, masked=upstream_is_pool)
         d_c3 = g.add(pre + ".bn3.bwd", "bn_add_relu_bwd", C3.shape, bn_parents(C3), phase="B",
-                     attrs=dict(bn=pre + ".bn3", **extra))
-        d_c3.hbm_bytes = (6 if upstream_is_pool else 5) * C3.nbytes
+                     attrs=dict(bn=pre + ".bn3", sums_fused=upstream_sums, **extra))
+        # sums fused upstream: read g and X, write dX; else a partial pass first
+        d_c3.hbm_bytes = (3 if upstream_sums else (6 if upstream_is_pool else 5)) * C3.nbytes
         d_cd = None
         if CD is not None:
             d_cd = g.add(pre + ".downsample.1.bwd", "bn_add_relu_bwd", CD.shape, bn_parents(CD),
@@ -199,12 +206,22 @@ def build_resnet(depth: int = 50, batch: int = 256, image: int = 224,
         else:
             parents = [d_c1.id, X.id, upstream.id]
             attrs = dict(conv=pre + ".conv1", from_pool=False, mask_out=mask_out)
+        # The gradient written here is the previous block's BN3 backward input:
+        # with a plain (full, stride-1) add and a previous block without a
+        # downsample BN, its epilogue also reduces (sum g, sum g*C3) for that
+        # BN3 — C3 becomes a parent (read by this node).
+        prev = blocks[bi - 1] if bi > 0 else None
+        upstream_sums = (FUSE_BN3_SUMS and prev is not None and prev[7] is None and mask_out
+                         and CD is None and not upstream_is_pool)
+        if upstream_sums:
+            attrs["sums_xc"] = len(parents)
+            parents = parents + [prev[6].id]
         d_x = g.add(pre + ".conv1.bwd", "conv_shortcut_bwd", X.shape, parents, phase="B",
                     attrs=attrs)
         d_x.flops = 2 * C1.flops + (2 * CD.flops if CD is not None else 0)
         # conv1 dgrad (read dY, write dX) + residual add + ReLU mask reads +
         # weight gradient (dY, X); the downsample's dgrad and wgrad likewise
-        d_x.hbm_bytes = 2 * d_c1.nbytes + 4 * X.nbytes + \
+        d_x.hbm_bytes = 2 * d_c1.nbytes + (5 if upstream_sums else 4) * X.nbytes + \
             (2 * d_cd.nbytes + 2 * X.nbytes if CD is not None else 0)
         upstream = d_x
         upstream_is_pool = False

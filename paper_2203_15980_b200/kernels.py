@@ -5,6 +5,7 @@ fallback: if libdelta or a CUDA launch fails, the call raises."""
 from __future__ import annotations
 
 import ctypes as C
+import os
 
 from ._lib import check, lib
 
@@ -96,13 +97,15 @@ class Conv:
         self.tile_n = tile_n
 
     def add_mask(self, x_ptr, y_ptr, stream, add=None, pool_hw=0, add_mask=None, out_mask=None,
-                 add_stride2=False):
+                 add_stride2=False, xc=None, partials_ptr=None):
         """y = (conv(x) + add') * [out_mask > 0]; add' = add, or the pooled add
         / pool_hw * [add_mask > 0] (add_mask is only read with a pooled add),
-        or (add_stride2) an [N,P/2,Q/2,K] add placed at the even rows/columns."""
+        or (add_stride2) an [N,P/2,Q/2,K] add placed at the even rows/columns.
+        xc + partials_ptr (full add, out_mask, tile_n 64): also the per-CTA
+        (sum y, sum y*xc) rows of the BN backward that consumes y."""
         e = ConvEpilogue(EPI_ADD_MASK, pool_hw, int(add_stride2), 0, add, add_mask, out_mask,
-                         None, None, None, None, None)
-        check(lib.delta_conv_forward_ex(self._h, x_ptr, y_ptr, None, C.byref(e), stream))
+                         xc, None, None, None, None)
+        check(lib.delta_conv_forward_ex(self._h, x_ptr, y_ptr, partials_ptr, C.byref(e), stream))
         _count(1)
 
     def bn_bwd(self, x_ptr, g_ptr, partials_ptr, xc, mean, invstd, gamma, beta, stream):
@@ -156,6 +159,10 @@ def pack_stem_weights(w_krsc, out=None):
 
 def bn_workspace_floats(M: int, C_: int) -> int:
     return lib.delta_bn_workspace_floats(M, C_)
+
+
+# bn_pool.cu bn_bwd_one_launch(): the streaming BN backward as one persistent launch
+BN_BWD_ONE_LAUNCH = os.environ.get("DELTA_BN_BWD_GRID", "1") != "0"
 
 
 def _merge_launches(parts: int) -> int:
@@ -223,7 +230,7 @@ def weight_views(table_dev, n, stream):
 def bn_backward(up, pool_hw, mask, x, dx, M, C_, mean, invstd, gamma, dgamma, dbeta, ws, stream):
     check(lib.delta_bn_backward(up, pool_hw, mask, x, dx, M, C_, mean, invstd, gamma, dgamma,
                                 dbeta, ws, stream))
-    _count(2 + _merge_launches(_chunks(M, C_)))
+    _count(1 if BN_BWD_ONE_LAUNCH else 2 + _merge_launches(_chunks(M, C_)))
 
 
 def bn_backward_from_partials(partials, g, x, dx, M, C_, mean, invstd, gamma, dgamma, dbeta,

@@ -185,7 +185,7 @@ def workspace_plan(g: G.Graph) -> dict:
     # BN-statistics partials: one (count, mean, M2) row per CTA of the conv
     parts = 4 * max(K.stats_partials_floats(n.shape[-1]) for n in nodes
                     if n.op in ("conv", "conv_bn_relu_bwd"))
-    ws["stats_main"] = ws["stats_ds"] = parts
+    ws["stats_main"] = ws["stats_ds"] = ws["stats_sums"] = parts
     short = [nodes[n.parents[2]].nbytes * g.convs[n.attrs["conv_short"]].cin
              // g.convs[n.attrs["conv_short"]].cout for n in nodes
              if n.op == "conv_shortcut_bwd" and "conv_short" in n.attrs
@@ -257,6 +257,8 @@ class DeltaRuntime:
         # their BN is applied together with the block's bn3.
         self.stats_main = f32("stats_main")
         self.stats_ds = f32("stats_ds")
+        # the BN3 backward sums reduced by the next block's shortcut dgrad
+        self.stats_sums = f32("stats_sums")
         # backward scratch outside the budget: the input gradient of a stride-2
         # shortcut conv at its sampling grid
         self.short_ws = u8("short_ws")
@@ -293,6 +295,8 @@ class DeltaRuntime:
         self._dconvs = {}
         self._wgrads = {}
         bn_bwd_convs = {n.attrs["conv"] for n in self.nodes if n.op == "conv_bn_relu_bwd"}
+        sums_convs = {n.attrs["conv"] for n in self.nodes
+                      if n.op == "conv_shortcut_bwd" and "sums_xc" in n.attrs}
         for n in self.nodes:
             if n.op == "conv":
                 cs = self.g.convs[n.attrs["conv"]]
@@ -319,6 +323,8 @@ class DeltaRuntime:
                         wide = (DGRAD_BN256 and cs.name in bn_bwd_convs
                                 and Nb * P_ * Q_ >= 2 * 148 * 128)
                         dconv.set_tile_n(256 if wide else 128)
+                    if cs.name in sums_convs:
+                        dconv.set_tile_n(64)  # three epilogue operands: 64-column tiles
                     self._dconvs[cs.name] = dconv
 
     def trace(self) -> P.Trace:
@@ -396,7 +402,9 @@ class DeltaRuntime:
 
         M = int(np.prod(node.shape[:-1])) if len(node.shape) == 4 else 0
         C = node.shape[-1]
-        bwd_n = 2 + K._merge_launches(K._chunks(M, C)) if M else 0  # streaming BN backward
+        # streaming BN backward: one persistent launch (bn_pool.cu k_bn_bwd_grid)
+        # or partial + merge(s) + apply
+        bwd_n = (1 if K.BN_BWD_ONE_LAUNCH else 2 + K._merge_launches(K._chunks(M, C))) if M else 0
         bnp = lambda bn: (_ptr(pr.bn_mean[bn]), _ptr(pr.bn_invstd[bn]))
         gb = lambda bn: (_ptr(pr.views["bn_g:" + bn]), _ptr(pr.views["bn_b:" + bn]))
         dgb = lambda bn: (_ptr(pr.gviews["bn_g:" + bn]), _ptr(pr.gviews["bn_b:" + bn]))
@@ -482,8 +490,14 @@ class DeltaRuntime:
             bn = node.attrs["bn"]
             pool_hw = int(node.shape[1] * node.shape[2]) if node.attrs.get("from_pool") else 0
             mask = X.IN(1) if node.attrs.get("masked") else None
-            add(X.kop(X.K_BN_BWD, (X.IN(0), mask, X.IN(len(node.parents) - 1), X.OUT()) + bnp(bn)
-                      + (gb(bn)[0],) + dgb(bn) + (_ptr(self.bn_ws),), (pool_hw, M, C)), bwd_n, bwd_n)
+            if node.attrs.get("sums_fused"):
+                # (sum g, sum g*X) came with g from the shortcut dgrad's epilogue
+                add(X.kop(X.K_BN_BWD_PARTS, (_ptr(self.stats_sums), X.IN(0), X.IN(1), X.OUT())
+                          + bnp(bn) + (gb(bn)[0],) + dgb(bn), (0, M, C)), 2, 2)
+            else:
+                add(X.kop(X.K_BN_BWD, (X.IN(0), mask, X.IN(len(node.parents) - 1), X.OUT())
+                          + bnp(bn) + (gb(bn)[0],) + dgb(bn) + (_ptr(self.bn_ws),),
+                          (pool_hw, M, C)), bwd_n, bwd_n)
         elif op == "conv_bn_relu_bwd":
             # parents [dC, R = relu(bn(X)), X]
             conv, bn = node.attrs["conv"], node.attrs["bn"]
@@ -531,8 +545,14 @@ class DeltaRuntime:
                 add_ = X.IN(2)
             if conv not in self._dconvs:
                 raise RuntimeError(f"{node.name}: the shortcut's conv1 must be a 1x1 (own dgrad)")
-            add(X.kop(X.K_CONV_EX, (X.IN(0), X.OUT(), None, add_, add_mask, out_mask),
-                      (K.EPI_ADD_MASK, pool_hw, stride2), conv=self._dconvs[conv]._h))
+            if "sums_xc" in node.attrs:
+                # + the previous block's BN3 backward sums over (g, its C3)
+                add(X.kop(X.K_CONV_EX, (X.IN(0), X.OUT(), _ptr(self.stats_sums), add_, add_mask,
+                                        out_mask, X.IN(node.attrs["sums_xc"])),
+                          (K.EPI_ADD_MASK, pool_hw, stride2), conv=self._dconvs[conv]._h))
+            else:
+                add(X.kop(X.K_CONV_EX, (X.IN(0), X.OUT(), None, add_, add_mask, out_mask),
+                          (K.EPI_ADD_MASK, pool_hw, stride2), conv=self._dconvs[conv]._h))
             add(wgrad(conv, 0, 1), 2, 2)
         elif op == "maxpool_bwd":
             Nb, H, W, Cs = self.nodes[node.parents[1]].shape

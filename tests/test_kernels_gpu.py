@@ -309,6 +309,37 @@ def test_dgrad_and_add_mask_epilogue(case):
     _close(y2, (ref + up) * (om.float() > 0), "pooled add")
 
 
+@pytest.mark.parametrize("case", [c for c in DGRAD_CASES if c[5] == 1])
+def test_add_mask_epilogue_with_bn_backward_sums(case):
+    """EPI_ADD_MASK + xc: y bit-exact against the plain add+mask launch, and the
+    per-CTA rows sum to (sum y, sum y*xc) per channel (the next BN backward's
+    reductions, so the streaming partial pass is skipped)."""
+    g, w, dy, conv, ref = _dgrad_setup(case, 9, tile_n=64)
+    N, H, W, Cin = ref.shape
+    add = torch.randn(N, H, W, Cin, device="cuda", generator=g).to(torch.bfloat16)
+    om = torch.randn(N, H, W, Cin, device="cuda", generator=g).to(torch.bfloat16)
+    xc = torch.randn(N, H, W, Cin, device="cuda", generator=g).to(torch.bfloat16)
+    y1 = torch.empty(N, H, W, Cin, device="cuda", dtype=torch.bfloat16)
+    y2 = torch.empty_like(y1)
+    conv.add_mask(dy.data_ptr(), y1.data_ptr(), _stream(), add=add.data_ptr(),
+                  out_mask=om.data_ptr())
+    parts = torch.full((K.stats_partials_floats(Cin),), float("nan"), device="cuda")
+    conv.add_mask(dy.data_ptr(), y2.data_ptr(), _stream(), add=add.data_ptr(),
+                  out_mask=om.data_ptr(), xc=xc.data_ptr(), partials_ptr=parts.data_ptr())
+    torch.cuda.synchronize()
+    assert torch.equal(y1, y2)
+    rows = parts[: K.stats_parts() * Cin * 4].view(K.stats_parts(), Cin, 4)
+    assert not torch.isnan(rows[:, :, :2]).any()
+    yf = y2.float().view(-1, Cin)
+    S = rows[:, :, 0].double().sum(0)
+    Q = rows[:, :, 1].double().sum(0)
+    Sr = yf.double().sum(0)
+    Qr = (yf.double() * xc.float().view(-1, Cin).double()).sum(0)
+    scale = yf.abs().double().sum(0) + 1
+    assert ((S - Sr).abs() / scale).max().item() < 1e-4
+    assert ((Q - Qr).abs() / (scale * 4)).max().item() < 1e-4
+
+
 @pytest.mark.parametrize("case,tile_n", [(c, 128) for c in DGRAD_CASES[:4]]
                          + [(c, 256) for c in DGRAD_CASES if c[3] >= 256])
 def test_dgrad_bn_backward_epilogue(case, tile_n):
