@@ -47,6 +47,10 @@ delta_status delta_conv_forward(const delta_conv* c, const void* x, void* y, flo
  *       add_stride2 = 1 the full add is the input gradient of a stride-2 1x1
  *       conv: given as [N][P/2][Q/2][K] at the even rows/columns, zero elsewhere.
  *       Null pointers are skipped.  (The residual-branch gradient sum.)
+ *       With a full add, out_mask, xc and `stats` all given (1x1, tile_n 64):
+ *       `stats` also receives the per-CTA (sum y, sum y*xc) rows of the BN
+ *       backward that consumes y (xc = that BN's input), for
+ *       delta_bn_backward_from_partials — its partial pass is skipped.
  *   DELTA_EPI_BN_BWD: y = g = bf16(acc) * [relu(bn(xc)) > 0] with the saved
  *       statistics (the forward's exact arithmetic), and `stats` receives the
  *       per-CTA (sum g, sum g*xc) partial rows for delta_bn_backward_from_partials.
@@ -69,7 +73,7 @@ typedef struct delta_conv_epilogue {
 delta_status delta_conv_forward_ex(const delta_conv* c, const void* x, void* y, float* stats,
                                    const delta_conv_epilogue* epi, void* stream);
 /* Override the output-channel tile (64, 128 or 256, dividing K).  The fused
- * epilogues (DELTA_EPI_ADD_MASK / DELTA_EPI_BN_BWD) require tile_n <= 128. */
+ * epilogues require tile_n <= 128, except DELTA_EPI_BN_BWD (256 allowed). */
 delta_status delta_conv_set_tile_n(delta_conv* c, int32_t tile_n);
 delta_status delta_conv_geometry(const delta_conv* c, int32_t* P, int32_t* Q, int32_t* kdim,
                                  int32_t* tile_n);
