@@ -115,6 +115,12 @@ delta_status delta_bn_apply(int32_t mode, const void* x, const void* res, void* 
                             const float* gamma, const float* beta, const float* mean2,
                             const float* invstd2, const float* gamma2, const float* beta2,
                             void* stream);
+/* Training-mode BN backward (dgamma, dbeta, dx) of g = up [* (mask > 0)]; up
+ * full [M][C] or pooled [N][C] / pool_hw.  One persistent launch of
+ * co-resident CTAs with two grid-wide barriers (partial sums -> fixed-order
+ * per-channel merge -> apply); deterministic.  `ws`: delta_bn_workspace_floats
+ * floats.  Not for concurrent launches from several streams (one barrier per
+ * device); DELTA_BN_BWD_GRID=0 selects the three-launch path. */
 delta_status delta_bn_backward(const void* up, int32_t pool_hw, const void* mask, const void* x,
                                void* dx, int64_t M, int32_t C, const float* mean,
                                const float* invstd, const float* gamma, float* dgamma,
