@@ -727,23 +727,12 @@ __global__ void __launch_bounds__(256)
 }
 
 // ----------------------------------------------------------------- pooling
-// The 9 taps of a 3x3/2 pad-1 window, all loads issued before any use
-// (out-of-image taps = -inf, which never wins a strict > scan)
-__device__ __forceinline__ void window_loads(const bf16* __restrict__ x, int n, int p, int q,
-                                             int c0, int H, int W, int C, uint4 (&v)[9]) {
-  const uint4 ninf = make_uint4(0xFF80FF80u, 0xFF80FF80u, 0xFF80FF80u, 0xFF80FF80u);
-#pragma unroll
-  for (int k = 0; k < 9; ++k) {
-    const int h = 2 * p - 1 + k / 3, w = 2 * q - 1 + k % 3;
-    const bool ok = (unsigned)h < (unsigned)H && (unsigned)w < (unsigned)W;
-    v[k] = ok ? *reinterpret_cast<const uint4*>(x + ((int64_t(n) * H + h) * W + w) * C + c0)
-              : ninf;
-  }
-}
-
 // Grids: blockIdx.x = one image row (n, row), blockIdx.y x 256 threads span
 // (column, 8-channel group) of that row; C/8 is a power of two, so the only
 // divisions left are one 32-bit div/mod per thread.
+// RPB output rows per block: the input rows shared by neighbouring windows
+// are read once (2 RPB + 1 input rows instead of 3 RPB)
+template <int RPB>
 __global__ void __launch_bounds__(256) k_maxpool_fwd(const bf16* __restrict__ x,
                                                      bf16* __restrict__ y, int N, int H, int W,
                                                      int C, int P, int Q, int lcg) {
@@ -753,14 +742,16 @@ __global__ void __launch_bounds__(256) k_maxpool_fwd(const bf16* __restrict__ x,
   const int item = blockIdx.y * 256 + threadIdx.x;
   if (item >= Q * cg) return;
   const int q = item >> lcg, c0 = (item & (cg - 1)) * 8;
-  const int n = blockIdx.x / P, p = blockIdx.x - n * P;
-  // (the compiler batches these loads itself; forcing all 9 up front measured
-  // slower: 161 vs 126 us at the ResNet-50 stem shape)
-  float best[8];
+  const int pb = P / RPB;
+  const int n = blockIdx.x / pb, p = (blockIdx.x - n * pb) * RPB;
+  float b[RPB][8];
 #pragma unroll
-  for (int j = 0; j < 8; ++j) best[j] = -INFINITY;
+  for (int r = 0; r < RPB; ++r)
 #pragma unroll
-  for (int dh = 0; dh < 3; ++dh) {
+    for (int j = 0; j < 8; ++j) b[r][j] = -INFINITY;
+  // input row 2p-1+dh feeds output rows p+r with 2r <= dh <= 2r+2
+#pragma unroll
+  for (int dh = 0; dh < 2 * RPB + 1; ++dh) {
     const int h = 2 * p - 1 + dh;
     if (h < 0 || h >= H) continue;
 #pragma unroll
@@ -770,16 +761,25 @@ __global__ void __launch_bounds__(256) k_maxpool_fwd(const bf16* __restrict__ x,
       float f[8];
       unpack8(*reinterpret_cast<const uint4*>(x + ((int64_t(n) * H + h) * W + w) * C + c0), f);
 #pragma unroll
-      for (int j = 0; j < 8; ++j) best[j] = f[j] > best[j] ? f[j] : best[j];
+      for (int r = 0; r < RPB; ++r) {
+        if (dh >= 2 * r && dh <= 2 * r + 2) {
+#pragma unroll
+          for (int j = 0; j < 8; ++j) b[r][j] = f[j] > b[r][j] ? f[j] : b[r][j];
+        }
+      }
     }
   }
-  reinterpret_cast<uint4*>(y)[(int64_t(blockIdx.x) * Q + q) * cg + (c0 >> 3)] = pack8(best);
+  const int64_t o = (int64_t(n) * P + p) * Q + q;
+#pragma unroll
+  for (int r = 0; r < RPB; ++r) reinterpret_cast<uint4*>(y)[(o + r * Q) * cg + (c0 >> 3)] = pack8(b[r]);
 }
 
 // Backward in two deterministic passes (no atomics):
 //   1. per output window, the first-in-scan-order argmax (0..8) of each
 //      channel -> one byte per output element (transient workspace);
 //   2. per input pixel, sum the gradient of the <= 4 windows whose argmax it is.
+// two output rows per block (P even), as k_maxpool_fwd<2>: scan order and
+// the first-maximum rule per window are unchanged
 __global__ void __launch_bounds__(256)
     k_maxpool_argmax(const bf16* __restrict__ x, uint8_t* __restrict__ idx, int N, int H, int W,
                      int C, int P, int Q, int lcg) {
@@ -789,31 +789,42 @@ __global__ void __launch_bounds__(256)
   const int item = blockIdx.y * 256 + threadIdx.x;
   if (item >= Q * cg) return;
   const int q = item >> lcg, c0 = (item & (cg - 1)) * 8;
-  const int n = blockIdx.x / P, p = blockIdx.x - n * P;
-  float best[8];
-  uint32_t arg[8];
+  const int pp = P >> 1;
+  const int n = blockIdx.x / pp, p = (blockIdx.x - n * pp) * 2;
+  const uint4 ninf = make_uint4(0xFF80FF80u, 0xFF80FF80u, 0xFF80FF80u, 0xFF80FF80u);
+  uint4 v[15];  // input rows 2p-1 .. 2p+3 x columns 2q-1 .. 2q+1
 #pragma unroll
-  for (int j = 0; j < 8; ++j) {
-    best[j] = -INFINITY;
-    arg[j] = 0;
+  for (int k = 0; k < 15; ++k) {
+    const int h = 2 * p - 1 + k / 3, w = 2 * q - 1 + k % 3;
+    const bool ok = (unsigned)h < (unsigned)H && (unsigned)w < (unsigned)W;
+    v[k] = ok ? *reinterpret_cast<const uint4*>(x + ((int64_t(n) * H + h) * W + w) * C + c0)
+              : ninf;
   }
-  uint4 v[9];
-  window_loads(x, n, p, q, c0, H, W, C, v);
 #pragma unroll
-  for (int k = 0; k < 9; ++k) {
-    float f[8];
-    unpack8(v[k], f);
+  for (int r = 0; r < 2; ++r) {
+    float best[8];
+    uint32_t arg[8];
 #pragma unroll
-    for (int j = 0; j < 8; ++j)
-      if (f[j] > best[j]) {
-        best[j] = f[j];
-        arg[j] = k;
-      }
+    for (int j = 0; j < 8; ++j) {
+      best[j] = -INFINITY;
+      arg[j] = 0;
+    }
+#pragma unroll
+    for (int k = 0; k < 9; ++k) {
+      float f[8];
+      unpack8(v[r * 6 + k], f);
+#pragma unroll
+      for (int j = 0; j < 8; ++j)
+        if (f[j] > best[j]) {
+          best[j] = f[j];
+          arg[j] = k;
+        }
+    }
+    uint2 packed;
+    packed.x = arg[0] | (arg[1] << 8) | (arg[2] << 16) | (arg[3] << 24);
+    packed.y = arg[4] | (arg[5] << 8) | (arg[6] << 16) | (arg[7] << 24);
+    reinterpret_cast<uint2*>(idx)[((int64_t(n) * P + p + r) * Q + q) * cg + (c0 >> 3)] = packed;
   }
-  uint2 packed;
-  packed.x = arg[0] | (arg[1] << 8) | (arg[2] << 16) | (arg[3] << 24);
-  packed.y = arg[4] | (arg[5] << 8) | (arg[6] << 16) | (arg[7] << 24);
-  reinterpret_cast<uint2*>(idx)[(int64_t(blockIdx.x) * Q + q) * cg + (c0 >> 3)] = packed;
 }
 
 // Thread per (output window (p, q), 8 channels): writes the 2x2 input block
@@ -1126,7 +1137,13 @@ cudaError_t maxpool3x3s2_fwd(const void* x, void* y, int N, int H, int W, int C,
   const int P = (H + 2 - 3) / 2 + 1, Q = (W + 2 - 3) / 2 + 1;
   if (C % 8 || ((C / 8) & (C / 8 - 1))) return cudaErrorInvalidValue;
   const int lcg = __builtin_ctz(C / 8);
-  if (cudaError_t e_ = launch_k(k_maxpool_fwd, dim3(dim3(unsigned(N) * P, (Q * (C / 8) + 255) / 256)), dim3(256), 0, st, static_cast<const bf16*>(x), static_cast<bf16*>(y), N, H, W, C, P, Q, lcg)) return e_;
+  static const int rpb_env = [] {
+    const char* e = std::getenv("DELTA_MAXPOOL_RPB");
+    return e ? std::atoi(e) : 2;
+  }();
+  const int rpb = P % rpb_env == 0 ? rpb_env : (P % 2 == 0 ? 2 : 1);
+  const auto k = rpb == 4 ? k_maxpool_fwd<4> : (rpb == 2 ? k_maxpool_fwd<2> : k_maxpool_fwd<1>);
+  if (cudaError_t e_ = launch_k(k, dim3(dim3(unsigned(N) * (P / rpb), (Q * (C / 8) + 255) / 256)), dim3(256), 0, st, static_cast<const bf16*>(x), static_cast<bf16*>(y), N, H, W, C, P, Q, lcg)) return e_;
   return cudaGetLastError();
 }
 
@@ -1140,7 +1157,8 @@ cudaError_t maxpool3x3s2_bwd(const void* dy, const void* x, void* dx, int N, int
   const int P = (H + 2 - 3) / 2 + 1, Q = (W + 2 - 3) / 2 + 1;
   if (C % 8 || ((C / 8) & (C / 8 - 1))) return cudaErrorInvalidValue;
   const int lcg = __builtin_ctz(C / 8);
-  if (cudaError_t e_ = launch_k(k_maxpool_argmax, dim3(dim3(unsigned(N) * P, (Q * (C / 8) + 255) / 256)), dim3(256), 0, st, static_cast<const bf16*>(x), static_cast<uint8_t*>(ws), N, H, W, C, P, Q, lcg)) return e_;
+  if (P & 1) return cudaErrorInvalidValue;  // argmax: two output rows per block
+  if (cudaError_t e_ = launch_k(k_maxpool_argmax, dim3(dim3(unsigned(N) * (P / 2), (Q * (C / 8) + 255) / 256)), dim3(256), 0, st, static_cast<const bf16*>(x), static_cast<uint8_t*>(ws), N, H, W, C, P, Q, lcg)) return e_;
   if (H != 2 * P || W != 2 * Q) return cudaErrorInvalidValue;  // even input sizes
   if (cudaError_t e_ = launch_k(k_maxpool_bwd_gather, dim3(dim3(unsigned(N) * P, (Q * (C / 8) + 255) / 256)), dim3(256), 0, st, static_cast<const bf16*>(dy), static_cast<const uint8_t*>(ws), static_cast<bf16*>(dx), N, H, W, C, P, Q, lcg)) return e_;
   return cudaGetLastError();
