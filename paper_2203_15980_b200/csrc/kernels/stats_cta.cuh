@@ -5,6 +5,8 @@
 // in the CTA's static tile order, so the result is deterministic:
 //   EPI_STORE   (count, mean, M2, 0) of the stored bf16 outputs (Chan's merge)
 //   EPI_BN_BWD  (sum g, sum g*xc, 0, 0)
+//   EPI_ADD_MASK with xc (conv_fwd.cu EV_ADD_OM_ST): (sum y, sum y*xc, 0, 0)
+//               of its output, the sums of the BN backward that consumes it
 // One merge launch then reduces the (at most SM-count) rows per channel in a
 // fixed order (bn_pool.cu) — no per-tile partials, no grouping pass.
 #pragma once
