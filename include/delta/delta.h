@@ -188,6 +188,14 @@ typedef struct delta_program_info {
 
 delta_status delta_lower(const delta_trace* t, const delta_config* c,
                          uint64_t align, delta_program** out);
+/* flags for delta_lower_ex.  Default (0): offloads AND reloads on one copy
+ * stream (DELTA_STREAM_D2H) in plan order — the reference's single copy
+ * stream (include/deltasim/device.hpp:45-74), so the executed timeline is
+ * checkable by its replay_check as is.  DUPLEX: reloads on DELTA_STREAM_H2D,
+ * concurrent with offloads (both PCIe directions). */
+enum { DELTA_LOWER_DUPLEX_COPIES = 1 };
+delta_status delta_lower_ex(const delta_trace* t, const delta_config* c, uint64_t align,
+                            uint32_t flags, delta_program** out);
 delta_status delta_program_info_get(const delta_program* p, delta_program_info* info);
 const delta_action* delta_program_actions(const delta_program* p, uint64_t* n);
 const uint64_t* delta_program_inputs(const delta_program* p, uint64_t* n);

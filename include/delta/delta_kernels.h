@@ -93,6 +93,9 @@ delta_status delta_wgrad_run(const delta_wgrad* w, const void* dy, const void* x
 void delta_wgrad_destroy(delta_wgrad* w);
 
 /* ---- recompute engine: BatchNorm (BNForward, ref src/trace.cpp:405) ---- */
+/* BN workspace (floats): a few words of grid-barrier state at its head,
+ * then partial rows.  Zero it once at allocation; every kernel leaves the
+ * barrier words in a reusable state. */
 int64_t delta_bn_workspace_floats(int64_t M, int32_t C);
 /* training-mode statistics; run_mean/run_var may be NULL (recompute never
  * touches them) */
@@ -117,10 +120,12 @@ delta_status delta_bn_apply(int32_t mode, const void* x, const void* res, void* 
                             void* stream);
 /* Training-mode BN backward (dgamma, dbeta, dx) of g = up [* (mask > 0)]; up
  * full [M][C] or pooled [N][C] / pool_hw.  One persistent launch of
- * co-resident CTAs with two grid-wide barriers (partial sums -> fixed-order
- * per-channel merge -> apply); deterministic.  `ws`: delta_bn_workspace_floats
- * floats.  Not for concurrent launches from several streams (one barrier per
- * device); DELTA_BN_BWD_GRID=0 selects the three-launch path. */
+ * co-resident CTAs (a cooperative launch) with two grid-wide barriers
+ * (partial sums -> fixed-order per-channel merge -> apply); deterministic.
+ * `ws`: delta_bn_workspace_floats floats, zeroed at allocation; the barrier
+ * state lives in it, so launches on different streams need different
+ * workspaces.  If the cooperative launch is refused, or with
+ * DELTA_BN_BWD_GRID=0, the three-launch path runs instead. */
 delta_status delta_bn_backward(const void* up, int32_t pool_hw, const void* mask, const void* x,
                                void* dx, int64_t M, int32_t C, const float* mean,
                                const float* invstd, const float* gamma, float* dgamma,

@@ -143,6 +143,16 @@ delta_status delta_rt_step(delta_rt* rt, void* stream);
  * events time device execution, not host enqueue latency. */
 delta_status delta_rt_step_timed(delta_rt* rt, void* stream, float* start_ms, float* end_ms,
                                  uint64_t n_actions);
+/* One step with a DEVICE-side action log: every compute/recompute/offload/
+ * reload action is bracketed on its own stream by a one-thread stamp kernel
+ * that appends {%globaltimer ns, arrival index, action*2 + (0 head|1 tail),
+ * node << 8 | action op} (4 x uint64) to a device log when the stream reaches
+ * it.  Synchronizes and copies the log (arrival order) into `records`
+ * (capacity `cap` records); *n_records = records written.  This is the
+ * observed record of what the GPU ran and when (executed-timeline twin of
+ * ref Timeline, include/deltasim/engine.hpp:44-70). */
+delta_status delta_rt_step_observed(delta_rt* rt, void* stream, uint64_t* records, uint64_t cap,
+                                    uint64_t* n_records);
 /* GPU cost model (ref OpNode::compute_cost_us, trace.hpp:17): `iters` timed
  * steps; per node, the median over steps of its first compute action, in
  * whole microseconds (ceil, >= 1), written to cost_us[node index in the

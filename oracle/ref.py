@@ -53,6 +53,20 @@ def lib():
     return _lib
 
 
+def config(budget: int, bandwidth_bytes_per_us=(64000, 1), effective_fraction=(7, 20),
+           policy_mode: int = 0, heuristic: int = 0):
+    """An EngineConfig-like object with the reference defaults
+    (include/deltasim/engine.hpp:25-40, policy.hpp:18-26) — lets the
+    reference arm drive the oracle without importing the product."""
+    from types import SimpleNamespace
+    cm = SimpleNamespace(bandwidth_bytes_per_us=tuple(bandwidth_bytes_per_us),
+                         effective_fraction=tuple(effective_fraction), swap_cost_mode=0)
+    return SimpleNamespace(budget=int(budget), heuristic=heuristic, policy_mode=policy_mode,
+                           cost_model=cm, watermark_fraction=(3, 4), prefetch_limit=2,
+                           prefetch_enabled=True, overlap_enabled=True, prefetch_guard=0,
+                           scripted_decisions=[])
+
+
 def _cfg(cfg) -> tuple:
     """Accepts a paper_2203_15980_b200.planner.EngineConfig-like object."""
     c = RefConfig()

@@ -103,6 +103,7 @@ def _load():
         "delta_plan_time_ns": (i32, [vp, P(DeltaConfig), u32, P(C.c_double)]),
         "delta_transfer_time_us": (i32, [u64, P(DeltaConfig), P(u64)]),
         "delta_lower": (i32, [vp, P(DeltaConfig), u64, P(vp)]),
+        "delta_lower_ex": (i32, [vp, P(DeltaConfig), u64, u32, P(vp)]),
         "delta_program_info_get": (i32, [vp, P(DeltaProgramInfo)]),
         "delta_program_actions": (P(DeltaAction), [vp, P(u64)]),
         "delta_program_inputs": (P(u64), [vp, P(u64)]),

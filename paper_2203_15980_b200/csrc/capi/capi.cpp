@@ -345,10 +345,15 @@ delta_status delta_transfer_time_us(uint64_t bytes, const delta_config* c, uint6
 
 delta_status delta_lower(const delta_trace* t, const delta_config* c, uint64_t align,
                          delta_program** out) {
+  return delta_lower_ex(t, c, align, 0, out);
+}
+
+delta_status delta_lower_ex(const delta_trace* t, const delta_config* c, uint64_t align,
+                            uint32_t flags, delta_program** out) {
   return guard([&] {
     auto* p = new delta_program;
     try {
-      p->p = delta_rt::lower_plan(t->t, to_cfg(c), align);
+      p->p = delta_rt::lower_plan(t->t, to_cfg(c), align, flags);
       p->plan.r = p->p.plan;
       fill(&p->plan);
     } catch (...) {

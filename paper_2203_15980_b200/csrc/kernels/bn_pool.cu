@@ -47,6 +47,15 @@ __device__ __forceinline__ uint4 ld_stream(const void* p) {
                : "l"(p));
   return r;
 }
+// coherent streaming load: for data the same kernel also writes (in place)
+__device__ __forceinline__ uint4 ld_coherent(const void* p) {
+  uint4 r;
+  asm volatile("ld.global.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(p)
+               : "memory");
+  return r;
+}
 __device__ __forceinline__ void unpack8(uint4 u, float (&f)[8]) {
   const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&u);
 #pragma unroll
@@ -465,25 +474,27 @@ __global__ void __launch_bounds__(256)
   bn_bwd_chunk<MASKED, POOLED>(up, pool_hw, mask, x, M, C, chunk, mean, invstd, ws);
 }
 
-// Grid-wide barrier for a grid whose CTAs are all co-resident (sized by the
-// occupancy API): generation counter, the last CTA to arrive resets the count
-// and then releases the others; reusable across launches without a memset.
-__device__ unsigned int g_bar_count;
-__device__ unsigned int g_bar_gen;
-__device__ __forceinline__ void grid_barrier() {
+// Grid-wide barrier for a grid whose CTAs are all co-resident (a cooperative
+// launch guarantees it).  The state is two words at the head of the launch's
+// own BN workspace (never a device global, so concurrent launches with their
+// own workspaces cannot interleave): bar[0] arrival count, bar[1] generation.
+// The last CTA to arrive resets the count and then releases the others, so
+// the words return to (0, gen+1): reusable across launches without a memset
+// once the workspace was zeroed at allocation.
+__device__ __forceinline__ void grid_barrier(unsigned int* bar) {
   __syncthreads();
   if (threadIdx.x == 0) {
     unsigned int gen;
-    asm volatile("ld.acquire.gpu.u32 %0, [%1];" : "=r"(gen) : "l"(&g_bar_gen) : "memory");
+    asm volatile("ld.acquire.gpu.u32 %0, [%1];" : "=r"(gen) : "l"(bar + 1) : "memory");
     __threadfence();
-    if (atomicAdd(&g_bar_count, 1u) == gridDim.x - 1) {
-      atomicExch(&g_bar_count, 0u);
+    if (atomicAdd(bar, 1u) == gridDim.x - 1) {
+      atomicExch(bar, 0u);
       __threadfence();
-      atomicAdd(&g_bar_gen, 1u);
+      atomicAdd(bar + 1, 1u);
     } else {
       unsigned int g;
       do {
-        asm volatile("ld.acquire.gpu.u32 %0, [%1];" : "=r"(g) : "l"(&g_bar_gen) : "memory");
+        asm volatile("ld.acquire.gpu.u32 %0, [%1];" : "=r"(g) : "l"(bar + 1) : "memory");
       } while (g == gen);
     }
     __threadfence();
@@ -504,10 +515,10 @@ __global__ void __launch_bounds__(256)
                   const bf16* __restrict__ x, bf16* __restrict__ dx, int64_t M, int C,
                   int64_t chunk, const float* __restrict__ mean,
                   const float* __restrict__ invstd, const float* __restrict__ gamma,
-                  float* dgamma, float* dbeta, float2* ws) {
+                  float* dgamma, float* dbeta, float2* ws, unsigned int* bar) {
   pdl_wait();
   bn_bwd_chunk<MASKED, POOLED>(up, pool_hw, mask, x, M, C, chunk, mean, invstd, ws);
-  grid_barrier();
+  grid_barrier(bar);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   for (int c = blockIdx.x * 8 + warp; c < C; c += gridDim.x * 8) {
     float A = 0.f, B = 0.f;
@@ -523,7 +534,7 @@ __global__ void __launch_bounds__(256)
       dgamma[c] = B;
     }
   }
-  grid_barrier();
+  grid_barrier(bar);
   pdl_trigger();
   const int tpr = C >> 3, rpi = 256 / tpr;
   const int tx = threadIdx.x % tpr, ty = threadIdx.x / tpr;
@@ -635,10 +646,13 @@ __global__ void __launch_bounds__(256)
 
 // dx = gamma*invstd*(g - dbeta/M - xhat*dgamma/M), xhat = (x-mean)*invstd,
 // folded per channel into dx = k1*g + k2*x + k3 (3 live coefficients).
-template <bool MASKED, bool POOLED>
+// INPLACE: dx == up (the conv-fused BN backward writes its masked gradient g
+// in the node's own output slot): `up` is read with coherent loads, not the
+// read-only path, since this kernel writes it.
+template <bool MASKED, bool POOLED, bool INPLACE = false>
 __global__ void __launch_bounds__(256)
-    k_bn_bwd_apply(const bf16* __restrict__ up, int pool_hw, const bf16* __restrict__ mask,
-                   const bf16* __restrict__ x, bf16* __restrict__ dx, int64_t vecs, int cmask,
+    k_bn_bwd_apply(const bf16* up, int pool_hw, const bf16* __restrict__ mask,
+                   const bf16* __restrict__ x, bf16* dx, int64_t vecs, int cmask,
                    int logC, int64_t M, const float* __restrict__ mean,
                    const float* __restrict__ invstd, const float* __restrict__ gamma,
                    const float* __restrict__ dgamma, const float* __restrict__ dbeta) {
@@ -666,8 +680,9 @@ __global__ void __launch_bounds__(256)
     for (int u = 0; u < UNROLL; ++u) {
       const int64_t i = i0 + u * stride;
       if (i < vecs) {
-        uv[u] = POOLED ? load_up<true>(up, pool_hw, (i * 8) >> logC, c0, C)
-                       : ld_stream(up + i * 8);
+        uv[u] = POOLED    ? load_up<true>(up, pool_hw, (i * 8) >> logC, c0, C)
+                : INPLACE ? ld_coherent(up + i * 8)
+                          : ld_stream(up + i * 8);
         if (MASKED) mv[u] = ld_stream(mask + i * 8);
         xv[u] = ld_stream(x + i * 8);
       }
@@ -963,10 +978,13 @@ __global__ void k_mean_rows(const float* row_loss, int N, float* loss) {
 
 }  // namespace
 
+// The BN workspace: kBarFloats words of grid-barrier state (zeroed once at
+// allocation, left zero-count by every launch), then the partial rows.
+constexpr int64_t kBarFloats = 64;
 int64_t bn_workspace_floats(int64_t M, int C) {
   const int64_t chunk = chunk_rows(M, C);
   const int64_t chunks = (M + chunk - 1) / chunk;
-  return 2 * (chunks + (chunks + GROUP - 1) / GROUP) * C;
+  return kBarFloats + 2 * (chunks + (chunks + GROUP - 1) / GROUP) * C;
 }
 
 namespace {
@@ -994,6 +1012,7 @@ cudaError_t merge_partials(const float2* ws, int parts, int64_t rows_per, int64_
 cudaError_t bn_stats(const void* x, int64_t M, int C, float* ws, float* mean, float* invstd,
                      float eps, float* rm, float* rv, float mom, cudaStream_t st) {
   if (C % SLICE || (C & (C - 1)) || C > 2048) return cudaErrorInvalidValue;
+  ws += kBarFloats;
   const int64_t chunk = chunk_rows(M, C);
   const int chunks = int((M + chunk - 1) / chunk);
   if (cudaError_t e_ = launch_k(k_bn_stats_partial, dim3(chunks), dim3(256), 0, st, static_cast<const bf16*>(x), M, C, chunk, reinterpret_cast<float2*>(ws))) return e_;
@@ -1073,6 +1092,8 @@ cudaError_t bn_backward(const void* up, int pool_hw, const void* mask, const voi
   auto U = static_cast<const bf16*>(up);
   auto Mk = static_cast<const bf16*>(mask);
   auto X = static_cast<const bf16*>(x);
+  auto* bar = reinterpret_cast<unsigned int*>(ws);
+  ws += kBarFloats;
   if (bn_bwd_one_launch()) {
     const auto k = Mk ? (pool_hw ? k_bn_bwd_grid<true, true> : k_bn_bwd_grid<true, false>)
                       : (pool_hw ? k_bn_bwd_grid<false, true> : k_bn_bwd_grid<false, false>);
@@ -1080,11 +1101,15 @@ cudaError_t bn_backward(const void* up, int pool_hw, const void* mask, const voi
     int64_t chunk = (M + cap - 1) / cap;
     chunk = (chunk + 15) / 16 * 16;
     const int grid = int((M + chunk - 1) / chunk);
-    if (cudaError_t e_ = launch_k(k, dim3(grid), dim3(256), 0, st, U, pool_hw, Mk, X,
-                                  static_cast<bf16*>(dx), M, C, chunk, mean, invstd, gamma,
-                                  dgamma, dbeta, reinterpret_cast<float2*>(ws)))
-      return e_;
-    return cudaGetLastError();
+    // cooperative: the runtime guarantees every CTA co-resident (even beside
+    // kernels on other streams) or refuses the launch; a refusal falls back
+    // to the three-launch path below
+    const cudaError_t e_ = launch_coop(k, dim3(grid), dim3(256), 0, st, U, pool_hw, Mk, X,
+                                       static_cast<bf16*>(dx), M, C, chunk, mean, invstd, gamma,
+                                       dgamma, dbeta, reinterpret_cast<float2*>(ws), bar);
+    if (e_ == cudaSuccess) return cudaGetLastError();
+    if (e_ != cudaErrorCooperativeLaunchTooLarge) return e_;
+    cudaGetLastError();  // clear the refusal
   }
   const int64_t chunk = chunk_rows(M, C);
   const int chunks = int((M + chunk - 1) / chunk);
@@ -1119,7 +1144,8 @@ cudaError_t bn_backward_from_partials(const float* partials, const void* g, cons
                                 invstd, dgamma, dbeta))
     return e_;
   const int64_t vecs = M * C / 8;
-  return launch_k(k_bn_bwd_apply<false, false>, dim3(grid_for(vecs, 256)), dim3(256), 0, st,
+  const auto app = g == dx ? k_bn_bwd_apply<false, false, true> : k_bn_bwd_apply<false, false>;
+  return launch_k(app, dim3(grid_for(vecs, 256)), dim3(256), 0, st,
                   static_cast<const bf16*>(g), 0, nullptr, static_cast<const bf16*>(x),
                   static_cast<bf16*>(dx), vecs, C - 1, __builtin_ctz(C), M, mean, invstd, gamma,
                   dgamma, dbeta);

@@ -57,6 +57,28 @@ __global__ void k_spin(long long cycles) {
   }
 }
 
+// Device-side action log of an observed step: one record per stamp, written
+// by the device when the stream reaches it — {%globaltimer ns, global
+// arrival order, action index * 2 + (0 head | 1 tail), node << 8 | op}.
+__global__ void k_stamp(unsigned long long* log, unsigned int* count, unsigned int cap,
+                        unsigned long long tag, unsigned long long what) {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  const unsigned int i = atomicAdd(count, 1u);
+  if (i < cap) {
+    log[4 * size_t(i) + 0] = t;
+    log[4 * size_t(i) + 1] = i;
+    log[4 * size_t(i) + 2] = tag;
+    log[4 * size_t(i) + 3] = what;
+  }
+}
+
+struct StampLog {
+  unsigned long long* log = nullptr;
+  unsigned int* count = nullptr;
+  unsigned int cap = 0;
+};
+
 delta_status fail(delta_status code, const std::string& msg) {
   delta_set_error(msg);
   return code;
@@ -239,8 +261,10 @@ delta_status run_node(delta_rt* rt, const delta_action& a, cudaStream_t st) {
 }
 
 // One pass over the actions.  `t0/t1` (optional) = per-action timing event
-// pairs recorded around compute and copy actions on their own stream.
-delta_status issue(delta_rt* rt, cudaStream_t cs, cudaEvent_t* t0, cudaEvent_t* t1) {
+// pairs recorded around compute and copy actions on their own stream;
+// `stamps` (optional) = device-logged head/tail stamps of the same actions.
+delta_status issue(delta_rt* rt, cudaStream_t cs, cudaEvent_t* t0, cudaEvent_t* t1,
+                   const StampLog* stamps = nullptr) {
   cudaStream_t streams[3] = {cs, rt->d2h, rt->h2d};
   char* arena = static_cast<char*>(rt->arena);
   char* host = static_cast<char*>(rt->host);
@@ -249,6 +273,13 @@ delta_status issue(delta_rt* rt, cudaStream_t cs, cudaEvent_t* t0, cudaEvent_t* 
     cudaStream_t st = streams[a.stream < 3 ? a.stream : 0];
     const bool timed = t0 && (a.op == DELTA_ACT_COMPUTE || a.op == DELTA_ACT_RECOMPUTE ||
                               a.op == DELTA_ACT_OFFLOAD || a.op == DELTA_ACT_RELOAD);
+    const bool work = a.op == DELTA_ACT_COMPUTE || a.op == DELTA_ACT_RECOMPUTE ||
+                      a.op == DELTA_ACT_OFFLOAD || a.op == DELTA_ACT_RELOAD;
+    const unsigned long long what = (static_cast<unsigned long long>(a.node) << 8) | a.op;
+    if (stamps && work) {
+      k_stamp<<<1, 1, 0, st>>>(stamps->log, stamps->count, stamps->cap, 2ull * ai, what);
+      RT_CUDA(cudaGetLastError());
+    }
     if (timed) RT_CUDA(cudaEventRecord(t0[ai], st));
     switch (a.op) {
       case DELTA_ACT_COMPUTE:
@@ -275,6 +306,10 @@ delta_status issue(delta_rt* rt, cudaStream_t cs, cudaEvent_t* t0, cudaEvent_t* 
         return fail(DELTA_E_ARGUMENT, "unknown action " + std::to_string(a.op));
     }
     if (timed) RT_CUDA(cudaEventRecord(t1[ai], st));
+    if (stamps && work) {
+      k_stamp<<<1, 1, 0, st>>>(stamps->log, stamps->count, stamps->cap, 2ull * ai + 1, what);
+      RT_CUDA(cudaGetLastError());
+    }
     if (rt->after_fn && (a.op == DELTA_ACT_COMPUTE || a.op == DELTA_ACT_RECOMPUTE))
       rt->after_fn(rt->ctx, ai, a.node, reinterpret_cast<uint64_t>(arena + a.offset), st);
   }
@@ -418,6 +453,38 @@ delta_status delta_rt_step_timed(delta_rt* rt, void* stream, float* start_ms, fl
   for (auto ev : t1)
     if (ev) cudaEventDestroy(ev);
   if (start) cudaEventDestroy(start);
+  return s;
+}
+
+delta_status delta_rt_step_observed(delta_rt* rt, void* stream, uint64_t* records,
+                                    uint64_t cap, uint64_t* n_records) {
+  cudaStream_t cs = static_cast<cudaStream_t>(stream);
+  StampLog sl;
+  sl.cap = static_cast<unsigned int>(cap);
+  void* mem = nullptr;
+  const size_t bytes = 32 * size_t(cap) + 256;
+  RT_CUDA(cudaMalloc(&mem, bytes));
+  sl.log = static_cast<unsigned long long*>(mem);
+  sl.count = reinterpret_cast<unsigned int*>(static_cast<char*>(mem) + 32 * size_t(cap));
+  delta_status s = DELTA_OK;
+  cudaError_t e = cudaMemsetAsync(sl.count, 0, 4, cs);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(cs);
+  if (e != cudaSuccess) s = cuda_fail(e, "delta_rt_step_observed setup");
+  if (!s) s = issue(rt, cs, nullptr, nullptr, &sl);
+  unsigned int n = 0;
+  if (!s) {
+    e = cudaStreamSynchronize(cs);
+    if (e == cudaSuccess) e = cudaMemcpy(&n, sl.count, 4, cudaMemcpyDeviceToHost);
+    if (e == cudaSuccess && n > cap) {
+      s = fail(DELTA_E_ARGUMENT, "delta_rt_step_observed: " + std::to_string(n) +
+                                     " records exceed the capacity " + std::to_string(cap));
+    } else if (e == cudaSuccess) {
+      e = cudaMemcpy(records, sl.log, 32 * size_t(n), cudaMemcpyDeviceToHost);
+    }
+    if (e != cudaSuccess && !s) s = cuda_fail(e, "delta_rt_step_observed readback");
+  }
+  cudaFree(mem);
+  if (n_records) *n_records = s ? 0 : n;
   return s;
 }
 

@@ -9,10 +9,17 @@
 //   2. assign arena offsets offline (greedy by size over known lifetimes:
 //      the footprint lands at or just above the pool high-watermark, and the
 //      difference is reported as fragmentation, never hidden);
-//   3. lower timeline events to actions on three streams (compute, D2H copy
-//      engine, H2D copy engine) and insert the minimal cross-stream event
-//      edges: read-after-write on a tensor, write-after-read/write on a
-//      reused arena range, and host-slab RAW between offload and reload.
+//   3. lower timeline events to actions on the compute stream and the copy
+//      stream(s) and insert the minimal cross-stream event edges:
+//      read-after-write on a tensor, write-after-read/write on a reused arena
+//      range, host-slab RAW between offload and reload, a copy never starting
+//      before the compute-stream point the plan issued it at, and a restore
+//      of a tensor never starting before its offload landed (the planner
+//      waits for that landing, src/engine.cpp:375-380).  With those edges the
+//      executed timeline keeps the plan's causal order, so the reference's
+//      replay_check can certify it with measured timestamps.
+//      Copies: ONE copy stream in plan order (the reference's single copy
+//      stream) unless DELTA_LOWER_DUPLEX_COPIES puts reloads on a second one.
 // Everything here runs once per plan; the step itself replays the program
 // (captured as a CUDA graph by the host runtime).
 #include "lower.hpp"
@@ -47,7 +54,9 @@ struct Pending {  // action before event insertion
 }  // namespace
 
 Program lower_plan(const Trace& trace, const EngineConfig& cfg,
-                   std::uint64_t align) {
+                   std::uint64_t align, std::uint32_t flags) {
+  const std::uint32_t reload_stream =
+      (flags & DELTA_LOWER_DUPLEX_COPIES) ? DELTA_STREAM_H2D : DELTA_STREAM_D2H;
   if (align == 0 || (align & (align - 1))) throw ArgumentError("lower: align must be a power of two");
   Program prog;
   std::vector<PoolOp> ops;
@@ -116,6 +125,9 @@ Program lower_plan(const Trace& trace, const EngineConfig& cfg,
   std::unordered_map<NodeId, std::uint64_t> host_slot;
   std::unordered_map<NodeId, std::pair<std::uint32_t, std::uint64_t>> host_writer;
   std::uint64_t host_bytes = 0;
+  // the latest compute-stream action: the plan's issue point of a copy
+  bool have_compute = false;
+  std::pair<std::uint32_t, std::uint64_t> last_compute{0, 0};
 
   // region hazards for a new allocation: every earlier, already-dead
   // allocation overlapping it contributes its touches.
@@ -173,7 +185,12 @@ Program lower_plan(const Trace& trace, const EngineConfig& cfg,
           in_allocs.push_back(pi);
           deps.push_back(writer.at(p));
         }
+        // a restore after an offload starts once that offload has landed
+        auto ho = host_writer.find(ev.node);
+        if (ho != host_writer.end()) deps.push_back(ho->second);
         auto me = emit(act, std::move(deps));
+        have_compute = true;
+        last_compute = me;
         a.touches.push_back(me);
         for (std::size_t pi : in_allocs) allocs[pi].touches.push_back(me);
         writer[ev.node] = me;
@@ -195,6 +212,7 @@ Program lower_plan(const Trace& trace, const EngineConfig& cfg,
         std::vector<std::pair<std::uint32_t, std::uint64_t>> deps{writer.at(ev.node)};
         auto hw = host_writer.find(ev.node);  // an earlier offload of this node
         if (hw != host_writer.end()) deps.push_back(hw->second);
+        if (have_compute) deps.push_back(last_compute);  // issue point
         auto me = emit(act, std::move(deps));
         a.touches.push_back(me);
         host_writer[ev.node] = me;
@@ -204,12 +222,13 @@ Program lower_plan(const Trace& trace, const EngineConfig& cfg,
         std::size_t ai = cur.at(ev.node);
         Alloc& a = allocs[ai];
         act.op = DELTA_ACT_RELOAD;
-        act.stream = DELTA_STREAM_H2D;
+        act.stream = reload_stream;
         act.offset = a.offset;
         act.bytes = ev.bytes;
         act.host_offset = host_slot.at(ev.node);
         std::vector<std::pair<std::uint32_t, std::uint64_t>> deps{host_writer.at(ev.node)};
         reuse_deps(ai, deps);
+        if (have_compute) deps.push_back(last_compute);  // issue point
         auto me = emit(act, std::move(deps));
         a.touches.push_back(me);
         writer[ev.node] = me;

@@ -17,7 +17,10 @@ struct Program {
   std::uint32_t n_events = 0;
 };
 
+// flags: DELTA_LOWER_DUPLEX_COPIES (delta.h) puts reloads on their own H2D
+// stream; by default every copy runs on ONE copy stream in plan order, the
+// reference's single copy stream (include/deltasim/device.hpp:45-74).
 Program lower_plan(const deltasim::Trace& trace, const deltasim::EngineConfig& cfg,
-                   std::uint64_t align);
+                   std::uint64_t align, std::uint32_t flags = 0);
 
 }  // namespace delta_rt

@@ -25,6 +25,10 @@ FIRST_ONLY, RECOMPUTE_ONLY, SIDE = 1, 2, 4
 
 
 
+OBSERVED_DTYPE = np.dtype([("t_ns", np.uint64), ("seq", np.uint64), ("action", np.uint64),
+                           ("tail", np.uint8), ("node", np.uint64), ("op", np.uint8)])
+
+
 class DeltaRef(C.Structure):
     _fields_ = [("kind", u32), ("index", u32), ("ptr", u64)]
 
@@ -51,6 +55,7 @@ _SIGS = {
     "delta_rt_step": (i32, [vp, vp]),
     "delta_rt_step_timed": (i32, [vp, vp, C.POINTER(f32), C.POINTER(f32), u64]),
     "delta_rt_measure_costs": (i32, [vp, vp, u32, C.POINTER(u64), u64]),
+    "delta_rt_step_observed": (i32, [vp, vp, C.POINTER(u64), u64, C.POINTER(u64)]),
     "delta_rt_destroy": (None, [vp]),
 }
 for _n, (_r, _a) in _SIGS.items():
@@ -184,6 +189,26 @@ class Executor:
         self._raise_pending()
         check(rc)
         return a, b
+
+    def step_observed(self, stream: int) -> np.ndarray:
+        """One step with the device-side action log (delta_rt_step_observed):
+        structured array of records in device arrival order."""
+        cap = 2 * self.n_actions + 16
+        rec = np.zeros((cap, 4), np.uint64)
+        n = u64()
+        rc = lib.delta_rt_step_observed(self._h, stream, rec.ctypes.data_as(C.POINTER(u64)), cap,
+                                        C.byref(n))
+        self._raise_pending()
+        check(rc)
+        rec = rec[:n.value]
+        out = np.zeros(n.value, OBSERVED_DTYPE)
+        out["t_ns"] = rec[:, 0]
+        out["seq"] = rec[:, 1]
+        out["action"] = rec[:, 2] >> 1
+        out["tail"] = rec[:, 2] & 1
+        out["node"] = rec[:, 3] >> 8
+        out["op"] = rec[:, 3] & 0xFF
+        return out
 
     def measure_costs(self, stream: int, iters: int, n_nodes: int) -> np.ndarray:
         out = np.zeros(n_nodes, np.uint64)

@@ -329,17 +329,22 @@ def transfer_time_us(nbytes: int, cfg: EngineConfig) -> int:
 
 ACT_COMPUTE, ACT_RECOMPUTE, ACT_OFFLOAD, ACT_RELOAD, ACT_RECORD, ACT_WAIT = range(6)
 STREAM_COMPUTE, STREAM_D2H, STREAM_H2D = range(3)
+LOWER_DUPLEX_COPIES = 1
 
 
 class Program:
-    """Lowered plan: arena offsets + 3-stream action list (csrc/rt/lower.cpp)."""
+    """Lowered plan: arena offsets + action list on the compute stream and the
+    copy stream(s) (csrc/rt/lower.cpp).  duplex=False (default): every copy on
+    one copy stream in plan order, the reference's single copy stream;
+    duplex=True: reloads on a second copy engine, concurrent with offloads."""
 
-    def __init__(self, trace: Trace, cfg: EngineConfig, align: int = 256):
+    def __init__(self, trace: Trace, cfg: EngineConfig, align: int = 256, duplex: bool = False):
         h = _CTrace(trace)
         try:
             c, keep = cfg.to_c()
             self._ptr = C.c_void_p()
-            check(lib.delta_lower(h.ptr, C.byref(c), align, C.byref(self._ptr)))
+            check(lib.delta_lower_ex(h.ptr, C.byref(c), align, LOWER_DUPLEX_COPIES if duplex else 0,
+                                     C.byref(self._ptr)))
         finally:
             h.close()
         info = DeltaProgramInfo()

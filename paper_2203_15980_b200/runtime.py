@@ -251,7 +251,8 @@ class DeltaRuntime:
         ws = workspace_plan(self.g)
         f32 = lambda key: torch.empty(ws[key] // 4, dtype=torch.float32, device=self.device)
         u8 = lambda key: torch.empty(ws[key], dtype=torch.uint8, device=self.device)
-        self.bn_ws = f32("bn_ws")
+        # zeroed: the one-launch BN backward keeps its grid-barrier words here
+        self.bn_ws = torch.zeros(ws["bn_ws"] // 4, dtype=torch.float32, device=self.device)
         # BN statistics partials written by the conv epilogue (one 128-row
         # tile per partial); downsample convs use their own scratch because
         # their BN is applied together with the block's bn3.
@@ -343,9 +344,11 @@ class DeltaRuntime:
         return base.peak_bytes
 
     def plan(self, budget_fraction: float | None = 0.5, budget: int | None = None,
-             policy=P.PolicyMode.Delta, **kw):
+             policy=P.PolicyMode.Delta, duplex: bool = False, **kw):
         """Plan with libdelta and lower onto the arena.  budget_fraction=None
-        plans the no-eviction baseline (Baseline policy, budget = sum)."""
+        plans the no-eviction baseline (Baseline policy, budget = sum).
+        duplex: reloads on a second copy engine (default: one copy stream in
+        plan order, the reference's model)."""
         t = self.trace()
         if budget_fraction is None and budget is None:
             total = sum(n.nbytes for n in self.nodes)
@@ -354,7 +357,7 @@ class DeltaRuntime:
             if budget is None:
                 budget = int(self.baseline_peak() * budget_fraction)
             cfg = self.engine_config(budget, policy, **kw)
-        prog = P.Program(t, cfg, align=G.ALIGN)
+        prog = P.Program(t, cfg, align=G.ALIGN, duplex=duplex)
         if prog.infeasible:
             node, deficit = prog.infeasible
             raise RuntimeError(f"plan infeasible at node {self.nodes[node].name} "
@@ -625,14 +628,15 @@ class DeltaRuntime:
 
     # -------------------------------------------------------- program
     def run_program(self, timing: dict | None = None, probe: dict | None = None,
-                    stamps: list | None = None):
+                    stamps: list | None = None, observe: list | None = None):
         """Issue one training step: the lowered action program through the
         C++ executor (csrc/rt/executor.cu) on the compute stream and the two
         copy engines, then the optimizer.  The loss stays on device.
         `timing`: node id -> [(ms, recomputed)], plus "swap" -> [(ms, op,
         bytes)]; `probe`: node id -> a clone of its output after its (last)
         production; `stamps`: receives (action index, start_ms, end_ms) of
-        every compute/recompute/offload/reload action."""
+        every compute/recompute/offload/reload action; `observe`: receives the
+        device-side action log of the step (Executor.step_observed)."""
         st = self.stream.cuda_stream
         if self._bound_slot != self._slot:
             self._bind()
@@ -642,7 +646,9 @@ class DeltaRuntime:
             def after(ai, node, out):
                 if node in probe:
                     probe[node] = self._arena_view(out, node).clone()
-        if timing is not None or stamps is not None:
+        if observe is not None:
+            observe.append(self.executor.step_observed(st))
+        elif timing is not None or stamps is not None:
             t0, t1 = self.executor.step_timed(st, after)
             acts = self.program.actions
             for ai, a in enumerate(acts):
@@ -751,35 +757,102 @@ class DeltaRuntime:
         self._use_slot(0)
         return self._loss_host[:n].tolist()
 
-    def executed_timeline(self) -> np.ndarray:
-        """One eager step with every device action time-stamped; returns the
-        plan's timeline (ref Timeline, engine.hpp:44-70) re-stamped with the
-        MEASURED device times (µs from the step start): Compute/Recompute/
-        Offload/Reload take their kernel's or copy's start and duration;
-        zero-duration markers (Use, Free, Evict, Stall) take the end of the
-        latest compute-stream action before them.  Feed it to the
-        reference's oracle::replay_check (oracle/ref.replay_check) for an
-        independent safety certificate of what the GPU actually did."""
-        stamps = []
+    def executed_timeline(self, findings: list | None = None) -> np.ndarray:
+        """One eager step with a DEVICE-side action log (delta_rt_step_observed:
+        a stamp kernel on each action's own stream appends %globaltimer, the
+        action and its node/op when the stream reaches it) turned into a
+        reference Timeline (engine.hpp:44-70) for oracle::replay_check:
+
+        * Compute / Recompute / Offload / Reload events are the device's
+          records: kind and node as the executor ran them, start = head stamp,
+          duration = tail - head (µs from the first stamp);
+        * the zero-duration markers of the plan (Use, Free, Evict) take the end
+          of the latest compute-stream action (or Stall) before them in plan
+          order; a Stall spans the measured gap from there to the next
+          compute-stream action.
+
+        `findings` (optional list) receives every disagreement between the
+        device log and the lowered program: an action missing, duplicated or
+        run with another node/op, or a stream that ran its actions out of
+        program order.  Empty == the GPU ran exactly the program, in order."""
+        recs = []
         with torch.cuda.stream(self.stream):
-            self.run_program(stamps=stamps)
+            self.run_program(observe=recs)
         torch.cuda.synchronize()
+        rec = recs[0]
+        acts = self.program.actions
+        found = [] if findings is None else findings
+        work_ops = (P.ACT_COMPUTE, P.ACT_RECOMPUTE, P.ACT_OFFLOAD, P.ACT_RELOAD)
+        head, tail = {}, {}
+        for r in rec:
+            ai = int(r["action"])
+            d = tail if r["tail"] else head
+            if ai in d:
+                found.append(f"action {ai}: duplicate {'tail' if r['tail'] else 'head'} stamp")
+            d[ai] = r
+            if ai >= len(acts):
+                found.append(f"action {ai}: not in the program")
+                continue
+            a = acts[ai]
+            if int(r["node"]) != int(a["node"]) or int(r["op"]) != int(a["op"]):
+                found.append(f"action {ai}: device ran op {int(r['op'])} of node {int(r['node'])}, "
+                             f"program has op {int(a['op'])} of node {int(a['node'])}")
+        last_seq = {}
+        for ai, a in enumerate(acts):
+            if int(a["op"]) not in work_ops:
+                continue
+            if ai not in head or ai not in tail:
+                found.append(f"action {ai} (op {int(a['op'])}, node {int(a['node'])}) not executed")
+                continue
+            if int(tail[ai]["seq"]) < int(head[ai]["seq"]) or tail[ai]["t_ns"] < head[ai]["t_ns"]:
+                found.append(f"action {ai}: tail stamp before its head")
+            s_ = int(a["stream"])
+            if s_ in last_seq and int(head[ai]["seq"]) < last_seq[s_]:
+                found.append(f"action {ai}: stream {s_} ran it before an earlier program action")
+            last_seq[s_] = int(tail[ai]["seq"])
+        t0 = int(rec["t_ns"].min()) if len(rec) else 0
+        us = lambda t: int(round((int(t) - t0) / 1000.0))
+        kind_of = {P.ACT_COMPUTE: P.EventKind.Compute, P.ACT_RECOMPUTE: P.EventKind.Recompute,
+                   P.ACT_OFFLOAD: P.EventKind.Offload, P.ACT_RELOAD: P.EventKind.Reload}
+        by_event = {}
+        for ai, a in enumerate(acts):
+            if int(a["op"]) in work_ops and ai in head and ai in tail:
+                by_event[int(a["plan_event"])] = ai
         plan = P.run_iteration(self.trace(), self.config).events
         ev = plan.copy()
-        t_of = {}
-        for ai, ms0, ms1 in stamps:
-            pe = int(self.program.actions[ai]["plan_event"])
-            t0, t1 = int(round(ms0 * 1e3)), int(round(ms1 * 1e3))
-            t_of[pe] = (t0, max(0, t1 - t0))
+        # compute-stream work starts in plan order (for Stall spans)
+        next_start = [None] * len(ev)
+        nxt = None
+        for i in range(len(ev) - 1, -1, -1):
+            next_start[i] = nxt
+            ai = by_event.get(i)
+            if ai is not None and int(acts[ai]["stream"]) == P.STREAM_COMPUTE:
+                nxt = us(head[ai]["t_ns"])
         now = 0
         for i in range(len(ev)):
-            if i in t_of:
-                ev[i]["ts"], ev[i]["duration"] = t_of[i]
+            ai = by_event.get(i)
+            if ai is not None:
+                h, t = head[ai], tail[ai]
+                ev[i]["kind"] = kind_of[int(h["op"])]
+                ev[i]["node"] = int(h["node"])
+                ev[i]["stream"] = (P.StreamKind.Compute if int(h["op"]) in (P.ACT_COMPUTE, P.ACT_RECOMPUTE)
+                                   else P.StreamKind.Copy)
+                ev[i]["ts"] = us(h["t_ns"])
+                ev[i]["duration"] = us(t["t_ns"]) - us(h["t_ns"])
                 if ev[i]["stream"] == P.StreamKind.Compute:
                     now = max(now, int(ev[i]["ts"] + ev[i]["duration"]))
+            elif int(ev[i]["kind"]) in (P.EventKind.Compute, P.EventKind.Recompute,
+                                        P.EventKind.Offload, P.EventKind.Reload):
+                found.append(f"plan event {i} ({int(ev[i]['kind'])} of node {int(ev[i]['node'])}) "
+                             "has no executed action")
             else:
                 ev[i]["ts"] = now
                 ev[i]["duration"] = 0
+                if int(ev[i]["kind"]) == P.EventKind.Stall and next_start[i] is not None:
+                    # the measured wait: up to the next compute-stream start;
+                    # later markers of this gap follow the stall
+                    ev[i]["duration"] = max(0, next_start[i] - now)
+                    now += int(ev[i]["duration"])
         return ev
 
     # ----------------------------------------------------- cost model
@@ -789,13 +862,18 @@ class DeltaRuntime:
         steps), quantise to whole microseconds (>= 1) and write them into the
         trace; probe the pinned host link for the swap cost."""
         self.plan(None)
-        lr = self.lr
-        self.lr = 0.0  # cost probing must not move the weights
         if self._bound_slot != self._slot:
             self._bind()
+        # the probe steps run the program only (no optimizer step), but their
+        # first productions update the BN running statistics: keep them
+        pr = self.params
+        saved = {n: (pr.bn_rmean[n].clone(), pr.bn_rvar[n].clone()) for n in pr.bn_rmean}
         with torch.cuda.stream(self.stream):
             costs = self.executor.measure_costs(self.stream.cuda_stream, iters, len(self.nodes))
-        self.lr = lr
+        torch.cuda.synchronize()
+        for n, (m, v) in saved.items():
+            pr.bn_rmean[n].copy_(m)
+            pr.bn_rvar[n].copy_(v)
         table = {}
         for n in self.nodes:
             n.cost_us = max(1, int(costs[n.id]))

@@ -65,7 +65,7 @@ r = torch.randn(M, C, device="cuda").to(torch.bfloat16)
 y = torch.empty_like(x)
 mean = torch.zeros(C, device="cuda"); inv = torch.ones(C, device="cuda")
 gam = torch.ones(C, device="cuda"); bet = torch.zeros(C, device="cuda")
-ws = torch.empty(K.bn_workspace_floats(M, C), device="cuda")
+ws = torch.zeros(K.bn_workspace_floats(M, C), device="cuda")
 dg = torch.empty(C, device="cuda"); db = torch.empty(C, device="cuda")
 nb = M * C * 2
 res = {}
@@ -78,7 +78,7 @@ res["add_grad_mask"] = (timeit(lambda: K.add_grad(x.data_ptr(), r.data_ptr(), 0,
 for (MM, CC) in [(N * 14 * 14, 1024), (N * 7 * 7, 2048), (N * 56 * 56, 64)]:
     xx = torch.randn(MM, CC, device="cuda").to(torch.bfloat16); rr = torch.randn(MM, CC, device="cuda").to(torch.bfloat16)
     yy = torch.empty_like(xx); m2 = torch.zeros(CC, device="cuda"); i2 = torch.ones(CC, device="cuda"); g2 = torch.ones(CC, device="cuda")
-    d1 = torch.empty(CC, device="cuda"); d2 = torch.empty(CC, device="cuda"); w2 = torch.empty(K.bn_workspace_floats(MM, CC), device="cuda")
+    d1 = torch.empty(CC, device="cuda"); d2 = torch.empty(CC, device="cuda"); w2 = torch.zeros(K.bn_workspace_floats(MM, CC), device="cuda")
     res[f"bn_backward_{MM}x{CC}"] = (timeit(lambda: K.bn_backward(rr.data_ptr(), 0, xx.data_ptr(), xx.data_ptr(), yy.data_ptr(), MM, CC, m2.data_ptr(), i2.data_ptr(), g2.data_ptr(), d1.data_ptr(), d2.data_ptr(), w2.data_ptr(), st)), 7 * MM * CC * 2)
 res["torch_copy"] = (timeit(lambda: y.copy_(x)), 2 * nb)
 for k, (ms, b) in res.items():

@@ -15,7 +15,7 @@ for (H, C) in [(56, 256), (56, 64), (28, 512), (14, 1024), (7, 2048)]:
     y = torch.empty_like(x)
     mean = torch.zeros(C, device="cuda"); inv = torch.ones(C, device="cuda")
     gam = torch.ones(C, device="cuda"); bet = torch.zeros(C, device="cuda")
-    ws = torch.empty(K.bn_workspace_floats(M, C), device="cuda")
+    ws = torch.zeros(K.bn_workspace_floats(M, C), device="cuda")
     dg = torch.empty(C, device="cuda"); db = torch.empty(C, device="cuda")
     fns = {"stats": lambda: K.bn_stats(x.data_ptr(), M, C, ws.data_ptr(), mean.data_ptr(), inv.data_ptr(), 1e-5, None, None, 0.1, st),
            "apply0": lambda: K.bn_apply(0, x.data_ptr(), None, y.data_ptr(), M, C, mean.data_ptr(), inv.data_ptr(), gam.data_ptr(), bet.data_ptr(), stream=st),

@@ -122,7 +122,7 @@ def test_bn_stats_apply_relu(M, C):
     g = torch.Generator(device="cuda").manual_seed(2)
     x = (torch.randn(M, C, device="cuda", generator=g) * 2 + 0.5).to(torch.bfloat16)
     gamma, beta = _bn_params(C, g)
-    ws = torch.empty(K.bn_workspace_floats(M, C), device="cuda")
+    ws = torch.zeros(K.bn_workspace_floats(M, C), device="cuda")
     mean = torch.empty(C, device="cuda"); invstd = torch.empty(C, device="cuda")
     rm = torch.zeros(C, device="cuda"); rv = torch.ones(C, device="cuda")
     K.bn_stats(x.data_ptr(), M, C, ws.data_ptr(), mean.data_ptr(), invstd.data_ptr(), 1e-5,
@@ -196,7 +196,7 @@ def test_bn_backward_matches_autograd(pool_hw):
     yy.backward(gfull)
     dx = torch.empty_like(x)
     dg = torch.empty(C, device="cuda"); db = torch.empty(C, device="cuda")
-    ws = torch.empty(K.bn_workspace_floats(M, C), device="cuda")
+    ws = torch.zeros(K.bn_workspace_floats(M, C), device="cuda")
     K.bn_backward(up.data_ptr(), pool_hw, yb.data_ptr(), x.data_ptr(), dx.data_ptr(), M, C,
                   mean.data_ptr(), invstd.data_ptr(), gamma.data_ptr(), dg.data_ptr(),
                   db.data_ptr(), ws.data_ptr(), _stream())

@@ -234,8 +234,8 @@ def test_trace_roundtrip_and_bothpinned_warning():
 
 
 # --------------------------------------------------- lowering invariants
-def _check_program(trace, cfg):
-    prog = P.Program(trace, cfg)
+def _check_program(trace, cfg, duplex=False):
+    prog = P.Program(trace, cfg, duplex=duplex)
     plan = P.run_iteration(trace, cfg)
     assert prog.decisions == plan.decisions
     assert prog.arena_bytes >= prog.pool_peak_bytes
@@ -252,7 +252,11 @@ def _check_program(trace, cfg):
         elif op == P.ACT_OFFLOAD:
             assert int(a["stream"]) == P.STREAM_D2H
         elif op == P.ACT_RELOAD:
-            assert int(a["stream"]) == P.STREAM_H2D
+            assert int(a["stream"]) == (P.STREAM_H2D if duplex else P.STREAM_D2H)
+    # one copy stream (default): every copy in plan order on it
+    copies = [int(a["plan_event"]) for a in acts if int(a["op"]) in (P.ACT_OFFLOAD, P.ACT_RELOAD)]
+    if not duplex:
+        assert copies == sorted(copies)
     n_compute = sum(1 for a in acts if int(a["op"]) in (P.ACT_COMPUTE, P.ACT_RECOMPUTE))
     assert n_compute == sum(1 for e in plan.events if e["kind"] in (0, 3))
     return prog
@@ -264,6 +268,7 @@ def test_lowering_resnet50_trace_zero_fragmentation():
     cfg = P.EngineConfig(budget=meta["budget"], cost_model=P.CostModel(
         tuple(meta["bandwidth_bytes_per_us"]), (1, 1)))
     prog = _check_program(t, cfg)
+    _check_program(t, cfg, duplex=True)
     assert prog.infeasible is None
     assert prog.arena_bytes <= cfg.budget
     assert prog.arena_bytes == prog.pool_peak_bytes
@@ -274,7 +279,7 @@ def test_lowering_fuzz_invariants():
         if v["ref"].get("infeasible"):
             continue
         t = P.Trace.from_json(_trace_json(v))
-        _check_program(t, cfg_from(v["cfg"]))
+        _check_program(t, cfg_from(v["cfg"]), duplex=bool(v.get("seed", 0) % 2))
 
 
 # ---------------------------------- the reference acceptance suite vs libdelta

@@ -1,13 +1,21 @@
-"""End-to-end GPU parity of the DELTA runtime.
+"""End-to-end GPU parity of the DELTA runtime, at the test batch (16) AND at
+the bench configuration (256, every M a multiple of 128, the 256-wide
+BN-backward dgrads, the large-grid one-launch BN backward, the bs256 wgrad
+splits) and at a batch with partial tiles (250).
 
 * the step through our kernels matches a plain PyTorch fp32 autograd
-  reference of the same ResNet (forward loss within 2e-2 relative, gradient
-  directions cos > 0.99 — bf16 activations);
+  reference of the same ResNet (loss within 2e-2 relative — bf16 activations);
+* every forward op and every backward node, re-evaluated in fp32 autograd on
+  the runtime's own (bf16) inputs, matches ELEMENTWISE within the kernel tests'
+  tolerance (|err| <= 1e-2 |ref| + 2e-2 rms(ref));
 * under a 50% activation budget (evictions + recomputes, sometimes
   offload/reload) the loss and every parameter gradient are BIT-IDENTICAL to
   the no-eviction run: recomputed activations equal the retained ones;
 * the executed plan's decisions equal the reference oracle's on the same
-  trace (bit-exact Filter/Director) when oracle/_ref is present.
+  trace (bit-exact Filter/Director) when oracle/_ref is present;
+* the timeline the GPU executed (device-side action log) passes the
+  reference's replay_check, unfiltered, for the 50% plan, other budgets and
+  policies, and an offload-heavy plan.
 """
 import numpy as np
 import pytest
@@ -62,19 +70,36 @@ def torch_reference_loss(rt, x, y):
     return loss.item(), {k: v.grad for k, v in params.items()}
 
 
-@pytest.fixture(scope="module")
-def rts():
+def _pair(batch):
     torch.backends.cudnn.deterministic = True
     torch.backends.cudnn.benchmark = False
-    base = DeltaRuntime(50, BATCH, seed=0, lr=0.0)
+    base = DeltaRuntime(50, batch, seed=0, lr=0.0)
     base.measure_costs(iters=2)
     base.plan(None)
-    delta = DeltaRuntime(50, BATCH, seed=0, lr=0.0)
+    delta = DeltaRuntime(50, batch, seed=0, lr=0.0)
     for n, m in zip(delta.nodes, base.nodes):
         n.cost_us = m.cost_us
     delta.link_gbs = base.link_gbs
     delta.plan(0.5)
     return base, delta
+
+
+@pytest.fixture(scope="module")
+def rts():
+    base, delta = _pair(BATCH)
+    yield base, delta
+    del base, delta
+    torch.cuda.empty_cache()
+
+
+@pytest.fixture(scope="module", params=[BATCH, 250, 256], ids=lambda b: f"bs{b}")
+def rts_any(request):
+    """the test batch, a batch with partial 128-row tiles (250) and the bench
+    configuration (256)"""
+    base, delta = _pair(request.param)
+    yield base, delta
+    del base, delta
+    torch.cuda.empty_cache()
 
 
 def _probe_all(rt, x, y):
@@ -87,26 +112,32 @@ def _probe_all(rt, x, y):
     return probe
 
 
-def _cos(a, b):
-    a = a.flatten().float()
-    b = b.flatten().float()
-    return F.cosine_similarity(a, b, dim=0).item(), (a.norm() / b.norm().clamp_min(1e-30)).item()
+def _close(ours, ref, what):
+    """elementwise, the kernel tests' tolerance (tests/test_kernels_gpu.py _close)"""
+    ours = ours.float().reshape(ref.shape)
+    ref = ref.float()
+    err = (ours - ref).abs()
+    tol = 1e-2 * ref.abs() + 2e-2 * ref.pow(2).mean().sqrt() + 1e-6
+    bad = err > tol
+    assert not bool(bad.any()), (f"{what}: {int(bad.sum())} of {ref.numel()} elements out of "
+                                 f"tolerance, max err {err.max().item():.3g} "
+                                 f"(rms ref {ref.pow(2).mean().sqrt().item():.3g})")
 
 
-def test_loss_matches_torch_fp32(rts):
-    base, _ = rts
-    x, y = make_batch(0)
+def test_loss_matches_torch_fp32(rts_any):
+    base, _ = rts_any
+    x, y = make_batch(0, base.batch)
     loss = base.step(x, y)
     ref_loss, _ = torch_reference_loss(base, x, y)
     assert abs(loss - ref_loss) <= 2e-2 * abs(ref_loss), (loss, ref_loss)
 
 
-def test_every_op_matches_fp32_autograd_on_its_inputs(rts):
+def test_every_op_matches_fp32_autograd_on_its_inputs(rts_any):
     """Each forward op and each backward node of the step, re-evaluated in
-    fp32 autograd from the runtime's own (bf16) inputs: cos > 0.999 and norm
-    within 2% (bf16 rounding of the stored result is the only difference)."""
-    base, _ = rts
-    x, y = make_batch(3)
+    fp32 autograd from the runtime's own (bf16) inputs, elementwise (bf16
+    rounding of the stored result is the only expected difference)."""
+    base, _ = rts_any
+    x, y = make_batch(3, base.batch)
     pv = _probe_all(base, x, y)
     g = base.g
     pr = base.params
@@ -135,9 +166,8 @@ def test_every_op_matches_fp32_autograd_on_its_inputs(rts):
     checked = []
 
     def expect(what, ours, ref):
-        c, r = _cos(ours, ref)
         checked.append(what)
-        assert c > 0.999 and abs(r - 1) < 0.02, (what, c, r)
+        _close(ours, ref, what)
 
     for n in g.nodes:
         ins = [T(p) for p in n.parents]
@@ -153,6 +183,8 @@ def test_every_op_matches_fp32_autograd_on_its_inputs(rts):
             expect(n.name, T(n.id), F.max_pool2d(ins[0], 3, 2, 1))
         elif n.op == "avgpool":
             expect(n.name, T(n.id), ins[0].mean((2, 3)))
+        elif n.op == "fc":
+            expect(n.name, T(n.id), ins[0] @ Pw["fc_w"].t() + Pw["fc_b"])
         elif n.op == "fc_bwd":
             L = ins[0].clone().requires_grad_(True)
             F.cross_entropy(L, y.cuda()).backward()
@@ -209,13 +241,13 @@ def test_every_op_matches_fp32_autograd_on_its_inputs(rts):
     assert len(checked) >= 260  # 178 nodes + parameter gradients
 
 
-def test_delta_50pct_bit_identical_to_no_eviction(rts):
-    base, delta = rts
+def test_delta_50pct_bit_identical_to_no_eviction(rts_any):
+    base, delta = rts_any
     prog = delta.program
     assert prog.plan_counts["evict"] + prog.plan_counts["offload"] > 0
     assert prog.plan_counts["recompute"] > 0
     assert prog.arena_bytes <= base.program.arena_bytes * 0.5 + 1
-    x, y = make_batch(1)
+    x, y = make_batch(1, base.batch)
     l0 = base.step(x, y)
     g0 = base.params.grad.clone()
     l1 = delta.step(x, y)
@@ -274,27 +306,48 @@ def test_training_under_delta_fits_a_fixed_batch():
     assert max(losses[-5:]) < 0.5 * losses[0], losses
 
 
-def test_executed_gpu_timeline_passes_reference_replay_check(rts):
-    """The timeline the GPU actually executed (plan events re-stamped with
-    measured device times) certified by the reference's own independent
-    verifier (ref src/oracle.cpp replay_check): budget never exceeded, no
-    read of an absent tensor, no backward release, monotone streams."""
-    _, delta = rts
-    oracle_ref = pytest.importorskip("oracle.ref")
-    if not oracle_ref.available():
+def test_bench_paths_are_exercised_at_bs256(rts_any):
+    """The code paths only the bench size takes are really in the bs256 step:
+    256-wide BN-backward dgrad tiles, M a multiple of 128 everywhere, and the
+    one-launch (cooperative, grid-barrier) BN backward."""
+    base, _ = rts_any
+    from paper_2203_15980_b200 import kernels as K
+    widths = {name: d.tile_n for name, d in base._dconvs.items()}
+    Ms = {int(np.prod(n.shape[:-1])) for n in base.nodes
+          if len(n.shape) == 4 and n.shape[0] == base.batch}
+    if base.batch == 256:
+        assert 256 in widths.values(), widths
+        assert all(m % 128 == 0 for m in Ms)
+        assert K.BN_BWD_ONE_LAUNCH
+    elif base.batch == 250:
+        assert any(m % 128 for m in Ms)  # partial tiles
+
+
+def _certify(rt, x, y):
+    certify = pytest.importorskip("oracle.certify")
+    rt.x_dev.copy_(x)
+    rt.y_dev.copy_(y)
+    out = certify.certify(rt)
+    assert out["findings"] == [], out["findings"][:5]
+    if out["violations"] is None:
         pytest.skip("oracle/_ref not built")
+    assert out["violations"] == [], out["violations"][:5]
+    return out
+
+
+def test_executed_gpu_timeline_passes_reference_replay_check(rts):
+    """The timeline the GPU actually executed — the executor's device-side
+    action log (kind, node, %globaltimer head/tail per action) — matches the
+    lowered program action for action and in per-stream order, and the
+    reference's own independent verifier (ref src/oracle.cpp replay_check)
+    finds nothing: budget never exceeded, no read of an absent tensor, no
+    backward release, monotone non-overlapping streams."""
+    _, delta = rts
     x, y = make_batch(4)
-    delta.x_dev.copy_(x)
-    delta.y_dev.copy_(y)
-    ev = delta.executed_timeline()
-    plan = P.run_iteration(delta.trace(), delta.config).events
-    assert len(ev) == len(plan)
-    assert (ev["kind"] == plan["kind"]).all() and (ev["node"] == plan["node"]).all()
+    out = _certify(delta, x, y)
+    ev = out["events"]
     measured = ev[np.isin(ev["kind"], [P.EventKind.Compute, P.EventKind.Recompute])]
     assert (measured["duration"] > 0).any()
-    chrome = P.chrome_trace_events(ev)
-    violations = oracle_ref.replay_check(delta.trace().to_json(), delta.config, chrome)
-    assert violations == [], violations[:5]
 
 
 @pytest.mark.parametrize("frac,policy", [(0.55, P.PolicyMode.Delta), (0.7, P.PolicyMode.Delta),
@@ -303,7 +356,8 @@ def test_executed_gpu_timeline_passes_reference_replay_check(rts):
 def test_budgets_and_policies_bit_identical_and_certified(rts, frac, policy):
     """Other budgets and the single-mechanism policies (many offloads through
     the swap engine, or recompute only): the step stays bit-identical to the
-    no-eviction one and the executed timeline passes the reference verifier."""
+    no-eviction one and the executed timeline passes the reference verifier
+    with no exemption."""
     base, _ = rts
     rt = DeltaRuntime(50, BATCH, seed=0, lr=0.0)
     for n, m in zip(rt.nodes, base.nodes):
@@ -321,16 +375,27 @@ def test_budgets_and_policies_bit_identical_and_certified(rts, frac, policy):
     l1 = rt.step(x, y)
     assert l0 == l1
     assert torch.equal(g0, rt.params.grad)
-    oracle_ref = pytest.importorskip("oracle.ref")
-    if oracle_ref.available():
-        rt.x_dev.copy_(x)
-        rt.y_dev.copy_(y)
-        ev = rt.executed_timeline()
-        viol = oracle_ref.replay_check(rt.trace().to_json(), rt.config, P.chrome_trace_events(ev))
-        # our D2H and H2D copy engines run concurrently; the reference models one
-        # copy stream, so only overlapping-copy clock findings are acceptable
-        bad = [v for v in viol if not (v[0] == "NonmonotoneClock" and "overlaps" in v[3])]
-        assert bad == [], bad[:3]
+    _certify(rt, x, y)
+
+
+def test_offload_heavy_plan_certified(rts):
+    """A cost table where recomputing is expensive (every cost x50, as a
+    profiler-serialised measurement can produce): the Director offloads many
+    tensors, prefetches and demand reloads flow through the copy engine, and
+    the executed timeline still certifies and the step stays bit-identical."""
+    base, _ = rts
+    rt = DeltaRuntime(50, BATCH, seed=0, lr=0.0)
+    for n, m in zip(rt.nodes, base.nodes):
+        n.cost_us = m.cost_us * 50
+    rt.link_gbs = base.link_gbs
+    prog = rt.plan(0.5)
+    assert prog.plan_counts["offload"] > 3 and prog.plan_counts["reload"] > 3, prog.plan_counts
+    x, y = make_batch(8)
+    l0 = base.step(x, y)
+    g0 = base.params.grad.clone()
+    assert rt.step(x, y) == l0
+    assert torch.equal(g0, rt.params.grad)
+    _certify(rt, x, y)
 
 
 def test_resnet101_step_matches_no_eviction():
