@@ -46,6 +46,23 @@ build/acceptance_product: $(CPP_OBJS) /root/reference/proj/tests/acceptance_main
 	  -DDELTASIM_BIN=\"$(CURDIR)/build/delta-sim\" \
 	  /root/reference/proj/tests/acceptance_main.cpp $(filter $(OBJ)/plan/%,$(CPP_OBJS)) build/reforacle.o -o $@
 
+# The reference's unit suites (tests/test_*.cpp, minus test_cli.cpp which
+# needs the CLI11 CLI binary), compiled UNMODIFIED against libdelta's planner
+# with tests/doctest_shim standing in for the absent doctest header.
+REFT       := /root/reference/proj/tests
+UNIT_SRCS  := main trace state policy device engine oracle metrics matrix
+UNIT_OBJS  := $(addprefix build/unit/test_,$(addsuffix .o,$(UNIT_SRCS)))
+UNIT_FLAGS := -std=c++20 -O1 -Itests/doctest_shim -Ioracle/include -Iinclude -I$(JINC) \
+              -DDELTASIM_DATA_DIR=\"/root/reference/proj/data\" \
+              -DDELTASIM_GOLDEN_DIR=\"/root/reference/proj/tests/golden\" \
+              -DDELTASIM_BIN=\"$(CURDIR)/build/delta-sim\"
+build/unit/test_%.o: $(REFT)/test_%.cpp tests/doctest_shim/doctest.h
+	@mkdir -p build/unit
+	$(CXX) $(UNIT_FLAGS) -c $< -o $@
+build/unit_tests: $(UNIT_OBJS) $(CPP_OBJS)
+	$(CXX) -std=c++20 -O2 -Ioracle/include -Iinclude -I$(JINC) -c /root/reference/proj/src/oracle.cpp -o build/reforacle.o
+	$(CXX) $(UNIT_OBJS) $(filter $(OBJ)/plan/%,$(CPP_OBJS)) build/reforacle.o -o $@
+
 clean:
 	rm -rf build $(LIB)
 
