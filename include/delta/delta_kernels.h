@@ -33,6 +33,14 @@ typedef struct delta_conv delta_conv;
 delta_status delta_conv_create(int32_t N, int32_t H, int32_t W, int32_t C, int32_t K,
                                int32_t R, int32_t S, int32_t stride, int32_t pad,
                                const void* weight, delta_conv** out);
+/* As delta_conv_create with `pad` before the first row/column and
+ * pad_end_h / pad_end_w after the last (-1 = pad): P = H + pad + pad_end_h -
+ * R + 1 (stride 1 only).  The sub-pixel convolutions of a stride-2 input
+ * gradient are R', S' in {1, 2} with pad 0 and pad_end = R'-1, S'-1. */
+delta_status delta_conv_create_ex(int32_t N, int32_t H, int32_t W, int32_t C, int32_t K,
+                                  int32_t R, int32_t S, int32_t stride, int32_t pad,
+                                  int32_t pad_end_h, int32_t pad_end_w, const void* weight,
+                                  delta_conv** out);
 /* `stats` (nullable): [ceil(N*P*Q/128)][K] float2 (mean, M2) per 128-row tile
  * of the bf16 outputs — BatchNorm statistics partials fused in the epilogue. */
 delta_status delta_conv_forward(const delta_conv* c, const void* x, void* y, float* stats,
@@ -54,13 +62,19 @@ delta_status delta_conv_forward(const delta_conv* c, const void* x, void* y, flo
  *   DELTA_EPI_BN_BWD: y = g = bf16(acc) * [relu(bn(xc)) > 0] with the saved
  *       statistics (the forward's exact arithmetic), and `stats` receives the
  *       per-CTA (sum g, sum g*xc) partial rows for delta_bn_backward_from_partials.
+ *   DELTA_EPI_SCATTER2: the input gradient of a stride-2 3x3 (pad 1) conv
+ *       as four sub-pixel stride-1 convolutions over dY (parity class (a, b),
+ *       scatter = 2a + b, with the class's taps of the flipped weights,
+ *       delta_weight_view DELTA_VIEW_DGRAD_S2): output pixel (p, q) of class
+ *       (a, b) is written to y[n][2p+a][2q+b][:] of the [N][2P][2Q][K]
+ *       gradient.  The four classes tile y exactly once.
  * Output channels must be a multiple of 32 for the fused modes. */
-enum { DELTA_EPI_STORE = 0, DELTA_EPI_ADD_MASK = 1, DELTA_EPI_BN_BWD = 2 };
+enum { DELTA_EPI_STORE = 0, DELTA_EPI_ADD_MASK = 1, DELTA_EPI_BN_BWD = 2, DELTA_EPI_SCATTER2 = 3 };
 typedef struct delta_conv_epilogue {
   int32_t mode;
   int32_t pool_hw;
   int32_t add_stride2;
-  int32_t reserved;
+  int32_t scatter;
   const void* add;
   const void* add_mask;
   const void* out_mask;
@@ -154,6 +168,16 @@ delta_status delta_avgpool_fwd(const void* x, void* y, int32_t N, int32_t HW, in
 delta_status delta_softmax_xent(const float* logits, const int64_t* labels, float* loss,
                                 float* dlogits, float* row_ws, int32_t N, int32_t K,
                                 void* stream);
+/* The classifier head after the tensor-core FC GEMM (a 1x1 delta_conv over
+ * the pooled features, bf16 logits [N][ld], ld >= K the padded class count):
+ * z = logits + bias (fp32); loss = mean_i (logsumexp z_i - z_i[label_i]);
+ * dlogits = (softmax(z) - onehot) / N as fp32 [N][K] and as bf16 [N][ld]
+ * with zero pad columns (the operand of the head's dgrad and wgrad GEMMs);
+ * dbias = column sums of dlogits in row order.  K <= 1024. */
+delta_status delta_softmax_xent_head(const void* logits, int32_t ld, const float* bias,
+                                     const int64_t* labels, float* loss, float* dlogits,
+                                     void* dlogits_bf16, float* dbias, float* row_ws, int32_t N,
+                                     int32_t K, void* stream);
 
 /* ---- optimizer step and the per-step weight views (optim.cu) ---- */
 /* SGD with momentum and weight decay over flat fp32 buffers (n floats, 16 B
@@ -167,8 +191,14 @@ delta_status delta_sgd_step(float* w, float* mom, const float* g, void* wbf, int
  *   DELTA_VIEW_DGRAD: dst[c][r][s][k] = src[k][R-1-r][S-1-s][c] (input-gradient
  *                     convs through our kernel)
  *   DELTA_VIEW_STEM:  dst[k][256] pixel-pair stem layout (C = 4, 7x7): column
- *                     (r*4+j)*8 + e*4 + c = src[k][r][2j+e-1][c], zero elsewhere */
-enum { DELTA_VIEW_DGRAD = 0, DELTA_VIEW_STEM = 1 };
+ *                     (r*4+j)*8 + e*4 + c = src[k][r][2j+e-1][c], zero elsewhere
+ *   DELTA_VIEW_DGRAD_S2: (3x3 source) the weights of parity class (a, b) =
+ *                     (reserved >> 1, reserved & 1) of the stride-2 input
+ *                     gradient: dst[c][r'][s'][k], r' < 1+a, s' < 1+b, =
+ *                     src[k][ra(r')][sb(s')][c] with ra = 1 for a = 0 and
+ *                     ra(r') = 2 - 2r' for a = 1 (sub-tap r' reads dY row
+ *                     i + r'); same for columns */
+enum { DELTA_VIEW_DGRAD = 0, DELTA_VIEW_STEM = 1, DELTA_VIEW_DGRAD_S2 = 2 };
 typedef struct delta_weight_view {
   int32_t kind, K, R, S, C, reserved;
   const void* src;

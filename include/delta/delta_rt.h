@@ -11,10 +11,11 @@
  * statistics, whose saved values it reuses) and reproduce the retained
  * tensor bit for bit.
  *
- * Library work the kernels do not cover (cuDNN weight gradients, cuBLAS for
- * the classifier) is a DELTA_K_HOST op: the executor calls the registered
- * host callback, which enqueues that work on the stream it is given and may
- * return a device pointer later ops of the recipe read as a scratch operand.
+ * A DELTA_K_HOST op calls a registered host callback, which enqueues work on
+ * the stream it is given and may return a device pointer later ops of the
+ * recipe read as a scratch operand: the plug-in point for ops a caller brings
+ * itself.  The built-in ResNet recipes use none (every op of the step is one
+ * of this library's kernels).
  * Everything is asynchronous on the caller's stream, so a whole step can be
  * captured into one CUDA graph.  Errors are delta_status (delta.h).
  */
@@ -65,6 +66,10 @@ typedef struct delta_ref {
  *  SOFTMAX_XENT    r0 logits, r1 labels, r2 loss, r3 dlogits, r4 row_ws, i0 N, i1 K
  *  HOST            i0 host op id (passed to the host callback)
  *  WGRAD           conv = a delta_wgrad*, r0 dy, r1 x, r2 dw (fp32 KRSC), r3 ws
+ *  XENT_HEAD       r0 logits (bf16 [N][i2]), r1 bias, r2 labels, r3 loss,
+ *                  r4 dlogits (fp32 [N][i1]), r5 dlogits (bf16 [N][i2]),
+ *                  r6 dbias, r7 row_ws, i0 N, i1 K, i2 ld  (softmax_xent_head)
+ *  CONV_EX with i0 = DELTA_EPI_SCATTER2: i3 = the parity class (2a + b)
  */
 enum {
   DELTA_K_COPY = 1,
@@ -81,7 +86,8 @@ enum {
   DELTA_K_AVGPOOL = 12,
   DELTA_K_SOFTMAX_XENT = 13,
   DELTA_K_HOST = 14,
-  DELTA_K_WGRAD = 15
+  DELTA_K_WGRAD = 15,
+  DELTA_K_XENT_HEAD = 16
 };
 enum {
   DELTA_KOP_FIRST_ONLY = 1,     /* skipped when the node is recomputed        */

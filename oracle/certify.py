@@ -23,12 +23,17 @@ from . import ref
 
 
 def certify(rt) -> dict:
+    """The budget checked is the CALLER's (rt.budget_bytes): the runtime may
+    have planned under a smaller one so the packed arena fits it."""
+    import dataclasses
+
     from paper_2203_15980_b200 import planner as P
 
     findings: list = []
     ev = rt.executed_timeline(findings)
     viol = None
     if ref.available():
-        viol = ref.replay_check(rt.trace().to_json(), rt.config, P.chrome_trace_events(ev))
+        cfg = dataclasses.replace(rt.config, budget=getattr(rt, "budget_bytes", rt.config.budget))
+        viol = ref.replay_check(rt.trace().to_json(), cfg, P.chrome_trace_events(ev))
     return {"findings": findings, "violations": viol, "events": ev,
             "ok": not findings and (viol is None or viol == [])}

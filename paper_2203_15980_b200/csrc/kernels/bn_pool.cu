@@ -966,6 +966,69 @@ __global__ void __launch_bounds__(256) k_softmax_xent(const float* __restrict__ 
   if (threadIdx.x == 0) row_loss[n] = logf(sum) + mx - l[lab];
 }
 
+// The classifier head on the tensor-core GEMM's bf16 logits ([N][ld], the
+// class dimension padded to ld): logits + bias in fp32, softmax cross-entropy
+// per row -> row loss, dlogits (fp32 [N][K]) and its bf16 copy [N][ld] with
+// zero pad columns (the A operand of the head's input- and weight-gradient
+// GEMMs).
+__global__ void __launch_bounds__(256) k_softmax_xent_head(
+    const bf16* __restrict__ logits, int ld, const float* __restrict__ bias,
+    const int64_t* __restrict__ labels, float* __restrict__ dlogits, bf16* __restrict__ dl_bf16,
+    float* __restrict__ row_loss, int N, int K) {
+  pdl_wait();
+  pdl_trigger();
+  const int n = blockIdx.x;
+  const bf16* l = logits + int64_t(n) * ld;
+  __shared__ float red[256];
+  __shared__ float z[1024];
+  float mx = -INFINITY;
+  for (int k = threadIdx.x; k < K; k += blockDim.x) {
+    const float v = __bfloat162float(l[k]) + bias[k];
+    if (k < 1024) z[k] = v;
+    mx = fmaxf(mx, v);
+  }
+  red[threadIdx.x] = mx;
+  __syncthreads();
+  for (int s = 128; s > 0; s >>= 1) {
+    if (threadIdx.x < s) red[threadIdx.x] = fmaxf(red[threadIdx.x], red[threadIdx.x + s]);
+    __syncthreads();
+  }
+  mx = red[0];
+  __syncthreads();
+  float sum = 0.f;
+  for (int k = threadIdx.x; k < K; k += blockDim.x) sum += __expf(z[k] - mx);
+  red[threadIdx.x] = sum;
+  __syncthreads();
+  for (int s = 128; s > 0; s >>= 1) {
+    if (threadIdx.x < s) red[threadIdx.x] += red[threadIdx.x + s];
+    __syncthreads();
+  }
+  sum = red[0];
+  const int lab = int(labels[n]);
+  const float invN = 1.f / float(N);
+  for (int k = threadIdx.x; k < ld; k += blockDim.x) {
+    float d = 0.f;
+    if (k < K) {
+      d = (__expf(z[k] - mx) / sum - (k == lab ? 1.f : 0.f)) * invN;
+      dlogits[int64_t(n) * K + k] = d;
+    }
+    dl_bf16[int64_t(n) * ld + k] = __float2bfloat16_rn(d);
+  }
+  if (threadIdx.x == 0) row_loss[n] = logf(sum) + mx - z[lab];
+}
+
+// column sums of an fp32 [N][K] matrix in a fixed (row) order: the bias gradient
+__global__ void __launch_bounds__(256) k_col_sums(const float* __restrict__ a, int N, int K,
+                                                  float* __restrict__ out) {
+  pdl_wait();
+  pdl_trigger();
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= K) return;
+  float s = 0.f;
+  for (int n = 0; n < N; ++n) s += a[int64_t(n) * K + k];
+  out[k] = s;
+}
+
 __global__ void k_mean_rows(const float* row_loss, int N, float* loss) {
   pdl_wait();
   pdl_trigger();
@@ -1193,6 +1256,22 @@ cudaError_t maxpool3x3s2_bwd(const void* dy, const void* x, void* dx, int N, int
 cudaError_t avgpool_fwd(const void* x, void* y, int N, int HW, int C, cudaStream_t st) {
   const int64_t total = int64_t(N) * (C / 8);
   if (cudaError_t e_ = launch_k(k_avgpool_fwd, dim3(grid_for(total, 128)), dim3(128), 0, st, static_cast<const bf16*>(x), static_cast<bf16*>(y), N, HW, C)) return e_;
+  return cudaGetLastError();
+}
+
+cudaError_t softmax_xent_head(const void* logits, int ld, const float* bias,
+                              const int64_t* labels, float* loss, float* dlogits, void* dl_bf16,
+                              float* dbias, float* row_loss_ws, int N, int K, cudaStream_t st) {
+  if (K > 1024 || ld < K || (ld & 7)) return cudaErrorInvalidValue;
+  if (cudaError_t e_ = launch_k(k_softmax_xent_head, dim3(N), dim3(256), 0, st,
+                                static_cast<const bf16*>(logits), ld, bias, labels, dlogits,
+                                static_cast<bf16*>(dl_bf16), row_loss_ws, N, K))
+    return e_;
+  if (cudaError_t e_ = launch_k(k_col_sums, dim3((K + 255) / 256), dim3(256), 0, st,
+                                static_cast<const float*>(dlogits), N, K, dbias))
+    return e_;
+  if (cudaError_t e_ = launch_k(k_mean_rows, dim3(1), dim3(32), 0, st, row_loss_ws, N, loss))
+    return e_;
   return cudaGetLastError();
 }
 

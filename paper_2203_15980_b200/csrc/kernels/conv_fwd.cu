@@ -132,6 +132,9 @@ constexpr int EV_ADD_OM = 2;   // y = (bf16(acc) + add) & [out_mask > 0]
 constexpr int EV_POOL = 3;     // y = bf16(acc + pooled/hw * [add_mask > 0]) & [out_mask > 0]
 constexpr int EV_BN_BWD = 4;   // y = g = bf16(acc) & [relu(bn(xc)) > 0]; partials (sum g, sum g*xc)
 constexpr int EV_ADD_OM_ST = 5;  // EV_ADD_OM + partials (sum y, sum y*xc): the next BN's backward sums
+constexpr int EV_SCATTER = 6;  // y[n][2p+a][2q+b] = bf16(acc): a stride-2 input gradient's parity class
+// epilogues that read [M][K] operand tiles (the operand ring / tile buffers)
+__host__ __device__ constexpr bool ev_fused(int ev) { return ev != EV_STORE && ev != EV_SCATTER; }
 __host__ __device__ constexpr int ev_operands(int ev) {
   return ev == EV_ADD || ev == EV_BN_BWD
              ? 1
@@ -185,7 +188,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   // epilogue staging: 4 warps x 2 buffers x (32 rows x 64 B), 64B-swizzled
   const uint32_t sOut = sA + STAGES * (A_STAGE + B_STAGE);
   // fused-epilogue operand ring: EPI_W warps x EPI_RING_WARP
-  constexpr bool FUSED = EV != EV_STORE;
+  constexpr bool FUSED = ev_fused(EV);
   constexpr uint32_t EPI_RING_WARP = epi_ring_bytes<BN, STAGES>() / EPI_W;
   constexpr int NOPS_ = ev_operands(EV);
   constexpr uint32_t OPT_TILE = uint32_t(NOPS_) * BN * 256;  // per tile: NOPS x [128][BN] bf16
@@ -677,6 +680,21 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
         }
         if constexpr (FUSED) __syncwarp();  // every lane has read the slot before it is refilled
+        if constexpr (EV == EV_SCATTER) {
+          // one parity class of a stride-2 input gradient: output pixel
+          // (n, p, q) lands at (2p + a, 2q + b) of the [N][2P][2Q][K] gradient;
+          // each lane stores its row's 64 contiguous bytes
+          const int m = m0 + quarter * 32 + lane;
+          if (m < a.M && col < a.K) {
+            const int q = m % a.Q, t = m / a.Q;
+            const int p = t % a.P, n = t / a.P;
+            bf16* dst = a.y + ((int64_t(n) * (2 * a.P) + 2 * p + (a.e.scatter >> 1)) * (2 * a.Q) +
+                               2 * q + (a.e.scatter & 1)) * a.K + col;
+#pragma unroll
+            for (int u = 0; u < 4; ++u) reinterpret_cast<uint4*>(dst)[u] = pk[u];
+          }
+          continue;
+        }
         const uint32_t buf = stage_base + (ec % NBUF) * 2048;
         // the TMA store that last read this buffer (NBUF chunks ago) is done
         if (lane == 0) bulk_wait_read<NBUF - 1>();
@@ -828,7 +846,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 
 template <int BN, int STAGES, int EV, bool OPT>
 constexpr size_t conv_smem_bytes() {
-  constexpr bool FUSED = EV != EV_STORE;
+  constexpr bool FUSED = ev_fused(EV);
   return size_t(STAGES) * (BM * 128 + BN * 128) + 16384 /*epilogue staging*/ +
          (!FUSED ? 0
           : OPT  ? size_t(OPT_NB) * ev_operands(EV) * BN * 256
@@ -888,7 +906,7 @@ bool encode_im2col(CUtensorMap* m, const void* x, const ConvPlan& cp) {
   cuuint64_t strides[3] = {cuuint64_t(cp.C) * 2, cuuint64_t(cp.W) * cp.C * 2,
                            cuuint64_t(cp.H) * cp.W * cp.C * 2};
   int lower[2] = {-cp.pad, -cp.pad};
-  int upper[2] = {cp.pad - (cp.S - 1), cp.pad - (cp.R - 1)};
+  int upper[2] = {cp.pad_end_w - (cp.S - 1), cp.pad_end_h - (cp.R - 1)};
   cuuint32_t estr[4] = {1, cuuint32_t(cp.stride), cuuint32_t(cp.stride), 1};
   return fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(x), dims, strides, lower,
             upper, 64, BM, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
@@ -1060,8 +1078,12 @@ int conv_plan_init(ConvPlan* cp, const void* w) {
   // the C=4 stem path is the 7x7/2 pad-3 ResNet stem over an even width
   if (cp->C == 4 && (cp->R != 7 || cp->S != 7 || cp->stride != 2 || cp->pad != 3 || (cp->W & 1)))
     return 1;
-  cp->P = (cp->H + 2 * cp->pad - cp->R) / cp->stride + 1;
-  cp->Q = (cp->W + 2 * cp->pad - cp->S) / cp->stride + 1;
+  if (cp->pad_end_h < 0) cp->pad_end_h = cp->pad;
+  if (cp->pad_end_w < 0) cp->pad_end_w = cp->pad;
+  if ((cp->pad_end_h != cp->pad || cp->pad_end_w != cp->pad) && (cp->C == 4 || cp->stride != 1))
+    return 1;  // asymmetric padding: stride-1, im2col / 1x1 paths only
+  cp->P = (cp->H + cp->pad + cp->pad_end_h - cp->R) / cp->stride + 1;
+  cp->Q = (cp->W + cp->pad + cp->pad_end_w - cp->S) / cp->stride + 1;
   cp->kdim = cp->C == 4 ? 256 : cp->R * cp->S * cp->C;
   cp->bn = cp->K <= 64 ? 64 : (cp->K <= 128 ? 128 : 256);
   // 3x3 stride-1, 64 -> 64 channels: stage the input halo once per tile with
@@ -1106,8 +1128,23 @@ cudaError_t conv_forward(const ConvPlan& cp, const void* x, void* y, float* stat
   if (e.mode == EPI_BN_BWD && (!e.xc || !e.mean || !e.invstd || !e.gamma || !e.beta))
     return cudaErrorInvalidValue;
   const bool stem = cp.C == 4;
-  const bool tma_a = !stem && cp.R == 1 && cp.S == 1 && cp.stride == 1 && cp.pad == 0;
+  const bool tma_a = !stem && cp.R == 1 && cp.S == 1 && cp.stride == 1 && cp.pad == 0 &&
+                     cp.pad_end_h == 0 && cp.pad_end_w == 0;
   const bool use_gather = gather_forced();
+  if (e.mode == EPI_SCATTER2) {
+    if (stats || (cp.K % 32) || stem || unsigned(e.scatter) > 3u) return cudaErrorInvalidValue;
+    switch (cp.bn) {
+      case 64:
+        return tma_a ? launch<64, 8, MODE_TMA, EV_SCATTER>(cp, x, y, nullptr, e, st)
+                     : launch<64, 8, MODE_IM2COL, EV_SCATTER>(cp, x, y, nullptr, e, st);
+      case 128:
+        return tma_a ? launch<128, 6, MODE_TMA, EV_SCATTER>(cp, x, y, nullptr, e, st)
+                     : launch<128, 6, MODE_IM2COL, EV_SCATTER>(cp, x, y, nullptr, e, st);
+      default:
+        return tma_a ? launch<256, 4, MODE_TMA, EV_SCATTER>(cp, x, y, nullptr, e, st)
+                     : launch<256, 4, MODE_IM2COL, EV_SCATTER>(cp, x, y, nullptr, e, st);
+    }
+  }
   if (cp.halo && e.mode == EPI_STORE && !use_gather) return conv_halo_forward(cp, x, y, stats, st);
   if (e.mode != EPI_STORE) {
     // fused epilogues (backward dgrad): fewer stages pay for the operand ring;

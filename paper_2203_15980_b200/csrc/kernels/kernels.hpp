@@ -11,6 +11,7 @@ namespace delta_k {
 // ---- implicit-GEMM convolution (conv_fwd.cu) ----
 struct ConvPlan {
   int N, H, W, C, K, R, S, stride, pad;
+  int pad_end_h, pad_end_w;  // padding after the last row / column (conv_plan_init: -1 = pad)
   int P, Q, kdim, bn;
   int halo, halo_slot, halo_rows;  // 3x3 stride-1: input halo staged per tile (conv_halo.cu)
   int stem_rows;                   // C=4 stem: one output row per tile (conv_fwd.cu MODE_STEMROW)
@@ -23,13 +24,16 @@ struct ConvPlan {
 //                add / pool_hw, times [add_mask > 0]             (gradient adds)
 //   EPI_BN_BWD   y = g = bf16(acc) * [relu(bn(xc)) > 0], partials (sum g,
 //                sum g*xc) per 128-row tile                     (BN+ReLU backward)
-constexpr int EPI_STORE = 0, EPI_ADD_MASK = 1, EPI_BN_BWD = 2;
+//   EPI_SCATTER2 y[n][2p+a][2q+b][k] = bf16(acc) into a [N][2P][2Q][K] tensor,
+//                (a, b) = (scatter >> 1, scatter & 1): one parity class of a
+//                stride-2 input gradient (sub-pixel decomposition)
+constexpr int EPI_STORE = 0, EPI_ADD_MASK = 1, EPI_BN_BWD = 2, EPI_SCATTER2 = 3;
 struct ConvEpilogue {
   int mode;
   int pool_hw;
   int add_stride2;  // EPI_ADD_MASK: `add` is given at the even rows/columns only,
                     // as a [N][P/2][Q/2][K] tensor (zero elsewhere)
-  int pad_;
+  int scatter;      // EPI_SCATTER2: parity class a*2 + b
   const void* add;
   const void* add_mask;
   const void* out_mask;
@@ -124,5 +128,10 @@ cudaError_t avgpool_fwd(const void* x, void* y, int N, int HW, int C, cudaStream
 // loss = mean_i -log softmax(logits_i)[label_i]; dlogits = (softmax - onehot) / N
 cudaError_t softmax_xent(const float* logits, const int64_t* labels, float* loss, float* dlogits,
                          float* row_loss_ws, int N, int K, cudaStream_t st);
+// classifier head on bf16 GEMM logits [N][ld] (+ fp32 bias): loss, dlogits
+// fp32 [N][K], its bf16 copy [N][ld] (zero pad columns), dbias = column sums
+cudaError_t softmax_xent_head(const void* logits, int ld, const float* bias,
+                              const int64_t* labels, float* loss, float* dlogits, void* dl_bf16,
+                              float* dbias, float* row_loss_ws, int N, int K, cudaStream_t st);
 
 }  // namespace delta_k

@@ -12,6 +12,8 @@
 //                   weights [K][R][S][C], one table entry per tensor:
 //                   DELTA_VIEW_DGRAD  W'[c][r][s][k] = W[k][R-1-r][S-1-s][c]
 //                                     (input-gradient convs on our kernel)
+//                   DELTA_VIEW_DGRAD_S2 the taps of one parity class of a
+//                                     stride-2 3x3 input gradient (sub-pixel)
 //                   DELTA_VIEW_STEM   [K][256] pixel-pair stem layout, column
 //                                     (r*4+j)*8 + e*4 + c = W[k][r][2j+e-1][c]
 #include <cuda_bf16.h>
@@ -79,22 +81,31 @@ __global__ void __launch_bounds__(256)
   const bf16* src = static_cast<const bf16*>(v.src);
   bf16* dst = static_cast<bf16*>(v.dst);
   const int K = v.K, R = v.R, S = v.S, C = v.C;
-  if (v.kind == DELTA_VIEW_DGRAD) {
-    // per filter tap (r, s): dst_tap[c][k] = src_tap'[k][c], tap' = (R-1-r, S-1-s)
-    // — a K x C transpose in 32 x 32 tiles through shared memory (both sides
-    // coalesced); 256 threads = 32 columns x 8 rows, 4 rows each
+  if (v.kind == DELTA_VIEW_DGRAD || v.kind == DELTA_VIEW_DGRAD_S2) {
+    // per destination filter tap (r, s): dst_tap[c][k] = src_tap'[k][c] — a
+    // K x C transpose in 32 x 32 tiles through shared memory (both sides
+    // coalesced); 256 threads = 32 columns x 8 rows, 4 rows each.
+    //   DGRAD:    R x S taps, tap' = (R-1-r, S-1-s)
+    //   DGRAD_S2: parity class (a, b) = (reserved >> 1, reserved & 1) of a
+    //             stride-2 3x3 conv: (1+a) x (1+b) taps; sub-pixel tap t of a
+    //             class reads dY at offset +t and weight row s2(a, t) with
+    //             s2(0, 0) = 1, s2(1, 0) = 2, s2(1, 1) = 0 (same for columns)
     __shared__ bf16 tile[32][33];
-    const int taps = R * S, tk = (K + 31) >> 5, tc = (C + 31) >> 5;
+    const bool s2 = v.kind == DELTA_VIEW_DGRAD_S2;
+    const int pa = v.reserved >> 1, pb = v.reserved & 1;
+    const int Rd = s2 ? 1 + pa : R, Sd = s2 ? 1 + pb : S;
+    const int taps = Rd * Sd, tk = (K + 31) >> 5, tc = (C + 31) >> 5;
     const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
     for (int t = blockIdx.x; t < taps * tk * tc; t += gridDim.x) {
       const int tap = t / (tk * tc), rem = t - tap * (tk * tc);
       const int k0 = (rem / tc) * 32, c0 = (rem % tc) * 32;
-      const int r = tap / S, s = tap - r * S;
-      const int src_tap = (R - 1 - r) * S + (S - 1 - s);
+      const int r = tap / Sd, s = tap - r * Sd;
+      const int src_tap = s2 ? (pa ? 2 - 2 * r : 1) * S + (pb ? 2 - 2 * s : 1)
+                             : (R - 1 - r) * S + (S - 1 - s);
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
         const int k = k0 + ty + 8 * i, c = c0 + tx;
-        if (k < K && c < C) tile[ty + 8 * i][tx] = src[(int64_t(k) * taps + src_tap) * C + c];
+        if (k < K && c < C) tile[ty + 8 * i][tx] = src[(int64_t(k) * R * S + src_tap) * C + c];
       }
       __syncthreads();
 #pragma unroll

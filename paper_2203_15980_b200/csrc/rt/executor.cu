@@ -132,6 +132,7 @@ delta_status run_kop(delta_rt* rt, const delta_kop& k, Frame& fr, uint64_t node,
       ep.mode = int(i[0]);
       ep.pool_hw = int(i[1]);
       ep.add_stride2 = int(i[2]);
+      ep.scatter = int(i[3]);
       ep.add = ref(fr, r[3]);
       ep.add_mask = ref(fr, r[4]);
       ep.out_mask = ref(fr, r[5]);
@@ -193,6 +194,12 @@ delta_status run_kop(delta_rt* rt, const delta_kop& k, Frame& fr, uint64_t node,
       e = delta_k::softmax_xent(rp<const float>(fr, r[0]), rp<const int64_t>(fr, r[1]),
                                 rp<float>(fr, r[2]), rp<float>(fr, r[3]), rp<float>(fr, r[4]),
                                 int(i[0]), int(i[1]), st);
+      break;
+    case DELTA_K_XENT_HEAD:
+      e = delta_k::softmax_xent_head(ref(fr, r[0]), int(i[2]), rp<const float>(fr, r[1]),
+                                     rp<const int64_t>(fr, r[2]), rp<float>(fr, r[3]),
+                                     rp<float>(fr, r[4]), ref(fr, r[5]), rp<float>(fr, r[6]),
+                                     rp<float>(fr, r[7]), int(i[0]), int(i[1]), st);
       break;
     case DELTA_K_WGRAD: {
       auto* w = reinterpret_cast<const delta_wgrad*>(k.conv);

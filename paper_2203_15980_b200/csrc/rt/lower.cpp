@@ -86,35 +86,94 @@ Program lower_plan(const Trace& trace, const EngineConfig& cfg,
     }
   }
 
-  // ---- 2. offsets: largest first, lowest non-conflicting offset ----
+  // ---- 2. offsets: offline packing of known lifetimes ----
+  // Several greedy orders (largest first; longest-lived first; size x
+  // lifetime; allocation order), each placing an allocation at the lowest
+  // offset clear of every already-placed overlapping lifetime; the smallest
+  // footprint wins (ties: the earlier order).  The footprint can only exceed
+  // the pool peak through fragmentation, which is reported, never hidden.
   {
-    std::vector<std::size_t> order(allocs.size());
-    for (std::size_t i = 0; i < order.size(); ++i) order[i] = i;
-    std::stable_sort(order.begin(), order.end(), [&](std::size_t a, std::size_t b) {
-      if (allocs[a].bytes != allocs[b].bytes) return allocs[a].bytes > allocs[b].bytes;
-      return allocs[a].born < allocs[b].born;
-    });
-    std::vector<std::size_t> placed;
-    std::vector<std::pair<std::uint64_t, std::uint64_t>> busy;
-    std::uint64_t footprint = 0;
-    for (std::size_t idx : order) {
-      Alloc& a = allocs[idx];
-      busy.clear();
-      for (std::size_t j : placed) {
-        const Alloc& b = allocs[j];
-        if (a.born < b.died && b.born < a.died) busy.push_back({b.offset, b.offset + b.bytes});
+    const std::size_t n = allocs.size();
+    auto life = [&](const Alloc& a) {
+      return (a.died == kNever ? std::uint64_t(ops.size()) : a.died) - a.born;
+    };
+    // best_fit: the smallest gap that holds the allocation (else the top)
+    auto pack = [&](const std::vector<std::size_t>& order, std::vector<std::uint64_t>& off,
+                    bool best_fit) {
+      off.assign(n, 0);
+      std::vector<std::size_t> placed;
+      placed.reserve(n);
+      std::vector<std::pair<std::uint64_t, std::uint64_t>> busy;
+      std::uint64_t footprint = 0;
+      for (std::size_t idx : order) {
+        const Alloc& a = allocs[idx];
+        busy.clear();
+        for (std::size_t j : placed) {
+          const Alloc& b = allocs[j];
+          if (a.born < b.died && b.born < a.died) busy.push_back({off[j], off[j] + b.bytes});
+        }
+        std::sort(busy.begin(), busy.end());
+        std::uint64_t o = 0, pick = kNever, pick_gap = kNever;
+        for (auto& r : busy) {
+          if (r.first >= o + a.bytes) {  // a gap [o, r.first) that fits
+            if (!best_fit) break;
+            if (r.first - o < pick_gap) {
+              pick_gap = r.first - o;
+              pick = o;
+            }
+          }
+          o = std::max(o, r.second);
+        }
+        if (!best_fit || pick == kNever) pick = o;
+        off[idx] = pick;
+        footprint = std::max(footprint, pick + a.bytes);
+        placed.push_back(idx);
       }
-      std::sort(busy.begin(), busy.end());
-      std::uint64_t off = 0;
-      for (auto& r : busy) {
-        if (r.first >= off + a.bytes) break;  // fits in the gap below r
-        off = std::max(off, r.second);
+      return footprint;
+    };
+    std::vector<std::size_t> base(n);
+    for (std::size_t i = 0; i < n; ++i) base[i] = i;
+    std::vector<std::vector<std::size_t>> orders;
+    auto by = [&](auto key) {
+      std::vector<std::size_t> o = base;
+      std::stable_sort(o.begin(), o.end(), [&](std::size_t x, std::size_t y) {
+        const auto kx = key(allocs[x]), ky = key(allocs[y]);
+        if (kx != ky) return kx > ky;
+        return allocs[x].born < allocs[y].born;
+      });
+      orders.push_back(std::move(o));
+    };
+    by([](const Alloc& a) { return a.bytes; });
+    by([&](const Alloc& a) { return life(a); });
+    by([&](const Alloc& a) { return static_cast<unsigned __int128>(a.bytes) * life(a); });
+    orders.push_back(base);  // allocation order
+    // a few deterministic perturbations of the size order (fixed seed: the
+    // packing is a pure function of the plan)
+    std::uint64_t rng = 0x9E3779B97F4A7C15ull;
+    for (int rep = 0; rep < 24; ++rep) {
+      std::vector<std::size_t> o = orders[0];
+      for (std::size_t i = 0; i + 1 < o.size(); ++i) {
+        rng ^= rng << 13;
+        rng ^= rng >> 7;
+        rng ^= rng << 17;
+        if ((rng & 3) == 0) std::swap(o[i], o[i + 1]);
       }
-      a.offset = off;
-      footprint = std::max(footprint, off + a.bytes);
-      placed.push_back(idx);
+      orders.push_back(std::move(o));
     }
-    prog.arena_bytes = footprint;
+    std::uint64_t best = kNever;
+    std::vector<std::uint64_t> off, best_off;
+    for (const auto& o : orders) {
+      for (int bf = 0; bf < 2; ++bf) {
+        const std::uint64_t f = pack(o, off, bf == 1);
+        if (f < best) {
+          best = f;
+          best_off = off;
+        }
+      }
+      if (best <= prog.plan.peak_bytes) break;  // cannot do better than the pool peak
+    }
+    for (std::size_t i = 0; i < n; ++i) allocs[i].offset = n ? best_off[i] : 0;
+    prog.arena_bytes = n ? best : 0;
   }
 
   // ---- 3. actions with dependencies ----

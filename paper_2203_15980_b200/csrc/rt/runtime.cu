@@ -44,10 +44,17 @@ extern "C" {
 delta_status delta_conv_create(int32_t N, int32_t H, int32_t W, int32_t C, int32_t K, int32_t R,
                                int32_t S_, int32_t stride, int32_t pad, const void* weight,
                                delta_conv** out) {
+  return delta_conv_create_ex(N, H, W, C, K, R, S_, stride, pad, -1, -1, weight, out);
+}
+
+delta_status delta_conv_create_ex(int32_t N, int32_t H, int32_t W, int32_t C, int32_t K, int32_t R,
+                                  int32_t S_, int32_t stride, int32_t pad, int32_t pad_end_h,
+                                  int32_t pad_end_w, const void* weight, delta_conv** out) {
   auto* c = new delta_conv;
   std::memset(&c->plan, 0, sizeof(c->plan));
   c->plan.N = N; c->plan.H = H; c->plan.W = W; c->plan.C = C; c->plan.K = K;
   c->plan.R = R; c->plan.S = S_; c->plan.stride = stride; c->plan.pad = pad;
+  c->plan.pad_end_h = pad_end_h; c->plan.pad_end_w = pad_end_w;
   c->weight = weight;
   int rc = delta_k::conv_plan_init(&c->plan, weight);
   if (rc != 0) {
@@ -76,6 +83,7 @@ delta_status delta_conv_forward_ex(const delta_conv* c, const void* x, void* y, 
     e.mode = epi->mode;
     e.pool_hw = epi->pool_hw;
     e.add_stride2 = epi->add_stride2;
+    e.scatter = epi->scatter;
     e.add = epi->add;
     e.add_mask = epi->add_mask;
     e.out_mask = epi->out_mask;
@@ -220,6 +228,15 @@ delta_status delta_maxpool3x3s2_bwd(const void* dy, const void* x, void* dx, int
 delta_status delta_avgpool_fwd(const void* x, void* y, int32_t N, int32_t HW, int32_t C,
                                void* stream) {
   return cuda_status(delta_k::avgpool_fwd(x, y, N, HW, C, S(stream)), "avgpool_fwd");
+}
+
+delta_status delta_softmax_xent_head(const void* logits, int32_t ld, const float* bias,
+                                     const int64_t* labels, float* loss, float* dlogits,
+                                     void* dlogits_bf16, float* dbias, float* row_ws, int32_t N,
+                                     int32_t K, void* stream) {
+  return cuda_status(delta_k::softmax_xent_head(logits, ld, bias, labels, loss, dlogits,
+                                                dlogits_bf16, dbias, row_ws, N, K, S(stream)),
+                     "softmax_xent_head");
 }
 
 delta_status delta_softmax_xent(const float* logits, const int64_t* labels, float* loss,

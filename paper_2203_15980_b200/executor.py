@@ -5,8 +5,8 @@ A recipe is the list of kernel ops that (re)produce one node; operands are
 symbolic arena references (OUT, IN(i)), absolute device pointers, or the
 pointer a HOST op of the same recipe returned (SCRATCH(k)).  The executor
 (csrc/rt/executor.cu) walks the lowered action program in C++ and launches
-them; HOST ops call back into Python for the library work (cuDNN weight
-gradients, cuBLAS classifier GEMMs)."""
+them; HOST ops (a plug-in point for caller-supplied work; the built-in
+ResNet recipes use none) call back into Python."""
 from __future__ import annotations
 
 import ctypes as C
@@ -20,7 +20,8 @@ vp, i32, i64, u32, u64, f32 = C.c_void_p, C.c_int32, C.c_int64, C.c_uint32, C.c_
 
 REF_PTR, REF_OUT, REF_IN, REF_SCRATCH = 0, 1, 2, 3
 (K_COPY, K_CONV, K_CONV_EX, K_BN_STATS, K_BN_STATS_PARTS, K_BN_APPLY, K_BN_BWD, K_BN_BWD_PARTS,
- K_ADD_GRAD, K_MAXPOOL_FWD, K_MAXPOOL_BWD, K_AVGPOOL, K_SOFTMAX_XENT, K_HOST, K_WGRAD) = range(1, 16)
+ K_ADD_GRAD, K_MAXPOOL_FWD, K_MAXPOOL_BWD, K_AVGPOOL, K_SOFTMAX_XENT, K_HOST, K_WGRAD,
+ K_XENT_HEAD) = range(1, 17)
 FIRST_ONLY, RECOMPUTE_ONLY, SIDE = 1, 2, 4
 
 

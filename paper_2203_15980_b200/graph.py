@@ -151,8 +151,13 @@ def build_resnet(depth: int = 50, batch: int = 256, image: int = 224,
     pooled = g.add("avgpool", "avgpool", (N, cur.shape[-1]), [cur.id])
     pooled.hbm_bytes = cur.nbytes + pooled.nbytes
     g.fc = (cur.shape[-1], num_classes)
-    logits = g.add("fc", "fc", (N, num_classes), [pooled.id], dtype_bytes=4)
+    # the classifier GEMM's bf16 logits, classes padded to a multiple of 64
+    # (zero weight rows): the tensor-core kernel's N tile; bias and softmax
+    # are applied in fp32 by the head kernel
+    g.fc_pad = (num_classes + 63) // 64 * 64
+    logits = g.add("fc", "fc", (N, g.fc_pad), [pooled.id])
     logits.flops = 2.0 * N * cur.shape[-1] * num_classes
+    logits.hbm_bytes = pooled.nbytes + logits.nbytes
 
     # ---- backward (one node per gradient the step writes) ----
     # head: softmax-xent + fc backward -> dPooled

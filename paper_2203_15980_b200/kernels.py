@@ -13,6 +13,8 @@ vp, i32, i64, u32, u64, f32 = C.c_void_p, C.c_int32, C.c_int64, C.c_uint32, C.c_
 P = C.POINTER
 _SIGS = {
     "delta_conv_create": (i32, [i32] * 9 + [vp, P(vp)]),
+    "delta_conv_create_ex": (i32, [i32] * 11 + [vp, P(vp)]),
+    "delta_softmax_xent_head": (i32, [vp, i32, vp, vp, vp, vp, vp, vp, vp, i32, i32, vp]),
     "delta_conv_forward": (i32, [vp, vp, vp, vp, vp]),
     "delta_stats_parts": (i32, []),
     "delta_stats_partials_floats": (i64, [i32]),
@@ -64,12 +66,12 @@ def _count(n: int):
     LAUNCHES[0] += n
 
 
-EPI_STORE, EPI_ADD_MASK, EPI_BN_BWD = 0, 1, 2
+EPI_STORE, EPI_ADD_MASK, EPI_BN_BWD, EPI_SCATTER2 = 0, 1, 2, 3
 
 
 class ConvEpilogue(C.Structure):
     """delta_conv_epilogue (include/delta/delta_kernels.h)."""
-    _fields_ = [("mode", i32), ("pool_hw", i32), ("add_stride2", i32), ("reserved", i32),
+    _fields_ = [("mode", i32), ("pool_hw", i32), ("add_stride2", i32), ("scatter", i32),
                 ("add", vp), ("add_mask", vp), ("out_mask", vp),
                 ("xc", vp), ("mean", vp), ("invstd", vp), ("gamma", vp), ("beta", vp)]
 
@@ -77,10 +79,13 @@ class ConvEpilogue(C.Structure):
 class Conv:
     """tcgen05 implicit-GEMM convolution with a cached weight TMA descriptor."""
 
-    def __init__(self, N, H, W, Cin, K, R, S, stride, pad, weight_ptr: int):
+    def __init__(self, N, H, W, Cin, K, R, S, stride, pad, weight_ptr: int,
+                 pad_end: tuple | None = None):
+        """pad_end = (rows, cols) of padding after the input (default: pad)."""
         self._h = vp()
-        check(lib.delta_conv_create(N, H, W, Cin, K, R, S, stride, pad, weight_ptr,
-                                    C.byref(self._h)))
+        pe_h, pe_w = pad_end if pad_end is not None else (-1, -1)
+        check(lib.delta_conv_create_ex(N, H, W, Cin, K, R, S, stride, pad, pe_h, pe_w, weight_ptr,
+                                       C.byref(self._h)))
         p, q, kd, tn = i32(), i32(), i32(), i32()
         lib.delta_conv_geometry(self._h, C.byref(p), C.byref(q), C.byref(kd), C.byref(tn))
         self.P, self.Q, self.kdim, self.tile_n = p.value, q.value, kd.value, tn.value
@@ -106,6 +111,13 @@ class Conv:
         e = ConvEpilogue(EPI_ADD_MASK, pool_hw, int(add_stride2), 0, add, add_mask, out_mask,
                          xc, None, None, None, None)
         check(lib.delta_conv_forward_ex(self._h, x_ptr, y_ptr, partials_ptr, C.byref(e), stream))
+        _count(1)
+
+    def scatter2(self, x_ptr, y_ptr, cls: int, stream):
+        """parity class `cls` = 2a + b of a stride-2 input gradient: output
+        (p, q) written to y[n][2p+a][2q+b] of the [N][2P][2Q][K] tensor."""
+        e = ConvEpilogue(EPI_SCATTER2, 0, 0, cls, None, None, None, None, None, None, None, None)
+        check(lib.delta_conv_forward_ex(self._h, x_ptr, y_ptr, None, C.byref(e), stream))
         _count(1)
 
     def bn_bwd(self, x_ptr, g_ptr, partials_ptr, xc, mean, invstd, gamma, beta, stream):
@@ -205,7 +217,7 @@ def bn_apply(mode, x, res, y, M, C_, mean, invstd, gamma, beta, mean2=None, invs
     _count(1)
 
 
-VIEW_DGRAD, VIEW_STEM = 0, 1
+VIEW_DGRAD, VIEW_STEM, VIEW_DGRAD_S2 = 0, 1, 2
 
 
 class WeightView(C.Structure):
@@ -263,6 +275,13 @@ def maxpool_bwd(dy, x, dx, N, H, W, C_, ws, stream):
 def avgpool_fwd(x, y, N, HW, C_, stream):
     check(lib.delta_avgpool_fwd(x, y, N, HW, C_, stream))
     _count(1)
+
+
+def softmax_xent_head(logits, ld, bias, labels, loss, dlogits, dl_bf16, dbias, row_ws, N, K,
+                      stream):
+    check(lib.delta_softmax_xent_head(logits, ld, bias, labels, loss, dlogits, dl_bf16, dbias,
+                                      row_ws, N, K, stream))
+    _count(3)
 
 
 def softmax_xent(logits, labels, loss, dlogits, row_ws, N, K, stream):

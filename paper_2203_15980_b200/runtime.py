@@ -13,12 +13,14 @@ and recompute of a node run the SAME sm_100a kernel on the same inputs, so a
 recomputed tensor is bit-identical to the one it replaces.
 
 Outside the activation budget (as in the paper): fp32 master weights, bf16
-weight copies, gradients, optimizer state, BN statistics and the transient
-workspace of cuDNN's conv backward (dgrad/wgrad, the one library call on the
-backward path).
+weight copies, gradients, optimizer state, BN statistics and the backward
+scratch (the stride-2 input gradients before their BN backward, the weight-
+gradient split-K partials).  Every op of the step is one of this library's
+sm_100a kernels: no cuDNN, cuBLAS or host callbacks on the step.
 """
 from __future__ import annotations
 
+import dataclasses
 import math
 import time
 from dataclasses import dataclass
@@ -36,23 +38,10 @@ BN_EPS = 1e-5
 # length is at least this; shorter convs get a separate streaming statistics
 # pass.  0 = every conv (measured A/B on one box with 8 epilogue warps:
 # 11.57k vs 11.44k img/s; with 4 epilogue warps it was a wash, hence the old 384).
-OWN_DGRAD_3X3 = __import__("os").environ.get("DELTA_OWN_DGRAD_3X3", "1") == "1"
 DGRAD_BN256 = __import__("os").environ.get("DELTA_DGRAD_BN256", "1") == "1"
 FUSE_STATS_MIN_KDIM = int(__import__("os").environ.get("DELTA_FUSE_STATS_MIN_KDIM", "0"))
 BN_MOMENTUM = 0.1
 _TORCH_OPTIM = __import__("os").environ.get("DELTA_TORCH_OPTIM", "0") == "1"
-
-
-class _tf32:
-    """The classifier's fp32 GEMMs (library calls, 1 GFLOP each) on the tensor
-    cores (TF32) instead of SIMT fp32: 90 -> ~25 us per fc backward."""
-
-    def __enter__(self):
-        self.prev = torch.backends.cuda.matmul.allow_tf32
-        torch.backends.cuda.matmul.allow_tf32 = True
-
-    def __exit__(self, *exc):
-        torch.backends.cuda.matmul.allow_tf32 = self.prev
 
 
 def _ptr(t: torch.Tensor) -> int:
@@ -69,11 +58,15 @@ class Params:
         specs = []  # (name, shape, init)
         for name, cs in g.convs.items():
             specs.append(("conv:" + name, (cs.cout, cs.k, cs.k, cs.cin), "kaiming", cs))
+        # the classifier weight right after the conv weights (its bf16 copy is
+        # part of the same leading slice), classes padded to the GEMM's tile
+        # with zero rows (zero gradient, so they stay zero)
+        cin, ncls = g.fc
+        self.fc_pad = g.fc_pad
+        specs.append(("fc_w_full", (g.fc_pad, cin), "linear", (cin, ncls)))
         for name, c in g.bns.items():
             specs.append(("bn_g:" + name, (c,), "ones", None))
             specs.append(("bn_b:" + name, (c,), "zeros", None))
-        cin, ncls = g.fc
-        specs.append(("fc_w", (ncls, cin), "linear", cin))
         specs.append(("fc_b", (ncls,), "linear_b", cin))
         sizes = [int(np.prod(s[1])) for s in specs]
         total = sum(sizes)
@@ -96,16 +89,23 @@ class Params:
                 host.fill_(1.0)
             elif init == "zeros":
                 host.zero_()
+            elif init == "linear":
+                fan_in, rows = extra
+                host.zero_()
+                host[:rows].uniform_(-1.0 / math.sqrt(fan_in), 1.0 / math.sqrt(fan_in), generator=gen)
             else:
                 bound = 1.0 / math.sqrt(extra)
                 host.uniform_(-bound, bound, generator=gen)
             self.master[off:off + n].copy_(host.reshape(-1))
             self.views[name] = self.master[off:off + n].view(shape)
             self.gviews[name] = self.grad[off:off + n].view(shape)
-            if init == "kaiming":
+            if init in ("kaiming", "linear"):
                 n_conv = off + n
             off += n
-        self.n_conv = n_conv  # conv weights are the leading slice
+        # the classifier weight as the (ncls, cin) parameter it is
+        self.views["fc_w"] = self.views["fc_w_full"][:ncls]
+        self.gviews["fc_w"] = self.gviews["fc_w_full"][:ncls]
+        self.n_conv = n_conv  # conv + classifier weights are the leading slice (bf16 copy)
         self.conv_bf16 = torch.empty(n_conv, dtype=torch.bfloat16, device=device)
         self.wbf = {}
         off = 0
@@ -113,6 +113,8 @@ class Params:
             n = cs.cout * cs.k * cs.k * cs.cin
             self.wbf[name] = self.conv_bf16[off:off + n].view(cs.cout, cs.k, cs.k, cs.cin)
             off += n
+        # classifier GEMM operand: [fc_pad][1][1][cin] (a 1x1 conv's KRSC weights)
+        self.wbf["fc"] = self.conv_bf16[off:off + g.fc_pad * cin].view(g.fc_pad, 1, 1, cin)
         # the stem kernel reads its weights in the pixel-pair layout
         self.stem_packed = {}
         for name, cs in g.convs.items():
@@ -126,6 +128,16 @@ class Params:
             if own_dgrad(cs):
                 self.wd[name] = torch.empty(cs.cin, cs.k, cs.k, cs.cout, dtype=torch.bfloat16,
                                             device=device)
+        # the classifier's input gradient: [cin][1][1][fc_pad] (transposed)
+        self.wd["fc"] = torch.empty(cin, 1, 1, g.fc_pad, dtype=torch.bfloat16, device=device)
+        # stride-2 3x3 input gradients: four sub-pixel parity classes (a, b),
+        # each [cin][1+a][1+b][cout]
+        self.wd_s2 = {}
+        for name, cs in g.convs.items():
+            if dgrad_s2(cs):
+                self.wd_s2[name] = [torch.empty(cs.cin, 1 + (c >> 1), 1 + (c & 1), cs.cout,
+                                                dtype=torch.bfloat16, device=device)
+                                    for c in range(4)]
         # every derived weight tensor as one table for the weight-view kernel
         views = []
         for name, packed in self.stem_packed.items():
@@ -133,9 +145,18 @@ class Params:
             views.append(K.WeightView(K.VIEW_STEM, cs.cout, cs.k, cs.k, cs.cin, 0,
                                       self.wbf[name].data_ptr(), packed.data_ptr()))
         for name, wd in self.wd.items():
+            if name == "fc":
+                views.append(K.WeightView(K.VIEW_DGRAD, g.fc_pad, 1, 1, cin, 0,
+                                          self.wbf["fc"].data_ptr(), wd.data_ptr()))
+                continue
             cs = g.convs[name]
             views.append(K.WeightView(K.VIEW_DGRAD, cs.cout, cs.k, cs.k, cs.cin, 0,
                                       self.wbf[name].data_ptr(), wd.data_ptr()))
+        for name, wds in self.wd_s2.items():
+            cs = g.convs[name]
+            for c, wd in enumerate(wds):
+                views.append(K.WeightView(K.VIEW_DGRAD_S2, cs.cout, cs.k, cs.k, cs.cin, c,
+                                          self.wbf[name].data_ptr(), wd.data_ptr()))
         self.n_views = len(views)
         arr = (K.WeightView * max(1, len(views)))(*views)
         self.views_dev = torch.frombuffer(bytearray(arr), dtype=torch.uint8).to(device)
@@ -164,6 +185,7 @@ class Params:
                 K.pack_stem_weights(self.wbf[name], packed)
             for name, wd in self.wd.items():
                 wd.copy_(self.wbf[name].flip(1, 2).permute(3, 1, 2, 0))
+            K.weight_views(self.views_dev.data_ptr(), self.n_views, st)
             return
         K.sgd_step(self.master.data_ptr(), self.mom.data_ptr(), self.grad.data_ptr(),
                    self.conv_bf16.data_ptr(), self.numel, self.n_conv, lr, momentum,
@@ -174,8 +196,9 @@ class Params:
 def workspace_plan(g: G.Graph) -> dict:
     """Bytes of every batch-proportional buffer DeltaRuntime allocates outside
     the activation budget (the max-batch search plans with the same numbers).
-    'transient' = the largest cuDNN output alive inside one backward node
-    (the 3x3 input gradients)."""
+    'transient' = the largest stride-2 3x3 input gradient (written by its four
+    sub-pixel convs, read by the BN backward of the same node); 'head' = the
+    classifier's loss, fp32 / bf16 logit gradients and per-row losses."""
     nodes = g.nodes
     M = lambda n: int(np.prod(n.shape[:-1]))
     batch = nodes[0].shape[0]
@@ -200,28 +223,34 @@ def workspace_plan(g: G.Graph) -> dict:
             Nb, H, W, Cin = nodes[n.parents[0]].shape
             wg = max(wg, K.Wgrad(Nb, H, W, Cin, cs.cout, cs.k, cs.k, cs.stride,
                                  cs.pad).workspace_bytes)
+    wg = max(wg, K.Wgrad(batch, 1, 1, g.fc[0], g.fc_pad, 1, 1, 1, 0).workspace_bytes)
     ws["wgrad_ws"] = wg
-    ws["head"] = 4 + batch * g.fc[1] * 4 + batch * 4
+    ws["head"] = 4 + batch * g.fc[1] * 4 + batch * g.fc_pad * 2 + batch * 4
     ws["input_slots"] = 2 * (nodes[0].nbytes + batch * 8)
-    trans = [0]
+    trans = [256]
     for n in nodes:
-        if n.op == "conv_bn_relu_bwd" and not own_dgrad(g.convs[n.attrs["conv"]]):
-            trans.append(nodes[n.parents[1]].nbytes)          # cuDNN dgrad output
+        if n.op == "conv_bn_relu_bwd" and dgrad_s2(g.convs[n.attrs["conv"]]):
+            trans.append(nodes[n.parents[1]].nbytes)          # stride-2 input gradient
     ws["transient"] = max(trans)
     return ws
 
 
 def own_dgrad(cs: G.ConvSpec) -> bool:
-    """Input gradients through our tcgen05 conv kernel (transposed / flipped
-    weights; fused backward epilogues: residual add + ReLU mask, BN-backward
-    reductions; a stride-2 1x1's gradient is computed on its sampling grid and
-    scattered by the consumer's epilogue): every 1x1 and every stride-1 3x3
-    (with TMA-loaded epilogue operands this is on par with cuDNN dgrad plus a
-    streaming BN backward: 11.60k vs 11.58k img/s A/B; DELTA_OWN_DGRAD_3X3=0
-    routes the 3x3s to cuDNN).  The three stride-2 3x3 input gradients stay
-    with cuDNN (a transposed-conv dgrad is not implemented); the stem has no
-    input gradient."""
-    return cs.k == 1 or (cs.stride == 1 and OWN_DGRAD_3X3)
+    """Input gradients as ONE conv through our tcgen05 kernel (transposed /
+    flipped weights; fused backward epilogues: residual add + ReLU mask,
+    BN-backward reductions; a stride-2 1x1's gradient is computed on its
+    sampling grid and scattered by the consumer's epilogue): every 1x1 and
+    every stride-1 3x3.  The stem has no input gradient."""
+    return cs.k == 1 or cs.stride == 1
+
+
+def dgrad_s2(cs: G.ConvSpec) -> bool:
+    """The stride-2 3x3 input gradients (conv2 of the first block of layers
+    2-4): four sub-pixel stride-1 convs over dY, one per output parity class
+    (a, b) — taps {1} or {2, 0} of the flipped weights per dimension, pad 0
+    before / 1 after — each writing its class of the gradient directly
+    (conv_fwd.cu EV_SCATTER); no zero-inserted upsampling, no wasted MMAs."""
+    return cs.k == 3 and cs.stride == 2
 
 
 @dataclass
@@ -265,9 +294,13 @@ class DeltaRuntime:
         self.short_ws = u8("short_ws")
         self.mp_ws = u8("mp_ws")
         self.wg_ws = u8("wgrad_ws")  # weight-gradient partials (side stream: serial use)
+        # a stride-2 3x3 input gradient between its sub-pixel convs and its BN backward
+        self.dg_ws = u8("transient")
         ncls = self.g.fc[1]
         self.loss = torch.zeros(1, dtype=torch.float32, device=self.device)
         self.dlogits = torch.empty(batch, ncls, dtype=torch.float32, device=self.device)
+        self.dlogits_bf16 = torch.empty(batch, self.g.fc_pad, dtype=torch.bfloat16,
+                                        device=self.device)
         self.row_loss = torch.empty(batch, dtype=torch.float32, device=self.device)
         self.x_slots = [torch.zeros(self.g.nodes[0].shape, dtype=torch.bfloat16,
                                     device=self.device) for _ in range(2)]
@@ -281,8 +314,6 @@ class DeltaRuntime:
         self.arena = None
         self.executor = None
         self._bound_slot = None
-        self._keep = []
-        self._cur_parents = ()
         self.graph = None
         self.cost_table = None
         self.link_gbs = None
@@ -294,6 +325,7 @@ class DeltaRuntime:
         # of MMA: fused only where the main loop hides them (K-dim >= 384)
         self._fuse_stats = {}
         self._dconvs = {}
+        self._dconvs_s2 = {}
         self._wgrads = {}
         bn_bwd_convs = {n.attrs["conv"] for n in self.nodes if n.op == "conv_bn_relu_bwd"}
         sums_convs = {n.attrs["conv"] for n in self.nodes
@@ -327,6 +359,24 @@ class DeltaRuntime:
                     if cs.name in sums_convs:
                         dconv.set_tile_n(64)  # three epilogue operands: 64-column tiles
                     self._dconvs[cs.name] = dconv
+                if dgrad_s2(cs):
+                    # four sub-pixel convs over dY [Nb][P][Q][cout], class (a, b):
+                    # (1+a) x (1+b) taps, pad 0 before, a / b after
+                    _, P_, Q_, _ = n.shape
+                    assert (2 * P_, 2 * Q_) == (H, W), (n.name, H, W, P_, Q_)
+                    self._dconvs_s2[cs.name] = [
+                        K.Conv(Nb, P_, Q_, cs.cout, cs.cin, 1 + (c >> 1), 1 + (c & 1), 1, 0,
+                               _ptr(self.params.wd_s2[cs.name][c]), pad_end=(c >> 1, c & 1))
+                        for c in range(4)]
+            elif n.op == "fc":
+                # the classifier as a 1x1 conv over the pooled features (tcgen05):
+                # logits [N][fc_pad] bf16; its input gradient likewise over the
+                # bf16 logit gradients, and its weight gradient on the wgrad kernel
+                Nb, cin = self.nodes[n.parents[0]].shape
+                pad = self.g.fc_pad
+                self._fc = K.Conv(Nb, 1, 1, cin, pad, 1, 1, 1, 0, _ptr(self.params.wbf["fc"]))
+                self._fc_d = K.Conv(Nb, 1, 1, pad, cin, 1, 1, 1, 0, _ptr(self.params.wd["fc"]))
+                self._fc_w = K.Wgrad(Nb, 1, 1, cin, pad, 1, 1, 1, 0)
 
     def trace(self) -> P.Trace:
         return G.to_trace(self.g)
@@ -348,7 +398,11 @@ class DeltaRuntime:
         """Plan with libdelta and lower onto the arena.  budget_fraction=None
         plans the no-eviction baseline (Baseline policy, budget = sum).
         duplex: reloads on a second copy engine (default: one copy stream in
-        plan order, the reference's model)."""
+        plan order, the reference's model).  The arena always fits the
+        budget: when the offline packing of a plan's lifetimes fragments past
+        it, the plan is redone under a budget smaller by the excess
+        (self.config = the config actually planned; self.budget_bytes = the
+        caller's budget)."""
         t = self.trace()
         if budget_fraction is None and budget is None:
             total = sum(n.nbytes for n in self.nodes)
@@ -357,11 +411,23 @@ class DeltaRuntime:
             if budget is None:
                 budget = int(self.baseline_peak() * budget_fraction)
             cfg = self.engine_config(budget, policy, **kw)
-        prog = P.Program(t, cfg, align=G.ALIGN, duplex=duplex)
-        if prog.infeasible:
-            node, deficit = prog.infeasible
-            raise RuntimeError(f"plan infeasible at node {self.nodes[node].name} "
-                               f"(deficit {deficit} B, budget {cfg.budget} B)")
+        target = cfg.budget
+        for _ in range(8):
+            prog = P.Program(t, cfg, align=G.ALIGN, duplex=duplex)
+            if prog.infeasible:
+                node, deficit = prog.infeasible
+                raise RuntimeError(f"plan infeasible at node {self.nodes[node].name} "
+                                   f"(deficit {deficit} B, budget {cfg.budget} B)")
+            if prog.arena_bytes <= target or cfg.policy_mode == P.PolicyMode.Baseline:
+                break
+            # the offline packing of this plan's lifetimes fragments past the
+            # budget (the reference's pool is a byte counter): plan again under
+            # a budget smaller by the excess, so the ARENA fits the caller's
+            # budget; the plan is then the reference's plan at that budget
+            cfg = dataclasses.replace(cfg, budget=cfg.budget - (prog.arena_bytes - target))
+        if prog.arena_bytes > target and cfg.policy_mode != P.PolicyMode.Baseline:
+            raise RuntimeError(f"arena {prog.arena_bytes} B exceeds the budget {target} B")
+        self.budget_bytes = target  # the caller's budget: the arena fits it
         self.program = prog
         self.config = cfg
         self.graph = None
@@ -386,11 +452,11 @@ class DeltaRuntime:
 
     # ------------------------------------------------------------ ops
     # ------------------------------------------------------------ recipes
-    def _recipe(self, node: G.Node, host) -> tuple:
+    def _recipe(self, node: G.Node) -> tuple:
         """The kernel ops that (re)produce `node` on the executor: symbolic
-        arena operands (OUT, IN(i)), parameter / workspace pointers, HOST ops
-        (registered through `host`) for the library calls.  Returns (ops,
-        (launches of our kernels on first production, on recompute))."""
+        arena operands (OUT, IN(i)) and parameter / workspace pointers, every
+        one a kernel of this library.  Returns (ops, (launches of our kernels
+        on first production, on recompute))."""
         pr = self.params
         op = node.op
         ops = []
@@ -466,27 +532,22 @@ class DeltaRuntime:
             Nb, H, W, Cs = self.nodes[node.parents[0]].shape
             add(X.kop(X.K_AVGPOOL, (X.IN(0), X.OUT()), (Nb, H * W, Cs)))
         elif op == "fc":
-            src = self.nodes[node.parents[0]]
-
-            def fc(out, ins, rec, stream, node=node, src=src):
-                a_ = self._view(ins[0] - self._base, src)
-                with _tf32():
-                    torch.addmm(pr.views["fc_b"], a_.float(), pr.views["fc_w"].t(),
-                                out=self._view(out - self._base, node))
-            add(X.kop(X.K_HOST, (), (host(fc),)), 0, 0)
+            # logits = pooled @ W^T on the tensor cores (bias: in the head kernel)
+            add(X.kop(X.K_CONV, (X.IN(0), X.OUT(), None), conv=self._fc._h))
         elif op == "fc_bwd":
-            logits_n, src = self.nodes[node.parents[0]], self.nodes[node.parents[1]]
-            Nb, ncls = logits_n.shape
-            add(X.kop(X.K_SOFTMAX_XENT, (X.IN(0), _ptr(self.y_dev), _ptr(self.loss),
-                                         _ptr(self.dlogits), _ptr(self.row_loss)), (Nb, ncls)), 2, 2)
-
-            def fc_bwd(out, ins, rec, stream, node=node, src=src):
-                a_ = self._view(ins[1] - self._base, src)
-                with _tf32():
-                    torch.mm(self.dlogits.t(), a_.float(), out=pr.gviews["fc_w"])
-                    torch.sum(self.dlogits, 0, out=pr.gviews["fc_b"])
-                    self._view(out - self._base, node).copy_(self.dlogits @ pr.views["fc_w"])
-            add(X.kop(X.K_HOST, (), (host(fc_bwd),)), 0, 0)
+            # softmax cross-entropy on logits + bias -> loss, dlogits (fp32 and
+            # padded bf16), dbias; then dPooled = dlogits @ W and dW = dlogits^T
+            # @ pooled on the tensor cores
+            Nb = node.shape[0]
+            ncls = self.g.fc[1]
+            add(X.kop(X.K_XENT_HEAD, (X.IN(0), _ptr(pr.views["fc_b"]), _ptr(self.y_dev),
+                                      _ptr(self.loss), _ptr(self.dlogits),
+                                      _ptr(self.dlogits_bf16), _ptr(pr.gviews["fc_b"]),
+                                      _ptr(self.row_loss)), (Nb, ncls, self.g.fc_pad)), 3, 3)
+            add(X.kop(X.K_CONV, (_ptr(self.dlogits_bf16), X.OUT(), None), conv=self._fc_d._h))
+            add(X.kop(X.K_WGRAD, (_ptr(self.dlogits_bf16), X.IN(1),
+                                  _ptr(pr.gviews["fc_w_full"]), _ptr(self.wg_ws)),
+                      conv=self._fc_w._h), 2, 2)
         elif op == "bn_add_relu_bwd":
             # parents: [upstream, (O if masked,) X]; upstream already masked
             # unless it is the pooled head gradient
@@ -513,12 +574,16 @@ class DeltaRuntime:
                           (K.EPI_BN_BWD, 0, 0), conv=self._dconvs[conv]._h))
                 add(X.kop(X.K_BN_BWD_PARTS, (_ptr(self.stats_main), X.OUT(), X.IN(2), X.OUT())
                           + bnp(bn) + (gb(bn)[0],) + dgb(bn), (0, M, C)), 2, 0)
-            else:
-                # cuDNN input gradient (3x3) -> SCRATCH(0)
-                dg = host(self._dgrad_op(conv, node.parents[0], node.parents[1]))
-                add(X.kop(X.K_HOST, (), (dg,)), 0, 0)
-                add(X.kop(X.K_BN_BWD, (X.SCRATCH(0), X.IN(1), X.IN(2), X.OUT()) + bnp(bn)
+            elif conv in self._dconvs_s2:
+                # stride-2 3x3: the four sub-pixel parity classes write the
+                # input gradient into the scratch, then the streaming BN backward
+                for cls, dc in enumerate(self._dconvs_s2[conv]):
+                    add(X.kop(X.K_CONV_EX, (X.IN(0), _ptr(self.dg_ws), None),
+                              (K.EPI_SCATTER2, 0, 0, cls), conv=dc._h))
+                add(X.kop(X.K_BN_BWD, (_ptr(self.dg_ws), X.IN(1), X.IN(2), X.OUT()) + bnp(bn)
                           + (gb(bn)[0],) + dgb(bn) + (_ptr(self.bn_ws),), (0, M, C)), bwd_n, bwd_n)
+            else:
+                raise RuntimeError(f"{node.name}: no input-gradient kernel for conv {conv}")
             add(wgrad(conv, 0, 1), 2, 2)
         elif op == "conv_shortcut_bwd":
             # out = (dgrad(conv1, dC1) + shortcut gradient) * [X > 0]; the sum
@@ -526,7 +591,6 @@ class DeltaRuntime:
             conv = node.attrs["conv"]
             out_mask = X.IN(1) if node.attrs.get("mask_out") else None
             add_, pool_hw, add_mask, stride2 = None, 0, None, 0
-            n_host = 0
             if "conv_short" in node.attrs:
                 short = node.attrs["conv_short"]
                 if short in self._dconvs:
@@ -536,11 +600,8 @@ class DeltaRuntime:
                         dst, stride2 = _ptr(self.short_ws), 1  # at its sampling grid
                     add(X.kop(X.K_CONV, (X.IN(2), dst, None), conv=self._dconvs[short]._h))
                     add_ = dst
-                else:  # cuDNN input gradient
-                    add(X.kop(X.K_HOST, (), (host(self._dgrad_op(short, node.parents[2],
-                                                                  node.parents[1])),)), 0, 0)
-                    add_ = X.SCRATCH(n_host)
-                    n_host += 1
+                else:
+                    raise RuntimeError(f"{node.name}: shortcut conv {short} must be a 1x1")
                 add(wgrad(short, 2, 1), 2, 2)
             elif node.attrs.get("from_pool"):
                 add_, pool_hw, add_mask = X.IN(2), int(node.shape[1] * node.shape[2]), X.IN(3)
@@ -579,52 +640,16 @@ class DeltaRuntime:
     def _arena_view(self, ptr: int, node_id: int) -> torch.Tensor:
         return self._view(ptr - self._base, self.nodes[node_id])
 
-    def _dgrad_op(self, conv: str, dy_node: int, x_node: int):
-        """HOST op: cuDNN input gradient (3x3 convs); returns its device
-        pointer (the recipe's SCRATCH operand).  Input slots are located by
-        node id among the consumer's parents (set by _bind's host-op wrapper)."""
-        def op(out, ins, rec, stream):
-            node = self._cur_parents
-            dY = self._arena_view(ins[node.index(dy_node)], dy_node)
-            Xv = self._arena_view(ins[node.index(x_node)], x_node)
-            gi = self._conv_bwd(conv, dY, Xv, need_dx=True)
-            # the caching allocator is stream-ordered: once dropped, this block
-            # is only reused by allocations enqueued after the recipe's consumer
-            # of it; holding the latest one just keeps the pointer valid until
-            # the executor has enqueued that consumer
-            self._keep = [gi]
-            return _ptr(gi)
-        return op
-
     def _bind(self):
         """(Re)build the recipe table for the current input slot and bind it,
         with the current program, to the executor."""
-        recipes, host_ops, launches = {}, [], {}
+        recipes, launches = {}, {}
         for node in self.nodes:
-            def host(fn, parents=tuple(node.parents)):
-                def call(out, ins, rec, stream, fn=fn, parents=parents):
-                    self._cur_parents = parents
-                    return fn(out, ins, rec, stream)
-                host_ops.append(call)
-                return len(host_ops) - 1
-            ops, nl = self._recipe(node, host)
+            ops, nl = self._recipe(node)
             recipes[node.id] = ops
             launches[node.id] = nl
-        self.executor.bind(self.program, recipes, host_ops, launches)
+        self.executor.bind(self.program, recipes, [], launches)
         self._bound_slot = self._slot
-
-    def _conv_bwd(self, name: str, dY: torch.Tensor, X: torch.Tensor, need_dx: bool = True):
-        """cuDNN input gradient (channels_last views of arena memory) — the 3x3
-        convs whose dgrad our kernel does not cover yet."""
-        cs = self.g.convs[name]
-        w = self.params.wbf[name].permute(0, 3, 1, 2)
-        gi, _, _ = torch.ops.aten.convolution_backward(
-            dY.permute(0, 3, 1, 2), X.permute(0, 3, 1, 2), w, None, [cs.stride] * 2,
-            [cs.pad] * 2, [1, 1], False, [0, 0], 1, [True, False, False])
-        gi = gi.permute(0, 2, 3, 1)
-        if not gi.is_contiguous():
-            gi = gi.contiguous()
-        return gi
 
     # -------------------------------------------------------- program
     def run_program(self, timing: dict | None = None, probe: dict | None = None,
@@ -640,7 +665,6 @@ class DeltaRuntime:
         st = self.stream.cuda_stream
         if self._bound_slot != self._slot:
             self._bind()
-        self._keep = []
         after = None
         if probe is not None:
             def after(ai, node, out):

@@ -9,7 +9,10 @@ KEYS = [("gpu__time_duration.sum", "us", 1e-3),
         ("dram__bytes_read.sum", "MB_rd", 1e-6),
         ("dram__bytes_write.sum", "MB_wr", 1e-6),
         ("FBSP.TriageCompute.dram__throughput.avg.pct_of_peak_sustained_elapsed", "dram%", 1),
-        ("TPC.TriageCompute.sm__pipe_tensor_cycles_active_realtime.avg.pct_of_peak_sustained_elapsed", "tensor%", 1),
+        # tcgen05 (UTCHMMA) bf16 tensor-op throughput: the counter that sees
+        # the 5th-gen tensor cores (sm__pipe_tensor_cycles_active does not)
+        ("sm__ops_path_tensor_op_utchmma_src_bf16_dst_fp32_sparsity_off.avg.pct_of_peak_sustained_elapsed", "tc05%", 1),
+        ("sm__ops_path_tensor_op_utchmma_src_bf16_dst_fp32_sparsity_off.sum", "GFLOP_tc05", 1e-9),
         ("sm__throughput.avg.pct_of_peak_sustained_elapsed", "sm%", 1),
         ("launch__grid_size", "grid", 1),
         ("launch__registers_per_thread", "regs", 1)]

@@ -18,7 +18,9 @@ all_ms = sum(tot.values())
 if len(sys.argv) > 2:
     print(sys.argv[2])
 print(f"launches {sum(cnt.values())}  total {all_ms:.2f} ms")
-ours = sum(v for k, v in tot.items() if "delta_k" in k)
-print(f"our kernels (delta_k::*): {ours:.2f} ms = {100 * ours / all_ms:.1f}%")
+OURS = re.compile(r"(delta_k::|unnamed>::|anonymous namespace\)::)k_")
+ours = sum(v for k, v in tot.items() if OURS.search(k))
+print(f"our kernels (delta_k::k_*): {ours:.2f} ms = {100 * ours / all_ms:.1f}%  "
+      f"(other: {', '.join(k for k in tot if not OURS.search(k)) or 'none'})")
 for k, v in sorted(tot.items(), key=lambda kv: -kv[1]):
     print(f"  {v:7.3f} ms {100 * v / all_ms:5.1f}%  n={cnt[k]:4d}  {k}")

@@ -494,3 +494,93 @@ def test_sgd_step_and_weight_views_match_torch():
     assert torch.equal(d3, conv.flip(1, 2).permute(3, 1, 2, 0))
     assert torch.equal(d1, one.flip(1, 2).permute(3, 1, 2, 0))
     assert torch.equal(sp, K.pack_stem_weights(stem))
+
+
+# ---- stride-2 3x3 input gradient: four sub-pixel parity classes (EV_SCATTER)
+S2_CASES = [  # (N, P, Q, Kout, Cin): dY [N][P][Q][Kout] -> dX [N][2P][2Q][Cin]
+    (4, 28, 28, 128, 128),
+    (3, 14, 14, 256, 256),
+    (5, 7, 7, 512, 512),
+]
+
+
+@pytest.mark.parametrize("case", S2_CASES)
+def test_dgrad_stride2_subpixel_matches_torch(case):
+    N, P_, Q_, Kout, Cin = case
+    g = torch.Generator(device="cuda").manual_seed(11)
+    w = (torch.randn(Kout, 3, 3, Cin, device="cuda", generator=g) / (9 * Kout) ** 0.5).to(torch.bfloat16)
+    dy = torch.randn(N, P_, Q_, Kout, device="cuda", generator=g).to(torch.bfloat16)
+    # the weight views through the library's own view kernel (DELTA_VIEW_DGRAD_S2)
+    wds = [torch.empty(Cin, 1 + (c >> 1), 1 + (c & 1), Kout, dtype=torch.bfloat16, device="cuda")
+           for c in range(4)]
+    views = (K.WeightView * 4)(*[K.WeightView(K.VIEW_DGRAD_S2, Kout, 3, 3, Cin, c, w.data_ptr(),
+                                              wds[c].data_ptr()) for c in range(4)])
+    vdev = torch.frombuffer(bytearray(views), dtype=torch.uint8).cuda()
+    K.weight_views(vdev.data_ptr(), 4, _stream())
+    # class (a, b): tap r' of dimension a reads weight row 1 (a = 0) or 2 - 2r'
+    for c in range(4):
+        a, b = c >> 1, c & 1
+        rows = [1] if a == 0 else [2, 0]
+        cols = [1] if b == 0 else [2, 0]
+        ref_w = w[:, rows][:, :, cols].permute(3, 1, 2, 0)
+        torch.cuda.synchronize()
+        assert torch.equal(wds[c], ref_w), c
+    dx = torch.full((N, 2 * P_, 2 * Q_, Cin), float("nan"), device="cuda", dtype=torch.bfloat16)
+    convs = [K.Conv(N, P_, Q_, Kout, Cin, 1 + (c >> 1), 1 + (c & 1), 1, 0, wds[c].data_ptr(),
+                    pad_end=(c >> 1, c & 1)) for c in range(4)]
+    for c, cv in enumerate(convs):
+        assert (cv.P, cv.Q) == (P_, Q_)
+        cv.scatter2(dy.data_ptr(), dx.data_ptr(), c, _stream())
+    torch.cuda.synchronize()
+    assert not bool(torch.isnan(dx.float()).any())  # the four classes tile dX exactly
+    ref = torch.nn.grad.conv2d_input((N, Cin, 2 * P_, 2 * Q_), w.permute(0, 3, 1, 2).float(),
+                                     dy.permute(0, 3, 1, 2).float(), stride=2, padding=1)
+    _close(dx, ref.permute(0, 2, 3, 1), "stride-2 dgrad")
+
+
+def test_classifier_head_on_tensor_cores():
+    """logits GEMM (1x1 conv, bf16, padded classes) + head kernel (bias, softmax
+    cross-entropy, dlogits fp32/bf16, dbias) + input-gradient GEMM + weight
+    gradient, against fp32 autograd."""
+    N, cin, ncls, pad = 64, 2048, 1000, 1024
+    g = torch.Generator(device="cuda").manual_seed(5)
+    a = torch.randn(N, cin, device="cuda", generator=g).to(torch.bfloat16)
+    wf = torch.zeros(pad, cin, device="cuda")
+    wf[:ncls] = torch.randn(ncls, cin, device="cuda", generator=g) / cin ** 0.5
+    wb = wf.to(torch.bfloat16)
+    wt = wb.t().contiguous()
+    bias = torch.randn(ncls, device="cuda", generator=g) * 0.1
+    lab = torch.randint(0, ncls, (N,), device="cuda", generator=g)
+    fc = K.Conv(N, 1, 1, cin, pad, 1, 1, 1, 0, wb.data_ptr())
+    fcd = K.Conv(N, 1, 1, pad, cin, 1, 1, 1, 0, wt.data_ptr())
+    wg = K.Wgrad(N, 1, 1, cin, pad, 1, 1, 1, 0)
+    logits = torch.empty(N, pad, device="cuda", dtype=torch.bfloat16)
+    fc(a.data_ptr(), logits.data_ptr(), _stream())
+    loss = torch.zeros(1, device="cuda")
+    dl = torch.empty(N, ncls, device="cuda")
+    dlb = torch.empty(N, pad, device="cuda", dtype=torch.bfloat16)
+    db = torch.empty(ncls, device="cuda")
+    rows = torch.empty(N, device="cuda")
+    K.softmax_xent_head(logits.data_ptr(), pad, bias.data_ptr(), lab.data_ptr(), loss.data_ptr(),
+                        dl.data_ptr(), dlb.data_ptr(), db.data_ptr(), rows.data_ptr(), N, ncls,
+                        _stream())
+    da = torch.empty(N, cin, device="cuda", dtype=torch.bfloat16)
+    fcd(dlb.data_ptr(), da.data_ptr(), _stream())
+    dw = torch.empty(pad, cin, device="cuda")
+    ws = torch.empty(wg.workspace_bytes, dtype=torch.uint8, device="cuda")
+    wg(dlb.data_ptr(), a.data_ptr(), dw.data_ptr(), ws.data_ptr(), _stream())
+    torch.cuda.synchronize()
+    af = a.float().requires_grad_(True)
+    W = wb[:ncls].float().requires_grad_(True)
+    bt = bias.clone().requires_grad_(True)
+    z = af @ W.t()
+    _close(logits[:, :ncls], z.detach(), "logits")
+    assert bool((logits[:, ncls:] == 0).all())
+    L = F.cross_entropy(z + bt, lab)
+    L.backward()
+    assert abs(loss.item() - L.item()) <= 1e-2 * abs(L.item())
+    assert bool((dlb[:, ncls:] == 0).all())
+    _close(da, af.grad, "dA")
+    _close(dw[:ncls], W.grad, "dW")
+    assert bool((dw[ncls:] == 0).all())
+    _close(db, bt.grad, "dbias")

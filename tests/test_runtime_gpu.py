@@ -184,12 +184,18 @@ def test_every_op_matches_fp32_autograd_on_its_inputs(rts_any):
         elif n.op == "avgpool":
             expect(n.name, T(n.id), ins[0].mean((2, 3)))
         elif n.op == "fc":
-            expect(n.name, T(n.id), ins[0] @ Pw["fc_w"].t() + Pw["fc_b"])
+            ncls = g.fc[1]
+            out = T(n.id)
+            expect(n.name, out[:, :ncls], ins[0] @ Pw["fc_w"].t())   # bias: in the head kernel
+            assert bool((out[:, ncls:] == 0).all())                  # zero-padded classes
         elif n.op == "fc_bwd":
-            L = ins[0].clone().requires_grad_(True)
+            ncls = g.fc[1]
+            L = (ins[0][:, :ncls] + Pw["fc_b"]).requires_grad_(True)
             F.cross_entropy(L, y.cuda()).backward()
             expect(n.name, T(n.id), L.grad @ Pw["fc_w"])
             expect("grad fc_w", pr.gviews["fc_w"], L.grad.t() @ ins[1])
+            expect("grad fc_b", pr.gviews["fc_b"], L.grad.sum(0))
+            assert bool((pr.gviews["fc_w_full"][ncls:] == 0).all())
         elif n.op in ("bn_add_relu_bwd", "bn_relu_bwd"):
             up, xin = ins[0], ins[-1]
             if n.attrs.get("from_pool"):
