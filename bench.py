@@ -310,6 +310,8 @@ def main():
         barrier()
         return max_over_ranks(e0.elapsed_time(e1) / n_steps)
 
+    graph_state = {"captured": not args.no_graph}
+
     def prepare(budget_fraction):
         prog = rt.plan(budget_fraction)
         rt.step_device()  # eager warm step (cuDNN autotune, allocator)
@@ -320,6 +322,9 @@ def main():
             except Exception as e:  # noqa: BLE001 - e.g. a collective not capturable here
                 if dp is None:
                     raise
+                # reported in the JSON line (config.graph), never silent
+                graph_state["captured"] = False
+                graph_state["error"] = str(e)[:200]
                 print(json.dumps({"warning": f"CUDA graph capture with NCCL failed ({e}); "
                                              "running eager steps"}), file=sys.stderr)
                 rt.graph = rt.graphs = None
@@ -504,7 +509,7 @@ def main():
                                    f"DELTA at {int(args.budget * 100)}% activation budget",
                        "global_batch": B * world, "image": 224, "budget_fraction": args.budget,
                        "budget_bytes": rt.config.budget, "anchors": args.anchors,
-                       "parallelism": f"dp{world}", "graph": not args.no_graph,
+                       "parallelism": f"dp{world}", "graph": graph_state,
                        "l2": "working set >> 126 MB L2 (no flush needed)"},
             "no_eviction": {"images_per_s": round(world * B / (base_ms * 1e-3), 1),
                             "ms_per_step": round(base_ms, 3),
@@ -592,7 +597,7 @@ def main():
                                         "vs_baseline", "dtype", "data")}
         line.update({
             "config": {k: detail["config"][k] for k in ("workload", "global_batch", "budget_bytes",
-                                                          "parallelism", "l2")},
+                                                          "parallelism", "graph", "l2")},
             "parity": parity,
             "no_eviction_ratio": detail["no_eviction"]["ratio"],
             "no_eviction_images_per_s": detail["no_eviction"]["images_per_s"],

@@ -139,6 +139,13 @@ delta_status delta_rt_bind(delta_rt* rt, const delta_program* prog, const delta_
                            uint64_t n_kops, const delta_recipe* recipes, uint64_t n_recipes);
 delta_status delta_rt_set_callbacks(delta_rt* rt, delta_host_fn host, delta_action_fn after,
                                     void* ctx);
+/* Ready events for overlapping work with the step (data-parallel gradient
+ * buckets): event i is recorded on the compute stream right after the
+ * compute action of nodes[i] in every step; delta_rt_wait_ready makes
+ * `stream` (e.g. a communication stream) wait for it.  Replaces any earlier
+ * set. */
+delta_status delta_rt_set_ready_nodes(delta_rt* rt, const uint64_t* nodes, uint32_t n);
+delta_status delta_rt_wait_ready(delta_rt* rt, void* stream, uint32_t i);
 /* Issue one step on `stream` (the compute stream); copy streams are joined
  * back into it at the end. */
 delta_status delta_rt_step(delta_rt* rt, void* stream);

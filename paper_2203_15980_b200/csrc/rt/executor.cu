@@ -45,6 +45,10 @@ struct delta_rt {
   delta_host_fn host_fn = nullptr;
   delta_action_fn after_fn = nullptr;
   void* ctx = nullptr;
+  // ready events: recorded on the compute stream right after the compute
+  // action of a node (e.g. the last weight gradient of a gradient bucket)
+  std::unordered_map<uint64_t, uint32_t> ready_of;
+  std::vector<cudaEvent_t> ready;
 };
 
 namespace {
@@ -317,6 +321,10 @@ delta_status issue(delta_rt* rt, cudaStream_t cs, cudaEvent_t* t0, cudaEvent_t* 
       k_stamp<<<1, 1, 0, st>>>(stamps->log, stamps->count, stamps->cap, 2ull * ai + 1, what);
       RT_CUDA(cudaGetLastError());
     }
+    if (a.op == DELTA_ACT_COMPUTE && !rt->ready_of.empty()) {
+      auto r = rt->ready_of.find(a.node);
+      if (r != rt->ready_of.end()) RT_CUDA(cudaEventRecord(rt->ready[r->second], st));
+    }
     if (rt->after_fn && (a.op == DELTA_ACT_COMPUTE || a.op == DELTA_ACT_RECOMPUTE))
       rt->after_fn(rt->ctx, ai, a.node, reinterpret_cast<uint64_t>(arena + a.offset), st);
   }
@@ -409,6 +417,24 @@ delta_status delta_rt_set_callbacks(delta_rt* rt, delta_host_fn host, delta_acti
   rt->host_fn = host;
   rt->after_fn = after;
   rt->ctx = ctx;
+  return DELTA_OK;
+}
+
+delta_status delta_rt_set_ready_nodes(delta_rt* rt, const uint64_t* nodes, uint32_t n) {
+  for (auto ev : rt->ready) cudaEventDestroy(ev);
+  rt->ready.assign(n, nullptr);
+  rt->ready_of.clear();
+  for (uint32_t i = 0; i < n; ++i) {
+    RT_CUDA(cudaEventCreateWithFlags(&rt->ready[i], cudaEventDisableTiming));
+    if (!rt->ready_of.emplace(nodes[i], i).second)
+      return fail(DELTA_E_ARGUMENT, "delta_rt_set_ready_nodes: node listed twice");
+  }
+  return DELTA_OK;
+}
+
+delta_status delta_rt_wait_ready(delta_rt* rt, void* stream, uint32_t i) {
+  if (i >= rt->ready.size()) return fail(DELTA_E_ARGUMENT, "delta_rt_wait_ready: no such event");
+  RT_CUDA(cudaStreamWaitEvent(static_cast<cudaStream_t>(stream), rt->ready[i], 0));
   return DELTA_OK;
 }
 
@@ -524,6 +550,8 @@ delta_status delta_rt_measure_costs(delta_rt* rt, void* stream, uint32_t iters, 
 
 void delta_rt_destroy(delta_rt* rt) {
   if (!rt) return;
+  for (auto ev : rt->ready)
+    if (ev) cudaEventDestroy(ev);
   for (auto ev : rt->events)
     if (ev) cudaEventDestroy(ev);
   for (int s = 1; s < 3; ++s)

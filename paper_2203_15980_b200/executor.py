@@ -57,6 +57,8 @@ _SIGS = {
     "delta_rt_step_timed": (i32, [vp, vp, C.POINTER(f32), C.POINTER(f32), u64]),
     "delta_rt_measure_costs": (i32, [vp, vp, u32, C.POINTER(u64), u64]),
     "delta_rt_step_observed": (i32, [vp, vp, C.POINTER(u64), u64, C.POINTER(u64)]),
+    "delta_rt_set_ready_nodes": (i32, [vp, C.POINTER(u64), u32]),
+    "delta_rt_wait_ready": (i32, [vp, vp, u32]),
     "delta_rt_destroy": (None, [vp]),
 }
 for _n, (_r, _a) in _SIGS.items():
@@ -210,6 +212,14 @@ class Executor:
         out["node"] = rec[:, 3] >> 8
         out["op"] = rec[:, 3] & 0xFF
         return out
+
+    def set_ready_nodes(self, nodes: list):
+        """event i recorded after the compute action of nodes[i] (every step)"""
+        arr = (u64 * max(1, len(nodes)))(*nodes)
+        check(lib.delta_rt_set_ready_nodes(self._h, arr, len(nodes)))
+
+    def wait_ready(self, stream: int, i: int):
+        check(lib.delta_rt_wait_ready(self._h, stream, i))
 
     def measure_costs(self, stream: int, iters: int, n_nodes: int) -> np.ndarray:
         out = np.zeros(n_nodes, np.uint64)

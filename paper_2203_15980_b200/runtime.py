@@ -318,6 +318,8 @@ class DeltaRuntime:
         self.cost_table = None
         self.link_gbs = None
         self.dp = None  # torch.distributed group when running data parallel
+        self.buckets = []
+        self._comm = None
 
     # ------------------------------------------------------------ setup
     def _build_convs(self):
@@ -649,6 +651,13 @@ class DeltaRuntime:
             recipes[node.id] = ops
             launches[node.id] = nl
         self.executor.bind(self.program, recipes, [], launches)
+        if self.dp is not None:
+            # gradient buckets released by ready events of their last writer
+            bk = self.grad_buckets()
+            nodes = sorted({b[2] for b in bk})
+            self.executor.set_ready_nodes(nodes)
+            self.ready_nodes = nodes
+            self.buckets = [(lo, hi, nodes.index(w)) for lo, hi, w in bk]
         self._bound_slot = self._slot
 
     # -------------------------------------------------------- program
@@ -691,10 +700,60 @@ class DeltaRuntime:
             self.executor.step(st, after)
         K._count(self.executor.launches_per_step)
         if self.dp is not None:
-            # data parallel: one DELTA instance per GPU, gradients averaged
-            # with NCCL over NVLink (one flat bucket, on the compute stream)
-            allreduce_mean(self.params.grad, self.dp)
+            self._allreduce_buckets()
         self.params.sgd_step(self.lr)
+
+    def _allreduce_buckets(self):
+        """Data parallel: one DELTA instance per GPU; the flat
+        fp32 gradient buffer is averaged across ranks in ~25 MB buckets on a
+        dedicated communication stream.  Bucket b waits (delta_rt_wait_ready)
+        for the event the executor records right after the backward node that
+        writes its last gradient, so its all-reduce overlaps the rest of the
+        backward pass; the compute stream joins the communication stream
+        before the optimizer step.  Capturable into the step's CUDA graph."""
+        if self._comm is None:
+            self._comm = torch.cuda.Stream(device=self.device)
+        cur = torch.cuda.current_stream()
+        g = self.params.grad
+        for lo, hi, ev in self.buckets:
+            self.executor.wait_ready(self._comm.cuda_stream, ev)
+            with torch.cuda.stream(self._comm):
+                allreduce_mean(g[lo:hi], self.dp)
+        cur.wait_stream(self._comm)
+
+    def grad_buckets(self, bucket_bytes: int = 25 * 2**20):
+        """Partition the flat gradient buffer into contiguous buckets of about
+        `bucket_bytes`, each released by the LAST backward node (in program
+        order) that writes a gradient inside it — read off the recipes: every
+        kernel operand pointing into the gradient buffer marks its node as a
+        writer of the parameter starting there.  Returns [(lo, hi, node)] in
+        float elements, ordered by release."""
+        g0 = self.params.grad.data_ptr()
+        g1 = g0 + self.params.grad.numel() * 4
+        writer = {}
+        for node in self.nodes:
+            ops, _ = self._recipe(node)
+            for k in ops:
+                for r in k.r:
+                    if r.kind == X.REF_PTR and g0 <= r.ptr < g1:
+                        writer[r.ptr] = max(writer.get(r.ptr, -1), node.id)
+        items = []
+        for name, gv in self.params.gviews.items():
+            if name == "fc_w":  # a view of fc_w_full
+                continue
+            p = gv.data_ptr()
+            if p not in writer:
+                raise RuntimeError(f"no backward node writes the gradient of {name}")
+            items.append(((p - g0) // 4, gv.numel(), writer[p]))
+        items.sort()
+        assert items[0][0] == 0 and all(a[0] + a[1] == b[0] for a, b in zip(items, items[1:]))
+        buckets, lo, last = [], 0, -1
+        for off, n, w in items:
+            last = max(last, w)
+            if (off + n - lo) * 4 >= bucket_bytes or off + n == self.params.grad.numel():
+                buckets.append((lo, off + n, last))
+                lo, last = off + n, -1
+        return sorted(buckets, key=lambda b: b[2])
 
 
     def capture(self):
