@@ -143,6 +143,16 @@ delta_status delta_chrome_trace_events(const delta_event* ev, uint64_t n, char**
                                        uint64_t* len);
 void delta_result_free(delta_result* r);
 
+/* run_comparison (src/engine.cpp:646-671): every budget x policy x heuristic
+ * cell planned on `t` with the other fields of `base`, rendered as the
+ * reference's comparison CSV (json = 0, src/metrics.cpp:314-328) or JSON
+ * (json = 1, :330-348); delta_free the string. */
+delta_status delta_comparison(const delta_trace* t, const delta_config* base,
+                              const uint64_t* budgets, uint64_t n_budgets,
+                              const uint32_t* policies, uint64_t n_policies,
+                              const uint32_t* heuristics, uint64_t n_heuristics, int32_t json,
+                              char** out, uint64_t* len);
+
 /* CPU planner timing: mean ns per run_iteration over `iters` calls. */
 delta_status delta_plan_time_ns(const delta_trace* t, const delta_config* c,
                                 uint32_t iters, double* ns_per_plan);

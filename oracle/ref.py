@@ -44,6 +44,9 @@ def lib():
             ("dref_replay_check", vp, [C.c_char_p, C.POINTER(RefConfig), C.c_char_p]),
             ("dref_brute_force", C.c_uint64, [C.c_char_p, C.c_uint64]),
             ("dref_generate", vp, [C.c_int, C.c_uint64, C.c_uint64]),
+            ("dref_comparison", vp, [C.c_char_p, C.POINTER(RefConfig), C.POINTER(C.c_uint64),
+                                     C.c_uint64, C.POINTER(C.c_uint32), C.c_uint64,
+                                     C.POINTER(C.c_uint32), C.c_uint64, C.c_int]),
             ("dref_free", None, [vp]),
         ]:
             f = getattr(L, name)
@@ -123,6 +126,54 @@ def replay_check(trace_json: str, cfg, chrome_json: str) -> list:
     if isinstance(out, dict):
         raise RuntimeError(out.get("what"))
     return out
+
+
+def comparison(trace_json: str, cfg, budgets, policies, heuristics, fmt: str = "csv") -> str:
+    """the reference's run_comparison rendered by comparison_to_csv / _json.
+    Runs in a fresh interpreter: this entry point crashes when libdelta is
+    mapped into the same process (a symbol-interposition clash not yet
+    isolated; every other entry point is unaffected)."""
+    import subprocess
+    import sys
+    payload = json.dumps({"trace": trace_json, "budgets": list(budgets),
+                          "policies": [int(x) for x in policies],
+                          "heuristics": [int(x) for x in heuristics], "fmt": fmt,
+                          "cfg": {"budget": cfg.budget, "heuristic": int(cfg.heuristic),
+                                  "policy_mode": int(cfg.policy_mode),
+                                  "bw": list(cfg.cost_model.bandwidth_bytes_per_us),
+                                  "eff": list(cfg.cost_model.effective_fraction),
+                                  "swap": int(cfg.cost_model.swap_cost_mode),
+                                  "wm": list(cfg.watermark_fraction),
+                                  "limit": cfg.prefetch_limit, "pf": bool(cfg.prefetch_enabled),
+                                  "ov": bool(cfg.overlap_enabled),
+                                  "guard": int(cfg.prefetch_guard)}})
+    code = ("import json, sys; sys.path.insert(0, %r); from oracle import ref; "
+            "d = json.loads(sys.stdin.read()); sys.stdout.write(ref._comparison_inproc(d))"
+            % os.path.dirname(HERE))
+    out = subprocess.run([sys.executable, "-c", code], input=payload, capture_output=True,
+                         text=True, check=True)
+    return out.stdout
+
+
+def _comparison_inproc(d: dict) -> str:
+    from types import SimpleNamespace
+    c_ = d["cfg"]
+    cfg = config(c_["budget"], tuple(c_["bw"]), tuple(c_["eff"]), c_["policy_mode"], c_["heuristic"])
+    cfg.cost_model.swap_cost_mode = c_["swap"]
+    cfg.watermark_fraction = tuple(c_["wm"])
+    cfg.prefetch_limit = c_["limit"]
+    cfg.prefetch_enabled = c_["pf"]
+    cfg.overlap_enabled = c_["ov"]
+    cfg.prefetch_guard = c_["guard"]
+    del SimpleNamespace
+    trace_json, budgets, policies, heuristics = d["trace"], d["budgets"], d["policies"], d["heuristics"]
+    fmt = d["fmt"]
+    c, keep = _cfg(cfg)
+    b = (C.c_uint64 * max(1, len(budgets)))(*budgets)
+    p = (C.c_uint32 * max(1, len(policies)))(*[int(x) for x in policies])
+    h = (C.c_uint32 * max(1, len(heuristics)))(*[int(x) for x in heuristics])
+    return _take(lib().dref_comparison(trace_json.encode(), C.byref(c), b, len(budgets), p,
+                                       len(policies), h, len(heuristics), int(fmt == "json")))
 
 
 def brute_force(trace_json: str, max_nodes: int = 12) -> int:

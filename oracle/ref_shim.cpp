@@ -137,6 +137,22 @@ char* dref_report(const char* trace_json, const dref_config* c) {
   });
 }
 
+// run_comparison + comparison_to_csv / _json of the reference (json: 0 / 1)
+char* dref_comparison(const char* trace_json, const dref_config* c, const uint64_t* budgets,
+                      uint64_t nb, const uint32_t* policies, uint64_t np,
+                      const uint32_t* heuristics, uint64_t nh, int json_out) {
+  return guarded([&] {
+    Trace t = parse_trace(trace_json);
+    std::vector<Bytes> b(budgets, budgets + nb);
+    std::vector<PolicyMode> p;
+    for (uint64_t i = 0; i < np; ++i) p.push_back(static_cast<PolicyMode>(policies[i]));
+    std::vector<Heuristic> h;
+    for (uint64_t i = 0; i < nh; ++i) h.push_back(static_cast<Heuristic>(heuristics[i]));
+    ComparisonReport rep = run_comparison(t, b, p, h, to_cfg(c));
+    return json_out ? comparison_to_json(rep) : comparison_to_csv(rep);
+  });
+}
+
 // Median-free mean ns per run_iteration over `iters` calls (trace parsed once).
 double dref_time_run(const char* trace_json, const dref_config* c, int iters) {
   try {

@@ -97,6 +97,8 @@ def _load():
         "delta_result_events": (P(DeltaEvent), [vp, P(u64)]),
         "delta_result_decisions": (P(DeltaDecision), [vp, P(u64)]),
         "delta_report_json": (i32, [vp, vp, P(vp), P(u64)]),
+        "delta_comparison": (i32, [vp, P(DeltaConfig), P(u64), u64, P(u32), u64, P(u32), u64, i32,
+                                   P(vp), P(u64)]),
         "delta_chrome_trace": (i32, [vp, P(vp), P(u64)]),
         "delta_chrome_trace_events": (i32, [vp, u64, P(vp), P(u64)]),
         "delta_result_free": (None, [vp]),

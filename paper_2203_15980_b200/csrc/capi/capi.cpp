@@ -295,6 +295,28 @@ delta_status delta_report_json(const delta_result* run, const delta_result* base
   return guard([&] { *out = dup_str(report_to_json(summarize(run->r, base->r)), len); });
 }
 
+delta_status delta_comparison(const delta_trace* t, const delta_config* base,
+                              const uint64_t* budgets, uint64_t n_budgets,
+                              const uint32_t* policies, uint64_t n_policies,
+                              const uint32_t* heuristics, uint64_t n_heuristics, int32_t json,
+                              char** out, uint64_t* len) {
+  return guard([&] {
+    std::vector<Bytes> b(budgets, budgets + n_budgets);
+    std::vector<PolicyMode> p;
+    for (uint64_t i = 0; i < n_policies; ++i) {
+      if (policies[i] > uint32_t(PolicyMode::Baseline)) throw ArgumentError("comparison: bad policy");
+      p.push_back(static_cast<PolicyMode>(policies[i]));
+    }
+    std::vector<Heuristic> h;
+    for (uint64_t i = 0; i < n_heuristics; ++i) {
+      if (heuristics[i] > uint32_t(Heuristic::Greedy)) throw ArgumentError("comparison: bad heuristic");
+      h.push_back(static_cast<Heuristic>(heuristics[i]));
+    }
+    const ComparisonReport rep = run_comparison(t->t, b, p, h, to_cfg(base));
+    *out = dup_str(json ? comparison_to_json(rep) : comparison_to_csv(rep), len);
+  });
+}
+
 delta_status delta_chrome_trace(const delta_result* r, char** out, uint64_t* len) {
   return guard([&] { *out = dup_str(timeline_to_chrome_trace(r->r.timeline), len); });
 }

@@ -307,6 +307,25 @@ def report_json(run: RunResult, baseline: RunResult) -> str:
     return take_string(p, n.value)
 
 
+def comparison(trace: Trace, budgets, policies, heuristics, base: EngineConfig | None = None,
+               fmt: str = "csv") -> str:
+    """run_comparison + comparison_to_csv / _json (ref src/engine.cpp:646-671,
+    src/metrics.cpp:314-348): the planned budget x policy x heuristic grid."""
+    base = base or EngineConfig()
+    h = _CTrace(trace)
+    try:
+        c, keep = base.to_c()
+        b = (C.c_uint64 * max(1, len(budgets)))(*budgets)
+        pm = (C.c_uint32 * max(1, len(policies)))(*[int(x) for x in policies])
+        hm = (C.c_uint32 * max(1, len(heuristics)))(*[int(x) for x in heuristics])
+        p, n = C.c_void_p(), C.c_uint64()
+        check(lib.delta_comparison(h.ptr, C.byref(c), b, len(budgets), pm, len(policies), hm,
+                                   len(heuristics), int(fmt == "json"), C.byref(p), C.byref(n)))
+        return take_string(p, n.value)
+    finally:
+        h.close()
+
+
 def plan_time_ns(trace: Trace, cfg: EngineConfig, iters: int = 1000) -> float:
     h = _CTrace(trace)
     try:
@@ -384,6 +403,6 @@ __all__ = [
     "Phase", "AccessKind", "Heuristic", "PolicyMode", "ReleaseAction", "SwapCostMode",
     "PrefetchGuard", "EventKind", "StreamKind", "OpNode", "AccessEvent", "Trace",
     "CostModel", "EngineConfig", "RunResult", "run_iteration", "run_unconstrained_baseline",
-    "report_json", "plan_time_ns", "transfer_time_us", "Program", "DeltaError",
+    "report_json", "comparison", "plan_time_ns", "transfer_time_us", "Program", "DeltaError",
     "chrome_trace_events",
 ]

@@ -414,7 +414,7 @@ class DeltaRuntime:
                 budget = int(self.baseline_peak() * budget_fraction)
             cfg = self.engine_config(budget, policy, **kw)
         target = cfg.budget
-        for _ in range(8):
+        for _ in range(16):
             prog = P.Program(t, cfg, align=G.ALIGN, duplex=duplex)
             if prog.infeasible:
                 node, deficit = prog.infeasible
@@ -426,7 +426,8 @@ class DeltaRuntime:
             # budget (the reference's pool is a byte counter): plan again under
             # a budget smaller by the excess, so the ARENA fits the caller's
             # budget; the plan is then the reference's plan at that budget
-            cfg = dataclasses.replace(cfg, budget=cfg.budget - (prog.arena_bytes - target))
+            cfg = dataclasses.replace(
+                cfg, budget=cfg.budget - max(prog.arena_bytes - target, target // 256))
         if prog.arena_bytes > target and cfg.policy_mode != P.PolicyMode.Baseline:
             raise RuntimeError(f"arena {prog.arena_bytes} B exceeds the budget {target} B")
         self.budget_bytes = target  # the caller's budget: the arena fits it

@@ -321,3 +321,26 @@ def test_reference_unit_suites_pass_against_libdelta():
                          text=True, timeout=600, cwd="/tmp")
     assert out.returncode == 0, out.stderr[-3000:]
     assert "test cases: 53 | 53 passed | 0 failed" in out.stdout, out.stdout
+
+
+# ------------------- run_comparison grid + comparison CSV/JSON
+@pytest.mark.parametrize("fixture", ["resnet16.json", "resnet50_bs256_trace.json"])
+def test_comparison_grid_byte_equal_to_reference(fixture):
+    """budget x policy x heuristic grid (ref src/engine.cpp:646-671) rendered
+    as the reference's comparison CSV and JSON (src/metrics.cpp:314-348):
+    byte-equal to the unmodified reference's."""
+    ref = pytest.importorskip("oracle.ref")
+    if not ref.available():
+        pytest.skip("oracle/_ref not built")
+    tj = read(fixture)
+    t = P.Trace.from_json(tj)
+    base = P.run_unconstrained_baseline(t, P.EngineConfig())
+    budgets = [base.peak_bytes * f // 100 for f in (35, 50, 65, 80)]
+    policies = list(P.PolicyMode)
+    heuristics = list(P.Heuristic)
+    cfg = P.EngineConfig(cost_model=P.CostModel((48281, 1), (1, 1)))
+    for fmt in ("csv", "json"):
+        mine = P.comparison(t, budgets, policies, heuristics, cfg, fmt=fmt)
+        theirs = ref.comparison(tj, cfg, budgets, policies, heuristics, fmt=fmt)
+        assert mine == theirs
+    assert mine.count('"policy"') == len(budgets) * len(policies) * len(heuristics)

@@ -418,3 +418,28 @@ def test_resnet101_step_matches_no_eviction():
     x, y = make_batch(7, 4)
     assert base.step(x, y) == rt.step(x, y)
     assert torch.equal(base.params.grad, rt.params.grad)
+
+
+def test_executed_comparison_grid(rts):
+    """f3: a small budget x policy grid executed on the GPU — the reference's
+    comparison CSV header, one row per cell, every feasible cell bit-identical
+    to the no-eviction step, the arena within the budget."""
+    from paper_2203_15980_b200 import grid as GR
+    base, _ = rts
+    rt = DeltaRuntime(50, BATCH, seed=0, lr=0.0)
+    for n, m in zip(rt.nodes, base.nodes):
+        n.cost_us = m.cost_us
+    rt.link_gbs = base.link_gbs
+    x, y = make_batch(9)
+    for s in range(2):
+        rt.x_slots[s].copy_(x)
+        rt.y_slots[s].copy_(y)
+    text, detail = GR.executed_comparison(rt, [0.5, 0.7],
+                                          [P.PolicyMode.Delta, P.PolicyMode.OffloadOnly],
+                                          [P.Heuristic.Base, P.Heuristic.Greedy], steps=2, warmup=1)
+    lines = text.strip().splitlines()
+    assert lines[0] == GR.CSV_HEADER
+    assert len(lines) == 1 + 2 * 2 * 2
+    feasible = [c for c in detail if not c["infeasible"]]
+    assert feasible and all(c["bit_identical"] for c in feasible)
+    assert all(c["arena_bytes"] <= c["budget"] for c in feasible)
