@@ -214,8 +214,8 @@ def workspace_plan(g: G.Graph) -> dict:
              if n.op == "conv_shortcut_bwd" and "conv_short" in n.attrs
              and g.convs[n.attrs["conv_short"]].stride != 1]
     ws["short_ws"] = max(short + [256])
-    mp = next(n for n in nodes if n.op == "maxpool")
-    ws["mp_ws"] = K.maxpool_workspace_bytes(*nodes[mp.parents[0]].shape)
+    ws["mp_ws"] = max([K.maxpool_workspace_bytes(*nodes[n.parents[0]].shape) for n in nodes
+                       if n.op == "maxpool"] + [256])
     wg = 0
     for n in nodes:
         if n.op == "conv":
@@ -262,11 +262,18 @@ class StepStats:
 class DeltaRuntime:
     """ResNet training step under a DELTA activation budget on one B200."""
 
-    def __init__(self, depth: int = 50, batch: int = 256, image: int = 224,
+    def __init__(self, depth: int | G.Graph = 50, batch: int = 256, image: int = 224,
                  device: str = "cuda", seed: int = 0, anchors: str = "out+narrow",
                  lr: float = 0.1):
+        """depth: 50 / 101 for the built-in ResNets, or a prebuilt graph (e.g.
+        importer.graph_from_module of a PyTorch model; batch / image are then
+        the graph's)."""
         self.device = torch.device(device)
-        self.g = G.build_resnet(depth, batch, image)
+        if isinstance(depth, G.Graph):
+            self.g = depth
+            batch = self.g.nodes[0].shape[0]
+        else:
+            self.g = G.build_resnet(depth, batch, image)
         self.batch = batch
         self.lr = lr
         self.anchors = anchors
@@ -620,6 +627,14 @@ class DeltaRuntime:
             else:
                 add(X.kop(X.K_CONV_EX, (X.IN(0), X.OUT(), None, add_, add_mask, out_mask),
                           (K.EPI_ADD_MASK, pool_hw, stride2), conv=self._dconvs[conv]._h))
+            add(wgrad(conv, 0, 1), 2, 2)
+        elif op == "conv_bwd":
+            # a conv fed by a maxpool (imported chains): plain input gradient on
+            # the tensor cores + weight gradient
+            conv = node.attrs["conv"]
+            if conv not in self._dconvs:
+                raise RuntimeError(f"{node.name}: no input-gradient kernel for conv {conv}")
+            add(X.kop(X.K_CONV, (X.IN(0), X.OUT(), None), conv=self._dconvs[conv]._h))
             add(wgrad(conv, 0, 1), 2, 2)
         elif op == "maxpool_bwd":
             Nb, H, W, Cs = self.nodes[node.parents[1]].shape
