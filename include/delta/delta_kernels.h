@@ -68,8 +68,20 @@ delta_status delta_conv_forward(const delta_conv* c, const void* x, void* y, flo
  *       delta_weight_view DELTA_VIEW_DGRAD_S2): output pixel (p, q) of class
  *       (a, b) is written to y[n][2p+a][2q+b][:] of the [N][2P][2Q][K]
  *       gradient.  The four classes tile y exactly once.
+ *   DELTA_EPI_BIAS: y = bf16(acc + beta[k]) — a linear layer (1x1, stride 1:
+ *       x = [tokens][in], weights [out][in]) with its bias (`beta`).
+ *   DELTA_EPI_GELU_BWD: y = bf16(acc * gelu'(xc)), xc = the [M][K] GELU input
+ *       (erf GELU): the MLP input gradient through the GELU (1x1 only,
+ *       tile_n <= 128).
  * Output channels must be a multiple of 32 for the fused modes. */
-enum { DELTA_EPI_STORE = 0, DELTA_EPI_ADD_MASK = 1, DELTA_EPI_BN_BWD = 2, DELTA_EPI_SCATTER2 = 3 };
+enum {
+  DELTA_EPI_STORE = 0,
+  DELTA_EPI_ADD_MASK = 1,
+  DELTA_EPI_BN_BWD = 2,
+  DELTA_EPI_SCATTER2 = 3,
+  DELTA_EPI_BIAS = 4,
+  DELTA_EPI_GELU_BWD = 5
+};
 typedef struct delta_conv_epilogue {
   int32_t mode;
   int32_t pool_hw;

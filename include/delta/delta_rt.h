@@ -26,6 +26,7 @@
 
 #include "delta/delta.h"
 #include "delta/delta_kernels.h"
+#include "delta/delta_xformer.h"
 
 #ifdef __cplusplus
 extern "C" {
@@ -70,6 +71,24 @@ typedef struct delta_ref {
  *                  r4 dlogits (fp32 [N][i1]), r5 dlogits (bf16 [N][i2]),
  *                  r6 dbias, r7 row_ws, i0 N, i1 K, i2 ld  (softmax_xent_head)
  *  CONV_EX with i0 = DELTA_EPI_SCATTER2: i3 = the parity class (2a + b)
+ * transformer ops (delta_xformer.h; rng = device {seed, step}):
+ *  LAYERNORM       r0 x, r1 y, r2 mean, r3 rstd, r4 gamma, r5 beta, i0 rows, i1 H, f0 eps
+ *  LAYERNORM_BWD   r0 dy, r1 x, r2 dres, r3 dx, r4 mean, r5 rstd, r6 gamma, r7 dgamma,
+ *                  r8 dbeta, r9 ws, i0 rows, i1 H
+ *  GELU            r0 x, r1 y, i0 n
+ *  ADD_DROPOUT     r0 a, r1 b, r2 y, r3 rng, i0 n, i1 tag, f0 p
+ *  DROPOUT_BWD     r0 dy, r1 dx, r2 rng, i0 n, i1 tag, f0 p
+ *  COLSUM          r0 x, r1 sel, r2 out, r3 ws, i0 rows, i1 cols, i2 sel_val, i3 accumulate
+ *  EMBED           r0 ids, r1 types, r2 word, r3 pos, r4 type, r5 y, r6 rng, i0 B, i1 S,
+ *                  i2 H, i3 tag, f0 p
+ *  EMBED_GRADS     r0 dsum, r1 csr, r2 types, r3 dword, r4 dpos, r5 dtype, r6 ws, i0 B,
+ *                  i1 S, i2 H, i3 vocab | n_types << 32
+ *  SPAN_HEAD       r0 h, r1 w, r2 bias, r3 label, r4 logits, r5 dlogits, r6 row_loss,
+ *                  r7 loss, i0 B, i1 S, i2 H
+ *  SPAN_HEAD_BWD   r0 h, r1 dlogits, r2 w, r3 dh, r4 dw, r5 dbias, r6 ws, i0 T, i1 H
+ *  ATTN            r0 qkv, r1 out, r2 lse, r3 rng, i0 B, i1 S, i2 heads, i3 tag, f0 p
+ *  ATTN_BWD        r0 qkv, r1 out, r2 dout, r3 lse, r4 D, r5 dqkv, r6 rng, i0 B, i1 S,
+ *                  i2 heads, i3 tag, f0 p
  */
 enum {
   DELTA_K_COPY = 1,
@@ -87,7 +106,19 @@ enum {
   DELTA_K_SOFTMAX_XENT = 13,
   DELTA_K_HOST = 14,
   DELTA_K_WGRAD = 15,
-  DELTA_K_XENT_HEAD = 16
+  DELTA_K_XENT_HEAD = 16,
+  DELTA_K_LAYERNORM = 17,
+  DELTA_K_LAYERNORM_BWD = 18,
+  DELTA_K_GELU = 19,
+  DELTA_K_ADD_DROPOUT = 20,
+  DELTA_K_DROPOUT_BWD = 21,
+  DELTA_K_COLSUM = 22,
+  DELTA_K_EMBED = 23,
+  DELTA_K_EMBED_GRADS = 24,
+  DELTA_K_SPAN_HEAD = 25,
+  DELTA_K_SPAN_HEAD_BWD = 26,
+  DELTA_K_ATTN = 27,
+  DELTA_K_ATTN_BWD = 28
 };
 enum {
   DELTA_KOP_FIRST_ONLY = 1,     /* skipped when the node is recomputed        */

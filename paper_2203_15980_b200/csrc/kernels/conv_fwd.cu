@@ -133,10 +133,14 @@ constexpr int EV_POOL = 3;     // y = bf16(acc + pooled/hw * [add_mask > 0]) & [
 constexpr int EV_BN_BWD = 4;   // y = g = bf16(acc) & [relu(bn(xc)) > 0]; partials (sum g, sum g*xc)
 constexpr int EV_ADD_OM_ST = 5;  // EV_ADD_OM + partials (sum y, sum y*xc): the next BN's backward sums
 constexpr int EV_SCATTER = 6;  // y[n][2p+a][2q+b] = bf16(acc): a stride-2 input gradient's parity class
+constexpr int EV_BIAS = 7;     // y = bf16(acc + bias[k])                     (linear layers)
+constexpr int EV_GELU_BWD = 8; // y = bf16(acc * gelu'(xc)), xc = the [M][K] pre-activation
 // epilogues that read [M][K] operand tiles (the operand ring / tile buffers)
-__host__ __device__ constexpr bool ev_fused(int ev) { return ev != EV_STORE && ev != EV_SCATTER; }
+__host__ __device__ constexpr bool ev_fused(int ev) {
+  return ev != EV_STORE && ev != EV_SCATTER && ev != EV_BIAS;
+}
 __host__ __device__ constexpr int ev_operands(int ev) {
-  return ev == EV_ADD || ev == EV_BN_BWD
+  return ev == EV_ADD || ev == EV_BN_BWD || ev == EV_GELU_BWD
              ? 1
              : (ev == EV_ADD_OM || ev == EV_POOL ? 2 : (ev == EV_ADD_OM_ST ? 3 : 0));
 }
@@ -506,7 +510,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     constexpr int CHW = CH / HALVES;    // chunks per tile of this warp
     static_assert(CHW >= 1 && CH % HALVES == 0, "epilogue split");
     const bf16* src0 = static_cast<const bf16*>(
-        EV == EV_BN_BWD ? a.e.xc : (EV == EV_POOL ? a.e.add_mask : a.e.add));
+        EV == EV_BN_BWD || EV == EV_GELU_BWD ? a.e.xc : (EV == EV_POOL ? a.e.add_mask : a.e.add));
     const bf16* src1 = static_cast<const bf16*>(a.e.out_mask);
     // stage this warp's chunk number e (tile = first + (e / CHW) * grid,
     // chunk j = half + (e % CHW) * HALVES)
@@ -609,6 +613,26 @@ __global__ void __launch_bounds__(kThreads, 1)
             unpack8f(ld_row16(sb, lane, u), mk);
 #pragma unroll
             for (int i = 0; i < 8; ++i) v[u * 8 + i] += mk[i] > 0.f ? g[i] * inv : 0.f;
+          }
+        }
+        if constexpr (EV == EV_BIAS) {
+          // lane c holds bias[col + c]; broadcast column by column
+          const float bl = col + lane < a.K ? __ldg(a.e.beta + col + lane) : 0.f;
+#pragma unroll
+          for (int i = 0; i < 32; ++i) v[i] += __shfl_sync(0xFFFFFFFFu, bl, i);
+        }
+        if constexpr (EV == EV_GELU_BWD) {
+          // d(pre-activation) = d(gelu output) * gelu'(pre-activation), fp32
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            float hx[8];
+            unpack8f(ld_row16(sb, lane, u), hx);
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+              const float x = hx[i];
+              const float cdf = 0.5f * (1.f + erff(x * 0.70710678118654752f));
+              v[u * 8 + i] *= fmaf(x * 0.3989422804014327f, __expf(-0.5f * x * x), cdf);
+            }
           }
         }
         if constexpr (row_tiled(MODE)) {
@@ -1051,7 +1075,8 @@ cudaError_t launch(const ConvPlan& cp, const void* x, void* y, float* stats,
   // OPT: the fused epilogue's [M][K] operands as 32-column x 128-row boxes
   alignas(64) CUtensorMap emap0 = ymap, emap1 = ymap, emap2 = ymap;
   if (OPT) {
-    const void* op0 = EV == EV_BN_BWD ? epi.xc : (EV == EV_POOL ? epi.add_mask : epi.add);
+    const void* op0 = EV == EV_BN_BWD || EV == EV_GELU_BWD ? epi.xc
+                                                           : (EV == EV_POOL ? epi.add_mask : epi.add);
     if (!tma_2d_bf16(&emap0, op0, uint64_t(cp.K), uint64_t(a.M), uint64_t(cp.K), 32, BM,
                      CU_TENSOR_MAP_SWIZZLE_64B))
       return cudaErrorInvalidValue;
@@ -1144,6 +1169,25 @@ cudaError_t conv_forward(const ConvPlan& cp, const void* x, void* y, float* stat
         return tma_a ? launch<256, 4, MODE_TMA, EV_SCATTER>(cp, x, y, nullptr, e, st)
                      : launch<256, 4, MODE_IM2COL, EV_SCATTER>(cp, x, y, nullptr, e, st);
     }
+  }
+  if (e.mode == EPI_BIAS || e.mode == EPI_GELU_BWD) {
+    // linear layers (a 1x1 conv over [tokens][features]): bias epilogue, or
+    // the MLP input gradient times gelu' of the saved pre-activation
+    if (!tma_a || stats) return cudaErrorInvalidValue;
+    if (e.mode == EPI_BIAS) {
+      if (!e.beta) return cudaErrorInvalidValue;
+      switch (cp.bn) {
+        case 64: return launch<64, 8, MODE_TMA, EV_BIAS>(cp, x, y, nullptr, e, st);
+        case 128: return launch<128, 6, MODE_TMA, EV_BIAS>(cp, x, y, nullptr, e, st);
+        default: return launch<256, 4, MODE_TMA, EV_BIAS>(cp, x, y, nullptr, e, st);
+      }
+    }
+    if (!e.xc || !operands_tma()) return cudaErrorInvalidValue;
+    if (cp.bn == 64) return launch<64, 4, MODE_TMA, EV_GELU_BWD, true>(cp, x, y, nullptr, e, st);
+    if (cp.bn == 128)
+      return launch<128, opt_stages<EV_GELU_BWD>(), MODE_TMA, EV_GELU_BWD, true>(cp, x, y, nullptr,
+                                                                                 e, st);
+    return cudaErrorInvalidValue;
   }
   if (cp.halo && e.mode == EPI_STORE && !use_gather) return conv_halo_forward(cp, x, y, stats, st);
   if (e.mode != EPI_STORE) {

@@ -27,7 +27,10 @@ struct ConvPlan {
 //   EPI_SCATTER2 y[n][2p+a][2q+b][k] = bf16(acc) into a [N][2P][2Q][K] tensor,
 //                (a, b) = (scatter >> 1, scatter & 1): one parity class of a
 //                stride-2 input gradient (sub-pixel decomposition)
-constexpr int EPI_STORE = 0, EPI_ADD_MASK = 1, EPI_BN_BWD = 2, EPI_SCATTER2 = 3;
+//   EPI_BIAS     y = bf16(acc + beta[k])                        (linear layers)
+//   EPI_GELU_BWD y = bf16(acc * gelu'(xc)), xc the [M][K] pre-activation
+constexpr int EPI_STORE = 0, EPI_ADD_MASK = 1, EPI_BN_BWD = 2, EPI_SCATTER2 = 3, EPI_BIAS = 4,
+              EPI_GELU_BWD = 5;
 struct ConvEpilogue {
   int mode;
   int pool_hw;

@@ -1,0 +1,805 @@
+// Transformer (BERT) ops of the recompute engine, the layers of the
+// reference's transformer trace (ref src/trace.cpp:422-466: Embedding,
+// LayerNorm1/2, QKVProj, Attention, OutProj, AddResid1/2, MlpUp, MlpDown).
+// The linear layers are the tcgen05 GEMM (conv_fwd.cu, a 1x1 conv over the
+// [tokens][features] matrix, bias / GELU-backward epilogues) and attention is
+// attention.cu; this file holds the HBM-bound rest:
+//
+//   k_layernorm_fwd / k_layernorm_bwd(+merge)  one warp per row, two-pass
+//       statistics in registers; per-CTA (dgamma, dbeta) partial rows merged
+//       in a fixed order (deterministic, so a recomputed LayerNorm output and
+//       the step's gradients reproduce bit for bit)
+//   k_gelu_fwd                                 erf GELU (BERT), the Gelu node
+//   k_add_dropout / k_dropout_bwd              AddResid = x + dropout(y), masks
+//       from philox.cuh (replayed on recompute and in the backward pass)
+//   k_colsum(+merge)                           bias gradients (column sums),
+//       optionally over the rows of one token type
+//   k_embed_*                                  word + position + type gather,
+//       dropout; the word-embedding gradient as a segmented sum over a host-
+//       built CSR of the batch's token ids (no atomics)
+//   k_span_head_*                              SQuAD span head: start/end
+//       logits, the per-sequence softmax cross-entropy and its backward
+//   k_attn_dvec                                D = rowsum(dO * O), attention
+//       backward preprocessing
+//   k_adamw / k_rng_advance                    AdamW over the flat fp32
+//       buffers (+ bf16 weight copies), then the dropout step counter
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdint>
+
+#include "kernels/launch.hpp"
+#include "kernels/philox.cuh"
+#include "kernels/xformer.hpp"
+
+namespace delta_k {
+
+namespace {
+
+using bf16 = __nv_bfloat16;
+
+__device__ __forceinline__ void unpack8(uint4 u, float* f) {
+  const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&u);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const float2 t = __bfloat1622float2(h[i]);
+    f[2 * i] = t.x;
+    f[2 * i + 1] = t.y;
+  }
+}
+__device__ __forceinline__ uint32_t pk2(float a, float b) {
+  __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
+  return *reinterpret_cast<uint32_t*>(&h);
+}
+__device__ __forceinline__ uint4 pack8(const float* f) {
+  return make_uint4(pk2(f[0], f[1]), pk2(f[2], f[3]), pk2(f[4], f[5]), pk2(f[6], f[7]));
+}
+__device__ __forceinline__ float warp_sum(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xFFFFFFFFu, v, o);
+  return v;
+}
+__device__ __forceinline__ float warp_max(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xFFFFFFFFu, v, o));
+  return v;
+}
+
+int g_sms = 0;
+int sms() {
+  if (!g_sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&g_sms, cudaDevAttrMultiProcessorCount, dev);
+    if (g_sms <= 0) g_sms = 148;
+  }
+  return g_sms;
+}
+
+// ---------------------------------------------------------------- LayerNorm
+// Row r = one warp; lane owns NV 16-byte chunks at columns (v*32 + lane)*8.
+template <int NV>
+__global__ void __launch_bounds__(256)
+    k_layernorm_fwd(const bf16* __restrict__ x, bf16* __restrict__ y, float* __restrict__ mean,
+                    float* __restrict__ rstd, const float* __restrict__ gamma,
+                    const float* __restrict__ beta, int64_t rows, float eps) {
+  pdl_wait();
+  pdl_trigger();
+  constexpr int H = NV * 256;
+  const int lane = threadIdx.x & 31;
+  const int64_t r = int64_t(blockIdx.x) * 8 + (threadIdx.x >> 5);
+  if (r >= rows) return;
+  float v[NV][8];
+#pragma unroll
+  for (int k = 0; k < NV; ++k)
+    unpack8(__ldg(reinterpret_cast<const uint4*>(x + r * H) + k * 32 + lane), v[k]);
+  float s = 0.f;
+#pragma unroll
+  for (int k = 0; k < NV; ++k)
+#pragma unroll
+    for (int i = 0; i < 8; ++i) s += v[k][i];
+  const float mu = warp_sum(s) * (1.f / H);
+  float q = 0.f;
+#pragma unroll
+  for (int k = 0; k < NV; ++k)
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const float d = v[k][i] - mu;
+      q = fmaf(d, d, q);
+    }
+  const float rs = rsqrtf(warp_sum(q) * (1.f / H) + eps);
+#pragma unroll
+  for (int k = 0; k < NV; ++k) {
+    const int c = (k * 32 + lane) * 8;
+    const float4 g0 = __ldg(reinterpret_cast<const float4*>(gamma + c));
+    const float4 g1 = __ldg(reinterpret_cast<const float4*>(gamma + c + 4));
+    const float4 b0 = __ldg(reinterpret_cast<const float4*>(beta + c));
+    const float4 b1 = __ldg(reinterpret_cast<const float4*>(beta + c + 4));
+    const float g[8] = {g0.x, g0.y, g0.z, g0.w, g1.x, g1.y, g1.z, g1.w};
+    const float b[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
+    float o[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) o[i] = fmaf((v[k][i] - mu) * rs, g[i], b[i]);
+    reinterpret_cast<uint4*>(y + r * H)[k * 32 + lane] = pack8(o);
+  }
+  if (lane == 0) {
+    mean[r] = mu;
+    rstd[r] = rs;
+  }
+}
+
+// dx = rstd * (g - mean(g) - xhat * mean(g * xhat)) + dres, g = dy * gamma;
+// block b owns rows [b*chunk, (b+1)*chunk), warps interleaved, and writes one
+// partial row pair (sum dy*xhat, sum dy) per column to ws[b][2][H].
+template <int NV>
+__global__ void __launch_bounds__(256)
+    k_layernorm_bwd(const bf16* __restrict__ dy, const bf16* __restrict__ x,
+                    const bf16* __restrict__ dres, bf16* __restrict__ dx,
+                    const float* __restrict__ mean, const float* __restrict__ rstd,
+                    const float* __restrict__ gamma, float* __restrict__ ws, int64_t rows,
+                    int64_t chunk) {
+  pdl_wait();
+  pdl_trigger();
+  constexpr int H = NV * 256;
+  __shared__ float red[8][2][256];  // per warp, per chunk pass
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  float acc_g[NV][8], acc_b[NV][8];
+#pragma unroll
+  for (int k = 0; k < NV; ++k)
+#pragma unroll
+    for (int i = 0; i < 8; ++i) acc_g[k][i] = acc_b[k][i] = 0.f;
+  float gm[NV][8];
+#pragma unroll
+  for (int k = 0; k < NV; ++k) {
+    const int c = (k * 32 + lane) * 8;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) gm[k][i] = __ldg(gamma + c + i);
+  }
+  const int64_t r0 = int64_t(blockIdx.x) * chunk;
+  const int64_t r1 = min(rows, r0 + chunk);
+  for (int64_t r = r0 + warp; r < r1; r += 8) {
+    float xv[NV][8], g[NV][8];
+    const float mu = __ldg(mean + r), rs = __ldg(rstd + r);
+    float sg = 0.f, sgx = 0.f;
+#pragma unroll
+    for (int k = 0; k < NV; ++k) {
+      float d[8];
+      unpack8(__ldg(reinterpret_cast<const uint4*>(dy + r * H) + k * 32 + lane), d);
+      unpack8(__ldg(reinterpret_cast<const uint4*>(x + r * H) + k * 32 + lane), xv[k]);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        xv[k][i] = (xv[k][i] - mu) * rs;  // xhat
+        g[k][i] = d[i] * gm[k][i];
+        sg += g[k][i];
+        sgx = fmaf(g[k][i], xv[k][i], sgx);
+        acc_g[k][i] = fmaf(d[i], xv[k][i], acc_g[k][i]);
+        acc_b[k][i] += d[i];
+      }
+    }
+    const float a = warp_sum(sg) * (1.f / H);
+    const float b = warp_sum(sgx) * (1.f / H);
+#pragma unroll
+    for (int k = 0; k < NV; ++k) {
+      float o[8], rr[8];
+      if (dres) {
+        unpack8(__ldg(reinterpret_cast<const uint4*>(dres + r * H) + k * 32 + lane), rr);
+      } else {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) rr[i] = 0.f;
+      }
+#pragma unroll
+      for (int i = 0; i < 8; ++i) o[i] = fmaf(rs, g[k][i] - a - xv[k][i] * b, rr[i]);
+      reinterpret_cast<uint4*>(dx + r * H)[k * 32 + lane] = pack8(o);
+    }
+  }
+  // fixed-order reduction over the 8 warps, 256 columns at a time
+#pragma unroll
+  for (int k = 0; k < NV; ++k) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      red[warp][0][lane * 8 + i] = acc_g[k][i];
+      red[warp][1][lane * 8 + i] = acc_b[k][i];
+    }
+    __syncthreads();
+    for (int t = threadIdx.x; t < 512; t += 256) {
+      const int which = t >> 8, c = t & 255;
+      float s = 0.f;
+#pragma unroll
+      for (int w = 0; w < 8; ++w) s += red[w][which][c];
+      // column (k*32 + c/8)*8 + c%8 of the row
+      ws[(int64_t(blockIdx.x) * 2 + which) * H + k * 256 + c] = s;
+    }
+    __syncthreads();
+  }
+}
+
+__global__ void __launch_bounds__(256)
+    k_rows_merge2(const float* __restrict__ ws, int parts, int H, float* __restrict__ out0,
+                  float* __restrict__ out1) {
+  pdl_wait();
+  pdl_trigger();
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= H) return;
+  float s0 = 0.f, s1 = 0.f;
+  for (int p = 0; p < parts; ++p) {
+    s0 += ws[(int64_t(p) * 2) * H + c];
+    s1 += ws[(int64_t(p) * 2 + 1) * H + c];
+  }
+  out0[c] = s0;
+  out1[c] = s1;
+}
+
+// ---------------------------------------------------------------- GELU
+__device__ __forceinline__ float gelu_erf(float x) {
+  return 0.5f * x * (1.f + erff(x * 0.70710678118654752f));
+}
+
+__global__ void __launch_bounds__(256)
+    k_gelu_fwd(const uint4* __restrict__ x, uint4* __restrict__ y, int64_t n8) {
+  pdl_wait();
+  pdl_trigger();
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n8;
+       i += int64_t(gridDim.x) * blockDim.x) {
+    float v[8];
+    unpack8(__ldg(x + i), v);
+#pragma unroll
+    for (int k = 0; k < 8; ++k) v[k] = gelu_erf(v[k]);
+    y[i] = pack8(v);
+  }
+}
+
+// ---------------------------------------------------------------- dropout
+// thread = one Philox block = 16 elements (two 16-byte vectors)
+template <bool BWD>
+__global__ void __launch_bounds__(256)
+    k_dropout(const uint4* __restrict__ a, const uint4* __restrict__ b, uint4* __restrict__ y,
+              int64_t n16, uint32_t thr, float scale, const uint64_t* __restrict__ rng,
+              uint32_t tag) {
+  pdl_wait();
+  pdl_trigger();
+  const uint64_t seed = rng[0], step = rng[1];
+  for (int64_t g = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; g < n16;
+       g += int64_t(gridDim.x) * blockDim.x) {
+    const uint32_t keep = thr ? keep16(drop_block(seed, step, tag, uint64_t(g)), thr) : 0xFFFFu;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      float vb[8], o[8];
+      unpack8(__ldg(b + 2 * g + h), vb);
+      if (BWD) {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) o[i] = (keep >> (h * 8 + i)) & 1u ? vb[i] * scale : 0.f;
+      } else {
+        float va[8];
+        unpack8(__ldg(a + 2 * g + h), va);
+#pragma unroll
+        for (int i = 0; i < 8; ++i)
+          o[i] = (keep >> (h * 8 + i)) & 1u ? fmaf(vb[i], scale, va[i]) : va[i];
+      }
+      y[2 * g + h] = pack8(o);
+    }
+  }
+}
+
+// ---------------------------------------------------------------- column sums
+// ws[part][cols]: part p sums rows [p*chunk, (p+1)*chunk) (rows with
+// sel[r] == sel_val only, when sel is given); thread = 8 columns.
+__global__ void __launch_bounds__(256)
+    k_colsum_part(const bf16* __restrict__ x, int64_t rows, int cols, const int32_t* __restrict__ sel,
+                  int sel_val, int64_t chunk, float* __restrict__ ws) {
+  pdl_wait();
+  pdl_trigger();
+  const int c8 = blockIdx.y * blockDim.x + threadIdx.x;
+  if (c8 * 8 >= cols) return;
+  const int64_t r0 = int64_t(blockIdx.x) * chunk, r1 = min(rows, r0 + chunk);
+  float s[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+  for (int64_t r = r0; r < r1; ++r) {
+    if (sel && __ldg(sel + r) != sel_val) continue;
+    float v[8];
+    unpack8(__ldg(reinterpret_cast<const uint4*>(x + r * cols) + c8), v);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) s[i] += v[i];
+  }
+  float4* o = reinterpret_cast<float4*>(ws + int64_t(blockIdx.x) * cols + c8 * 8);
+  o[0] = make_float4(s[0], s[1], s[2], s[3]);
+  o[1] = make_float4(s[4], s[5], s[6], s[7]);
+}
+
+__global__ void __launch_bounds__(256)
+    k_colsum_merge(const float* __restrict__ ws, int parts, int cols, float* __restrict__ out,
+                   int accumulate) {
+  pdl_wait();
+  pdl_trigger();
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= cols) return;
+  float s = 0.f;
+  for (int p = 0; p < parts; ++p) s += ws[int64_t(p) * cols + c];
+  out[c] = accumulate ? out[c] + s : s;
+}
+
+// ---------------------------------------------------------------- embeddings
+// y[t] = dropout(word[id[t]] + pos[t % S] + type[tt[t]]); warp per token,
+// a lane pair shares each Philox block (16 columns).
+template <int NV>
+__global__ void __launch_bounds__(256)
+    k_embed_fwd(const int32_t* __restrict__ ids, const int32_t* __restrict__ types,
+                const bf16* __restrict__ word, const bf16* __restrict__ pos,
+                const bf16* __restrict__ type, bf16* __restrict__ y, int64_t T, int S,
+                uint32_t thr, float scale, const uint64_t* __restrict__ rng, uint32_t tag) {
+  pdl_wait();
+  pdl_trigger();
+  constexpr int H = NV * 256;
+  const int lane = threadIdx.x & 31;
+  const int64_t t = int64_t(blockIdx.x) * 8 + (threadIdx.x >> 5);
+  if (t >= T) return;
+  const uint64_t seed = rng[0], step = rng[1];
+  const int64_t id = __ldg(ids + t), tt = types ? __ldg(types + t) : 0, s = t % S;
+#pragma unroll
+  for (int k = 0; k < NV; ++k) {
+    const int v = k * 32 + lane;
+    float a[8], b[8], c[8], o[8];
+    unpack8(__ldg(reinterpret_cast<const uint4*>(word + id * H) + v), a);
+    unpack8(__ldg(reinterpret_cast<const uint4*>(pos + s * H) + v), b);
+    unpack8(__ldg(reinterpret_cast<const uint4*>(type + tt * H) + v), c);
+    const uint64_t e = uint64_t(t) * H + uint64_t(v) * 8;  // first element
+    const uint32_t keep =
+        thr ? (keep16(drop_block(seed, step, tag, e >> 4), thr) >> (e & 15)) : 0xFFu;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) o[i] = (keep >> i) & 1u ? (a[i] + b[i] + c[i]) * scale : 0.f;
+    reinterpret_cast<uint4*>(y + t * H)[v] = pack8(o);
+  }
+}
+
+// word-embedding gradient: block u sums the rows of unique id uniq[u] in
+// token order (perm[seg[u] .. seg[u+1])) into dword[uniq[u]] (fp32, rows of
+// ids absent from the batch were zeroed by the caller)
+__global__ void __launch_bounds__(128)
+    k_embed_word_grad(const bf16* __restrict__ d, const int32_t* __restrict__ csr, int T, int H,
+                      float* __restrict__ dword) {
+  pdl_wait();
+  pdl_trigger();
+  const int u = blockIdx.x;
+  if (u >= __ldg(csr)) return;
+  const int32_t* uniq = csr + 1;
+  const int32_t* seg = csr + 1 + T;
+  const int32_t* perm = csr + 2 + 2 * T;
+  const int id = __ldg(uniq + u), b = __ldg(seg + u), e = __ldg(seg + u + 1);
+  for (int c8 = threadIdx.x; c8 * 8 < H; c8 += blockDim.x) {
+    float s[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+    for (int j = b; j < e; ++j) {
+      float v[8];
+      unpack8(__ldg(reinterpret_cast<const uint4*>(d + int64_t(__ldg(perm + j)) * H) + c8), v);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) s[i] += v[i];
+    }
+    float4* o = reinterpret_cast<float4*>(dword + int64_t(id) * H + c8 * 8);
+    o[0] = make_float4(s[0], s[1], s[2], s[3]);
+    o[1] = make_float4(s[4], s[5], s[6], s[7]);
+  }
+}
+
+// position-embedding gradient: dpos[s] = sum over the batch in order
+__global__ void __launch_bounds__(128)
+    k_embed_pos_grad(const bf16* __restrict__ d, int B, int S, int H, float* __restrict__ dpos) {
+  pdl_wait();
+  pdl_trigger();
+  const int s = blockIdx.x;
+  for (int c8 = threadIdx.x; c8 * 8 < H; c8 += blockDim.x) {
+    float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+    for (int b = 0; b < B; ++b) {
+      float v[8];
+      unpack8(__ldg(reinterpret_cast<const uint4*>(d + (int64_t(b) * S + s) * H) + c8), v);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) acc[i] += v[i];
+    }
+    float4* o = reinterpret_cast<float4*>(dpos + int64_t(s) * H + c8 * 8);
+    o[0] = make_float4(acc[0], acc[1], acc[2], acc[3]);
+    o[1] = make_float4(acc[4], acc[5], acc[6], acc[7]);
+  }
+}
+
+// ---------------------------------------------------------------- span head
+// Block b = sequence b: logits z[t][j] = h[t] . w[j] + bias[j] (j = start,
+// end), log-softmax over the S positions, loss_b = (CE_start + CE_end) / 2,
+// dlogits = (softmax - onehot) / (2B).
+template <int NV>
+__global__ void __launch_bounds__(256)
+    k_span_head_fwd(const bf16* __restrict__ h, const float* __restrict__ w,
+                    const float* __restrict__ bias, const int32_t* __restrict__ label, int S,
+                    int B, float* __restrict__ logits, float* __restrict__ dlogits,
+                    float* __restrict__ row_loss) {
+  pdl_wait();
+  pdl_trigger();
+  constexpr int H = NV * 256;
+  extern __shared__ float z[];  // [S][2]
+  __shared__ float red[2][2];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int b = blockIdx.x;
+  float w0[NV][8], w1[NV][8];
+#pragma unroll
+  for (int k = 0; k < NV; ++k)
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      w0[k][i] = __ldg(w + (k * 32 + lane) * 8 + i);
+      w1[k][i] = __ldg(w + H + (k * 32 + lane) * 8 + i);
+    }
+  const float b0 = __ldg(bias), b1 = __ldg(bias + 1);
+  for (int s = warp; s < S; s += 8) {
+    const int64_t t = int64_t(b) * S + s;
+    float d0 = 0.f, d1 = 0.f;
+#pragma unroll
+    for (int k = 0; k < NV; ++k) {
+      float v[8];
+      unpack8(__ldg(reinterpret_cast<const uint4*>(h + t * H) + k * 32 + lane), v);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        d0 = fmaf(v[i], w0[k][i], d0);
+        d1 = fmaf(v[i], w1[k][i], d1);
+      }
+    }
+    d0 = warp_sum(d0) + b0;
+    d1 = warp_sum(d1) + b1;
+    if (lane == 0) {
+      z[2 * s] = d0;
+      z[2 * s + 1] = d1;
+      logits[2 * t] = d0;
+      logits[2 * t + 1] = d1;
+    }
+  }
+  __syncthreads();
+  if (warp < 2) {
+    const int j = warp;
+    float m = -INFINITY;
+    for (int s = lane; s < S; s += 32) m = fmaxf(m, z[2 * s + j]);
+    m = warp_max(m);
+    float l = 0.f;
+    for (int s = lane; s < S; s += 32) l += __expf(z[2 * s + j] - m);
+    l = warp_sum(l);
+    const float lse = m + __logf(l);
+    const int y = __ldg(label + 2 * b + j);
+    const float inv = 0.5f / float(B);
+    for (int s = lane; s < S; s += 32)
+      dlogits[2 * (int64_t(b) * S + s) + j] = (__expf(z[2 * s + j] - lse) - (s == y ? 1.f : 0.f)) * inv;
+    if (lane == 0) red[j][0] = lse - z[2 * y + j];
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) row_loss[b] = 0.5f * (red[0][0] + red[1][0]);
+}
+
+__global__ void k_mean_loss(const float* __restrict__ row_loss, int B, float* __restrict__ loss) {
+  pdl_wait();
+  pdl_trigger();
+  if (threadIdx.x == 0) {
+    float s = 0.f;
+    for (int b = 0; b < B; ++b) s += row_loss[b];
+    loss[0] = s / float(B);
+  }
+}
+
+// dh[t] = dl[t][0] w[0] + dl[t][1] w[1]; partial dw over the block's token
+// chunk (fixed warp order) to ws[blk][2][H]
+template <int NV>
+__global__ void __launch_bounds__(256)
+    k_span_head_bwd(const bf16* __restrict__ h, const float* __restrict__ dl,
+                    const float* __restrict__ w, bf16* __restrict__ dh, float* __restrict__ ws,
+                    int64_t T, int64_t chunk) {
+  pdl_wait();
+  pdl_trigger();
+  constexpr int H = NV * 256;
+  __shared__ float red[8][2][256];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  float w0[NV][8], w1[NV][8], a0[NV][8], a1[NV][8];
+#pragma unroll
+  for (int k = 0; k < NV; ++k)
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      w0[k][i] = __ldg(w + (k * 32 + lane) * 8 + i);
+      w1[k][i] = __ldg(w + H + (k * 32 + lane) * 8 + i);
+      a0[k][i] = a1[k][i] = 0.f;
+    }
+  const int64_t t0 = int64_t(blockIdx.x) * chunk, t1 = min(T, t0 + chunk);
+  for (int64_t t = t0 + warp; t < t1; t += 8) {
+    const float g0 = __ldg(dl + 2 * t), g1 = __ldg(dl + 2 * t + 1);
+#pragma unroll
+    for (int k = 0; k < NV; ++k) {
+      float v[8], o[8];
+      unpack8(__ldg(reinterpret_cast<const uint4*>(h + t * H) + k * 32 + lane), v);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        o[i] = fmaf(g0, w0[k][i], g1 * w1[k][i]);
+        a0[k][i] = fmaf(g0, v[i], a0[k][i]);
+        a1[k][i] = fmaf(g1, v[i], a1[k][i]);
+      }
+      reinterpret_cast<uint4*>(dh + t * H)[k * 32 + lane] = pack8(o);
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < NV; ++k) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      red[warp][0][lane * 8 + i] = a0[k][i];
+      red[warp][1][lane * 8 + i] = a1[k][i];
+    }
+    __syncthreads();
+    for (int x = threadIdx.x; x < 512; x += 256) {
+      const int which = x >> 8, c = x & 255;
+      float s = 0.f;
+#pragma unroll
+      for (int q = 0; q < 8; ++q) s += red[q][which][c];
+      ws[(int64_t(blockIdx.x) * 2 + which) * H + k * 256 + c] = s;
+    }
+    __syncthreads();
+  }
+}
+
+// dbias[j] = sum_t dl[t][j] in token order (one warp per j, fixed lane
+// partition, xor-tree combine)
+__global__ void k_span_dbias(const float* __restrict__ dl, int64_t T, float* __restrict__ dbias) {
+  pdl_wait();
+  pdl_trigger();
+  const int j = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (j >= 2) return;
+  float s = 0.f;
+  for (int64_t t = lane; t < T; t += 32) s += dl[2 * t + j];
+  s = warp_sum(s);
+  if (lane == 0) dbias[j] = s;
+}
+
+// ---------------------------------------------------------------- attention prep
+// D[(b*heads + hd)*S + s] = sum_d dO[t][hd*64 + d] * O[t][hd*64 + d]; warp per
+// token, lane = 32 columns (half a head), lane pairs combined
+__global__ void __launch_bounds__(256)
+    k_attn_dvec(const bf16* __restrict__ o, const bf16* __restrict__ d, int64_t T, int S, int heads,
+                float* __restrict__ D) {
+  pdl_wait();
+  pdl_trigger();
+  const int lane = threadIdx.x & 31;
+  const int64_t t = int64_t(blockIdx.x) * 8 + (threadIdx.x >> 5);
+  if (t >= T) return;
+  const int H = heads * 64;
+  for (int base = 0; base < H; base += 1024) {
+    float s = 0.f;
+    const int c0 = base + lane * 32;
+    if (c0 < H) {
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        float a[8], b[8];
+        unpack8(__ldg(reinterpret_cast<const uint4*>(o + t * H + c0) + u), a);
+        unpack8(__ldg(reinterpret_cast<const uint4*>(d + t * H + c0) + u), b);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) s = fmaf(a[i], b[i], s);
+      }
+    }
+    s += __shfl_xor_sync(0xFFFFFFFFu, s, 1);
+    if (c0 < H && (lane & 1) == 0) {
+      const int hd = c0 / 64;
+      const int64_t bb = t / S, ss = t % S;
+      D[(bb * heads + hd) * S + ss] = s;
+    }
+  }
+}
+
+// ---------------------------------------------------------------- optimizer
+// AdamW (decoupled weight decay on the first n_bf elements: the matrices and
+// embedding tables), bias-corrected with the device step counter rng[1] + 1;
+// the leading n_bf fp32 masters also written as bf16 (the GEMM operands).
+__global__ void __launch_bounds__(256)
+    k_adamw(float* __restrict__ w, float* __restrict__ m, float* __restrict__ v,
+            const float* __restrict__ g, bf16* __restrict__ wbf, int64_t n, int64_t n_bf, float lr,
+            float b1, float b2, float eps, float wd, const uint64_t* __restrict__ rng) {
+  pdl_wait();
+  pdl_trigger();
+  const float t = float(rng[1] + 1);
+  const float c1 = 1.f / (1.f - powf(b1, t)), c2 = 1.f / (1.f - powf(b2, t));
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += int64_t(gridDim.x) * blockDim.x) {
+    const float gi = g[i];
+    const float mi = fmaf(b1, m[i], (1.f - b1) * gi);
+    const float vi = fmaf(b2, v[i], (1.f - b2) * gi * gi);
+    m[i] = mi;
+    v[i] = vi;
+    float wi = w[i];
+    const float upd = (mi * c1) / (sqrtf(vi * c2) + eps) + (i < n_bf ? wd * wi : 0.f);
+    wi = fmaf(-lr, upd, wi);
+    w[i] = wi;
+    if (i < n_bf) wbf[i] = __float2bfloat16_rn(wi);
+  }
+}
+
+__global__ void k_rng_advance(uint64_t* rng) {
+  if (threadIdx.x == 0) rng[1] += 1;
+}
+
+int grid_for(int64_t work, int per_block) {
+  const int64_t b = (work + per_block - 1) / per_block;
+  return int(std::max<int64_t>(1, std::min<int64_t>(b, int64_t(sms()) * 16)));
+}
+
+}  // namespace
+
+// ================================================================ launchers
+#define DELTA_NV_SWITCH(H, CALL)      \
+  switch ((H) / 256) {                \
+    case 1: { constexpr int NV = 1; CALL; break; } \
+    case 2: { constexpr int NV = 2; CALL; break; } \
+    case 3: { constexpr int NV = 3; CALL; break; } \
+    case 4: { constexpr int NV = 4; CALL; break; } \
+    case 8: { constexpr int NV = 8; CALL; break; } \
+    default: return cudaErrorInvalidValue;        \
+  }
+
+bool xf_width_ok(int H) { return H % 256 == 0 && (H / 256 <= 4 || H / 256 == 8); }
+
+cudaError_t layernorm_fwd(const void* x, void* y, float* mean, float* rstd, const float* gamma,
+                          const float* beta, int64_t rows, int H, float eps, cudaStream_t st) {
+  if (!xf_width_ok(H) || rows <= 0) return cudaErrorInvalidValue;
+  const dim3 grid(unsigned((rows + 7) / 8));
+  DELTA_NV_SWITCH(H, if (cudaError_t e = launch_k(k_layernorm_fwd<NV>, grid, dim3(256), 0, st,
+                                                  static_cast<const bf16*>(x), static_cast<bf16*>(y),
+                                                  mean, rstd, gamma, beta, rows, eps)) return e);
+  return cudaGetLastError();
+}
+
+int ln_bwd_parts(int64_t rows) {
+  return int(std::max<int64_t>(1, std::min<int64_t>((rows + 63) / 64, 2 * sms())));
+}
+int64_t layernorm_bwd_workspace_floats(int64_t rows, int H) {
+  return int64_t(2 * sms()) * 2 * H;
+}
+
+cudaError_t layernorm_bwd(const void* dy, const void* x, const void* dres, void* dx,
+                          const float* mean, const float* rstd, const float* gamma, float* dgamma,
+                          float* dbeta, float* ws, int64_t rows, int H, cudaStream_t st) {
+  if (!xf_width_ok(H) || rows <= 0 || H / 256 > 4) return cudaErrorInvalidValue;
+  const int parts = ln_bwd_parts(rows);
+  const int64_t chunk = (rows + parts - 1) / parts;
+  DELTA_NV_SWITCH(H, if (cudaError_t e = launch_k(k_layernorm_bwd<NV>, dim3(parts), dim3(256), 0,
+                                                  st, static_cast<const bf16*>(dy),
+                                                  static_cast<const bf16*>(x),
+                                                  static_cast<const bf16*>(dres),
+                                                  static_cast<bf16*>(dx), mean, rstd, gamma, ws,
+                                                  rows, chunk)) return e);
+  if (cudaError_t e = launch_k(k_rows_merge2, dim3((H + 255) / 256), dim3(256), 0, st,
+                               static_cast<const float*>(ws), parts, H, dgamma, dbeta))
+    return e;
+  return cudaGetLastError();
+}
+
+cudaError_t gelu_fwd(const void* x, void* y, int64_t n, cudaStream_t st) {
+  if (n % 8) return cudaErrorInvalidValue;
+  if (cudaError_t e = launch_k(k_gelu_fwd, dim3(grid_for(n / 8, 256)), dim3(256), 0, st,
+                               static_cast<const uint4*>(x), static_cast<uint4*>(y), n / 8))
+    return e;
+  return cudaGetLastError();
+}
+
+cudaError_t add_dropout(const void* a, const void* b, void* y, int64_t n, float p,
+                        const uint64_t* rng, uint32_t tag, cudaStream_t st) {
+  if (n % 16) return cudaErrorInvalidValue;
+  const DropParams dp = drop_params(p);
+  if (cudaError_t e = launch_k(k_dropout<false>, dim3(grid_for(n / 16, 256)), dim3(256), 0, st,
+                               static_cast<const uint4*>(a), static_cast<const uint4*>(b),
+                               static_cast<uint4*>(y), n / 16, dp.thr, dp.scale, rng, tag))
+    return e;
+  return cudaGetLastError();
+}
+
+cudaError_t dropout_bwd(const void* dy, void* dx, int64_t n, float p, const uint64_t* rng,
+                        uint32_t tag, cudaStream_t st) {
+  if (n % 16) return cudaErrorInvalidValue;
+  const DropParams dp = drop_params(p);
+  if (cudaError_t e = launch_k(k_dropout<true>, dim3(grid_for(n / 16, 256)), dim3(256), 0, st,
+                               static_cast<const uint4*>(nullptr), static_cast<const uint4*>(dy),
+                               static_cast<uint4*>(dx), n / 16, dp.thr, dp.scale, rng, tag))
+    return e;
+  return cudaGetLastError();
+}
+
+int colsum_parts(int64_t rows) {
+  return int(std::max<int64_t>(1, std::min<int64_t>((rows + 31) / 32, 2 * sms())));
+}
+int64_t colsum_workspace_floats(int64_t rows, int cols) {
+  return int64_t(2 * sms()) * cols;
+}
+
+cudaError_t colsum(const void* x, int64_t rows, int cols, const int32_t* sel, int sel_val,
+                   float* out, float* ws, int accumulate, cudaStream_t st) {
+  if (cols % 8 || rows <= 0) return cudaErrorInvalidValue;
+  const int parts = colsum_parts(rows);
+  const int64_t chunk = (rows + parts - 1) / parts;
+  const dim3 grid(parts, unsigned((cols / 8 + 255) / 256));
+  if (cudaError_t e = launch_k(k_colsum_part, grid, dim3(256), 0, st, static_cast<const bf16*>(x),
+                               rows, cols, sel, sel_val, chunk, ws))
+    return e;
+  if (cudaError_t e = launch_k(k_colsum_merge, dim3((cols + 255) / 256), dim3(256), 0, st,
+                               static_cast<const float*>(ws), parts, cols, out, accumulate))
+    return e;
+  return cudaGetLastError();
+}
+
+cudaError_t embed_fwd(const int32_t* ids, const int32_t* types, const void* word, const void* pos,
+                      const void* type, void* y, int B, int S, int H, float p, const uint64_t* rng,
+                      uint32_t tag, cudaStream_t st) {
+  if (!xf_width_ok(H)) return cudaErrorInvalidValue;
+  const int64_t T = int64_t(B) * S;
+  const DropParams dp = drop_params(p);
+  DELTA_NV_SWITCH(H, if (cudaError_t e = launch_k(k_embed_fwd<NV>, dim3(unsigned((T + 7) / 8)),
+                                                  dim3(256), 0, st, ids, types,
+                                                  static_cast<const bf16*>(word),
+                                                  static_cast<const bf16*>(pos),
+                                                  static_cast<const bf16*>(type),
+                                                  static_cast<bf16*>(y), T, S, dp.thr, dp.scale,
+                                                  rng, tag)) return e);
+  return cudaGetLastError();
+}
+
+cudaError_t embed_grads(const void* dsum, const int32_t* csr, const int32_t* types, int B, int S,
+                        int H, int vocab, int n_types, float* dword, float* dpos, float* dtype,
+                        float* ws, cudaStream_t st) {
+  const int T = B * S;
+  if (H % 8) return cudaErrorInvalidValue;
+  if (cudaError_t e = cudaMemsetAsync(dword, 0, size_t(vocab) * H * 4, st)) return e;
+  if (cudaError_t e = launch_k(k_embed_word_grad, dim3(T), dim3(128), 0, st,
+                               static_cast<const bf16*>(dsum), csr, T, H, dword))
+    return e;
+  if (cudaError_t e = launch_k(k_embed_pos_grad, dim3(S), dim3(128), 0, st,
+                               static_cast<const bf16*>(dsum), B, S, H, dpos))
+    return e;
+  for (int j = 0; j < n_types; ++j)
+    if (cudaError_t e = colsum(dsum, T, H, types, j, dtype + int64_t(j) * H, ws, 0, st)) return e;
+  return cudaGetLastError();
+}
+
+cudaError_t span_head_fwd(const void* h, const float* w, const float* bias, const int32_t* label,
+                          float* logits, float* dlogits, float* row_loss, float* loss, int B,
+                          int S, int H, cudaStream_t st) {
+  if (!xf_width_ok(H) || H / 256 > 4) return cudaErrorInvalidValue;
+  const size_t smem = size_t(S) * 2 * sizeof(float);
+  DELTA_NV_SWITCH(H, if (cudaError_t e = launch_k(k_span_head_fwd<NV>, dim3(B), dim3(256), smem,
+                                                  st, static_cast<const bf16*>(h), w, bias, label,
+                                                  S, B, logits, dlogits, row_loss)) return e);
+  if (cudaError_t e = launch_k(k_mean_loss, dim3(1), dim3(32), 0, st,
+                               static_cast<const float*>(row_loss), B, loss))
+    return e;
+  return cudaGetLastError();
+}
+
+int64_t span_head_workspace_floats(int64_t T, int H) { return int64_t(2 * sms()) * 2 * H; }
+
+cudaError_t span_head_bwd(const void* h, const float* dlogits, const float* w, void* dh, float* dw,
+                          float* dbias, float* ws, int64_t T, int H, cudaStream_t st) {
+  if (!xf_width_ok(H) || H / 256 > 4) return cudaErrorInvalidValue;
+  const int parts = ln_bwd_parts(T);
+  const int64_t chunk = (T + parts - 1) / parts;
+  DELTA_NV_SWITCH(H, if (cudaError_t e = launch_k(k_span_head_bwd<NV>, dim3(parts), dim3(256), 0,
+                                                  st, static_cast<const bf16*>(h), dlogits, w,
+                                                  static_cast<bf16*>(dh), ws, T, chunk)) return e);
+  if (cudaError_t e = launch_k(k_rows_merge2, dim3((H + 255) / 256), dim3(256), 0, st,
+                               static_cast<const float*>(ws), parts, H, dw, dw + H))
+    return e;
+  if (cudaError_t e = launch_k(k_span_dbias, dim3(1), dim3(64), 0, st, dlogits, T, dbias))
+    return e;
+  return cudaGetLastError();
+}
+
+cudaError_t attn_dvec(const void* o, const void* dout, int64_t T, int S, int heads, float* D,
+                      cudaStream_t st) {
+  if (cudaError_t e = launch_k(k_attn_dvec, dim3(unsigned((T + 7) / 8)), dim3(256), 0, st,
+                               static_cast<const bf16*>(o), static_cast<const bf16*>(dout), T, S,
+                               heads, D))
+    return e;
+  return cudaGetLastError();
+}
+
+cudaError_t adamw_step(float* w, float* m, float* v, const float* g, void* wbf, int64_t n,
+                       int64_t n_bf, float lr, float b1, float b2, float eps, float wd,
+                       uint64_t* rng, cudaStream_t st) {
+  if (cudaError_t e = launch_k(k_adamw, dim3(grid_for(n, 256)), dim3(256), 0, st, w, m, v, g,
+                               static_cast<bf16*>(wbf), n, n_bf, lr, b1, b2, eps, wd,
+                               static_cast<const uint64_t*>(rng)))
+    return e;
+  if (cudaError_t e = launch_k(k_rng_advance, dim3(1), dim3(32), 0, st, rng)) return e;
+  return cudaGetLastError();
+}
+
+}  // namespace delta_k

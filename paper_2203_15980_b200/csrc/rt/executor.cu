@@ -19,6 +19,7 @@
 #include <vector>
 
 #include "delta/delta_rt.h"
+#include "kernels/xformer.hpp"
 #include "kernels/kernels.hpp"
 #include "rt/handles.hpp"
 
@@ -212,6 +213,64 @@ delta_status run_kop(delta_rt* rt, const delta_kop& k, Frame& fr, uint64_t node,
                          rp<float>(fr, r[3]), st);
       break;
     }
+    case DELTA_K_LAYERNORM:
+      e = delta_k::layernorm_fwd(ref(fr, r[0]), ref(fr, r[1]), rp<float>(fr, r[2]), rp<float>(fr, r[3]),
+                                 rp<const float>(fr, r[4]), rp<const float>(fr, r[5]), i[0],
+                                 int(i[1]), k.f[0], st);
+      break;
+    case DELTA_K_LAYERNORM_BWD:
+      e = delta_k::layernorm_bwd(ref(fr, r[0]), ref(fr, r[1]), ref(fr, r[2]), ref(fr, r[3]),
+                                 rp<const float>(fr, r[4]), rp<const float>(fr, r[5]),
+                                 rp<const float>(fr, r[6]), rp<float>(fr, r[7]), rp<float>(fr, r[8]),
+                                 rp<float>(fr, r[9]), i[0], int(i[1]), st);
+      break;
+    case DELTA_K_GELU:
+      e = delta_k::gelu_fwd(ref(fr, r[0]), ref(fr, r[1]), i[0], st);
+      break;
+    case DELTA_K_ADD_DROPOUT:
+      e = delta_k::add_dropout(ref(fr, r[0]), ref(fr, r[1]), ref(fr, r[2]), i[0], k.f[0],
+                               rp<const uint64_t>(fr, r[3]), uint32_t(i[1]), st);
+      break;
+    case DELTA_K_DROPOUT_BWD:
+      e = delta_k::dropout_bwd(ref(fr, r[0]), ref(fr, r[1]), i[0], k.f[0],
+                               rp<const uint64_t>(fr, r[2]), uint32_t(i[1]), st);
+      break;
+    case DELTA_K_COLSUM:
+      e = delta_k::colsum(ref(fr, r[0]), i[0], int(i[1]), rp<const int32_t>(fr, r[1]), int(i[2]),
+                          rp<float>(fr, r[2]), rp<float>(fr, r[3]), int(i[3]), st);
+      break;
+    case DELTA_K_EMBED:
+      e = delta_k::embed_fwd(rp<const int32_t>(fr, r[0]), rp<const int32_t>(fr, r[1]), ref(fr, r[2]),
+                             ref(fr, r[3]), ref(fr, r[4]), ref(fr, r[5]), int(i[0]), int(i[1]),
+                             int(i[2]), k.f[0], rp<const uint64_t>(fr, r[6]), uint32_t(i[3]), st);
+      break;
+    case DELTA_K_EMBED_GRADS:
+      e = delta_k::embed_grads(ref(fr, r[0]), rp<const int32_t>(fr, r[1]), rp<const int32_t>(fr, r[2]),
+                               int(i[0]), int(i[1]), int(i[2]), int(i[3] & 0xFFFFFFFF),
+                               int(i[3] >> 32), rp<float>(fr, r[3]), rp<float>(fr, r[4]),
+                               rp<float>(fr, r[5]), rp<float>(fr, r[6]), st);
+      break;
+    case DELTA_K_SPAN_HEAD:
+      e = delta_k::span_head_fwd(ref(fr, r[0]), rp<const float>(fr, r[1]), rp<const float>(fr, r[2]),
+                                 rp<const int32_t>(fr, r[3]), rp<float>(fr, r[4]), rp<float>(fr, r[5]),
+                                 rp<float>(fr, r[6]), rp<float>(fr, r[7]), int(i[0]), int(i[1]),
+                                 int(i[2]), st);
+      break;
+    case DELTA_K_SPAN_HEAD_BWD:
+      e = delta_k::span_head_bwd(ref(fr, r[0]), rp<const float>(fr, r[1]), rp<const float>(fr, r[2]),
+                                 ref(fr, r[3]), rp<float>(fr, r[4]), rp<float>(fr, r[5]),
+                                 rp<float>(fr, r[6]), i[0], int(i[1]), st);
+      break;
+    case DELTA_K_ATTN:
+      e = delta_k::attention_fwd(ref(fr, r[0]), ref(fr, r[1]), rp<float>(fr, r[2]), int(i[0]),
+                                 int(i[1]), int(i[2]), k.f[0], rp<const uint64_t>(fr, r[3]),
+                                 uint32_t(i[3]), st);
+      break;
+    case DELTA_K_ATTN_BWD:
+      e = delta_k::attention_bwd(ref(fr, r[0]), ref(fr, r[1]), ref(fr, r[2]), rp<const float>(fr, r[3]),
+                                 rp<float>(fr, r[4]), ref(fr, r[5]), int(i[0]), int(i[1]), int(i[2]),
+                                 k.f[0], rp<const uint64_t>(fr, r[6]), uint32_t(i[3]), st);
+      break;
     case DELTA_K_HOST: {
       if (!rt->host_fn) return fail(DELTA_E_ARGUMENT, "recipe: HOST op without a host callback");
       std::vector<uint64_t> ins(fr.n_in);

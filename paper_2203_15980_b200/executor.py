@@ -22,6 +22,8 @@ REF_PTR, REF_OUT, REF_IN, REF_SCRATCH = 0, 1, 2, 3
 (K_COPY, K_CONV, K_CONV_EX, K_BN_STATS, K_BN_STATS_PARTS, K_BN_APPLY, K_BN_BWD, K_BN_BWD_PARTS,
  K_ADD_GRAD, K_MAXPOOL_FWD, K_MAXPOOL_BWD, K_AVGPOOL, K_SOFTMAX_XENT, K_HOST, K_WGRAD,
  K_XENT_HEAD) = range(1, 17)
+(K_LAYERNORM, K_LAYERNORM_BWD, K_GELU, K_ADD_DROPOUT, K_DROPOUT_BWD, K_COLSUM, K_EMBED,
+ K_EMBED_GRADS, K_SPAN_HEAD, K_SPAN_HEAD_BWD, K_ATTN, K_ATTN_BWD) = range(17, 29)
 FIRST_ONLY, RECOMPUTE_ONLY, SIDE = 1, 2, 4
 
 

@@ -66,7 +66,7 @@ def _count(n: int):
     LAUNCHES[0] += n
 
 
-EPI_STORE, EPI_ADD_MASK, EPI_BN_BWD, EPI_SCATTER2 = 0, 1, 2, 3
+EPI_STORE, EPI_ADD_MASK, EPI_BN_BWD, EPI_SCATTER2, EPI_BIAS, EPI_GELU_BWD = 0, 1, 2, 3, 4, 5
 
 
 class ConvEpilogue(C.Structure):
@@ -117,6 +117,18 @@ class Conv:
         """parity class `cls` = 2a + b of a stride-2 input gradient: output
         (p, q) written to y[n][2p+a][2q+b] of the [N][2P][2Q][K] tensor."""
         e = ConvEpilogue(EPI_SCATTER2, 0, 0, cls, None, None, None, None, None, None, None, None)
+        check(lib.delta_conv_forward_ex(self._h, x_ptr, y_ptr, None, C.byref(e), stream))
+        _count(1)
+
+    def bias(self, x_ptr, y_ptr, bias_ptr, stream):
+        """linear layer: y = bf16(x W^T + bias) (1x1 over [rows][in])"""
+        e = ConvEpilogue(EPI_BIAS, 0, 0, 0, None, None, None, None, None, None, None, bias_ptr)
+        check(lib.delta_conv_forward_ex(self._h, x_ptr, y_ptr, None, C.byref(e), stream))
+        _count(1)
+
+    def gelu_bwd(self, x_ptr, y_ptr, pre_ptr, stream):
+        """y = bf16(conv(x) * gelu'(pre)): an MLP input gradient through the GELU"""
+        e = ConvEpilogue(EPI_GELU_BWD, 0, 0, 0, None, None, None, pre_ptr, None, None, None, None)
         check(lib.delta_conv_forward_ex(self._h, x_ptr, y_ptr, None, C.byref(e), stream))
         _count(1)
 
@@ -333,3 +345,109 @@ def probe_link(nbytes: int = 256 << 20, iters: int = 8):
     a, b, c = C.c_double(), C.c_double(), C.c_double()
     check(lib.delta_probe_link(nbytes, iters, C.byref(a), C.byref(b), C.byref(c)))
     return a.value, b.value, c.value
+
+
+# ---------------------------------------------------------------- transformer
+# (include/delta/delta_xformer.h)
+_XSIGS = {
+    "delta_layernorm_fwd": (i32, [vp, vp, vp, vp, vp, vp, i64, i32, f32, vp]),
+    "delta_layernorm_bwd_workspace_floats": (i64, [i64, i32]),
+    "delta_layernorm_bwd": (i32, [vp] * 10 + [i64, i32, vp]),
+    "delta_gelu_fwd": (i32, [vp, vp, i64, vp]),
+    "delta_add_dropout": (i32, [vp, vp, vp, i64, f32, vp, u32, vp]),
+    "delta_dropout_bwd": (i32, [vp, vp, i64, f32, vp, u32, vp]),
+    "delta_colsum_workspace_floats": (i64, [i64, i32]),
+    "delta_colsum": (i32, [vp, i64, i32, vp, i32, vp, vp, i32, vp]),
+    "delta_embed_fwd": (i32, [vp, vp, vp, vp, vp, vp, i32, i32, i32, f32, vp, u32, vp]),
+    "delta_embed_grads": (i32, [vp, vp, vp, i32, i32, i32, i32, i32, vp, vp, vp, vp, vp]),
+    "delta_span_head_fwd": (i32, [vp] * 8 + [i32, i32, i32, vp]),
+    "delta_span_head_workspace_floats": (i64, [i64, i32]),
+    "delta_span_head_bwd": (i32, [vp] * 7 + [i64, i32, vp]),
+    "delta_attention_fwd": (i32, [vp, vp, vp, i32, i32, i32, f32, vp, u32, vp]),
+    "delta_attention_bwd": (i32, [vp] * 6 + [i32, i32, i32, f32, vp, u32, vp]),
+    "delta_adamw_step": (i32, [vp] * 5 + [i64, i64, f32, f32, f32, f32, f32, vp, vp]),
+}
+for _n, (_r, _a) in _XSIGS.items():
+    _f = getattr(lib, _n)
+    _f.restype = _r
+    _f.argtypes = _a
+
+
+def layernorm_fwd(x, y, mean, rstd, gamma, beta, rows, H, eps, stream):
+    check(lib.delta_layernorm_fwd(x, y, mean, rstd, gamma, beta, rows, H, eps, stream))
+    _count(1)
+
+
+def layernorm_bwd_workspace_floats(rows, H) -> int:
+    return int(lib.delta_layernorm_bwd_workspace_floats(rows, H))
+
+
+def layernorm_bwd(dy, x, dres, dx, mean, rstd, gamma, dgamma, dbeta, ws, rows, H, stream):
+    check(lib.delta_layernorm_bwd(dy, x, dres, dx, mean, rstd, gamma, dgamma, dbeta, ws, rows, H,
+                                  stream))
+    _count(2)
+
+
+def gelu_fwd(x, y, n, stream):
+    check(lib.delta_gelu_fwd(x, y, n, stream))
+    _count(1)
+
+
+def add_dropout(a, b, y, n, p, rng, tag, stream):
+    check(lib.delta_add_dropout(a, b, y, n, p, rng, tag, stream))
+    _count(1)
+
+
+def dropout_bwd(dy, dx, n, p, rng, tag, stream):
+    check(lib.delta_dropout_bwd(dy, dx, n, p, rng, tag, stream))
+    _count(1)
+
+
+def colsum_workspace_floats(rows, cols) -> int:
+    return int(lib.delta_colsum_workspace_floats(rows, cols))
+
+
+def colsum(x, rows, cols, out, ws, stream, sel=None, sel_val=0, accumulate=False):
+    check(lib.delta_colsum(x, rows, cols, sel, sel_val, out, ws, int(accumulate), stream))
+    _count(2)
+
+
+def embed_fwd(ids, types, word, pos, type_, y, B, S, H, p, rng, tag, stream):
+    check(lib.delta_embed_fwd(ids, types, word, pos, type_, y, B, S, H, p, rng, tag, stream))
+    _count(1)
+
+
+def embed_grads(dsum, csr, types, B, S, H, vocab, n_types, dword, dpos, dtype, ws, stream):
+    check(lib.delta_embed_grads(dsum, csr, types, B, S, H, vocab, n_types, dword, dpos, dtype, ws,
+                                stream))
+    _count(2 + 2 * n_types)
+
+
+def span_head_fwd(h, w, bias, label, logits, dlogits, row_loss, loss, B, S, H, stream):
+    check(lib.delta_span_head_fwd(h, w, bias, label, logits, dlogits, row_loss, loss, B, S, H,
+                                  stream))
+    _count(2)
+
+
+def span_head_workspace_floats(T, H) -> int:
+    return int(lib.delta_span_head_workspace_floats(T, H))
+
+
+def span_head_bwd(h, dlogits, w, dh, dw, dbias, ws, T, H, stream):
+    check(lib.delta_span_head_bwd(h, dlogits, w, dh, dw, dbias, ws, T, H, stream))
+    _count(3)
+
+
+def attention_fwd(qkv, out, lse, B, S, heads, p, rng, tag, stream):
+    check(lib.delta_attention_fwd(qkv, out, lse, B, S, heads, p, rng, tag, stream))
+    _count(1)
+
+
+def attention_bwd(qkv, out, dout, lse, D, dqkv, B, S, heads, p, rng, tag, stream):
+    check(lib.delta_attention_bwd(qkv, out, dout, lse, D, dqkv, B, S, heads, p, rng, tag, stream))
+    _count(3)
+
+
+def adamw_step(w, m, v, g, wbf, n, n_bf, lr, b1, b2, eps, wd, rng, stream):
+    check(lib.delta_adamw_step(w, m, v, g, wbf, n, n_bf, lr, b1, b2, eps, wd, rng, stream))
+    _count(2)

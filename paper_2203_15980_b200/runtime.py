@@ -717,7 +717,15 @@ class DeltaRuntime:
         K._count(self.executor.launches_per_step)
         if self.dp is not None:
             self._allreduce_buckets()
+        self._optimizer_step()
+
+    def _optimizer_step(self):
         self.params.sgd_step(self.lr)
+
+    def _slot_tensors(self, slot: int) -> list:
+        """the device tensors one staged batch occupies (same order as the
+        host tuple a batch is given as)"""
+        return [self.x_slots[slot], self.y_slots[slot]]
 
     def _allreduce_buckets(self):
         """Data parallel: one DELTA instance per GPU; the flat
@@ -807,9 +815,12 @@ class DeltaRuntime:
     def step(self, x_host: torch.Tensor, y_host: torch.Tensor) -> float:
         """One synchronous step through the public API with HOST buffers:
         H2D of the batch, the step, D2H of the loss."""
+        return self._step_host((x_host, y_host))
+
+    def _step_host(self, batch) -> float:
         with torch.cuda.stream(self.stream):
-            self.x_dev.copy_(x_host, non_blocking=True)
-            self.y_dev.copy_(y_host, non_blocking=True)
+            for dst, src in zip(self._slot_tensors(self._slot), batch):
+                dst.copy_(src, non_blocking=True)
         self.step_device()
         with torch.cuda.stream(self.stream):
             loss = self.loss.to("cpu", non_blocking=False)
@@ -837,8 +848,8 @@ class DeltaRuntime:
             with torch.cuda.stream(self._h2d):
                 if i >= 2:
                     self._h2d.wait_event(ev_done[slot])  # step i-2 read this slot
-                self.x_slots[slot].copy_(batches[i][0], non_blocking=True)
-                self.y_slots[slot].copy_(batches[i][1], non_blocking=True)
+                for dst, src in zip(self._slot_tensors(slot), batches[i]):
+                    dst.copy_(src, non_blocking=True)
                 ev_in[slot].record(self._h2d)
 
         h2d(0)

@@ -199,7 +199,7 @@ def test_live_reference_fuzz():
 # ------------------------------------------------------------- C ABI surface
 def test_c_abi_exports_every_declared_symbol():
     names = set()
-    for h in ("delta.h", "delta_kernels.h", "delta_rt.h"):
+    for h in ("delta.h", "delta_kernels.h", "delta_rt.h", "delta_xformer.h"):
         text = open(os.path.join(ROOT, "include", "delta", h)).read()
         names |= set(re.findall(r"^[\w ]*?[\w\*]+\s+\**(delta_[a-z0-9_]+)\s*\(", text, re.M))
     assert len(names) > 60
