@@ -9,7 +9,7 @@ import pytest
 import torch
 import torch.nn.functional as F
 
-from tests import xf_ref as R
+import xf_ref as R  # noqa: E402  (tests/ is on sys.path via conftest)
 
 pytestmark = pytest.mark.gpu
 
