@@ -3,26 +3,28 @@
 // backward, with attention-probability dropout whose mask is replayed
 // (philox.cuh), so a recomputed Attention output is bit-identical.
 //
-// BERT shapes: head dim 64, sequence S <= 512 (a multiple of 128).  One CTA
-// owns one 128-row tile of one (sequence, head) and keeps the WHOLE key range
-// on chip — no online-softmax rescaling:
+// BERT shapes: head dim 64, sequence S <= 512 (a multiple of 128); all keys
+// of a (sequence, head) stay on chip, so there is no online-softmax
+// rescaling and no atomics anywhere (deterministic gradients).
 //
-// forward (grid S/128 x heads x B): S = Q K^T for all S keys in TMEM (S <= 512
-//   fp32 columns = the SM's whole TMEM); 8 softmax warps (two per TMEM lane
-//   quarter, each half of the keys) take the row max, then write
-//   P = exp2(s*c - m*c) * keep (bf16, unnormalised) to shared memory in the
-//   K-major SW128 layout the tensor core reads; K's buffer is refilled with V
-//   meanwhile; O = P V (B operand V MN-major) lands in TMEM columns 0-63 and is
-//   scaled by dropout_scale / rowsum on the way out.  lse (log2 units) saved.
-// backward: two roles of one kernel, both recomputing S and dP = dO V^T per
-//   128 x 128 block (thread = one query row, the saved lse and D = rowsum(dO*O)
-//   in registers): dS = P (dP*keep*scale - D);
-//   ROLE_DQ  (tile = 128 queries, loop over key blocks):  dQ += dS K
-//   ROLE_DKV (tile = 128 keys, loop over query blocks):   dV += (P*keep*scale)^T dO,
-//                                                          dK += dS^T Q
-//   (the transposed products read the same [query][key] smem tiles through
-//   MN-major descriptors).  No atomics: every output element is written once,
-//   so gradients are deterministic.
+// forward (grid S/128 x heads x B, one CTA per 128 query rows): S = Q K^T for
+//   all S keys in TMEM (S <= 512 fp32 columns = the SM's whole TMEM); 16
+//   softmax warps (four per TMEM lane quarter, a quarter of the keys each)
+//   take the row max, then write P = exp2(s*c - m*c) * keep (bf16,
+//   unnormalised) to shared memory in the K-major SW128 layout the tensor core
+//   reads, while K's buffer is refilled with V; O = P V (V as an MN-major B
+//   operand) lands in TMEM columns 0-63 and is scaled by
+//   dropout_scale / rowsum on the way out.  lse (log2 units) saved.
+// backward (grid heads x B, one CTA per (sequence, head)): for every key
+//   block j (128 keys, K_j / V_j loaded by TMA) and query block i
+//   (Q, dO of the whole sequence resident): S_ij = Q_i K_j^T and
+//   dPd_ij = dO_i V_j^T in two 64-key halves (TMEM 384-511), the softmax
+//   warps form P = exp2(s*c - lse), Pd = P*keep*scale and
+//   dS = P (dPd*keep*scale - D) into shared memory, then
+//     dV_j += Pd^T dO_i,  dK_j += dS^T Q_i   (TMEM 320 / 256, drained per j)
+//     dQ_i += dS K_j                         (TMEM 64*i, drained at the end)
+//   the transposed products read the [query][key] tiles through MN-major
+//   descriptors.  Every softmax term is computed once.
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
@@ -45,8 +47,9 @@ using bf16 = __nv_bfloat16;
 constexpr int HD = 64;            // head dim
 constexpr int TILE = 128;         // rows per tile
 constexpr uint32_t TILE_BYTES = TILE * 128;  // a [128][64] bf16 SW128 tile
-constexpr int kThreads = 9 * 32;  // 8 math warps + 1 control warp
-constexpr int CTRL = 8;
+constexpr int MATH_W = 16;        // softmax warps: 4 per TMEM lane quarter
+constexpr int CTRL = MATH_W;      // TMA / MMA / TMEM warp
+constexpr int kThreads = (MATH_W + 1) * 32;
 constexpr float kScale = 0.125f;                              // 1/sqrt(64)
 constexpr float kCl2 = 0.125f * 1.4426950408889634f;          // scale * log2(e)
 
@@ -72,17 +75,63 @@ __device__ __forceinline__ uint8_t* align1024(uint8_t* p) {
   return reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(p) + 1023) & ~uintptr_t(1023));
 }
 
-__device__ __forceinline__ void bar_math() { asm volatile("bar.sync 1, 256;" ::: "memory"); }
+__device__ __forceinline__ void bar_math() {
+  asm volatile("bar.sync 1, %0;" ::"n"(MATH_W * 32) : "memory");
+}
 
-// 32 consecutive bf16 of row r at key column `col` (multiple of 32) of a
-// [128][ncols] K-major SW128 tile set (64-column atoms of 16 KB)
-__device__ __forceinline__ void st_row32(uint32_t base, int r, int col, const uint32_t* w) {
+// tcgen05.ld of 16 consecutive fp32 columns of this warp's 32 lanes, without
+// the wait (issue several, then tmem_wait once)
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+        "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_wait() {
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
+// keep masks of one Philox block (16 elements): byte i of v[w] = 0xFF iff
+// element 4w + i is kept (all kept when thr == 0)
+__device__ __forceinline__ uint4 keep_bytes(uint64_t seed, uint64_t step, uint32_t tag, uint64_t g,
+                                            uint32_t thr) {
+  if (!thr) return make_uint4(~0u, ~0u, ~0u, ~0u);
+  const uint4 w = drop_block(seed, step, tag, g);
+  const uint32_t t4 = thr * 0x01010101u;
+  return make_uint4(__vcmpgeu4(w.x, t4), __vcmpgeu4(w.y, t4), __vcmpgeu4(w.z, t4),
+                    __vcmpgeu4(w.w, t4));
+}
+// 16-bit lane masks of elements (2j, 2j+1) of a 4-byte keep word
+__device__ __forceinline__ uint32_t pair_mask(uint32_t kb, int j) {
+  return __byte_perm(kb, 0, j ? 0x3322 : 0x1100);
+}
+// fp32 all-ones / zero mask of element i of a 4-byte keep word
+__device__ __forceinline__ uint32_t elem_mask(uint32_t kb, int i) {
+  return __byte_perm(kb, 0, 0x1111u * uint32_t(i));
+}
+
+// 16 bf16 (two 16-byte chunks) of row r at key column `col` (a multiple of
+// 16) of a [128][ncols] K-major SW128 tile set (64-column atoms of 16 KB)
+__device__ __forceinline__ void st_row16(uint32_t base, int r, int col, const uint32_t* w) {
   const uint32_t atom = base + uint32_t(col >> 6) * TILE_BYTES + uint32_t(r) * 128;
   const int u0 = (col & 63) >> 3;
 #pragma unroll
-  for (int u = 0; u < 4; ++u)
+  for (int u = 0; u < 2; ++u)
     st_shared_v4(atom + ((uint32_t((u0 + u) ^ (r & 7))) << 4),
                  make_uint4(w[4 * u], w[4 * u + 1], w[4 * u + 2], w[4 * u + 3]));
+}
+
+__device__ __forceinline__ void store16(bf16* dst, const uint32_t (&v)[16], float s) {
+  uint4* d = reinterpret_cast<uint4*>(dst);
+#pragma unroll
+  for (int u = 0; u < 2; ++u)
+    d[u] = make_uint4(pack_bf16x2(__uint_as_float(v[8 * u]) * s, __uint_as_float(v[8 * u + 1]) * s),
+                      pack_bf16x2(__uint_as_float(v[8 * u + 2]) * s, __uint_as_float(v[8 * u + 3]) * s),
+                      pack_bf16x2(__uint_as_float(v[8 * u + 4]) * s, __uint_as_float(v[8 * u + 5]) * s),
+                      pack_bf16x2(__uint_as_float(v[8 * u + 6]) * s, __uint_as_float(v[8 * u + 7]) * s));
 }
 
 struct AttnArgs {
@@ -107,7 +156,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   const uint32_t sKV = sQ + TILE_BYTES;
   const uint32_t sP = sKV + uint32_t(S) * 128;
   float* red = reinterpret_cast<float*>(smem + TILE_BYTES + size_t(S) * 128 + size_t(S) * 256);
-  uint64_t* bars = reinterpret_cast<uint64_t*>(red + 4 * TILE);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(red + 8 * TILE);
   uint64_t* bar_qk = bars;
   uint64_t* bar_v = bars + 1;
   uint64_t* bar_s = bars + 2;
@@ -122,7 +171,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     mbar_init(bar_qk, 1);
     mbar_init(bar_v, 1);
     mbar_init(bar_s, 1);
-    mbar_init(bar_p, 8);
+    mbar_init(bar_p, MATH_W);
     mbar_init(bar_o, 1);
     fence_mbar_init();
     tma_prefetch_desc(&qkv_map);
@@ -180,69 +229,70 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     __syncwarp();
   } else {
-    // ---- softmax warps: row r of the tile, keys [half*S/2, (half+1)*S/2) ----
-    const int quarter = warp & 3, half = warp >> 2;
+    // ---- softmax warps: row r of the tile, keys [part*S/4, (part+1)*S/4) ----
+    const int quarter = warp & 3, part = warp >> 2;
     const int r = quarter * 32 + lane;
     const int q = qt * TILE + r;
     const uint32_t trow = tmem + (uint32_t(quarter * 32) << 16);
-    const int hs = S / 2, nch = hs / 32;
+    const int ps = S / 4, nch = ps / 16;  // 16-column chunks of this warp
+    const int c0 = part * ps;
     mbar_wait(bar_s, 0);
     tc_fence_after();
     float m = -INFINITY;
-    for (int c = 0; c < nch; ++c) {
-      float v[32];
-      tmem_ld_32x32b_x32(trow + half * hs + c * 32, v);
+    {
+      uint32_t v0[16], v1[16];
+      for (int c = 0; c < nch; c += 2) {
+        tmem_ld16(trow + c0 + c * 16, v0);
+        tmem_ld16(trow + c0 + c * 16 + 16, v1);
+        tmem_wait();
 #pragma unroll
-      for (int i = 0; i < 32; ++i) m = fmaxf(m, v[i]);
+        for (int i = 0; i < 16; ++i) m = fmaxf(m, fmaxf(__uint_as_float(v0[i]), __uint_as_float(v1[i])));
+      }
     }
-    red[half * TILE + r] = m;
+    red[part * TILE + r] = m;
     bar_math();
-    m = fmaxf(red[r], red[TILE + r]);
+    m = fmaxf(fmaxf(red[r], red[TILE + r]), fmaxf(red[2 * TILE + r], red[3 * TILE + r]));
     const float mc = m * kCl2;
     const uint64_t seed = a.rng[0], step = a.rng[1];
-    const uint64_t erow = (uint64_t(b * a.heads + h) * S + q) * uint64_t(S);
+    const uint64_t g0 = ((uint64_t(b * a.heads + h) * S + q) * uint64_t(S) + c0) >> 4;
     float l = 0.f;
-    for (int c = 0; c < nch; ++c) {
-      float v[32];
-      const int col = half * hs + c * 32;
-      tmem_ld_32x32b_x32(trow + col, v);
-      uint32_t keep = 0xFFFFFFFFu;
-      if (a.thr) {
-        const uint64_t g = (erow + col) >> 4;
-        keep = keep16(drop_block(seed, step, a.tag, g), a.thr) |
-               (keep16(drop_block(seed, step, a.tag, g + 1), a.thr) << 16);
-      }
-      uint32_t w[16];
+    for (int c = 0; c < nch; c += 2) {
+      uint32_t v[2][16];
+      tmem_ld16(trow + c0 + c * 16, v[0]);
+      tmem_ld16(trow + c0 + c * 16 + 16, v[1]);
+      const uint4 kb0 = keep_bytes(seed, step, a.tag, g0 + c, a.thr);
+      const uint4 kb1 = keep_bytes(seed, step, a.tag, g0 + c + 1, a.thr);
+      tmem_wait();
 #pragma unroll
-      for (int i = 0; i < 32; i += 2) {
-        const float p0 = ex2(fmaf(v[i], kCl2, -mc));
-        const float p1 = ex2(fmaf(v[i + 1], kCl2, -mc));
-        l += p0 + p1;
-        w[i >> 1] = pack_bf16x2((keep >> i) & 1u ? p0 : 0.f, (keep >> (i + 1)) & 1u ? p1 : 0.f);
+      for (int hh = 0; hh < 2; ++hh) {
+        const uint4 kb = hh ? kb1 : kb0;
+        uint32_t w[8];
+#pragma unroll
+        for (int i = 0; i < 16; i += 2) {
+          const float p0 = ex2(fmaf(__uint_as_float(v[hh][i]), kCl2, -mc));
+          const float p1 = ex2(fmaf(__uint_as_float(v[hh][i + 1]), kCl2, -mc));
+          l += p0 + p1;
+          w[i >> 1] = pack_bf16x2(p0, p1) & pair_mask((&kb.x)[i >> 2], (i >> 1) & 1);
+        }
+        st_row16(sP, r, c0 + (c + hh) * 16, w);
       }
-      st_row32(sP, r, col, w);
     }
-    red[2 * TILE + half * TILE + r] = l;
+    red[4 * TILE + part * TILE + r] = l;
     fence_proxy_async_smem();
     tc_fence_before();
     bar_math();
-    l = red[2 * TILE + r] + red[3 * TILE + r];
-    if (half == 0) a.lse[uint64_t(b * a.heads + h) * S + q] = mc + __log2f(l);
+    l = (red[4 * TILE + r] + red[5 * TILE + r]) + (red[6 * TILE + r] + red[7 * TILE + r]);
+    if (part == 0) a.lse[uint64_t(b * a.heads + h) * S + q] = mc + __log2f(l);
     __syncwarp();
     if (lane == 0) mbar_arrive(bar_p);
     const float inv = a.dscale / l;
-    // ---- epilogue: O columns [half*32, half*32+32) of row r ----
+    // ---- epilogue: O columns [part*16, part*16+16) of row r ----
     mbar_wait(bar_o, 0);
     tc_fence_after();
-    float v[32];
-    tmem_ld_32x32b_x32(trow + half * 32, v);
-    uint4* dst = reinterpret_cast<uint4*>(a.out + (int64_t(row0) + q) * a.Hd + h * HD + half * 32);
-#pragma unroll
-    for (int u = 0; u < 4; ++u)
-      dst[u] = make_uint4(pack_bf16x2(v[8 * u] * inv, v[8 * u + 1] * inv),
-                          pack_bf16x2(v[8 * u + 2] * inv, v[8 * u + 3] * inv),
-                          pack_bf16x2(v[8 * u + 4] * inv, v[8 * u + 5] * inv),
-                          pack_bf16x2(v[8 * u + 6] * inv, v[8 * u + 7] * inv));
+    uint32_t v[16];
+    tmem_ld16(trow + part * 16, v);
+    tmem_wait();
+    store16(a.out + (int64_t(row0) + q) * a.Hd + h * HD + part * 16, v, inv);
   }
   tc_fence_before();
   __syncthreads();
@@ -251,9 +301,9 @@ __global__ void __launch_bounds__(kThreads, 1)
 }
 
 // ======================================================================= bwd
-constexpr int ROLE_DQ = 0, ROLE_DKV = 1;
+// TMEM columns
+constexpr uint32_t T_DK = 256, T_DV = 320, T_S = 384, T_DP = 448;
 
-template <int ROLE>
 __global__ void __launch_bounds__(kThreads, 1)
     k_attn_bwd(const __grid_constant__ CUtensorMap qkv_map, const __grid_constant__ CUtensorMap do_map,
                const AttnArgs a) {
@@ -261,30 +311,30 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint8_t* smem = align1024(smem_raw);
   const int S = a.S;
   const int nt = S / TILE;
-  // ROLE_DQ : sA0 = Q_i, sA1 = dO_i, sB0 = K (all), sB1 = V (all)
-  // ROLE_DKV: sA0 = K_j, sA1 = V_j,  sB0 = Q (all), sB1 = dO (all)
-  const uint32_t sA0 = smem_u32(smem);
-  const uint32_t sA1 = sA0 + TILE_BYTES;
-  const uint32_t sB0 = sA1 + TILE_BYTES;
-  const uint32_t sB1 = sB0 + uint32_t(S) * 128;
-  const uint32_t sDS = sB1 + uint32_t(S) * 128;  // dS [128 q][128 keys]
-  const uint32_t sPD = sDS + 2 * TILE_BYTES;     // ROLE_DKV: P*keep*scale, same layout
-  const uint32_t used = 2 * TILE_BYTES + 2 * uint32_t(S) * 128 + (ROLE == ROLE_DKV ? 4 : 2) * TILE_BYTES;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + used);
-  uint64_t* bar_ld = bars;
-  uint64_t* bar_sp = bars + 1;
-  uint64_t* bar_ds = bars + 2;
-  uint64_t* bar_acc = bars + 3;
-  uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 4);
+  const uint32_t sQ = smem_u32(smem);                  // [S][64] Q of the sequence
+  const uint32_t sDO = sQ + uint32_t(S) * 128;         // [S][64] dO
+  const uint32_t sKV = sDO + uint32_t(S) * 128;        // K_j, V_j
+  const uint32_t sP = sKV + 2 * TILE_BYTES;            // Pd [128 q][128 keys]
+  const uint32_t sDS = sP + 2 * TILE_BYTES;            // dS [128 q][128 keys]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + 2 * size_t(S) * 128 + 6 * TILE_BYTES);
+  uint64_t* bar_qd = bars;       // Q, dO landed
+  uint64_t* bar_kv = bars + 1;   // K_j / V_j landed
+  uint64_t* bar_sp = bars + 3;   // S/dP half computed
+  uint64_t* bar_h = bars + 4;    // half consumed (TMEM read, smem written)
+  uint64_t* bar_acc = bars + 5;  // accumulate MMAs of a block done
+  uint64_t* bar_dr = bars + 6;   // dK/dV of a key block drained
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 7);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int tile = blockIdx.x, h = blockIdx.y, b = blockIdx.z;
+  const int h = blockIdx.x, b = blockIdx.y;
   const int row0 = b * S;
 
   if (threadIdx.x == 0) {
-    mbar_init(bar_ld, 1);
+    mbar_init(bar_qd, 1);
+    mbar_init(bar_kv, 1);
     mbar_init(bar_sp, 1);
-    mbar_init(bar_ds, 8);
+    mbar_init(bar_h, MATH_W);
     mbar_init(bar_acc, 1);
+    mbar_init(bar_dr, MATH_W);
     fence_mbar_init();
     tma_prefetch_desc(&qkv_map);
     tma_prefetch_desc(&do_map);
@@ -296,154 +346,183 @@ __global__ void __launch_bounds__(kThreads, 1)
   const uint32_t tmem = *tslot;
   pdl_wait();
   pdl_trigger();
-  // TMEM: S [0,128), dP [128,256), acc0 (dQ | dV) [256,320), acc1 (dK) [320,384)
+  const int nblk = nt * nt;  // (j, i) blocks, j outer
   if (warp == CTRL) {
+    auto load_kv = [&](int j) {
+      mbar_arrive_expect_tx(bar_kv, 2 * TILE_BYTES);
+      tma_load_2d(sKV, &qkv_map, bar_kv, a.Hd + h * HD, row0 + j * TILE);
+      tma_load_2d(sKV + TILE_BYTES, &qkv_map, bar_kv, 2 * a.Hd + h * HD, row0 + j * TILE);
+    };
     if (lane == 0) {
-      mbar_arrive_expect_tx(bar_ld, 2 * TILE_BYTES + 2 * uint32_t(S) * 128);
-      if (ROLE == ROLE_DQ) {
-        tma_load_2d(sA0, &qkv_map, bar_ld, h * HD, row0 + tile * TILE);
-        tma_load_2d(sA1, &do_map, bar_ld, h * HD, row0 + tile * TILE);
-        for (int i = 0; i < nt; ++i) {
-          tma_load_2d(sB0 + i * TILE_BYTES, &qkv_map, bar_ld, a.Hd + h * HD, row0 + i * TILE);
-          tma_load_2d(sB1 + i * TILE_BYTES, &qkv_map, bar_ld, 2 * a.Hd + h * HD, row0 + i * TILE);
-        }
-      } else {
-        tma_load_2d(sA0, &qkv_map, bar_ld, a.Hd + h * HD, row0 + tile * TILE);
-        tma_load_2d(sA1, &qkv_map, bar_ld, 2 * a.Hd + h * HD, row0 + tile * TILE);
-        for (int i = 0; i < nt; ++i) {
-          tma_load_2d(sB0 + i * TILE_BYTES, &qkv_map, bar_ld, h * HD, row0 + i * TILE);
-          tma_load_2d(sB1 + i * TILE_BYTES, &do_map, bar_ld, h * HD, row0 + i * TILE);
-        }
+      mbar_arrive_expect_tx(bar_qd, 2 * uint32_t(S) * 128);
+      for (int i = 0; i < nt; ++i) {
+        tma_load_2d(sQ + i * TILE_BYTES, &qkv_map, bar_qd, h * HD, row0 + i * TILE);
+        tma_load_2d(sDO + i * TILE_BYTES, &do_map, bar_qd, h * HD, row0 + i * TILE);
       }
+      load_kv(0);
     }
-    mbar_wait(bar_ld, 0);
-    tc_fence_after();
-    constexpr uint32_t idS = umma_idesc_bf16(128, 128);
-    // S = Q K^T and dP = dO V^T of block `it` (rows = queries, cols = keys)
-    auto issue_sp = [&](int it) {
-      uint32_t q_, k_, do_, v_;
-      if (ROLE == ROLE_DQ) {
-        q_ = sA0; do_ = sA1; k_ = sB0 + it * TILE_BYTES; v_ = sB1 + it * TILE_BYTES;
-      } else {
-        q_ = sB0 + it * TILE_BYTES; do_ = sB1 + it * TILE_BYTES; k_ = sA0; v_ = sA1;
-      }
+    mbar_wait(bar_qd, 0);
+    constexpr uint32_t idH = umma_idesc_bf16(128, 64);                          // S / dP halves
+    constexpr uint32_t idQ = umma_idesc_bf16(128, HD) | (1u << 16);             // dQ: B MN-major
+    constexpr uint32_t idKV = umma_idesc_bf16(128, HD) | (1u << 15) | (1u << 16);  // dK, dV
+    uint32_t nsp = 0;  // S/dP halves issued
+    // S_ij, dPd_ij for keys [hh*64, hh*64+64) of block j
+    auto issue_half = [&](int blk, int hh) {
+      const int i = blk % nt;
+      const uint32_t kb = sKV;
       if (elect_one()) {
-        const uint64_t dq = umma_desc_sw128(q_), dk = umma_desc_sw128(k_);
-        const uint64_t dd = umma_desc_sw128(do_), dv = umma_desc_sw128(v_);
+        const uint64_t dq = umma_desc_sw128(sQ + i * TILE_BYTES);
+        const uint64_t dd = umma_desc_sw128(sDO + i * TILE_BYTES);
+        const uint64_t dk = umma_desc_sw128(kb + hh * 64 * 128);
+        const uint64_t dv = umma_desc_sw128(kb + TILE_BYTES + hh * 64 * 128);
 #pragma unroll
         for (int k = 0; k < HD / 16; ++k)
-          umma_bf16(tmem, dq + uint64_t(k * 2), dk + uint64_t(k * 2), idS, k > 0);
+          umma_bf16(tmem + T_S, dq + uint64_t(k * 2), dk + uint64_t(k * 2), idH, k > 0);
 #pragma unroll
         for (int k = 0; k < HD / 16; ++k)
-          umma_bf16(tmem + 128, dd + uint64_t(k * 2), dv + uint64_t(k * 2), idS, k > 0);
+          umma_bf16(tmem + T_DP, dd + uint64_t(k * 2), dv + uint64_t(k * 2), idH, k > 0);
         umma_commit(bar_sp);
       }
       __syncwarp();
+      ++nsp;
     };
-    issue_sp(0);
-    for (int it = 0; it < nt; ++it) {
-      mbar_wait(bar_ds, it & 1);
+    mbar_wait(bar_kv, 0);
+    tc_fence_after();
+    issue_half(0, 0);
+    for (int blk = 0; blk < nblk; ++blk) {
+      const int j = blk / nt, i = blk % nt;
+      const uint32_t kb = sKV;
+      // half 0 consumed -> half 1
+      mbar_wait(bar_h, (nsp - 1) & 1);
       tc_fence_after();
-      if (it + 1 < nt) issue_sp(it + 1);
+      issue_half(blk, 1);
+      mbar_wait(bar_h, (nsp - 1) & 1);
+      tc_fence_after();
+      // the previous key block's dK / dV drained before this block zeroes them
+      if (i == 0 && j > 0) {
+        mbar_wait(bar_dr, (j - 1) & 1);
+        tc_fence_after();
+      }
       if (elect_one()) {
-        if (ROLE == ROLE_DQ) {
-          // dQ += dS K_it : A = dS (K-major over keys), B = K rows MN-major
-          constexpr uint32_t id = umma_idesc_bf16(128, HD) | (1u << 16);
-          for (int at = 0; at < 2; ++at) {
-            const uint64_t da = umma_desc_sw128(sDS + at * TILE_BYTES);
 #pragma unroll
-            for (int k = 0; k < 4; ++k)
-              umma_bf16(tmem + 256, da + uint64_t(k * 2),
-                        desc_mn(sB0 + it * TILE_BYTES + uint32_t(at * 64 + k * 16) * 128, 0), id,
-                        (it | at | k) != 0);
-          }
-        } else {
-          // dV += Pd^T dO_it, dK += dS^T Q_it : A MN-major over keys (two
-          // 64-key atoms 16 KB apart), B MN-major (query rows = K)
-          constexpr uint32_t id = umma_idesc_bf16(128, HD) | (1u << 15) | (1u << 16);
+        for (int k = 0; k < TILE / 16; ++k) {
+          // dV_j += Pd^T dO_i ; dK_j += dS^T Q_i   (A MN-major over the 128 keys)
+          umma_bf16(tmem + T_DV, desc_mn(sP + k * 2048, TILE_BYTES),
+                    desc_mn(sDO + i * TILE_BYTES + k * 2048, 0), idKV, (i | k) != 0);
+          umma_bf16(tmem + T_DK, desc_mn(sDS + k * 2048, TILE_BYTES),
+                    desc_mn(sQ + i * TILE_BYTES + k * 2048, 0), idKV, (i | k) != 0);
+        }
+        // dQ_i += dS K_j  (A K-major over keys, B = K_j rows MN-major)
+        for (int at = 0; at < 2; ++at) {
+          const uint64_t da = umma_desc_sw128(sDS + at * TILE_BYTES);
 #pragma unroll
-          for (int k = 0; k < TILE / 16; ++k) {
-            umma_bf16(tmem + 256, desc_mn(sPD + k * 2048, TILE_BYTES),
-                      desc_mn(sB1 + it * TILE_BYTES + k * 2048, 0), id, (it | k) != 0);
-            umma_bf16(tmem + 320, desc_mn(sDS + k * 2048, TILE_BYTES),
-                      desc_mn(sB0 + it * TILE_BYTES + k * 2048, 0), id, (it | k) != 0);
-          }
+          for (int k = 0; k < 4; ++k)
+            umma_bf16(tmem + 64 * i, da + uint64_t(k * 2),
+                      desc_mn(kb + uint32_t(at * 64 + k * 16) * 128, 0), idQ, (j | at | k) != 0);
         }
         umma_commit(bar_acc);
       }
       __syncwarp();
+      if (blk + 1 < nblk) {
+        const int jn = (blk + 1) / nt;
+        if (jn != j) {
+          // next key block: once every MMA reading K_j / V_j is done, load
+          // K_j+1 / V_j+1 into the buffer (the dK/dV drain overlaps the load)
+          mbar_wait(bar_acc, blk & 1);
+          if (lane == 0) load_kv(jn);
+          __syncwarp();
+          mbar_wait(bar_kv, jn & 1);
+          tc_fence_after();
+        }
+        issue_half(blk + 1, 0);
+      }
     }
   } else {
-    const int quarter = warp & 3, half = warp >> 2;
+    const int quarter = warp & 3, part = warp >> 2;
     const int r = quarter * 32 + lane;
     const uint32_t trow = tmem + (uint32_t(quarter * 32) << 16);
     const uint64_t seed = a.rng[0], step = a.rng[1];
     const uint64_t bh = uint64_t(b * a.heads + h);
-    for (int it = 0; it < nt; ++it) {
-      const int qtile = ROLE == ROLE_DQ ? tile : it;
-      const int ktile = ROLE == ROLE_DQ ? it : tile;
-      const int q = qtile * TILE + r;
-      const float lse2 = __ldg(a.lse + bh * S + q);
-      const float Dv = __ldg(a.D + bh * S + q);
-      const uint64_t erow = (bh * S + q) * uint64_t(S);
-      mbar_wait(bar_sp, it & 1);
-      tc_fence_after();
-      uint32_t wds[2][16], wpd[2][16];
-#pragma unroll
-      for (int c = 0; c < 2; ++c) {
-        const int lc = half * 64 + c * 32;  // column within the 128-key block
-        float sv[32], dp[32];
-        tmem_ld_32x32b_x32(trow + lc, sv);
-        tmem_ld_32x32b_x32(trow + 128 + lc, dp);
-        uint32_t keep = 0xFFFFFFFFu;
-        if (a.thr) {
-          const uint64_t g = (erow + uint64_t(ktile * TILE + lc)) >> 4;
-          keep = keep16(drop_block(seed, step, a.tag, g), a.thr) |
-                 (keep16(drop_block(seed, step, a.tag, g + 1), a.thr) << 16);
-        }
-#pragma unroll
-        for (int i = 0; i < 32; i += 2) {
-          const float p0 = ex2(fmaf(sv[i], kCl2, -lse2));
-          const float p1 = ex2(fmaf(sv[i + 1], kCl2, -lse2));
-          const float k0 = (keep >> i) & 1u ? a.dscale : 0.f;
-          const float k1 = (keep >> (i + 1)) & 1u ? a.dscale : 0.f;
-          wds[c][i >> 1] = pack_bf16x2(p0 * fmaf(dp[i], k0, -Dv), p1 * fmaf(dp[i + 1], k1, -Dv));
-          if (ROLE == ROLE_DKV) wpd[c][i >> 1] = pack_bf16x2(p0 * k0, p1 * k1);
-        }
-      }
-      // the previous block's accumulate MMAs have read sDS / sPD
-      if (it > 0) mbar_wait(bar_acc, (it - 1) & 1);
-#pragma unroll
-      for (int c = 0; c < 2; ++c) {
-        st_row32(sDS, r, half * 64 + c * 32, wds[c]);
-        if (ROLE == ROLE_DKV) st_row32(sPD, r, half * 64 + c * 32, wpd[c]);
-      }
-      fence_proxy_async_smem();
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(bar_ds);
+    float lse2[4], Dv[4];
+    for (int i = 0; i < nt; ++i) {
+      lse2[i] = __ldg(a.lse + bh * S + i * TILE + r);
+      Dv[i] = __ldg(a.D + bh * S + i * TILE + r);
     }
-    // ---- epilogue ----
-    mbar_wait(bar_acc, (nt - 1) & 1);
-    tc_fence_after();
-    const int row = tile * TILE + r;  // DQ: query row; DKV: key row (acc lanes)
-    bf16* base = a.out + (int64_t(row0) + row) * (3 * a.Hd) + h * HD + half * 32;
-    auto store = [&](uint32_t col, bf16* dst, float s) {
-      float v[32];
-      tmem_ld_32x32b_x32(trow + col, v);
-      uint4* d = reinterpret_cast<uint4*>(dst);
+    uint32_t nsp = 0;
+    for (int blk = 0; blk < nblk; ++blk) {
+      const int j = blk / nt, i = blk % nt;
+      const int q = i * TILE + r;
+      float ls = 0.f, dv = 0.f;
 #pragma unroll
-      for (int u = 0; u < 4; ++u)
-        d[u] = make_uint4(pack_bf16x2(v[8 * u] * s, v[8 * u + 1] * s),
-                          pack_bf16x2(v[8 * u + 2] * s, v[8 * u + 3] * s),
-                          pack_bf16x2(v[8 * u + 4] * s, v[8 * u + 5] * s),
-                          pack_bf16x2(v[8 * u + 6] * s, v[8 * u + 7] * s));
-    };
-    if (ROLE == ROLE_DQ) {
-      store(256 + half * 32, base, kScale);
-    } else {
-      store(256 + half * 32, base + 2 * a.Hd, 1.f);   // dV
-      store(320 + half * 32, base + a.Hd, kScale);    // dK
+      for (int ii = 0; ii < 4; ++ii)
+        if (ii == i) ls = lse2[ii], dv = Dv[ii];
+#pragma unroll 1
+      for (int hh = 0; hh < 2; ++hh) {
+        const int col = hh * 64 + part * 16;  // key column within the block
+        mbar_wait(bar_sp, nsp & 1);
+        ++nsp;
+        tc_fence_after();
+        uint32_t sv[16], dp[16];
+        tmem_ld16(trow + T_S + part * 16, sv);
+        tmem_ld16(trow + T_DP + part * 16, dp);
+        const uint4 kb = keep_bytes(seed, step, a.tag,
+                                    ((bh * S + q) * uint64_t(S) + j * TILE + col) >> 4, a.thr);
+        tmem_wait();
+        uint32_t wds[8], wpd[8];
+#pragma unroll
+        for (int e = 0; e < 16; e += 2) {
+          const float p0 = ex2(fmaf(__uint_as_float(sv[e]), kCl2, -ls));
+          const float p1 = ex2(fmaf(__uint_as_float(sv[e + 1]), kCl2, -ls));
+          const uint32_t w = (&kb.x)[e >> 2];
+          const float k0 = __uint_as_float(__float_as_uint(a.dscale) & elem_mask(w, e & 3));
+          const float k1 = __uint_as_float(__float_as_uint(a.dscale) & elem_mask(w, (e & 3) + 1));
+          wds[e >> 1] = pack_bf16x2(p0 * fmaf(__uint_as_float(dp[e]), k0, -dv),
+                                    p1 * fmaf(__uint_as_float(dp[e + 1]), k1, -dv));
+          wpd[e >> 1] = pack_bf16x2(p0 * k0, p1 * k1);
+        }
+        // the previous block's accumulate MMAs have read sP / sDS
+        if (hh == 0 && blk > 0) mbar_wait(bar_acc, (blk - 1) & 1);
+        st_row16(sDS, r, col, wds);
+        st_row16(sP, r, col, wpd);
+        fence_proxy_async_smem();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(bar_h);
+      }
+      if (i == nt - 1) {
+        // key block j complete: drain dK_j, dV_j (TMEM lane = key row)
+        mbar_wait(bar_acc, blk & 1);
+        tc_fence_after();
+        uint32_t v0[16], v1[16];
+        const int which = part >> 1;            // 0: dK, 1: dV
+        const uint32_t col = (which ? T_DV : T_DK) + (part & 1) * 32;
+        tmem_ld16(trow + col, v0);
+        tmem_ld16(trow + col + 16, v1);
+        tmem_wait();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(bar_dr);
+        bf16* dst = a.out + (int64_t(row0) + j * TILE + r) * (3 * a.Hd) + (which ? 2 : 1) * a.Hd +
+                    h * HD + (part & 1) * 32;
+        store16(dst, v0, which ? 1.f : kScale);
+        store16(dst + 16, v1, which ? 1.f : kScale);
+      }
+    }
+    // ---- dQ of every query block (TMEM 64 i, lane = query row) ----
+    mbar_wait(bar_acc, (nblk - 1) & 1);
+    tc_fence_after();
+    for (int i = part; i < nt; i += 4) {
+      uint32_t v0[16], v1[16], v2[16], v3[16];
+      tmem_ld16(trow + 64 * i, v0);
+      tmem_ld16(trow + 64 * i + 16, v1);
+      tmem_ld16(trow + 64 * i + 32, v2);
+      tmem_ld16(trow + 64 * i + 48, v3);
+      tmem_wait();
+      bf16* dst = a.out + (int64_t(row0) + i * TILE + r) * (3 * a.Hd) + h * HD;
+      store16(dst, v0, kScale);
+      store16(dst + 16, v1, kScale);
+      store16(dst + 32, v2, kScale);
+      store16(dst + 48, v3, kScale);
     }
   }
   tc_fence_before();
@@ -453,11 +532,9 @@ __global__ void __launch_bounds__(kThreads, 1)
 }
 
 size_t fwd_smem(int S) {
-  return 1024 + TILE_BYTES + size_t(S) * 128 + size_t(S) * 256 + 4 * TILE * 4 + 64;
+  return 1024 + TILE_BYTES + size_t(S) * 128 + size_t(S) * 256 + 8 * TILE * 4 + 64;
 }
-size_t bwd_smem(int S, int role) {
-  return 1024 + 2 * TILE_BYTES + 2 * size_t(S) * 128 + (role == ROLE_DKV ? 4 : 2) * TILE_BYTES + 64;
-}
+size_t bwd_smem(int S) { return 1024 + 2 * size_t(S) * 128 + 6 * TILE_BYTES + 64; }
 
 bool shape_ok(int S, int heads) { return S > 0 && S % TILE == 0 && S <= 512 && heads > 0; }
 
@@ -473,7 +550,6 @@ cudaError_t attention_fwd(const void* qkv, void* out, float* lse, int B, int S, 
     return cudaErrorInvalidValue;
   const DropParams dp = drop_params(p);
   AttnArgs a{B, S, heads, Hd, static_cast<bf16*>(out), lse, nullptr, dp.thr, dp.scale, rng, tag};
-  const size_t smem = fwd_smem(S);
   static bool attr = false;
   if (!attr) {
     if (cudaError_t e = cudaFuncSetAttribute(k_attn_fwd, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -481,7 +557,8 @@ cudaError_t attention_fwd(const void* qkv, void* out, float* lse, int B, int S, 
       return e;
     attr = true;
   }
-  if (cudaError_t e = launch_k(k_attn_fwd, dim3(S / TILE, heads, B), dim3(kThreads), smem, st, qm, a))
+  if (cudaError_t e = launch_k(k_attn_fwd, dim3(S / TILE, heads, B), dim3(kThreads), fwd_smem(S),
+                               st, qm, a))
     return e;
   return cudaGetLastError();
 }
@@ -504,22 +581,12 @@ cudaError_t attention_bwd(const void* qkv, const void* out, const void* dout, co
              dp.scale, rng, tag};
   static bool attr = false;
   if (!attr) {
-    if (cudaError_t e = cudaFuncSetAttribute(k_attn_bwd<ROLE_DQ>,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             int(bwd_smem(512, ROLE_DQ))))
-      return e;
-    if (cudaError_t e = cudaFuncSetAttribute(k_attn_bwd<ROLE_DKV>,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             int(bwd_smem(512, ROLE_DKV))))
+    if (cudaError_t e = cudaFuncSetAttribute(k_attn_bwd, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             int(bwd_smem(512))))
       return e;
     attr = true;
   }
-  const dim3 grid(S / TILE, heads, B);
-  if (cudaError_t e = launch_k(k_attn_bwd<ROLE_DKV>, grid, dim3(kThreads), bwd_smem(S, ROLE_DKV),
-                               st, qm, dm, a))
-    return e;
-  if (cudaError_t e = launch_k(k_attn_bwd<ROLE_DQ>, grid, dim3(kThreads), bwd_smem(S, ROLE_DQ), st,
-                               qm, dm, a))
+  if (cudaError_t e = launch_k(k_attn_bwd, dim3(heads, B), dim3(kThreads), bwd_smem(S), st, qm, dm, a))
     return e;
   return cudaGetLastError();
 }

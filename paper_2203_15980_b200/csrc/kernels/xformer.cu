@@ -214,20 +214,34 @@ __global__ void __launch_bounds__(256)
   }
 }
 
+// out[c] (=|+=) sum over p < parts of ws[p * pstride + c], in p order: block
+// = 32 columns x 8 warps, warp w sums parts w, w+8, ... (coalesced 128-byte
+// rows), the 8 warp sums combined in warp order (deterministic)
 __global__ void __launch_bounds__(256)
-    k_rows_merge2(const float* __restrict__ ws, int parts, int H, float* __restrict__ out0,
-                  float* __restrict__ out1) {
+    k_parts_merge(const float* __restrict__ ws, int parts, int64_t pstride, int cols,
+                  float* __restrict__ out, int accumulate) {
   pdl_wait();
   pdl_trigger();
-  const int c = blockIdx.x * blockDim.x + threadIdx.x;
-  if (c >= H) return;
-  float s0 = 0.f, s1 = 0.f;
-  for (int p = 0; p < parts; ++p) {
-    s0 += ws[(int64_t(p) * 2) * H + c];
-    s1 += ws[(int64_t(p) * 2 + 1) * H + c];
+  __shared__ float red[8][32];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int c = blockIdx.x * 32 + lane;
+  float s = 0.f;
+  if (c < cols)
+    for (int p = w; p < parts; p += 8) s += ws[int64_t(p) * pstride + c];
+  red[w][lane] = s;
+  __syncthreads();
+  if (w == 0 && c < cols) {
+    float t = 0.f;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) t += red[k][lane];
+    out[c] = accumulate ? out[c] + t : t;
   }
-  out0[c] = s0;
-  out1[c] = s1;
+}
+
+cudaError_t parts_merge(const float* ws, int parts, int64_t pstride, int cols, float* out,
+                        int accumulate, cudaStream_t st) {
+  return launch_k(k_parts_merge, dim3((cols + 31) / 32), dim3(256), 0, st, ws, parts, pstride, cols,
+                  out, accumulate);
 }
 
 // ---------------------------------------------------------------- GELU
@@ -303,18 +317,6 @@ __global__ void __launch_bounds__(256)
   float4* o = reinterpret_cast<float4*>(ws + int64_t(blockIdx.x) * cols + c8 * 8);
   o[0] = make_float4(s[0], s[1], s[2], s[3]);
   o[1] = make_float4(s[4], s[5], s[6], s[7]);
-}
-
-__global__ void __launch_bounds__(256)
-    k_colsum_merge(const float* __restrict__ ws, int parts, int cols, float* __restrict__ out,
-                   int accumulate) {
-  pdl_wait();
-  pdl_trigger();
-  const int c = blockIdx.x * blockDim.x + threadIdx.x;
-  if (c >= cols) return;
-  float s = 0.f;
-  for (int p = 0; p < parts; ++p) s += ws[int64_t(p) * cols + c];
-  out[c] = accumulate ? out[c] + s : s;
 }
 
 // ---------------------------------------------------------------- embeddings
@@ -583,6 +585,14 @@ __global__ void __launch_bounds__(256)
 // AdamW (decoupled weight decay on the first n_bf elements: the matrices and
 // embedding tables), bias-corrected with the device step counter rng[1] + 1;
 // the leading n_bf fp32 masters also written as bf16 (the GEMM operands).
+__device__ __forceinline__ void adamw1(float& w, float& m, float& v, float g, bool decay, float lr,
+                                       float b1, float b2, float eps, float wd, float c1, float c2) {
+  m = fmaf(b1, m, (1.f - b1) * g);
+  v = fmaf(b2, v, (1.f - b2) * g * g);
+  const float upd = (m * c1) / (sqrtf(v * c2) + eps) + (decay ? wd * w : 0.f);
+  w = fmaf(-lr, upd, w);
+}
+
 __global__ void __launch_bounds__(256)
     k_adamw(float* __restrict__ w, float* __restrict__ m, float* __restrict__ v,
             const float* __restrict__ g, bf16* __restrict__ wbf, int64_t n, int64_t n_bf, float lr,
@@ -591,17 +601,33 @@ __global__ void __launch_bounds__(256)
   pdl_trigger();
   const float t = float(rng[1] + 1);
   const float c1 = 1.f / (1.f - powf(b1, t)), c2 = 1.f / (1.f - powf(b2, t));
-  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
-       i += int64_t(gridDim.x) * blockDim.x) {
-    const float gi = g[i];
-    const float mi = fmaf(b1, m[i], (1.f - b1) * gi);
-    const float vi = fmaf(b2, v[i], (1.f - b2) * gi * gi);
+  const int64_t n4 = n >> 2, stride = int64_t(gridDim.x) * blockDim.x;
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n4; i += stride) {
+    float4 wv = reinterpret_cast<const float4*>(w)[i];
+    float4 mv = reinterpret_cast<const float4*>(m)[i];
+    float4 vv = reinterpret_cast<const float4*>(v)[i];
+    const float4 gv = __ldg(reinterpret_cast<const float4*>(g) + i);
+    const int64_t e = 4 * i;
+    adamw1(wv.x, mv.x, vv.x, gv.x, e < n_bf, lr, b1, b2, eps, wd, c1, c2);
+    adamw1(wv.y, mv.y, vv.y, gv.y, e + 1 < n_bf, lr, b1, b2, eps, wd, c1, c2);
+    adamw1(wv.z, mv.z, vv.z, gv.z, e + 2 < n_bf, lr, b1, b2, eps, wd, c1, c2);
+    adamw1(wv.w, mv.w, vv.w, gv.w, e + 3 < n_bf, lr, b1, b2, eps, wd, c1, c2);
+    reinterpret_cast<float4*>(w)[i] = wv;
+    reinterpret_cast<float4*>(m)[i] = mv;
+    reinterpret_cast<float4*>(v)[i] = vv;
+    if (e + 3 < n_bf) {
+      reinterpret_cast<uint2*>(wbf)[i] = make_uint2(pk2(wv.x, wv.y), pk2(wv.z, wv.w));
+    } else if (e < n_bf) {
+      const float f[4] = {wv.x, wv.y, wv.z, wv.w};
+      for (int k = 0; k < 4 && e + k < n_bf; ++k) wbf[e + k] = __float2bfloat16_rn(f[k]);
+    }
+  }
+  for (int64_t i = 4 * n4 + int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride) {
+    float wi = w[i], mi = m[i], vi = v[i];
+    adamw1(wi, mi, vi, g[i], i < n_bf, lr, b1, b2, eps, wd, c1, c2);
+    w[i] = wi;
     m[i] = mi;
     v[i] = vi;
-    float wi = w[i];
-    const float upd = (mi * c1) / (sqrtf(vi * c2) + eps) + (i < n_bf ? wd * wi : 0.f);
-    wi = fmaf(-lr, upd, wi);
-    w[i] = wi;
     if (i < n_bf) wbf[i] = __float2bfloat16_rn(wi);
   }
 }
@@ -659,9 +685,8 @@ cudaError_t layernorm_bwd(const void* dy, const void* x, const void* dres, void*
                                                   static_cast<const bf16*>(dres),
                                                   static_cast<bf16*>(dx), mean, rstd, gamma, ws,
                                                   rows, chunk)) return e);
-  if (cudaError_t e = launch_k(k_rows_merge2, dim3((H + 255) / 256), dim3(256), 0, st,
-                               static_cast<const float*>(ws), parts, H, dgamma, dbeta))
-    return e;
+  if (cudaError_t e = parts_merge(ws, parts, 2 * int64_t(H), H, dgamma, 0, st)) return e;
+  if (cudaError_t e = parts_merge(ws + H, parts, 2 * int64_t(H), H, dbeta, 0, st)) return e;
   return cudaGetLastError();
 }
 
@@ -711,9 +736,7 @@ cudaError_t colsum(const void* x, int64_t rows, int cols, const int32_t* sel, in
   if (cudaError_t e = launch_k(k_colsum_part, grid, dim3(256), 0, st, static_cast<const bf16*>(x),
                                rows, cols, sel, sel_val, chunk, ws))
     return e;
-  if (cudaError_t e = launch_k(k_colsum_merge, dim3((cols + 255) / 256), dim3(256), 0, st,
-                               static_cast<const float*>(ws), parts, cols, out, accumulate))
-    return e;
+  if (cudaError_t e = parts_merge(ws, parts, cols, cols, out, accumulate, st)) return e;
   return cudaGetLastError();
 }
 
@@ -774,9 +797,8 @@ cudaError_t span_head_bwd(const void* h, const float* dlogits, const float* w, v
   DELTA_NV_SWITCH(H, if (cudaError_t e = launch_k(k_span_head_bwd<NV>, dim3(parts), dim3(256), 0,
                                                   st, static_cast<const bf16*>(h), dlogits, w,
                                                   static_cast<bf16*>(dh), ws, T, chunk)) return e);
-  if (cudaError_t e = launch_k(k_rows_merge2, dim3((H + 255) / 256), dim3(256), 0, st,
-                               static_cast<const float*>(ws), parts, H, dw, dw + H))
-    return e;
+  if (cudaError_t e = parts_merge(ws, parts, 2 * int64_t(H), H, dw, 0, st)) return e;
+  if (cudaError_t e = parts_merge(ws + H, parts, 2 * int64_t(H), H, dw + H, 0, st)) return e;
   if (cudaError_t e = launch_k(k_span_dbias, dim3(1), dim3(64), 0, st, dlogits, T, dbias))
     return e;
   return cudaGetLastError();
