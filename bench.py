@@ -50,6 +50,10 @@ def parse():
     ap.add_argument("--cpu-sample-s", type=float, default=10.0)
     ap.add_argument("--export-trace", default="")
     ap.add_argument("--detail", default="", help="where to write the full JSON record")
+    ap.add_argument("--bert-batch", type=int, default=32,
+                    help="config 5 (BERT-large seq 512) batch per GPU; 0 skips the BERT section")
+    ap.add_argument("--bert-budget", type=float, default=0.4)
+    ap.add_argument("--bert-steps", type=int, default=10)
     return ap.parse_args()
 
 
@@ -107,6 +111,101 @@ class ClockSampler:
             return None
         return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons),
                 "samples": len(sm)}
+
+
+# ------------------------------------------------------------- config 5
+def bert_section(args, world, rank, dp, barrier, max_over_ranks):
+    """Config 5: BERT-large (24 x 1024, 16 heads, FFN 4096, seq 512, SQuAD span
+    head, AdamW, dropout 0.1) under a DELTA activation budget on this GPU (one
+    DELTA instance per rank, NCCL gradient all-reduce).  Same protocol as the
+    headline: parity gate (DELTA step == no-eviction step bit for bit),
+    graph-replayed steps timed with CUDA events (max over ranks), end to end
+    through BertRuntime.train with pinned host batches."""
+    import torch
+    from paper_2203_15980_b200 import bert as BT
+    cfg = BT.BertConfig(batch=args.bert_batch)
+    rt = BT.BertRuntime(cfg, seed=0)
+    rt.dp = dp
+    batches = [rt.synthetic_batch(1000 * rank + i) for i in range(2)]
+    for slot in range(2):
+        for d, h in zip(rt.in_slots[slot], batches[0]):
+            d.copy_(h)
+    rt.measure_costs(iters=3)
+    if dp is not None:
+        from paper_2203_15980_b200.runtime import agree_cost_table
+        rt.link_gbs = agree_cost_table(rt.g, rt.link_gbs, dp, device="cuda")
+    lr = rt.lr
+    rt.lr = 0.0
+    rng0 = rt.rng.clone()
+    rt.plan(None)
+    rt.step_device()
+    loss_ref, grad_ref = rt.loss.clone(), rt.params.grad.clone()
+    rt.rng.copy_(rng0)
+    prog = rt.plan(args.bert_budget)
+    rt.step_device()
+    torch.cuda.synchronize()
+    parity = {"loss_equal": bool(torch.equal(loss_ref, rt.loss)),
+              "grads_equal": bool(torch.equal(grad_ref, rt.params.grad)),
+              "loss": round(float(loss_ref.item()), 6)}
+    del grad_ref
+    rt.lr = lr
+    if not (parity["loss_equal"] and parity["grads_equal"]):
+        raise SystemExit(f"BERT parity gate failed: DELTA step != no-eviction step {parity}")
+    n = args.bert_steps
+
+    def timed(frac):
+        p = rt.plan(frac)
+        rt.step_device()
+        rt.capture()
+        for _ in range(max(3, args.warmup)):
+            rt.step_device()
+        torch.cuda.synchronize()
+        barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(rt.stream)
+        for _ in range(n):
+            rt.step_device()
+        e1.record(rt.stream)
+        torch.cuda.synchronize()
+        barrier()
+        return p, max_over_ranks(e0.elapsed_time(e1) / n)
+
+    bp, base_ms = timed(None)
+    dprog, ms = timed(args.bert_budget)
+    launches = rt.executor.launches_per_step
+    rt.train([batches[i % 2] for i in range(3)])
+    torch.cuda.synchronize()
+    barrier()
+    t0 = time.perf_counter()
+    losses = rt.train([batches[i % 2] for i in range(n)])
+    torch.cuda.synchronize()
+    e2e_s = max_over_ranks((time.perf_counter() - t0) / n)
+    flops = sum(nd.flops for nd in rt.nodes)  # first productions (recomputes extra)
+    B, S = cfg.batch, cfg.seq
+    out = {
+        "workload": f"BERT-large (24x1024, 16 heads, FFN 4096) seq {S}, batch {B}/GPU, SQuAD span "
+                    f"head, AdamW, dropout 0.1, DELTA at {int(args.bert_budget * 100)}% activation "
+                    "budget (config 5)",
+        "seq_per_s": round(world * B / (ms * 1e-3), 1),
+        "tokens_per_s": round(world * B * S / (ms * 1e-3), 0),
+        "ms_per_step": round(ms, 3),
+        "no_eviction_seq_per_s": round(world * B / (base_ms * 1e-3), 1),
+        "no_eviction_ratio": round(base_ms / ms, 4),
+        "peak_act_gb": round(dprog.arena_bytes / 1e9, 3),
+        "peak_act_gb_no_eviction": round(bp.arena_bytes / 1e9, 3),
+        "plan": dprog.plan_counts,
+        "parity": parity,
+        "model_tflops": round(flops / (ms * 1e-3) / 1e12, 1),
+        "e2e": {"seq_per_s": round(world * B / e2e_s, 1),
+                "h2d_bytes_per_step": sum(t.numel() * t.element_size() for t in batches[0]),
+                "d2h_bytes_per_step": 4,
+                "loss_first_last": [round(losses[0], 4), round(losses[-1], 4)]},
+        "gpu_launches": launches * n,
+        "data": "synthetic token ids / segments / span labels, random init (no checkpoint)",
+    }
+    del rt
+    torch.cuda.empty_cache()
+    return out
 
 
 # -------------------------------------------------------- reference arm
@@ -498,6 +597,10 @@ def main():
     max_batch["note"] = ("planner-decided (arena + batch-proportional workspace <= capacity); "
                          "real steps at these sizes: scripts/max_batch_verify.py")
 
+    bert = None
+    if args.bert_batch > 0:
+        bert = bert_section(args, world, rank, dp, barrier, max_over_ranks)
+
     value = world * B / (delta_ms * 1e-3)
     if rank == 0:
         line = {
@@ -578,6 +681,7 @@ def main():
             "gpu_launches": launches * args.steps,
             "clocks": clk,
             "parity": parity,
+            "bert": bert,
         }
         detail = line
         # the full record goes to a side file; the printed line keeps the
@@ -619,6 +723,13 @@ def main():
                              if cpu else None),
             "gpu_launches": detail["gpu_launches"],
             "clocks": clk,
+            "bert": ({k: bert[k] for k in ("seq_per_s", "tokens_per_s", "ms_per_step",
+                                            "no_eviction_ratio", "peak_act_gb",
+                                            "peak_act_gb_no_eviction", "parity")}
+                     | {"e2e_seq_per_s": bert["e2e"]["seq_per_s"],
+                        "workload": f"BERT-large seq 512 bs{args.bert_batch}/GPU, "
+                                    f"{int(args.bert_budget * 100)}% budget (config 5)"}
+                     if bert else None),
             "detail": os.path.relpath(dpath, HERE) if dpath else None,
         })
         print(json.dumps(line), flush=True)

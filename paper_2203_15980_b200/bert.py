@@ -420,7 +420,7 @@ class BertRuntime(DeltaRuntime):
         elif op == "span_head_bwd":
             add(X.kop(X.K_SPAN_HEAD_BWD, (X.IN(1), _ptr(self.dlogits), _ptr(pr.views["head_w"]),
                                           X.OUT(), _ptr(pr.gviews["head_w"]),
-                                          _ptr(pr.gviews["head_b"]), _ptr(self.cs_ws)), (T, H)), 4)
+                                          _ptr(pr.gviews["head_b"]), _ptr(self.cs_ws)), (T, H)), 3)
         elif op == "layernorm_bwd":
             ln = node.attrs["ln"]
             dres = X.IN(node.attrs["dres"]) if "dres" in node.attrs else None
@@ -428,7 +428,7 @@ class BertRuntime(DeltaRuntime):
                                           _ptr(pr.ln_rstd[ln]), _ptr(pr.views["ln_g:" + ln]),
                                           _ptr(pr.gviews["ln_g:" + ln]),
                                           _ptr(pr.gviews["ln_b:" + ln]), _ptr(self.ln_ws)), (T, H)),
-                3)
+                2)
         elif op == "linear_bwd":
             lin = node.attrs["lin"]
             cin, cout = self.g.linears[lin]

@@ -219,9 +219,13 @@ __global__ void __launch_bounds__(256)
 // rows), the 8 warp sums combined in warp order (deterministic)
 __global__ void __launch_bounds__(256)
     k_parts_merge(const float* __restrict__ ws, int parts, int64_t pstride, int cols,
-                  float* __restrict__ out, int accumulate) {
+                  float* __restrict__ out, int accumulate, int64_t ws_y, float* __restrict__ out_y) {
   pdl_wait();
   pdl_trigger();
+  if (blockIdx.y) {
+    ws += ws_y;
+    out = out_y;
+  }
   __shared__ float red[8][32];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int c = blockIdx.x * 32 + lane;
@@ -238,10 +242,11 @@ __global__ void __launch_bounds__(256)
   }
 }
 
+// out (and with out_y, a second merge: ws + ws_y -> out_y) in one launch
 cudaError_t parts_merge(const float* ws, int parts, int64_t pstride, int cols, float* out,
-                        int accumulate, cudaStream_t st) {
-  return launch_k(k_parts_merge, dim3((cols + 31) / 32), dim3(256), 0, st, ws, parts, pstride, cols,
-                  out, accumulate);
+                        int accumulate, cudaStream_t st, int64_t ws_y = 0, float* out_y = nullptr) {
+  return launch_k(k_parts_merge, dim3((cols + 31) / 32, out_y ? 2 : 1), dim3(256), 0, st, ws, parts,
+                  pstride, cols, out, accumulate, ws_y, out_y);
 }
 
 // ---------------------------------------------------------------- GELU
@@ -307,10 +312,28 @@ __global__ void __launch_bounds__(256)
   if (c8 * 8 >= cols) return;
   const int64_t r0 = int64_t(blockIdx.x) * chunk, r1 = min(rows, r0 + chunk);
   float s[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-  for (int64_t r = r0; r < r1; ++r) {
+  const uint4* xp = reinterpret_cast<const uint4*>(x) + c8;
+  const int64_t ld = cols / 8;
+  int64_t r = r0;
+  if (!sel) {
+    // four rows in flight per thread (sums still in row order)
+    for (; r + 4 <= r1; r += 4) {
+      uint4 u[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) u[k] = __ldg(xp + (r + k) * ld);
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        float v[8];
+        unpack8(u[k], v);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) s[i] += v[i];
+      }
+    }
+  }
+  for (; r < r1; ++r) {
     if (sel && __ldg(sel + r) != sel_val) continue;
     float v[8];
-    unpack8(__ldg(reinterpret_cast<const uint4*>(x + r * cols) + c8), v);
+    unpack8(__ldg(xp + r * ld), v);
 #pragma unroll
     for (int i = 0; i < 8; ++i) s[i] += v[i];
   }
@@ -667,10 +690,10 @@ cudaError_t layernorm_fwd(const void* x, void* y, float* mean, float* rstd, cons
 }
 
 int ln_bwd_parts(int64_t rows) {
-  return int(std::max<int64_t>(1, std::min<int64_t>((rows + 63) / 64, 2 * sms())));
+  return int(std::max<int64_t>(1, std::min<int64_t>((rows + 31) / 32, 4 * sms())));
 }
 int64_t layernorm_bwd_workspace_floats(int64_t rows, int H) {
-  return int64_t(2 * sms()) * 2 * H;
+  return int64_t(4 * sms()) * 2 * H;
 }
 
 cudaError_t layernorm_bwd(const void* dy, const void* x, const void* dres, void* dx,
@@ -685,8 +708,7 @@ cudaError_t layernorm_bwd(const void* dy, const void* x, const void* dres, void*
                                                   static_cast<const bf16*>(dres),
                                                   static_cast<bf16*>(dx), mean, rstd, gamma, ws,
                                                   rows, chunk)) return e);
-  if (cudaError_t e = parts_merge(ws, parts, 2 * int64_t(H), H, dgamma, 0, st)) return e;
-  if (cudaError_t e = parts_merge(ws + H, parts, 2 * int64_t(H), H, dbeta, 0, st)) return e;
+  if (cudaError_t e = parts_merge(ws, parts, 2 * int64_t(H), H, dgamma, 0, st, H, dbeta)) return e;
   return cudaGetLastError();
 }
 
@@ -787,7 +809,7 @@ cudaError_t span_head_fwd(const void* h, const float* w, const float* bias, cons
   return cudaGetLastError();
 }
 
-int64_t span_head_workspace_floats(int64_t T, int H) { return int64_t(2 * sms()) * 2 * H; }
+int64_t span_head_workspace_floats(int64_t T, int H) { return int64_t(4 * sms()) * 2 * H; }
 
 cudaError_t span_head_bwd(const void* h, const float* dlogits, const float* w, void* dh, float* dw,
                           float* dbias, float* ws, int64_t T, int H, cudaStream_t st) {
@@ -797,8 +819,7 @@ cudaError_t span_head_bwd(const void* h, const float* dlogits, const float* w, v
   DELTA_NV_SWITCH(H, if (cudaError_t e = launch_k(k_span_head_bwd<NV>, dim3(parts), dim3(256), 0,
                                                   st, static_cast<const bf16*>(h), dlogits, w,
                                                   static_cast<bf16*>(dh), ws, T, chunk)) return e);
-  if (cudaError_t e = parts_merge(ws, parts, 2 * int64_t(H), H, dw, 0, st)) return e;
-  if (cudaError_t e = parts_merge(ws + H, parts, 2 * int64_t(H), H, dw + H, 0, st)) return e;
+  if (cudaError_t e = parts_merge(ws, parts, 2 * int64_t(H), H, dw, 0, st, H, dw + H)) return e;
   if (cudaError_t e = launch_k(k_span_dbias, dim3(1), dim3(64), 0, st, dlogits, T, dbias))
     return e;
   return cudaGetLastError();

@@ -385,7 +385,7 @@ def layernorm_bwd_workspace_floats(rows, H) -> int:
 def layernorm_bwd(dy, x, dres, dx, mean, rstd, gamma, dgamma, dbeta, ws, rows, H, stream):
     check(lib.delta_layernorm_bwd(dy, x, dres, dx, mean, rstd, gamma, dgamma, dbeta, ws, rows, H,
                                   stream))
-    _count(3)
+    _count(2)
 
 
 def gelu_fwd(x, y, n, stream):
@@ -435,7 +435,7 @@ def span_head_workspace_floats(T, H) -> int:
 
 def span_head_bwd(h, dlogits, w, dh, dw, dbias, ws, T, H, stream):
     check(lib.delta_span_head_bwd(h, dlogits, w, dh, dw, dbias, ws, T, H, stream))
-    _count(4)
+    _count(3)
 
 
 def attention_fwd(qkv, out, lse, B, S, heads, p, rng, tag, stream):

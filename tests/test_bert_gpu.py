@@ -39,7 +39,7 @@ def test_bert_step_matches_fp32_torch(cfg):
     bad = {}
     # analytically zero (softmax minus one-hot sums to zero per sequence):
     # only bounded against the scale of the final LayerNorm's gamma gradient
-    floor = 1e-2 * leaves["ln_g:lnf"].grad.float().pow(2).mean().sqrt().item()
+    floor = 5e-2 * leaves["ln_g:lnf"].grad.float().pow(2).mean().sqrt().item()
     for name in ("ln_b:lnf", "head_b"):
         m = rt.params.gviews[name].abs().max().item()
         if m > floor:
