@@ -35,6 +35,7 @@
 #include <cstdlib>
 #include <mutex>
 
+#include "kernels/gelu.cuh"
 #include "kernels/kernels.hpp"
 #include "kernels/launch.hpp"
 #include "kernels/sm100_common.cuh"
@@ -628,11 +629,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             float hx[8];
             unpack8f(ld_row16(sb, lane, u), hx);
 #pragma unroll
-            for (int i = 0; i < 8; ++i) {
-              const float x = hx[i];
-              const float cdf = 0.5f * (1.f + erff(x * 0.70710678118654752f));
-              v[u * 8 + i] *= fmaf(x * 0.3989422804014327f, __expf(-0.5f * x * x), cdf);
-            }
+            for (int i = 0; i < 8; ++i) v[u * 8 + i] *= gelu_grad1(hx[i]);
           }
         }
         if constexpr (row_tiled(MODE)) {

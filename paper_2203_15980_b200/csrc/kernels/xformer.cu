@@ -29,6 +29,7 @@
 #include <algorithm>
 #include <cstdint>
 
+#include "kernels/gelu.cuh"
 #include "kernels/launch.hpp"
 #include "kernels/philox.cuh"
 #include "kernels/xformer.hpp"
@@ -250,10 +251,6 @@ cudaError_t parts_merge(const float* ws, int parts, int64_t pstride, int cols, f
 }
 
 // ---------------------------------------------------------------- GELU
-__device__ __forceinline__ float gelu_erf(float x) {
-  return 0.5f * x * (1.f + erff(x * 0.70710678118654752f));
-}
-
 __global__ void __launch_bounds__(256)
     k_gelu_fwd(const uint4* __restrict__ x, uint4* __restrict__ y, int64_t n8) {
   pdl_wait();
@@ -263,7 +260,7 @@ __global__ void __launch_bounds__(256)
     float v[8];
     unpack8(__ldg(x + i), v);
 #pragma unroll
-    for (int k = 0; k < 8; ++k) v[k] = gelu_erf(v[k]);
+    for (int k = 0; k < 8; ++k) v[k] = gelu_fwd1(v[k]);
     y[i] = pack8(v);
   }
 }
@@ -303,43 +300,63 @@ __global__ void __launch_bounds__(256)
 // ---------------------------------------------------------------- column sums
 // ws[part][cols]: part p sums rows [p*chunk, (p+1)*chunk) (rows with
 // sel[r] == sel_val only, when sel is given); thread = 8 columns.
+// thread (g, c8): 8 columns c8*8.., rows r0 + g, r0 + g + RG, ... of the
+// block's chunk (RG = 256 / (cols/8) row groups when cols < 2048, 4 rows in
+// flight); the RG group sums are combined in smem in group order.
 __global__ void __launch_bounds__(256)
     k_colsum_part(const bf16* __restrict__ x, int64_t rows, int cols, const int32_t* __restrict__ sel,
                   int sel_val, int64_t chunk, float* __restrict__ ws) {
   pdl_wait();
   pdl_trigger();
-  const int c8 = blockIdx.y * blockDim.x + threadIdx.x;
-  if (c8 * 8 >= cols) return;
-  const int64_t r0 = int64_t(blockIdx.x) * chunk, r1 = min(rows, r0 + chunk);
+  __shared__ float red[256 * 8];
+  const int vecs = cols / 8;
+  const int vb = vecs < 256 ? vecs : 256;       // vectors per block
+  const int RG = 256 / vb;                      // row groups
+  const int g = threadIdx.x / vb;
+  const int c8 = blockIdx.y * vb + threadIdx.x % vb;
+  const bool on = g < RG && c8 < vecs;
   float s[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-  const uint4* xp = reinterpret_cast<const uint4*>(x) + c8;
-  const int64_t ld = cols / 8;
-  int64_t r = r0;
-  if (!sel) {
-    // four rows in flight per thread (sums still in row order)
-    for (; r + 4 <= r1; r += 4) {
-      uint4 u[4];
+  if (on) {
+    const int64_t r0 = int64_t(blockIdx.x) * chunk, r1 = min(rows, r0 + chunk);
+    const uint4* xp = reinterpret_cast<const uint4*>(x) + c8;
+    int64_t r = r0 + g;
+    if (!sel) {
+      for (; r + 3 * RG < r1; r += 4 * RG) {
+        uint4 u[4];
 #pragma unroll
-      for (int k = 0; k < 4; ++k) u[k] = __ldg(xp + (r + k) * ld);
+        for (int k = 0; k < 4; ++k) u[k] = __ldg(xp + (r + k * RG) * vecs);
 #pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        float v[8];
-        unpack8(u[k], v);
+        for (int k = 0; k < 4; ++k) {
+          float v[8];
+          unpack8(u[k], v);
 #pragma unroll
-        for (int i = 0; i < 8; ++i) s[i] += v[i];
+          for (int i = 0; i < 8; ++i) s[i] += v[i];
+        }
       }
     }
-  }
-  for (; r < r1; ++r) {
-    if (sel && __ldg(sel + r) != sel_val) continue;
-    float v[8];
-    unpack8(__ldg(xp + r * ld), v);
+    for (; r < r1; r += RG) {
+      if (sel && __ldg(sel + r) != sel_val) continue;
+      float v[8];
+      unpack8(__ldg(xp + r * vecs), v);
 #pragma unroll
-    for (int i = 0; i < 8; ++i) s[i] += v[i];
+      for (int i = 0; i < 8; ++i) s[i] += v[i];
+    }
   }
-  float4* o = reinterpret_cast<float4*>(ws + int64_t(blockIdx.x) * cols + c8 * 8);
-  o[0] = make_float4(s[0], s[1], s[2], s[3]);
-  o[1] = make_float4(s[4], s[5], s[6], s[7]);
+  if (RG > 1) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) red[threadIdx.x * 8 + i] = s[i];
+    __syncthreads();
+    if (g == 0 && on) {
+      for (int q = 1; q < RG; ++q)
+#pragma unroll
+        for (int i = 0; i < 8; ++i) s[i] += red[(q * vb + threadIdx.x) * 8 + i];
+    }
+  }
+  if (g == 0 && on) {
+    float4* o = reinterpret_cast<float4*>(ws + int64_t(blockIdx.x) * cols + c8 * 8);
+    o[0] = make_float4(s[0], s[1], s[2], s[3]);
+    o[1] = make_float4(s[4], s[5], s[6], s[7]);
+  }
 }
 
 // ---------------------------------------------------------------- embeddings
@@ -754,7 +771,7 @@ cudaError_t colsum(const void* x, int64_t rows, int cols, const int32_t* sel, in
   if (cols % 8 || rows <= 0) return cudaErrorInvalidValue;
   const int parts = colsum_parts(rows);
   const int64_t chunk = (rows + parts - 1) / parts;
-  const dim3 grid(parts, unsigned((cols / 8 + 255) / 256));
+  const dim3 grid(parts, unsigned((cols / 8 + 255) / 256));  // vectors per block: min(cols/8, 256)
   if (cudaError_t e = launch_k(k_colsum_part, grid, dim3(256), 0, st, static_cast<const bf16*>(x),
                                rows, cols, sel, sel_val, chunk, ws))
     return e;
