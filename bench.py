@@ -54,6 +54,8 @@ def parse():
                     help="config 5 (BERT-large seq 512) batch per GPU; 0 skips the BERT section")
     ap.add_argument("--bert-budget", type=float, default=0.4)
     ap.add_argument("--bert-steps", type=int, default=10)
+    ap.add_argument("--no-verify-max-batch", action="store_true",
+                    help="skip the real training steps at the planner-decided max batches")
     return ap.parse_args()
 
 
@@ -205,6 +207,39 @@ def bert_section(args, world, rank, dp, barrier, max_over_ranks):
     }
     del rt
     torch.cuda.empty_cache()
+    return out
+
+
+# ------------------------------------------------------------- config 3
+def verify_batch(depth, batch, anchors, delta, per_sample, link_gbs, cap, MB):
+    """One ResNet training step (plus a timed second one) at `batch` under the
+    DELTA plan whose budget is the HBM the planner search gave it (or no
+    eviction): the planner's max-batch answer, trained for real."""
+    import torch
+    from paper_2203_15980_b200.runtime import DeltaRuntime
+    torch.cuda.reset_peak_memory_stats()
+    rt = DeltaRuntime(depth, batch, seed=0, anchors=anchors)
+    ps = MB.per_sample_costs(depth, per_sample)
+    for n in rt.nodes:
+        n.cost_us = max(1, int(round(ps.get(n.name, 1 / 256) * batch)))
+    rt.link_gbs = link_gbs
+    room = cap - MB.workspace_bytes(rt.g, batch)
+    prog = rt.plan(budget=room) if delta else rt.plan(None)
+    gen = torch.Generator().manual_seed(7)
+    x = torch.zeros(rt.x_dev.shape, dtype=torch.bfloat16)
+    k = min(batch, 256)  # random images in the first 256 slots (host memory stays modest)
+    x[:k, ..., :3] = torch.randn(k, 224, 224, 3, generator=gen).to(torch.bfloat16)
+    y = torch.randint(0, 1000, (batch,), generator=gen)
+    rt.step(x, y)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    loss = rt.step(x, y)
+    torch.cuda.synchronize()
+    dt = time.perf_counter() - t0
+    out = {"batch": batch, "anchors": anchors, "arena_gb": round(prog.arena_bytes / 1e9, 2),
+           "plan": prog.plan_counts, "peak_alloc_gb": round(torch.cuda.max_memory_allocated() / 1e9, 2),
+           "img_s": round(batch / dt, 1), "loss": round(loss, 4)}
+    del rt, prog
     return out
 
 
@@ -595,11 +630,36 @@ def main():
                               "delta": d101.batch if d101 else None,
                               "ratio": round(d101.batch / b101.batch, 3) if b101 and d101 else None}
     max_batch["note"] = ("planner-decided (arena + batch-proportional workspace <= capacity); "
-                         "real steps at these sizes: scripts/max_batch_verify.py")
+                         "'verified': real training steps at those sizes in this run")
 
     bert = None
     if args.bert_batch > 0:
         bert = bert_section(args, world, rank, dp, barrier, max_over_ranks)
+
+    # ---- config 3, verified: free this process's ResNet-50 bs256 state and
+    # ---- train real steps at the planned max batches (DELTA and no eviction)
+    budget_bytes, link_gbs = rt.config.budget, rt.link_gbs
+    saved_graph = None
+    if not args.no_verify_max_batch and world == 1 and best and mb_base:
+        import gc
+        a_best = max((a for a in mb_delta if mb_delta[a]), key=lambda a: mb_delta[a].batch)
+        del rt
+        gc.collect()
+        torch.cuda.empty_cache()
+        ver = {}
+        for label, batch, anchors, delta in (("no_eviction", mb_base.batch, "out", False),
+                                             ("delta", mb_delta[a_best].batch, a_best, True)):
+            try:
+                ver[label] = verify_batch(args.depth, batch, anchors, delta, per_sample, link_gbs,
+                                          cap, MB)
+            except Exception as e:  # noqa: BLE001 - reported, never fatal
+                ver[label] = {"batch": batch, "error": str(e)[:200]}
+            gc.collect()
+            torch.cuda.empty_cache()
+        max_batch["verified"] = ver
+        ok = all("img_s" in v for v in ver.values())
+        max_batch["verified_ratio"] = (round(ver["delta"]["batch"] / ver["no_eviction"]["batch"], 3)
+                                       if ok else None)
 
     value = world * B / (delta_ms * 1e-3)
     if rank == 0:
@@ -611,7 +671,7 @@ def main():
             "config": {"workload": f"ResNet-{args.depth} training step, batch {B}/GPU, "
                                    f"DELTA at {int(args.budget * 100)}% activation budget",
                        "global_batch": B * world, "image": 224, "budget_fraction": args.budget,
-                       "budget_bytes": rt.config.budget, "anchors": args.anchors,
+                       "budget_bytes": budget_bytes, "anchors": args.anchors,
                        "parallelism": f"dp{world}", "graph": graph_state,
                        "l2": "working set >> 126 MB L2 (no flush needed)"},
             "no_eviction": {"images_per_s": round(world * B / (base_ms * 1e-3), 1),
@@ -625,7 +685,7 @@ def main():
                             "saving": round(1 - prog.arena_bytes / base_arena, 4)},
             "plan": {"counts": prog.plan_counts, "decisions": len(prog.decisions),
                      "host_slab_mb": round(prog.host_bytes / 2**20, 1),
-                     "link_gbs": round(rt.link_gbs, 2) if rt.link_gbs else None,
+                     "link_gbs": round(link_gbs, 2) if link_gbs else None,
                      "simulated_wall_us": prog.plan_wall_us,
                      "planner_ms": round(ours_plan_ns * 1e-6, 4)},
             "e2e": {"value": round(world * B / e2e_s, 1), "unit": "images/s",
@@ -670,7 +730,7 @@ def main():
             "swap": {"copies": swap_n, "bytes_per_step": swap_bytes,
                      "ms_per_step": round(swap_ms, 3),
                      "achieved_gbs": round(swap_bytes / (swap_ms * 1e6), 2) if swap_ms else None,
-                     "link_probe_gbs": round(rt.link_gbs, 2) if rt.link_gbs else None,
+                     "link_probe_gbs": round(link_gbs, 2) if link_gbs else None,
                      "peak_gbs": PCIE5_X16_GBS,
                      "frac_of_link_peak": round(swap_bytes / (swap_ms * 1e6) / PCIE5_X16_GBS, 4)
                      if swap_ms else None,
@@ -710,7 +770,9 @@ def main():
             "max_batch_ratio": mb.get("ratio"),
             "max_batch": {"no_eviction": mb["no_eviction"], "delta": max(
                 (v for v in mb["delta"].values() if v), default=None),
-                "resnet101_ratio": mb["resnet101"]["ratio"], "kind": "planner-decided"},
+                "resnet101_ratio": mb["resnet101"]["ratio"],
+                "kind": "trained" if mb.get("verified_ratio") else "planner-decided",
+                "verified_ratio": mb.get("verified_ratio")},
             "plan": detail["plan"]["counts"],
             "e2e": {k: detail["e2e"][k] for k in ("value", "unit", "h2d_bytes_per_step",
                                                    "d2h_bytes_per_step")},

@@ -707,7 +707,7 @@ cudaError_t layernorm_fwd(const void* x, void* y, float* mean, float* rstd, cons
 }
 
 int ln_bwd_parts(int64_t rows) {
-  return int(std::max<int64_t>(1, std::min<int64_t>((rows + 31) / 32, 4 * sms())));
+  return int(std::max<int64_t>(1, std::min<int64_t>((rows + 63) / 64, 2 * sms())));
 }
 int64_t layernorm_bwd_workspace_floats(int64_t rows, int H) {
   return int64_t(4 * sms()) * 2 * H;
