@@ -174,7 +174,11 @@ __device__ __forceinline__ uint8_t* align1024(uint8_t* p) {
 // uses), instead of per-chunk cp.async gathers by the epilogue warps.
 constexpr int OPT_NB = 2;
 
-template <int BN, int STAGES, int MODE, int EV, bool OPT = false>
+// PAIR: a 2-CTA cluster (cta_group::2) computes 256-row tiles — each CTA
+// stages its 128 rows of A and half of the BN weight rows, the leader issues
+// M=256 MMAs that read both CTAs' operands, each CTA's TMEM holds its rows —
+// halving the per-SM operand traffic of the B tile (MODE_TMA only).
+template <int BN, int STAGES, int MODE, int EV, bool OPT = false, bool PAIR = false>
 __global__ void __launch_bounds__(kThreads, 1)
     k_conv_fwd(const __grid_constant__ CUtensorMap wmap, const __grid_constant__ CUtensorMap amap,
                const __grid_constant__ CUtensorMap ymap, const __grid_constant__ CUtensorMap emap0,
@@ -184,8 +188,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint8_t* smem = align1024(smem_raw);
   // producer signalling lag: a thread keeps LAG+1 stages of gathers in flight
   constexpr uint32_t LAG = STAGES - 2;
+  static_assert(!PAIR || (MODE == MODE_TMA && !OPT && BN == 256), "pair mode: 1x1 TMA path");
   constexpr uint32_t A_STAGE = BM * 128;
-  constexpr uint32_t B_STAGE = BN * 128;
+  constexpr uint32_t B_STAGE = (PAIR ? BN / 2 : BN) * 128;  // this CTA's weight rows
   constexpr uint32_t ACC_COLS = BN;
   constexpr uint32_t TMEM_COLS = 2 * BN < 32 ? 32 : 2 * BN;
   const uint32_t sA = smem_u32(smem);
@@ -217,6 +222,12 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
+  // tile scheduling unit: the CTA, or the CTA pair
+  const uint32_t rank = PAIR ? cluster_rank() : 0u;
+  const int unit = PAIR ? int(blockIdx.x >> 1) : int(blockIdx.x);
+  const int units = PAIR ? int(gridDim.x >> 1) : int(gridDim.x);
+  constexpr int TM = PAIR ? 2 * BM : BM;  // rows per tile
+  auto tile_m0 = [&](int tile) { return (tile / a.n_tiles) * TM + int(rank) * BM; };
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
@@ -225,7 +236,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&tfull[i], 1);
-      mbar_init(&tempty[i], EPI_W);
+      // pair: the leader's MMA waits for both CTAs' epilogues
+      mbar_init(&tempty[i], PAIR ? 2 * EPI_W : EPI_W);
     }
     mbar_init(bfull, 1);
     for (int i = 0; i < OPT_NB; ++i) {
@@ -253,9 +265,15 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     fence_proxy_async_smem();
   }
-  if (warp == MMA_WARP) tmem_alloc(tslot, TMEM_COLS);
+  if (warp == MMA_WARP) {
+    if constexpr (PAIR)
+      tmem_alloc_pair(tslot, TMEM_COLS);
+    else
+      tmem_alloc(tslot, TMEM_COLS);
+  }
   tc_fence_before();
   __syncthreads();
+  if constexpr (PAIR) cluster_sync_all();  // the peer's barriers exist before any remote use
   tc_fence_after();
   const uint32_t tmem = *tslot;
   // prologue done (barriers, TMEM, descriptors): now wait for the predecessor
@@ -270,8 +288,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         // epilogue operands of every tile of this CTA, two tiles ahead
         if (lane == 0) {
           uint32_t lt = 0;
-          for (int tile = blockIdx.x; tile < a.tiles; tile += gridDim.x, ++lt) {
-            const int m0 = (tile / a.n_tiles) * BM;
+          for (int tile = unit; tile < a.tiles; tile += units, ++lt) {
+            const int m0 = tile_m0(tile);
             const int n0 = (tile % a.n_tiles) * BN;
             const uint32_t b = lt % OPT_NB;
             if (lt >= OPT_NB) mbar_wait(&oempty[b], ((lt / OPT_NB) - 1) & 1);
@@ -290,8 +308,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     } else {
     uint32_t it = 0;  // global k-iteration counter (stage ring position)
-    for (int tile = blockIdx.x; tile < a.tiles; tile += gridDim.x) {
-      const int m0 = (tile / a.n_tiles) * BM;
+    for (int tile = unit; tile < a.tiles; tile += units) {
+      const int m0 = tile_m0(tile);
       const int n0 = (tile % a.n_tiles) * BN;
       if constexpr (MODE == MODE_IM2COL) {
         if (tid == 0) {
@@ -371,9 +389,17 @@ __global__ void __launch_bounds__(kThreads, 1)
           for (int kb = 0; kb < a.kblocks; ++kb, ++it) {
             const uint32_t s = it % STAGES;
             if (it >= STAGES) mbar_wait(&empty[s], ((it / STAGES) - 1) & 1);
-            mbar_arrive_expect_tx(&full[s], A_STAGE + B_STAGE);
-            tma_load_2d(sA + s * A_STAGE, &amap, &full[s], kb * BK, m0);
-            tma_load_2d(sB + s * B_STAGE, &wmap, &full[s], kb * BK, n0);
+            if constexpr (PAIR) {
+              // both CTAs' bytes complete on the leader's barrier
+              if (rank == 0) mbar_arrive_expect_tx(&full[s], 2 * (A_STAGE + B_STAGE));
+              tma_load_2d_pair(sA + s * A_STAGE, &amap, &full[s], kb * BK, m0);
+              tma_load_2d_pair(sB + s * B_STAGE, &wmap, &full[s], kb * BK,
+                               n0 + int(rank) * (BN / 2));
+            } else {
+              mbar_arrive_expect_tx(&full[s], A_STAGE + B_STAGE);
+              tma_load_2d(sA + s * A_STAGE, &amap, &full[s], kb * BK, m0);
+              tma_load_2d(sB + s * B_STAGE, &wmap, &full[s], kb * BK, n0);
+            }
           }
         }
       } else {
@@ -518,10 +544,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     // with cp.async: 4 x 16 B per lane per operand, 8 full rows per instruction,
     // rows past M zero-filled; one commit group per chunk (possibly empty)
     auto prefetch = [&](uint32_t e) {
-      const int tile_ = blockIdx.x + int(e / CHW) * gridDim.x;
+      const int tile_ = unit + int(e / CHW) * units;
       if (tile_ < a.tiles) {
         const uint32_t sb = ring + (e % NSLOTS) * SLOT;
-        const int pm = (tile_ / a.n_tiles) * BM + quarter * 32;
+        const int pm = tile_m0(tile_) + quarter * 32;
         const int pc = (tile_ % a.n_tiles) * BN + (half + int(e % CHW) * HALVES) * 32;
         // stride-2 add: (n, p, q) of the block's first row, once per chunk
         int q0 = 0, p0 = 0, n0_ = 0;
@@ -577,9 +603,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       stats_row_zero(a.stats, a.K, BN, (warp - 4) * 32 + lane, EPI_W * 32);
     uint32_t ec = 0;  // chunks consumed by this warp
     uint32_t lt = 0;
-    for (int tile = blockIdx.x; tile < a.tiles; tile += gridDim.x, ++lt) {
+    for (int tile = unit; tile < a.tiles; tile += units, ++lt) {
       // row-tiled stem: tile = one output row of Q pixels (rows >= Q are junk)
-      const int m0 = (tile / a.n_tiles) * (row_tiled(MODE) ? a.Q : BM);
+      const int m0 = row_tiled(MODE) ? (tile / a.n_tiles) * a.Q : tile_m0(tile);
       const int n0 = (tile % a.n_tiles) * BN;
       const uint32_t acc = lt & 1;
       mbar_wait(&tfull[acc], (lt >> 1) & 1);
@@ -764,7 +790,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             S += red[qq * BN + c].x;
             Q += red[qq * BN + c].y;
           }
-          if (n0 + c < a.K)
+          if (n0 + c < a.K && n_rows > 0)
             stats_fold_tile<ev_cross(EV)>(a.stats, a.K, n0 + c, float(n_rows), S, Q);
         }
         asm volatile("bar.sync 1, %0;" ::"n"(EPI_W * 32) : "memory");
@@ -772,7 +798,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       tc_fence_before();
       __syncwarp();
       if (lane == 0) {
-        mbar_arrive(&tempty[acc]);
+        if constexpr (PAIR)
+          mbar_arrive_cluster(mapa_shared(smem_u32(&tempty[acc]), 0));  // the leader's
+        else
+          mbar_arrive(&tempty[acc]);
         if (FUSED && OPT) mbar_arrive(&oempty[lt % OPT_NB]);  // operand tile read
       }
     }
@@ -809,9 +838,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     // built by 64-bit adds), one elected lane issues each k-block's MMAs:
     // issuing from lane 0 alone cost a dozen dependent uniform-datapath
     // instructions per MMA, the pacing stage for the N <= 128 tiles.
-    constexpr uint32_t idesc = umma_idesc_bf16(BM, BN);
+    constexpr uint32_t idesc = umma_idesc_bf16(PAIR ? 2 * BM : BM, BN);
     uint32_t it = 0, lt = 0;
-    for (int tile = blockIdx.x; tile < a.tiles; tile += gridDim.x, ++lt) {
+    // pair: only the leader issues (its MMAs read both CTAs' smem, write both TMEMs)
+    for (int tile = unit; tile < ((PAIR && rank != 0) ? 0 : a.tiles); tile += units, ++lt) {
       const uint32_t acc = lt & 1;
       if (lt >= 2) mbar_wait(&tempty[acc], ((lt >> 1) - 1) & 1);
       tc_fence_after();
@@ -846,29 +876,48 @@ __global__ void __launch_bounds__(kThreads, 1)
                                                : umma_desc_sw128(sA + s * A_STAGE);
         const uint64_t bd0 = umma_desc_sw128(sB + s * B_STAGE);
         if (elect_one()) {
+          if constexpr (PAIR) {
 #pragma unroll
-          for (int k = 0; k < BK / 16; ++k)
-            umma_bf16(d, ad0 + uint64_t(MODE == MODE_STEM ? k * 256 : k * 2), bd0 + uint64_t(k * 2),
-                      idesc, (kb | k) != 0 ? 1u : 0u);
-          umma_commit(&empty[s]);
+            for (int k = 0; k < BK / 16; ++k)
+              umma_bf16_pair(d, ad0 + uint64_t(k * 2), bd0 + uint64_t(k * 2), idesc,
+                             (kb | k) != 0 ? 1u : 0u);
+            umma_commit_pair(&empty[s]);
+          } else {
+#pragma unroll
+            for (int k = 0; k < BK / 16; ++k)
+              umma_bf16(d, ad0 + uint64_t(MODE == MODE_STEM ? k * 256 : k * 2),
+                        bd0 + uint64_t(k * 2), idesc, (kb | k) != 0 ? 1u : 0u);
+            umma_commit(&empty[s]);
+          }
         }
         __syncwarp();
       }
-      if (elect_one()) umma_commit(&tfull[acc]);
+      if (elect_one()) {
+        if constexpr (PAIR)
+          umma_commit_pair(&tfull[acc]);
+        else
+          umma_commit(&tfull[acc]);
+      }
       __syncwarp();
     }
   }
   if (warp >= 4 && warp < MMA_WARP && lane == 0) bulk_wait<0>();  // output visible before exit
   tc_fence_before();
   __syncthreads();
+  if constexpr (PAIR) cluster_sync_all();  // both CTAs done with the pair's TMEM
   tc_fence_after();
-  if (warp == MMA_WARP) tmem_dealloc(tmem, TMEM_COLS);
+  if (warp == MMA_WARP) {
+    if constexpr (PAIR)
+      tmem_dealloc_pair(tmem, TMEM_COLS);
+    else
+      tmem_dealloc(tmem, TMEM_COLS);
+  }
 }
 
-template <int BN, int STAGES, int EV, bool OPT>
+template <int BN, int STAGES, int EV, bool OPT, bool PAIR = false>
 constexpr size_t conv_smem_bytes() {
   constexpr bool FUSED = ev_fused(EV);
-  return size_t(STAGES) * (BM * 128 + BN * 128) + 16384 /*epilogue staging*/ +
+  return size_t(STAGES) * (BM * 128 + (PAIR ? BN / 2 : BN) * 128) + 16384 /*epilogue staging*/ +
          (!FUSED ? 0
           : OPT  ? size_t(OPT_NB) * ev_operands(EV) * BN * 256
                  : epi_ring_bytes<BN, STAGES>()) /*epilogue operands*/ + 4 * BN * 8 /*stats scratch*/ +
@@ -1018,6 +1067,22 @@ bool stem_tma() {
   return v == 1;
 }
 
+// CTA-pair (cta_group::2) tiles for the 1x1 path: N tile 256, at least one
+// wave of pairs; DELTA_PAIR=0 disables, =1 enables (default: off until
+// measured on by default)
+int num_sms();
+bool pair_ok(const ConvPlan& cp) {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = std::getenv("DELTA_PAIR");
+    v = (e && e[0] == '1') ? 1 : 0;
+  }
+  if (!v || cp.bn != 256 || cp.C == 4) return false;
+  const int64_t M = int64_t(cp.N) * cp.P * cp.Q;
+  const int64_t tiles = (M + 255) / 256 * ((cp.K + 255) / 256);
+  return tiles >= num_sms() / 2;
+}
+
 int num_sms() {
   static int n = 0;
   if (!n) {
@@ -1029,11 +1094,11 @@ int num_sms() {
   return n;
 }
 
-template <int BN, int STAGES, int MODE, int EV, bool OPT = false>
+template <int BN, int STAGES, int MODE, int EV, bool OPT = false, bool PAIR = false>
 cudaError_t launch(const ConvPlan& cp, const void* x, void* y, float* stats,
                    const ConvEpilogue& epi, cudaStream_t st) {
-  auto kern = k_conv_fwd<BN, STAGES, MODE, EV, OPT>;
-  constexpr size_t smem = conv_smem_bytes<BN, STAGES, EV, OPT>();
+  auto kern = k_conv_fwd<BN, STAGES, MODE, EV, OPT, PAIR>;
+  constexpr size_t smem = conv_smem_bytes<BN, STAGES, EV, OPT, PAIR>();
   static_assert(smem <= 227 * 1024, "shared memory");
   static bool attr = false;
   if (!attr) {
@@ -1050,7 +1115,8 @@ cudaError_t launch(const ConvPlan& cp, const void* x, void* y, float* stats,
   a.kblocks = cp.kdim / BK;
   a.taps = cp.R * cp.S;
   a.n_tiles = (cp.K + BN - 1) / BN;
-  a.tiles = (row_tiled(MODE) ? cp.N * cp.P : (a.M + BM - 1) / BM) * a.n_tiles;
+  constexpr int TM = PAIR ? 2 * BM : BM;
+  a.tiles = (row_tiled(MODE) ? cp.N * cp.P : (a.M + TM - 1) / TM) * a.n_tiles;
   a.stats = reinterpret_cast<float4*>(stats);
   a.e = epi;
   alignas(64) CUtensorMap amap;
@@ -1087,6 +1153,18 @@ cudaError_t launch(const ConvPlan& cp, const void* x, void* y, float* stats,
       return cudaErrorInvalidValue;
   }
   // statistics come as one partial row per CTA: always one CTA per SM then
+  if constexpr (PAIR) {
+    // CTA pairs: the weight map's box is this CTA's half of the N tile
+    alignas(64) CUtensorMap wmap;
+    if (!encode_2d(&wmap, cp.wptr, uint64_t(cp.kdim), uint64_t(cp.K), uint32_t(BN / 2)))
+      return cudaErrorInvalidValue;
+    const int sms2 = num_sms() & ~1;
+    const int grid = (stats != nullptr || 2 * a.tiles > sms2) ? sms2 : 2 * a.tiles;
+    if (cudaError_t e_ = launch_cluster(kern, dim3(grid), dim3(kThreads), smem, st, 2u, wmap, amap,
+                                        ymap, emap0, emap1, emap2, a))
+      return e_;
+    return cudaGetLastError();
+  }
   const int grid = (stats != nullptr || a.tiles > num_sms()) ? num_sms() : a.tiles;
   if (cudaError_t e_ = launch_k(kern, dim3(grid), dim3(kThreads), smem, st, *reinterpret_cast<const CUtensorMap*>(cp.wmap), amap, ymap, emap0, emap1, emap2, a)) return e_;
   return cudaGetLastError();
@@ -1095,6 +1173,7 @@ cudaError_t launch(const ConvPlan& cp, const void* x, void* y, float* stats,
 }  // namespace
 
 int conv_plan_init(ConvPlan* cp, const void* w) {
+  cp->wptr = w;
   if (cp->C % 64 != 0 && cp->C != 4) return 1;
   if (cp->K % 8 != 0) return 1;
   // the C=4 stem path is the 7x7/2 pad-3 ResNet stem over an even width
@@ -1167,6 +1246,7 @@ cudaError_t conv_forward(const ConvPlan& cp, const void* x, void* y, float* stat
                      : launch<256, 4, MODE_IM2COL, EV_SCATTER>(cp, x, y, nullptr, e, st);
     }
   }
+  const bool pair = tma_a && pair_ok(cp);
   if (e.mode == EPI_BIAS || e.mode == EPI_GELU_BWD) {
     // linear layers (a 1x1 conv over [tokens][features]): bias epilogue, or
     // the MLP input gradient times gelu' of the saved pre-activation
@@ -1176,7 +1256,9 @@ cudaError_t conv_forward(const ConvPlan& cp, const void* x, void* y, float* stat
       switch (cp.bn) {
         case 64: return launch<64, 8, MODE_TMA, EV_BIAS>(cp, x, y, nullptr, e, st);
         case 128: return launch<128, 6, MODE_TMA, EV_BIAS>(cp, x, y, nullptr, e, st);
-        default: return launch<256, 4, MODE_TMA, EV_BIAS>(cp, x, y, nullptr, e, st);
+        default:
+          return pair ? launch<256, 6, MODE_TMA, EV_BIAS, false, true>(cp, x, y, nullptr, e, st)
+                      : launch<256, 4, MODE_TMA, EV_BIAS>(cp, x, y, nullptr, e, st);
       }
     }
     if (!e.xc || !operands_tma()) return cudaErrorInvalidValue;
@@ -1257,6 +1339,7 @@ cudaError_t conv_forward(const ConvPlan& cp, const void* x, void* y, float* stat
              : use_gather ? launch<128, 6, MODE_GATHER, EV_STORE>(cp, x, y, stats, e, st)
                           : launch<128, 6, MODE_IM2COL, EV_STORE>(cp, x, y, stats, e, st);
     default:
+      if (pair) return launch<256, 6, MODE_TMA, EV_STORE, false, true>(cp, x, y, stats, e, st);
       return stem ? launch<256, 4, MODE_STEM, EV_STORE>(cp, x, y, stats, e, st)
              : tma_a ? launch<256, 4, MODE_TMA, EV_STORE>(cp, x, y, stats, e, st)
              : use_gather ? launch<256, 4, MODE_GATHER, EV_STORE>(cp, x, y, stats, e, st)

@@ -15,6 +15,7 @@ struct ConvPlan {
   int P, Q, kdim, bn;
   int halo, halo_slot, halo_rows;  // 3x3 stride-1: input halo staged per tile (conv_halo.cu)
   int stem_rows;                   // C=4 stem: one output row per tile (conv_fwd.cu MODE_STEMROW)
+  const void* wptr;                // the weights (pair mode encodes its half-tile map per launch)
   alignas(64) unsigned char wmap[128];  // CUtensorMap over the [K][kdim] weight matrix
 };
 // Fused epilogues (the backward pass runs input-gradient convolutions through

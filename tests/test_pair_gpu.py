@@ -1,0 +1,31 @@
+"""CTA-pair (cta_group::2, M=256) tiles of the 1x1 GEMM path: the same
+outputs as the 1-CTA kernel, bit for bit (each output element is the same
+K-ordered sum), including the per-CTA BN-statistics rows.  Each variant runs
+in its own process (the mode is chosen once per process from DELTA_PAIR)."""
+import os
+import subprocess
+import sys
+
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _run(pair: str, path: str):
+    env = dict(os.environ, DELTA_PAIR=pair)
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "scripts", "pair_check.py"), path],
+                       env=env, capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stderr[-2000:]
+    return r.stdout
+
+
+def test_pair_tiles_bit_identical_to_single_cta(tmp_path):
+    a, b = str(tmp_path / "off.pt"), str(tmp_path / "on.pt")
+    _run("0", a)
+    print(_run("1", b))
+    off, on = torch.load(a), torch.load(b)
+    assert off.keys() == on.keys()
+    bad = [k for k in off if not torch.equal(off[k], on[k])]
+    assert not bad, bad
