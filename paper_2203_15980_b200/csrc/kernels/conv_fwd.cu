@@ -1067,17 +1067,19 @@ bool stem_tma() {
   return v == 1;
 }
 
-// CTA-pair (cta_group::2) tiles for the 1x1 path: N tile 256, at least one
-// wave of pairs; DELTA_PAIR=0 disables, =1 enables (default: off until
-// measured on by default)
+// CTA-pair (cta_group::2) tiles for the 1x1 path: N tile 256, a reduction of
+// >= 512 (measured: +5-13 % on the BERT GEMMs at K = 1024-4096; no gain on the
+// short-K ResNet 1x1 convs, slower at K = 64), no BN statistics (the per-CTA
+// partial rows would change decomposition), at least one wave of pairs.
+// DELTA_PAIR=0 disables.
 int num_sms();
-bool pair_ok(const ConvPlan& cp) {
+bool pair_ok(const ConvPlan& cp, bool stats) {
   static int v = -1;
   if (v < 0) {
     const char* e = std::getenv("DELTA_PAIR");
-    v = (e && e[0] == '1') ? 1 : 0;
+    v = (e && e[0] == '0') ? 0 : 1;
   }
-  if (!v || cp.bn != 256 || cp.C == 4) return false;
+  if (!v || stats || cp.bn != 256 || cp.C == 4 || cp.kdim < 512) return false;
   const int64_t M = int64_t(cp.N) * cp.P * cp.Q;
   const int64_t tiles = (M + 255) / 256 * ((cp.K + 255) / 256);
   return tiles >= num_sms() / 2;
@@ -1246,7 +1248,7 @@ cudaError_t conv_forward(const ConvPlan& cp, const void* x, void* y, float* stat
                      : launch<256, 4, MODE_IM2COL, EV_SCATTER>(cp, x, y, nullptr, e, st);
     }
   }
-  const bool pair = tma_a && pair_ok(cp);
+  const bool pair = tma_a && pair_ok(cp, stats != nullptr);
   if (e.mode == EPI_BIAS || e.mode == EPI_GELU_BWD) {
     // linear layers (a 1x1 conv over [tokens][features]): bias epilogue, or
     // the MLP input gradient times gelu' of the saved pre-activation
