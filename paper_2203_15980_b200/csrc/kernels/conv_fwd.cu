@@ -188,7 +188,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint8_t* smem = align1024(smem_raw);
   // producer signalling lag: a thread keeps LAG+1 stages of gathers in flight
   constexpr uint32_t LAG = STAGES - 2;
-  static_assert(!PAIR || (MODE == MODE_TMA && !OPT && BN == 256), "pair mode: 1x1 TMA path");
+  static_assert(!PAIR || ((MODE == MODE_TMA || MODE == MODE_IM2COL) && BN >= 128),
+                "pair mode: TMA / TMA-im2col operand paths, N tile 128 or 256");
   constexpr uint32_t A_STAGE = BM * 128;
   constexpr uint32_t B_STAGE = (PAIR ? BN / 2 : BN) * 128;  // this CTA's weight rows
   constexpr uint32_t ACC_COLS = BN;
@@ -324,10 +325,18 @@ __global__ void __launch_bounds__(kThreads, 1)
             const uint32_t s = it % STAGES;
             if (it >= STAGES) mbar_wait(&empty[s], ((it / STAGES) - 1) & 1);
             const int r = tap / a.S, sx = tap - r * a.S;
-            mbar_arrive_expect_tx(&full[s], A_STAGE + B_STAGE);
-            tma_load_im2col_4d(sA + s * A_STAGE, &amap, &full[s], c0, wb, hb, n, uint16_t(sx),
-                               uint16_t(r));
-            tma_load_2d(sB + s * B_STAGE, &wmap, &full[s], kb * BK, n0);
+            if constexpr (PAIR) {
+              if (rank == 0) mbar_arrive_expect_tx(&full[s], 2 * (A_STAGE + B_STAGE));
+              tma_load_im2col_4d_pair(sA + s * A_STAGE, &amap, &full[s], c0, wb, hb, n,
+                                      uint16_t(sx), uint16_t(r));
+              tma_load_2d_pair(sB + s * B_STAGE, &wmap, &full[s], kb * BK,
+                               n0 + int(rank) * (BN / 2));
+            } else {
+              mbar_arrive_expect_tx(&full[s], A_STAGE + B_STAGE);
+              tma_load_im2col_4d(sA + s * A_STAGE, &amap, &full[s], c0, wb, hb, n, uint16_t(sx),
+                                 uint16_t(r));
+              tma_load_2d(sB + s * B_STAGE, &wmap, &full[s], kb * BK, n0);
+            }
             c0 += 64;
             if (c0 == a.C) {
               c0 = 0;
@@ -1067,21 +1076,26 @@ bool stem_tma() {
   return v == 1;
 }
 
-// CTA-pair (cta_group::2) tiles for the 1x1 path: N tile 256, a reduction of
-// >= 512 (measured: +5-13 % on the BERT GEMMs at K = 1024-4096; no gain on the
-// short-K ResNet 1x1 convs, slower at K = 64), no BN statistics (the per-CTA
-// partial rows would change decomposition), at least one wave of pairs.
-// DELTA_PAIR=0 disables.
+// CTA-pair (cta_group::2) tiles: N tile 128 or 256, a reduction of >= 512
+// (measured: +5-13 % on the BERT GEMMs at K = 1024-4096; no gain on the
+// short-K ResNet 1x1 convs, slower at K = 64), at least one wave of pairs.
+// Outputs are bit-identical to the 1-CTA tiles; BN-statistics rows are per
+// CTA either way (a pair CTA folds 128-row half tiles).  DELTA_PAIR=0
+// disables; DELTA_PAIR_IM2COL=0 keeps the im2col (3x3, strided) convs on
+// 1-CTA tiles.
 int num_sms();
-bool pair_ok(const ConvPlan& cp, bool stats) {
-  static int v = -1;
+bool pair_ok(const ConvPlan& cp, bool tma_a) {
+  static int v = -1, vi = -1;
   if (v < 0) {
     const char* e = std::getenv("DELTA_PAIR");
     v = (e && e[0] == '0') ? 0 : 1;
+    const char* f = std::getenv("DELTA_PAIR_IM2COL");
+    vi = (f && f[0] == '0') ? 0 : 1;
   }
-  if (!v || stats || cp.bn != 256 || cp.C == 4 || cp.kdim < 512) return false;
+  if (!v || (cp.bn != 256 && cp.bn != 128) || cp.C == 4 || cp.kdim < 512) return false;
+  if (!tma_a && (!vi || cp.halo || gather_forced())) return false;
   const int64_t M = int64_t(cp.N) * cp.P * cp.Q;
-  const int64_t tiles = (M + 255) / 256 * ((cp.K + 255) / 256);
+  const int64_t tiles = (M + 255) / 256 * ((cp.K + cp.bn - 1) / cp.bn);
   return tiles >= num_sms() / 2;
 }
 
@@ -1248,7 +1262,7 @@ cudaError_t conv_forward(const ConvPlan& cp, const void* x, void* y, float* stat
                      : launch<256, 4, MODE_IM2COL, EV_SCATTER>(cp, x, y, nullptr, e, st);
     }
   }
-  const bool pair = tma_a && pair_ok(cp, stats != nullptr);
+  const bool pair = pair_ok(cp, tma_a);
   if (e.mode == EPI_BIAS || e.mode == EPI_GELU_BWD) {
     // linear layers (a 1x1 conv over [tokens][features]): bias epilogue, or
     // the MLP input gradient times gelu' of the saved pre-activation
@@ -1259,12 +1273,14 @@ cudaError_t conv_forward(const ConvPlan& cp, const void* x, void* y, float* stat
         case 64: return launch<64, 8, MODE_TMA, EV_BIAS>(cp, x, y, nullptr, e, st);
         case 128: return launch<128, 6, MODE_TMA, EV_BIAS>(cp, x, y, nullptr, e, st);
         default:
-          return pair ? launch<256, 6, MODE_TMA, EV_BIAS, false, true>(cp, x, y, nullptr, e, st)
-                      : launch<256, 4, MODE_TMA, EV_BIAS>(cp, x, y, nullptr, e, st);
+          return pair && tma_a ? launch<256, 6, MODE_TMA, EV_BIAS, false, true>(cp, x, y, nullptr, e, st)
+                               : launch<256, 4, MODE_TMA, EV_BIAS>(cp, x, y, nullptr, e, st);
       }
     }
     if (!e.xc || !operands_tma()) return cudaErrorInvalidValue;
     if (cp.bn == 64) return launch<64, 4, MODE_TMA, EV_GELU_BWD, true>(cp, x, y, nullptr, e, st);
+    if (cp.bn == 128 && pair)
+      return launch<128, 4, MODE_TMA, EV_GELU_BWD, true, true>(cp, x, y, nullptr, e, st);
     if (cp.bn == 128)
       return launch<128, opt_stages<EV_GELU_BWD>(), MODE_TMA, EV_GELU_BWD, true>(cp, x, y, nullptr,
                                                                                  e, st);
@@ -1336,12 +1352,17 @@ cudaError_t conv_forward(const ConvPlan& cp, const void* x, void* y, float* stat
              : use_gather ? launch<64, 8, MODE_GATHER, EV_STORE>(cp, x, y, stats, e, st)
                           : launch<64, 8, MODE_IM2COL, EV_STORE>(cp, x, y, stats, e, st);
     case 128:
+      if (pair)
+        return tma_a ? launch<128, 8, MODE_TMA, EV_STORE, false, true>(cp, x, y, stats, e, st)
+                     : launch<128, 8, MODE_IM2COL, EV_STORE, false, true>(cp, x, y, stats, e, st);
       return stem ? launch<128, 6, MODE_STEM, EV_STORE>(cp, x, y, stats, e, st)
              : tma_a ? launch<128, 6, MODE_TMA, EV_STORE>(cp, x, y, stats, e, st)
              : use_gather ? launch<128, 6, MODE_GATHER, EV_STORE>(cp, x, y, stats, e, st)
                           : launch<128, 6, MODE_IM2COL, EV_STORE>(cp, x, y, stats, e, st);
     default:
-      if (pair) return launch<256, 6, MODE_TMA, EV_STORE, false, true>(cp, x, y, stats, e, st);
+      if (pair)
+        return tma_a ? launch<256, 6, MODE_TMA, EV_STORE, false, true>(cp, x, y, stats, e, st)
+                     : launch<256, 6, MODE_IM2COL, EV_STORE, false, true>(cp, x, y, stats, e, st);
       return stem ? launch<256, 4, MODE_STEM, EV_STORE>(cp, x, y, stats, e, st)
              : tma_a ? launch<256, 4, MODE_TMA, EV_STORE>(cp, x, y, stats, e, st)
              : use_gather ? launch<256, 4, MODE_GATHER, EV_STORE>(cp, x, y, stats, e, st)
