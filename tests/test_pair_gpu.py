@@ -2,6 +2,7 @@
 outputs as the 1-CTA kernel, bit for bit (each output element is the same
 K-ordered sum), including the per-CTA BN-statistics rows.  Each variant runs
 in its own process (the mode is chosen once per process from DELTA_PAIR)."""
+import json
 import os
 import subprocess
 import sys
@@ -18,17 +19,20 @@ def _run(pair: str, path: str):
     r = subprocess.run([sys.executable, os.path.join(ROOT, "scripts", "pair_check.py"), path],
                        env=env, capture_output=True, text=True, timeout=300)
     assert r.returncode == 0, r.stderr[-2000:]
-    return r.stdout
+    return json.loads(r.stdout.strip().splitlines()[-1])["times"]
 
 
 def test_pair_tiles_bit_identical_to_single_cta(tmp_path):
     a, b = str(tmp_path / "off.pt"), str(tmp_path / "on.pt")
     _run("0", a)
-    print(_run("1", b))
+    times = _run("1", b)
     off, on = torch.load(a), torch.load(b)
     assert off.keys() == on.keys()
-    bad = [k for k in off if not torch.equal(off[k], on[k])]
+    # outputs bit for bit; the raw per-CTA BN-statistics rows legitimately
+    # differ (a pair CTA folds 128-row half tiles), so those are checked
+    # merged, against the statistics of the output itself
+    bad = [k for k in off if not k.endswith("_stats") and not torch.equal(off[k], on[k])]
     assert not bad, bad
-    # (pair tiles are never used with BN statistics: the per-CTA partial rows
-    # would cover different row sets; pair_ok declines those launches, so the
-    # statistics rows are the 1-CTA kernel's in both runs)
+    for k, v in times.items():
+        if k.endswith("_stats_err"):
+            assert v["mean"] < 1e-6 and v["invstd_rel"] < 1e-5, (k, v)
