@@ -108,8 +108,11 @@ void delta_conv_destroy(delta_conv* c);
 /* ---- backward: convolution weight gradient ----
  * dW[k][r][s][c] = sum over output pixels of dY[n,p,q,k] * X[n, p*st-pad+r,
  * q*st-pad+s, c]; fp32 KRSC output (overwritten), deterministic split-K over
- * pixels (tcgen05, MN-major operands).  C == 4 is the 7x7/2 stem (input
- * channel 3 is the zero pad).  `ws` must hold delta_wgrad_workspace_bytes. */
+ * pixels (tcgen05, MN-major operands): the last split of each tile to land
+ * sums the tile's partials in split order (one launch, no atomics on data).
+ * C == 4 is the 7x7/2 stem (input channel 3 is the zero pad).  `ws` must hold
+ * delta_wgrad_workspace_bytes and be ZEROED once at allocation (it carries
+ * self-resetting per-tile split counters); one launch at a time per `ws`. */
 typedef struct delta_wgrad delta_wgrad;
 delta_status delta_wgrad_create(int32_t N, int32_t H, int32_t W, int32_t C, int32_t K, int32_t R,
                                 int32_t S, int32_t stride, int32_t pad, delta_wgrad** out);

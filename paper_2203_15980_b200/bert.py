@@ -306,7 +306,7 @@ class BertRuntime(DeltaRuntime):
             self._lin_d[name] = d
             self._lin_w[name] = K.Wgrad(T, 1, 1, cin, cout, 1, 1, 1, 0)
             wg_ws = max(wg_ws, self._lin_w[name].workspace_bytes)
-        self.wg_ws = torch.empty(wg_ws, dtype=torch.uint8, device=dev)
+        self.wg_ws = torch.zeros(wg_ws, dtype=torch.uint8, device=dev)  # split counters: zero once
         self.ln_ws = torch.empty(K.layernorm_bwd_workspace_floats(T, H), device=dev)
         self.cs_ws = torch.empty(max(K.colsum_workspace_floats(T, cfg.ffn),
                                      K.span_head_workspace_floats(T, H)), device=dev)

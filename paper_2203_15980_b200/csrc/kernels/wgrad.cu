@@ -55,7 +55,10 @@ struct WgArgs {
   int tiles;         // tiles_m * ceil(ntot / BN) (stem: tiles_m)
   int splits, kb_per_split;
   int items;         // splits * tiles
-  float* ws;         // [items][128 * MT][BN] fp32 partials
+  float* ws;         // [items][128 * MT][BN] fp32 partials (splits > 1, and the stem)
+  float* dw;         // fp32 [K][ntot] gradient (non-stem modes: written by this kernel)
+  unsigned* counters;  // [tiles] splits landed per tile (zero at allocation, self-resetting)
+  int fused;         // finish the gradient in this kernel (else: partials + the reduce launch)
 };
 
 __device__ __forceinline__ uint8_t* align1024(uint8_t* p) {
@@ -327,6 +330,13 @@ __global__ void __launch_bounds__(WG_THREADS, 1)
     }
   } else {
     // =============================== epilogue ================================
+    // Non-stem modes finish the gradient here: one split -> straight into the
+    // fp32 KRSC gradient; several -> fp32 partial tiles, and the LAST split of
+    // a tile to land (device-scope counter) sums the tile's partials in split
+    // order into the gradient (deterministic whichever CTA is last; no
+    // separate reduce launch).  The stem keeps its layout-permuting reduce.
+    constexpr bool STEMLIKE = MODE == WG_STEM || MODE == WG_STEMRAW;
+    __shared__ int s_last;
     const int quarter = warp & 3;
     uint32_t lt = 0;
     for (int item = blockIdx.x; item < a.items; item += gridDim.x, ++lt) {
@@ -336,12 +346,25 @@ __global__ void __launch_bounds__(WG_THREADS, 1)
       // WG_STEMRAW (M=64 MMAs): this quarter's lanes 0-15 hold rows 16q..16q+15
       const int row = MODE == WG_STEMRAW ? quarter * 16 + lane : quarter * 32 + lane;
       const bool live = MODE != WG_STEMRAW || lane < 16;
+      int m0, n0, kb0, kb1;
+      decode(item, m0, n0, kb0, kb1);
+      const bool direct = !STEMLIKE && a.fused && a.splits == 1;
       for (int h = 0; h < MT; ++h) {
       float* out = a.ws + (size_t(item) * 128 * MT + h * 128 + row) * BN;
+      const int k = m0 + h * 128 + row;
 #pragma unroll 1
       for (int j = 0; j < BN / 32; ++j) {
         float v[32];
         tmem_ld_32x32b_x32(tmem + (uint32_t(quarter * 32) << 16) + (acc + h) * BN + j * 32, v);
+        if (direct) {
+          if (k < a.K && n0 + j * 32 < a.ntot) {
+            float4* o = reinterpret_cast<float4*>(a.dw + size_t(k) * a.ntot + n0 + j * 32);
+#pragma unroll
+            for (int u = 0; u < 8; ++u)
+              o[u] = make_float4(v[4 * u], v[4 * u + 1], v[4 * u + 2], v[4 * u + 3]);
+          }
+          continue;
+        }
         float4* o = reinterpret_cast<float4*>(out + j * 32);
         if (live) {
 #pragma unroll
@@ -353,6 +376,49 @@ __global__ void __launch_bounds__(WG_THREADS, 1)
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&tempty[acc]);
+      if (!STEMLIKE && a.fused && !direct) {
+        // publish this split's partial, then count it in
+        __threadfence();
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+        const int tile = item % a.tiles;
+        if (threadIdx.x == 64) {
+          const unsigned prev = atomicAdd(a.counters + tile, 1u);
+          s_last = prev == unsigned(a.splits - 1);
+          if (s_last) a.counters[tile] = 0u;  // ready for the next launch
+        }
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+        if (s_last) {
+          __threadfence();
+          for (int h = 0; h < MT; ++h) {
+            const int k = m0 + h * 128 + row;
+            if (k >= a.K) continue;
+            const size_t base = (size_t(tile) * 128 * MT + h * 128 + row) * BN;
+            const size_t sstride = size_t(a.tiles) * 128 * MT * BN;
+#pragma unroll 1
+            for (int j = 0; j < BN / 32; ++j) {
+              if (n0 + j * 32 >= a.ntot) break;
+              float4 acc4[8];
+#pragma unroll
+              for (int u = 0; u < 8; ++u) acc4[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+              for (int sp = 0; sp < a.splits; ++sp) {
+                const float4* src =
+                    reinterpret_cast<const float4*>(a.ws + sp * sstride + base + j * 32);
+#pragma unroll
+                for (int u = 0; u < 8; ++u) {
+                  const float4 t = __ldcg(src + u);
+                  acc4[u].x += t.x;
+                  acc4[u].y += t.y;
+                  acc4[u].z += t.z;
+                  acc4[u].w += t.w;
+                }
+              }
+              float4* o = reinterpret_cast<float4*>(a.dw + size_t(k) * a.ntot + n0 + j * 32);
+#pragma unroll
+              for (int u = 0; u < 8; ++u) o[u] = acc4[u];
+            }
+          }
+        }
+      }
     }
   }
   tc_fence_before();
@@ -424,6 +490,15 @@ int num_sms_wg() {
   return n;
 }
 
+bool fused_reduce_off() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = std::getenv("DELTA_WGRAD_FUSED_REDUCE");
+    v = (e && e[0] == '0') ? 1 : 0;
+  }
+  return v == 1;
+}
+
 template <int BN, int MODE, int MT = 1>
 cudaError_t wg_launch(const WgradPlan& wp, const void* dy, const void* x, float* dw, float* ws,
                       cudaStream_t st) {
@@ -449,6 +524,10 @@ cudaError_t wg_launch(const WgradPlan& wp, const void* dy, const void* x, float*
   a.kb_per_split = wp.kb_per_split;
   a.items = wp.splits * wp.tiles;
   a.ws = ws;
+  a.dw = dw;
+  a.fused = fused_reduce_off() ? 0 : 1;
+  a.counters = reinterpret_cast<unsigned*>(
+      reinterpret_cast<char*>(ws) + size_t(wp.splits) * wp.tiles * 128 * MT * BN * sizeof(float));
   alignas(64) CUtensorMap amap, bmap;
   if (!tma_2d_bf16(&amap, dy, uint64_t(wp.K), uint64_t(a.M), uint64_t(wp.K), 64,
                    MODE == WG_STEMRAW ? uint32_t(wp.Q) : uint32_t(KPIX), CU_TENSOR_MAP_SWIZZLE_128B))
@@ -475,7 +554,7 @@ cudaError_t wg_launch(const WgradPlan& wp, const void* dy, const void* x, float*
   if (e != cudaSuccess) return e;
   if (MODE == WG_STEM || MODE == WG_STEMRAW) {
     if (cudaError_t e_ = launch_k(k_wgrad_reduce_stem, dim3((wp.K * 196 + 255) / 256), dim3(256), 0, st, ws, dw, wp.K, wp.splits, wp.tiles)) return e_;
-  } else {
+  } else if (fused_reduce_off()) {  // DELTA_WGRAD_FUSED_REDUCE=0: the separate reduce (A/B)
     const int64_t total = int64_t(wp.K) * a.ntot;
     const int64_t blocks = std::min<int64_t>((total + 255) / 256, 148 * 16);
     if (cudaError_t e_ = launch_k(k_wgrad_reduce<BN, 128 * MT>, dim3(int(blocks)), dim3(256), 0, st, ws, dw, wp.K, a.ntot, a.tiles_m, wp.tiles, wp.splits)) return e_;
@@ -550,7 +629,9 @@ int wgrad_plan_init(WgradPlan* wp) {
 }
 
 size_t wgrad_workspace_bytes(const WgradPlan& wp) {
-  return size_t(wp.splits) * wp.tiles * 128 * wp.mt * wp.bn * sizeof(float);
+  // partial tiles + the per-tile split counters (must be zero at allocation)
+  return size_t(wp.splits) * wp.tiles * 128 * wp.mt * wp.bn * sizeof(float) +
+         (size_t(wp.tiles) * sizeof(unsigned) + 15) / 16 * 16;
 }
 
 cudaError_t wgrad(const WgradPlan& wp, const void* dy, const void* x, float* dw, float* ws,

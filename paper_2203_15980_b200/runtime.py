@@ -300,7 +300,8 @@ class DeltaRuntime:
         # shortcut conv at its sampling grid
         self.short_ws = u8("short_ws")
         self.mp_ws = u8("mp_ws")
-        self.wg_ws = u8("wgrad_ws")  # weight-gradient partials (side stream: serial use)
+        # weight-gradient partials + split counters (zeroed once; side stream: serial use)
+        self.wg_ws = torch.zeros(ws["wgrad_ws"], dtype=torch.uint8, device=self.device)
         # a stride-2 3x3 input gradient between its sub-pixel convs and its BN backward
         self.dg_ws = u8("transient")
         ncls = self.g.fc[1]

@@ -428,7 +428,7 @@ def test_wgrad_matches_fp32_reference(case):
     P_, Q_ = (H + 2 * pad - R) // st + 1, (W + 2 * pad - R) // st + 1
     dy = torch.randn(N, P_, Q_, Kout, device="cuda", generator=g).to(torch.bfloat16)
     wg = K.Wgrad(N, H, W, Cin, Kout, R, R, st, pad)
-    ws = torch.empty(wg.workspace_bytes, dtype=torch.uint8, device="cuda")
+    ws = torch.zeros(wg.workspace_bytes, dtype=torch.uint8, device="cuda")  # zero at allocation
     dw = torch.full((Kout, R, R, Cin), float("nan"), device="cuda")
     wg(dy.data_ptr(), x.data_ptr(), dw.data_ptr(), ws.data_ptr(), _stream())
     torch.cuda.synchronize()
@@ -449,7 +449,7 @@ def test_wgrad_stem_pairs():
     x[..., :3] = torch.randn(N, H, W, 3, device="cuda", generator=g).to(torch.bfloat16)
     dy = torch.randn(N, 112, 112, 64, device="cuda", generator=g).to(torch.bfloat16)
     wg = K.Wgrad(N, H, W, 4, 64, 7, 7, 2, 3)
-    ws = torch.empty(wg.workspace_bytes, dtype=torch.uint8, device="cuda")
+    ws = torch.zeros(wg.workspace_bytes, dtype=torch.uint8, device="cuda")  # zero at allocation
     dw = torch.full((64, 7, 7, 4), float("nan"), device="cuda")
     wg(dy.data_ptr(), x.data_ptr(), dw.data_ptr(), ws.data_ptr(), _stream())
     torch.cuda.synchronize()
@@ -567,7 +567,7 @@ def test_classifier_head_on_tensor_cores():
     da = torch.empty(N, cin, device="cuda", dtype=torch.bfloat16)
     fcd(dlb.data_ptr(), da.data_ptr(), _stream())
     dw = torch.empty(pad, cin, device="cuda")
-    ws = torch.empty(wg.workspace_bytes, dtype=torch.uint8, device="cuda")
+    ws = torch.zeros(wg.workspace_bytes, dtype=torch.uint8, device="cuda")  # zero at allocation
     wg(dlb.data_ptr(), a.data_ptr(), dw.data_ptr(), ws.data_ptr(), _stream())
     torch.cuda.synchronize()
     af = a.float().requires_grad_(True)
