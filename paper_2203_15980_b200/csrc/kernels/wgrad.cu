@@ -40,6 +40,8 @@ namespace {
 constexpr int WG_THREADS = 192;
 constexpr int KPIX = 64;  // pixels per k-block
 constexpr int WG_PLAIN = 0, WG_IM2COL = 1, WG_STEM = 2, WG_STEMRAW = 3;
+// head of the workspace: per-tile split counters (up to 4096 tiles)
+constexpr size_t WG_COUNTER_BYTES = 16384;
 // WG_STEMRAW: a k-block is one output row (n, p) of the stem; its 7 input
 // rows are staged raw (pixel pairs, zero pads around them, conv_fwd.cu
 // MODE_STEMRAW) and the B operand is addressed straight into them
@@ -523,11 +525,13 @@ cudaError_t wg_launch(const WgradPlan& wp, const void* dy, const void* x, float*
   a.splits = wp.splits;
   a.kb_per_split = wp.kb_per_split;
   a.items = wp.splits * wp.tiles;
+  // the split counters sit at a FIXED place at the head of the workspace (every
+  // weight gradient sharing the buffer leaves them zero), the partials after it
+  a.counters = reinterpret_cast<unsigned*>(ws);
+  ws = reinterpret_cast<float*>(reinterpret_cast<char*>(ws) + WG_COUNTER_BYTES);
   a.ws = ws;
   a.dw = dw;
-  a.fused = fused_reduce_off() ? 0 : 1;
-  a.counters = reinterpret_cast<unsigned*>(
-      reinterpret_cast<char*>(ws) + size_t(wp.splits) * wp.tiles * 128 * MT * BN * sizeof(float));
+  a.fused = (fused_reduce_off() || wp.tiles > int(WG_COUNTER_BYTES / 4)) ? 0 : 1;
   alignas(64) CUtensorMap amap, bmap;
   if (!tma_2d_bf16(&amap, dy, uint64_t(wp.K), uint64_t(a.M), uint64_t(wp.K), 64,
                    MODE == WG_STEMRAW ? uint32_t(wp.Q) : uint32_t(KPIX), CU_TENSOR_MAP_SWIZZLE_128B))
@@ -629,9 +633,8 @@ int wgrad_plan_init(WgradPlan* wp) {
 }
 
 size_t wgrad_workspace_bytes(const WgradPlan& wp) {
-  // partial tiles + the per-tile split counters (must be zero at allocation)
-  return size_t(wp.splits) * wp.tiles * 128 * wp.mt * wp.bn * sizeof(float) +
-         (size_t(wp.tiles) * sizeof(unsigned) + 15) / 16 * 16;
+  // the per-tile split counters (must be zero at allocation) + partial tiles
+  return WG_COUNTER_BYTES + size_t(wp.splits) * wp.tiles * 128 * wp.mt * wp.bn * sizeof(float);
 }
 
 cudaError_t wgrad(const WgradPlan& wp, const void* dy, const void* x, float* dw, float* ws,
