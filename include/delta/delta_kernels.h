@@ -117,6 +117,9 @@ typedef struct delta_wgrad delta_wgrad;
 delta_status delta_wgrad_create(int32_t N, int32_t H, int32_t W, int32_t C, int32_t K, int32_t R,
                                 int32_t S, int32_t stride, int32_t pad, delta_wgrad** out);
 uint64_t delta_wgrad_workspace_bytes(const delta_wgrad* w);
+/* kernel launches one delta_wgrad_run issues (1, or 2 with a separate split
+ * reduce: the stem, and tiles split more than 4-way over the pixels) */
+int32_t delta_wgrad_launches(const delta_wgrad* w);
 delta_status delta_wgrad_run(const delta_wgrad* w, const void* dy, const void* x, float* dw, void* ws,
                          void* stream);
 void delta_wgrad_destroy(delta_wgrad* w);

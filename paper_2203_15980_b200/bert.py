@@ -445,7 +445,7 @@ class BertRuntime(DeltaRuntime):
             else:
                 add(X.kop(X.K_CONV, (dy, X.OUT(), None), conv=dconv))
             add(X.kop(X.K_WGRAD, (dy, X.IN(1), _ptr(pr.gviews["w:" + lin]), _ptr(self.wg_ws)),
-                      conv=self._lin_w[lin]._h))
+                      conv=self._lin_w[lin]._h), self._lin_w[lin].launches)
             add(X.kop(X.K_COLSUM, (dy, None, _ptr(pr.gviews["b:" + lin]), _ptr(self.cs_ws)),
                       (T, cout, 0, 0)), 2)
         elif op == "attention_bwd":

@@ -76,6 +76,7 @@ struct WgradPlan {
 // 0 ok, 1 unsupported shape
 int wgrad_plan_init(WgradPlan* wp);
 size_t wgrad_workspace_bytes(const WgradPlan& wp);
+int wgrad_launches(const WgradPlan& wp);  // 1, or 2 with the separate split reduce
 // dw: fp32 [K][R][S][C] (overwritten); ws: wgrad_workspace_bytes of scratch
 cudaError_t wgrad(const WgradPlan& wp, const void* dy, const void* x, float* dw, float* ws,
                   cudaStream_t st);

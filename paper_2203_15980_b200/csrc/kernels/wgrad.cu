@@ -42,6 +42,7 @@ constexpr int KPIX = 64;  // pixels per k-block
 constexpr int WG_PLAIN = 0, WG_IM2COL = 1, WG_STEM = 2, WG_STEMRAW = 3;
 // head of the workspace: per-tile split counters (up to 4096 tiles)
 constexpr size_t WG_COUNTER_BYTES = 16384;
+constexpr int WG_FUSE_MAX_SPLITS = 4;
 // WG_STEMRAW: a k-block is one output row (n, p) of the stem; its 7 input
 // rows are staged raw (pixel pairs, zero pads around them, conv_fwd.cu
 // MODE_STEMRAW) and the B operand is addressed straight into them
@@ -402,18 +403,27 @@ __global__ void __launch_bounds__(WG_THREADS, 1)
               float4 acc4[8];
 #pragma unroll
               for (int u = 0; u < 8; ++u) acc4[u] = make_float4(0.f, 0.f, 0.f, 0.f);
-              for (int sp = 0; sp < a.splits; ++sp) {
-                const float4* src =
-                    reinterpret_cast<const float4*>(a.ws + sp * sstride + base + j * 32);
+              // every split's chunk in flight at once, summed in split order
+              float4 t[WG_FUSE_MAX_SPLITS][8];
 #pragma unroll
-                for (int u = 0; u < 8; ++u) {
-                  const float4 t = __ldcg(src + u);
-                  acc4[u].x += t.x;
-                  acc4[u].y += t.y;
-                  acc4[u].z += t.z;
-                  acc4[u].w += t.w;
+              for (int sp = 0; sp < WG_FUSE_MAX_SPLITS; ++sp)
+                if (sp < a.splits) {
+                  const float4* src =
+                      reinterpret_cast<const float4*>(a.ws + sp * sstride + base + j * 32);
+#pragma unroll
+                  for (int u = 0; u < 8; ++u) t[sp][u] = __ldcg(src + u);
                 }
-              }
+#pragma unroll
+              for (int sp = 0; sp < WG_FUSE_MAX_SPLITS; ++sp)
+                if (sp < a.splits) {
+#pragma unroll
+                  for (int u = 0; u < 8; ++u) {
+                    acc4[u].x += t[sp][u].x;
+                    acc4[u].y += t[sp][u].y;
+                    acc4[u].z += t[sp][u].z;
+                    acc4[u].w += t[sp][u].w;
+                  }
+                }
               float4* o = reinterpret_cast<float4*>(a.dw + size_t(k) * a.ntot + n0 + j * 32);
 #pragma unroll
               for (int u = 0; u < 8; ++u) o[u] = acc4[u];
@@ -531,7 +541,11 @@ cudaError_t wg_launch(const WgradPlan& wp, const void* dy, const void* x, float*
   ws = reinterpret_cast<float*>(reinterpret_cast<char*>(ws) + WG_COUNTER_BYTES);
   a.ws = ws;
   a.dw = dw;
-  a.fused = (fused_reduce_off() || wp.tiles > int(WG_COUNTER_BYTES / 4)) ? 0 : 1;
+  // fused finish only for few splits: the last split's CTA sums the tile alone
+  // (with many splits the all-SM reduce launch is faster: 28 vs 21 ms/step for
+  // ResNet-50, whose 1x1 weight gradients split 100-way over the pixels)
+  a.fused = (fused_reduce_off() || wp.tiles > int(WG_COUNTER_BYTES / 4) ||
+             wp.splits > WG_FUSE_MAX_SPLITS) ? 0 : 1;
   alignas(64) CUtensorMap amap, bmap;
   if (!tma_2d_bf16(&amap, dy, uint64_t(wp.K), uint64_t(a.M), uint64_t(wp.K), 64,
                    MODE == WG_STEMRAW ? uint32_t(wp.Q) : uint32_t(KPIX), CU_TENSOR_MAP_SWIZZLE_128B))
@@ -558,7 +572,7 @@ cudaError_t wg_launch(const WgradPlan& wp, const void* dy, const void* x, float*
   if (e != cudaSuccess) return e;
   if (MODE == WG_STEM || MODE == WG_STEMRAW) {
     if (cudaError_t e_ = launch_k(k_wgrad_reduce_stem, dim3((wp.K * 196 + 255) / 256), dim3(256), 0, st, ws, dw, wp.K, wp.splits, wp.tiles)) return e_;
-  } else if (fused_reduce_off()) {  // DELTA_WGRAD_FUSED_REDUCE=0: the separate reduce (A/B)
+  } else if (!a.fused) {  // many splits, or DELTA_WGRAD_FUSED_REDUCE=0: the all-SM reduce
     const int64_t total = int64_t(wp.K) * a.ntot;
     const int64_t blocks = std::min<int64_t>((total + 255) / 256, 148 * 16);
     if (cudaError_t e_ = launch_k(k_wgrad_reduce<BN, 128 * MT>, dim3(int(blocks)), dim3(256), 0, st, ws, dw, wp.K, a.ntot, a.tiles_m, wp.tiles, wp.splits)) return e_;
@@ -630,6 +644,13 @@ int wgrad_plan_init(WgradPlan* wp) {
   p.kb_per_split = (kblocks + splits - 1) / splits;
   p.splits = (kblocks + p.kb_per_split - 1) / p.kb_per_split;
   return 0;
+}
+
+int wgrad_launches(const WgradPlan& wp) {
+  const bool stem = wp.mode == WG_STEM || wp.mode == WG_STEMRAW;
+  const bool fused = !fused_reduce_off() && wp.tiles <= int(WG_COUNTER_BYTES / 4) &&
+                     wp.splits <= WG_FUSE_MAX_SPLITS;
+  return stem || !fused ? 2 : 1;
 }
 
 size_t wgrad_workspace_bytes(const WgradPlan& wp) {

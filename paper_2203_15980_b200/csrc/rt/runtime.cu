@@ -111,6 +111,8 @@ delta_status delta_wgrad_create(int32_t N, int32_t H, int32_t W, int32_t C, int3
   return DELTA_OK;
 }
 
+int32_t delta_wgrad_launches(const delta_wgrad* w) { return delta_k::wgrad_launches(w->plan); }
+
 uint64_t delta_wgrad_workspace_bytes(const delta_wgrad* w) {
   return delta_k::wgrad_workspace_bytes(w->plan);
 }

@@ -23,6 +23,7 @@ _SIGS = {
     "delta_conv_set_tile_n": (i32, [vp, i32]),
     "delta_wgrad_create": (i32, [i32] * 9 + [P(vp)]),
     "delta_wgrad_workspace_bytes": (u64, [vp]),
+    "delta_wgrad_launches": (i32, [vp]),
     "delta_wgrad_run": (i32, [vp, vp, vp, vp, vp, vp]),
     "delta_wgrad_destroy": (None, [vp]),
     "delta_bn_backward_from_partials": (i32, [vp, vp, vp, vp, i64, i32, vp, vp, vp, vp, vp, vp]),
@@ -151,11 +152,11 @@ class Wgrad:
         self._h = vp()
         check(lib.delta_wgrad_create(N, H, W, Cin, K, R, S, stride, pad, C.byref(self._h)))
         self.workspace_bytes = int(lib.delta_wgrad_workspace_bytes(self._h))
-        self.shape = (N, H, W, Cin, K, R, S, stride, pad)
+        self.launches = int(lib.delta_wgrad_launches(self._h))
 
     def __call__(self, dy_ptr: int, x_ptr: int, dw_ptr: int, ws_ptr: int, stream: int):
         check(lib.delta_wgrad_run(self._h, dy_ptr, x_ptr, dw_ptr, ws_ptr, stream))
-        _count(2 if self.shape[3] == 4 else 1)  # the stem keeps its reduce launch
+        _count(self.launches)
 
     def __del__(self):
         if getattr(self, "_h", None) and lib is not None:

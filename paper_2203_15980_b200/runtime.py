@@ -558,7 +558,7 @@ class DeltaRuntime:
             add(X.kop(X.K_CONV, (_ptr(self.dlogits_bf16), X.OUT(), None), conv=self._fc_d._h))
             add(X.kop(X.K_WGRAD, (_ptr(self.dlogits_bf16), X.IN(1),
                                   _ptr(pr.gviews["fc_w_full"]), _ptr(self.wg_ws)),
-                      conv=self._fc_w._h), 1, 1)
+                      conv=self._fc_w._h), self._fc_w.launches, self._fc_w.launches)
         elif op == "bn_add_relu_bwd":
             # parents: [upstream, (O if masked,) X]; upstream already masked
             # unless it is the pooled head gradient
@@ -595,7 +595,7 @@ class DeltaRuntime:
                           + (gb(bn)[0],) + dgb(bn) + (_ptr(self.bn_ws),), (0, M, C)), bwd_n, bwd_n)
             else:
                 raise RuntimeError(f"{node.name}: no input-gradient kernel for conv {conv}")
-            add(wgrad(conv, 0, 1), 1, 1)
+            add(wgrad(conv, 0, 1), *(self._wgrads[conv].launches,) * 2)
         elif op == "conv_shortcut_bwd":
             # out = (dgrad(conv1, dC1) + shortcut gradient) * [X > 0]; the sum
             # and the mask are the dgrad kernel's epilogue
@@ -613,7 +613,7 @@ class DeltaRuntime:
                     add_ = dst
                 else:
                     raise RuntimeError(f"{node.name}: shortcut conv {short} must be a 1x1")
-                add(wgrad(short, 2, 1), 1, 1)
+                add(wgrad(short, 2, 1), *(self._wgrads[short].launches,) * 2)
             elif node.attrs.get("from_pool"):
                 add_, pool_hw, add_mask = X.IN(2), int(node.shape[1] * node.shape[2]), X.IN(3)
             else:
@@ -628,7 +628,7 @@ class DeltaRuntime:
             else:
                 add(X.kop(X.K_CONV_EX, (X.IN(0), X.OUT(), None, add_, add_mask, out_mask),
                           (K.EPI_ADD_MASK, pool_hw, stride2), conv=self._dconvs[conv]._h))
-            add(wgrad(conv, 0, 1), 1, 1)
+            add(wgrad(conv, 0, 1), *(self._wgrads[conv].launches,) * 2)
         elif op == "conv_bwd":
             # a conv fed by a maxpool (imported chains): plain input gradient on
             # the tensor cores + weight gradient
@@ -636,7 +636,7 @@ class DeltaRuntime:
             if conv not in self._dconvs:
                 raise RuntimeError(f"{node.name}: no input-gradient kernel for conv {conv}")
             add(X.kop(X.K_CONV, (X.IN(0), X.OUT(), None), conv=self._dconvs[conv]._h))
-            add(wgrad(conv, 0, 1), 1, 1)
+            add(wgrad(conv, 0, 1), *(self._wgrads[conv].launches,) * 2)
         elif op == "maxpool_bwd":
             Nb, H, W, Cs = self.nodes[node.parents[1]].shape
             add(X.kop(X.K_MAXPOOL_BWD, (X.IN(0), X.IN(1), X.OUT(), _ptr(self.mp_ws)),
