@@ -42,7 +42,7 @@ constexpr int KPIX = 64;  // pixels per k-block
 constexpr int WG_PLAIN = 0, WG_IM2COL = 1, WG_STEM = 2, WG_STEMRAW = 3;
 // head of the workspace: per-tile split counters (up to 4096 tiles)
 constexpr size_t WG_COUNTER_BYTES = 16384;
-constexpr int WG_FUSE_MAX_SPLITS = 4;
+constexpr int WG_FUSE_MAX_SPLITS = 1;  // measured: last-CTA sums of 2-4 splits -1 % ResNet, BERT neutral
 // WG_STEMRAW: a k-block is one output row (n, p) of the stem; its 7 input
 // rows are staged raw (pixel pairs, zero pads around them, conv_fwd.cu
 // MODE_STEMRAW) and the B operand is addressed straight into them
