@@ -38,27 +38,41 @@ def _batch(seed):
     return x, y
 
 
-def _worker(rank, world, port, q):
+def _worker(rank, world, port, q, model="resnet"):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
         torch.cuda.set_device(0)
         from paper_2203_15980_b200.runtime import DeltaRuntime, agree_cost_table
         grp = dist.group.WORLD
-        rt = DeltaRuntime(50, BATCH, seed=0, lr=0.0)
+        if model == "bert":
+            from paper_2203_15980_b200 import bert as B
+            rt = B.BertRuntime(B.BertConfig(layers=2, hidden=256, heads=4, ffn=1024, seq=128,
+                                            batch=2, vocab=512), seed=0, lr=0.0)
+            batch = rt.synthetic_batch(100 + rank, pin=False)[:3]  # a different batch per rank
+        else:
+            rt = DeltaRuntime(50, BATCH, seed=0, lr=0.0)
+            batch = _batch(100 + rank)  # a different batch per rank
         rt.measure_costs(iters=1, link=True)
         rt.link_gbs = agree_cost_table(rt.g, rt.link_gbs, grp)
-        prog = rt.plan(0.5)
-        x, y = _batch(100 + rank)  # a different batch per rank
+        prog = rt.plan(0.5 if model == "resnet" else 0.4)
         # this rank's own gradient (no data parallelism)
-        rt.step(x, y)
+        rt.step(*batch)
         g_local = rt.params.grad.detach().cpu().clone()
-        # the data-parallel step: bucketed all-reduce on the comm stream, SGD
+        # the data-parallel step: bucketed all-reduce on the comm stream, then
+        # the optimizer (optimizer state and the dropout step reset, so the
+        # step sees the same masks and starts from the same state)
         rt.dp = grp
         rt._bound_slot = None  # rebind: ready events for the buckets
-        rt.params.mom.zero_()  # the local step's momentum is rank-specific
-        rt.lr = 0.1
-        rt.step(x, y)
+        if model == "bert":
+            rt.params.m.zero_()
+            rt.params.v.zero_()
+            rt.rng[1] = 0
+            rt.lr = 1e-3
+        else:
+            rt.params.mom.zero_()  # the local step's momentum is rank-specific
+            rt.lr = 0.1
+        rt.step(*batch)
         torch.cuda.synchronize()
         g_dp = rt.params.grad.detach().cpu().clone()
         w = rt.params.master.detach().cpu().clone()
@@ -89,12 +103,13 @@ def _worker(rank, world, port, q):
         dist.destroy_process_group()
 
 
-def test_two_ranks_bucketed_allreduce_real_steps():
+@pytest.mark.parametrize("model", ["resnet", "bert"])
+def test_two_ranks_bucketed_allreduce_real_steps(model):
     world = 2
     port = _free_port()
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
-    ps = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
+    ps = [ctx.Process(target=_worker, args=(r, world, port, q, model)) for r in range(world)]
     for p in ps:
         p.start()
     res = [q.get(timeout=900) for _ in ps]
@@ -108,7 +123,7 @@ def test_two_ranks_bucketed_allreduce_real_steps():
         assert r["grad_is_mean"], r["rank"]
         assert r["weights_equal"], r["rank"]
         b = r["buckets"]
-        assert len(b) >= 3                  # ~25 MB buckets over ~102 MB of gradients
+        assert len(b) >= (3 if model == "resnet" else 1)  # ~25 MB buckets
         assert sorted((lo, hi) for lo, hi, _ in b)[0][0] == 0
         assert sum(hi - lo for lo, hi, _ in b) == r["numel"]
         assert all(phase == "B" for _, _, phase in b)
