@@ -1280,7 +1280,7 @@ cudaError_t conv_forward(const ConvPlan& cp, const void* x, void* y, float* stat
     if (!e.xc || !operands_tma()) return cudaErrorInvalidValue;
     if (cp.bn == 64) return launch<64, 4, MODE_TMA, EV_GELU_BWD, true>(cp, x, y, nullptr, e, st);
     if (cp.bn == 128 && pair)
-      return launch<128, 4, MODE_TMA, EV_GELU_BWD, true, true>(cp, x, y, nullptr, e, st);
+      return launch<128, 5, MODE_TMA, EV_GELU_BWD, true, true>(cp, x, y, nullptr, e, st);
     if (cp.bn == 128)
       return launch<128, opt_stages<EV_GELU_BWD>(), MODE_TMA, EV_GELU_BWD, true>(cp, x, y, nullptr,
                                                                                  e, st);

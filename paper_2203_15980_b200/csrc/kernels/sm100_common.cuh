@@ -268,10 +268,13 @@ __device__ __forceinline__ uint32_t mapa_shared(uint32_t local, uint32_t rank) {
   asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(local), "r"(rank));
   return r;
 }
-// arrive on an mbarrier of another CTA of the cluster (cluster-scope release)
+// arrive on an mbarrier of another CTA of the cluster.  Default semantics
+// (release at CTA scope, as CUTLASS's ClusterBarrier::arrive): the arrival
+// only publishes TMEM reads, ordered by the tcgen05 fences — a cluster-scope
+// release compiled to MEMBAR.GPU per arrival (15 % of the pair epilogue's
+// stall samples).
 __device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
-  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr)
-               : "memory");
+  asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
 }
 // TMA load by either CTA of a pair whose completion bytes land on the LEADER's
 // mbarrier (the barrier address with the peer bit cleared, as CUTLASS's
