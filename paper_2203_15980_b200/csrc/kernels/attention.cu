@@ -134,6 +134,16 @@ __device__ __forceinline__ void store16(bf16* dst, const uint32_t (&v)[16], floa
                       pack_bf16x2(__uint_as_float(v[8 * u + 6]) * s, __uint_as_float(v[8 * u + 7]) * s));
 }
 
+// debug: progress words in mapped host memory (null = off), set by
+// attention_debug(); the host can read them while a kernel is stuck
+__device__ uint32_t* g_attn_dbg = nullptr;
+__device__ __forceinline__ void dbg_mark(int slot, uint32_t v) {
+  uint32_t* d = g_attn_dbg;
+  if (d) {
+    *reinterpret_cast<volatile uint32_t*>(d + (blockIdx.y * gridDim.x + blockIdx.x) * 32 + slot) = v;
+  }
+}
+
 struct AttnArgs {
   int B, S, heads;
   int Hd;        // heads * 64
@@ -176,7 +186,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     fence_mbar_init();
     tma_prefetch_desc(&qkv_map);
   }
+  if (threadIdx.x == 0) dbg_mark(20, 0xF1);
   if (warp == CTRL) tmem_alloc(tslot, tcols);
+  if (threadIdx.x == CTRL * 32) dbg_mark(21, 0xF2);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -320,10 +332,15 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* bar_qd = bars;       // Q, dO landed
   uint64_t* bar_kv = bars + 1;   // K_j / V_j landed
   uint64_t* bar_sp = bars + 3;   // S/dP half computed
-  uint64_t* bar_h = bars + 4;    // half consumed (TMEM read, smem written)
+  uint64_t* bar_h = bars + 4;    // half 0 of a block written to smem (bar_h1: half 1) — one
+                                 // barrier per half, so the MMA warp, which waits for both
+                                 // after issuing the next half early, is never two phases
+                                 // behind (a parity wait cannot tell phase k from k+2)
   uint64_t* bar_acc = bars + 5;  // accumulate MMAs of a block done
   uint64_t* bar_dr = bars + 6;   // dK/dV of a key block drained
-  uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 7);
+  uint64_t* bar_t = bars + 7;    // S/dP half read out of TMEM (the next half may overwrite)
+  uint64_t* bar_h1 = bars + 8;
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 9);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int h = blockIdx.x, b = blockIdx.y;
   const int row0 = b * S;
@@ -335,11 +352,15 @@ __global__ void __launch_bounds__(kThreads, 1)
     mbar_init(bar_h, MATH_W);
     mbar_init(bar_acc, 1);
     mbar_init(bar_dr, MATH_W);
+    mbar_init(bar_t, MATH_W);
+    mbar_init(bar_h1, MATH_W);
     fence_mbar_init();
     tma_prefetch_desc(&qkv_map);
     tma_prefetch_desc(&do_map);
   }
+  if (threadIdx.x == 0) dbg_mark(20, 0xB1);
   if (warp == CTRL) tmem_alloc(tslot, 512);
+  if (threadIdx.x == CTRL * 32) dbg_mark(21, 0xB2);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -389,15 +410,28 @@ __global__ void __launch_bounds__(kThreads, 1)
     mbar_wait(bar_kv, 0);
     tc_fence_after();
     issue_half(0, 0);
+    uint32_t nt_ = 0;  // bar_t completions consumed
     for (int blk = 0; blk < nblk; ++blk) {
       const int j = blk / nt, i = blk % nt;
       const uint32_t kb = sKV;
-      // half 0 consumed -> half 1
-      mbar_wait(bar_h, (nsp - 1) & 1);
+      // S/dP of a half are issued as soon as the previous half has been read
+      // out of TMEM, so they run while the softmax warps still compute
+      if (lane == 0) dbg_mark(16, 0x10000 | blk);
+      mbar_wait(bar_t, nt_++ & 1);
       tc_fence_after();
       issue_half(blk, 1);
-      mbar_wait(bar_h, (nsp - 1) & 1);
+      if (lane == 0) dbg_mark(16, 0x20000 | blk);
+      mbar_wait(bar_t, nt_++ & 1);
       tc_fence_after();
+      if (lane == 0) dbg_mark(16, 0x30000 | blk);
+      const bool next_same_j = blk + 1 < nblk && (blk + 1) / nt == j;
+      if (next_same_j) issue_half(blk + 1, 0);
+      // both halves' P and dS in shared memory
+      mbar_wait(bar_h, blk & 1);
+      if (lane == 0) dbg_mark(16, 0x40000 | blk);
+      mbar_wait(bar_h1, blk & 1);
+      tc_fence_after();
+      if (lane == 0) dbg_mark(16, 0x50000 | blk);
       // the previous key block's dK / dV drained before this block zeroes them
       if (i == 0 && j > 0) {
         mbar_wait(bar_dr, (j - 1) & 1);
@@ -423,17 +457,15 @@ __global__ void __launch_bounds__(kThreads, 1)
         umma_commit(bar_acc);
       }
       __syncwarp();
-      if (blk + 1 < nblk) {
+      if (blk + 1 < nblk && !next_same_j) {
+        // next key block: once every MMA reading K_j / V_j is done, load
+        // K_j+1 / V_j+1 into the buffer (the dK/dV drain overlaps the load)
         const int jn = (blk + 1) / nt;
-        if (jn != j) {
-          // next key block: once every MMA reading K_j / V_j is done, load
-          // K_j+1 / V_j+1 into the buffer (the dK/dV drain overlaps the load)
-          mbar_wait(bar_acc, blk & 1);
-          if (lane == 0) load_kv(jn);
-          __syncwarp();
-          mbar_wait(bar_kv, jn & 1);
-          tc_fence_after();
-        }
+        mbar_wait(bar_acc, blk & 1);
+        if (lane == 0) load_kv(jn);
+        __syncwarp();
+        mbar_wait(bar_kv, jn & 1);
+        tc_fence_after();
         issue_half(blk + 1, 0);
       }
     }
@@ -459,15 +491,20 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll 1
       for (int hh = 0; hh < 2; ++hh) {
         const int col = hh * 64 + part * 16;  // key column within the block
+        if (lane == 0) dbg_mark(warp, 0x10000 | (blk << 1) | hh);
         mbar_wait(bar_sp, nsp & 1);
         ++nsp;
         tc_fence_after();
+        if (lane == 0) dbg_mark(warp, 0x20000 | (blk << 1) | hh);
         uint32_t sv[16], dp[16];
         tmem_ld16(trow + T_S + part * 16, sv);
         tmem_ld16(trow + T_DP + part * 16, dp);
         const uint4 kb = keep_bytes(seed, step, a.tag,
                                     ((bh * S + q) * uint64_t(S) + j * TILE + col) >> 4, a.thr);
         tmem_wait();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(bar_t);  // this half's TMEM may be overwritten
         uint32_t wds[8], wpd[8];
 #pragma unroll
         for (int e = 0; e < 16; e += 2) {
@@ -481,13 +518,15 @@ __global__ void __launch_bounds__(kThreads, 1)
           wpd[e >> 1] = pack_bf16x2(p0 * k0, p1 * k1);
         }
         // the previous block's accumulate MMAs have read sP / sDS
+        if (lane == 0) dbg_mark(warp, 0x30000 | (blk << 1) | hh);
         if (hh == 0 && blk > 0) mbar_wait(bar_acc, (blk - 1) & 1);
+        if (lane == 0) dbg_mark(warp, 0x40000 | (blk << 1) | hh);
         st_row16(sDS, r, col, wds);
         st_row16(sP, r, col, wpd);
         fence_proxy_async_smem();
         tc_fence_before();
         __syncwarp();
-        if (lane == 0) mbar_arrive(bar_h);
+        if (lane == 0) mbar_arrive(hh ? bar_h1 : bar_h);
       }
       if (i == nt - 1) {
         // key block j complete: drain dK_j, dV_j (TMEM lane = key row)
@@ -534,7 +573,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 size_t fwd_smem(int S) {
   return 1024 + TILE_BYTES + size_t(S) * 128 + size_t(S) * 256 + 8 * TILE * 4 + 64;
 }
-size_t bwd_smem(int S) { return 1024 + 2 * size_t(S) * 128 + 6 * TILE_BYTES + 64; }
+size_t bwd_smem(int S) { return 1024 + 2 * size_t(S) * 128 + 6 * TILE_BYTES + 128; }  // 10 words
 
 bool shape_ok(int S, int heads) { return S > 0 && S % TILE == 0 && S <= 512 && heads > 0; }
 
@@ -561,6 +600,11 @@ cudaError_t attention_fwd(const void* qkv, void* out, float* lse, int B, int S, 
                                st, qm, a))
     return e;
   return cudaGetLastError();
+}
+
+cudaError_t attention_debug(void* host_words) {
+  uint32_t* p = static_cast<uint32_t*>(host_words);
+  return cudaMemcpyToSymbol(g_attn_dbg, &p, sizeof(p));
 }
 
 cudaError_t attention_bwd(const void* qkv, const void* out, const void* dout, const float* lse,

@@ -48,6 +48,8 @@ cudaError_t adamw_step(float* w, float* m, float* v, const float* g, void* wbf, 
 // log2 units of the scaled scores.
 cudaError_t attention_fwd(const void* qkv, void* out, float* lse, int B, int S, int heads,
                           float p, const uint64_t* rng, uint32_t tag, cudaStream_t st);
+// debug: progress words of the backward kernel in mapped host memory (32 per CTA)
+cudaError_t attention_debug(void* host_words);
 // dqkv [B*S][3*heads*64]; D = rowsum(dO * O) scratch [B*heads][S]
 cudaError_t attention_bwd(const void* qkv, const void* out, const void* dout, const float* lse,
                           float* D, void* dqkv, int B, int S, int heads, float p,

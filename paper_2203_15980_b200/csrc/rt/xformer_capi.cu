@@ -102,6 +102,9 @@ delta_status delta_attention_bwd(const void* qkv, const void* out, const void* d
                                     S(stream)),
              "attention_bwd");
 }
+delta_status delta_attention_debug(void* host_words) {
+  return st_(delta_k::attention_debug(host_words), "attention_debug");
+}
 delta_status delta_adamw_step(float* w, float* m, float* v, const float* g, void* wbf, int64_t n,
                               int64_t n_bf, float lr, float beta1, float beta2, float eps,
                               float weight_decay, uint64_t* rng, void* stream) {
