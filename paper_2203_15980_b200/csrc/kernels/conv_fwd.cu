@@ -136,12 +136,15 @@ constexpr int EV_ADD_OM_ST = 5;  // EV_ADD_OM + partials (sum y, sum y*xc): the 
 constexpr int EV_SCATTER = 6;  // y[n][2p+a][2q+b] = bf16(acc): a stride-2 input gradient's parity class
 constexpr int EV_BIAS = 7;     // y = bf16(acc + bias[k])                     (linear layers)
 constexpr int EV_GELU_BWD = 8; // y = bf16(acc * gelu'(xc)), xc = the [M][K] pre-activation
+constexpr int EV_ADD_S2 = 9;   // y = (bf16(acc) + add at even (p, q)) & [out_mask > 0]: the add is
+                               // a stride-2 shortcut gradient on its [N][P/2][Q/2] grid, read
+                               // straight by the lanes of even rows; out_mask by TMA
 // epilogues that read [M][K] operand tiles (the operand ring / tile buffers)
 __host__ __device__ constexpr bool ev_fused(int ev) {
   return ev != EV_STORE && ev != EV_SCATTER && ev != EV_BIAS;
 }
 __host__ __device__ constexpr int ev_operands(int ev) {
-  return ev == EV_ADD || ev == EV_BN_BWD || ev == EV_GELU_BWD
+  return ev == EV_ADD || ev == EV_BN_BWD || ev == EV_GELU_BWD || ev == EV_ADD_S2
              ? 1
              : (ev == EV_ADD_OM || ev == EV_POOL ? 2 : (ev == EV_ADD_OM_ST ? 3 : 0));
 }
@@ -204,6 +207,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   constexpr int NOPS_ = ev_operands(EV);
   constexpr uint32_t OPT_TILE = uint32_t(NOPS_) * BN * 256;  // per tile: NOPS x [128][BN] bf16
   static_assert(EV != EV_ADD_OM_ST || OPT, "three-operand epilogue: TMA-loaded operands only");
+  static_assert(EV != EV_ADD_S2 || OPT, "stride-2 add epilogue: TMA-loaded mask only");
   constexpr uint32_t IN_BYTES = !FUSED ? 0 : (OPT ? OPT_NB * OPT_TILE : EPI_W * EPI_RING_WARP);
   const uint32_t sIn = sOut + 16384;
   // BN-statistics scratch: per quarter-warp column (sum, sumsq), [4][BN] float2
@@ -617,6 +621,16 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int m0 = row_tiled(MODE) ? (tile / a.n_tiles) * a.Q : tile_m0(tile);
       const int n0 = (tile % a.n_tiles) * BN;
       const uint32_t acc = lt & 1;
+      // EV_ADD_S2: this lane's row -> its shortcut-gradient row (even p and q only)
+      int64_t s2row = -1;
+      if constexpr (EV == EV_ADD_S2) {
+        const int m = m0 + quarter * 32 + lane;
+        if (m < a.M) {
+          const int q = m % a.Q, t = m / a.Q;
+          const int p = t % a.P, n = t / a.P;
+          if (!((p | q) & 1)) s2row = (int64_t(n) * (a.P >> 1) + (p >> 1)) * (a.Q >> 1) + (q >> 1);
+        }
+      }
       mbar_wait(&tfull[acc], (lt >> 1) & 1);
       tc_fence_after();
       const uint32_t obuf = sIn + (lt % OPT_NB) * OPT_TILE;
@@ -691,6 +705,27 @@ __global__ void __launch_bounds__(kThreads, 1)
             pk[u].y = add_bf16x2(pk[u].y, ad.y);
             pk[u].z = add_bf16x2(pk[u].z, ad.z);
             pk[u].w = add_bf16x2(pk[u].w, ad.w);
+          }
+        }
+        if constexpr (EV == EV_ADD_S2) {
+          if (s2row >= 0) {
+            const bf16* addp = static_cast<const bf16*>(a.e.add) + s2row * a.K + col;
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+              const uint4 ad = ldg16(addp + u * 8);
+              pk[u].x = add_bf16x2(pk[u].x, ad.x);
+              pk[u].y = add_bf16x2(pk[u].y, ad.y);
+              pk[u].z = add_bf16x2(pk[u].z, ad.z);
+              pk[u].w = add_bf16x2(pk[u].w, ad.w);
+            }
+          }
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const uint4 om = ld_row16(sb, lane, u);
+            pk[u].x &= pos_mask2(om.x);
+            pk[u].y &= pos_mask2(om.y);
+            pk[u].z &= pos_mask2(om.z);
+            pk[u].w &= pos_mask2(om.w);
           }
         }
         if constexpr (EV == EV_ADD_OM || EV == EV_POOL || EV == EV_ADD_OM_ST) {
@@ -1053,6 +1088,15 @@ bool operands_tma() {
   return v == 1;
 }
 
+bool s2_ring() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = std::getenv("DELTA_S2_RING");
+    v = (e && e[0] == '1') ? 1 : 0;
+  }
+  return v == 1;
+}
+
 // DELTA_CONV_GATHER=1 selects the cp.async im2col gather instead of the TMA
 // im2col unit (kept as the reference path for the A operand).
 bool gather_forced() {
@@ -1155,7 +1199,8 @@ cudaError_t launch(const ConvPlan& cp, const void* x, void* y, float* stats,
   alignas(64) CUtensorMap emap0 = ymap, emap1 = ymap, emap2 = ymap;
   if (OPT) {
     const void* op0 = EV == EV_BN_BWD || EV == EV_GELU_BWD ? epi.xc
-                                                           : (EV == EV_POOL ? epi.add_mask : epi.add);
+                       : EV == EV_ADD_S2                  ? epi.out_mask
+                       : (EV == EV_POOL ? epi.add_mask : epi.add);
     if (!tma_2d_bf16(&emap0, op0, uint64_t(cp.K), uint64_t(a.M), uint64_t(cp.K), 32, BM,
                      CU_TENSOR_MAP_SWIZZLE_64B))
       return cudaErrorInvalidValue;
@@ -1312,6 +1357,17 @@ cudaError_t conv_forward(const ConvPlan& cp, const void* x, void* y, float* stat
     if (cp.bn != 64 && cp.bn != 128) return cudaErrorInvalidValue;
     if (e.add_stride2 && (ev == EV_POOL || ev == EV_BN_BWD || (cp.P & 1) || (cp.Q & 1)))
       return cudaErrorInvalidValue;
+    // stride-2 shortcut gradient + ReLU mask: the mask by TMA tiles, the
+    // quarter-density add read straight by the even rows' lanes (the cp.async
+    // operand ring ran at ~0.55 of HBM: 322 us for layer2.0 conv1; DELTA_S2_RING=1
+    // keeps it)
+    if (ev == EV_ADD_OM && e.add_stride2 && !stats && operands_tma() && !s2_ring()) {
+      if (cp.bn == 64)
+        return tma_a ? launch<64, 4, MODE_TMA, EV_ADD_S2, true>(cp, x, y, nullptr, e, st)
+                     : launch<64, 4, MODE_IM2COL, EV_ADD_S2, true>(cp, x, y, nullptr, e, st);
+      return tma_a ? launch<128, opt_stages<EV_ADD_S2>(), MODE_TMA, EV_ADD_S2, true>(cp, x, y, nullptr, e, st)
+                   : launch<128, opt_stages<EV_ADD_S2>(), MODE_IM2COL, EV_ADD_S2, true>(cp, x, y, nullptr, e, st);
+    }
     // Operands by TMA (per-tile boxes into two tile buffers) unless the add is
     // the stride-2 shortcut gradient (cp.async gather from its sampling grid).
     // One-operand epilogues (BN backward, plain add) keep the usual stage

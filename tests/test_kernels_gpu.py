@@ -307,6 +307,16 @@ def test_dgrad_and_add_mask_epilogue(case):
     torch.cuda.synchronize()
     up = (pooled.float() / (H * W))[:, None, None, :] * (am.float() > 0)
     _close(y2, (ref + up) * (om.float() > 0), "pooled add")
+    if H % 2 == 0 and W % 2 == 0:
+        # a stride-2 shortcut gradient given on its [N][H/2][W/2] sampling
+        # grid, added at the even rows / columns (conv_fwd.cu EV_ADD_S2)
+        s2 = torch.randn(N, H // 2, W // 2, Cin, device="cuda", generator=g).to(torch.bfloat16)
+        conv.add_mask(dy.data_ptr(), y2.data_ptr(), _stream(), add=s2.data_ptr(),
+                      out_mask=om.data_ptr(), add_stride2=True)
+        torch.cuda.synchronize()
+        full = torch.zeros(N, H, W, Cin, device="cuda")
+        full[:, ::2, ::2] = s2.float()
+        _close(y2, (ref + full) * (om.float() > 0), "stride-2 add")
 
 
 @pytest.mark.parametrize("case", [c for c in DGRAD_CASES if c[5] == 1])
