@@ -72,6 +72,7 @@ struct WgradPlan {
   int N, H, W, C, K, R, S, stride, pad;  // the forward conv (C == 4: the pair-view stem)
   int P, Q, mode, bn, taps, tiles, splits, kb_per_split;
   int mt;  // 128-row output-channel blocks per tile (2: two accumulators share each B tile)
+  int pair;  // 256-channel tiles on a CTA pair (cta_group::2)
 };
 // 0 ok, 1 unsupported shape
 int wgrad_plan_init(WgradPlan* wp);

@@ -93,22 +93,28 @@ __device__ __forceinline__ uint64_t desc_mn_interleave(uint32_t addr, uint32_t l
 // MT = 2: a tile is 256 output channels x BN columns — two accumulators (the
 // whole TMEM, so no double buffering) fed by the same B tile, halving the B
 // traffic per flop (the operand stream from L2 paces the large-K shapes)
-template <int MODE, int BN, int MT>
+template <int MODE, int BN, int MT, bool PAIR = false>
 constexpr int wg_stages() {
-  return MODE == WG_STEMRAW ? 6 : (MT == 2 ? 3 : (BN >= 192 ? 4 : 6));
+  return PAIR ? 6 : (MODE == WG_STEMRAW ? 6 : (MT == 2 ? 3 : (BN >= 192 ? 4 : 6)));
 }
 
-template <int BN, int MODE, int MT>
+// PAIR: a 2-CTA cluster computes 256-channel tiles (cta_group::2 M=256): each
+// CTA stages its own 128 output channels of dY and HALF of the BN input
+// channels of X; both CTAs' bytes land on the leader's barrier, the leader
+// issues the pair MMAs, commits are multicast, each CTA drains its own TMEM.
+template <int BN, int MODE, int MT, bool PAIR = false>
 __global__ void __launch_bounds__(WG_THREADS, 1)
     k_wgrad(const __grid_constant__ CUtensorMap amap, const __grid_constant__ CUtensorMap bmap,
             const WgArgs a) {
+  static_assert(!PAIR || (MT == 1 && BN == 256 && (MODE == WG_PLAIN || MODE == WG_IM2COL)),
+                "pair weight gradient: 256-column plain / im2col tiles");
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = align1024(smem_raw);
-  constexpr int STAGES = wg_stages<MODE, BN, MT>();
+  constexpr int STAGES = wg_stages<MODE, BN, MT, PAIR>();
   constexpr uint32_t A_STAGE = MT * 2 * KPIX * 128;                      // 2 boxes of 64 ch per 128
   constexpr uint32_t B_STAGE = MODE == WG_STEMRAW ? 7 * RAW_ROW
                                : MODE == WG_STEM  ? 32 * KPIX * 16
-                                                  : (BN / 64) * KPIX * 128;
+                                                  : ((PAIR ? BN / 2 : BN) / 64) * KPIX * 128;
   const uint32_t sA = smem_u32(smem);
   const uint32_t sB = sA + STAGES * A_STAGE;
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * (A_STAGE + B_STAGE));
@@ -119,6 +125,9 @@ __global__ void __launch_bounds__(WG_THREADS, 1)
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
+  const uint32_t rank = PAIR ? cluster_rank() : 0u;
+  const int unit = PAIR ? int(blockIdx.x >> 1) : int(blockIdx.x);
+  const int units = PAIR ? int(gridDim.x >> 1) : int(gridDim.x);
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full[s], 1);
@@ -126,7 +135,7 @@ __global__ void __launch_bounds__(WG_THREADS, 1)
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&tfull[i], 1);
-      mbar_init(&tempty[i], 4);
+      mbar_init(&tempty[i], PAIR ? 8 : 4);  // pair: both CTAs' epilogue warps
     }
     fence_mbar_init();
     tma_prefetch_desc(&amap);
@@ -145,9 +154,15 @@ __global__ void __launch_bounds__(WG_THREADS, 1)
   // MT=1: two accumulators; MT=2: lo/hi halves (allocation: a power of two)
   constexpr uint32_t TMEM_COLS = 2 * BN <= 256 ? 2 * BN : 512;
   constexpr uint32_t NACC = MT == 2 ? 1 : 2;  // accumulator buffers
-  if (warp == 1) tmem_alloc(tslot, TMEM_COLS);
+  if (warp == 1) {
+    if constexpr (PAIR)
+      tmem_alloc_pair(tslot, TMEM_COLS);
+    else
+      tmem_alloc(tslot, TMEM_COLS);
+  }
   tc_fence_before();
   __syncthreads();
+  if constexpr (PAIR) cluster_sync_all();
   tc_fence_after();
   const uint32_t tmem = *tslot;
   // prologue done (barriers, TMEM, descriptors): now wait for the predecessor
@@ -158,7 +173,7 @@ __global__ void __launch_bounds__(WG_THREADS, 1)
   // a tile's BN columns may span several taps when C < BN
   auto decode = [&](int item, int& m0, int& n0, int& kb0, int& kb1) {
     const int split = item / a.tiles, tile = item % a.tiles;
-    m0 = (tile % a.tiles_m) * 128 * MT;
+    m0 = (tile % a.tiles_m) * 128 * (PAIR ? 2 : MT) + int(rank) * 128;
     n0 = (tile / a.tiles_m) * BN;
     kb0 = split * a.kb_per_split;
     kb1 = min(a.kblocks, kb0 + a.kb_per_split);
@@ -168,11 +183,13 @@ __global__ void __launch_bounds__(WG_THREADS, 1)
     // ================================ producer ================================
     if (lane == 0) {
       uint32_t it = 0;
-      for (int item = blockIdx.x; item < a.items; item += gridDim.x) {
+      for (int item = unit; item < a.items; item += units) {
         int m0, n0, kb0, kb1;
         decode(item, m0, n0, kb0, kb1);
+        if (PAIR) n0 += int(rank) * (BN / 2);  // this CTA's half of the N tile
+        constexpr int BNL = PAIR ? BN / 2 : BN;
         // B boxes of this tile: 64 flattened columns each, inside [0, ntot)
-        const int nbox = MODE == WG_STEM ? 28 : min(BN / 64, (a.ntot - n0) / 64);
+        const int nbox = MODE == WG_STEM ? 28 : max(0, min(BNL / 64, (a.ntot - n0) / 64));
         const uint32_t b_bytes = MODE == WG_STEM ? 28 * KPIX * 16 : nbox * KPIX * 128;
         // per item: each B box's (channel, tap column, tap row) — the single
         // producer thread must not spend its k-loop on divisions
@@ -219,6 +236,26 @@ __global__ void __launch_bounds__(WG_THREADS, 1)
           const int pix = kb * KPIX;
           // the 64-channel boxes of the A tile only where K has them (rows of D
           // past K are never read back); MT=2 implies K % 256 == 0
+          if constexpr (PAIR) {
+            // both CTAs' full A halves and B halves land on the leader's
+            // barrier; boxes past K / ntot are loaded anyway (zero-filled by
+            // the TMA unit) so the byte count is the same in both CTAs
+            if (rank == 0) mbar_arrive_expect_tx(&full[s], 2 * (A_STAGE + B_STAGE));
+#pragma unroll
+            for (int h = 0; h < 2; ++h)
+              tma_load_2d_pair(sA + s * A_STAGE + h * KPIX * 128, &amap, &full[s], m0 + 64 * h, pix);
+            if constexpr (MODE == WG_PLAIN) {
+#pragma unroll
+              for (int b = 0; b < BN / 128; ++b)
+                tma_load_2d_pair(sB + s * B_STAGE + b * KPIX * 128, &bmap, &full[s], n0 + 64 * b, pix);
+            } else {
+              const int wb = q * a.stride - a.pad, hb = p * a.stride - a.pad;
+#pragma unroll
+              for (int b = 0; b < BN / 128; ++b)
+                tma_load_im2col_4d_pair(sB + s * B_STAGE + b * KPIX * 128, &bmap, &full[s], bc[b],
+                                        wb, hb, n, uint16_t(bs[b]), uint16_t(br[b]));
+            }
+          } else {
           const bool a2 = m0 + 64 < a.K;
           mbar_arrive_expect_tx(&full[s], (MT == 2 || a2 ? A_STAGE : A_STAGE / 2) + b_bytes);
 #pragma unroll
@@ -244,6 +281,7 @@ __global__ void __launch_bounds__(WG_THREADS, 1)
               tma_load_im2col_4d(sB + s * B_STAGE + u * KPIX * 16, &bmap, &full[s], 0, wb, hb, n,
                                  uint16_t(u & 3), uint16_t(u >> 2));
           }
+          }  // !PAIR
           if (MODE != WG_PLAIN) {
             q += KPIX;
             while (q >= a.Q) {
@@ -298,9 +336,10 @@ __global__ void __launch_bounds__(WG_THREADS, 1)
         __syncwarp();
       }
     } else {
-      constexpr uint32_t idesc = umma_idesc_bf16(128, BN) | (1u << 15) | (1u << 16);
+      constexpr uint32_t idesc = umma_idesc_bf16(PAIR ? 256 : 128, BN) | (1u << 15) | (1u << 16);
       uint32_t it = 0, lt = 0;
-      for (int item = blockIdx.x; item < a.items; item += gridDim.x, ++lt) {
+      // pair: only the leader issues
+      for (int item = unit; item < ((PAIR && rank != 0) ? 0 : a.items); item += units, ++lt) {
         int m0, n0, kb0, kb1;
         decode(item, m0, n0, kb0, kb1);
         const uint32_t acc = lt % NACC;
@@ -316,6 +355,13 @@ __global__ void __launch_bounds__(WG_THREADS, 1)
           const uint64_t bd0 = MODE == WG_STEM ? desc_mn_interleave(sB + s * B_STAGE, 128, KPIX * 16)
                                                : desc_mn_sw128(sB + s * B_STAGE, KPIX * 128);
           if (elect_one()) {
+            if constexpr (PAIR) {
+#pragma unroll
+              for (int k = 0; k < KPIX / 16; ++k)
+                umma_bf16_pair(d, ad0 + uint64_t(k * 128), bd0 + uint64_t(k * 128), idesc,
+                               (kb != kb0 || k) ? 1u : 0u);
+              umma_commit_pair(&empty[s]);
+            } else {
 #pragma unroll
             for (int k = 0; k < KPIX / 16; ++k)
 #pragma unroll
@@ -324,10 +370,16 @@ __global__ void __launch_bounds__(WG_THREADS, 1)
                           bd0 + uint64_t(MODE == WG_STEM ? k * 16 : k * 128), idesc,
                           (kb != kb0 || k) ? 1u : 0u);
             umma_commit(&empty[s]);
+            }
           }
           __syncwarp();
         }
-        if (elect_one()) umma_commit(&tfull[acc]);
+        if (elect_one()) {
+          if constexpr (PAIR)
+            umma_commit_pair(&tfull[acc]);
+          else
+            umma_commit(&tfull[acc]);
+        }
         __syncwarp();
       }
     }
@@ -342,7 +394,7 @@ __global__ void __launch_bounds__(WG_THREADS, 1)
     __shared__ int s_last;
     const int quarter = warp & 3;
     uint32_t lt = 0;
-    for (int item = blockIdx.x; item < a.items; item += gridDim.x, ++lt) {
+    for (int item = unit; item < a.items; item += units, ++lt) {
       const uint32_t acc = lt % NACC;
       mbar_wait(&tfull[acc], (lt / NACC) & 1);
       tc_fence_after();
@@ -353,7 +405,8 @@ __global__ void __launch_bounds__(WG_THREADS, 1)
       decode(item, m0, n0, kb0, kb1);
       const bool direct = !STEMLIKE && a.fused && a.splits == 1;
       for (int h = 0; h < MT; ++h) {
-      float* out = a.ws + (size_t(item) * 128 * MT + h * 128 + row) * BN;
+      // partial tiles are 128*MT rows (pair: 256, this CTA's at +128*rank)
+      float* out = a.ws + (size_t(item) * 128 * (PAIR ? 2 : MT) + rank * 128 + h * 128 + row) * BN;
       const int k = m0 + h * 128 + row;
 #pragma unroll 1
       for (int j = 0; j < BN / 32; ++j) {
@@ -378,8 +431,13 @@ __global__ void __launch_bounds__(WG_THREADS, 1)
       }
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&tempty[acc]);
-      if (!STEMLIKE && a.fused && !direct) {
+      if (lane == 0) {
+        if constexpr (PAIR)
+          mbar_arrive_cluster(mapa_shared(smem_u32(&tempty[acc]), 0));  // the leader's
+        else
+          mbar_arrive(&tempty[acc]);
+      }
+      if (!STEMLIKE && a.fused && !direct && !PAIR) {
         // publish this split's partial, then count it in
         __threadfence();
         asm volatile("bar.sync 1, 128;" ::: "memory");
@@ -435,8 +493,14 @@ __global__ void __launch_bounds__(WG_THREADS, 1)
   }
   tc_fence_before();
   __syncthreads();
+  if constexpr (PAIR) cluster_sync_all();
   tc_fence_after();
-  if (warp == 1) tmem_dealloc(tmem, TMEM_COLS);
+  if (warp == 1) {
+    if constexpr (PAIR)
+      tmem_dealloc_pair(tmem, TMEM_COLS);
+    else
+      tmem_dealloc(tmem, TMEM_COLS);
+  }
 }
 
 // dW[k][n] (KRSC, n = tap*C + c, fp32) = sum over splits of the partial tiles,
@@ -481,13 +545,13 @@ __global__ void __launch_bounds__(256)
   }
 }
 
-template <int BN, int MODE, int MT>
+template <int BN, int MODE, int MT, bool PAIR = false>
 constexpr size_t wg_smem_bytes() {
-  constexpr int STAGES = wg_stages<MODE, BN, MT>();
+  constexpr int STAGES = wg_stages<MODE, BN, MT, PAIR>();
   constexpr size_t A = MT * 2 * KPIX * 128;
   constexpr size_t B = MODE == WG_STEMRAW ? 7 * RAW_ROW
                        : MODE == WG_STEM  ? 32 * KPIX * 16
-                                          : (BN / 64) * KPIX * 128;
+                                          : ((PAIR ? BN / 2 : BN) / 64) * KPIX * 128;
   return STAGES * (A + B) + 1024 + 256;
 }
 
@@ -511,11 +575,11 @@ bool fused_reduce_off() {
   return v == 1;
 }
 
-template <int BN, int MODE, int MT = 1>
+template <int BN, int MODE, int MT = 1, bool PAIR = false>
 cudaError_t wg_launch(const WgradPlan& wp, const void* dy, const void* x, float* dw, float* ws,
                       cudaStream_t st) {
-  auto kern = k_wgrad<BN, MODE, MT>;
-  constexpr size_t smem = wg_smem_bytes<BN, MODE, MT>();
+  auto kern = k_wgrad<BN, MODE, MT, PAIR>;
+  constexpr size_t smem = wg_smem_bytes<BN, MODE, MT, PAIR>();
   static_assert(smem <= 227 * 1024, "shared memory");
   static bool attr = false;
   if (!attr) {
@@ -529,7 +593,8 @@ cudaError_t wg_launch(const WgradPlan& wp, const void* dy, const void* x, float*
   a.M = wp.N * wp.P * wp.Q;
   a.kblocks = MODE == WG_STEMRAW ? wp.N * wp.P : (a.M + KPIX - 1) / KPIX;
   a.W2 = wp.W / 2;
-  a.tiles_m = (wp.K + 128 * MT - 1) / (128 * MT);
+  constexpr int TM = 128 * (PAIR ? 2 : MT);  // output channels per tile
+  a.tiles_m = (wp.K + TM - 1) / TM;
   a.ntot = wp.taps * wp.C;
   a.tiles = wp.tiles;
   a.splits = wp.splits;
@@ -539,6 +604,7 @@ cudaError_t wg_launch(const WgradPlan& wp, const void* dy, const void* x, float*
   // weight gradient sharing the buffer leaves them zero), the partials after it
   a.counters = reinterpret_cast<unsigned*>(ws);
   ws = reinterpret_cast<float*>(reinterpret_cast<char*>(ws) + WG_COUNTER_BYTES);
+  (void)TM;
   a.ws = ws;
   a.dw = dw;
   // fused finish only for few splits: the last split's CTA sums the tile alone
@@ -550,6 +616,7 @@ cudaError_t wg_launch(const WgradPlan& wp, const void* dy, const void* x, float*
   if (!tma_2d_bf16(&amap, dy, uint64_t(wp.K), uint64_t(a.M), uint64_t(wp.K), 64,
                    MODE == WG_STEMRAW ? uint32_t(wp.Q) : uint32_t(KPIX), CU_TENSOR_MAP_SWIZZLE_128B))
     return cudaErrorInvalidValue;
+  static_assert(!PAIR || MT == 1, "pair tiles: one accumulator per CTA");
   bool ok;
   if (MODE == WG_PLAIN) {
     ok = tma_2d_bf16(&bmap, x, uint64_t(wp.C), uint64_t(a.M), uint64_t(wp.C), 64, KPIX,
@@ -566,8 +633,15 @@ cudaError_t wg_launch(const WgradPlan& wp, const void* dy, const void* x, float*
                          1, 2, 8, KPIX, CU_TENSOR_MAP_SWIZZLE_NONE);
   }
   if (!ok) return cudaErrorInvalidValue;
-  const int grid = std::min(a.items, num_sms_wg());
-  if (cudaError_t e_ = launch_k(kern, dim3(grid), dim3(WG_THREADS), smem, st, amap, bmap, a)) return e_;
+  if constexpr (PAIR) {
+    const int pairs = std::min(a.items, num_sms_wg() / 2);
+    if (cudaError_t e_ = launch_cluster(kern, dim3(2 * pairs), dim3(WG_THREADS), smem, st, 2u, amap,
+                                        bmap, a))
+      return e_;
+  } else {
+    const int grid = std::min(a.items, num_sms_wg());
+    if (cudaError_t e_ = launch_k(kern, dim3(grid), dim3(WG_THREADS), smem, st, amap, bmap, a)) return e_;
+  }
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   if (MODE == WG_STEM || MODE == WG_STEMRAW) {
@@ -575,7 +649,7 @@ cudaError_t wg_launch(const WgradPlan& wp, const void* dy, const void* x, float*
   } else if (!a.fused) {  // many splits, or DELTA_WGRAD_FUSED_REDUCE=0: the all-SM reduce
     const int64_t total = int64_t(wp.K) * a.ntot;
     const int64_t blocks = std::min<int64_t>((total + 255) / 256, 148 * 16);
-    if (cudaError_t e_ = launch_k(k_wgrad_reduce<BN, 128 * MT>, dim3(int(blocks)), dim3(256), 0, st, ws, dw, wp.K, a.ntot, a.tiles_m, wp.tiles, wp.splits)) return e_;
+    if (cudaError_t e_ = launch_k(k_wgrad_reduce<BN, 128 * (PAIR ? 2 : MT)>, dim3(int(blocks)), dim3(256), 0, st, ws, dw, wp.K, a.ntot, a.tiles_m, wp.tiles, wp.splits)) return e_;
   }
   return cudaGetLastError();
 }
@@ -614,7 +688,16 @@ int wgrad_plan_init(WgradPlan* wp) {
     return !(e && e[0] == '0');
   }();
   p.mt = (!stem && mt2_on && p.taps > 1 && p.bn == 256 && p.K % 256 == 0) ? 2 : 1;
-  const int tiles_m = (p.K + 128 * p.mt - 1) / (128 * p.mt);
+  // CTA-pair 256-channel tiles (cta_group::2) for the plain 1x1 shapes with
+  // whole 256x256 tiles (DELTA_WGRAD_PAIR=0 disables)
+  static const bool pair_on = [] {
+    const char* e = std::getenv("DELTA_WGRAD_PAIR");
+    return !(e && e[0] == '0');
+  }();
+  p.pair = (pair_on && !stem && p.mt == 1 && p.mode == WG_PLAIN && p.bn == 256 &&
+            p.K % 256 == 0 && ntot % 256 == 0) ? 1 : 0;
+  const int tm = 128 * (p.pair ? 2 : p.mt);
+  const int tiles_m = (p.K + tm - 1) / tm;
   p.tiles = stem ? tiles_m : tiles_m * ((ntot + p.bn - 1) / p.bn);
   const int M = p.N * p.P * p.Q;
   const int kblocks = p.mode == WG_STEMRAW ? p.N * p.P : (M + KPIX - 1) / KPIX;
@@ -622,11 +705,11 @@ int wgrad_plan_init(WgradPlan* wp) {
   // over the SMs (a partial last wave costs a full one) times the item
   // length, plus the fp32 partials written and re-read by the reduce.
   // (Rounding "two waves" up left 30% of the SMs idle in the last wave.)
-  const int sms = 148;
+  const int sms = p.pair ? 74 : 148;  // scheduling units (CTA pairs)
   const double t_kb = p.mode == WG_STEMRAW ? 1.3e-6                       // one output row
-                                           : 2.0 * 128 * p.mt * p.bn * KPIX / (1.0e15 / sms);
+                                           : 2.0 * 128 * p.mt * p.bn * KPIX / (1.0e15 / 148);
   const double t_ramp = 1.5 * t_kb;  // per item: pipeline fill + accumulator drain
-  const double part_bytes = 8.0 * p.tiles * 128 * p.mt * p.bn;  // per split: write + reduce read
+  const double part_bytes = 8.0 * p.tiles * tm * p.bn;  // per split: write + reduce read
   const int smax = std::max(1, kblocks / (p.mode == WG_STEMRAW ? 4 : 8));
   int splits = 1;
   double best = 1e30;
@@ -655,7 +738,8 @@ int wgrad_launches(const WgradPlan& wp) {
 
 size_t wgrad_workspace_bytes(const WgradPlan& wp) {
   // the per-tile split counters (must be zero at allocation) + partial tiles
-  return WG_COUNTER_BYTES + size_t(wp.splits) * wp.tiles * 128 * wp.mt * wp.bn * sizeof(float);
+  return WG_COUNTER_BYTES +
+         size_t(wp.splits) * wp.tiles * 128 * (wp.pair ? 2 : wp.mt) * wp.bn * sizeof(float);
 }
 
 cudaError_t wgrad(const WgradPlan& wp, const void* dy, const void* x, float* dw, float* ws,
@@ -673,6 +757,7 @@ cudaError_t wgrad(const WgradPlan& wp, const void* dy, const void* x, float* dw,
       return wp.mode == WG_PLAIN ? wg_launch<192, WG_PLAIN>(wp, dy, x, dw, ws, st)
                                  : wg_launch<192, WG_IM2COL>(wp, dy, x, dw, ws, st);
     default:
+      if (wp.pair) return wg_launch<256, WG_PLAIN, 1, true>(wp, dy, x, dw, ws, st);
       if (wp.mt == 2)
         return wp.mode == WG_PLAIN ? wg_launch<256, WG_PLAIN, 2>(wp, dy, x, dw, ws, st)
                                    : wg_launch<256, WG_IM2COL, 2>(wp, dy, x, dw, ws, st);
