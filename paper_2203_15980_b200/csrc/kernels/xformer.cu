@@ -134,7 +134,7 @@ __global__ void __launch_bounds__(256)
 // block b owns rows [b*chunk, (b+1)*chunk), warps interleaved, and writes one
 // partial row pair (sum dy*xhat, sum dy) per column to ws[b][2][H].
 template <int NV>
-__global__ void __launch_bounds__(256, 2)
+__global__ void __launch_bounds__(256)
     k_layernorm_bwd(const bf16* __restrict__ dy, const bf16* __restrict__ x,
                     const bf16* __restrict__ dres, bf16* __restrict__ dx,
                     const float* __restrict__ mean, const float* __restrict__ rstd,
@@ -143,67 +143,46 @@ __global__ void __launch_bounds__(256, 2)
   pdl_wait();
   pdl_trigger();
   constexpr int H = NV * 256;
-  // per-warp (dgamma, dbeta) accumulators in shared memory [8][2][H] (each lane
-  // owns its columns: no conflicts, fixed order), the row's dy and x packed
-  // between the two passes, gamma through L1: 2 CTAs per SM (was 213
-  // registers, 1 CTA)
-  extern __shared__ float acc_s[];
+  __shared__ float red[8][2][256];  // per warp, per chunk pass
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  float* accg = acc_s + warp * 2 * H;
-  float* accb = accg + H;
-  for (int i = lane * 4; i < 2 * H; i += 128)
-    *reinterpret_cast<float4*>(accg + i) = make_float4(0.f, 0.f, 0.f, 0.f);
-  __syncwarp();
+  float acc_g[NV][8], acc_b[NV][8];
+#pragma unroll
+  for (int k = 0; k < NV; ++k)
+#pragma unroll
+    for (int i = 0; i < 8; ++i) acc_g[k][i] = acc_b[k][i] = 0.f;
+  float gm[NV][8];
+#pragma unroll
+  for (int k = 0; k < NV; ++k) {
+    const int c = (k * 32 + lane) * 8;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) gm[k][i] = __ldg(gamma + c + i);
+  }
   const int64_t r0 = int64_t(blockIdx.x) * chunk;
   const int64_t r1 = min(rows, r0 + chunk);
   for (int64_t r = r0 + warp; r < r1; r += 8) {
-    uint4 du[NV], xu[NV];
-#pragma unroll
-    for (int k = 0; k < NV; ++k) {
-      du[k] = __ldg(reinterpret_cast<const uint4*>(dy + r * H) + k * 32 + lane);
-      xu[k] = __ldg(reinterpret_cast<const uint4*>(x + r * H) + k * 32 + lane);
-    }
+    float xv[NV][8], g[NV][8];
     const float mu = __ldg(mean + r), rs = __ldg(rstd + r);
     float sg = 0.f, sgx = 0.f;
 #pragma unroll
     for (int k = 0; k < NV; ++k) {
-      float d[8], xv[8];
-      unpack8(du[k], d);
-      unpack8(xu[k], xv);
-      const int c = (k * 32 + lane) * 8;
-      const float4 g0 = __ldg(reinterpret_cast<const float4*>(gamma + c));
-      const float4 g1 = __ldg(reinterpret_cast<const float4*>(gamma + c + 4));
-      const float gm[8] = {g0.x, g0.y, g0.z, g0.w, g1.x, g1.y, g1.z, g1.w};
-      float4* ag = reinterpret_cast<float4*>(accg + c);
-      float4* ab = reinterpret_cast<float4*>(accb + c);
-      const float4 ag0 = ag[0], ag1 = ag[1], ab0 = ab[0], ab1 = ab[1];
-      float G[8] = {ag0.x, ag0.y, ag0.z, ag0.w, ag1.x, ag1.y, ag1.z, ag1.w};
-      float Bs[8] = {ab0.x, ab0.y, ab0.z, ab0.w, ab1.x, ab1.y, ab1.z, ab1.w};
+      float d[8];
+      unpack8(__ldg(reinterpret_cast<const uint4*>(dy + r * H) + k * 32 + lane), d);
+      unpack8(__ldg(reinterpret_cast<const uint4*>(x + r * H) + k * 32 + lane), xv[k]);
 #pragma unroll
       for (int i = 0; i < 8; ++i) {
-        const float xh = (xv[i] - mu) * rs;  // xhat
-        const float g = d[i] * gm[i];
-        sg += g;
-        sgx = fmaf(g, xh, sgx);
-        G[i] = fmaf(d[i], xh, G[i]);
-        Bs[i] += d[i];
+        xv[k][i] = (xv[k][i] - mu) * rs;  // xhat
+        g[k][i] = d[i] * gm[k][i];
+        sg += g[k][i];
+        sgx = fmaf(g[k][i], xv[k][i], sgx);
+        acc_g[k][i] = fmaf(d[i], xv[k][i], acc_g[k][i]);
+        acc_b[k][i] += d[i];
       }
-      ag[0] = make_float4(G[0], G[1], G[2], G[3]);
-      ag[1] = make_float4(G[4], G[5], G[6], G[7]);
-      ab[0] = make_float4(Bs[0], Bs[1], Bs[2], Bs[3]);
-      ab[1] = make_float4(Bs[4], Bs[5], Bs[6], Bs[7]);
     }
     const float a = warp_sum(sg) * (1.f / H);
     const float b = warp_sum(sgx) * (1.f / H);
 #pragma unroll
     for (int k = 0; k < NV; ++k) {
-      float d[8], xv[8], o[8], rr[8];
-      unpack8(du[k], d);
-      unpack8(xu[k], xv);
-      const int c = (k * 32 + lane) * 8;
-      const float4 g0 = __ldg(reinterpret_cast<const float4*>(gamma + c));
-      const float4 g1 = __ldg(reinterpret_cast<const float4*>(gamma + c + 4));
-      const float gm[8] = {g0.x, g0.y, g0.z, g0.w, g1.x, g1.y, g1.z, g1.w};
+      float o[8], rr[8];
       if (dres) {
         unpack8(__ldg(reinterpret_cast<const uint4*>(dres + r * H) + k * 32 + lane), rr);
       } else {
@@ -211,23 +190,34 @@ __global__ void __launch_bounds__(256, 2)
         for (int i = 0; i < 8; ++i) rr[i] = 0.f;
       }
 #pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        const float xh = (xv[i] - mu) * rs;
-        o[i] = fmaf(rs, d[i] * gm[i] - a - xh * b, rr[i]);
-      }
+      for (int i = 0; i < 8; ++i) o[i] = fmaf(rs, g[k][i] - a - xv[k][i] * b, rr[i]);
       reinterpret_cast<uint4*>(dx + r * H)[k * 32 + lane] = pack8(o);
     }
   }
-  // fixed-order reduction over the 8 warps
-  __syncthreads();
-  for (int t = threadIdx.x; t < 2 * H; t += 256) {
-    float sum = 0.f;
+  // fixed-order reduction over the 8 warps, 256 columns at a time
 #pragma unroll
-    for (int w = 0; w < 8; ++w) sum += acc_s[w * 2 * H + t];
-    ws[int64_t(blockIdx.x) * 2 * H + t] = sum;
+  for (int k = 0; k < NV; ++k) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      red[warp][0][lane * 8 + i] = acc_g[k][i];
+      red[warp][1][lane * 8 + i] = acc_b[k][i];
+    }
+    __syncthreads();
+    for (int t = threadIdx.x; t < 512; t += 256) {
+      const int which = t >> 8, c = t & 255;
+      float s = 0.f;
+#pragma unroll
+      for (int w = 0; w < 8; ++w) s += red[w][which][c];
+      // column (k*32 + c/8)*8 + c%8 of the row
+      ws[(int64_t(blockIdx.x) * 2 + which) * H + k * 256 + c] = s;
+    }
+    __syncthreads();
   }
 }
 
+// out[c] (=|+=) sum over p < parts of ws[p * pstride + c], in p order: block
+// = 32 columns x 8 warps, warp w sums parts w, w+8, ... (coalesced 128-byte
+// rows), the 8 warp sums combined in warp order (deterministic)
 __global__ void __launch_bounds__(256)
     k_parts_merge(const float* __restrict__ ws, int parts, int64_t pstride, int cols,
                   float* __restrict__ out, int accumulate, int64_t ws_y, float* __restrict__ out_y) {
@@ -729,15 +719,7 @@ cudaError_t layernorm_bwd(const void* dy, const void* x, const void* dres, void*
   if (!xf_width_ok(H) || rows <= 0 || H / 256 > 4) return cudaErrorInvalidValue;
   const int parts = ln_bwd_parts(rows);
   const int64_t chunk = (rows + parts - 1) / parts;
-  static bool attr = false;
-  if (!attr) {  // 64 KB of per-warp accumulators at H = 1024
-    if (cudaError_t e = cudaFuncSetAttribute(k_layernorm_bwd<4>,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize, 65536))
-      return e;
-    attr = true;
-  }
-  const size_t smem = size_t(8) * 2 * H * sizeof(float);
-  DELTA_NV_SWITCH(H, if (cudaError_t e = launch_k(k_layernorm_bwd<NV>, dim3(parts), dim3(256), smem,
+  DELTA_NV_SWITCH(H, if (cudaError_t e = launch_k(k_layernorm_bwd<NV>, dim3(parts), dim3(256), 0,
                                                   st, static_cast<const bf16*>(dy),
                                                   static_cast<const bf16*>(x),
                                                   static_cast<const bf16*>(dres),
