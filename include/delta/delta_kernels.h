@@ -41,6 +41,12 @@ delta_status delta_conv_create_ex(int32_t N, int32_t H, int32_t W, int32_t C, in
                                   int32_t R, int32_t S, int32_t stride, int32_t pad,
                                   int32_t pad_end_h, int32_t pad_end_w, const void* weight,
                                   delta_conv** out);
+/* A 1x1 GEMM y[M][K] = x[M][C] . W with the weights stored [C][K] (read
+ * through MN-major descriptors): e.g. a linear layer's input gradient straight
+ * from its forward weights [out][in], no transposed copy.  Plain
+ * (DELTA_EPI_STORE) and DELTA_EPI_GELU_BWD epilogues. */
+delta_status delta_conv_create_t(int32_t M, int32_t C, int32_t K, const void* weight_ck,
+                                 delta_conv** out);
 /* `stats` (nullable): [ceil(N*P*Q/128)][K] float2 (mean, M2) per 128-row tile
  * of the bf16 outputs — BatchNorm statistics partials fused in the epilogue. */
 delta_status delta_conv_forward(const delta_conv* c, const void* x, void* y, float* stats,

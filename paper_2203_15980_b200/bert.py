@@ -191,8 +191,7 @@ def token_csr(ids: np.ndarray) -> np.ndarray:
 class BertParams:
     """fp32 masters (one flat buffer: embedding tables and weight matrices
     first — their bf16 copy is the GEMM operand — then biases, LayerNorm
-    parameters and the head), AdamW moments, flat fp32 gradients, transposed
-    bf16 weights for the input-gradient GEMMs."""
+    parameters and the head), AdamW moments, flat fp32 gradients."""
 
     def __init__(self, g: G.Graph, device, seed: int = 0):
         cfg = g.cfg
@@ -238,16 +237,8 @@ class BertParams:
             n = int(np.prod(shape))
             self.wbf[name] = self.wbf_flat[off:off + n].view(shape)
             off += n
-        # input-gradient weights W^T ([in][out]) for every linear layer
-        self.wd = {}
-        views = []
-        for name, (cin, cout) in g.linears.items():
-            self.wd[name] = torch.empty(cin, cout, dtype=torch.bfloat16, device=device)
-            views.append(K.WeightView(K.VIEW_DGRAD, cout, 1, 1, cin, 0,
-                                      self.wbf["w:" + name].data_ptr(), self.wd[name].data_ptr()))
-        self.n_views = len(views)
-        arr = (K.WeightView * max(1, len(views)))(*views)
-        self.views_dev = torch.frombuffer(bytearray(arr), dtype=torch.uint8).to(device)
+        # (the input-gradient GEMMs read the forward weights [out][in] through
+        # MN-major descriptors: no transposed copies, no per-step view launch)
         T = cfg.tokens
         self.ln_mean = {n: torch.zeros(T, device=device) for n in g.lns}
         self.ln_rstd = {n: torch.ones(T, device=device) for n in g.lns}
@@ -259,15 +250,12 @@ class BertParams:
 
     def refresh_bf16(self):
         self.wbf_flat.copy_(self.master[:self.n_bf])
-        K.weight_views(self.views_dev.data_ptr(), self.n_views,
-                       torch.cuda.current_stream().cuda_stream)
 
     def adamw_step(self, rng_ptr: int, lr: float, b1=0.9, b2=0.999, eps=1e-6, wd=0.01):
         st = torch.cuda.current_stream().cuda_stream
         K.adamw_step(self.master.data_ptr(), self.m.data_ptr(), self.v.data_ptr(),
                      self.grad.data_ptr(), self.wbf_flat.data_ptr(), self.numel, self.n_bf, lr, b1,
                      b2, eps, wd, rng_ptr, st)
-        K.weight_views(self.views_dev.data_ptr(), self.n_views, st)
 
 
 class BertRuntime(DeltaRuntime):
@@ -300,7 +288,8 @@ class BertRuntime(DeltaRuntime):
         for name, (cin, cout) in self.g.linears.items():
             self._lin[name] = K.Conv(T, 1, 1, cin, cout, 1, 1, 1, 0,
                                      _ptr(self.params.wbf["w:" + name]))
-            d = K.Conv(T, 1, 1, cout, cin, 1, 1, 1, 0, _ptr(self.params.wd[name]))
+            d = K.Conv(T, 1, 1, cout, cin, 1, 1, 1, 0, _ptr(self.params.wbf["w:" + name]),
+                       weights_ck=True)
             if name.endswith("down") and d.tile_n > 128:
                 d.set_tile_n(128)  # gelu' epilogue: N tiles <= 128
             self._lin_d[name] = d

@@ -181,7 +181,11 @@ constexpr int OPT_NB = 2;
 // stages its 128 rows of A and half of the BN weight rows, the leader issues
 // M=256 MMAs that read both CTAs' operands, each CTA's TMEM holds its rows —
 // halving the per-SM operand traffic of the B tile (MODE_TMA only).
-template <int BN, int STAGES, int MODE, int EV, bool OPT = false, bool PAIR = false>
+// BMN: the weight tile is MN-major — weights stored [kdim][K], loaded as
+// 64 x 64 boxes (64 K-rows of 128 B along N) and read through MN-major
+// descriptors (no transposed weight copy for the input-gradient GEMMs).
+template <int BN, int STAGES, int MODE, int EV, bool OPT = false, bool PAIR = false,
+          bool BMN = false>
 __global__ void __launch_bounds__(kThreads, 1)
     k_conv_fwd(const __grid_constant__ CUtensorMap wmap, const __grid_constant__ CUtensorMap amap,
                const __grid_constant__ CUtensorMap ymap, const __grid_constant__ CUtensorMap emap0,
@@ -406,12 +410,25 @@ __global__ void __launch_bounds__(kThreads, 1)
               // both CTAs' bytes complete on the leader's barrier
               if (rank == 0) mbar_arrive_expect_tx(&full[s], 2 * (A_STAGE + B_STAGE));
               tma_load_2d_pair(sA + s * A_STAGE, &amap, &full[s], kb * BK, m0);
-              tma_load_2d_pair(sB + s * B_STAGE, &wmap, &full[s], kb * BK,
-                               n0 + int(rank) * (BN / 2));
+              if constexpr (BMN) {
+#pragma unroll
+                for (int b = 0; b < BN / 128; ++b)
+                  tma_load_2d_pair(sB + s * B_STAGE + b * 8192, &wmap, &full[s],
+                                   n0 + int(rank) * (BN / 2) + 64 * b, kb * BK);
+              } else {
+                tma_load_2d_pair(sB + s * B_STAGE, &wmap, &full[s], kb * BK,
+                                 n0 + int(rank) * (BN / 2));
+              }
             } else {
               mbar_arrive_expect_tx(&full[s], A_STAGE + B_STAGE);
               tma_load_2d(sA + s * A_STAGE, &amap, &full[s], kb * BK, m0);
-              tma_load_2d(sB + s * B_STAGE, &wmap, &full[s], kb * BK, n0);
+              if constexpr (BMN) {
+#pragma unroll
+                for (int b = 0; b < BN / 64; ++b)
+                  tma_load_2d(sB + s * B_STAGE + b * 8192, &wmap, &full[s], n0 + 64 * b, kb * BK);
+              } else {
+                tma_load_2d(sB + s * B_STAGE, &wmap, &full[s], kb * BK, n0);
+              }
             }
           }
         }
@@ -882,7 +899,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     // built by 64-bit adds), one elected lane issues each k-block's MMAs:
     // issuing from lane 0 alone cost a dozen dependent uniform-datapath
     // instructions per MMA, the pacing stage for the N <= 128 tiles.
-    constexpr uint32_t idesc = umma_idesc_bf16(PAIR ? 2 * BM : BM, BN);
+    constexpr uint32_t idesc = umma_idesc_bf16(PAIR ? 2 * BM : BM, BN) | (BMN ? (1u << 16) : 0u);
     uint32_t it = 0, lt = 0;
     // pair: only the leader issues (its MMAs read both CTAs' smem, write both TMEMs)
     for (int tile = unit; tile < ((PAIR && rank != 0) ? 0 : a.tiles); tile += units, ++lt) {
@@ -918,19 +935,22 @@ __global__ void __launch_bounds__(kThreads, 1)
         tc_fence_after();
         const uint64_t ad0 = MODE == MODE_STEM ? umma_desc_noswz(sA + s * A_STAGE, 2048, 128)
                                                : umma_desc_sw128(sA + s * A_STAGE);
-        const uint64_t bd0 = umma_desc_sw128(sB + s * B_STAGE);
+        // BMN: K step of 16 rows = 2 KB into the MN-major boxes (8 KB apart along N)
+        const uint64_t bd0 = BMN ? umma_desc_mn_sw128(sB + s * B_STAGE, 8192)
+                                 : umma_desc_sw128(sB + s * B_STAGE);
+        constexpr int BSTEP = BMN ? 128 : 2;
         if (elect_one()) {
           if constexpr (PAIR) {
 #pragma unroll
             for (int k = 0; k < BK / 16; ++k)
-              umma_bf16_pair(d, ad0 + uint64_t(k * 2), bd0 + uint64_t(k * 2), idesc,
+              umma_bf16_pair(d, ad0 + uint64_t(k * 2), bd0 + uint64_t(k * BSTEP), idesc,
                              (kb | k) != 0 ? 1u : 0u);
             umma_commit_pair(&empty[s]);
           } else {
 #pragma unroll
             for (int k = 0; k < BK / 16; ++k)
               umma_bf16(d, ad0 + uint64_t(MODE == MODE_STEM ? k * 256 : k * 2),
-                        bd0 + uint64_t(k * 2), idesc, (kb | k) != 0 ? 1u : 0u);
+                        bd0 + uint64_t(k * BSTEP), idesc, (kb | k) != 0 ? 1u : 0u);
             umma_commit(&empty[s]);
           }
         }
@@ -1154,10 +1174,11 @@ int num_sms() {
   return n;
 }
 
-template <int BN, int STAGES, int MODE, int EV, bool OPT = false, bool PAIR = false>
+template <int BN, int STAGES, int MODE, int EV, bool OPT = false, bool PAIR = false,
+          bool BMN = false>
 cudaError_t launch(const ConvPlan& cp, const void* x, void* y, float* stats,
                    const ConvEpilogue& epi, cudaStream_t st) {
-  auto kern = k_conv_fwd<BN, STAGES, MODE, EV, OPT, PAIR>;
+  auto kern = k_conv_fwd<BN, STAGES, MODE, EV, OPT, PAIR, BMN>;
   constexpr size_t smem = conv_smem_bytes<BN, STAGES, EV, OPT, PAIR>();
   static_assert(smem <= 227 * 1024, "shared memory");
   static bool attr = false;
@@ -1215,9 +1236,10 @@ cudaError_t launch(const ConvPlan& cp, const void* x, void* y, float* stats,
   }
   // statistics come as one partial row per CTA: always one CTA per SM then
   if constexpr (PAIR) {
-    // CTA pairs: the weight map's box is this CTA's half of the N tile
-    alignas(64) CUtensorMap wmap;
-    if (!encode_2d(&wmap, cp.wptr, uint64_t(cp.kdim), uint64_t(cp.K), uint32_t(BN / 2)))
+    // CTA pairs: the weight map's box is this CTA's half of the N tile (BMN:
+    // 64 x 64 boxes either way)
+    alignas(64) CUtensorMap wmap = *reinterpret_cast<const CUtensorMap*>(cp.wmap);
+    if (!BMN && !encode_2d(&wmap, cp.wptr, uint64_t(cp.kdim), uint64_t(cp.K), uint32_t(BN / 2)))
       return cudaErrorInvalidValue;
     const int sms2 = num_sms() & ~1;
     const int grid = (stats != nullptr || 2 * a.tiles > sms2) ? sms2 : 2 * a.tiles;
@@ -1266,6 +1288,14 @@ int conv_plan_init(ConvPlan* cp, const void* w) {
     if (cp->halo_rows == 0) cp->halo = 0;
   }
   if (!encode_fn()) return 2;
+  if (cp->bmn) {
+    // [kdim][K] weights: 64 (N) x 64 (K) boxes, 128-byte swizzle (MN-major)
+    if (cp->R != 1 || cp->S != 1 || cp->stride != 1 || cp->pad != 0 || cp->K % 64) return 1;
+    return tma_2d_bf16(reinterpret_cast<CUtensorMap*>(cp->wmap), w, uint64_t(cp->K),
+                       uint64_t(cp->kdim), uint64_t(cp->K), 64, 64, CU_TENSOR_MAP_SWIZZLE_128B)
+               ? 0
+               : 3;
+  }
   return encode_2d(reinterpret_cast<CUtensorMap*>(cp->wmap), w, uint64_t(cp->kdim),
                    uint64_t(cp->K), uint32_t(cp->bn))
              ? 0
@@ -1276,6 +1306,7 @@ int conv_plan_set_tile_n(ConvPlan* cp, int bn, const void* w) {
   if (bn != 64 && bn != 128 && bn != 256) return 1;
   if (cp->C == 4 || cp->K % bn != 0) return 1;
   cp->bn = bn;
+  if (cp->bmn) return 0;  // its 64 x 64 boxes do not depend on the tile
   return encode_2d(reinterpret_cast<CUtensorMap*>(cp->wmap), w, uint64_t(cp->kdim),
                    uint64_t(cp->K), uint32_t(cp->bn))
              ? 0
@@ -1293,6 +1324,27 @@ cudaError_t conv_forward(const ConvPlan& cp, const void* x, void* y, float* stat
   const bool tma_a = !stem && cp.R == 1 && cp.S == 1 && cp.stride == 1 && cp.pad == 0 &&
                      cp.pad_end_h == 0 && cp.pad_end_w == 0;
   const bool use_gather = gather_forced();
+  if (cp.bmn) {
+    // [kdim][K] weights (MN-major B): the linear layers' input gradients
+    if (!tma_a || stats) return cudaErrorInvalidValue;
+    const bool pr = pair_ok(cp, true);
+    if (e.mode == EPI_STORE) {
+      switch (cp.bn) {
+        case 64: return launch<64, 8, MODE_TMA, EV_STORE, false, false, true>(cp, x, y, nullptr, e, st);
+        case 128: return launch<128, 6, MODE_TMA, EV_STORE, false, false, true>(cp, x, y, nullptr, e, st);
+        default:
+          return pr ? launch<256, 6, MODE_TMA, EV_STORE, false, true, true>(cp, x, y, nullptr, e, st)
+                    : launch<256, 4, MODE_TMA, EV_STORE, false, false, true>(cp, x, y, nullptr, e, st);
+      }
+    }
+    if (e.mode == EPI_GELU_BWD && e.xc && operands_tma()) {
+      if (cp.bn == 64) return launch<64, 4, MODE_TMA, EV_GELU_BWD, true, false, true>(cp, x, y, nullptr, e, st);
+      if (cp.bn == 128)
+        return pr ? launch<128, 5, MODE_TMA, EV_GELU_BWD, true, true, true>(cp, x, y, nullptr, e, st)
+                  : launch<128, 4, MODE_TMA, EV_GELU_BWD, true, false, true>(cp, x, y, nullptr, e, st);
+    }
+    return cudaErrorInvalidValue;
+  }
   if (e.mode == EPI_SCATTER2) {
     if (stats || (cp.K % 32) || stem || unsigned(e.scatter) > 3u) return cudaErrorInvalidValue;
     switch (cp.bn) {

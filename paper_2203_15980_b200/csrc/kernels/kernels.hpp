@@ -16,6 +16,8 @@ struct ConvPlan {
   int halo, halo_slot, halo_rows;  // 3x3 stride-1: input halo staged per tile (conv_halo.cu)
   int stem_rows;                   // C=4 stem: one output row per tile (conv_fwd.cu MODE_STEMROW)
   const void* wptr;                // the weights (pair mode encodes its half-tile map per launch)
+  int bmn;                         // 1x1 only: weights stored [kdim][K] (read MN-major; e.g. an
+                                   // input gradient straight from the forward's [out][in])
   alignas(64) unsigned char wmap[128];  // CUtensorMap over the [K][kdim] weight matrix
 };
 // Fused epilogues (the backward pass runs input-gradient convolutions through

@@ -68,6 +68,26 @@ delta_status delta_conv_create_ex(int32_t N, int32_t H, int32_t W, int32_t C, in
   return DELTA_OK;
 }
 
+delta_status delta_conv_create_t(int32_t M, int32_t C, int32_t K, const void* weight_ck,
+                                 delta_conv** out) {
+  auto* c = new delta_conv;
+  std::memset(&c->plan, 0, sizeof(c->plan));
+  c->plan.N = M; c->plan.H = 1; c->plan.W = 1; c->plan.C = C; c->plan.K = K;
+  c->plan.R = 1; c->plan.S = 1; c->plan.stride = 1; c->plan.pad = 0;
+  c->plan.pad_end_h = -1; c->plan.pad_end_w = -1;
+  c->plan.bmn = 1;
+  c->weight = weight_ck;
+  int rc = delta_k::conv_plan_init(&c->plan, weight_ck);
+  if (rc != 0) {
+    delete c;
+    delta_rt::set_error(rc == 1 ? "conv_t: unsupported shape (need C%64==0, K%64==0)"
+                                : "conv_t: tensor map encode failed");
+    return rc == 1 ? DELTA_E_UNSUPPORTED : DELTA_E_CUDA;
+  }
+  *out = c;
+  return DELTA_OK;
+}
+
 delta_status delta_conv_forward(const delta_conv* c, const void* x, void* y, float* stats,
                                 void* stream) {
   return cuda_status(delta_k::conv_forward(c->plan, x, y, stats, S(stream)), "conv_forward");

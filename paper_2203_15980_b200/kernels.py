@@ -14,6 +14,7 @@ P = C.POINTER
 _SIGS = {
     "delta_conv_create": (i32, [i32] * 9 + [vp, P(vp)]),
     "delta_conv_create_ex": (i32, [i32] * 11 + [vp, P(vp)]),
+    "delta_conv_create_t": (i32, [i32, i32, i32, vp, P(vp)]),
     "delta_softmax_xent_head": (i32, [vp, i32, vp, vp, vp, vp, vp, vp, vp, i32, i32, vp]),
     "delta_conv_forward": (i32, [vp, vp, vp, vp, vp]),
     "delta_stats_parts": (i32, []),
@@ -81,12 +82,19 @@ class Conv:
     """tcgen05 implicit-GEMM convolution with a cached weight TMA descriptor."""
 
     def __init__(self, N, H, W, Cin, K, R, S, stride, pad, weight_ptr: int,
-                 pad_end: tuple | None = None):
-        """pad_end = (rows, cols) of padding after the input (default: pad)."""
+                 pad_end: tuple | None = None, weights_ck: bool = False):
+        """pad_end = (rows, cols) of padding after the input (default: pad).
+        weights_ck: a 1x1 GEMM over N rows whose weights are stored [Cin][K]
+        (read MN-major: a linear layer's input gradient from the forward's
+        [out][in] weights, no transposed copy)."""
         self._h = vp()
-        pe_h, pe_w = pad_end if pad_end is not None else (-1, -1)
-        check(lib.delta_conv_create_ex(N, H, W, Cin, K, R, S, stride, pad, pe_h, pe_w, weight_ptr,
-                                       C.byref(self._h)))
+        if weights_ck:
+            assert H == W == R == S == stride == 1 and pad == 0
+            check(lib.delta_conv_create_t(N, Cin, K, weight_ptr, C.byref(self._h)))
+        else:
+            pe_h, pe_w = pad_end if pad_end is not None else (-1, -1)
+            check(lib.delta_conv_create_ex(N, H, W, Cin, K, R, S, stride, pad, pe_h, pe_w,
+                                           weight_ptr, C.byref(self._h)))
         p, q, kd, tn = i32(), i32(), i32(), i32()
         lib.delta_conv_geometry(self._h, C.byref(p), C.byref(q), C.byref(kd), C.byref(tn))
         self.P, self.Q, self.kdim, self.tile_n = p.value, q.value, kd.value, tn.value

@@ -155,6 +155,37 @@ def test_linear_gelu_backward_epilogue():
     close(y, pr.grad)
 
 
+@pytest.mark.parametrize("mode", ["store", "gelu_bwd"])
+def test_linear_input_gradient_from_forward_weights(mode):
+    """delta_conv_create_t: the input-gradient GEMM reads the forward weights
+    [out][in] through MN-major descriptors — same result as the transposed
+    copy, bit for bit, and vs fp32 torch"""
+    M, out_f, in_f = 4096, 1024, 4096
+    dy = rnd(M, out_f)
+    w = rnd(out_f, in_f, scale=out_f ** -0.5, seed=1)          # forward weights [out][in]
+    wt = w.t().contiguous()                                      # the transposed copy [in][out]
+    pre = rnd(M, in_f, scale=2.0, seed=2)
+    c_t = K.Conv(M, 1, 1, out_f, in_f, 1, 1, 1, 0, w.data_ptr(), weights_ck=True)
+    c_c = _linear(M, out_f, in_f, wt)
+    if mode == "gelu_bwd":
+        c_t.set_tile_n(128)
+        c_c.set_tile_n(128)
+    y_t = torch.empty(M, in_f, device=dev, dtype=torch.bfloat16)
+    y_c = torch.empty_like(y_t)
+    if mode == "store":
+        c_t(dy.data_ptr(), y_t.data_ptr(), _st())
+        c_c(dy.data_ptr(), y_c.data_ptr(), _st())
+        ref = dy.float() @ w.float()
+    else:
+        c_t.gelu_bwd(dy.data_ptr(), y_t.data_ptr(), pre.data_ptr(), _st())
+        c_c.gelu_bwd(dy.data_ptr(), y_c.data_ptr(), pre.data_ptr(), _st())
+        pr = pre.float().requires_grad_(True)
+        F.gelu(pr).backward(dy.float() @ w.float())
+        ref = pr.grad
+    close(y_t, ref)
+    assert torch.equal(y_t, y_c)
+
+
 def _attn_inputs(B, S, heads, seed=0):
     return rnd(B * S, 3 * heads * 64, seed=seed)
 
