@@ -246,47 +246,65 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int r = quarter * 32 + lane;
     const int q = qt * TILE + r;
     const uint32_t trow = tmem + (uint32_t(quarter * 32) << 16);
-    const int ps = S / 4, nch = ps / 16;  // 16-column chunks of this warp
+    const int ps = S / 4, nch = ps / 16;  // 16-column chunks of this warp (<= 8)
     const int c0 = part * ps;
+    // the dropout keep bits of this row's keys do not depend on S: draw them
+    // while the Q/K loads and the S MMA are in flight (16 bits per chunk)
+    const uint64_t seed = a.rng[0], step = a.rng[1];
+    const uint64_t g0 = ((uint64_t(b * a.heads + h) * S + q) * uint64_t(S) + c0) >> 4;
+    uint32_t kbits[8];
+#pragma unroll
+    for (int c = 0; c < 8; ++c)
+      kbits[c] = (c < nch && a.thr) ? keep16(drop_block(seed, step, a.tag, g0 + c), a.thr) : 0xFFFFu;
     mbar_wait(bar_s, 0);
     tc_fence_after();
     float m = -INFINITY;
     {
-      uint32_t v0[16], v1[16];
-      for (int c = 0; c < nch; c += 2) {
+      uint32_t v0[16], v1[16], v2[16], v3[16];
+      for (int c = 0; c < nch; c += 4) {
         tmem_ld16(trow + c0 + c * 16, v0);
         tmem_ld16(trow + c0 + c * 16 + 16, v1);
+        if (c + 2 < nch) {
+          tmem_ld16(trow + c0 + c * 16 + 32, v2);
+          tmem_ld16(trow + c0 + c * 16 + 48, v3);
+        }
         tmem_wait();
 #pragma unroll
         for (int i = 0; i < 16; ++i) m = fmaxf(m, fmaxf(__uint_as_float(v0[i]), __uint_as_float(v1[i])));
+        if (c + 2 < nch) {
+#pragma unroll
+          for (int i = 0; i < 16; ++i)
+            m = fmaxf(m, fmaxf(__uint_as_float(v2[i]), __uint_as_float(v3[i])));
+        }
       }
     }
     red[part * TILE + r] = m;
     bar_math();
     m = fmaxf(fmaxf(red[r], red[TILE + r]), fmaxf(red[2 * TILE + r], red[3 * TILE + r]));
     const float mc = m * kCl2;
-    const uint64_t seed = a.rng[0], step = a.rng[1];
-    const uint64_t g0 = ((uint64_t(b * a.heads + h) * S + q) * uint64_t(S) + c0) >> 4;
     float l = 0.f;
-    for (int c = 0; c < nch; c += 2) {
-      uint32_t v[2][16];
-      tmem_ld16(trow + c0 + c * 16, v[0]);
-      tmem_ld16(trow + c0 + c * 16 + 16, v[1]);
-      const uint4 kb0 = keep_bytes(seed, step, a.tag, g0 + c, a.thr);
-      const uint4 kb1 = keep_bytes(seed, step, a.tag, g0 + c + 1, a.thr);
-      tmem_wait();
 #pragma unroll
-      for (int hh = 0; hh < 2; ++hh) {
-        const uint4 kb = hh ? kb1 : kb0;
-        uint32_t w[8];
+    for (int c = 0; c < 8; c += 2) {
+      if (c < nch) {
+        uint32_t v[2][16];
+        tmem_ld16(trow + c0 + c * 16, v[0]);
+        tmem_ld16(trow + c0 + c * 16 + 16, v[1]);
+        tmem_wait();
 #pragma unroll
-        for (int i = 0; i < 16; i += 2) {
-          const float p0 = ex2(fmaf(__uint_as_float(v[hh][i]), kCl2, -mc));
-          const float p1 = ex2(fmaf(__uint_as_float(v[hh][i + 1]), kCl2, -mc));
-          l += p0 + p1;
-          w[i >> 1] = pack_bf16x2(p0, p1) & pair_mask((&kb.x)[i >> 2], (i >> 1) & 1);
+        for (int hh = 0; hh < 2; ++hh) {
+          const uint32_t bits = kbits[c + hh];
+          uint32_t w[8];
+#pragma unroll
+          for (int i = 0; i < 16; i += 2) {
+            const float p0 = ex2(fmaf(__uint_as_float(v[hh][i]), kCl2, -mc));
+            const float p1 = ex2(fmaf(__uint_as_float(v[hh][i + 1]), kCl2, -mc));
+            l += p0 + p1;
+            const uint32_t mk = ((0u - ((bits >> i) & 1u)) & 0xFFFFu) |
+                                ((0u - ((bits >> (i + 1)) & 1u)) << 16);
+            w[i >> 1] = pack_bf16x2(p0, p1) & mk;
+          }
+          st_row16(sP, r, c0 + (c + hh) * 16, w);
         }
-        st_row16(sP, r, c0 + (c + hh) * 16, w);
       }
     }
     red[4 * TILE + part * TILE + r] = l;
@@ -491,6 +509,9 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll 1
       for (int hh = 0; hh < 2; ++hh) {
         const int col = hh * 64 + part * 16;  // key column within the block
+        // the half's keep bytes while its S/dP MMAs are in flight
+        const uint4 kb = keep_bytes(seed, step, a.tag,
+                                    ((bh * S + q) * uint64_t(S) + j * TILE + col) >> 4, a.thr);
         if (lane == 0) dbg_mark(warp, 0x10000 | (blk << 1) | hh);
         mbar_wait(bar_sp, nsp & 1);
         ++nsp;
@@ -499,8 +520,6 @@ __global__ void __launch_bounds__(kThreads, 1)
         uint32_t sv[16], dp[16];
         tmem_ld16(trow + T_S + part * 16, sv);
         tmem_ld16(trow + T_DP + part * 16, dp);
-        const uint4 kb = keep_bytes(seed, step, a.tag,
-                                    ((bh * S + q) * uint64_t(S) + j * TILE + col) >> 4, a.thr);
         tmem_wait();
         tc_fence_before();
         __syncwarp();
