@@ -184,6 +184,23 @@ def bert_section(args, world, rank, dp, barrier, max_over_ranks):
     e2e_s = max_over_ranks((time.perf_counter() - t0) / n)
     flops = sum(nd.flops for nd in rt.nodes)  # first productions (recomputes extra)
     B, S = cfg.batch, cfg.seq
+    # the reference simulator planning this run's BERT trace on one host core
+    cpu = None
+    if rank == 0:
+        try:
+            from oracle import ref as oref
+            if oref.available():
+                tj = rt.trace().to_json()
+                ns = oref.time_run_ns(tj, rt.config, 50)
+                sim = oref.run(tj, rt.config)
+                cpu = {"value": round(B / (sim["wall_time_us"] * 1e-6), 1), "unit": "seq/s",
+                       "cores": 1, "kind": "reference",
+                       "sample": f"reference simulator on this run's {len(rt.nodes)}-node BERT trace: "
+                                 f"predicted step {sim['wall_time_us']} us (simulated, not trained); "
+                                 f"{ns * 1e-3:.0f} us per run_iteration on one core",
+                       "same_decisions": sim["decisions"] == [[n, int(a)] for n, a in dprog.decisions]}
+        except Exception as e:  # noqa: BLE001 - never breaks the bench
+            cpu = {"value": None, "sample": f"unavailable: {e}"}
     out = {
         "workload": f"BERT-large (24x1024, 16 heads, FFN 4096) seq {S}, batch {B}/GPU, SQuAD span "
                     f"head, AdamW, dropout 0.1, DELTA at {int(args.bert_budget * 100)}% activation "
@@ -203,6 +220,7 @@ def bert_section(args, world, rank, dp, barrier, max_over_ranks):
                 "d2h_bytes_per_step": 4,
                 "loss_first_last": [round(losses[0], 4), round(losses[-1], 4)]},
         "gpu_launches": launches * n,
+        "cpu_baseline": cpu,
         "data": "synthetic token ids / segments / span labels, random init (no checkpoint)",
     }
     del rt
@@ -787,7 +805,7 @@ def main():
             "clocks": clk,
             "bert": ({k: bert[k] for k in ("seq_per_s", "tokens_per_s", "ms_per_step",
                                             "no_eviction_ratio", "peak_act_gb",
-                                            "peak_act_gb_no_eviction", "parity")}
+                                            "peak_act_gb_no_eviction", "parity", "model_tflops")}
                      | {"e2e_seq_per_s": bert["e2e"]["seq_per_s"],
                         "workload": f"BERT-large seq 512 bs{args.bert_batch}/GPU, "
                                     f"{int(args.bert_budget * 100)}% budget (config 5)"}
