@@ -150,6 +150,11 @@ int64_t delta_stats_partials_floats(int32_t C);
 delta_status delta_bn_stats_from_partials(const float* partials, int32_t C, float* mean,
                                           float* invstd, float eps, float* run_mean,
                                           float* run_var, float momentum, void* stream);
+/* out[c] (=, or += with accumulate) = the column sums of the bf16 outputs a
+ * conv launched with a `stats` buffer reduced: sum over the partial rows of
+ * count * mean, fixed order (a bias gradient without another pass) */
+delta_status delta_stats_col_sum(const float* partials, int32_t C, float* out, int32_t accumulate,
+                                 void* stream);
 /* mode 0 relu(bn(x)), 1 relu(bn(x)+res), 2 relu(bn(x)+bn2(res)) */
 delta_status delta_bn_apply(int32_t mode, const void* x, const void* res, void* y, int64_t M,
                             int32_t C, const float* mean, const float* invstd,

@@ -89,6 +89,7 @@ typedef struct delta_ref {
  *  ATTN            r0 qkv, r1 out, r2 lse, r3 rng, i0 B, i1 S, i2 heads, i3 tag, f0 p
  *  ATTN_BWD        r0 qkv, r1 out, r2 dout, r3 lse, r4 D, r5 dqkv, r6 rng, i0 B, i1 S,
  *                  i2 heads, i3 tag, f0 p
+ *  STATS_SUM       r0 partials, r1 out, i0 C, i1 accumulate  (delta_stats_col_sum)
  */
 enum {
   DELTA_K_COPY = 1,
@@ -118,7 +119,8 @@ enum {
   DELTA_K_SPAN_HEAD = 25,
   DELTA_K_SPAN_HEAD_BWD = 26,
   DELTA_K_ATTN = 27,
-  DELTA_K_ATTN_BWD = 28
+  DELTA_K_ATTN_BWD = 28,
+  DELTA_K_STATS_SUM = 29
 };
 enum {
   DELTA_KOP_FIRST_ONLY = 1,     /* skipped when the node is recomputed        */

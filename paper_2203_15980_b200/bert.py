@@ -134,12 +134,12 @@ def build_bert(cfg: BertConfig) -> G.Graph:
               attrs=dict(ln="lnf"))
     d.hbm_bytes = 4 * act(d)
 
-    def linear_bwd(name, dy, x, pre_act=None, drop=None):
+    def linear_bwd(name, dy, x, pre_act=None, drop=None, bias_done=False):
         lin = name
         parents = [dy.id, x.id] + ([pre_act.id] if pre_act is not None else [])
         cin, cout = g.linears[lin]
         n = g.add(lin + ".bwd", "linear_bwd", (T, cin), parents, phase="B",
-                  attrs=dict(lin=lin, gelu=pre_act is not None, drop=drop))
+                  attrs=dict(lin=lin, gelu=pre_act is not None, drop=drop, bias_done=bias_done))
         n.flops = 4.0 * T * cin * cout
         n.hbm_bytes = 3 * T * cout * 2 + act(x) + act(n) + (act(n) if pre_act is not None else 0)
         return n
@@ -148,7 +148,8 @@ def build_bert(cfg: BertConfig) -> G.Graph:
             reversed(layers), reversed(range(cfg.layers))):
         g_out = d                                   # d add2
         d_up = linear_bwd(pre + "down", g_out, ge, pre_act=up, drop=drop_tag(l, 2))
-        d_ln2 = linear_bwd(pre + "up", d_up, ln2)
+        # (its bias gradient comes from the gelu' GEMM's epilogue statistics)
+        d_ln2 = linear_bwd(pre + "up", d_up, ln2, bias_done=True)
         d_add1 = g.add(pre + "ln2.bwd", "layernorm_bwd", (T, H), [d_ln2.id, add1.id, g_out.id],
                        phase="B", attrs=dict(ln=pre + "ln2", dres=2))
         d_add1.hbm_bytes = 5 * act(d_add1)
@@ -300,6 +301,9 @@ class BertRuntime(DeltaRuntime):
         self.cs_ws = torch.empty(max(K.colsum_workspace_floats(T, cfg.ffn),
                                      K.span_head_workspace_floats(T, H)), device=dev)
         self.drop_ws = torch.empty(T, H, dtype=torch.bfloat16, device=dev)  # dropout-bwd scratch
+        # per-CTA column statistics of the gelu' input gradient (its column
+        # sums are the up-projection's bias gradient: no extra pass over it)
+        self.gstats = torch.empty(K.stats_partials_floats(cfg.ffn), device=dev)
         self.attn_D = torch.empty(cfg.batch * cfg.heads * cfg.seq, device=dev)
         self.dlogits = torch.empty(T, 2, device=dev)
         self.row_loss = torch.empty(cfg.batch, device=dev)
@@ -429,14 +433,21 @@ class BertRuntime(DeltaRuntime):
                 dy = _ptr(self.drop_ws)
             dconv = self._lin_d[lin]._h
             if node.attrs.get("gelu"):
-                add(X.kop(X.K_CONV_EX, (dy, X.OUT(), None, None, None, None, X.IN(2)),
+                # the gelu' input gradient also reduces its per-CTA column
+                # statistics: the bias gradient of the up projection (whose
+                # output gradient it is) follows from them below
+                up = self.g.nodes[node.parents[2]].attrs["lin"]
+                add(X.kop(X.K_CONV_EX, (dy, X.OUT(), _ptr(self.gstats), None, None, None, X.IN(2)),
                           (K.EPI_GELU_BWD, 0, 0), conv=dconv))
+                add(X.kop(X.K_STATS_SUM, (_ptr(self.gstats), _ptr(pr.gviews["b:" + up])),
+                          (self.g.linears[up][1], 0)))
             else:
                 add(X.kop(X.K_CONV, (dy, X.OUT(), None), conv=dconv))
             add(X.kop(X.K_WGRAD, (dy, X.IN(1), _ptr(pr.gviews["w:" + lin]), _ptr(self.wg_ws)),
                       conv=self._lin_w[lin]._h), self._lin_w[lin].launches)
-            add(X.kop(X.K_COLSUM, (dy, None, _ptr(pr.gviews["b:" + lin]), _ptr(self.cs_ws)),
-                      (T, cout, 0, 0)), 2)
+            if not node.attrs.get("bias_done"):
+                add(X.kop(X.K_COLSUM, (dy, None, _ptr(pr.gviews["b:" + lin]), _ptr(self.cs_ws)),
+                          (T, cout, 0, 0)), 2)
         elif op == "attention_bwd":
             l = node.attrs["layer"]
             add(X.kop(X.K_ATTN_BWD, (X.IN(1), X.IN(2), X.IN(0), _ptr(pr.lse[l]), _ptr(self.attn_D),

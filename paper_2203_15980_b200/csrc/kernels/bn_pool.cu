@@ -258,6 +258,20 @@ __global__ void __launch_bounds__(256)
   }
 }
 
+// Column sums from the per-CTA statistics rows (count, mean, M2): sum =
+// sum over rows of count * mean, fixed order — a bias gradient from the
+// statistics a GEMM epilogue already reduced (no separate pass over dY)
+__global__ void __launch_bounds__(256)
+    k_stats_col_sum(const float4* __restrict__ ws, int parts, int C, float* out, int accumulate) {
+  pdl_wait();
+  pdl_trigger();
+  const int c0 = blockIdx.x * 8;
+  const float2 sn = rows_sum8(ws, parts, C, c0,
+                              [](float4 p) { return make_float2(p.x * p.y, 0.f); });
+  const int c = c0 + threadIdx.x;
+  if (threadIdx.x < 8 && c < C) out[c] = accumulate ? out[c] + sn.x : sn.x;
+}
+
 // BN backward reductions from the per-CTA rows (sum g, sum g*xc): dbeta,
 // dgamma per channel, fixed order
 __global__ void __launch_bounds__(256)
@@ -1212,6 +1226,12 @@ cudaError_t bn_backward_from_partials(const float* partials, const void* g, cons
                   static_cast<const bf16*>(g), 0, nullptr, static_cast<const bf16*>(x),
                   static_cast<bf16*>(dx), vecs, C - 1, __builtin_ctz(C), M, mean, invstd, gamma,
                   dgamma, dbeta);
+}
+
+cudaError_t stats_col_sum(const float* partials, int C, float* out, int accumulate,
+                          cudaStream_t st) {
+  return launch_k(k_stats_col_sum, dim3((C + 7) / 8), dim3(256), 0, st,
+                  reinterpret_cast<const float4*>(partials), stats_parts(), C, out, accumulate);
 }
 
 cudaError_t add_grad(const void* a, const void* up, int pool_hw, const void* up_mask,

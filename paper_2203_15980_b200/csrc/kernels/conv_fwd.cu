@@ -1325,8 +1325,10 @@ cudaError_t conv_forward(const ConvPlan& cp, const void* x, void* y, float* stat
                      cp.pad_end_h == 0 && cp.pad_end_w == 0;
   const bool use_gather = gather_forced();
   if (cp.bmn) {
-    // [kdim][K] weights (MN-major B): the linear layers' input gradients
-    if (!tma_a || stats) return cudaErrorInvalidValue;
+    // [kdim][K] weights (MN-major B): the linear layers' input gradients;
+    // `stats` (gelu' epilogue): per-CTA column statistics of the output
+    // (its column sums are the up-projection's bias gradient)
+    if (!tma_a || (stats && e.mode != EPI_GELU_BWD)) return cudaErrorInvalidValue;
     const bool pr = pair_ok(cp, true);
     if (e.mode == EPI_STORE) {
       switch (cp.bn) {
@@ -1338,10 +1340,10 @@ cudaError_t conv_forward(const ConvPlan& cp, const void* x, void* y, float* stat
       }
     }
     if (e.mode == EPI_GELU_BWD && e.xc && operands_tma()) {
-      if (cp.bn == 64) return launch<64, 4, MODE_TMA, EV_GELU_BWD, true, false, true>(cp, x, y, nullptr, e, st);
+      if (cp.bn == 64) return launch<64, 4, MODE_TMA, EV_GELU_BWD, true, false, true>(cp, x, y, stats, e, st);
       if (cp.bn == 128)
-        return pr ? launch<128, 5, MODE_TMA, EV_GELU_BWD, true, true, true>(cp, x, y, nullptr, e, st)
-                  : launch<128, 4, MODE_TMA, EV_GELU_BWD, true, false, true>(cp, x, y, nullptr, e, st);
+        return pr ? launch<128, 5, MODE_TMA, EV_GELU_BWD, true, true, true>(cp, x, y, stats, e, st)
+                  : launch<128, 4, MODE_TMA, EV_GELU_BWD, true, false, true>(cp, x, y, stats, e, st);
     }
     return cudaErrorInvalidValue;
   }

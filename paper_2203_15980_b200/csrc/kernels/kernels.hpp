@@ -98,6 +98,11 @@ cudaError_t bn_stats_from_partials(const float* partials, int C, float* mean, fl
                                    float eps, float* run_mean, float* run_var, float momentum,
                                    cudaStream_t st);
 
+// out[c] (=|+=) sum over the rows of count * mean: column sums of the
+// outputs a conv/GEMM epilogue reduced into statistics partials
+cudaError_t stats_col_sum(const float* partials, int C, float* out, int accumulate,
+                          cudaStream_t st);
+
 // mode 0: y = relu(bn(x)); 1: y = relu(bn(x) + res); 2: y = relu(bn(x) + bn2(res))
 cudaError_t bn_apply(int mode, const void* x, const void* res, void* y, int64_t M, int C,
                      const float* mean, const float* invstd, const float* gamma, const float* beta,

@@ -271,6 +271,10 @@ delta_status run_kop(delta_rt* rt, const delta_kop& k, Frame& fr, uint64_t node,
                                  rp<float>(fr, r[4]), ref(fr, r[5]), int(i[0]), int(i[1]), int(i[2]),
                                  k.f[0], rp<const uint64_t>(fr, r[6]), uint32_t(i[3]), st);
       break;
+    case DELTA_K_STATS_SUM:
+      e = delta_k::stats_col_sum(rp<const float>(fr, r[0]), int(i[0]), rp<float>(fr, r[1]), int(i[1]),
+                                 st);
+      break;
     case DELTA_K_HOST: {
       if (!rt->host_fn) return fail(DELTA_E_ARGUMENT, "recipe: HOST op without a host callback");
       std::vector<uint64_t> ins(fr.n_in);

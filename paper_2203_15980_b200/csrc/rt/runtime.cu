@@ -178,6 +178,12 @@ int32_t delta_stats_parts(void) { return delta_k::stats_parts(); }
 
 int64_t delta_stats_partials_floats(int32_t C) { return delta_k::stats_partials_floats(C); }
 
+delta_status delta_stats_col_sum(const float* partials, int32_t C, float* out, int32_t accumulate,
+                                 void* stream) {
+  DELTA_CUDA(delta_k::stats_col_sum(partials, C, out, accumulate, S(stream)));
+  return DELTA_OK;
+}
+
 delta_status delta_bn_stats_from_partials(const float* partials, int32_t C, float* mean,
                                           float* invstd, float eps, float* rm, float* rv,
                                           float mom, void* stream) {

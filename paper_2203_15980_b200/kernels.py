@@ -20,6 +20,7 @@ _SIGS = {
     "delta_stats_parts": (i32, []),
     "delta_stats_partials_floats": (i64, [i32]),
     "delta_bn_stats_from_partials": (i32, [vp, i32, vp, vp, f32, vp, vp, f32, vp]),
+    "delta_stats_col_sum": (i32, [vp, i32, vp, i32, vp]),
     "delta_conv_forward_ex": (i32, [vp, vp, vp, vp, vp, vp]),
     "delta_conv_set_tile_n": (i32, [vp, i32]),
     "delta_wgrad_create": (i32, [i32] * 9 + [P(vp)]),
@@ -135,10 +136,11 @@ class Conv:
         check(lib.delta_conv_forward_ex(self._h, x_ptr, y_ptr, None, C.byref(e), stream))
         _count(1)
 
-    def gelu_bwd(self, x_ptr, y_ptr, pre_ptr, stream):
-        """y = bf16(conv(x) * gelu'(pre)): an MLP input gradient through the GELU"""
+    def gelu_bwd(self, x_ptr, y_ptr, pre_ptr, stream, stats_ptr=None):
+        """y = bf16(conv(x) * gelu'(pre)): an MLP input gradient through the GELU;
+        stats_ptr: per-CTA column statistics of y (stats_col_sum -> its column sums)"""
         e = ConvEpilogue(EPI_GELU_BWD, 0, 0, 0, None, None, None, pre_ptr, None, None, None, None)
-        check(lib.delta_conv_forward_ex(self._h, x_ptr, y_ptr, None, C.byref(e), stream))
+        check(lib.delta_conv_forward_ex(self._h, x_ptr, y_ptr, stats_ptr, C.byref(e), stream))
         _count(1)
 
     def bn_bwd(self, x_ptr, g_ptr, partials_ptr, xc, mean, invstd, gamma, beta, stream):
@@ -224,6 +226,11 @@ def stats_parts() -> int:
 
 def stats_partials_floats(C_: int) -> int:
     return int(lib.delta_stats_partials_floats(C_))
+
+
+def stats_col_sum(partials, C_, out, stream, accumulate=False):
+    check(lib.delta_stats_col_sum(partials, C_, out, int(accumulate), stream))
+    _count(1)
 
 
 def bn_stats_from_partials(partials, C_, mean, invstd, eps, run_mean, run_var, momentum, stream):
