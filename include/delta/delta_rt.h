@@ -87,8 +87,8 @@ typedef struct delta_ref {
  *                  r7 loss, i0 B, i1 S, i2 H
  *  SPAN_HEAD_BWD   r0 h, r1 dlogits, r2 w, r3 dh, r4 dw, r5 dbias, r6 ws, i0 T, i1 H
  *  ATTN            r0 qkv, r1 out, r2 lse, r3 rng, i0 B, i1 S, i2 heads, i3 tag, f0 p
- *  ATTN_BWD        r0 qkv, r1 out, r2 dout, r3 lse, r4 D, r5 dqkv, r6 rng, i0 B, i1 S,
- *                  i2 heads, i3 tag, f0 p
+ *  ATTN_BWD        r0 qkv, r1 out, r2 dout, r3 lse, r4 D, r5 dqkv, r6 rng, r7 dbias
+ *                  (optional), r8 ws, i0 B, i1 S, i2 heads, i3 tag, f0 p
  *  STATS_SUM       r0 partials, r1 out, i0 C, i1 accumulate  (delta_stats_col_sum)
  */
 enum {

@@ -86,11 +86,14 @@ delta_status delta_span_head_bwd(const void* h, const float* dlogits, const floa
 delta_status delta_attention_fwd(const void* qkv, void* out, float* lse, int32_t B, int32_t S,
                                  int32_t heads, float p, const uint64_t* rng, uint32_t tag,
                                  void* stream);
-/* dqkv [B*S][3*heads*64] from dout; D: fp32 [B*heads][S] scratch */
+/* dqkv [B*S][3*heads*64] from dout; D: fp32 [B*heads][S] scratch.  dbias
+ * (optional, fp32 [3*heads*64], overwritten): the column sums of dqkv — the
+ * QKV projection's bias gradient — reduced inside the kernel per sequence
+ * into ws (fp32 [B][3*heads*64]) and merged in sequence order. */
 delta_status delta_attention_bwd(const void* qkv, const void* out, const void* dout,
                                  const float* lse, float* D, void* dqkv, int32_t B, int32_t S,
                                  int32_t heads, float p, const uint64_t* rng, uint32_t tag,
-                                 void* stream);
+                                 float* dbias, float* ws, void* stream);
 /* debugging aid: the backward kernel writes progress words (32 per CTA) to
  * this mapped host buffer (NULL = off) */
 delta_status delta_attention_debug(void* host_words);

@@ -159,7 +159,8 @@ def build_bert(cfg: BertConfig) -> G.Graph:
                       attrs=dict(layer=l, tag=drop_tag(l, 0)))
         d_qkv.flops = 2.5 * att.flops + 2 * att.flops  # 5 GEMMs + S/dP recomputed by both roles
         d_qkv.hbm_bytes = 2 * act(qkv) + 3 * act(att)
-        d_ln1 = linear_bwd(pre + "qkv", d_qkv, ln1)
+        # (its bias gradient is reduced inside the attention backward)
+        d_ln1 = linear_bwd(pre + "qkv", d_qkv, ln1, bias_done=True)
         d = g.add(pre + "ln1.bwd", "layernorm_bwd", (T, H), [d_ln1.id, X_.id, d_add1.id],
                   phase="B", attrs=dict(ln=pre + "ln1", dres=2))
         d.hbm_bytes = 5 * act(d)
@@ -299,7 +300,8 @@ class BertRuntime(DeltaRuntime):
         self.wg_ws = torch.zeros(wg_ws, dtype=torch.uint8, device=dev)  # split counters: zero once
         self.ln_ws = torch.empty(K.layernorm_bwd_workspace_floats(T, H), device=dev)
         self.cs_ws = torch.empty(max(K.colsum_workspace_floats(T, cfg.ffn),
-                                     K.span_head_workspace_floats(T, H)), device=dev)
+                                     K.span_head_workspace_floats(T, H),
+                                     cfg.batch * 3 * H), device=dev)
         self.drop_ws = torch.empty(T, H, dtype=torch.bfloat16, device=dev)  # dropout-bwd scratch
         # per-CTA column statistics of the gelu' input gradient (its column
         # sums are the up-projection's bias gradient: no extra pass over it)
@@ -450,9 +452,13 @@ class BertRuntime(DeltaRuntime):
                           (T, cout, 0, 0)), 2)
         elif op == "attention_bwd":
             l = node.attrs["layer"]
+            # dqkv and, reduced per sequence inside the kernel, its column
+            # sums: the QKV projection's bias gradient
+            qkv_lin = self.g.nodes[node.parents[1]].attrs["lin"]
             add(X.kop(X.K_ATTN_BWD, (X.IN(1), X.IN(2), X.IN(0), _ptr(pr.lse[l]), _ptr(self.attn_D),
-                                     X.OUT(), rng),
-                      (cfg.batch, cfg.seq, cfg.heads, node.attrs["tag"]), (cfg.p_attn,)), 2)
+                                     X.OUT(), rng, _ptr(pr.gviews["b:" + qkv_lin]),
+                                     _ptr(self.cs_ws)),
+                      (cfg.batch, cfg.seq, cfg.heads, node.attrs["tag"]), (cfg.p_attn,)), 3)
         elif op == "embed_bwd":
             add(X.kop(X.K_DROPOUT_BWD, (X.IN(0), X.OUT(), rng), (T * H, EMBED_TAG),
                       (cfg.p_hidden,)))

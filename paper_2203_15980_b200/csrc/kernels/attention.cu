@@ -134,6 +134,32 @@ __device__ __forceinline__ void store16(bf16* dst, const uint32_t (&v)[16], floa
                       pack_bf16x2(__uint_as_float(v[8 * u + 6]) * s, __uint_as_float(v[8 * u + 7]) * s));
 }
 
+// column sums of a warp's [32 rows (lanes)][32 columns (v)] block: lane c
+// returns the sum over the 32 lanes of column c (recursive halving, 31
+// shuffles; a fixed combination order, so deterministic)
+__device__ __forceinline__ float warp_colsum32(float (&v)[32], int lane) {
+#pragma unroll
+  for (int o = 16; o >= 1; o >>= 1) {
+    const bool up = lane & o;
+#pragma unroll
+    for (int k = 0; k < o; ++k) {
+      const float got = __shfl_xor_sync(0xffffffffu, up ? v[k] : v[k + o], o);
+      v[k] = (up ? v[k + o] : v[k]) + got;
+    }
+  }
+  return v[0];
+}
+__device__ __forceinline__ float warp_colsum_scaled(const uint32_t (&a)[16], const uint32_t (&b)[16],
+                                                    float s, int lane) {
+  float v[32];
+#pragma unroll
+  for (int e = 0; e < 16; ++e) {
+    v[e] = __uint_as_float(a[e]) * s;
+    v[16 + e] = __uint_as_float(b[e]) * s;
+  }
+  return warp_colsum32(v, lane);
+}
+
 // debug: progress words in mapped host memory (null = off), set by
 // attention_debug(); the host can read them while a kernel is stuck
 __device__ uint32_t* g_attn_dbg = nullptr;
@@ -154,6 +180,7 @@ struct AttnArgs {
   float dscale;
   const uint64_t* rng;
   uint32_t tag;
+  float* colpart;  // bwd, optional: [B][3 Hd] per-sequence column sums of dqkv (bias gradient)
 };
 
 // ======================================================================= fwd
@@ -499,6 +526,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       Dv[i] = __ldg(a.D + bh * S + i * TILE + r);
     }
     uint32_t nsp = 0;
+    float csum_kv = 0.f;
     for (int blk = 0; blk < nblk; ++blk) {
       const int j = blk / nt, i = blk % nt;
       const int q = i * TILE + r;
@@ -564,11 +592,15 @@ __global__ void __launch_bounds__(kThreads, 1)
                     h * HD + (part & 1) * 32;
         store16(dst, v0, which ? 1.f : kScale);
         store16(dst + 16, v1, which ? 1.f : kScale);
+        // bias gradient: this warp's 32 key rows summed per column, lane c
+        // keeps column c across the key blocks
+        if (a.colpart) csum_kv += warp_colsum_scaled(v0, v1, which ? 1.f : kScale, lane);
       }
     }
     // ---- dQ of every query block (TMEM 64 i, lane = query row) ----
     mbar_wait(bar_acc, (nblk - 1) & 1);
     tc_fence_after();
+    float csum_q0 = 0.f, csum_q1 = 0.f;
     for (int i = part; i < nt; i += 4) {
       uint32_t v0[16], v1[16], v2[16], v3[16];
       tmem_ld16(trow + 64 * i, v0);
@@ -581,6 +613,34 @@ __global__ void __launch_bounds__(kThreads, 1)
       store16(dst + 16, v1, kScale);
       store16(dst + 32, v2, kScale);
       store16(dst + 48, v3, kScale);
+      if (a.colpart) {
+        csum_q0 = warp_colsum_scaled(v0, v1, kScale, lane);
+        csum_q1 = warp_colsum_scaled(v2, v3, kScale, lane);
+      }
+    }
+    if (a.colpart) {
+      // every MMA is done: P's buffer is scratch.  Combine the warps' column
+      // sums in a fixed order into this (sequence, head)'s 192 bias columns.
+      float* cs = reinterpret_cast<float*>(smem + (sP - sQ));
+      cs[(quarter * 4 + part) * 32 + lane] = csum_kv;             // [quarter][part][32]
+      cs[512 + (part * 4 + quarter) * 64 + lane] = csum_q0;       // [tile][quarter][64]
+      cs[512 + (part * 4 + quarter) * 64 + 32 + lane] = csum_q1;
+      bar_math();
+      const int t = threadIdx.x;
+      if (t < 3 * HD) {
+        float s = 0.f;
+        int third, c = t % HD;
+        if (t < HD) {
+          third = 0;
+          for (int i = 0; i < nt; ++i)
+            for (int qq = 0; qq < 4; ++qq) s += cs[512 + (i * 4 + qq) * 64 + c];
+        } else {
+          third = t / HD;  // 1: dK (parts 0, 1), 2: dV (parts 2, 3)
+          const int pp = (third - 1) * 2 + c / 32;
+          for (int qq = 0; qq < 4; ++qq) s += cs[(qq * 4 + pp) * 32 + (c & 31)];
+        }
+        a.colpart[int64_t(b) * 3 * a.Hd + third * a.Hd + h * HD + c] = s;
+      }
     }
   }
   tc_fence_before();
@@ -628,8 +688,9 @@ cudaError_t attention_debug(void* host_words) {
 
 cudaError_t attention_bwd(const void* qkv, const void* out, const void* dout, const float* lse,
                           float* D, void* dqkv, int B, int S, int heads, float p,
-                          const uint64_t* rng, uint32_t tag, cudaStream_t st) {
-  if (!shape_ok(S, heads)) return cudaErrorInvalidValue;
+                          const uint64_t* rng, uint32_t tag, float* dbias, float* ws,
+                          cudaStream_t st) {
+  if (!shape_ok(S, heads) || (dbias && !ws)) return cudaErrorInvalidValue;
   const int Hd = heads * HD;
   const int64_t T = int64_t(B) * S;
   if (cudaError_t e = attn_dvec(out, dout, T, S, heads, D, st)) return e;
@@ -641,7 +702,7 @@ cudaError_t attention_bwd(const void* qkv, const void* out, const void* dout, co
     return cudaErrorInvalidValue;
   const DropParams dp = drop_params(p);
   AttnArgs a{B, S, heads, Hd, static_cast<bf16*>(dqkv), const_cast<float*>(lse), D, dp.thr,
-             dp.scale, rng, tag};
+             dp.scale, rng, tag, dbias ? ws : nullptr};
   static bool attr = false;
   if (!attr) {
     if (cudaError_t e = cudaFuncSetAttribute(k_attn_bwd, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -651,6 +712,8 @@ cudaError_t attention_bwd(const void* qkv, const void* out, const void* dout, co
   }
   if (cudaError_t e = launch_k(k_attn_bwd, dim3(heads, B), dim3(kThreads), bwd_smem(S), st, qm, dm, a))
     return e;
+  if (dbias)
+    if (cudaError_t e = merge_parts(ws, B, 3 * Hd, dbias, st)) return e;
   return cudaGetLastError();
 }
 

@@ -683,6 +683,10 @@ int grid_for(int64_t work, int per_block) {
 
 }  // namespace
 
+cudaError_t merge_parts(const float* ws, int parts, int cols, float* out, cudaStream_t st) {
+  return parts_merge(ws, parts, cols, cols, out, 0, st);
+}
+
 // ================================================================ launchers
 #define DELTA_NV_SWITCH(H, CALL)      \
   switch ((H) / 256) {                \

@@ -38,6 +38,8 @@ cudaError_t span_head_bwd(const void* h, const float* dlogits, const float* w, v
                           float* dbias, float* ws, int64_t T, int H, cudaStream_t st);
 cudaError_t attn_dvec(const void* o, const void* dout, int64_t T, int S, int heads, float* D,
                       cudaStream_t st);
+// out[c] = sum over p < parts of ws[p * cols + c], in order of p
+cudaError_t merge_parts(const float* ws, int parts, int cols, float* out, cudaStream_t st);
 cudaError_t adamw_step(float* w, float* m, float* v, const float* g, void* wbf, int64_t n,
                        int64_t n_bf, float lr, float b1, float b2, float eps, float wd,
                        uint64_t* rng, cudaStream_t st);
@@ -50,9 +52,12 @@ cudaError_t attention_fwd(const void* qkv, void* out, float* lse, int B, int S, 
                           float p, const uint64_t* rng, uint32_t tag, cudaStream_t st);
 // debug: progress words of the backward kernel in mapped host memory (32 per CTA)
 cudaError_t attention_debug(void* host_words);
-// dqkv [B*S][3*heads*64]; D = rowsum(dO * O) scratch [B*heads][S]
+// dqkv [B*S][3*heads*64]; D = rowsum(dO * O) scratch [B*heads][S]; if dbias
+// (fp32 [3*heads*64], overwritten): the column sums of dqkv, per-sequence
+// partials in ws [B][3*heads*64] merged in sequence order
 cudaError_t attention_bwd(const void* qkv, const void* out, const void* dout, const float* lse,
                           float* D, void* dqkv, int B, int S, int heads, float p,
-                          const uint64_t* rng, uint32_t tag, cudaStream_t st);
+                          const uint64_t* rng, uint32_t tag, float* dbias, float* ws,
+                          cudaStream_t st);
 
 }  // namespace delta_k

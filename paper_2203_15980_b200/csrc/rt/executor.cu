@@ -269,7 +269,8 @@ delta_status run_kop(delta_rt* rt, const delta_kop& k, Frame& fr, uint64_t node,
     case DELTA_K_ATTN_BWD:
       e = delta_k::attention_bwd(ref(fr, r[0]), ref(fr, r[1]), ref(fr, r[2]), rp<const float>(fr, r[3]),
                                  rp<float>(fr, r[4]), ref(fr, r[5]), int(i[0]), int(i[1]), int(i[2]),
-                                 k.f[0], rp<const uint64_t>(fr, r[6]), uint32_t(i[3]), st);
+                                 k.f[0], rp<const uint64_t>(fr, r[6]), uint32_t(i[3]),
+                                 rp<float>(fr, r[7]), rp<float>(fr, r[8]), st);
       break;
     case DELTA_K_STATS_SUM:
       e = delta_k::stats_col_sum(rp<const float>(fr, r[0]), int(i[0]), rp<float>(fr, r[1]), int(i[1]),

@@ -97,9 +97,9 @@ delta_status delta_attention_fwd(const void* qkv, void* out, float* lse, int32_t
 delta_status delta_attention_bwd(const void* qkv, const void* out, const void* dout,
                                  const float* lse, float* D, void* dqkv, int32_t B, int32_t S_,
                                  int32_t heads, float p, const uint64_t* rng, uint32_t tag,
-                                 void* stream) {
-  return st_(delta_k::attention_bwd(qkv, out, dout, lse, D, dqkv, B, S_, heads, p, rng, tag,
-                                    S(stream)),
+                                 float* dbias, float* ws, void* stream) {
+  return st_(delta_k::attention_bwd(qkv, out, dout, lse, D, dqkv, B, S_, heads, p, rng, tag, dbias,
+                                    ws, S(stream)),
              "attention_bwd");
 }
 delta_status delta_attention_debug(void* host_words) {

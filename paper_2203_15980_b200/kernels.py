@@ -381,7 +381,7 @@ _XSIGS = {
     "delta_span_head_workspace_floats": (i64, [i64, i32]),
     "delta_span_head_bwd": (i32, [vp] * 7 + [i64, i32, vp]),
     "delta_attention_fwd": (i32, [vp, vp, vp, i32, i32, i32, f32, vp, u32, vp]),
-    "delta_attention_bwd": (i32, [vp] * 6 + [i32, i32, i32, f32, vp, u32, vp]),
+    "delta_attention_bwd": (i32, [vp] * 6 + [i32, i32, i32, f32, vp, u32, vp, vp, vp]),
     "delta_adamw_step": (i32, [vp] * 5 + [i64, i64, f32, f32, f32, f32, f32, vp, vp]),
 }
 for _n, (_r, _a) in _XSIGS.items():
@@ -460,8 +460,11 @@ def attention_fwd(qkv, out, lse, B, S, heads, p, rng, tag, stream):
     _count(1)
 
 
-def attention_bwd(qkv, out, dout, lse, D, dqkv, B, S, heads, p, rng, tag, stream):
-    check(lib.delta_attention_bwd(qkv, out, dout, lse, D, dqkv, B, S, heads, p, rng, tag, stream))
+def attention_bwd(qkv, out, dout, lse, D, dqkv, B, S, heads, p, rng, tag, stream, dbias=None,
+                  ws=None):
+    """dbias (fp32 [3*heads*64]) = column sums of dqkv when given; ws fp32 [B][3*heads*64]"""
+    check(lib.delta_attention_bwd(qkv, out, dout, lse, D, dqkv, B, S, heads, p, rng, tag, dbias, ws,
+                                  stream))
     _count(2)
 
 

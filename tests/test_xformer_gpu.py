@@ -228,10 +228,20 @@ def test_attention_forward_backward(B, S, heads, p):
     for i, name in enumerate("qkv"):
         # dQ/dK/dV: bf16 P and dS operands on the tensor cores -> looser tolerance
         close(got[:, i], g[:, i], 3e-2, 3e-2)
+    # with the QKV bias gradient reduced in the kernel: dqkv unchanged, the
+    # column sums match the fp32 reference's, and are deterministic
     dqkv2 = torch.empty_like(dqkv)
-    K.attention_bwd(qkv.data_ptr(), out.data_ptr(), dout.data_ptr(), lse.data_ptr(), D.data_ptr(),
-                    dqkv2.data_ptr(), B, S, heads, p, rng.data_ptr(), 11, _st())
-    assert torch.equal(dqkv, dqkv2)
+    db = torch.empty(3 * Hd, device=dev)
+    ws = torch.empty(B * 3 * Hd, device=dev)
+    dbs = []
+    for _ in range(2):
+        K.attention_bwd(qkv.data_ptr(), out.data_ptr(), dout.data_ptr(), lse.data_ptr(),
+                        D.data_ptr(), dqkv2.data_ptr(), B, S, heads, p, rng.data_ptr(), 11, _st(),
+                        db.data_ptr(), ws.data_ptr())
+        assert torch.equal(dqkv, dqkv2)
+        dbs.append(db.clone())
+    assert torch.equal(dbs[0], dbs[1])
+    close(db, qr.grad.view(B * S, 3 * Hd).sum(0), 3e-2, 3e-2)
 
 
 def test_embeddings_forward_and_table_gradients():
