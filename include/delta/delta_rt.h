@@ -90,6 +90,8 @@ typedef struct delta_ref {
  *  ATTN_BWD        r0 qkv, r1 out, r2 dout, r3 lse, r4 D, r5 dqkv, r6 rng, r7 dbias
  *                  (optional), r8 ws, i0 B, i1 S, i2 heads, i3 tag, f0 p
  *  STATS_SUM       r0 partials, r1 out, i0 C, i1 accumulate  (delta_stats_col_sum)
+ *  LAYERNORM_BWD_DROP  as LAYERNORM_BWD, + r10 dxd, r11 dbias, r12 rng, i2 tag, f0 p
+ *                  (delta_layernorm_bwd_drop)
  */
 enum {
   DELTA_K_COPY = 1,
@@ -120,7 +122,8 @@ enum {
   DELTA_K_SPAN_HEAD_BWD = 26,
   DELTA_K_ATTN = 27,
   DELTA_K_ATTN_BWD = 28,
-  DELTA_K_STATS_SUM = 29
+  DELTA_K_STATS_SUM = 29,
+  DELTA_K_LAYERNORM_BWD_DROP = 30
 };
 enum {
   DELTA_KOP_FIRST_ONLY = 1,     /* skipped when the node is recomputed        */
@@ -136,7 +139,7 @@ typedef struct delta_kop {
   int64_t i[4];
   float f[2];
   uint32_t pad;
-  delta_ref r[11];
+  delta_ref r[14];
 } delta_kop;
 
 /* node -> its ops: kops[first .. first + count) */

@@ -43,6 +43,16 @@ delta_status delta_layernorm_bwd(const void* dy, const void* x, const void* dres
                                  const float* mean, const float* rstd, const float* gamma,
                                  float* dgamma, float* dbeta, float* ws, int64_t rows, int32_t H,
                                  void* stream);
+/* delta_layernorm_bwd, and the gradient through the dropout (p, tag) of the
+ * residual branch that fed this LayerNorm's input, in the same pass:
+ * dxd = dropout mask * scale * dx (bf16, the mask of delta_add_dropout(tag))
+ * and dbias = its column sums (fp32 [H], overwritten: that branch's bias
+ * gradient).  ws: delta_layernorm_bwd_workspace_floats. */
+delta_status delta_layernorm_bwd_drop(const void* dy, const void* x, const void* dres, void* dx,
+                                      const float* mean, const float* rstd, const float* gamma,
+                                      float* dgamma, float* dbeta, float* ws, int64_t rows,
+                                      int32_t H, void* dxd, float* dbias, float p,
+                                      const uint64_t* rng, uint32_t tag, void* stream);
 /* y = x * Phi(x) (erf GELU), n a multiple of 8 */
 delta_status delta_gelu_fwd(const void* x, void* y, int64_t n, void* stream);
 /* y = a + dropout(b) (n a multiple of 16) — AddResid */

@@ -147,12 +147,16 @@ def build_bert(cfg: BertConfig) -> G.Graph:
     for (pre, X_, ln1, qkv, att, proj, add1, ln2, up, ge, down, add2), l in zip(
             reversed(layers), reversed(range(cfg.layers))):
         g_out = d                                   # d add2
+        # the LayerNorm backward that produced g_out also applies the mask of
+        # add2's dropout and reduces the down projection's bias gradient
+        g_out.attrs.update(drop=drop_tag(l, 2), drop_lin=pre + "down")
         d_up = linear_bwd(pre + "down", g_out, ge, pre_act=up, drop=drop_tag(l, 2))
         # (its bias gradient comes from the gelu' GEMM's epilogue statistics)
         d_ln2 = linear_bwd(pre + "up", d_up, ln2, bias_done=True)
         d_add1 = g.add(pre + "ln2.bwd", "layernorm_bwd", (T, H), [d_ln2.id, add1.id, g_out.id],
                        phase="B", attrs=dict(ln=pre + "ln2", dres=2))
         d_add1.hbm_bytes = 5 * act(d_add1)
+        d_add1.attrs.update(drop=drop_tag(l, 1), drop_lin=pre + "out")
         d_att = linear_bwd(pre + "out", d_add1, att, drop=drop_tag(l, 1))
         d_qkv = g.add(pre + "attention.bwd", "attention_bwd", (T, 3 * H),
                       [d_att.id, qkv.id, att.id], phase="B",
@@ -419,19 +423,32 @@ class BertRuntime(DeltaRuntime):
         elif op == "layernorm_bwd":
             ln = node.attrs["ln"]
             dres = X.IN(node.attrs["dres"]) if "dres" in node.attrs else None
-            add(X.kop(X.K_LAYERNORM_BWD, (X.IN(0), X.IN(1), dres, X.OUT(), _ptr(pr.ln_mean[ln]),
-                                          _ptr(pr.ln_rstd[ln]), _ptr(pr.views["ln_g:" + ln]),
-                                          _ptr(pr.gviews["ln_g:" + ln]),
-                                          _ptr(pr.gviews["ln_b:" + ln]), _ptr(self.ln_ws)), (T, H)),
-                2)
+            refs = (X.IN(0), X.IN(1), dres, X.OUT(), _ptr(pr.ln_mean[ln]), _ptr(pr.ln_rstd[ln]),
+                    _ptr(pr.views["ln_g:" + ln]), _ptr(pr.gviews["ln_g:" + ln]),
+                    _ptr(pr.gviews["ln_b:" + ln]), _ptr(self.ln_ws))
+            if node.attrs.get("drop") is not None:
+                # + the gradient through the dropout of the residual branch
+                # into drop_ws (read by the very next node, that branch's
+                # linear_bwd) and the branch's bias gradient
+                add(X.kop(X.K_LAYERNORM_BWD_DROP,
+                          refs + (_ptr(self.drop_ws), _ptr(pr.gviews["b:" + node.attrs["drop_lin"]]),
+                                  rng),
+                          (T, H, node.attrs["drop"]), (cfg.p_hidden,)), 2)
+            else:
+                add(X.kop(X.K_LAYERNORM_BWD, refs, (T, H)), 2)
         elif op == "linear_bwd":
             lin = node.attrs["lin"]
             cin, cout = self.g.linears[lin]
             dy = X.IN(0)
+            fused_drop = False
             if node.attrs.get("drop") is not None:
-                # the residual branch's dropout, backward: its mask replayed
-                add(X.kop(X.K_DROPOUT_BWD, (X.IN(0), _ptr(self.drop_ws), rng),
-                          (T * cout, node.attrs["drop"]), (cfg.p_hidden,)))
+                # the residual branch's dropout, backward (its mask replayed):
+                # done by the LayerNorm backward that produced dy, with the
+                # bias gradient, when that node carries it
+                fused_drop = self.g.nodes[node.parents[0]].attrs.get("drop_lin") == lin
+                if not fused_drop:
+                    add(X.kop(X.K_DROPOUT_BWD, (X.IN(0), _ptr(self.drop_ws), rng),
+                              (T * cout, node.attrs["drop"]), (cfg.p_hidden,)))
                 dy = _ptr(self.drop_ws)
             dconv = self._lin_d[lin]._h
             if node.attrs.get("gelu"):
@@ -447,7 +464,7 @@ class BertRuntime(DeltaRuntime):
                 add(X.kop(X.K_CONV, (dy, X.OUT(), None), conv=dconv))
             add(X.kop(X.K_WGRAD, (dy, X.IN(1), _ptr(pr.gviews["w:" + lin]), _ptr(self.wg_ws)),
                       conv=self._lin_w[lin]._h), self._lin_w[lin].launches)
-            if not node.attrs.get("bias_done"):
+            if not node.attrs.get("bias_done") and not fused_drop:
                 add(X.kop(X.K_COLSUM, (dy, None, _ptr(pr.gviews["b:" + lin]), _ptr(self.cs_ws)),
                           (T, cout, 0, 0)), 2)
         elif op == "attention_bwd":

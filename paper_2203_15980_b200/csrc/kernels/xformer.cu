@@ -32,12 +32,14 @@
 #include "kernels/gelu.cuh"
 #include "kernels/launch.hpp"
 #include "kernels/philox.cuh"
+#include "kernels/sm100_common.cuh"
 #include "kernels/xformer.hpp"
 
 namespace delta_k {
 
 namespace {
 
+using namespace dsm100;
 using bf16 = __nv_bfloat16;
 
 __device__ __forceinline__ void unpack8(uint4 u, float* f) {
@@ -80,119 +82,268 @@ int sms() {
 
 // ---------------------------------------------------------------- LayerNorm
 // Row r = one warp; lane owns NV 16-byte chunks at columns (v*32 + lane)*8.
+// Warp w of block b takes rows b*8 + w + i*(8*gridDim), each arriving by a
+// bulk copy (TMA) LNF_ST rows ahead into the warp's shared-memory stages;
+// gamma / beta are staged once per block.
+constexpr int LNF_ST = 3;
+template <int NV>
+constexpr size_t ln_fwd_smem() {
+  return size_t(NV) * 256 * 8 + size_t(8) * LNF_ST * NV * 256 * 2;
+}
 template <int NV>
 __global__ void __launch_bounds__(256)
     k_layernorm_fwd(const bf16* __restrict__ x, bf16* __restrict__ y, float* __restrict__ mean,
                     float* __restrict__ rstd, const float* __restrict__ gamma,
                     const float* __restrict__ beta, int64_t rows, float eps) {
+  constexpr int H = NV * 256;
+  constexpr uint32_t RB = H * 2;
+  extern __shared__ __align__(128) uint8_t lnf_smem[];
+  __shared__ uint64_t bar[8][LNF_ST];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  float* sg = reinterpret_cast<float*>(lnf_smem);
+  float* sb = sg + H;
+  uint8_t* stage0 = lnf_smem + H * 8 + size_t(warp) * LNF_ST * RB;
+  if (lane == 0) {
+#pragma unroll
+    for (int s = 0; s < LNF_ST; ++s) mbar_init(&bar[warp][s], 1);
+    fence_mbar_init();
+  }
   pdl_wait();
   pdl_trigger();
-  constexpr int H = NV * 256;
-  const int lane = threadIdx.x & 31;
-  const int64_t r = int64_t(blockIdx.x) * 8 + (threadIdx.x >> 5);
-  if (r >= rows) return;
-  float v[NV][8];
-#pragma unroll
-  for (int k = 0; k < NV; ++k)
-    unpack8(__ldg(reinterpret_cast<const uint4*>(x + r * H) + k * 32 + lane), v[k]);
-  float s = 0.f;
-#pragma unroll
-  for (int k = 0; k < NV; ++k)
-#pragma unroll
-    for (int i = 0; i < 8; ++i) s += v[k][i];
-  const float mu = warp_sum(s) * (1.f / H);
-  float q = 0.f;
-#pragma unroll
-  for (int k = 0; k < NV; ++k)
-#pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      const float d = v[k][i] - mu;
-      q = fmaf(d, d, q);
-    }
-  const float rs = rsqrtf(warp_sum(q) * (1.f / H) + eps);
-#pragma unroll
-  for (int k = 0; k < NV; ++k) {
-    const int c = (k * 32 + lane) * 8;
-    const float4 g0 = __ldg(reinterpret_cast<const float4*>(gamma + c));
-    const float4 g1 = __ldg(reinterpret_cast<const float4*>(gamma + c + 4));
-    const float4 b0 = __ldg(reinterpret_cast<const float4*>(beta + c));
-    const float4 b1 = __ldg(reinterpret_cast<const float4*>(beta + c + 4));
-    const float g[8] = {g0.x, g0.y, g0.z, g0.w, g1.x, g1.y, g1.z, g1.w};
-    const float b[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
-    float o[8];
-#pragma unroll
-    for (int i = 0; i < 8; ++i) o[i] = fmaf((v[k][i] - mu) * rs, g[i], b[i]);
-    reinterpret_cast<uint4*>(y + r * H)[k * 32 + lane] = pack8(o);
+  for (int c = threadIdx.x; c < H; c += 256) {
+    sg[c] = __ldg(gamma + c);
+    sb[c] = __ldg(beta + c);
   }
-  if (lane == 0) {
-    mean[r] = mu;
-    rstd[r] = rs;
+  __syncthreads();
+  const int64_t stride = int64_t(gridDim.x) * 8;
+  const int64_t r0 = int64_t(blockIdx.x) * 8 + warp;
+  const int n = r0 < rows ? int((rows - r0 + stride - 1) / stride) : 0;
+  auto issue = [&](int it) {
+    uint64_t* b = &bar[warp][it % LNF_ST];
+    mbar_arrive_expect_tx(b, RB);
+    bulk_load(smem_u32(stage0 + size_t(it % LNF_ST) * RB), x + (r0 + it * stride) * H, RB, b);
+  };
+  if (lane == 0)
+    for (int it = 0; it < min(n, LNF_ST); ++it) issue(it);
+  for (int it = 0; it < n; ++it) {
+    const int64_t r = r0 + it * stride;
+    const int s = it % LNF_ST;
+    mbar_wait(&bar[warp][s], uint32_t(it / LNF_ST) & 1u);
+    const uint4* sx = reinterpret_cast<const uint4*>(stage0 + size_t(s) * RB);
+    float v[NV][8];
+#pragma unroll
+    for (int k = 0; k < NV; ++k) unpack8(sx[k * 32 + lane], v[k]);
+    __syncwarp();  // the row is in registers: refill its stage
+    if (lane == 0 && it + LNF_ST < n) issue(it + LNF_ST);
+    float sum = 0.f;
+#pragma unroll
+    for (int k = 0; k < NV; ++k)
+#pragma unroll
+      for (int i = 0; i < 8; ++i) sum += v[k][i];
+    const float mu = warp_sum(sum) * (1.f / H);
+    float q = 0.f;
+#pragma unroll
+    for (int k = 0; k < NV; ++k)
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const float d = v[k][i] - mu;
+        q = fmaf(d, d, q);
+      }
+    const float rs = rsqrtf(warp_sum(q) * (1.f / H) + eps);
+#pragma unroll
+    for (int k = 0; k < NV; ++k) {
+      const int c = (k * 32 + lane) * 8;
+      float g[8], b[8], o[8];
+      *reinterpret_cast<float4*>(g) = *reinterpret_cast<const float4*>(sg + c);
+      *reinterpret_cast<float4*>(g + 4) = *reinterpret_cast<const float4*>(sg + c + 4);
+      *reinterpret_cast<float4*>(b) = *reinterpret_cast<const float4*>(sb + c);
+      *reinterpret_cast<float4*>(b + 4) = *reinterpret_cast<const float4*>(sb + c + 4);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) o[i] = fmaf((v[k][i] - mu) * rs, g[i], b[i]);
+      reinterpret_cast<uint4*>(y + r * H)[k * 32 + lane] = pack8(o);
+    }
+    if (lane == 0) {
+      mean[r] = mu;
+      rstd[r] = rs;
+    }
   }
 }
 
-// dx = rstd * (g - mean(g) - xhat * mean(g * xhat)) + dres, g = dy * gamma;
-// block b owns rows [b*chunk, (b+1)*chunk), warps interleaved, and writes one
-// partial row pair (sum dy*xhat, sum dy) per column to ws[b][2][H].
+// The optional second output of the LayerNorm backward: the gradient that
+// flows on through the dropout of the residual branch feeding this
+// LayerNorm's input (dxd = mask * scale * bf16(dx), the same mask as
+// add_dropout(tag)), whose column sums are that branch's bias gradient.
+struct LnDrop {
+  bf16* dxd;
+  uint32_t thr;
+  float scale;
+  const uint64_t* rng;
+  uint32_t tag;
+};
+
+// dx = rstd * (g - mean(g) - xhat * mean(g * xhat)) + dres, g = dy * gamma.
+// Block b owns rows [b*chunk, (b+1)*chunk), one row per warp at a time (warps
+// interleaved).  The rows a warp reads (dy, x, dres: 2 KB each at H = 1024)
+// arrive by bulk copies (TMA) LN_ST rows ahead into the warp's own shared-
+// memory stages, so every warp keeps several rows of loads in flight without
+// holding them in registers; the two passes over a row (its statistics, then
+// dx) both read the staged row.  Each block writes one partial row per reduced
+// quantity (sum dy*xhat, sum dy[, sum dxd]) per column to ws[b][NQ][H].
+constexpr int LN_ST = 3;
 template <int NV>
-__global__ void __launch_bounds__(256)
+constexpr size_t ln_bwd_smem() {
+  return size_t(NV) * 256 * 4 + size_t(8) * LN_ST * 3 * NV * 256 * 2;
+}
+
+template <int NV, bool DROP>
+__global__ void __launch_bounds__(256, 1)
     k_layernorm_bwd(const bf16* __restrict__ dy, const bf16* __restrict__ x,
                     const bf16* __restrict__ dres, bf16* __restrict__ dx,
                     const float* __restrict__ mean, const float* __restrict__ rstd,
                     const float* __restrict__ gamma, float* __restrict__ ws, int64_t rows,
-                    int64_t chunk) {
+                    int64_t chunk, const LnDrop dr) {
+  constexpr int H = NV * 256;
+  constexpr uint32_t RB = H * 2;  // bytes per bf16 row
+  constexpr int NQ = DROP ? 3 : 2;
+  extern __shared__ __align__(128) uint8_t ln_smem[];
+  __shared__ float red[8][NQ][256];  // per warp, per chunk pass
+  __shared__ uint64_t bar[8][LN_ST];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  float* sgam = reinterpret_cast<float*>(ln_smem);
+  uint8_t* stage0 = ln_smem + H * 4 + size_t(warp) * LN_ST * 3 * RB;
+  if (lane == 0) {
+#pragma unroll
+    for (int s = 0; s < LN_ST; ++s) mbar_init(&bar[warp][s], 1);
+    fence_mbar_init();
+  }
   pdl_wait();
   pdl_trigger();
-  constexpr int H = NV * 256;
-  __shared__ float red[8][2][256];  // per warp, per chunk pass
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  float acc_g[NV][8], acc_b[NV][8];
+  for (int c = threadIdx.x; c < H; c += 256) sgam[c] = __ldg(gamma + c);
+  __syncthreads();
+
+  float acc_g[NV][8], acc_b[NV][8], acc_d[DROP ? NV : 1][8];
 #pragma unroll
   for (int k = 0; k < NV; ++k)
 #pragma unroll
     for (int i = 0; i < 8; ++i) acc_g[k][i] = acc_b[k][i] = 0.f;
-  float gm[NV][8];
 #pragma unroll
-  for (int k = 0; k < NV; ++k) {
-    const int c = (k * 32 + lane) * 8;
+  for (int k = 0; k < (DROP ? NV : 1); ++k)
 #pragma unroll
-    for (int i = 0; i < 8; ++i) gm[k][i] = __ldg(gamma + c + i);
-  }
-  const int64_t r0 = int64_t(blockIdx.x) * chunk;
-  const int64_t r1 = min(rows, r0 + chunk);
-  for (int64_t r = r0 + warp; r < r1; r += 8) {
-    float xv[NV][8], g[NV][8];
-    const float mu = __ldg(mean + r), rs = __ldg(rstd + r);
+    for (int i = 0; i < 8; ++i) acc_d[k][i] = 0.f;
+  uint64_t seed = 0, step = 0;
+  if (DROP) seed = dr.rng[0], step = dr.rng[1];
+
+  const int64_t rbeg = int64_t(blockIdx.x) * chunk + warp;
+  const int64_t rend = min(rows, int64_t(blockIdx.x + 1) * chunk);
+  const int n = rbeg < rend ? int((rend - rbeg + 7) / 8) : 0;
+  const uint32_t nbytes = (dres ? 3 : 2) * RB;
+  auto issue = [&](int it) {
+    const int s = it % LN_ST;
+    const int64_t r = rbeg + 8 * int64_t(it);
+    uint64_t* b = &bar[warp][s];
+    const uint32_t d = smem_u32(stage0 + size_t(s) * 3 * RB);
+    mbar_arrive_expect_tx(b, nbytes);
+    bulk_load(d, dy + r * H, RB, b);
+    bulk_load(d + RB, x + r * H, RB, b);
+    if (dres) bulk_load(d + 2 * RB, dres + r * H, RB, b);
+  };
+  if (lane == 0)
+    for (int it = 0; it < min(n, LN_ST); ++it) issue(it);
+
+  float mu_l = 0.f, rs_l = 0.f;  // lane j: mean / rstd of row it + j of the next 32
+  for (int it = 0; it < n; ++it) {
+    const int64_t r = rbeg + 8 * int64_t(it);
+    const int s = it % LN_ST;
+    if ((it & 31) == 0 && it + lane < n) {
+      mu_l = __ldg(mean + r + 8 * lane);
+      rs_l = __ldg(rstd + r + 8 * lane);
+    }
+    const float mu = __shfl_sync(0xFFFFFFFFu, mu_l, it & 31);
+    const float rs = __shfl_sync(0xFFFFFFFFu, rs_l, it & 31);
+    mbar_wait(&bar[warp][s], uint32_t(it / LN_ST) & 1u);
+    const uint4* sdy = reinterpret_cast<const uint4*>(stage0 + size_t(s) * 3 * RB);
+    const uint4* sx = sdy + RB / 16;
+    const uint4* sres = sdy + 2 * (RB / 16);
     float sg = 0.f, sgx = 0.f;
 #pragma unroll
     for (int k = 0; k < NV; ++k) {
-      float d[8];
-      unpack8(__ldg(reinterpret_cast<const uint4*>(dy + r * H) + k * 32 + lane), d);
-      unpack8(__ldg(reinterpret_cast<const uint4*>(x + r * H) + k * 32 + lane), xv[k]);
+      float d[8], xv[8], gm[8];
+      unpack8(sdy[k * 32 + lane], d);
+      unpack8(sx[k * 32 + lane], xv);
+      const float4* gp = reinterpret_cast<const float4*>(sgam + (k * 32 + lane) * 8);
+      *reinterpret_cast<float4*>(gm) = gp[0];
+      *reinterpret_cast<float4*>(gm + 4) = gp[1];
 #pragma unroll
       for (int i = 0; i < 8; ++i) {
-        xv[k][i] = (xv[k][i] - mu) * rs;  // xhat
-        g[k][i] = d[i] * gm[k][i];
-        sg += g[k][i];
-        sgx = fmaf(g[k][i], xv[k][i], sgx);
-        acc_g[k][i] = fmaf(d[i], xv[k][i], acc_g[k][i]);
+        const float xh = (xv[i] - mu) * rs;
+        const float g = d[i] * gm[i];
+        sg += g;
+        sgx = fmaf(g, xh, sgx);
+        acc_g[k][i] = fmaf(d[i], xh, acc_g[k][i]);
         acc_b[k][i] += d[i];
       }
     }
     const float a = warp_sum(sg) * (1.f / H);
     const float b = warp_sum(sgx) * (1.f / H);
+    // dropout keep bits of this lane's 8 columns per chunk k: element
+    // e = r*H + (k*32 + lane)*8 is in Philox block r*H/16 + k*16 + lane/2,
+    // half lane & 1.  Lanes 2m and 2m+1 share each block: each draws the
+    // block of one chunk of a chunk pair and they swap.
+    uint32_t keep[DROP ? NV : 1];
+    if (DROP) {
+      const uint64_t blk0 = uint64_t(r) * (H / 16) + uint64_t(lane >> 1);
+      const int odd = lane & 1;
+#pragma unroll
+      for (int k = 0; k + 1 < NV; k += 2) {
+        const uint32_t mine =
+            dr.thr ? keep16(drop_block(seed, step, dr.tag, blk0 + uint64_t(k + odd) * 16), dr.thr)
+                   : 0xFFFFu;
+        const uint32_t other = __shfl_xor_sync(0xFFFFFFFFu, mine, 1);
+        keep[DROP ? k : 0] = ((odd ? other : mine) >> (8 * odd)) & 0xFFu;
+        keep[DROP ? k + 1 : 0] = ((odd ? mine : other) >> (8 * odd)) & 0xFFu;
+      }
+      if (NV & 1) {
+        const uint32_t w =
+            dr.thr ? keep16(drop_block(seed, step, dr.tag, blk0 + uint64_t(NV - 1) * 16), dr.thr)
+                   : 0xFFFFu;
+        keep[DROP ? NV - 1 : 0] = (w >> (8 * odd)) & 0xFFu;
+      }
+    }
 #pragma unroll
     for (int k = 0; k < NV; ++k) {
-      float o[8], rr[8];
+      float d[8], xv[8], gm[8], rr[8], o[8];
+      unpack8(sdy[k * 32 + lane], d);
+      unpack8(sx[k * 32 + lane], xv);
+      const float4* gp = reinterpret_cast<const float4*>(sgam + (k * 32 + lane) * 8);
+      *reinterpret_cast<float4*>(gm) = gp[0];
+      *reinterpret_cast<float4*>(gm + 4) = gp[1];
       if (dres) {
-        unpack8(__ldg(reinterpret_cast<const uint4*>(dres + r * H) + k * 32 + lane), rr);
+        unpack8(sres[k * 32 + lane], rr);
       } else {
 #pragma unroll
         for (int i = 0; i < 8; ++i) rr[i] = 0.f;
       }
 #pragma unroll
-      for (int i = 0; i < 8; ++i) o[i] = fmaf(rs, g[k][i] - a - xv[k][i] * b, rr[i]);
-      reinterpret_cast<uint4*>(dx + r * H)[k * 32 + lane] = pack8(o);
+      for (int i = 0; i < 8; ++i) {
+        const float xh = (xv[i] - mu) * rs;
+        o[i] = fmaf(rs, d[i] * gm[i] - a - xh * b, rr[i]);
+      }
+      const uint4 packed = pack8(o);
+      reinterpret_cast<uint4*>(dx + r * H)[k * 32 + lane] = packed;
+      if (DROP) {
+        float q[8];
+        unpack8(packed, q);  // the stored (bf16) gradient, as a separate pass would read it
+#pragma unroll
+        for (int i = 0; i < 8; ++i) q[i] = (keep[DROP ? k : 0] >> i) & 1u ? q[i] * dr.scale : 0.f;
+        const uint4 pd = pack8(q);
+        reinterpret_cast<uint4*>(dr.dxd + r * H)[k * 32 + lane] = pd;
+        unpack8(pd, q);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) acc_d[DROP ? k : 0][i] += q[i];
+      }
     }
+    __syncwarp();  // every lane has read stage s: refill it
+    if (lane == 0 && it + LN_ST < n) issue(it + LN_ST);
   }
   // fixed-order reduction over the 8 warps, 256 columns at a time
 #pragma unroll
@@ -201,15 +352,16 @@ __global__ void __launch_bounds__(256)
     for (int i = 0; i < 8; ++i) {
       red[warp][0][lane * 8 + i] = acc_g[k][i];
       red[warp][1][lane * 8 + i] = acc_b[k][i];
+      if (DROP) red[warp][NQ - 1][lane * 8 + i] = acc_d[DROP ? k : 0][i];
     }
     __syncthreads();
-    for (int t = threadIdx.x; t < 512; t += 256) {
+    for (int t = threadIdx.x; t < NQ * 256; t += 256) {
       const int which = t >> 8, c = t & 255;
       float s = 0.f;
 #pragma unroll
       for (int w = 0; w < 8; ++w) s += red[w][which][c];
       // column (k*32 + c/8)*8 + c%8 of the row
-      ws[(int64_t(blockIdx.x) * 2 + which) * H + k * 256 + c] = s;
+      ws[(int64_t(blockIdx.x) * NQ + which) * H + k * 256 + c] = s;
     }
     __syncthreads();
   }
@@ -220,12 +372,13 @@ __global__ void __launch_bounds__(256)
 // rows), the 8 warp sums combined in warp order (deterministic)
 __global__ void __launch_bounds__(256)
     k_parts_merge(const float* __restrict__ ws, int parts, int64_t pstride, int cols,
-                  float* __restrict__ out, int accumulate, int64_t ws_y, float* __restrict__ out_y) {
+                  float* __restrict__ out, int accumulate, int64_t ws_y, float* __restrict__ out_y,
+                  float* __restrict__ out_z) {
   pdl_wait();
   pdl_trigger();
   if (blockIdx.y) {
-    ws += ws_y;
-    out = out_y;
+    ws += ws_y * blockIdx.y;
+    out = blockIdx.y == 1 ? out_y : out_z;
   }
   __shared__ float red[8][32];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -243,11 +396,13 @@ __global__ void __launch_bounds__(256)
   }
 }
 
-// out (and with out_y, a second merge: ws + ws_y -> out_y) in one launch
+// out (and with out_y, a second merge: ws + ws_y -> out_y; with out_z a third,
+// ws + 2 ws_y -> out_z) in one launch
 cudaError_t parts_merge(const float* ws, int parts, int64_t pstride, int cols, float* out,
-                        int accumulate, cudaStream_t st, int64_t ws_y = 0, float* out_y = nullptr) {
-  return launch_k(k_parts_merge, dim3((cols + 31) / 32, out_y ? 2 : 1), dim3(256), 0, st, ws, parts,
-                  pstride, cols, out, accumulate, ws_y, out_y);
+                        int accumulate, cudaStream_t st, int64_t ws_y = 0, float* out_y = nullptr,
+                        float* out_z = nullptr) {
+  return launch_k(k_parts_merge, dim3((cols + 31) / 32, out_z ? 3 : out_y ? 2 : 1), dim3(256), 0,
+                  st, ws, parts, pstride, cols, out, accumulate, ws_y, out_y, out_z);
 }
 
 // ---------------------------------------------------------------- GELU
@@ -688,13 +843,13 @@ cudaError_t merge_parts(const float* ws, int parts, int cols, float* out, cudaSt
 }
 
 // ================================================================ launchers
-#define DELTA_NV_SWITCH(H, CALL)      \
+#define DELTA_NV_SWITCH(H, ...)       \
   switch ((H) / 256) {                \
-    case 1: { constexpr int NV = 1; CALL; break; } \
-    case 2: { constexpr int NV = 2; CALL; break; } \
-    case 3: { constexpr int NV = 3; CALL; break; } \
-    case 4: { constexpr int NV = 4; CALL; break; } \
-    case 8: { constexpr int NV = 8; CALL; break; } \
+    case 1: { constexpr int NV = 1; __VA_ARGS__; break; } \
+    case 2: { constexpr int NV = 2; __VA_ARGS__; break; } \
+    case 3: { constexpr int NV = 3; __VA_ARGS__; break; } \
+    case 4: { constexpr int NV = 4; __VA_ARGS__; break; } \
+    case 8: { constexpr int NV = 8; __VA_ARGS__; break; } \
     default: return cudaErrorInvalidValue;        \
   }
 
@@ -703,33 +858,81 @@ bool xf_width_ok(int H) { return H % 256 == 0 && (H / 256 <= 4 || H / 256 == 8);
 cudaError_t layernorm_fwd(const void* x, void* y, float* mean, float* rstd, const float* gamma,
                           const float* beta, int64_t rows, int H, float eps, cudaStream_t st) {
   if (!xf_width_ok(H) || rows <= 0) return cudaErrorInvalidValue;
-  const dim3 grid(unsigned((rows + 7) / 8));
-  DELTA_NV_SWITCH(H, if (cudaError_t e = launch_k(k_layernorm_fwd<NV>, grid, dim3(256), 0, st,
-                                                  static_cast<const bf16*>(x), static_cast<bf16*>(y),
-                                                  mean, rstd, gamma, beta, rows, eps)) return e);
+  // two blocks per SM, each warp walking rows (ln_fwd_smem: 56 KB at H = 1024)
+  const dim3 grid(unsigned(std::min<int64_t>((rows + 7) / 8, 2 * int64_t(sms()))));
+  DELTA_NV_SWITCH(H, {
+    static bool attr = false;
+    if (!attr) {
+      if (cudaError_t e = cudaFuncSetAttribute(k_layernorm_fwd<NV>,
+                                               cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                               int(ln_fwd_smem<NV>())))
+        return e;
+      attr = true;
+    }
+    if (cudaError_t e = launch_k(k_layernorm_fwd<NV>, grid, dim3(256), ln_fwd_smem<NV>(), st,
+                                 static_cast<const bf16*>(x), static_cast<bf16*>(y), mean, rstd,
+                                 gamma, beta, rows, eps))
+      return e;
+  });
   return cudaGetLastError();
 }
 
+// one wave of one block per SM (the staged rows keep the loads in flight)
 int ln_bwd_parts(int64_t rows) {
-  return int(std::max<int64_t>(1, std::min<int64_t>((rows + 63) / 64, 2 * sms())));
+  return int(std::max<int64_t>(1, std::min<int64_t>((rows + 63) / 64, sms())));
+}
+template <int NV, bool DROP, typename... Args>
+cudaError_t ln_bwd_launch(int parts, cudaStream_t st, Args... args) {
+  static bool attr = false;
+  if (!attr) {
+    if (cudaError_t e = cudaFuncSetAttribute(k_layernorm_bwd<NV, DROP>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             int(ln_bwd_smem<NV>())))
+      return e;
+    attr = true;
+  }
+  return launch_k(k_layernorm_bwd<NV, DROP>, dim3(parts), dim3(256), ln_bwd_smem<NV>(), st,
+                  args...);
 }
 int64_t layernorm_bwd_workspace_floats(int64_t rows, int H) {
-  return int64_t(4 * sms()) * 2 * H;
+  return int64_t(4 * sms()) * 3 * H;
 }
 
 cudaError_t layernorm_bwd(const void* dy, const void* x, const void* dres, void* dx,
                           const float* mean, const float* rstd, const float* gamma, float* dgamma,
                           float* dbeta, float* ws, int64_t rows, int H, cudaStream_t st) {
+  return layernorm_bwd_drop(dy, x, dres, dx, mean, rstd, gamma, dgamma, dbeta, ws, rows, H,
+                            nullptr, nullptr, 0.f, nullptr, 0, st);
+}
+
+cudaError_t layernorm_bwd_drop(const void* dy, const void* x, const void* dres, void* dx,
+                               const float* mean, const float* rstd, const float* gamma,
+                               float* dgamma, float* dbeta, float* ws, int64_t rows, int H,
+                               void* dxd, float* dbias, float p, const uint64_t* rng, uint32_t tag,
+                               cudaStream_t st) {
   if (!xf_width_ok(H) || rows <= 0 || H / 256 > 4) return cudaErrorInvalidValue;
+  if (dxd && (!dbias || !rng)) return cudaErrorInvalidValue;
   const int parts = ln_bwd_parts(rows);
   const int64_t chunk = (rows + parts - 1) / parts;
-  DELTA_NV_SWITCH(H, if (cudaError_t e = launch_k(k_layernorm_bwd<NV>, dim3(parts), dim3(256), 0,
-                                                  st, static_cast<const bf16*>(dy),
-                                                  static_cast<const bf16*>(x),
-                                                  static_cast<const bf16*>(dres),
-                                                  static_cast<bf16*>(dx), mean, rstd, gamma, ws,
-                                                  rows, chunk)) return e);
-  if (cudaError_t e = parts_merge(ws, parts, 2 * int64_t(H), H, dgamma, 0, st, H, dbeta)) return e;
+  const DropParams dp = drop_params(p);
+  const LnDrop dr{static_cast<bf16*>(dxd), dp.thr, dp.scale, rng, tag};
+  const auto* dy_ = static_cast<const bf16*>(dy);
+  const auto* x_ = static_cast<const bf16*>(x);
+  const auto* dres_ = static_cast<const bf16*>(dres);
+  auto* dx_ = static_cast<bf16*>(dx);
+  if (dxd) {
+    DELTA_NV_SWITCH(H, if (cudaError_t e = ln_bwd_launch<NV, true>(parts, st, dy_, x_, dres_, dx_,
+                                                                   mean, rstd, gamma, ws, rows,
+                                                                   chunk, dr)) return e);
+    if (cudaError_t e = parts_merge(ws, parts, 3 * int64_t(H), H, dgamma, 0, st, H, dbeta, dbias))
+      return e;
+  } else {
+    DELTA_NV_SWITCH(H, if (cudaError_t e = ln_bwd_launch<NV, false>(parts, st, dy_, x_, dres_, dx_,
+                                                                    mean, rstd, gamma, ws, rows,
+                                                                    chunk, dr)) return e);
+    if (cudaError_t e = parts_merge(ws, parts, 2 * int64_t(H), H, dgamma, 0, st, H, dbeta))
+      return e;
+  }
   return cudaGetLastError();
 }
 

@@ -16,6 +16,14 @@ int64_t layernorm_bwd_workspace_floats(int64_t rows, int H);
 cudaError_t layernorm_bwd(const void* dy, const void* x, const void* dres, void* dx,
                           const float* mean, const float* rstd, const float* gamma, float* dgamma,
                           float* dbeta, float* ws, int64_t rows, int H, cudaStream_t st);
+// the same, and the gradient through the dropout(p, tag) of the residual
+// branch feeding this LayerNorm: dxd = mask * scale * dx (bf16), dbias = its
+// column sums (the branch's bias gradient, overwritten)
+cudaError_t layernorm_bwd_drop(const void* dy, const void* x, const void* dres, void* dx,
+                               const float* mean, const float* rstd, const float* gamma,
+                               float* dgamma, float* dbeta, float* ws, int64_t rows, int H,
+                               void* dxd, float* dbias, float p, const uint64_t* rng, uint32_t tag,
+                               cudaStream_t st);
 cudaError_t gelu_fwd(const void* x, void* y, int64_t n, cudaStream_t st);
 cudaError_t add_dropout(const void* a, const void* b, void* y, int64_t n, float p,
                         const uint64_t* rng, uint32_t tag, cudaStream_t st);

@@ -224,6 +224,13 @@ delta_status run_kop(delta_rt* rt, const delta_kop& k, Frame& fr, uint64_t node,
                                  rp<const float>(fr, r[6]), rp<float>(fr, r[7]), rp<float>(fr, r[8]),
                                  rp<float>(fr, r[9]), i[0], int(i[1]), st);
       break;
+    case DELTA_K_LAYERNORM_BWD_DROP:
+      e = delta_k::layernorm_bwd_drop(
+          ref(fr, r[0]), ref(fr, r[1]), ref(fr, r[2]), ref(fr, r[3]), rp<const float>(fr, r[4]),
+          rp<const float>(fr, r[5]), rp<const float>(fr, r[6]), rp<float>(fr, r[7]),
+          rp<float>(fr, r[8]), rp<float>(fr, r[9]), i[0], int(i[1]), ref(fr, r[10]),
+          rp<float>(fr, r[11]), k.f[0], rp<const uint64_t>(fr, r[12]), uint32_t(i[2]), st);
+      break;
     case DELTA_K_GELU:
       e = delta_k::gelu_fwd(ref(fr, r[0]), ref(fr, r[1]), i[0], st);
       break;

@@ -38,6 +38,15 @@ delta_status delta_layernorm_bwd(const void* dy, const void* x, const void* dres
                                     S(stream)),
              "layernorm_bwd");
 }
+delta_status delta_layernorm_bwd_drop(const void* dy, const void* x, const void* dres, void* dx,
+                                      const float* mean, const float* rstd, const float* gamma,
+                                      float* dgamma, float* dbeta, float* ws, int64_t rows,
+                                      int32_t H, void* dxd, float* dbias, float p,
+                                      const uint64_t* rng, uint32_t tag, void* stream) {
+  return st_(delta_k::layernorm_bwd_drop(dy, x, dres, dx, mean, rstd, gamma, dgamma, dbeta, ws, rows,
+                                         H, dxd, dbias, p, rng, tag, S(stream)),
+             "layernorm_bwd_drop");
+}
 delta_status delta_gelu_fwd(const void* x, void* y, int64_t n, void* stream) {
   return st_(delta_k::gelu_fwd(x, y, n, S(stream)), "gelu_fwd");
 }

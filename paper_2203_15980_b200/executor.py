@@ -23,7 +23,8 @@ REF_PTR, REF_OUT, REF_IN, REF_SCRATCH = 0, 1, 2, 3
  K_ADD_GRAD, K_MAXPOOL_FWD, K_MAXPOOL_BWD, K_AVGPOOL, K_SOFTMAX_XENT, K_HOST, K_WGRAD,
  K_XENT_HEAD) = range(1, 17)
 (K_LAYERNORM, K_LAYERNORM_BWD, K_GELU, K_ADD_DROPOUT, K_DROPOUT_BWD, K_COLSUM, K_EMBED,
- K_EMBED_GRADS, K_SPAN_HEAD, K_SPAN_HEAD_BWD, K_ATTN, K_ATTN_BWD, K_STATS_SUM) = range(17, 30)
+ K_EMBED_GRADS, K_SPAN_HEAD, K_SPAN_HEAD_BWD, K_ATTN, K_ATTN_BWD, K_STATS_SUM,
+ K_LAYERNORM_BWD_DROP) = range(17, 31)
 FIRST_ONLY, RECOMPUTE_ONLY, SIDE = 1, 2, 4
 
 
@@ -38,7 +39,7 @@ class DeltaRef(C.Structure):
 
 class DeltaKop(C.Structure):
     _fields_ = [("kind", u32), ("flags", u32), ("conv", vp), ("i", i64 * 4), ("f", f32 * 2),
-                ("pad", u32), ("r", DeltaRef * 11)]
+                ("pad", u32), ("r", DeltaRef * 14)]
 
 
 class DeltaRecipe(C.Structure):

@@ -370,6 +370,7 @@ _XSIGS = {
     "delta_layernorm_fwd": (i32, [vp, vp, vp, vp, vp, vp, i64, i32, f32, vp]),
     "delta_layernorm_bwd_workspace_floats": (i64, [i64, i32]),
     "delta_layernorm_bwd": (i32, [vp] * 10 + [i64, i32, vp]),
+    "delta_layernorm_bwd_drop": (i32, [vp] * 10 + [i64, i32, vp, vp, f32, vp, u32, vp]),
     "delta_gelu_fwd": (i32, [vp, vp, i64, vp]),
     "delta_add_dropout": (i32, [vp, vp, vp, i64, f32, vp, u32, vp]),
     "delta_dropout_bwd": (i32, [vp, vp, i64, f32, vp, u32, vp]),
@@ -402,6 +403,14 @@ def layernorm_bwd_workspace_floats(rows, H) -> int:
 def layernorm_bwd(dy, x, dres, dx, mean, rstd, gamma, dgamma, dbeta, ws, rows, H, stream):
     check(lib.delta_layernorm_bwd(dy, x, dres, dx, mean, rstd, gamma, dgamma, dbeta, ws, rows, H,
                                   stream))
+    _count(2)
+
+
+def layernorm_bwd_drop(dy, x, dres, dx, mean, rstd, gamma, dgamma, dbeta, ws, rows, H, dxd, dbias,
+                       p, rng, tag, stream):
+    """layernorm_bwd + dxd = dropout_bwd(dx; p, tag), dbias = colsum(dxd)"""
+    check(lib.delta_layernorm_bwd_drop(dy, x, dres, dx, mean, rstd, gamma, dgamma, dbeta, ws, rows,
+                                       H, dxd, dbias, p, rng, tag, stream))
     _count(2)
 
 

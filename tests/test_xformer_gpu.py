@@ -77,6 +77,21 @@ def test_layernorm_fwd_bwd(H):
                     rstd.data_ptr(), gamma.data_ptr(), dg2.data_ptr(), db.data_ptr(), ws.data_ptr(),
                     rows, H, _st())
     assert torch.equal(dx, dx2) and torch.equal(dg, dg2)
+    # fused with the residual branch's dropout backward and its bias gradient:
+    # dx, dgamma, dbeta unchanged; dxd == dropout_bwd(dx) bit for bit; dbias ==
+    # the column sums of dxd
+    for p in (0.1, 0.0):
+        rng = _rng()
+        dx3, dxd, dxd_ref = (torch.empty_like(x) for _ in range(3))
+        dg3, db3, dbias = (torch.empty(H, device=dev) for _ in range(3))
+        K.layernorm_bwd_drop(dy.data_ptr(), x.data_ptr(), dres.data_ptr(), dx3.data_ptr(),
+                             mean.data_ptr(), rstd.data_ptr(), gamma.data_ptr(), dg3.data_ptr(),
+                             db3.data_ptr(), ws.data_ptr(), rows, H, dxd.data_ptr(),
+                             dbias.data_ptr(), p, rng.data_ptr(), 7, _st())
+        assert torch.equal(dx3, dx) and torch.equal(dg3, dg) and torch.equal(db3, db)
+        K.dropout_bwd(dx.data_ptr(), dxd_ref.data_ptr(), rows * H, p, rng.data_ptr(), 7, _st())
+        assert torch.equal(dxd, dxd_ref)
+        close(dbias, dxd_ref.double().sum(0).float(), 1e-4, 1e-4)
 
 
 def test_gelu_fwd():
