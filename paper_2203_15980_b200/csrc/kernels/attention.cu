@@ -7,14 +7,16 @@
 // of a (sequence, head) stay on chip, so there is no online-softmax
 // rescaling and no atomics anywhere (deterministic gradients).
 //
-// forward (grid S/128 x heads x B, one CTA per 128 query rows): S = Q K^T for
-//   all S keys in TMEM (S <= 512 fp32 columns = the SM's whole TMEM); 16
-//   softmax warps (four per TMEM lane quarter, a quarter of the keys each)
-//   take the row max, then write P = exp2(s*c - m*c) * keep (bf16,
-//   unnormalised) to shared memory in the K-major SW128 layout the tensor core
-//   reads, while K's buffer is refilled with V; O = P V (V as an MN-major B
-//   operand) lands in TMEM columns 0-63 and is scaled by
-//   dropout_scale / rowsum on the way out.  lse (log2 units) saved.
+// forward (grid S/256 x heads x B, two 128-row query tiles per CTA, K and V
+//   of the sequence resident): per tile and 128-key chunk j, S_j = Q K_j^T in
+//   TMEM (128 columns per tile); 8 softmax warps per tile (two per TMEM lane
+//   quarter, 64 keys each).  Pass 1 takes the row max over all chunks, pass 2
+//   recomputes S_j (the tensor cores have the capacity) and writes
+//   P = exp2(s*c - m*c) * keep (bf16, unnormalised) to shared memory in the
+//   K-major SW128 layout, O += P V_j (V as an MN-major B operand) accumulating
+//   in TMEM; O is scaled by dropout_scale / rowsum on the way out, lse (log2
+//   units) saved.  One MMA warp alternates between the tiles, so each tile's
+//   MMAs run under the other's softmax.
 // backward (grid heads x B, one CTA per (sequence, head)): for every key
 //   block j (128 keys, K_j / V_j loaded by TMA) and query block i
 //   (Q, dO of the whole sequence resident): S_ij = Q_i K_j^T and
@@ -99,10 +101,7 @@ __device__ __forceinline__ void tmem_wait() {
 __device__ __forceinline__ uint4 keep_bytes(uint64_t seed, uint64_t step, uint32_t tag, uint64_t g,
                                             uint32_t thr) {
   if (!thr) return make_uint4(~0u, ~0u, ~0u, ~0u);
-  const uint4 w = drop_block(seed, step, tag, g);
-  const uint32_t t4 = thr * 0x01010101u;
-  return make_uint4(__vcmpgeu4(w.x, t4), __vcmpgeu4(w.y, t4), __vcmpgeu4(w.z, t4),
-                    __vcmpgeu4(w.w, t4));
+  return keep_mask_bytes(drop_block(seed, step, tag, g), thr);
 }
 // 16-bit lane masks of elements (2j, 2j+1) of a 4-byte keep word
 __device__ __forceinline__ uint32_t pair_mask(uint32_t kb, int j) {
@@ -184,177 +183,218 @@ struct AttnArgs {
 };
 
 // ======================================================================= fwd
-__global__ void __launch_bounds__(kThreads, 1)
-    k_attn_fwd(const __grid_constant__ CUtensorMap qkv_map, const AttnArgs a) {
+// Two query tiles per CTA (grid ceil(S/256) x heads x B), K and V of the
+// (sequence, head) resident in shared memory, 8 softmax warps per tile (two
+// per TMEM lane quarter, 64 keys of a 128-key chunk each).  TMEM: S of each
+// tile's current key chunk (128 columns each) and the two O accumulators.
+// The scores are computed twice (S_j = Q K_j^T per chunk, twice): pass 1
+// takes the row max, pass 2 forms P = exp2(s*c - m*c) * keep into shared
+// memory and accumulates O += P V_j — the tensor cores have the capacity, and
+// no online rescaling is needed.  The one MMA warp alternates between the two
+// tiles, so one tile's MMAs run under the other tile's softmax, and the
+// prologue / epilogue of the CTA is shared by two tiles.
+constexpr int F2_SW = 8;                       // softmax warps per query tile
+constexpr int F2_CTRL = 2 * F2_SW;             // TMA + MMA warp
+constexpr int kThreadsF2 = (F2_CTRL + 1) * 32;
+
+__device__ __forceinline__ void bar_tile(int t) {
+  asm volatile("bar.sync %0, %1;" ::"r"(2 + t), "n"(F2_SW * 32) : "memory");
+}
+
+__global__ void __launch_bounds__(kThreadsF2, 1)
+    k_attn_fwd2(const __grid_constant__ CUtensorMap qkv_map, const AttnArgs a) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = align1024(smem_raw);
-  const int S = a.S;
-  const uint32_t sQ = smem_u32(smem);
-  const uint32_t sKV = sQ + TILE_BYTES;
-  const uint32_t sP = sKV + uint32_t(S) * 128;
-  float* red = reinterpret_cast<float*>(smem + TILE_BYTES + size_t(S) * 128 + size_t(S) * 256);
-  uint64_t* bars = reinterpret_cast<uint64_t*>(red + 8 * TILE);
-  uint64_t* bar_qk = bars;
-  uint64_t* bar_v = bars + 1;
-  uint64_t* bar_s = bars + 2;
-  uint64_t* bar_p = bars + 3;
-  uint64_t* bar_o = bars + 4;
-  uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 5);
+  const int S = a.S, nt = S / TILE;
+  const uint32_t sQ = smem_u32(smem);               // [2 tiles][128][64]
+  const uint32_t sK = sQ + 2 * TILE_BYTES;          // [nt][128 keys][64]
+  const uint32_t sV = sK + uint32_t(nt) * TILE_BYTES;
+  const uint32_t sP = sV + uint32_t(nt) * TILE_BYTES;  // [2 tiles][2 atoms][128][64 keys]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + (sP - sQ) + 4 * TILE_BYTES);
+  uint64_t* bar_qk = bars;       // Q tiles and K landed
+  uint64_t* bar_v = bars + 1;    // V landed
+  uint64_t* bar_s = bars + 2;    // [2] S of a tile computed
+  uint64_t* bar_t = bars + 4;    // [2] S of a tile read out of TMEM
+  uint64_t* bar_p = bars + 6;    // [2] P of a tile written
+  uint64_t* bar_o = bars + 8;    // [2] a tile's PV MMAs done
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 10);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int qt = blockIdx.x, h = blockIdx.y, b = blockIdx.z;
-  const uint32_t tcols = S <= 128 ? 128 : (S <= 256 ? 256 : 512);
+  const int qp = blockIdx.x, h = blockIdx.y, b = blockIdx.z;
+  const int ntile = min(2, nt - 2 * qp);
 
   if (threadIdx.x == 0) {
     mbar_init(bar_qk, 1);
     mbar_init(bar_v, 1);
-    mbar_init(bar_s, 1);
-    mbar_init(bar_p, MATH_W);
-    mbar_init(bar_o, 1);
+    for (int t = 0; t < 2; ++t) {
+      mbar_init(bar_s + t, 1);
+      mbar_init(bar_t + t, F2_SW);
+      mbar_init(bar_p + t, F2_SW);
+      mbar_init(bar_o + t, 1);
+    }
     fence_mbar_init();
     tma_prefetch_desc(&qkv_map);
   }
-  if (threadIdx.x == 0) dbg_mark(20, 0xF1);
-  if (warp == CTRL) tmem_alloc(tslot, tcols);
-  if (threadIdx.x == CTRL * 32) dbg_mark(21, 0xF2);
+  if (warp == F2_CTRL) tmem_alloc(tslot, 512);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tslot;
   pdl_wait();
   pdl_trigger();
-  const int row0 = b * S;  // first token of the sequence
+  const int row0 = b * S;
+  const int nk = 2 * nt;  // S steps: nt of pass 1 (max), nt of pass 2 (P, O)
 
-  if (warp == CTRL) {
+  if (warp == F2_CTRL) {
     if (lane == 0) {
-      mbar_arrive_expect_tx(bar_qk, TILE_BYTES + uint32_t(S) * 128);
-      tma_load_2d(sQ, &qkv_map, bar_qk, h * HD, row0 + qt * TILE);
-      for (int i = 0; i < S / TILE; ++i)
-        tma_load_2d(sKV + i * TILE_BYTES, &qkv_map, bar_qk, a.Hd + h * HD, row0 + i * TILE);
+      mbar_arrive_expect_tx(bar_qk, uint32_t(ntile + nt) * TILE_BYTES);
+      for (int t = 0; t < ntile; ++t)
+        tma_load_2d(sQ + t * TILE_BYTES, &qkv_map, bar_qk, h * HD, row0 + (2 * qp + t) * TILE);
+      for (int j = 0; j < nt; ++j)
+        tma_load_2d(sK + j * TILE_BYTES, &qkv_map, bar_qk, a.Hd + h * HD, row0 + j * TILE);
+      mbar_arrive_expect_tx(bar_v, uint32_t(nt) * TILE_BYTES);
+      for (int j = 0; j < nt; ++j)
+        tma_load_2d(sV + j * TILE_BYTES, &qkv_map, bar_v, 2 * a.Hd + h * HD, row0 + j * TILE);
     }
+    constexpr uint32_t idS = umma_idesc_bf16(128, 128);
+    constexpr uint32_t idO = umma_idesc_bf16(128, HD) | (1u << 16);  // B (V) MN-major
+    auto issue_s = [&](int t, int k) {
+      if (elect_one()) {
+        const uint64_t dq = umma_desc_sw128(sQ + t * TILE_BYTES);
+        const uint64_t dk = umma_desc_sw128(sK + (k % nt) * TILE_BYTES);
+#pragma unroll
+        for (int kk = 0; kk < HD / 16; ++kk)
+          umma_bf16(tmem + t * TILE, dq + uint64_t(kk * 2), dk + uint64_t(kk * 2), idS, kk > 0);
+        umma_commit(bar_s + t);
+      }
+      __syncwarp();
+    };
     mbar_wait(bar_qk, 0);
     tc_fence_after();
-    constexpr uint32_t idS = umma_idesc_bf16(128, 128);
-    if (elect_one()) {
-      const uint64_t dq = umma_desc_sw128(sQ);
-      for (int nb = 0; nb < S / TILE; ++nb) {
-        const uint64_t dk = umma_desc_sw128(sKV + nb * TILE_BYTES);
-#pragma unroll
-        for (int k = 0; k < HD / 16; ++k)
-          umma_bf16(tmem + nb * TILE, dq + uint64_t(k * 2), dk + uint64_t(k * 2), idS, k > 0);
+    for (int t = 0; t < ntile; ++t) issue_s(t, 0);
+    for (int k = 0; k < nk; ++k) {
+      for (int t = 0; t < ntile; ++t) {
+        mbar_wait(bar_t + t, k & 1);
+        tc_fence_after();
+        if (k + 1 < nk) issue_s(t, k + 1);
       }
-      umma_commit(bar_s);
-    }
-    __syncwarp();
-    // K consumed: refill the buffer with V while the softmax runs
-    mbar_wait(bar_s, 0);
-    if (lane == 0) {
-      mbar_arrive_expect_tx(bar_v, uint32_t(S) * 128);
-      for (int i = 0; i < S / TILE; ++i)
-        tma_load_2d(sKV + i * TILE_BYTES, &qkv_map, bar_v, 2 * a.Hd + h * HD, row0 + i * TILE);
-    }
-    mbar_wait(bar_v, 0);
-    mbar_wait(bar_p, 0);
-    tc_fence_after();
-    constexpr uint32_t idO = umma_idesc_bf16(128, HD) | (1u << 16);  // B (V) MN-major
-    if (elect_one()) {
-      for (int j = 0; j < S / 64; ++j) {
-        const uint64_t dp = umma_desc_sw128(sP + j * TILE_BYTES);
+      if (k >= nt) {
+        const int j = k - nt;
+        if (j == 0) mbar_wait(bar_v, 0);
+        for (int t = 0; t < ntile; ++t) {
+          mbar_wait(bar_p + t, j & 1);
+          tc_fence_after();
+          if (elect_one()) {
+            const uint32_t p0 = sP + t * 2 * TILE_BYTES;
 #pragma unroll
-        for (int k = 0; k < 4; ++k)
-          umma_bf16(tmem, dp + uint64_t(k * 2), desc_mn(sKV + uint32_t(j * 64 + k * 16) * 128, 0),
-                    idO, (j | k) != 0);
-      }
-      umma_commit(bar_o);
-    }
-    __syncwarp();
-  } else {
-    // ---- softmax warps: row r of the tile, keys [part*S/4, (part+1)*S/4) ----
-    const int quarter = warp & 3, part = warp >> 2;
-    const int r = quarter * 32 + lane;
-    const int q = qt * TILE + r;
-    const uint32_t trow = tmem + (uint32_t(quarter * 32) << 16);
-    const int ps = S / 4, nch = ps / 16;  // 16-column chunks of this warp (<= 8)
-    const int c0 = part * ps;
-    // the dropout keep bits of this row's keys do not depend on S: draw them
-    // while the Q/K loads and the S MMA are in flight (16 bits per chunk)
-    const uint64_t seed = a.rng[0], step = a.rng[1];
-    const uint64_t g0 = ((uint64_t(b * a.heads + h) * S + q) * uint64_t(S) + c0) >> 4;
-    uint32_t kbits[8];
+            for (int at = 0; at < 2; ++at) {
+              const uint64_t dp = umma_desc_sw128(p0 + at * TILE_BYTES);
 #pragma unroll
-    for (int c = 0; c < 8; ++c)
-      kbits[c] = (c < nch && a.thr) ? keep16(drop_block(seed, step, a.tag, g0 + c), a.thr) : 0xFFFFu;
-    mbar_wait(bar_s, 0);
-    tc_fence_after();
-    float m = -INFINITY;
-    {
-      uint32_t v0[16], v1[16], v2[16], v3[16];
-      for (int c = 0; c < nch; c += 4) {
-        tmem_ld16(trow + c0 + c * 16, v0);
-        tmem_ld16(trow + c0 + c * 16 + 16, v1);
-        if (c + 2 < nch) {
-          tmem_ld16(trow + c0 + c * 16 + 32, v2);
-          tmem_ld16(trow + c0 + c * 16 + 48, v3);
-        }
-        tmem_wait();
-#pragma unroll
-        for (int i = 0; i < 16; ++i) m = fmaxf(m, fmaxf(__uint_as_float(v0[i]), __uint_as_float(v1[i])));
-        if (c + 2 < nch) {
-#pragma unroll
-          for (int i = 0; i < 16; ++i)
-            m = fmaxf(m, fmaxf(__uint_as_float(v2[i]), __uint_as_float(v3[i])));
-        }
-      }
-    }
-    red[part * TILE + r] = m;
-    bar_math();
-    m = fmaxf(fmaxf(red[r], red[TILE + r]), fmaxf(red[2 * TILE + r], red[3 * TILE + r]));
-    const float mc = m * kCl2;
-    float l = 0.f;
-#pragma unroll
-    for (int c = 0; c < 8; c += 2) {
-      if (c < nch) {
-        uint32_t v[2][16];
-        tmem_ld16(trow + c0 + c * 16, v[0]);
-        tmem_ld16(trow + c0 + c * 16 + 16, v[1]);
-        tmem_wait();
-#pragma unroll
-        for (int hh = 0; hh < 2; ++hh) {
-          const uint32_t bits = kbits[c + hh];
-          uint32_t w[8];
-#pragma unroll
-          for (int i = 0; i < 16; i += 2) {
-            const float p0 = ex2(fmaf(__uint_as_float(v[hh][i]), kCl2, -mc));
-            const float p1 = ex2(fmaf(__uint_as_float(v[hh][i + 1]), kCl2, -mc));
-            l += p0 + p1;
-            const uint32_t mk = ((0u - ((bits >> i) & 1u)) & 0xFFFFu) |
-                                ((0u - ((bits >> (i + 1)) & 1u)) << 16);
-            w[i >> 1] = pack_bf16x2(p0, p1) & mk;
+              for (int kk = 0; kk < 4; ++kk)
+                umma_bf16(tmem + 256 + t * HD, dp + uint64_t(kk * 2),
+                          desc_mn(sV + j * TILE_BYTES + uint32_t(at * 64 + kk * 16) * 128, 0), idO,
+                          (j | at | kk) != 0);
+            }
+            umma_commit(bar_o + t);
           }
-          st_row16(sP, r, c0 + (c + hh) * 16, w);
+          __syncwarp();
         }
       }
     }
-    red[4 * TILE + part * TILE + r] = l;
-    fence_proxy_async_smem();
-    tc_fence_before();
-    bar_math();
-    l = (red[4 * TILE + r] + red[5 * TILE + r]) + (red[6 * TILE + r] + red[7 * TILE + r]);
-    if (part == 0) a.lse[uint64_t(b * a.heads + h) * S + q] = mc + __log2f(l);
-    __syncwarp();
-    if (lane == 0) mbar_arrive(bar_p);
+  } else if (warp / F2_SW < ntile) {
+    const int t = warp / F2_SW, w = warp % F2_SW;
+    const int quarter = w & 3, half = w >> 2;
+    const int r = quarter * 32 + lane;
+    const int q = (2 * qp + t) * TILE + r;
+    const uint32_t trow = tmem + (uint32_t(quarter * 32) << 16);
+    const uint32_t tS = trow + t * TILE + half * 64;
+    const uint64_t seed = a.rng[0], step = a.rng[1];
+    const uint64_t bh = uint64_t(b * a.heads + h);
+    // Philox block of keys [j*128 + half*64 + c*16, +16) of row q
+    const uint64_t g0 = ((bh * S + q) * uint64_t(S) + half * 64) >> 4;
+    // ---- pass 1: row max
+    float m = -INFINITY;
+#pragma unroll 1
+    for (int j = 0; j < nt; ++j) {
+      mbar_wait(bar_s + t, j & 1);
+      tc_fence_after();
+      uint32_t v[4][16];
+#pragma unroll
+      for (int c = 0; c < 4; ++c) tmem_ld16(tS + c * 16, v[c]);
+      tmem_wait();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(bar_t + t);
+#pragma unroll
+      for (int c = 0; c < 4; ++c)
+#pragma unroll
+        for (int i = 0; i < 16; ++i) m = fmaxf(m, __uint_as_float(v[c][i]));
+    }
+    // the two half-warps of a row combine their maxima (P's buffer is free)
+    float* red = reinterpret_cast<float*>(smem + (sP - sQ) + t * 2 * TILE_BYTES);
+    red[half * TILE + r] = m;
+    bar_tile(t);
+    m = fmaxf(red[r], red[TILE + r]);
+    bar_tile(t);
+    const float mc = m * kCl2;
+    const uint32_t pT = sP + t * 2 * TILE_BYTES;
+    // ---- pass 2: P = exp2(s*c - m*c) * keep into shared memory, O += P V_j
+    float l = 0.f;
+#pragma unroll 1
+    for (int j = 0; j < nt; ++j) {
+      mbar_wait(bar_s + t, (nt + j) & 1);
+      tc_fence_after();
+      uint32_t v[4][16];
+#pragma unroll
+      for (int c = 0; c < 4; ++c) tmem_ld16(tS + c * 16, v[c]);
+      tmem_wait();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(bar_t + t);
+      uint32_t wv[4][8];
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        // keep bytes of these 16 keys (0xFF = kept): a pair's bf16x2 mask is
+        // one byte permute
+        const uint4 kb = keep_bytes(seed, step, a.tag, g0 + j * 8 + c, a.thr);
+#pragma unroll
+        for (int i = 0; i < 16; i += 2) {
+          const float p0 = ex2(fmaf(__uint_as_float(v[c][i]), kCl2, -mc));
+          const float p1 = ex2(fmaf(__uint_as_float(v[c][i + 1]), kCl2, -mc));
+          l += p0 + p1;
+          wv[c][i >> 1] = pack_bf16x2(p0, p1) & pair_mask((&kb.x)[i >> 2], (i >> 1) & 1);
+        }
+      }
+      // the previous chunk's PV MMAs have read P
+      if (j > 0) mbar_wait(bar_o + t, (j - 1) & 1);
+#pragma unroll
+      for (int c = 0; c < 4; ++c) st_row16(pT, r, half * 64 + c * 16, wv[c]);
+      fence_proxy_async_smem();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(bar_p + t);
+    }
+    // row sum: the tile's Q buffer is free (its last S MMA has completed)
+    float* red2 = reinterpret_cast<float*>(smem + t * TILE_BYTES);
+    red2[half * TILE + r] = l;
+    bar_tile(t);
+    l = red2[r] + red2[TILE + r];
+    if (half == 0) a.lse[bh * S + q] = mc + __log2f(l);
     const float inv = a.dscale / l;
-    // ---- epilogue: O columns [part*16, part*16+16) of row r ----
-    mbar_wait(bar_o, 0);
+    // ---- epilogue: O columns [half*32, half*32 + 32) of row r
+    mbar_wait(bar_o + t, (nt - 1) & 1);
     tc_fence_after();
-    uint32_t v[16];
-    tmem_ld16(trow + part * 16, v);
+    uint32_t o0[16], o1[16];
+    tmem_ld16(trow + 256 + t * HD + half * 32, o0);
+    tmem_ld16(trow + 256 + t * HD + half * 32 + 16, o1);
     tmem_wait();
-    store16(a.out + (int64_t(row0) + q) * a.Hd + h * HD + part * 16, v, inv);
+    bf16* dst = a.out + (int64_t(row0) + q) * a.Hd + h * HD + half * 32;
+    store16(dst, o0, inv);
+    store16(dst + 16, o1, inv);
   }
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  if (warp == CTRL) tmem_dealloc(tmem, tcols);
+  if (warp == F2_CTRL) tmem_dealloc(tmem, 512);
 }
 
 // ======================================================================= bwd
@@ -649,14 +689,16 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == CTRL) tmem_dealloc(tmem, 512);
 }
 
-size_t fwd_smem(int S) {
-  return 1024 + TILE_BYTES + size_t(S) * 128 + size_t(S) * 256 + 8 * TILE * 4 + 64;
-}
 size_t bwd_smem(int S) { return 1024 + 2 * size_t(S) * 128 + 6 * TILE_BYTES + 128; }  // 10 words
 
 bool shape_ok(int S, int heads) { return S > 0 && S % TILE == 0 && S <= 512 && heads > 0; }
 
 }  // namespace
+
+// Q (2 tiles) + P (2 tiles x 2 atoms) + K + V + barriers
+static size_t fwd2_smem(int S) {
+  return 1024 + 6 * size_t(TILE_BYTES) + 2 * size_t(S) * 128 + 128;
+}
 
 cudaError_t attention_fwd(const void* qkv, void* out, float* lse, int B, int S, int heads,
                           float p, const uint64_t* rng, uint32_t tag, cudaStream_t st) {
@@ -670,13 +712,14 @@ cudaError_t attention_fwd(const void* qkv, void* out, float* lse, int B, int S, 
   AttnArgs a{B, S, heads, Hd, static_cast<bf16*>(out), lse, nullptr, dp.thr, dp.scale, rng, tag};
   static bool attr = false;
   if (!attr) {
-    if (cudaError_t e = cudaFuncSetAttribute(k_attn_fwd, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             int(fwd_smem(512))))
+    if (cudaError_t e = cudaFuncSetAttribute(k_attn_fwd2, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             int(fwd2_smem(512))))
       return e;
     attr = true;
   }
-  if (cudaError_t e = launch_k(k_attn_fwd, dim3(S / TILE, heads, B), dim3(kThreads), fwd_smem(S),
-                               st, qm, a))
+  const int nt = S / TILE;
+  if (cudaError_t e = launch_k(k_attn_fwd2, dim3((nt + 1) / 2, heads, B), dim3(kThreadsF2),
+                               fwd2_smem(S), st, qm, a))
     return e;
   return cudaGetLastError();
 }

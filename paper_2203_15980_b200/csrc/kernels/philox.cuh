@@ -56,4 +56,16 @@ __device__ __forceinline__ uint32_t keep16(uint4 b, uint32_t thr) {
          (keep4(b.w, thr) << 12);
 }
 
+// the same decisions as 16 byte masks (byte i of word w = 0xFF iff element
+// 4w + i is kept): SIMD byte compares, no per-element bit extraction
+__device__ __forceinline__ uint4 keep_mask_bytes(uint4 b, uint32_t thr) {
+  const uint32_t t4 = thr * 0x01010101u;
+  return make_uint4(__vcmpgeu4(b.x, t4), __vcmpgeu4(b.y, t4), __vcmpgeu4(b.z, t4),
+                    __vcmpgeu4(b.w, t4));
+}
+// fp32 all-ones / zero mask of byte i of a keep-mask word
+__device__ __forceinline__ uint32_t keep_mask_elem(uint32_t kb, int i) {
+  return __byte_perm(kb, 0, 0x1111u * uint32_t(i));
+}
+
 }  // namespace delta_k

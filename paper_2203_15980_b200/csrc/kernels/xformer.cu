@@ -289,24 +289,35 @@ __global__ void __launch_bounds__(256, 1)
     // e = r*H + (k*32 + lane)*8 is in Philox block r*H/16 + k*16 + lane/2,
     // half lane & 1.  Lanes 2m and 2m+1 share each block: each draws the
     // block of one chunk of a chunk pair and they swap.
-    uint32_t keep[DROP ? NV : 1];
+    // dropout keep masks of this lane's 8 columns per chunk k (2 words of byte
+    // masks): element e = r*H + (k*32 + lane)*8 is in Philox block
+    // r*H/16 + k*16 + lane/2, half lane & 1.  Lanes 2m and 2m+1 share each
+    // block: each draws the block of one chunk of a chunk pair and they swap
+    // the halves the other needs.
+    uint2 keep[DROP ? NV : 1];
     if (DROP) {
       const uint64_t blk0 = uint64_t(r) * (H / 16) + uint64_t(lane >> 1);
       const int odd = lane & 1;
+      const uint4 all = make_uint4(~0u, ~0u, ~0u, ~0u);
 #pragma unroll
       for (int k = 0; k + 1 < NV; k += 2) {
-        const uint32_t mine =
-            dr.thr ? keep16(drop_block(seed, step, dr.tag, blk0 + uint64_t(k + odd) * 16), dr.thr)
-                   : 0xFFFFu;
-        const uint32_t other = __shfl_xor_sync(0xFFFFFFFFu, mine, 1);
-        keep[DROP ? k : 0] = ((odd ? other : mine) >> (8 * odd)) & 0xFFu;
-        keep[DROP ? k + 1 : 0] = ((odd ? mine : other) >> (8 * odd)) & 0xFFu;
+        const uint4 mine =
+            dr.thr ? keep_mask_bytes(drop_block(seed, step, dr.tag, blk0 + uint64_t(k + odd) * 16),
+                                     dr.thr)
+                   : all;
+        // even lane: block k (keeps words 0,1; sends 2,3); odd: block k+1 (keeps 2,3; sends 0,1)
+        const uint32_t s0 = odd ? mine.x : mine.z, s1 = odd ? mine.y : mine.w;
+        const uint32_t g0 = __shfl_xor_sync(0xFFFFFFFFu, s0, 1);
+        const uint32_t g1 = __shfl_xor_sync(0xFFFFFFFFu, s1, 1);
+        keep[DROP ? k : 0] = odd ? make_uint2(g0, g1) : make_uint2(mine.x, mine.y);
+        keep[DROP ? k + 1 : 0] = odd ? make_uint2(mine.z, mine.w) : make_uint2(g0, g1);
       }
       if (NV & 1) {
-        const uint32_t w =
-            dr.thr ? keep16(drop_block(seed, step, dr.tag, blk0 + uint64_t(NV - 1) * 16), dr.thr)
-                   : 0xFFFFu;
-        keep[DROP ? NV - 1 : 0] = (w >> (8 * odd)) & 0xFFu;
+        const uint4 w =
+            dr.thr ? keep_mask_bytes(drop_block(seed, step, dr.tag, blk0 + uint64_t(NV - 1) * 16),
+                                     dr.thr)
+                   : all;
+        keep[DROP ? NV - 1 : 0] = odd ? make_uint2(w.z, w.w) : make_uint2(w.x, w.y);
       }
     }
 #pragma unroll
@@ -334,7 +345,10 @@ __global__ void __launch_bounds__(256, 1)
         float q[8];
         unpack8(packed, q);  // the stored (bf16) gradient, as a separate pass would read it
 #pragma unroll
-        for (int i = 0; i < 8; ++i) q[i] = (keep[DROP ? k : 0] >> i) & 1u ? q[i] * dr.scale : 0.f;
+        for (int i = 0; i < 8; ++i)
+          q[i] = __uint_as_float(__float_as_uint(q[i] * dr.scale) &
+                                 keep_mask_elem(i < 4 ? keep[DROP ? k : 0].x : keep[DROP ? k : 0].y,
+                                                i & 3));
         const uint4 pd = pack8(q);
         reinterpret_cast<uint4*>(dr.dxd + r * H)[k * 32 + lane] = pd;
         unpack8(pd, q);
