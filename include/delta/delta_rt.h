@@ -92,6 +92,7 @@ typedef struct delta_ref {
  *  STATS_SUM       r0 partials, r1 out, i0 C, i1 accumulate  (delta_stats_col_sum)
  *  LAYERNORM_BWD_DROP  as LAYERNORM_BWD, + r10 dxd, r11 dbias, r12 rng, i2 tag, f0 p
  *                  (delta_layernorm_bwd_drop)
+ *  PARTS_MERGE     r0 ws, r1 out, i0 parts, i1 cols  (delta_parts_merge)
  */
 enum {
   DELTA_K_COPY = 1,
@@ -123,7 +124,8 @@ enum {
   DELTA_K_ATTN = 27,
   DELTA_K_ATTN_BWD = 28,
   DELTA_K_STATS_SUM = 29,
-  DELTA_K_LAYERNORM_BWD_DROP = 30
+  DELTA_K_LAYERNORM_BWD_DROP = 30,
+  DELTA_K_PARTS_MERGE = 31
 };
 enum {
   DELTA_KOP_FIRST_ONLY = 1,     /* skipped when the node is recomputed        */

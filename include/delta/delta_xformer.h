@@ -104,9 +104,14 @@ delta_status delta_attention_bwd(const void* qkv, const void* out, const void* d
                                  const float* lse, float* D, void* dqkv, int32_t B, int32_t S,
                                  int32_t heads, float p, const uint64_t* rng, uint32_t tag,
                                  float* dbias, float* ws, void* stream);
-/* debugging aid: the backward kernel writes progress words (32 per CTA) to
- * this mapped host buffer (NULL = off) */
+/* debugging aid (libraries built with -DDELTA_ATTN_DEBUG; a no-op
+ * otherwise): the backward kernel writes progress words (32 per CTA) to this
+ * mapped host buffer (NULL = off) */
 delta_status delta_attention_debug(void* host_words);
+/* out[c] = sum over p < parts of ws[p * cols + c], summed in order of p
+ * (partial rows of a column reduction, e.g. DELTA_EPI_GELU_BWD's) */
+delta_status delta_parts_merge(const float* ws, int32_t parts, int32_t cols, float* out,
+                               void* stream);
 /* AdamW over flat fp32 buffers (decoupled weight decay on the first n_bf
  * elements, which are also written as bf16 to wbf), bias correction with step
  * rng[1] + 1; then rng[1] += 1 (the next step's dropout masks). */

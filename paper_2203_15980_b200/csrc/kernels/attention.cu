@@ -133,21 +133,6 @@ __device__ __forceinline__ void store16(bf16* dst, const uint32_t (&v)[16], floa
                       pack_bf16x2(__uint_as_float(v[8 * u + 6]) * s, __uint_as_float(v[8 * u + 7]) * s));
 }
 
-// column sums of a warp's [32 rows (lanes)][32 columns (v)] block: lane c
-// returns the sum over the 32 lanes of column c (recursive halving, 31
-// shuffles; a fixed combination order, so deterministic)
-__device__ __forceinline__ float warp_colsum32(float (&v)[32], int lane) {
-#pragma unroll
-  for (int o = 16; o >= 1; o >>= 1) {
-    const bool up = lane & o;
-#pragma unroll
-    for (int k = 0; k < o; ++k) {
-      const float got = __shfl_xor_sync(0xffffffffu, up ? v[k] : v[k + o], o);
-      v[k] = (up ? v[k + o] : v[k]) + got;
-    }
-  }
-  return v[0];
-}
 __device__ __forceinline__ float warp_colsum_scaled(const uint32_t (&a)[16], const uint32_t (&b)[16],
                                                     float s, int lane) {
   float v[32];
@@ -159,14 +144,17 @@ __device__ __forceinline__ float warp_colsum_scaled(const uint32_t (&a)[16], con
   return warp_colsum32(v, lane);
 }
 
-// debug: progress words in mapped host memory (null = off), set by
-// attention_debug(); the host can read them while a kernel is stuck
+// debug (builds with -DDELTA_ATTN_DEBUG): progress words in mapped host
+// memory (null = off), set by attention_debug(); the host can read them while
+// a kernel is stuck.  Compiled out otherwise (they cost issue slots).
 __device__ uint32_t* g_attn_dbg = nullptr;
 __device__ __forceinline__ void dbg_mark(int slot, uint32_t v) {
+#ifdef DELTA_ATTN_DEBUG
   uint32_t* d = g_attn_dbg;
   if (d) {
     *reinterpret_cast<volatile uint32_t*>(d + (blockIdx.y * gridDim.x + blockIdx.x) * 32 + slot) = v;
   }
+#endif
 }
 
 struct AttnArgs {

@@ -39,6 +39,45 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 
+// ---- warp column sums of a [32 rows = lanes][32 columns] block: lane c
+// returns column c's sum (recursive halving: 31 shuffles, a fixed combination
+// order, so deterministic) ----
+__device__ __forceinline__ float warp_colsum32(float (&v)[32], int lane) {
+#pragma unroll
+  for (int o = 16; o >= 1; o >>= 1) {
+    const bool up = lane & o;
+#pragma unroll
+    for (int k = 0; k < o; ++k) {
+      const float got = __shfl_xor_sync(0xffffffffu, up ? v[k] : v[k + o], o);
+      v[k] = (up ? v[k + o] : v[k]) + got;
+    }
+  }
+  return v[0];
+}
+// ... of bf16 values packed two per word (word w = columns 2w, 2w+1): the first
+// halving step exchanges packed words, the rest runs in fp32
+__device__ __forceinline__ float warp_colsum32_bf16(const uint32_t (&w)[16], int lane) {
+  const bool up = lane & 16;
+  float v[32];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    const uint32_t keep = up ? w[k + 8] : w[k];
+    const uint32_t got = __shfl_xor_sync(0xffffffffu, up ? w[k] : w[k + 8], 16);
+    v[2 * k] = __uint_as_float(keep << 16) + __uint_as_float(got << 16);
+    v[2 * k + 1] = __uint_as_float(keep & 0xFFFF0000u) + __uint_as_float(got & 0xFFFF0000u);
+  }
+#pragma unroll
+  for (int o = 8; o >= 1; o >>= 1) {
+    const bool u = lane & o;
+#pragma unroll
+    for (int k = 0; k < o; ++k) {
+      const float got = __shfl_xor_sync(0xffffffffu, u ? v[k] : v[k + o], o);
+      v[k] = (u ? v[k + o] : v[k]) + got;
+    }
+  }
+  return v[0];
+}
+
 // ---- bulk copy (TMA, non-tensor): `bytes` (multiple of 16) global -> shared,
 // completion as transaction bytes on an mbarrier ----
 __device__ __forceinline__ void bulk_load(uint32_t dst, const void* src, uint32_t bytes,

@@ -279,6 +279,9 @@ delta_status run_kop(delta_rt* rt, const delta_kop& k, Frame& fr, uint64_t node,
                                  k.f[0], rp<const uint64_t>(fr, r[6]), uint32_t(i[3]),
                                  rp<float>(fr, r[7]), rp<float>(fr, r[8]), st);
       break;
+    case DELTA_K_PARTS_MERGE:
+      e = delta_k::merge_parts(rp<const float>(fr, r[0]), int(i[0]), int(i[1]), rp<float>(fr, r[1]), st);
+      break;
     case DELTA_K_STATS_SUM:
       e = delta_k::stats_col_sum(rp<const float>(fr, r[0]), int(i[0]), rp<float>(fr, r[1]), int(i[1]),
                                  st);

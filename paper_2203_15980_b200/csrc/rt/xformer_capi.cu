@@ -114,6 +114,14 @@ delta_status delta_attention_bwd(const void* qkv, const void* out, const void* d
 delta_status delta_attention_debug(void* host_words) {
   return st_(delta_k::attention_debug(host_words), "attention_debug");
 }
+delta_status delta_parts_merge(const float* ws, int32_t parts, int32_t cols, float* out,
+                               void* stream) {
+  if (parts <= 0 || cols <= 0) {
+    delta_rt::set_error("parts_merge: empty");
+    return DELTA_E_ARGUMENT;
+  }
+  return st_(delta_k::merge_parts(ws, parts, cols, out, S(stream)), "parts_merge");
+}
 delta_status delta_adamw_step(float* w, float* m, float* v, const float* g, void* wbf, int64_t n,
                               int64_t n_bf, float lr, float beta1, float beta2, float eps,
                               float weight_decay, uint64_t* rng, void* stream) {

@@ -21,6 +21,7 @@ _SIGS = {
     "delta_stats_partials_floats": (i64, [i32]),
     "delta_bn_stats_from_partials": (i32, [vp, i32, vp, vp, f32, vp, vp, f32, vp]),
     "delta_stats_col_sum": (i32, [vp, i32, vp, i32, vp]),
+    "delta_parts_merge": (i32, [vp, i32, i32, vp, vp]),
     "delta_conv_forward_ex": (i32, [vp, vp, vp, vp, vp, vp]),
     "delta_conv_set_tile_n": (i32, [vp, i32]),
     "delta_wgrad_create": (i32, [i32] * 9 + [P(vp)]),
@@ -138,7 +139,8 @@ class Conv:
 
     def gelu_bwd(self, x_ptr, y_ptr, pre_ptr, stream, stats_ptr=None):
         """y = bf16(conv(x) * gelu'(pre)): an MLP input gradient through the GELU;
-        stats_ptr: per-CTA column statistics of y (stats_col_sum -> its column sums)"""
+        stats_ptr: y's column sums per (128-row block, lane quarter),
+        gelu_bwd_colsum_floats(M, K) floats (parts_merge -> its column sums)"""
         e = ConvEpilogue(EPI_GELU_BWD, 0, 0, 0, None, None, None, pre_ptr, None, None, None, None)
         check(lib.delta_conv_forward_ex(self._h, x_ptr, y_ptr, stats_ptr, C.byref(e), stream))
         _count(1)
@@ -226,6 +228,17 @@ def stats_parts() -> int:
 
 def stats_partials_floats(C_: int) -> int:
     return int(lib.delta_stats_partials_floats(C_))
+
+
+def parts_merge(ws, parts, cols, out, stream):
+    """out[c] = sum_p ws[p*cols + c] in order of p"""
+    check(lib.delta_parts_merge(ws, parts, cols, out, stream))
+    _count(1)
+
+
+def gelu_bwd_colsum_floats(M, K) -> int:
+    """size of EPI_GELU_BWD's column-sum table: [ceil(M/128)][4][K] floats"""
+    return ((M + 127) // 128) * 4 * K
 
 
 def stats_col_sum(partials, C_, out, stream, accumulate=False):
