@@ -123,25 +123,33 @@ __device__ __forceinline__ void st_row16(uint32_t base, int r, int col, const ui
                  make_uint4(w[4 * u], w[4 * u + 1], w[4 * u + 2], w[4 * u + 3]));
 }
 
-__device__ __forceinline__ void store16(bf16* dst, const uint32_t (&v)[16], float s) {
-  uint4* d = reinterpret_cast<uint4*>(dst);
+// 16 fp32 values * s -> 8 packed bf16x2 words
+__device__ __forceinline__ void pack16(const uint32_t (&v)[16], float s, uint32_t* w) {
 #pragma unroll
-  for (int u = 0; u < 2; ++u)
-    d[u] = make_uint4(pack_bf16x2(__uint_as_float(v[8 * u]) * s, __uint_as_float(v[8 * u + 1]) * s),
-                      pack_bf16x2(__uint_as_float(v[8 * u + 2]) * s, __uint_as_float(v[8 * u + 3]) * s),
-                      pack_bf16x2(__uint_as_float(v[8 * u + 4]) * s, __uint_as_float(v[8 * u + 5]) * s),
-                      pack_bf16x2(__uint_as_float(v[8 * u + 6]) * s, __uint_as_float(v[8 * u + 7]) * s));
+  for (int e = 0; e < 8; ++e)
+    w[e] = pack_bf16x2(__uint_as_float(v[2 * e]) * s, __uint_as_float(v[2 * e + 1]) * s);
 }
-
-__device__ __forceinline__ float warp_colsum_scaled(const uint32_t (&a)[16], const uint32_t (&b)[16],
-                                                    float s, int lane) {
-  float v[32];
-#pragma unroll
-  for (int e = 0; e < 16; ++e) {
-    v[e] = __uint_as_float(a[e]) * s;
-    v[16 + e] = __uint_as_float(b[e]) * s;
-  }
-  return warp_colsum32(v, lane);
+__device__ __forceinline__ void store16w(bf16* dst, const uint32_t* w) {
+  uint4* d = reinterpret_cast<uint4*>(dst);
+  d[0] = make_uint4(w[0], w[1], w[2], w[3]);
+  d[1] = make_uint4(w[4], w[5], w[6], w[7]);
+}
+__device__ __forceinline__ void store16(bf16* dst, const uint32_t (&v)[16], float s) {
+  uint32_t w[8];
+  pack16(v, s, w);
+  store16w(dst, w);
+}
+// 32 columns of a row scaled, stored as bf16, and (sum) the warp's column sums
+// of the stored values: lane c returns column c's sum over the warp's 32 rows
+__device__ __forceinline__ float store32_colsum(bf16* dst, const uint32_t (&a)[16],
+                                                const uint32_t (&b)[16], float s, bool sum,
+                                                int lane) {
+  uint32_t w[16];
+  pack16(a, s, w);
+  pack16(b, s, w + 8);
+  store16w(dst, w);
+  store16w(dst + 16, w + 8);
+  return sum ? warp_colsum32_bf16(w, lane) : 0.f;
 }
 
 // debug (builds with -DDELTA_ATTN_DEBUG): progress words in mapped host
@@ -548,10 +556,11 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t trow = tmem + (uint32_t(quarter * 32) << 16);
     const uint64_t seed = a.rng[0], step = a.rng[1];
     const uint64_t bh = uint64_t(b * a.heads + h);
-    float lse2[4], Dv[4];
-    for (int i = 0; i < nt; ++i) {
-      lse2[i] = __ldg(a.lse + bh * S + i * TILE + r);
-      Dv[i] = __ldg(a.D + bh * S + i * TILE + r);
+    float lse2[4], Dv[4];  // registers: constant indices only
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      lse2[i] = i < nt ? __ldg(a.lse + bh * S + i * TILE + r) : 0.f;
+      Dv[i] = i < nt ? __ldg(a.D + bh * S + i * TILE + r) : 0.f;
     }
     uint32_t nsp = 0;
     float csum_kv = 0.f;
@@ -618,11 +627,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (lane == 0) mbar_arrive(bar_dr);
         bf16* dst = a.out + (int64_t(row0) + j * TILE + r) * (3 * a.Hd) + (which ? 2 : 1) * a.Hd +
                     h * HD + (part & 1) * 32;
-        store16(dst, v0, which ? 1.f : kScale);
-        store16(dst + 16, v1, which ? 1.f : kScale);
-        // bias gradient: this warp's 32 key rows summed per column, lane c
-        // keeps column c across the key blocks
-        if (a.colpart) csum_kv += warp_colsum_scaled(v0, v1, which ? 1.f : kScale, lane);
+        // bias gradient: this warp's 32 key rows summed per column (of the
+        // stored values), lane c keeps column c across the key blocks
+        csum_kv += store32_colsum(dst, v0, v1, which ? 1.f : kScale, a.colpart != nullptr, lane);
       }
     }
     // ---- dQ of every query block (TMEM 64 i, lane = query row) ----
@@ -637,14 +644,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       tmem_ld16(trow + 64 * i + 48, v3);
       tmem_wait();
       bf16* dst = a.out + (int64_t(row0) + i * TILE + r) * (3 * a.Hd) + h * HD;
-      store16(dst, v0, kScale);
-      store16(dst + 16, v1, kScale);
-      store16(dst + 32, v2, kScale);
-      store16(dst + 48, v3, kScale);
-      if (a.colpart) {
-        csum_q0 = warp_colsum_scaled(v0, v1, kScale, lane);
-        csum_q1 = warp_colsum_scaled(v2, v3, kScale, lane);
-      }
+      csum_q0 = store32_colsum(dst, v0, v1, kScale, a.colpart != nullptr, lane);
+      csum_q1 = store32_colsum(dst + 32, v2, v3, kScale, a.colpart != nullptr, lane);
     }
     if (a.colpart) {
       // every MMA is done: P's buffer is scratch.  Combine the warps' column
