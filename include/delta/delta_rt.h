@@ -130,9 +130,12 @@ enum {
 enum {
   DELTA_KOP_FIRST_ONLY = 1,     /* skipped when the node is recomputed        */
   DELTA_KOP_RECOMPUTE_ONLY = 2, /* run only when the node is recomputed       */
-  DELTA_KOP_SIDE = 4            /* with DELTA_SIDE_STREAM=1: run on the side
+  DELTA_KOP_SIDE = 4,           /* with DELTA_SIDE_STREAM=1: run on the side
                                    compute stream, concurrent with the node's
                                    other ops, joined at the node's end        */
+  DELTA_KOP_SIDE_ALWAYS = 8     /* on the side stream whatever DELTA_SIDE_STREAM
+                                   says (an op placed there to fill another
+                                   kernel's idle SMs), joined the same way   */
 };
 
 typedef struct delta_kop {

@@ -33,6 +33,7 @@ token ids / labels / the id CSR, and the backward scratch.
 from __future__ import annotations
 
 import math
+import os
 from dataclasses import dataclass
 
 import numpy as np
@@ -272,6 +273,10 @@ class BertRuntime(DeltaRuntime):
         loss = rt.step(ids, types, labels)      # host int tensors
     """
 
+    # the output projection's weight gradient runs on the side stream during
+    # the attention backward (DELTA_BERT_OVERLAP=0: in its own node, serially)
+    overlap_attn_wgrad = os.environ.get("DELTA_BERT_OVERLAP", "1") != "0"
+
     def __init__(self, cfg: BertConfig = BERT_LARGE, device: str = "cuda", seed: int = 0,
                  lr: float = 1e-4, dropout_seed: int = 0x5EED_0F_DE17A):
         self.device = torch.device(device)
@@ -463,8 +468,11 @@ class BertRuntime(DeltaRuntime):
                           (self.gstats.numel() // cfg.ffn, cfg.ffn)))
             else:
                 add(X.kop(X.K_CONV, (dy, X.OUT(), None), conv=dconv))
-            add(X.kop(X.K_WGRAD, (dy, X.IN(1), _ptr(pr.gviews["w:" + lin]), _ptr(self.wg_ws)),
-                      conv=self._lin_w[lin]._h), self._lin_w[lin].launches)
+            if not (fused_drop and self.g.nodes[node.parents[1]].op == "attention"
+                    and self.overlap_attn_wgrad):
+                add(X.kop(X.K_WGRAD, (dy, X.IN(1), _ptr(pr.gviews["w:" + lin]), _ptr(self.wg_ws)),
+                          conv=self._lin_w[lin]._h), self._lin_w[lin].launches)
+            # (else: the attention backward node runs it, see there)
             if not node.attrs.get("bias_done") and not fused_drop:
                 add(X.kop(X.K_COLSUM, (dy, None, _ptr(pr.gviews["b:" + lin]), _ptr(self.cs_ws)),
                           (T, cout, 0, 0)), 2)
@@ -473,6 +481,17 @@ class BertRuntime(DeltaRuntime):
             # dqkv and, reduced per sequence inside the kernel, its column
             # sums: the QKV projection's bias gradient
             qkv_lin = self.g.nodes[node.parents[1]].attrs["lin"]
+            if self.overlap_attn_wgrad:
+                # the output projection's weight gradient (its inputs: the
+                # dropout-masked gradient still in drop_ws and this node's
+                # input `att`) on the side stream, concurrent with the
+                # attention backward: its CTAs fill the SMs the attention
+                # kernel's last partial wave leaves idle
+                out_lin = self.g.nodes[node.parents[0]].attrs["lin"]
+                add(X.kop(X.K_WGRAD, (_ptr(self.drop_ws), X.IN(2), _ptr(pr.gviews["w:" + out_lin]),
+                                      _ptr(self.wg_ws)),
+                          conv=self._lin_w[out_lin]._h, flags=X.SIDE_ALWAYS),
+                    self._lin_w[out_lin].launches)
             add(X.kop(X.K_ATTN_BWD, (X.IN(1), X.IN(2), X.IN(0), _ptr(pr.lse[l]), _ptr(self.attn_D),
                                      X.OUT(), rng, _ptr(pr.gviews["b:" + qkv_lin]),
                                      _ptr(self.cs_ws)),

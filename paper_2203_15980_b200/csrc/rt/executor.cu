@@ -327,7 +327,7 @@ delta_status run_node(delta_rt* rt, const delta_action& a, cudaStream_t st) {
     if (recompute && (k.flags & DELTA_KOP_FIRST_ONLY)) continue;
     if (!recompute && (k.flags & DELTA_KOP_RECOMPUTE_ONLY)) continue;
     cudaStream_t ks = st;
-    if ((k.flags & DELTA_KOP_SIDE) && rt->side_enabled) {
+    if (((k.flags & DELTA_KOP_SIDE) && rt->side_enabled) || (k.flags & DELTA_KOP_SIDE_ALWAYS)) {
       if (!forked) {  // the side stream starts after everything before this node
         RT_CUDA(cudaEventRecord(rt->fork, st));
         RT_CUDA(cudaStreamWaitEvent(rt->side, rt->fork, 0));

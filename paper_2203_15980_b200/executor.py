@@ -25,7 +25,7 @@ REF_PTR, REF_OUT, REF_IN, REF_SCRATCH = 0, 1, 2, 3
 (K_LAYERNORM, K_LAYERNORM_BWD, K_GELU, K_ADD_DROPOUT, K_DROPOUT_BWD, K_COLSUM, K_EMBED,
  K_EMBED_GRADS, K_SPAN_HEAD, K_SPAN_HEAD_BWD, K_ATTN, K_ATTN_BWD, K_STATS_SUM,
  K_LAYERNORM_BWD_DROP, K_PARTS_MERGE) = range(17, 32)
-FIRST_ONLY, RECOMPUTE_ONLY, SIDE = 1, 2, 4
+FIRST_ONLY, RECOMPUTE_ONLY, SIDE, SIDE_ALWAYS = 1, 2, 4, 8
 
 
 
