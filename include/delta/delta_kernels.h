@@ -78,10 +78,7 @@ delta_status delta_conv_forward(const delta_conv* c, const void* x, void* y, flo
  *       x = [tokens][in], weights [out][in]) with its bias (`beta`).
  *   DELTA_EPI_GELU_BWD: y = bf16(acc * gelu'(xc)), xc = the [M][K] GELU input
  *       (erf GELU): the MLP input gradient through the GELU (1x1 only,
- *       tile_n <= 128).  With `stats` (weights [C][K], delta_conv_create_t):
- *       the column sums of the stored y per (128-row block, TMEM lane
- *       quarter), [ceil(M/128)][4][K] floats — delta_parts_merge over the
- *       ceil(M/128)*4 rows gives sum_m y[m][k] (a bias gradient).
+ *       tile_n <= 128).
  * Output channels must be a multiple of 32 for the fused modes. */
 enum {
   DELTA_EPI_STORE = 0,

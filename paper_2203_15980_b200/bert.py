@@ -312,10 +312,9 @@ class BertRuntime(DeltaRuntime):
                                      K.span_head_workspace_floats(T, H),
                                      cfg.batch * 3 * H), device=dev)
         self.drop_ws = torch.empty(T, H, dtype=torch.bfloat16, device=dev)  # dropout-bwd scratch
-        # column sums of the gelu' input gradient per (128-row block, lane
-        # quarter) from its GEMM epilogue: merged, the up-projection's bias
-        # gradient (no extra pass over the [tokens][4096] gradient)
-        self.gstats = torch.empty(K.gelu_bwd_colsum_floats(T, cfg.ffn), device=dev)
+        # per-CTA column statistics of the gelu' input gradient (its column
+        # sums are the up-projection's bias gradient: no extra pass over it)
+        self.gstats = torch.empty(K.stats_partials_floats(cfg.ffn), device=dev)
         self.attn_D = torch.empty(cfg.batch * cfg.heads * cfg.seq, device=dev)
         self.dlogits = torch.empty(T, 2, device=dev)
         self.row_loss = torch.empty(cfg.batch, device=dev)
@@ -458,14 +457,14 @@ class BertRuntime(DeltaRuntime):
                 dy = _ptr(self.drop_ws)
             dconv = self._lin_d[lin]._h
             if node.attrs.get("gelu"):
-                # the gelu' input gradient also reduces its column sums per
-                # row block: the bias gradient of the up projection (whose
+                # the gelu' input gradient also reduces its per-CTA column
+                # statistics: the bias gradient of the up projection (whose
                 # output gradient it is) follows from them below
                 up = self.g.nodes[node.parents[2]].attrs["lin"]
                 add(X.kop(X.K_CONV_EX, (dy, X.OUT(), _ptr(self.gstats), None, None, None, X.IN(2)),
                           (K.EPI_GELU_BWD, 0, 0), conv=dconv))
-                add(X.kop(X.K_PARTS_MERGE, (_ptr(self.gstats), _ptr(pr.gviews["b:" + up])),
-                          (self.gstats.numel() // cfg.ffn, cfg.ffn)))
+                add(X.kop(X.K_STATS_SUM, (_ptr(self.gstats), _ptr(pr.gviews["b:" + up])),
+                          (self.g.linears[up][1], 0)))
             else:
                 add(X.kop(X.K_CONV, (dy, X.OUT(), None), conv=dconv))
             if not (fused_drop and self.g.nodes[node.parents[1]].op == "attention"

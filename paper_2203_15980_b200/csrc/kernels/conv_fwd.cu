@@ -98,9 +98,6 @@ struct ConvArgs {
   int tiles;    // m_tiles * n_tiles
   float4* stats;  // optional per-CTA partials [grid][K] (stats_cta.cuh): EPI_STORE (count,
                   // mean, M2) of the bf16 outputs; EPI_BN_BWD (sum g, sum g*xc)
-  float* colsum;  // optional (EV_GELU_BWD): column sums of the stored bf16 outputs per
-                  // (128-row block, TMEM lane quarter), [ceil(M/128)][4][K] — warp
-                  // shuffles only, no barrier or read-modify-write
   ConvEpilogue e;
 };
 
@@ -806,14 +803,6 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
           continue;
         }
-        if constexpr (EV == EV_GELU_BWD) {
-          if (a.colsum != nullptr) {
-            const uint32_t (&wds)[16] = *reinterpret_cast<const uint32_t(*)[16]>(pk);
-            const float cs = warp_colsum32_bf16(wds, lane);
-            if (col + lane < a.K)
-              a.colsum[(int64_t(m0 / BM) * 4 + quarter) * a.K + col + lane] = cs;
-          }
-        }
         const uint32_t buf = stage_base + (ec % NBUF) * 2048;
         // the TMA store that last read this buffer (NBUF chunks ago) is done
         if (lane == 0) bulk_wait_read<NBUF - 1>();
@@ -1209,9 +1198,7 @@ cudaError_t launch(const ConvPlan& cp, const void* x, void* y, float* stats,
   a.n_tiles = (cp.K + BN - 1) / BN;
   constexpr int TM = PAIR ? 2 * BM : BM;
   a.tiles = (row_tiled(MODE) ? cp.N * cp.P : (a.M + TM - 1) / TM) * a.n_tiles;
-  // EV_GELU_BWD: `stats` is the column-sum table (ConvArgs::colsum)
-  a.stats = EV == EV_GELU_BWD ? nullptr : reinterpret_cast<float4*>(stats);
-  a.colsum = EV == EV_GELU_BWD ? stats : nullptr;
+  a.stats = reinterpret_cast<float4*>(stats);
   a.e = epi;
   alignas(64) CUtensorMap amap;
   alignas(64) CUtensorMap ymap;
@@ -1339,9 +1326,8 @@ cudaError_t conv_forward(const ConvPlan& cp, const void* x, void* y, float* stat
   const bool use_gather = gather_forced();
   if (cp.bmn) {
     // [kdim][K] weights (MN-major B): the linear layers' input gradients;
-    // `stats` (gelu' epilogue): the output's column sums per (128-row block,
-    // lane quarter), [ceil(M/128)][4][K] floats — merged, the up-projection's
-    // bias gradient
+    // `stats` (gelu' epilogue): per-CTA column statistics of the output
+    // (its column sums are the up-projection's bias gradient)
     if (!tma_a || (stats && e.mode != EPI_GELU_BWD)) return cudaErrorInvalidValue;
     const bool pr = pair_ok(cp, true);
     if (e.mode == EPI_STORE) {

@@ -139,8 +139,8 @@ class Conv:
 
     def gelu_bwd(self, x_ptr, y_ptr, pre_ptr, stream, stats_ptr=None):
         """y = bf16(conv(x) * gelu'(pre)): an MLP input gradient through the GELU;
-        stats_ptr: y's column sums per (128-row block, lane quarter),
-        gelu_bwd_colsum_floats(M, K) floats (parts_merge -> its column sums)"""
+        stats_ptr: per-CTA column statistics of y, stats_partials_floats(K)
+        floats (stats_col_sum -> its column sums)"""
         e = ConvEpilogue(EPI_GELU_BWD, 0, 0, 0, None, None, None, pre_ptr, None, None, None, None)
         check(lib.delta_conv_forward_ex(self._h, x_ptr, y_ptr, stats_ptr, C.byref(e), stream))
         _count(1)
@@ -234,11 +234,6 @@ def parts_merge(ws, parts, cols, out, stream):
     """out[c] = sum_p ws[p*cols + c] in order of p"""
     check(lib.delta_parts_merge(ws, parts, cols, out, stream))
     _count(1)
-
-
-def gelu_bwd_colsum_floats(M, K) -> int:
-    """size of EPI_GELU_BWD's column-sum table: [ceil(M/128)][4][K] floats"""
-    return ((M + 127) // 128) * 4 * K
 
 
 def stats_col_sum(partials, C_, out, stream, accumulate=False):

@@ -202,10 +202,10 @@ def test_linear_input_gradient_from_forward_weights(mode):
 
 
 @pytest.mark.parametrize("M", [4096, 1000])
-def test_gelu_bwd_column_sums(M):
-    """EPI_GELU_BWD's column sums per (128-row block, lane quarter): merged,
-    the column sums of the stored output (the up projection's bias gradient);
-    the output itself is unchanged by computing them"""
+def test_gelu_bwd_column_statistics(M):
+    """EPI_GELU_BWD with per-CTA column statistics: stats_col_sum of them is
+    the column sums of the stored output (the up projection's bias
+    gradient); the output itself is unchanged by computing them"""
     out_f, in_f = 1024, 4096
     dy = rnd(M, out_f)
     w = rnd(out_f, in_f, scale=out_f ** -0.5, seed=1)
@@ -215,16 +215,25 @@ def test_gelu_bwd_column_sums(M):
     y0 = torch.empty(M, in_f, device=dev, dtype=torch.bfloat16)
     c.gelu_bwd(dy.data_ptr(), y0.data_ptr(), pre.data_ptr(), _st())
     y = torch.empty_like(y0)
-    ws = torch.full((K.gelu_bwd_colsum_floats(M, in_f),), float("nan"), device=dev)
+    ws = torch.full((K.stats_partials_floats(in_f),), float("nan"), device=dev)
     c.gelu_bwd(dy.data_ptr(), y.data_ptr(), pre.data_ptr(), _st(), stats_ptr=ws.data_ptr())
     assert torch.equal(y, y0)
     out = torch.empty(in_f, device=dev)
-    K.parts_merge(ws.data_ptr(), ws.numel() // in_f, in_f, out.data_ptr(), _st())
+    K.stats_col_sum(ws.data_ptr(), in_f, out.data_ptr(), _st())
     close(out, y.double().sum(0).float(), 1e-4, 1e-4)
     out2 = torch.empty_like(out)
     c.gelu_bwd(dy.data_ptr(), y.data_ptr(), pre.data_ptr(), _st(), stats_ptr=ws.data_ptr())
-    K.parts_merge(ws.data_ptr(), ws.numel() // in_f, in_f, out2.data_ptr(), _st())
+    K.stats_col_sum(ws.data_ptr(), in_f, out2.data_ptr(), _st())
     assert torch.equal(out, out2)
+
+
+def test_parts_merge():
+    """delta_parts_merge: column sums of partial rows in row order"""
+    parts, cols = 37, 3000
+    ws = torch.randn(parts, cols, device=dev)
+    out = torch.empty(cols, device=dev)
+    K.parts_merge(ws.data_ptr(), parts, cols, out.data_ptr(), _st())
+    close(out, ws.double().sum(0).float(), 1e-5, 1e-5)
 
 
 def _attn_inputs(B, S, heads, seed=0):
