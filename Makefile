@@ -14,7 +14,8 @@ INC      := -Iinclude -I$(CSRC) -I$(JINC) -I$(CUDA)/include
 CXXFLAGS := -std=c++20 -O2 -fPIC -Wall -Wextra -Wno-unused-parameter $(INC)
 ARCH     := -gencode arch=compute_100a,code=sm_100a
 NVFLAGS  := -std=c++20 -O3 $(ARCH) -lineinfo -Xcompiler -fPIC --expt-relaxed-constexpr \
-            -Xptxas -v $(INC)
+            -Xptxas -v $(INC) $(NVEXTRA)
+# A/B builds of a variant: make OBJ=build/obj_x LIB=build/ab/libdelta_x.so NVEXTRA=-DFOO
 
 CPP_SRCS := $(wildcard $(CSRC)/plan/*.cpp) $(wildcard $(CSRC)/capi/*.cpp) \
             $(wildcard $(CSRC)/rt/*.cpp)
