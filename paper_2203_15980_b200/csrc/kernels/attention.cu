@@ -215,8 +215,14 @@ __global__ void __launch_bounds__(kThreadsF2, 1)
   uint64_t* bar_o = bars + 8;    // [2] a tile's PV MMAs done
   uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 10);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int qp = blockIdx.x, h = blockIdx.y, b = blockIdx.z;
-  const int ntile = min(2, nt - 2 * qp);
+  // persistent: work item w = (query-tile pair, head, sequence), qp fastest
+  const int nqp = (nt + 1) / 2;
+  const int items = nqp * a.heads * a.B;
+  auto item = [&](int w, int& qp, int& h, int& b) {
+    qp = w % nqp;
+    h = (w / nqp) % a.heads;
+    b = w / (nqp * a.heads);
+  };
 
   if (threadIdx.x == 0) {
     mbar_init(bar_qk, 1);
@@ -237,22 +243,30 @@ __global__ void __launch_bounds__(kThreadsF2, 1)
   const uint32_t tmem = *tslot;
   pdl_wait();
   pdl_trigger();
-  const int row0 = b * S;
-  const int nk = 2 * nt;  // S steps: nt of pass 1 (max), nt of pass 2 (P, O)
+  const int nk = 2 * nt;  // S steps per item: nt of pass 1 (max), nt of pass 2 (P, O)
 
   if (warp == F2_CTRL) {
-    if (lane == 0) {
-      mbar_arrive_expect_tx(bar_qk, uint32_t(ntile + nt) * TILE_BYTES);
-      for (int t = 0; t < ntile; ++t)
-        tma_load_2d(sQ + t * TILE_BYTES, &qkv_map, bar_qk, h * HD, row0 + (2 * qp + t) * TILE);
-      for (int j = 0; j < nt; ++j)
-        tma_load_2d(sK + j * TILE_BYTES, &qkv_map, bar_qk, a.Hd + h * HD, row0 + j * TILE);
-      mbar_arrive_expect_tx(bar_v, uint32_t(nt) * TILE_BYTES);
-      for (int j = 0; j < nt; ++j)
-        tma_load_2d(sV + j * TILE_BYTES, &qkv_map, bar_v, 2 * a.Hd + h * HD, row0 + j * TILE);
-    }
     constexpr uint32_t idS = umma_idesc_bf16(128, 128);
     constexpr uint32_t idO = umma_idesc_bf16(128, HD) | (1u << 16);  // B (V) MN-major
+    // the next item's Q and K (once this item's last S MMAs are done), V (once
+    // its last PV MMAs are done) are loaded under this item's tail
+    auto load_qk = [&](int w) {
+      int qp, h, b;
+      item(w, qp, h, b);
+      const int ntl = min(2, nt - 2 * qp);
+      mbar_arrive_expect_tx(bar_qk, uint32_t(ntl + nt) * TILE_BYTES);
+      for (int t = 0; t < ntl; ++t)
+        tma_load_2d(sQ + t * TILE_BYTES, &qkv_map, bar_qk, h * HD, b * S + (2 * qp + t) * TILE);
+      for (int j = 0; j < nt; ++j)
+        tma_load_2d(sK + j * TILE_BYTES, &qkv_map, bar_qk, a.Hd + h * HD, b * S + j * TILE);
+    };
+    auto load_v = [&](int w) {
+      int qp, h, b;
+      item(w, qp, h, b);
+      mbar_arrive_expect_tx(bar_v, uint32_t(nt) * TILE_BYTES);
+      for (int j = 0; j < nt; ++j)
+        tma_load_2d(sV + j * TILE_BYTES, &qkv_map, bar_v, 2 * a.Hd + h * HD, b * S + j * TILE);
+    };
     auto issue_s = [&](int t, int k) {
       if (elect_one()) {
         const uint64_t dq = umma_desc_sw128(sQ + t * TILE_BYTES);
@@ -264,128 +278,158 @@ __global__ void __launch_bounds__(kThreadsF2, 1)
       }
       __syncwarp();
     };
-    mbar_wait(bar_qk, 0);
-    tc_fence_after();
-    for (int t = 0; t < ntile; ++t) issue_s(t, 0);
-    for (int k = 0; k < nk; ++k) {
-      for (int t = 0; t < ntile; ++t) {
-        mbar_wait(bar_t + t, k & 1);
-        tc_fence_after();
-        if (k + 1 < nk) issue_s(t, k + 1);
-      }
-      if (k >= nt) {
-        const int j = k - nt;
-        if (j == 0) mbar_wait(bar_v, 0);
+    // running phase counters (barrier completions so far)
+    uint32_t n_qk = 0, n_v = 0, n_t0 = 0, n_t1 = 0, n_p0 = 0, n_p1 = 0, n_o0 = 0, n_o1 = 0;
+    if (lane == 0 && blockIdx.x < items) {
+      load_qk(blockIdx.x);
+      load_v(blockIdx.x);
+    }
+    for (int w = blockIdx.x; w < items; w += gridDim.x) {
+      int qp, h, b;
+      item(w, qp, h, b);
+      const int ntile = min(2, nt - 2 * qp);
+      const int wn = w + gridDim.x;  // the next item of this CTA
+      mbar_wait(bar_qk, n_qk++ & 1);
+      tc_fence_after();
+      for (int t = 0; t < ntile; ++t) issue_s(t, 0);
+      for (int k = 0; k < nk; ++k) {
         for (int t = 0; t < ntile; ++t) {
-          mbar_wait(bar_p + t, j & 1);
+          mbar_wait(bar_t + t, (t ? n_t1++ : n_t0++) & 1);
           tc_fence_after();
-          if (elect_one()) {
-            const uint32_t p0 = sP + t * 2 * TILE_BYTES;
+          if (k + 1 < nk) issue_s(t, k + 1);
+        }
+        // every S MMA of this item is done: Q and K may be refilled
+        if (k + 1 == nk && lane == 0 && wn < items) load_qk(wn);
+        if (k >= nt) {
+          const int j = k - nt;
+          if (j == 0) mbar_wait(bar_v, n_v++ & 1);
+          for (int t = 0; t < ntile; ++t) {
+            mbar_wait(bar_p + t, (t ? n_p1++ : n_p0++) & 1);
+            tc_fence_after();
+            if (elect_one()) {
+              const uint32_t p0 = sP + t * 2 * TILE_BYTES;
 #pragma unroll
-            for (int at = 0; at < 2; ++at) {
-              const uint64_t dp = umma_desc_sw128(p0 + at * TILE_BYTES);
+              for (int at = 0; at < 2; ++at) {
+                const uint64_t dp = umma_desc_sw128(p0 + at * TILE_BYTES);
 #pragma unroll
-              for (int kk = 0; kk < 4; ++kk)
-                umma_bf16(tmem + 256 + t * HD, dp + uint64_t(kk * 2),
-                          desc_mn(sV + j * TILE_BYTES + uint32_t(at * 64 + kk * 16) * 128, 0), idO,
-                          (j | at | kk) != 0);
+                for (int kk = 0; kk < 4; ++kk)
+                  umma_bf16(tmem + 256 + t * HD, dp + uint64_t(kk * 2),
+                            desc_mn(sV + j * TILE_BYTES + uint32_t(at * 64 + kk * 16) * 128, 0),
+                            idO, (j | at | kk) != 0);
+              }
+              umma_commit(bar_o + t);
             }
-            umma_commit(bar_o + t);
+            __syncwarp();
           }
-          __syncwarp();
         }
       }
+      // V is free once this item's last PV MMAs are done
+      if (wn < items) {
+        for (int t = 0; t < ntile; ++t) mbar_wait(bar_o + t, ((t ? n_o1 : n_o0) + nt - 1) & 1);
+        if (lane == 0) load_v(wn);
+        __syncwarp();
+      }
+      n_o0 += nt;
+      if (ntile > 1) n_o1 += nt;
     }
-  } else if (warp / F2_SW < ntile) {
-    const int t = warp / F2_SW, w = warp % F2_SW;
-    const int quarter = w & 3, half = w >> 2;
+  } else {
+    const int t = warp / F2_SW, w8 = warp % F2_SW;
+    const int quarter = w8 & 3, half = w8 >> 2;
     const int r = quarter * 32 + lane;
-    const int q = (2 * qp + t) * TILE + r;
     const uint32_t trow = tmem + (uint32_t(quarter * 32) << 16);
     const uint32_t tS = trow + t * TILE + half * 64;
     const uint64_t seed = a.rng[0], step = a.rng[1];
-    const uint64_t bh = uint64_t(b * a.heads + h);
-    // Philox block of keys [j*128 + half*64 + c*16, +16) of row q
-    const uint64_t g0 = ((bh * S + q) * uint64_t(S) + half * 64) >> 4;
-    // ---- pass 1: row max
-    float m = -INFINITY;
-#pragma unroll 1
-    for (int j = 0; j < nt; ++j) {
-      mbar_wait(bar_s + t, j & 1);
-      tc_fence_after();
-      uint32_t v[4][16];
-#pragma unroll
-      for (int c = 0; c < 4; ++c) tmem_ld16(tS + c * 16, v[c]);
-      tmem_wait();
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(bar_t + t);
-#pragma unroll
-      for (int c = 0; c < 4; ++c)
-#pragma unroll
-        for (int i = 0; i < 16; ++i) m = fmaxf(m, __uint_as_float(v[c][i]));
-    }
-    // the two half-warps of a row combine their maxima (P's buffer is free)
-    float* red = reinterpret_cast<float*>(smem + (sP - sQ) + t * 2 * TILE_BYTES);
-    red[half * TILE + r] = m;
-    bar_tile(t);
-    m = fmaxf(red[r], red[TILE + r]);
-    bar_tile(t);
-    const float mc = m * kCl2;
+    float* red = reinterpret_cast<float*>(smem + (sP - sQ) + t * 2 * TILE_BYTES);  // P's buffer
     const uint32_t pT = sP + t * 2 * TILE_BYTES;
-    // ---- pass 2: P = exp2(s*c - m*c) * keep into shared memory, O += P V_j
-    float l = 0.f;
+    uint32_t n_s = 0, n_o = 0;  // completions of bar_s[t], bar_o[t] seen so far
+    for (int w = blockIdx.x; w < items; w += gridDim.x) {
+      int qp, h, b;
+      item(w, qp, h, b);
+      if (t >= min(2, nt - 2 * qp)) continue;  // this item has one query tile
+      const int q = (2 * qp + t) * TILE + r;
+      const uint64_t bh = uint64_t(b * a.heads + h);
+      // Philox block of keys [j*128 + half*64 + c*16, +16) of row q
+      const uint64_t g0 = ((bh * S + q) * uint64_t(S) + half * 64) >> 4;
+      // ---- pass 1: row max
+      float m = -INFINITY;
 #pragma unroll 1
-    for (int j = 0; j < nt; ++j) {
-      mbar_wait(bar_s + t, (nt + j) & 1);
-      tc_fence_after();
-      uint32_t v[4][16];
+      for (int j = 0; j < nt; ++j) {
+        mbar_wait(bar_s + t, n_s++ & 1);
+        tc_fence_after();
+        uint32_t v[4][16];
 #pragma unroll
-      for (int c = 0; c < 4; ++c) tmem_ld16(tS + c * 16, v[c]);
+        for (int c = 0; c < 4; ++c) tmem_ld16(tS + c * 16, v[c]);
+        tmem_wait();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(bar_t + t);
+#pragma unroll
+        for (int c = 0; c < 4; ++c)
+#pragma unroll
+          for (int i = 0; i < 16; ++i) m = fmaxf(m, __uint_as_float(v[c][i]));
+      }
+      // the two half-warps of a row combine their maxima (P's buffer is free:
+      // the previous item's PV MMAs were waited for before its epilogue)
+      red[half * TILE + r] = m;
+      bar_tile(t);
+      m = fmaxf(red[r], red[TILE + r]);
+      bar_tile(t);
+      const float mc = m * kCl2;
+      // ---- pass 2: P = exp2(s*c - m*c) * keep into shared memory, O += P V_j
+      float l = 0.f;
+#pragma unroll 1
+      for (int j = 0; j < nt; ++j) {
+        mbar_wait(bar_s + t, n_s++ & 1);
+        tc_fence_after();
+        uint32_t v[4][16];
+#pragma unroll
+        for (int c = 0; c < 4; ++c) tmem_ld16(tS + c * 16, v[c]);
+        tmem_wait();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(bar_t + t);
+        uint32_t wv[4][8];
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          // keep bytes of these 16 keys (0xFF = kept): a pair's bf16x2 mask is
+          // one byte permute
+          const uint4 kb = keep_bytes(seed, step, a.tag, g0 + j * 8 + c, a.thr);
+#pragma unroll
+          for (int i = 0; i < 16; i += 2) {
+            const float p0 = ex2(fmaf(__uint_as_float(v[c][i]), kCl2, -mc));
+            const float p1 = ex2(fmaf(__uint_as_float(v[c][i + 1]), kCl2, -mc));
+            l += p0 + p1;
+            wv[c][i >> 1] = pack_bf16x2(p0, p1) & pair_mask((&kb.x)[i >> 2], (i >> 1) & 1);
+          }
+        }
+        // the previous chunk's PV MMAs have read P
+        if (j > 0) mbar_wait(bar_o + t, n_o++ & 1);
+#pragma unroll
+        for (int c = 0; c < 4; ++c) st_row16(pT, r, half * 64 + c * 16, wv[c]);
+        fence_proxy_async_smem();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(bar_p + t);
+      }
+      // the last PV MMAs (P's buffer is then free for the row sums)
+      mbar_wait(bar_o + t, n_o++ & 1);
+      tc_fence_after();
+      red[half * TILE + r] = l;
+      bar_tile(t);
+      l = red[r] + red[TILE + r];
+      bar_tile(t);
+      if (half == 0) a.lse[bh * S + q] = mc + __log2f(l);
+      const float inv = a.dscale / l;
+      // ---- epilogue: O columns [half*32, half*32 + 32) of row r
+      uint32_t o0[16], o1[16];
+      tmem_ld16(trow + 256 + t * HD + half * 32, o0);
+      tmem_ld16(trow + 256 + t * HD + half * 32 + 16, o1);
       tmem_wait();
       tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(bar_t + t);
-      uint32_t wv[4][8];
-#pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        // keep bytes of these 16 keys (0xFF = kept): a pair's bf16x2 mask is
-        // one byte permute
-        const uint4 kb = keep_bytes(seed, step, a.tag, g0 + j * 8 + c, a.thr);
-#pragma unroll
-        for (int i = 0; i < 16; i += 2) {
-          const float p0 = ex2(fmaf(__uint_as_float(v[c][i]), kCl2, -mc));
-          const float p1 = ex2(fmaf(__uint_as_float(v[c][i + 1]), kCl2, -mc));
-          l += p0 + p1;
-          wv[c][i >> 1] = pack_bf16x2(p0, p1) & pair_mask((&kb.x)[i >> 2], (i >> 1) & 1);
-        }
-      }
-      // the previous chunk's PV MMAs have read P
-      if (j > 0) mbar_wait(bar_o + t, (j - 1) & 1);
-#pragma unroll
-      for (int c = 0; c < 4; ++c) st_row16(pT, r, half * 64 + c * 16, wv[c]);
-      fence_proxy_async_smem();
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(bar_p + t);
+      bf16* dst = a.out + (int64_t(b) * S + q) * a.Hd + h * HD + half * 32;
+      store16(dst, o0, inv);
+      store16(dst + 16, o1, inv);
     }
-    // row sum: the tile's Q buffer is free (its last S MMA has completed)
-    float* red2 = reinterpret_cast<float*>(smem + t * TILE_BYTES);
-    red2[half * TILE + r] = l;
-    bar_tile(t);
-    l = red2[r] + red2[TILE + r];
-    if (half == 0) a.lse[bh * S + q] = mc + __log2f(l);
-    const float inv = a.dscale / l;
-    // ---- epilogue: O columns [half*32, half*32 + 32) of row r
-    mbar_wait(bar_o + t, (nt - 1) & 1);
-    tc_fence_after();
-    uint32_t o0[16], o1[16];
-    tmem_ld16(trow + 256 + t * HD + half * 32, o0);
-    tmem_ld16(trow + 256 + t * HD + half * 32 + 16, o1);
-    tmem_wait();
-    bf16* dst = a.out + (int64_t(row0) + q) * a.Hd + h * HD + half * 32;
-    store16(dst, o0, inv);
-    store16(dst + 16, o1, inv);
   }
   tc_fence_before();
   __syncthreads();
@@ -684,6 +728,17 @@ bool shape_ok(int S, int heads) { return S > 0 && S % TILE == 0 && S <= 512 && h
 
 }  // namespace
 
+static int attn_sms() {
+  static int n = 0;
+  if (!n) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (n <= 0) n = 148;
+  }
+  return n;
+}
+
 // Q (2 tiles) + P (2 tiles x 2 atoms) + K + V + barriers
 static size_t fwd2_smem(int S) {
   return 1024 + 6 * size_t(TILE_BYTES) + 2 * size_t(S) * 128 + 128;
@@ -706,8 +761,8 @@ cudaError_t attention_fwd(const void* qkv, void* out, float* lse, int B, int S, 
       return e;
     attr = true;
   }
-  const int nt = S / TILE;
-  if (cudaError_t e = launch_k(k_attn_fwd2, dim3((nt + 1) / 2, heads, B), dim3(kThreadsF2),
+  const int items = (S / TILE + 1) / 2 * heads * B;
+  if (cudaError_t e = launch_k(k_attn_fwd2, dim3(items < attn_sms() ? items : attn_sms()), dim3(kThreadsF2),
                                fwd2_smem(S), st, qm, a))
     return e;
   return cudaGetLastError();
