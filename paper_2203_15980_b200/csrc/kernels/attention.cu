@@ -388,24 +388,24 @@ __global__ void __launch_bounds__(kThreadsF2, 1)
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(bar_t + t);
-        uint32_t wv[4][8];
+        // the previous chunk's PV MMAs have read P (each 16-key block is
+        // stored as soon as it is formed: no second 32-register copy of P)
+        if (j > 0) mbar_wait(bar_o + t, n_o++ & 1);
 #pragma unroll
         for (int c = 0; c < 4; ++c) {
           // keep bytes of these 16 keys (0xFF = kept): a pair's bf16x2 mask is
           // one byte permute
           const uint4 kb = keep_bytes(seed, step, a.tag, g0 + j * 8 + c, a.thr);
+          uint32_t wv[8];
 #pragma unroll
           for (int i = 0; i < 16; i += 2) {
             const float p0 = ex2(fmaf(__uint_as_float(v[c][i]), kCl2, -mc));
             const float p1 = ex2(fmaf(__uint_as_float(v[c][i + 1]), kCl2, -mc));
             l += p0 + p1;
-            wv[c][i >> 1] = pack_bf16x2(p0, p1) & pair_mask((&kb.x)[i >> 2], (i >> 1) & 1);
+            wv[i >> 1] = pack_bf16x2(p0, p1) & pair_mask((&kb.x)[i >> 2], (i >> 1) & 1);
           }
+          st_row16(pT, r, half * 64 + c * 16, wv);
         }
-        // the previous chunk's PV MMAs have read P
-        if (j > 0) mbar_wait(bar_o + t, n_o++ & 1);
-#pragma unroll
-        for (int c = 0; c < 4; ++c) st_row16(pT, r, half * 64 + c * 16, wv[c]);
         fence_proxy_async_smem();
         tc_fence_before();
         __syncwarp();
