@@ -518,8 +518,18 @@ __global__ void __launch_bounds__(256)
     const int k = int(e / ntot);
     const int tile = (n / BN) * tiles_m + k / TM;
     const size_t off = (size_t(tile) * TM + (k % TM)) * BN + (n % BN);
+    const size_t stride = size_t(tiles) * TM * BN;
     float s = 0.f;
-    for (int sp = 0; sp < splits; ++sp) s += ws[size_t(sp) * tiles * TM * BN + off];
+    int sp = 0;
+    for (; sp + 3 < splits; sp += 4) {  // four loads in flight, same summation order
+      const float a0 = ws[size_t(sp) * stride + off], a1 = ws[size_t(sp + 1) * stride + off];
+      const float a2 = ws[size_t(sp + 2) * stride + off], a3 = ws[size_t(sp + 3) * stride + off];
+      s += a0;
+      s += a1;
+      s += a2;
+      s += a3;
+    }
+    for (; sp < splits; ++sp) s += ws[size_t(sp) * stride + off];
     dw[e] = s;
   }
 }

@@ -398,8 +398,19 @@ __global__ void __launch_bounds__(256)
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int c = blockIdx.x * 32 + lane;
   float s = 0.f;
-  if (c < cols)
-    for (int p = w; p < parts; p += 8) s += ws[int64_t(p) * pstride + c];
+  if (c < cols) {
+    // four loads in flight, summed in the same order as one at a time
+    int p = w;
+    for (; p + 24 < parts; p += 32) {
+      const float a0 = ws[int64_t(p) * pstride + c], a1 = ws[int64_t(p + 8) * pstride + c];
+      const float a2 = ws[int64_t(p + 16) * pstride + c], a3 = ws[int64_t(p + 24) * pstride + c];
+      s += a0;
+      s += a1;
+      s += a2;
+      s += a3;
+    }
+    for (; p < parts; p += 8) s += ws[int64_t(p) * pstride + c];
+  }
   red[w][lane] = s;
   __syncthreads();
   if (w == 0 && c < cols) {
