@@ -34,7 +34,8 @@ def resident_workspace_bytes(g: G.Graph, batch: int) -> int:
 
 
 def transient_workspace_bytes(g: G.Graph, batch: int) -> int:
-    """cuDNN input-gradient outputs alive at once inside one backward node."""
+    """the stride-2 3x3 input-gradient scratch alive inside one backward node
+    (runtime.workspace_plan's 'transient')."""
     from .runtime import workspace_plan
     return workspace_plan(g)["transient"]
 
