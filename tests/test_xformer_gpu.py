@@ -39,9 +39,9 @@ def rnd(*shape, scale=1.0, seed=0):
     return (torch.randn(*shape, device=dev, generator=g) * scale).to(torch.bfloat16)
 
 
-@pytest.mark.parametrize("H", [256, 1024])
-def test_layernorm_fwd_bwd(H):
-    rows = 1000
+@pytest.mark.parametrize("H,rows", [(256, 1000), (1024, 1000), (1024, 16384)])
+def test_layernorm_fwd_bwd(H, rows):
+    # 16384 rows: every warp walks several staged rows (stage refills)
     x = rnd(rows, H, scale=2.0)
     gamma = torch.rand(H, device=dev) + 0.5
     beta = torch.randn(H, device=dev) * 0.1
@@ -241,7 +241,11 @@ def _attn_inputs(B, S, heads, seed=0):
 
 
 @pytest.mark.parametrize("B,S,heads,p", [(2, 512, 4, 0.0), (2, 256, 3, 0.0), (1, 128, 2, 0.0),
-                                         (2, 512, 2, 0.1), (3, 384, 2, 0.1)])
+                                         (2, 512, 2, 0.1), (3, 384, 2, 0.1),
+                                         # more work items than SMs: the persistent forward
+                                         # walks several per CTA (next item prefetched),
+                                         # incl. one-tile items (S = 384)
+                                         (8, 512, 16, 0.1), (20, 384, 16, 0.1)])
 def test_attention_forward_backward(B, S, heads, p):
     Hd = heads * 64
     qkv = _attn_inputs(B, S, heads)
