@@ -95,6 +95,18 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]) {
 __device__ __forceinline__ void tmem_wait() {
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
+// tcgen05.st of 16 consecutive fp32 columns of this warp's 32 lanes
+__device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t (&r)[16]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], "
+      "{%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(taddr),
+      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]),
+      "r"(r[8]), "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15])
+      : "memory");
+}
+__device__ __forceinline__ void tmem_wait_st() {
+  asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+}
 
 // keep masks of one Philox block (16 elements): byte i of v[w] = 0xFF iff
 // element 4w + i is kept (all kept when thr == 0)
@@ -179,19 +191,22 @@ struct AttnArgs {
 };
 
 // ======================================================================= fwd
-// Two query tiles per CTA (grid ceil(S/256) x heads x B), K and V of the
-// (sequence, head) resident in shared memory, 8 softmax warps per tile (two
-// per TMEM lane quarter, 64 keys of a 128-key chunk each).  TMEM: S of each
-// tile's current key chunk (128 columns each) and the two O accumulators.
-// The scores are computed twice (S_j = Q K_j^T per chunk, twice): pass 1
-// takes the row max, pass 2 forms P = exp2(s*c - m*c) * keep into shared
-// memory and accumulates O += P V_j — the tensor cores have the capacity, and
-// no online rescaling is needed.  The one MMA warp alternates between the two
-// tiles, so one tile's MMAs run under the other tile's softmax, and the
-// prologue / epilogue of the CTA is shared by two tiles.
+// Persistent (one CTA per SM walking (query-tile pair, head, sequence) items;
+// the next item's Q/K load under the current item's last chunk, V under its
+// epilogue); two 128-row query tiles per CTA, K and V of the (sequence, head)
+// resident.  Per tile and 128-key chunk j: S_j = Q K_j^T in TMEM (128
+// columns); 8 softmax warps per tile, two per TMEM lane quarter, each owning
+// one 64-key half of every chunk.  Single pass, online softmax per half: a
+// warp keeps its own running max m_h and row sum l_h and accumulates its own
+// O_h += P_h V_h (two O accumulators per tile, 64 columns each) — no exchange
+// between the halves until the end, where O = O_0 2^(m_0-m) + O_1 2^(m_1-m).
+// A half's running max is only raised when a chunk exceeds it by more than
+// 2^8 (P <= 256 otherwise, harmless in bf16 / fp32), so the O_h rescale
+// (TMEM load, scale, store) is rare.  The one MMA warp alternates the tiles.
 constexpr int F2_SW = 8;                       // softmax warps per query tile
 constexpr int F2_CTRL = 2 * F2_SW;             // TMA + MMA warp
 constexpr int kThreadsF2 = (F2_CTRL + 1) * 32;
+constexpr float kRescale = 8.f;                // log2 headroom before a rescale
 
 __device__ __forceinline__ void bar_tile(int t) {
   asm volatile("bar.sync %0, %1;" ::"r"(2 + t), "n"(F2_SW * 32) : "memory");
@@ -205,17 +220,17 @@ __global__ void __launch_bounds__(kThreadsF2, 1)
   const uint32_t sQ = smem_u32(smem);               // [2 tiles][128][64]
   const uint32_t sK = sQ + 2 * TILE_BYTES;          // [nt][128 keys][64]
   const uint32_t sV = sK + uint32_t(nt) * TILE_BYTES;
-  const uint32_t sP = sV + uint32_t(nt) * TILE_BYTES;  // [2 tiles][2 atoms][128][64 keys]
+  const uint32_t sP = sV + uint32_t(nt) * TILE_BYTES;  // [2 tiles][2 halves][128][64 keys]
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + (sP - sQ) + 4 * TILE_BYTES);
   uint64_t* bar_qk = bars;       // Q tiles and K landed
   uint64_t* bar_v = bars + 1;    // V landed
   uint64_t* bar_s = bars + 2;    // [2] S of a tile computed
   uint64_t* bar_t = bars + 4;    // [2] S of a tile read out of TMEM
-  uint64_t* bar_p = bars + 6;    // [2] P of a tile written
+  uint64_t* bar_p = bars + 6;    // [2] P of a tile written (and O_h rescaled)
   uint64_t* bar_o = bars + 8;    // [2] a tile's PV MMAs done
   uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 10);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  // persistent: work item w = (query-tile pair, head, sequence), qp fastest
+  // TMEM: S of tile t at columns 128 t; O_h of tile t at 256 + 128 t + 64 h
   const int nqp = (nt + 1) / 2;
   const int items = nqp * a.heads * a.B;
   auto item = [&](int w, int& qp, int& h, int& b) {
@@ -243,13 +258,10 @@ __global__ void __launch_bounds__(kThreadsF2, 1)
   const uint32_t tmem = *tslot;
   pdl_wait();
   pdl_trigger();
-  const int nk = 2 * nt;  // S steps per item: nt of pass 1 (max), nt of pass 2 (P, O)
 
   if (warp == F2_CTRL) {
     constexpr uint32_t idS = umma_idesc_bf16(128, 128);
     constexpr uint32_t idO = umma_idesc_bf16(128, HD) | (1u << 16);  // B (V) MN-major
-    // the next item's Q and K (once this item's last S MMAs are done), V (once
-    // its last PV MMAs are done) are loaded under this item's tail
     auto load_qk = [&](int w) {
       int qp, h, b;
       item(w, qp, h, b);
@@ -270,7 +282,7 @@ __global__ void __launch_bounds__(kThreadsF2, 1)
     auto issue_s = [&](int t, int k) {
       if (elect_one()) {
         const uint64_t dq = umma_desc_sw128(sQ + t * TILE_BYTES);
-        const uint64_t dk = umma_desc_sw128(sK + (k % nt) * TILE_BYTES);
+        const uint64_t dk = umma_desc_sw128(sK + k * TILE_BYTES);
 #pragma unroll
         for (int kk = 0; kk < HD / 16; ++kk)
           umma_bf16(tmem + t * TILE, dq + uint64_t(kk * 2), dk + uint64_t(kk * 2), idS, kk > 0);
@@ -278,7 +290,6 @@ __global__ void __launch_bounds__(kThreadsF2, 1)
       }
       __syncwarp();
     };
-    // running phase counters (barrier completions so far)
     uint32_t n_qk = 0, n_v = 0, n_t0 = 0, n_t1 = 0, n_p0 = 0, n_p1 = 0, n_o0 = 0, n_o1 = 0;
     if (lane == 0 && blockIdx.x < items) {
       load_qk(blockIdx.x);
@@ -292,35 +303,32 @@ __global__ void __launch_bounds__(kThreadsF2, 1)
       mbar_wait(bar_qk, n_qk++ & 1);
       tc_fence_after();
       for (int t = 0; t < ntile; ++t) issue_s(t, 0);
-      for (int k = 0; k < nk; ++k) {
+      for (int k = 0; k < nt; ++k) {
         for (int t = 0; t < ntile; ++t) {
           mbar_wait(bar_t + t, (t ? n_t1++ : n_t0++) & 1);
           tc_fence_after();
-          if (k + 1 < nk) issue_s(t, k + 1);
+          if (k + 1 < nt) issue_s(t, k + 1);
         }
         // every S MMA of this item is done: Q and K may be refilled
-        if (k + 1 == nk && lane == 0 && wn < items) load_qk(wn);
-        if (k >= nt) {
-          const int j = k - nt;
-          if (j == 0) mbar_wait(bar_v, n_v++ & 1);
-          for (int t = 0; t < ntile; ++t) {
-            mbar_wait(bar_p + t, (t ? n_p1++ : n_p0++) & 1);
-            tc_fence_after();
-            if (elect_one()) {
-              const uint32_t p0 = sP + t * 2 * TILE_BYTES;
+        if (k + 1 == nt && lane == 0 && wn < items) load_qk(wn);
+        if (k == 0) mbar_wait(bar_v, n_v++ & 1);
+        for (int t = 0; t < ntile; ++t) {
+          mbar_wait(bar_p + t, (t ? n_p1++ : n_p0++) & 1);
+          tc_fence_after();
+          if (elect_one()) {
+            // O_h += P_h V_h: half h = keys [64 h, 64 h + 64) of chunk k
 #pragma unroll
-              for (int at = 0; at < 2; ++at) {
-                const uint64_t dp = umma_desc_sw128(p0 + at * TILE_BYTES);
+            for (int hf = 0; hf < 2; ++hf) {
+              const uint64_t dp = umma_desc_sw128(sP + (t * 2 + hf) * TILE_BYTES);
 #pragma unroll
-                for (int kk = 0; kk < 4; ++kk)
-                  umma_bf16(tmem + 256 + t * HD, dp + uint64_t(kk * 2),
-                            desc_mn(sV + j * TILE_BYTES + uint32_t(at * 64 + kk * 16) * 128, 0),
-                            idO, (j | at | kk) != 0);
-              }
-              umma_commit(bar_o + t);
+              for (int kk = 0; kk < 4; ++kk)
+                umma_bf16(tmem + 256 + t * 128 + hf * HD, dp + uint64_t(kk * 2),
+                          desc_mn(sV + k * TILE_BYTES + uint32_t(hf * 64 + kk * 16) * 128, 0),
+                          idO, (k | kk) != 0);
             }
-            __syncwarp();
+            umma_commit(bar_o + t);
           }
+          __syncwarp();
         }
       }
       // V is free once this item's last PV MMAs are done
@@ -338,9 +346,10 @@ __global__ void __launch_bounds__(kThreadsF2, 1)
     const int r = quarter * 32 + lane;
     const uint32_t trow = tmem + (uint32_t(quarter * 32) << 16);
     const uint32_t tS = trow + t * TILE + half * 64;
+    const uint32_t tOh = trow + 256 + t * 128 + half * HD;  // this warp's O_h rows
     const uint64_t seed = a.rng[0], step = a.rng[1];
     float* red = reinterpret_cast<float*>(smem + (sP - sQ) + t * 2 * TILE_BYTES);  // P's buffer
-    const uint32_t pT = sP + t * 2 * TILE_BYTES;
+    const uint32_t pT = sP + (t * 2 + half) * TILE_BYTES;  // this half's P atom
     uint32_t n_s = 0, n_o = 0;  // completions of bar_s[t], bar_o[t] seen so far
     for (int w = blockIdx.x; w < items; w += gridDim.x) {
       int qp, h, b;
@@ -350,8 +359,7 @@ __global__ void __launch_bounds__(kThreadsF2, 1)
       const uint64_t bh = uint64_t(b * a.heads + h);
       // Philox block of keys [j*128 + half*64 + c*16, +16) of row q
       const uint64_t g0 = ((bh * S + q) * uint64_t(S) + half * 64) >> 4;
-      // ---- pass 1: row max
-      float m = -INFINITY;
+      float mc = 0.f, l = 0.f;  // running max (scaled, log2 units) and row sum of this half
 #pragma unroll 1
       for (int j = 0; j < nt; ++j) {
         mbar_wait(bar_s + t, n_s++ & 1);
@@ -363,40 +371,25 @@ __global__ void __launch_bounds__(kThreadsF2, 1)
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(bar_t + t);
+        float m = -INFINITY;
 #pragma unroll
         for (int c = 0; c < 4; ++c)
 #pragma unroll
           for (int i = 0; i < 16; ++i) m = fmaxf(m, __uint_as_float(v[c][i]));
-      }
-      // the two half-warps of a row combine their maxima (P's buffer is free:
-      // the previous item's PV MMAs were waited for before its epilogue)
-      red[half * TILE + r] = m;
-      bar_tile(t);
-      m = fmaxf(red[r], red[TILE + r]);
-      bar_tile(t);
-      const float mc = m * kCl2;
-      // ---- pass 2: P = exp2(s*c - m*c) * keep into shared memory, O += P V_j
-      float l = 0.f;
-#pragma unroll 1
-      for (int j = 0; j < nt; ++j) {
-        mbar_wait(bar_s + t, n_s++ & 1);
-        tc_fence_after();
-        uint32_t v[4][16];
-#pragma unroll
-        for (int c = 0; c < 4; ++c) tmem_ld16(tS + c * 16, v[c]);
-        tmem_wait();
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(bar_t + t);
-        // the previous chunk's PV MMAs have read P (each 16-key block is
-        // stored as soon as it is formed: no second 32-register copy of P)
-        if (j > 0) mbar_wait(bar_o + t, n_o++ & 1);
-#pragma unroll
-        for (int c = 0; c < 4; ++c) {
-          // keep bytes of these 16 keys (0xFF = kept): a pair's bf16x2 mask is
-          // one byte permute
+        const float mj = m * kCl2;
+        // raise the running max only past the headroom (rare after chunk 0)
+        float f = 1.f;
+        if (j == 0) {
+          mc = mj;
+        } else if (mj > mc + kRescale) {
+          f = ex2(mc - mj);
+          l *= f;
+          mc = mj;
+        }
+        // P = exp2(s*c - mc) * keep: the first two 16-key blocks before waiting
+        // for the previous chunk's PV MMAs (which run meanwhile), the rest after
+        auto form = [&](int c, uint32_t* wv) {
           const uint4 kb = keep_bytes(seed, step, a.tag, g0 + j * 8 + c, a.thr);
-          uint32_t wv[8];
 #pragma unroll
           for (int i = 0; i < 16; i += 2) {
             const float p0 = ex2(fmaf(__uint_as_float(v[c][i]), kCl2, -mc));
@@ -404,31 +397,70 @@ __global__ void __launch_bounds__(kThreadsF2, 1)
             l += p0 + p1;
             wv[i >> 1] = pack_bf16x2(p0, p1) & pair_mask((&kb.x)[i >> 2], (i >> 1) & 1);
           }
-          st_row16(pT, r, half * 64 + c * 16, wv);
+        };
+        uint32_t w0[8], w1[8];
+        form(0, w0);
+        form(1, w1);
+        // the previous chunk's PV MMAs have read P and updated O_h
+        if (j > 0) {
+          mbar_wait(bar_o + t, n_o++ & 1);
+          if (__any_sync(0xFFFFFFFFu, f != 1.f)) {
+            // rare: this half's O (accumulated at the old max) scaled down
+            tc_fence_after();
+#pragma unroll 1
+            for (int c = 0; c < 4; ++c) {
+              uint32_t o[16];
+              tmem_ld16(tOh + c * 16, o);
+              tmem_wait();
+#pragma unroll
+              for (int i = 0; i < 16; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * f);
+              tmem_st16(tOh + c * 16, o);
+            }
+            tmem_wait_st();
+          }
         }
+        st_row16(pT, r, 0, w0);
+        st_row16(pT, r, 16, w1);
+        form(2, w0);
+        st_row16(pT, r, 32, w0);
+        form(3, w1);
+        st_row16(pT, r, 48, w1);
         fence_proxy_async_smem();
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(bar_p + t);
       }
-      // the last PV MMAs (P's buffer is then free for the row sums)
+      // the last PV MMAs: P's buffer is then free for the halves' exchange
       mbar_wait(bar_o + t, n_o++ & 1);
       tc_fence_after();
-      red[half * TILE + r] = l;
+      red[half * TILE + r] = mc;
+      red[2 * TILE + half * TILE + r] = l;
       bar_tile(t);
-      l = red[r] + red[TILE + r];
+      const float m0 = red[r], m1 = red[TILE + r];
+      const float l0 = red[2 * TILE + r], l1 = red[3 * TILE + r];
       bar_tile(t);
-      if (half == 0) a.lse[bh * S + q] = mc + __log2f(l);
-      const float inv = a.dscale / l;
-      // ---- epilogue: O columns [half*32, half*32 + 32) of row r
-      uint32_t o0[16], o1[16];
-      tmem_ld16(trow + 256 + t * HD + half * 32, o0);
-      tmem_ld16(trow + 256 + t * HD + half * 32 + 16, o1);
+      const float mrow = fmaxf(m0, m1);
+      const float f0 = ex2(m0 - mrow), f1 = ex2(m1 - mrow);
+      const float lrow = fmaf(l0, f0, l1 * f1);
+      if (half == 0) a.lse[bh * S + q] = mrow + __log2f(lrow);
+      const float inv = a.dscale / lrow;
+      // ---- epilogue: O columns [half*32, half*32 + 32) of row r from both halves' O
+      uint32_t x0[16], x1[16], y0[16], y1[16];
+      tmem_ld16(trow + 256 + t * 128 + half * 32, x0);
+      tmem_ld16(trow + 256 + t * 128 + half * 32 + 16, x1);
+      tmem_ld16(trow + 256 + t * 128 + HD + half * 32, y0);
+      tmem_ld16(trow + 256 + t * 128 + HD + half * 32 + 16, y1);
       tmem_wait();
       tc_fence_before();
+      const float g0f = f0 * inv, g1f = f1 * inv;
+#pragma unroll
+      for (int i = 0; i < 16; ++i) {
+        x0[i] = __float_as_uint(fmaf(__uint_as_float(x0[i]), g0f, __uint_as_float(y0[i]) * g1f));
+        x1[i] = __float_as_uint(fmaf(__uint_as_float(x1[i]), g0f, __uint_as_float(y1[i]) * g1f));
+      }
       bf16* dst = a.out + (int64_t(b) * S + q) * a.Hd + h * HD + half * 32;
-      store16(dst, o0, inv);
-      store16(dst + 16, o1, inv);
+      store16(dst, x0, 1.f);
+      store16(dst + 16, x1, 1.f);
     }
   }
   tc_fence_before();
