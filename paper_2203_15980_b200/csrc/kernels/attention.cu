@@ -4,19 +4,22 @@
 // (philox.cuh), so a recomputed Attention output is bit-identical.
 //
 // BERT shapes: head dim 64, sequence S <= 512 (a multiple of 128); all keys
-// of a (sequence, head) stay on chip, so there is no online-softmax
-// rescaling and no atomics anywhere (deterministic gradients).
+// of a (sequence, head) stay on chip; no atomics anywhere (deterministic
+// gradients).
 //
-// forward (grid S/256 x heads x B, two 128-row query tiles per CTA, K and V
-//   of the sequence resident): per tile and 128-key chunk j, S_j = Q K_j^T in
-//   TMEM (128 columns per tile); 8 softmax warps per tile (two per TMEM lane
-//   quarter, 64 keys each).  Pass 1 takes the row max over all chunks, pass 2
-//   recomputes S_j (the tensor cores have the capacity) and writes
-//   P = exp2(s*c - m*c) * keep (bf16, unnormalised) to shared memory in the
-//   K-major SW128 layout, O += P V_j (V as an MN-major B operand) accumulating
-//   in TMEM; O is scaled by dropout_scale / rowsum on the way out, lse (log2
-//   units) saved.  One MMA warp alternates between the tiles, so each tile's
-//   MMAs run under the other's softmax.
+// forward (persistent, one CTA per SM walking (query-tile pair, head,
+//   sequence) items, the next item's loads under the current one's tail; two
+//   128-row query tiles per CTA, K and V of the sequence resident): per tile
+//   and 128-key chunk j, S_j = Q K_j^T in TMEM (128 columns per tile); 8
+//   softmax warps per tile, two per TMEM lane quarter, each owning one 64-key
+//   half of every chunk with its own running max, row sum and accumulator
+//   O_h += P_h V_h (single-pass online softmax; the max is raised, and O_h
+//   rescaled in TMEM, only past 2^8 of headroom).  P = exp2(s*c - m*c) * keep
+//   (bf16, unnormalised) goes to shared memory in the K-major SW128 layout, V
+//   is an MN-major B operand; at the end the halves combine,
+//   O = (O_0 2^(m_0-m) + O_1 2^(m_1-m)) * dropout_scale / rowsum, and lse (log2
+//   units) is saved.  One MMA warp alternates between the tiles, so each
+//   tile's MMAs run under the other's softmax.
 // backward (grid heads x B, one CTA per (sequence, head)): for every key
 //   block j (128 keys, K_j / V_j loaded by TMA) and query block i
 //   (Q, dO of the whole sequence resident): S_ij = Q_i K_j^T and
