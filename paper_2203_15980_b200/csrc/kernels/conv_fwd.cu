@@ -29,6 +29,7 @@
 // tcgen05.commit releases a stage the moment the tensor core has consumed it.
 #include <cuda.h>
 #include <cuda_bf16.h>
+#include <cuda_fp16.h>
 #include <cuda_runtime.h>
 #include <cudaTypedefs.h>
 
@@ -227,7 +228,13 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* bfull = tempty + 2;      // MODE_STEMRAW: resident weights landed
   uint64_t* ofull = bfull + 1;       // OPT: epilogue operand tile landed [OPT_NB]
   uint64_t* oempty = ofull + OPT_NB; // OPT: ... and consumed [OPT_NB]
-  uint32_t* tslot = reinterpret_cast<uint32_t*>(oempty + OPT_NB);
+  uint64_t* otrans = oempty + OPT_NB; // XFORM: ... and transformed [OPT_NB]
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(otrans + OPT_NB);
+  // EV_GELU_BWD: producer warps 1-3 (idle in the TMA mode; warp 0 then also
+  // loads the operand tiles) turn each landed pre-activation tile into
+  // gelu'(pre) in place (fp16), so the epilogue's per-element work is one
+  // multiply
+  constexpr bool XFORM = EV == EV_GELU_BWD && OPT;
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -252,6 +259,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int i = 0; i < OPT_NB; ++i) {
       mbar_init(&ofull[i], 1);
       mbar_init(&oempty[i], EPI_W);
+      mbar_init(&otrans[i], 3);
     }
     fence_mbar_init();
     if (OPT) {
@@ -292,7 +300,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp < 4) {
     // ============================ producers ============================
     const int tid = threadIdx.x;
-    if (OPT && warp == 1) {
+    if (OPT && !XFORM && warp == 1) {
       if constexpr (OPT) {
         // epilogue operands of every tile of this CTA, two tiles ahead
         if (lane == 0) {
@@ -313,6 +321,32 @@ __global__ void __launch_bounds__(kThreads, 1)
                 tma_load_2d(base + 2 * BN * 256 + j * 8192, &emap2, &ofull[b], n0 + j * 32, m0);
             }
           }
+        }
+      }
+    } else if (XFORM && warp >= 1) {
+      if constexpr (XFORM) {
+        // gelu'(pre) of every operand tile, in place, as fp16 pairs
+        const int t2 = threadIdx.x - 32;
+        uint32_t lt = 0;
+        for (int tile = unit; tile < a.tiles; tile += units, ++lt) {
+          const uint32_t b = lt % OPT_NB;
+          mbar_wait(&ofull[b], (lt / OPT_NB) & 1);
+          uint4* buf = reinterpret_cast<uint4*>(smem + (sIn - sA) + b * OPT_TILE);
+#pragma unroll 2
+          for (int i = t2; i < int(OPT_TILE / 16); i += 96) {
+            float f[8];
+            unpack8f(buf[i], f);
+            uint32_t o[4];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+              const __half2 hv = __floats2half2_rn(gelu_grad1(f[2 * k]), gelu_grad1(f[2 * k + 1]));
+              o[k] = *reinterpret_cast<const uint32_t*>(&hv);
+            }
+            buf[i] = make_uint4(o[0], o[1], o[2], o[3]);
+          }
+          fence_proxy_async_smem();  // before the buffer's next TMA refill
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&otrans[b]);
         }
       }
     } else {
@@ -403,6 +437,16 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
       } else if constexpr (MODE == MODE_TMA) {
         if (tid == 0) {
+          if constexpr (XFORM) {
+            // this tile's epilogue operand (two tiles of buffering)
+            const uint32_t lt = it / uint32_t(a.kblocks);  // tiles issued so far
+            const uint32_t b = lt % OPT_NB;
+            if (lt >= OPT_NB) mbar_wait(&oempty[b], ((lt / OPT_NB) - 1) & 1);
+            mbar_arrive_expect_tx(&ofull[b], OPT_TILE);
+#pragma unroll
+            for (int j = 0; j < BN / 32; ++j)
+              tma_load_2d(sIn + b * OPT_TILE + j * 8192, &emap0, &ofull[b], n0 + j * 32, m0);
+          }
           for (int kb = 0; kb < a.kblocks; ++kb, ++it) {
             const uint32_t s = it % STAGES;
             if (it >= STAGES) mbar_wait(&empty[s], ((it / STAGES) - 1) & 1);
@@ -651,7 +695,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_wait(&tfull[acc], (lt >> 1) & 1);
       tc_fence_after();
       const uint32_t obuf = sIn + (lt % OPT_NB) * OPT_TILE;
-      if constexpr (FUSED && OPT) mbar_wait(&ofull[lt % OPT_NB], (lt / OPT_NB) & 1);
+      if constexpr (FUSED && OPT)
+        mbar_wait(XFORM ? &otrans[lt % OPT_NB] : &ofull[lt % OPT_NB], (lt / OPT_NB) & 1);
       // TMA-store staging: 16 KB over the epilogue warps, NBUF 2 KB buffers each
       constexpr int NBUF = 16384 / EPI_W / 2048;
       const uint32_t stage_base = sOut + (warp - 4) * (NBUF * 2048);
@@ -689,13 +734,18 @@ __global__ void __launch_bounds__(kThreads, 1)
           for (int i = 0; i < 32; ++i) v[i] += __shfl_sync(0xFFFFFFFFu, bl, i);
         }
         if constexpr (EV == EV_GELU_BWD) {
-          // d(pre-activation) = d(gelu output) * gelu'(pre-activation), fp32
+          // d(pre-activation) = d(gelu output) * gelu'(pre-activation), fp32;
+          // gelu' already formed (fp16) by the transform warps
 #pragma unroll
           for (int u = 0; u < 4; ++u) {
-            float hx[8];
-            unpack8f(ld_row16(sb, lane, u), hx);
+            const uint4 q = ld_row16(sb, lane, u);
+            const __half2* hq = reinterpret_cast<const __half2*>(&q);
 #pragma unroll
-            for (int i = 0; i < 8; ++i) v[u * 8 + i] *= gelu_grad1(hx[i]);
+            for (int k = 0; k < 4; ++k) {
+              const float2 g = __half22float2(hq[k]);
+              v[u * 8 + 2 * k] *= g.x;
+              v[u * 8 + 2 * k + 1] *= g.y;
+            }
           }
         }
         if constexpr (row_tiled(MODE)) {
