@@ -39,23 +39,11 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 
-// ---- warp column sums of a [32 rows = lanes][32 columns] block: lane c
-// returns column c's sum (recursive halving: 31 shuffles, a fixed combination
+// ---- warp column sums of a [32 rows = lanes][32 bf16 columns] block: lane c
+// returns column c's sum (recursive halving: 23 shuffles, a fixed combination
 // order, so deterministic) ----
-__device__ __forceinline__ float warp_colsum32(float (&v)[32], int lane) {
-#pragma unroll
-  for (int o = 16; o >= 1; o >>= 1) {
-    const bool up = lane & o;
-#pragma unroll
-    for (int k = 0; k < o; ++k) {
-      const float got = __shfl_xor_sync(0xffffffffu, up ? v[k] : v[k + o], o);
-      v[k] = (up ? v[k + o] : v[k]) + got;
-    }
-  }
-  return v[0];
-}
-// ... of bf16 values packed two per word (word w = columns 2w, 2w+1): the first
-// halving step exchanges packed words, the rest runs in fp32
+// values packed two per word (word w = columns 2w, 2w+1): the first halving
+// step exchanges packed words, the rest runs in fp32
 __device__ __forceinline__ float warp_colsum32_bf16(const uint32_t (&w)[16], int lane) {
   const bool up = lane & 16;
   float v[32];
