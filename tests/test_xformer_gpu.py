@@ -156,13 +156,16 @@ def test_linear_bias_epilogue(shape):
     close(y, x.float() @ w.float().t() + b)
 
 
-def test_linear_gelu_backward_epilogue():
-    M, Cin, Cout = 2048, 1024, 4096   # dgrad of MlpDown: [M][1024] x W2 -> [M][4096]
+@pytest.mark.parametrize("M,tile_n", [(2048, 128), (256, 128), (2048, 64), (1000, 64)])
+def test_linear_gelu_backward_epilogue(M, tile_n):
+    # CTA-pair tiles (2048 x 128), single-CTA tiles (few tiles), 64-column
+    # tiles; the gelu' operand transform runs in all of them
+    Cin, Cout = 1024, 4096   # dgrad of MlpDown: [M][1024] x W2 -> [M][4096]
     dy = rnd(M, Cin)
     wt = rnd(Cout, Cin, scale=Cin ** -0.5, seed=1)     # transposed W2 ([4096][1024])
     pre = rnd(M, Cout, scale=2.0, seed=2)
     conv = _linear(M, Cin, Cout, wt)
-    conv.set_tile_n(128)
+    conv.set_tile_n(tile_n)
     y = torch.empty(M, Cout, device=dev, dtype=torch.bfloat16)
     conv.gelu_bwd(dy.data_ptr(), y.data_ptr(), pre.data_ptr(), _st())
     pr = pre.float().requires_grad_(True)
