@@ -351,20 +351,36 @@ __global__ void __launch_bounds__(256)
                const float* __restrict__ beta, const float* __restrict__ mean2,
                const float* __restrict__ invstd2, const float* __restrict__ gamma2,
                const float* __restrict__ beta2) {
+  // per-channel scale / shift of all C (<= 2048) channels, once per block with
+  // coalesced loads (a thread's 8 channels read back from shared memory: the
+  // per-thread scattered loads of 4 x 8 parameters cost ~30 us per launch)
+  __shared__ __align__(16) float s_sc[2048], s_sh[2048];
+  __shared__ __align__(16) float s_sc2[MODE == 2 ? 2048 : 1], s_sh2[MODE == 2 ? 2048 : 1];
   pdl_wait();
   pdl_trigger();
+  for (int c = threadIdx.x; c <= cmask; c += blockDim.x) {
+    // explicit FMAs: the dgrad BN-backward epilogue (conv_fwd.cu) recomputes
+    // this ReLU mask with the identical arithmetic
+    const float a = invstd[c] * gamma[c];
+    s_sc[c] = a;
+    s_sh[c] = fmaf(-mean[c], a, beta[c]);
+    if (MODE == 2) {
+      const float a2 = invstd2[c] * gamma2[c];
+      s_sc2[MODE == 2 ? c : 0] = a2;
+      s_sh2[MODE == 2 ? c : 0] = fmaf(-mean2[c], a2, beta2[c]);
+    }
+  }
+  __syncthreads();
   const int64_t first = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   const int c0 = int(first * 8) & cmask;
   float sc[8], sh[8], sc2[8], sh2[8];
 #pragma unroll
   for (int j = 0; j < 8; ++j) {
-    // explicit FMAs: the dgrad BN-backward epilogue (conv_fwd.cu) recomputes
-    // this ReLU mask with the identical arithmetic
-    sc[j] = invstd[c0 + j] * gamma[c0 + j];
-    sh[j] = fmaf(-mean[c0 + j], sc[j], beta[c0 + j]);
+    sc[j] = s_sc[c0 + j];
+    sh[j] = s_sh[c0 + j];
     if (MODE == 2) {
-      sc2[j] = invstd2[c0 + j] * gamma2[c0 + j];
-      sh2[j] = fmaf(-mean2[c0 + j], sc2[j], beta2[c0 + j]);
+      sc2[j] = s_sc2[MODE == 2 ? c0 + j : 0];
+      sh2[j] = s_sh2[MODE == 2 ? c0 + j : 0];
     }
   }
   const int64_t stride = int64_t(gridDim.x) * blockDim.x;
@@ -670,21 +686,30 @@ __global__ void __launch_bounds__(256)
                    int logC, int64_t M, const float* __restrict__ mean,
                    const float* __restrict__ invstd, const float* __restrict__ gamma,
                    const float* __restrict__ dgamma, const float* __restrict__ dbeta) {
+  // per-channel coefficients of all C (<= 2048) channels, once per block with
+  // coalesced loads, read back from shared memory (as k_bn_apply)
+  __shared__ __align__(16) float s_k1[2048], s_k2[2048], s_k3[2048];
   pdl_wait();
   pdl_trigger();
+  const float invM = 1.f / float(M);
+  for (int c = threadIdx.x; c <= cmask; c += blockDim.x) {
+    const float is = invstd[c];
+    const float a = gamma[c] * is;
+    const float kd = dgamma[c] * invM * is;  // coefficient of (x - mean)
+    s_k1[c] = a;
+    s_k2[c] = -a * kd;
+    s_k3[c] = a * (kd * mean[c] - dbeta[c] * invM);
+  }
+  __syncthreads();
   const int64_t first = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   const int c0 = int(first * 8) & cmask;
   const int C = cmask + 1;
-  const float invM = 1.f / float(M);
   float k1[8], k2[8], k3[8];
 #pragma unroll
   for (int j = 0; j < 8; ++j) {
-    const float is = invstd[c0 + j];
-    const float a = gamma[c0 + j] * is;
-    const float kd = dgamma[c0 + j] * invM * is;  // coefficient of (x - mean)
-    k1[j] = a;
-    k2[j] = -a * kd;
-    k3[j] = a * (kd * mean[c0 + j] - dbeta[c0 + j] * invM);
+    k1[j] = s_k1[c0 + j];
+    k2[j] = s_k2[c0 + j];
+    k3[j] = s_k3[c0 + j];
   }
   const float inv_hw = POOLED ? 1.f / float(pool_hw) : 1.f;
   const int64_t stride = int64_t(gridDim.x) * blockDim.x;

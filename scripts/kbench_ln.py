@@ -17,7 +17,9 @@ rstd = torch.empty(rows, device=dev)
 g = torch.ones(H, device=dev)
 b = torch.zeros(H, device=dev)
 st = torch.cuda.current_stream().cuda_stream
-flush = torch.empty(256 * 2**20, dtype=torch.uint8, device=dev)
+# L2 flush by READING 256 MB (writing it would leave dirty lines the timed
+# kernel would pay to write back)
+flush = torch.ones(64 * 2**20, device=dev)
 
 
 def timed(fn, n=200):
@@ -26,7 +28,7 @@ def timed(fn, n=200):
     torch.cuda.synchronize()
     tot = 0.0
     for _ in range(n):
-        flush.zero_()
+        flush.sum()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
         fn()
