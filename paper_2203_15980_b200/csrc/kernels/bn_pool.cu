@@ -570,15 +570,24 @@ __global__ void __launch_bounds__(256)
   const int tx = threadIdx.x % tpr, ty = threadIdx.x / tpr;
   const int c0 = tx * 8;
   const float invM = 1.f / float(M);
+  // the per-channel coefficients once per block, coalesced, through shared
+  // memory (as k_bn_bwd_apply)
+  __shared__ __align__(16) float s_k1[2048], s_k2[2048], s_k3[2048];
+  for (int c = threadIdx.x; c < C; c += blockDim.x) {
+    const float is = invstd[c];
+    const float a = gamma[c] * is;
+    const float kd = __ldcg(dgamma + c) * invM * is;
+    s_k1[c] = a;
+    s_k2[c] = -a * kd;
+    s_k3[c] = a * (kd * mean[c] - __ldcg(dbeta + c) * invM);
+  }
+  __syncthreads();
   float k1[8], k2[8], k3[8];
 #pragma unroll
   for (int j = 0; j < 8; ++j) {
-    const float is = invstd[c0 + j];
-    const float a = gamma[c0 + j] * is;
-    const float kd = __ldcg(dgamma + c0 + j) * invM * is;
-    k1[j] = a;
-    k2[j] = -a * kd;
-    k3[j] = a * (kd * mean[c0 + j] - __ldcg(dbeta + c0 + j) * invM);
+    k1[j] = s_k1[c0 + j];
+    k2[j] = s_k2[c0 + j];
+    k3[j] = s_k3[c0 + j];
   }
   const float inv_hw = POOLED ? 1.f / float(pool_hw) : 1.f;
   const int64_t r0 = int64_t(blockIdx.x) * chunk;
