@@ -769,7 +769,7 @@ __global__ void k_span_dbias(const float* __restrict__ dl, int64_t T, float* __r
 
 // ---------------------------------------------------------------- attention prep
 // D[(b*heads + hd)*S + s] = sum_d dO[t][hd*64 + d] * O[t][hd*64 + d]; warp per
-// token, lane = 32 columns (half a head), lane pairs combined
+// token
 __global__ void __launch_bounds__(256)
     k_attn_dvec(const bf16* __restrict__ o, const bf16* __restrict__ d, int64_t T, int S, int heads,
                 float* __restrict__ D) {
@@ -779,25 +779,24 @@ __global__ void __launch_bounds__(256)
   const int64_t t = int64_t(blockIdx.x) * 8 + (threadIdx.x >> 5);
   if (t >= T) return;
   const int H = heads * 64;
-  for (int base = 0; base < H; base += 1024) {
+  const int64_t bb = t / S, ss = t % S;
+  // lane-interleaved 16-byte chunks (each load instruction reads 512
+  // contiguous bytes): chunk u covers columns [u*256, u*256 + 256), four heads,
+  // lane l its 8 columns u*256 + 8 l; a head's sum is an 8-lane reduction
+  for (int u = 0; u * 256 < H; ++u) {
+    const int c0 = u * 256 + lane * 8;
     float s = 0.f;
-    const int c0 = base + lane * 32;
     if (c0 < H) {
+      float a[8], b[8];
+      unpack8(__ldg(reinterpret_cast<const uint4*>(o + t * H + c0)), a);
+      unpack8(__ldg(reinterpret_cast<const uint4*>(d + t * H + c0)), b);
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        float a[8], b[8];
-        unpack8(__ldg(reinterpret_cast<const uint4*>(o + t * H + c0) + u), a);
-        unpack8(__ldg(reinterpret_cast<const uint4*>(d + t * H + c0) + u), b);
-#pragma unroll
-        for (int i = 0; i < 8; ++i) s = fmaf(a[i], b[i], s);
-      }
+      for (int i = 0; i < 8; ++i) s = fmaf(a[i], b[i], s);
     }
+    s += __shfl_xor_sync(0xFFFFFFFFu, s, 4);
+    s += __shfl_xor_sync(0xFFFFFFFFu, s, 2);
     s += __shfl_xor_sync(0xFFFFFFFFu, s, 1);
-    if (c0 < H && (lane & 1) == 0) {
-      const int hd = c0 / 64;
-      const int64_t bb = t / S, ss = t % S;
-      D[(bb * heads + hd) * S + ss] = s;
-    }
+    if (c0 < H && (lane & 7) == 0) D[(bb * heads + c0 / 64) * S + ss] = s;
   }
 }
 
