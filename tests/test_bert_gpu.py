@@ -86,3 +86,24 @@ def test_bert_delta40_bit_identical_to_no_eviction():
     # the plan really released tensors
     acts = prog.actions
     assert int((acts["op"] == 1).sum()) > 0, c  # recompute actions
+
+
+def test_bert_attention_wgrad_overlap_bit_identical():
+    """The output projection's weight gradient on the side stream during the
+    attention backward (DELTA_KOP_SIDE_ALWAYS) gives the same step, bit for
+    bit, as running it in its own node"""
+    cfg = TINY
+    grads, losses = [], []
+    saved = B.BertRuntime.overlap_attn_wgrad
+    try:
+        for overlap in (True, False):
+            B.BertRuntime.overlap_attn_wgrad = overlap
+            rt = B.BertRuntime(cfg, seed=0, lr=0.0)
+            rt.plan(None)
+            batch = rt.synthetic_batch(2, pin=False)
+            losses.append(rt.step(*batch[:3]))
+            grads.append(rt.params.grad.clone())
+    finally:
+        B.BertRuntime.overlap_attn_wgrad = saved
+    assert losses[0] == losses[1]
+    assert torch.equal(grads[0], grads[1])
